@@ -1,0 +1,256 @@
+/*
+ * janus.h — C ABI of the B200-native speculative-graph executor (JANUS, arXiv 1812.01329).
+ *
+ * The library executes the *speculatively specialised* symbolic dataflow graph of an imperative
+ * DL training step on one B200 (§2.3 "generates a symbolic graph tailored for the
+ * assumptions"; §3.1 "the Speculative Graph Executor executes the symbolic graph"), checks
+ * the assumptions on the device (§3.2 AssertOp), commits state all-or-nothing
+ * (§3.2; §4.2.3) and offers the imperative per-op GPU executor as the fallback
+ * (§3.2, Figure 2 (E)).
+ *
+ * Citations: P:NNN = line of the paper text, S:NNN = line of SPEC.md.
+ *
+ * Conventions
+ *  - Every pointer argument is BORROWED for the duration of the call unless stated otherwise.
+ *  - janus_tensor.data may point to device memory (normal case) or, for `args` and `outs` only,
+ *    to host memory: the library then stages the bytes through the workspace (H2D before the
+ *    step, D2H after), inside the same call. State tensors and the workspace must be device memory.
+ *  - Strides are in elements. Every tensor passed to janus_run must be contiguous (row-major).
+ *  - No call allocates device memory. The caller (PyTorch caching allocator) owns args, state,
+ *    outs and the workspace; the graph object owns host metadata only.
+ *  - Errors: every call returns a janus_status. JANUS_ERR_* codes never leave state modified.
+ */
+#ifndef JANUS_H
+#define JANUS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JANUS_ABI_VERSION 1
+
+/* ---------------------------------------------------------------------------------------------
+ * Status codes. ASSUMPTION_FAILED is the AssertOp abort of P:168 ("aborts the graph execution if
+ * the given condition fails. It also reports which assumption has been broken"). ERR_RUNTIME is a
+ * runtime error inside a pure node (index out of range), reported distinctly from an assumption
+ * failure as in S:429; it also commits nothing.
+ * ------------------------------------------------------------------------------------------- */
+typedef enum {
+  JANUS_OK = 0,
+  JANUS_ASSUMPTION_FAILED = 1,
+  JANUS_ERR_INVALID = 2,      /* malformed op list / bad arguments (text in err buffer)      */
+  JANUS_ERR_UNSUPPORTED = 3,  /* graph valid but the device path cannot run it exactly       */
+  JANUS_ERR_RUNTIME = 4,      /* runtime error in a node (bad token id, bad child id)         */
+  JANUS_ERR_CUDA = 5,
+  JANUS_ERR_NCCL = 6
+} janus_status;
+
+typedef enum { JANUS_F32 = 0, JANUS_BF16 = 1, JANUS_I32 = 2, JANUS_I64 = 3, JANUS_U8 = 4 } janus_dtype;
+
+typedef struct {
+  void *data;         /* device pointer (or host pointer for args/outs, see conventions) */
+  int32_t dtype;      /* janus_dtype */
+  int32_t ndim;       /* 0..4 */
+  int64_t shape[4];
+  int64_t stride[4];  /* elements; must describe a contiguous row-major tensor */
+} janus_tensor;
+
+/* ---------------------------------------------------------------------------------------------
+ * Op kinds of the symbolic graph. A graph is an array of janus_op; a node is referenced by its
+ * index in that array. The graph vocabulary follows the paper's conversion rules:
+ *   ARG = PlaceholderOp for input parameters; CONST = ConstantOp for literals;
+ *   STATE_READ/STATE_WRITE = PyGetAttrOp/PySetAttrOp with local copies (Figure 5);
+ *   SWITCH/MERGE = `if`; ENTER/EXIT/NEXT_ITERATION/LOOP_COND = `while`/`for` frames
+ *   (P:222); INVOKE = function call / recursion (InvokeOp); the whitelisted framework
+ *   functions are EMBEDDING, LINEAR, LSTM_CELL, TREELSTM_LEAF, TREELSTM_CELL,
+ *   SOFTMAX_XENT; SGD_APPLY is the automatically inserted differentiation + parameter update
+ *    and, being a state mutation, is deferred until all assumptions hold.
+ *
+ * Port conventions: SWITCH output port 0 = false branch, port 1 = true branch (TF SwitchOp).
+ * MERGE output port 0 = value, port 1 = index of the live input. LSTM_CELL/TREELSTM_* output
+ * port 0 = h, port 1 = c.
+ *
+ * Attribute table (iattr[k] / fattr[k]); "scalar" means an int32 or f32 0-d value:
+ *   ARG            iattr0 = argument index
+ *   CONST          iattr0 = dtype (JANUS_I32 | JANUS_F32); scalar value in fattr0
+ *   STATE_READ     iattr0 = state slot, iattr1 = dtype, iattr2 = ndim, iattr3..6 = dims
+ *   STATE_WRITE    in0 = value; iattr0 = state slot, iattr1 = effect sequence number
+ *   OUTPUT         in0 = value; iattr0 = output index
+ *   ADD, LESS, EQ  in0, in1 (scalar ∘ scalar, or scalar ∘ vector elementwise; LESS/EQ give int32)
+ *   MAX_REDUCE     in0 int32 vector -> int32 scalar
+ *   SUM            in0 f32 tensor -> f32 scalar (sum of all elements)
+ *   ZEROS_LIKE     in0 -> zeros of the same dtype/shape
+ *   COLUMN         in0 = matrix [B,T], in1 = scalar t -> vector [B] = in0[:, t]
+ *   ELEMENT        in0 = vector, in1 = scalar i -> scalar in0[i]
+ *   EMBEDDING      in0 = table [V,E] f32, in1 = int ids (scalar or [n]) -> rows [n,E]
+ *   LINEAR         in0 = x [n,K], in1 = W [N,K], in2 = b [N] -> x W^T + b  [n,N]
+ *   LSTM_CELL      in0 = x [B,E], in1 = h [B,H], in2 = c [B,H], in3 = W_ih [4H,E],
+ *                  in4 = W_hh [4H,H], in5 = b [4H] (gate blocks i,f,g,o), in6 = valid mask int32 [B]
+ *                  (rows with valid==0 carry h,c unchanged)
+ *   TREELSTM_LEAF  in0 = x [1,E], in1 = W_leaf [3H,E] (blocks i,o,u), in2 = b [4H] (blocks i,f,o,u)
+ *   TREELSTM_CELL  in0 = h_l, in1 = c_l, in2 = h_r, in3 = c_r ([1,H] each), in4 = U [5H,2H]
+ *                  (blocks i,f_l,f_r,o,u), in5 = b [4H]
+ *   SOFTMAX_XENT   in0 = logits [n,C], in1 = targets int32 [n], in2 = mask int32 [n] -> f32
+ *                  scalar: mean over masked rows of (logsumexp(logits_r) - logits_r[target_r])
+ *   SEQ_MASK       in0 = lengths [B], in1 = scalar T -> int32 [T*B], row t*B+b = (t < len_b)
+ *   TIME_MAJOR     in0 = int matrix [B,W], in1 = scalar T -> int32 [T*B], row t*B+b = in0[b,t]
+ *   TA_NEW         -> empty tensor array (list)
+ *   TA_WRITE       in0 = array, in1 = scalar index, in2 = value -> array with element set
+ *   TA_STACK       in0 = array of n values [k, D] -> [n*k, D] (concatenate rows in index order)
+ *   SWITCH         in0 = data, in1 = int predicate scalar
+ *   MERGE          in0.. = candidate inputs (n_in >= 2)
+ *   ENTER          in0 = value; iattr0 = frame id (>0), iattr1 = 1 if loop-invariant
+ *   EXIT, NEXT_ITERATION, LOOP_COND, IDENTITY: in0
+ *   INVOKE         iattr0 = callee function id; inputs = callee arguments; output port k =
+ *                  the callee's RETURN input k
+ *   RETURN         inputs = return values of the enclosing function (func > 0)
+ *   SGD_APPLY      in0 = scalar loss; iattr0 = state slot of the parameter, iattr1 = effect seq;
+ *                  fattr0 = learning rate. Effect: slot -= lr * (d loss / d value read from slot),
+ *                  averaged over data-parallel ranks ("average of gradients").
+ * janus_op.func = id of the function body the node belongs to (0 = main program). Function
+ * bodies use ARG nodes for their parameters (iattr0 = parameter index) and one RETURN node.
+ * ------------------------------------------------------------------------------------------- */
+typedef enum {
+  JOP_ARG = 0, JOP_CONST = 1, JOP_STATE_READ = 2, JOP_STATE_WRITE = 3, JOP_OUTPUT = 4,
+  JOP_ADD = 5, JOP_LESS = 6, JOP_EQ = 7, JOP_MAX_REDUCE = 8, JOP_SUM = 9, JOP_ZEROS_LIKE = 10,
+  JOP_COLUMN = 11, JOP_ELEMENT = 12,
+  JOP_EMBEDDING = 13, JOP_LINEAR = 14, JOP_LSTM_CELL = 15, JOP_TREELSTM_LEAF = 16,
+  JOP_TREELSTM_CELL = 17, JOP_SOFTMAX_XENT = 18, JOP_SEQ_MASK = 19, JOP_TIME_MAJOR = 20,
+  JOP_TA_NEW = 21, JOP_TA_WRITE = 22, JOP_TA_STACK = 23,
+  JOP_SWITCH = 24, JOP_MERGE = 25, JOP_ENTER = 26, JOP_EXIT = 27, JOP_NEXT_ITERATION = 28,
+  JOP_LOOP_COND = 29, JOP_IDENTITY = 30, JOP_INVOKE = 31, JOP_RETURN = 32,
+  JOP_SGD_APPLY = 33,
+  JOP__COUNT = 34
+} janus_op_kind;
+
+#define JANUS_MAX_IN 8
+typedef struct {
+  int32_t kind;                  /* janus_op_kind */
+  int32_t func;                  /* function body id, 0 = main */
+  int32_t n_in;
+  int32_t in_node[JANUS_MAX_IN]; /* producer node index into the ops array */
+  int32_t in_port[JANUS_MAX_IN]; /* producer output port */
+  int64_t iattr[8];
+  double fattr[2];
+} janus_op;
+
+/* ---------------------------------------------------------------------------------------------
+ * Assumptions ("the optimized graph and the assumption that were used to generate the
+ * graph"; Figure 4 specialisation hierarchy P:240-248).
+ *   mode DISPATCH: validated from tensor metadata before launch ("checked when retrieving
+ *                  the graph from the graph cache"); failure launches nothing.
+ *   mode RUNTIME : validated on the device by AssertOps over input data.
+ *
+ *   JA_DTYPE_EQ     args[target].dtype == dtype                                    (DISPATCH)
+ *   JA_SHAPE_MATCH  args[target] has ndim dims and dims[k] == -1 ('?') or equal    (DISPATCH)
+ *                   (Figure 4: (4,8) relaxed to (?,8))
+ *   JA_TRIP_COUNT   every element of int32 args[target] == value: the loop whose trip count is
+ *                   max(lengths) runs exactly `value` iterations with no masked rows; the graph is
+ *                   unrolled ("unrolls the loop with this fixed iteration count, and adds
+ *                   an assertion operation")                                          (RUNTIME)
+ *   JA_TYPE_TAG     int32 state[target][0] == value: the `self.state is None` branch takes the
+ *                   tensor arm (P:226-228 single-arm branch; P:238 attribute type)    (RUNTIME)
+ *   JA_RANGE        lo <= args[target][i] <= hi for all i; if ref_arg >= 0 then also
+ *                   args[target][i] <= args[ref_arg].shape[ref_dim]                   (RUNTIME)
+ *   JA_TREE_BINARY  the forest args (kind,left,right,word,tree_off = args target..target+4) is a
+ *                   list of binary trees in per-tree post-order: every node is a leaf (kind 0,
+ *                   0 <= word < hi) or binary (kind 1, two distinct children with ids in
+ *                   [tree_off[t], node), each node having exactly one parent), tree root = last
+ *                   node, at most `value` nodes per tree — the structure the level-batched
+ *                   lowering of the recursive InvokeOp (P:224, P:316 fn6) relies on (RUNTIME)
+ *   JA_VALUE_EQ     int32 args[target][0] == value (constant promotion)        (RUNTIME)
+ * ------------------------------------------------------------------------------------------- */
+typedef enum {
+  JA_DTYPE_EQ = 0, JA_SHAPE_MATCH = 1, JA_TRIP_COUNT = 2, JA_TYPE_TAG = 3, JA_RANGE = 4,
+  JA_TREE_BINARY = 5, JA_VALUE_EQ = 6
+} janus_assumption_kind;
+
+enum { JANUS_MODE_DISPATCH = 0, JANUS_MODE_RUNTIME = 1 };
+
+typedef struct {
+  uint32_t id;        /* assumption id reported on failure (smaller id wins) */
+  int32_t kind;       /* janus_assumption_kind */
+  int32_t mode;       /* JANUS_MODE_* */
+  int32_t target;     /* argument index (state slot for JA_TYPE_TAG) */
+  int32_t dtype;      /* JA_DTYPE_EQ */
+  int32_t ndim;       /* JA_SHAPE_MATCH */
+  int64_t dims[4];    /* JA_SHAPE_MATCH, -1 = '?' */
+  int64_t lo, hi, value;
+  int32_t ref_arg, ref_dim; /* JA_RANGE optional shape bound, -1 = none */
+} janus_assumption;
+
+/* Failure report. observed = the offending value (dim size, dtype code, element value);
+ * index = dim index (DISPATCH) or flat element index (RUNTIME). */
+typedef struct {
+  uint32_t assumption_id;
+  int32_t rank;
+  int64_t index;
+  int64_t observed;
+} janus_failure;
+
+typedef struct {
+  int32_t world_size;        /* data-parallel ranks; 1 = single GPU                 */
+  int32_t rank;
+  uint8_t nccl_id[128];      /* ncclUniqueId bytes from rank 0 (ignored when world_size==1) */
+  int32_t gemm_dtype;        /* JANUS_BF16: bf16 operands, fp32 accumulate (tcgen05);
+                                JANUS_F32: fp32 SIMT everywhere                             */
+  int32_t strip_asserts;     /* test/ablation only: drop RUNTIME AssertOps (P:392 overhead) */
+  int32_t fail_assert_id;    /* fault injection: force this assumption id to fail, -1 = off */
+  int32_t reserved[5];
+} janus_build_opts;
+
+typedef struct janus_graph janus_graph;
+
+/* Validate the op list, split assumptions into DISPATCH/RUNTIME, specialise (unroll trip-count
+ * loops, drop single-arm branches, lower recursive INVOKE to level-batched tree evaluation) and
+ * encode the device program. Keeps the generic op list for janus_run_imperative.
+ * On JANUS_ERR_INVALID / JANUS_ERR_UNSUPPORTED a message is written to err (if err_len > 0) and
+ * *out is NULL — except that ERR_UNSUPPORTED still returns a graph usable by
+ * janus_run_imperative (the device graph is absent; janus_run then returns ERR_UNSUPPORTED). */
+janus_status janus_graph_build(const janus_op *ops, int32_t n_ops, const janus_assumption *asms,
+                               int32_t n_asms, const janus_build_opts *opts, janus_graph **out,
+                               char *err, size_t err_len);
+
+/* Device bytes the caller must allocate for `workspace` (graph path and imperative path). The
+ * workspace must stay alive and unmodified between calls (it caches bf16 operand copies). */
+janus_status janus_workspace_bytes(const janus_graph *g, size_t *bytes);
+
+/* One speculative graph step. Enqueues on cuda_stream (a cudaStream_t; NULL = default)
+ * and returns after ONE stream synchronisation on the 16-byte status word.
+ *   JANUS_OK                : outputs written; every STATE_WRITE / SGD_APPLY effect committed.
+ *   JANUS_ASSUMPTION_FAILED : *fail filled (minimum failing id); every state tensor is
+ *                             byte-identical to its value before the call; outs unspecified.
+ *   JANUS_ERR_RUNTIME       : nothing committed.
+ * With world_size > 1 the call is collective: every rank gets the same status. */
+janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
+                       const janus_tensor *state, int32_t n_state, const janus_tensor *outs,
+                       int32_t n_outs, janus_tensor workspace, void *cuda_stream,
+                       janus_failure *fail);
+
+/* Imperative fallback (Figure 2 (E)): runs the generic op list op by op, one kernel
+ * launch per op instance, control predicates read back to the host (TF-Eager analogue). No
+ * assumptions; never returns ASSUMPTION_FAILED; commits unless ERR_RUNTIME. */
+janus_status janus_run_imperative(janus_graph *g, const janus_tensor *args, int32_t n_args,
+                                  const janus_tensor *state, int32_t n_state,
+                                  const janus_tensor *outs, int32_t n_outs,
+                                  janus_tensor workspace, void *cuda_stream);
+
+/* Cumulative counters of this graph: kernel launches issued by the library, host
+ * synchronisations, and aborts (ASSUMPTION_FAILED returns). */
+janus_status janus_counters(const janus_graph *g, uint64_t *launches, uint64_t *host_syncs,
+                            uint64_t *aborts);
+
+/* Human-readable description of the lowered device program (phases), for tests and docs. */
+janus_status janus_describe(const janus_graph *g, char *buf, size_t buf_len);
+
+void janus_graph_destroy(janus_graph *g); /* NULL-safe */
+const char *janus_status_str(janus_status s);
+int32_t janus_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* JANUS_H */

@@ -1,0 +1,213 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY. Op numerics (forward + vector-Jacobian products) of the
+whitelisted framework functions the graph may contain (§4.3.1: "matmul", ...).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may import
+this package. It shares no code with the CUDA path.
+
+Arithmetic: float64 throughout. Precision mode "f32" computes in fp64 with no rounding (the paper's
+fp32 models; C1 is compared at 1e-5). Mode "bf16" additionally rounds, round-to-nearest-even,
+at the three points of DESIGN.md reading R (SURVEY §8(c) rounding points):
+  R1  GEMM operand copies of weight matrices (W_ih, W_hh, W_dec, W_leaf, U, E) = rb(master)
+  R2  every h / x that feeds a GEMM = rb(h)
+  R3  dz and dy are rounded before the dgrad / wgrad GEMMs; bias gradients are sums of the
+      rounded rows (the bias gradient is the wgrad of a ones column)
+The cell equations follow the cited models because the paper gives none (P:312 cites [51] LSTM and
+[40] TreeLSTM): readings Q1 and Q5 of DESIGN.md, written out in the docstrings below.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class RuntimeFault(Exception):
+    """A runtime error inside a pure node (bad index) — reported distinctly from an assumption
+    failure and commits nothing."""
+
+
+def rb(x):
+    """Round float64 values to the nearest bfloat16 (ties to even), returned as float64.
+    Goes through fp32 first, as a GPU rounds its fp32 registers."""
+    a = np.asarray(x, dtype=np.float64).astype(np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 16) & 1
+    u = (u + 0x7FFF + lsb) & 0xFFFF0000
+    out = u.astype(np.uint32).view(np.float32).astype(np.float64)
+    nan = np.isnan(a)
+    if nan.any():
+        out = np.where(nan, np.nan, out)
+    return out
+
+
+def sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+class Prec:
+    """Precision mode: `g(x)` applies the GEMM operand rounding (R1/R2/R3) in bf16 mode."""
+
+    def __init__(self, mode):
+        assert mode in ("f32", "bf16")
+        self.mode = mode
+
+    def g(self, x):
+        return rb(x) if self.mode == "bf16" else np.asarray(x, np.float64)
+
+
+# ------------------------------------------------------------------------ embedding (KP3)
+def embedding_fwd(P, E, ids):
+    """X[r] = E[id_r]; ids outside [0, V) are a runtime error."""
+    ids = np.asarray(ids, np.int64).reshape(-1)
+    V = E.shape[0]
+    bad = (ids < 0) | (ids >= V)
+    if bad.any():
+        raise RuntimeFault(f"embedding id out of range at {int(np.argmax(bad))}")
+    return P.g(E)[ids]
+
+
+def embedding_vjp(E_shape, ids, dX):
+    """dE[w] = sum over rows r with id_r = w of dX[r], in ascending r (segmented sum)."""
+    ids = np.asarray(ids, np.int64).reshape(-1)
+    dE = np.zeros(E_shape)
+    for r, w in enumerate(ids):
+        dE[w] += dX[r]
+    return dE
+
+
+# ------------------------------------------------------------------------ linear (KP1)
+def linear_fwd(P, x, W, b):
+    """y = x W^T + b with bf16-rounded operands in bf16 mode (R1, R2)."""
+    return P.g(x) @ P.g(W).T + b
+
+
+def linear_vjp(P, x, W, dy):
+    """dx = rb(dy) W, dW = rb(dy)^T x, db = sum_rows rb(dy)   (R3)."""
+    d = P.g(dy)
+    return d @ P.g(W), d.T @ P.g(x), d.sum(axis=0)
+
+
+# ------------------------------------------------------------------------ LSTM cell (Fig 1 rnn_cell)
+def lstm_fwd(P, x, h, c, W_ih, W_hh, b, valid):
+    """Zaremba/torch.nn.LSTM cell (reading Q1; gate blocks i, f, g, o; one folded bias):
+        z = x W_ih^T + h W_hh^T + b;  i, f, o = sigmoid;  g = tanh
+        c' = f * c + i * g;  h' = o * tanh(c')
+    Rows with valid == 0 carry (h, c) unchanged (masked step, reading Q18 / C4)."""
+    H = h.shape[1]
+    z = P.g(x) @ P.g(W_ih).T + P.g(h) @ P.g(W_hh).T + b
+    i = sigmoid(z[:, 0:H]); f = sigmoid(z[:, H:2 * H])
+    g = np.tanh(z[:, 2 * H:3 * H]); o = sigmoid(z[:, 3 * H:4 * H])
+    c2 = f * c + i * g
+    h2 = o * np.tanh(c2)
+    v = (np.asarray(valid).reshape(-1, 1) != 0)
+    h2 = np.where(v, h2, h)
+    c2 = np.where(v, c2, c)
+    return h2, c2, (i, f, g, o, c, c2, v)
+
+
+def lstm_vjp(P, saved, x, h, W_ih, W_hh, dh2, dc2):
+    """Backward of lstm_fwd (SURVEY §8(c) "LSTM bwd"):
+        tc = tanh(c');  do = dh tc;  dc = dc' + dh o (1 - tc^2)
+        di = dc g;  dg = dc i;  df = dc c;  dc_prev = dc f
+        dz = [di i(1-i), df f(1-f), dg (1-g^2), do o(1-o)]
+        dx = rb(dz) W_ih;  dh_prev = rb(dz) W_hh;  dW_ih = rb(dz)^T x;  dW_hh = rb(dz)^T h;
+        db = sum_rows rb(dz).   Masked rows pass dh, dc through and contribute no dz."""
+    i, f, g, o, c, c2, v = saved
+    tc = np.tanh(c2)
+    do = dh2 * tc
+    dc = dc2 + dh2 * o * (1.0 - tc * tc)
+    di, dg, df = dc * g, dc * i, dc * c
+    dz = np.concatenate([di * i * (1 - i), df * f * (1 - f), dg * (1 - g * g), do * o * (1 - o)], axis=1)
+    dz = np.where(v, dz, 0.0)
+    d = P.g(dz)
+    dx = d @ P.g(W_ih)
+    dh_prev = np.where(v, d @ P.g(W_hh), dh2)
+    dc_prev = np.where(v, dc * f, dc2)
+    return dx, dh_prev, dc_prev, d.T @ P.g(x), d.T @ P.g(h), d.sum(axis=0)
+
+
+# ------------------------------------------------------------------------ TreeLSTM (Tai et al. [40])
+def tree_leaf_fwd(P, x, W_leaf, b):
+    """Leaf (reading Q5): z = x W_leaf^T + [b_i; b_o; b_u]; i, o = sigmoid, u = tanh;
+    c = i u; h = o tanh(c).  b has blocks (i, f, o, u)."""
+    H = W_leaf.shape[0] // 3
+    bb = np.concatenate([b[0:H], b[2 * H:3 * H], b[3 * H:4 * H]])
+    z = P.g(x) @ P.g(W_leaf).T + bb
+    i = sigmoid(z[:, 0:H]); o = sigmoid(z[:, H:2 * H]); u = np.tanh(z[:, 2 * H:3 * H])
+    c = i * u
+    h = o * np.tanh(c)
+    return h, c, (i, o, u, c)
+
+
+def tree_leaf_vjp(P, saved, x, W_leaf, dh, dc_in):
+    """tc = tanh c; do = dh tc; dc = dc_in + dh o (1 - tc^2); di = dc u; du = dc i;
+    dz = [di i(1-i), do o(1-o), du (1-u^2)]; dW_leaf = rb(dz)^T x; db_{i,o,u} = sum rb(dz);
+    dx = rb(dz) W_leaf."""
+    i, o, u, c = saved
+    H = i.shape[1]
+    tc = np.tanh(c)
+    do = dh * tc
+    dc = dc_in + dh * o * (1 - tc * tc)
+    dz = np.concatenate([dc * u * i * (1 - i), do * o * (1 - o), dc * i * (1 - u * u)], axis=1)
+    d = P.g(dz)
+    s = d.sum(axis=0)
+    db = np.concatenate([s[0:H], np.zeros(H), s[H:2 * H], s[2 * H:3 * H]])
+    return d @ P.g(W_leaf), d.T @ P.g(x), db
+
+
+def tree_cell_fwd(P, hl, cl, hr, cr, U, b):
+    """Binary N-ary TreeLSTM cell (reading Q5): z = [h_l; h_r] U^T + [b_i; b_f; b_f; b_o; b_u];
+    i, f_l, f_r, o = sigmoid, u = tanh; c = i u + f_l c_l + f_r c_r; h = o tanh(c)."""
+    H = hl.shape[1]
+    bb = np.concatenate([b[0:H], b[H:2 * H], b[H:2 * H], b[2 * H:3 * H], b[3 * H:4 * H]])
+    hh = np.concatenate([hl, hr], axis=1)
+    z = P.g(hh) @ P.g(U).T + bb
+    i = sigmoid(z[:, 0:H]); fl = sigmoid(z[:, H:2 * H]); fr = sigmoid(z[:, 2 * H:3 * H])
+    o = sigmoid(z[:, 3 * H:4 * H]); u = np.tanh(z[:, 4 * H:5 * H])
+    c = i * u + fl * cl + fr * cr
+    h = o * np.tanh(c)
+    return h, c, (i, fl, fr, o, u, cl, cr, c, hh)
+
+
+def tree_cell_vjp(P, saved, U, dh, dc_in):
+    """tc = tanh c; do = dh tc; dc = dc_in + dh o (1-tc^2); di = dc u; du = dc i;
+    df_l = dc c_l; df_r = dc c_r; dz = [di i(1-i), df_l f_l(1-f_l), df_r f_r(1-f_r), do o(1-o),
+    du (1-u^2)]; [dh_l; dh_r] = rb(dz) U; dc_l = dc f_l; dc_r = dc f_r; dU = rb(dz)^T [h_l; h_r];
+    db_i, db_o, db_u = sums of rb(dz) blocks; db_f = sum of the rb(dz_fl) + rb(dz_fr) blocks."""
+    i, fl, fr, o, u, cl, cr, c, hh = saved
+    H = i.shape[1]
+    tc = np.tanh(c)
+    do = dh * tc
+    dc = dc_in + dh * o * (1 - tc * tc)
+    dz = np.concatenate([dc * u * i * (1 - i), dc * cl * fl * (1 - fl), dc * cr * fr * (1 - fr),
+                         do * o * (1 - o), dc * i * (1 - u * u)], axis=1)
+    d = P.g(dz)
+    dhh = d @ P.g(U)
+    s = d.sum(axis=0)
+    db = np.concatenate([s[0:H], s[H:2 * H] + s[2 * H:3 * H], s[3 * H:4 * H], s[4 * H:5 * H]])
+    return dhh[:, :H], dc * fl, dhh[:, H:], dc * fr, d.T @ P.g(hh), db
+
+
+# ------------------------------------------------------------------------ loss (KP4)
+def xent_fwd(logits, tgt, mask):
+    """loss = sum_r mask_r (logsumexp(y_r) - y_r[tgt_r]) / max(1, sum_r mask_r)  (reading Q3).
+    Targets of masked rows outside [0, C) are a runtime error."""
+    tgt = np.asarray(tgt, np.int64).reshape(-1)
+    m = np.asarray(mask).reshape(-1) != 0
+    C = logits.shape[1]
+    bad = m & ((tgt < 0) | (tgt >= C))
+    if bad.any():
+        raise RuntimeFault(f"target out of range at {int(np.argmax(bad))}")
+    n = max(1, int(m.sum()))
+    mx = logits.max(axis=1, keepdims=True)
+    lse = (mx + np.log(np.exp(logits - mx).sum(axis=1, keepdims=True)))[:, 0]
+    t = np.clip(tgt, 0, C - 1)
+    lr = lse - logits[np.arange(len(t)), t]
+    loss = float(np.where(m, lr, 0.0).sum() / n)
+    return loss, (lse, t, m, n)
+
+
+def xent_vjp(logits, saved, dloss):
+    """dy = mask (softmax(y) - onehot(tgt)) / n_valid * dloss."""
+    lse, t, m, n = saved
+    p = np.exp(logits - lse[:, None])
+    p[np.arange(len(t)), t] -= 1.0
+    return np.where(m[:, None], p, 0.0) * (dloss / n)
