@@ -126,7 +126,7 @@ typedef enum {
   JOP__COUNT = 34
 } janus_op_kind;
 
-#define JANUS_MAX_IN 8
+#define JANUS_MAX_IN 12
 typedef struct {
   int32_t kind;                  /* janus_op_kind */
   int32_t func;                  /* function body id, 0 = main */

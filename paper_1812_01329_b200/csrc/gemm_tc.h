@@ -1,0 +1,37 @@
+// gemm_tc.h — host interface of the tcgen05 bf16 GEMM (gemm_tc.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace jk {
+
+struct GemmEpilogue {
+  float *C = nullptr;               // fp32 output [M, ldc] (row-major), may be null
+  int ldc = 0;
+  __nv_bfloat16 *Cb = nullptr;      // optional bf16 copy of the output
+  int ldcb = 0;
+  const float *bias_col = nullptr;  // + bias[n]
+  const float *bias_row = nullptr;  // + bias[m]
+  int accumulate = 0;               // C += result
+};
+
+// D[M,N] = A[M,K] . B[N,K]^T.
+//  a_mn == 0: A stored [M][lda] (K contiguous);  a_mn == 1: A stored [K][lda] (M contiguous).
+//  b_mn == 0: B stored [N][ldb] (K contiguous);  b_mn == 1: B stored [K][ldb] (N contiguous).
+// lda/ldb multiples of 8 elements; base pointers 16-B aligned. Out-of-range K/M/N reads are
+// zero-filled by TMA.
+struct GemmOp {
+  int M = 0, N = 0, K = 0;
+  const __nv_bfloat16 *A = nullptr;
+  int lda = 0, a_mn = 0;
+  const __nv_bfloat16 *B = nullptr;
+  int ldb = 0, b_mn = 0;
+  GemmEpilogue ep;
+};
+
+cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);
+bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_outer);
+
+}  // namespace jk

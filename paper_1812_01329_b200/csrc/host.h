@@ -1,0 +1,109 @@
+// host.h — host runtime of libjanus: the graph object, speculative lowering plans, dispatch.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/janus.h"
+#include "step_kernels.h"
+
+namespace jk {
+
+// Lowered device program for the Figure 1 LSTM language model (unrolled or device While loop).
+struct LmPlan {
+  int V = 0, E = 0, H = 0, L = 0, B = 0;
+  int T = 0;        // unrolled trip count (TRIP_COUNT) or maximum width W (While mode)
+  bool while_mode = false;
+  bool tag_specialised = false;  // TYPE_TAG assumed; otherwise the tag Switch runs on the device
+  bool bf16 = true;              // tcgen05 path; false = single-CTA fp32 SIMT path
+  // state slots
+  int slot_E = -1, slot_Wih[4] = {-1, -1, -1, -1}, slot_Whh[4] = {-1, -1, -1, -1},
+      slot_b[4] = {-1, -1, -1, -1}, slot_Wdec = -1, slot_bdec = -1;
+  int slot_h[4] = {-1, -1, -1, -1}, slot_c[4] = {-1, -1, -1, -1}, slot_tag = -1;
+  // learning rates (0 = parameter not updated / frozen)
+  float lr_E = 0, lr_Wih[4] = {}, lr_Whh[4] = {}, lr_b[4] = {}, lr_Wdec = 0, lr_bdec = 0;
+  bool write_h = false, write_tag = false;
+  // device guards
+  struct RG { int kind; uint32_t id; int arg; int slot; int64_t value, lo, hi; int ref_arg, ref_dim; };
+  std::vector<RG> runtime_guards;
+  // workspace layout (bytes)
+  size_t ws_bytes = 0;
+  struct Off {
+    size_t status = 0, barriers = 0, stage_args = 0;
+    size_t Wih_b[4], Whh_b[4], WhhT_b[4], bil[4], Wdec_b = 0;
+    size_t X = 0, Hs[4], Cs[4], G[4], DZ[4], dX[4];
+    size_t logits = 0, dy = 0, rowloss = 0, dHtop = 0, hT[4], cT[4];
+    size_t gWih[4], gWhh[4], gWdec = 0;
+    size_t seg_word = 0, seg_start = 0, seg_grad = 0, nseg = 0, keys = 0;
+    size_t small_ws = 0;
+  } off;
+  int Ep = 0, Hp = 0;  // padded row pitches (elements)
+  int nbar = 0;
+};
+
+// Lowered device program for the TreeLSTM (recursive InvokeOp flattened to level batches).
+struct TreePlan {
+  int V = 0, E = 0, H = 0, C = 0, B = 0, max_nodes = 127, max_N = 0;
+  bool bf16 = true;
+  int slot_E = -1, slot_Wleaf = -1, slot_U = -1, slot_b = -1, slot_Wc = -1, slot_bc = -1;
+  float lr_Wleaf = 0, lr_U = 0, lr_b = 0, lr_Wc = 0, lr_bc = 0;
+  uint32_t tree_guard_id = 0;
+  bool tree_guard = false;
+  std::vector<LmPlan::RG> runtime_guards;
+  size_t ws_bytes = 0;
+};
+
+struct Graph {
+  std::vector<janus_op> ops;
+  std::vector<janus_assumption> asms;
+  janus_build_opts opts{};
+  int n_args = 0, n_state = 0;
+  std::string kind;  // "lstm_lm" | "treelstm" | "" (no device lowering)
+  std::string unsupported_reason;
+  LmPlan lm;
+  TreePlan tree;
+  size_t ws_bytes = 0;       // max over graph path and imperative path
+  size_t imp_ws_bytes = 0;
+  // counters
+  uint64_t launches = 0, host_syncs = 0, aborts = 0;
+  // pinned status readback
+  DevStatus *h_status = nullptr;
+  void *nccl = nullptr;  // ncclComm_t when world_size > 1
+  std::string describe;
+};
+
+// host_graph.cpp
+janus_status validate_graph(Graph &g, std::string &err);
+bool check_dispatch(const Graph &g, const janus_tensor *args, int n_args, janus_failure *fail);
+
+// host_lm.cpp
+bool lower_lm(Graph &g, std::string &why);
+janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *state,
+                    const janus_tensor *outs, int n_outs, const janus_tensor &ws,
+                    cudaStream_t st, janus_failure *fail);
+
+// host_tree.cpp
+bool lower_tree(Graph &g, std::string &why);
+janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janus_tensor *state,
+                      const janus_tensor *outs, int n_outs, const janus_tensor &ws,
+                      cudaStream_t st, janus_failure *fail);
+
+// host_imperative.cpp
+size_t imperative_ws_bytes(const Graph &g);
+janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
+                            const janus_tensor *state, int n_state, const janus_tensor *outs,
+                            int n_outs, const janus_tensor &ws, cudaStream_t st);
+
+// one D2H of the status word + stream sync; decodes the failure (host_lm.cpp)
+janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_outs,
+                    cudaStream_t st, janus_failure *fail);
+
+// helpers
+int producer_origin(const Graph &g, int node);     // follows Enter/Identity/Switch/Merge(in0)
+const janus_op &op_at(const Graph &g, int node);
+janus_status cuda_status(cudaError_t e);
+bool is_device_ptr(const void *p);
+
+}  // namespace jk

@@ -1,0 +1,515 @@
+// host_lm.cpp — speculative lowering and device program of the Figure 1 LSTM language model
+// (Table 2 LSTM on PTB).
+//
+// lower_lm recognises the generic graph built by the imperative program (loop frame over
+// time steps with LSTM_CELL layers, embedding lookup, decoder LINEAR + SOFTMAX_XENT, SGD_APPLY
+// effects, STATE_WRITE of the carried state) and specialises it under the assumptions:
+//   TRIP_COUNT(lengths == T) -> the loop is unrolled to T steps with no masking;
+//   RANGE(1 <= lengths <= W) -> device-resident While loop, trip count max(lengths) computed on
+//                               the device, masked rows carry their state;
+//   TYPE_TAG(tag == TENSOR)  -> the `self.state is None` Switch/Merge is dropped;
+//                               without it the predicate is evaluated on the device.
+// Every RUNTIME assumption becomes a device AssertOp; the commit is predicated on all of them.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+
+#include "gemm_tc.h"
+#include "host.h"
+#include "lm_rec.h"
+#include "lm_small.h"
+#include "step_kernels.h"
+
+namespace jk {
+
+static int r8(int x) { return (x + 7) & ~7; }
+static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static bool slot_of(const Graph &g, int node, int *slot, int64_t dims[4] = nullptr, int *ndim = nullptr) {
+  const int o = producer_origin(g, node);
+  if (o < 0 || g.ops[o].kind != JOP_STATE_READ) return false;
+  *slot = (int)g.ops[o].iattr[0];
+  if (dims) for (int k = 0; k < 4; ++k) dims[k] = g.ops[o].iattr[3 + k];
+  if (ndim) *ndim = (int)g.ops[o].iattr[2];
+  return true;
+}
+
+static bool is_arg(const Graph &g, int node, int idx) {
+  const int o = producer_origin(g, node);
+  return o >= 0 && g.ops[o].kind == JOP_ARG && g.ops[o].iattr[0] == idx;
+}
+
+bool lower_lm(Graph &g, std::string &why) {
+  LmPlan &p = g.lm;
+  p = LmPlan();
+  std::vector<int> cells;
+  int emb = -1, dec = -1, xent = -1;
+  for (int i = 0; i < (int)g.ops.size(); ++i) {
+    const janus_op &o = g.ops[i];
+    if (o.func != 0) continue;
+    if (o.kind == JOP_LSTM_CELL) cells.push_back(i);
+    if (o.kind == JOP_EMBEDDING) emb = i;
+    if (o.kind == JOP_SOFTMAX_XENT) xent = i;
+  }
+  if (cells.empty()) { why = "no LSTM_CELL"; return false; }
+  p.L = (int)cells.size();
+  if (p.L > 4) { why = "more than 4 layers"; return false; }
+  int64_t d[4];
+  int nd;
+  for (int l = 0; l < p.L; ++l) {
+    const janus_op &c = g.ops[cells[l]];
+    if (!slot_of(g, c.in_node[3], &p.slot_Wih[l], d, &nd) || nd != 2) { why = "W_ih not a state slot"; return false; }
+    if (l == 0) { p.H = (int)(d[0] / 4); p.E = (int)d[1]; }
+    else if (d[1] != p.H) { why = "layer input width"; return false; }
+    if (d[0] != 4 * p.H) { why = "W_ih rows != 4H"; return false; }
+    if (!slot_of(g, c.in_node[4], &p.slot_Whh[l], d, &nd) || d[0] != 4 * p.H || d[1] != p.H) { why = "W_hh"; return false; }
+    if (!slot_of(g, c.in_node[5], &p.slot_b[l], d, &nd) || d[0] != 4 * p.H) { why = "bias"; return false; }
+    if (!slot_of(g, c.in_node[1], &p.slot_h[l], d, &nd) || nd != 2 || d[1] != p.H) { why = "h state"; return false; }
+    if (l == 0) p.B = (int)d[0];
+    else if (d[0] != p.B) { why = "h batch"; return false; }
+    if (!slot_of(g, c.in_node[2], &p.slot_c[l], d, &nd) || d[0] != p.B || d[1] != p.H) { why = "c state"; return false; }
+    if (l == 0) {
+      if (c.in_node[0] != emb) { why = "layer-0 input is not the embedding"; return false; }
+    } else if (c.in_node[0] != cells[l - 1] || c.in_port[0] != 0) { why = "layer chain"; return false; }
+    const janus_op &v = g.ops[c.in_node[6]];
+    if (v.kind != JOP_LESS || !is_arg(g, v.in_node[1], 2)) { why = "valid mask"; return false; }
+  }
+  if (emb < 0) { why = "no EMBEDDING"; return false; }
+  {
+    const janus_op &e = g.ops[emb];
+    if (!slot_of(g, e.in_node[0], &p.slot_E, d, &nd) || nd != 2 || d[1] != p.E) { why = "embedding table"; return false; }
+    p.V = (int)d[0];
+    const janus_op &col = g.ops[e.in_node[1]];
+    if (col.kind != JOP_COLUMN || !is_arg(g, col.in_node[0], 0)) { why = "embedding ids"; return false; }
+  }
+  if (xent < 0) { why = "no SOFTMAX_XENT"; return false; }
+  {
+    const janus_op &x = g.ops[xent];
+    dec = x.in_node[0];
+    const janus_op &lin = g.ops[dec];
+    if (lin.kind != JOP_LINEAR || g.ops[lin.in_node[0]].kind != JOP_TA_STACK) { why = "decoder"; return false; }
+    if (!slot_of(g, lin.in_node[1], &p.slot_Wdec, d, &nd) || d[0] != p.V || d[1] != p.H) { why = "W_dec"; return false; }
+    if (!slot_of(g, lin.in_node[2], &p.slot_bdec, d, &nd) || d[0] != p.V) { why = "b_dec"; return false; }
+    const janus_op &tm = g.ops[x.in_node[1]];
+    const janus_op &mk = g.ops[x.in_node[2]];
+    if (tm.kind != JOP_TIME_MAJOR || !is_arg(g, tm.in_node[0], 1)) { why = "targets"; return false; }
+    if (mk.kind != JOP_SEQ_MASK || !is_arg(g, mk.in_node[0], 2)) { why = "mask"; return false; }
+  }
+  bool has_output = false;
+  for (const auto &o : g.ops) {
+    if (o.func != 0) continue;
+    if (o.kind == JOP_OUTPUT && o.in_node[0] == xent && o.iattr[0] == 0) has_output = true;
+    if (o.kind == JOP_SGD_APPLY) {
+      if (o.in_node[0] != xent) { why = "SGD of another loss"; return false; }
+      const int s = (int)o.iattr[0];
+      const float lr = (float)o.fattr[0];
+      bool hit = false;
+      if (s == p.slot_E) { p.lr_E = lr; hit = true; }
+      if (s == p.slot_Wdec) { p.lr_Wdec = lr; hit = true; }
+      if (s == p.slot_bdec) { p.lr_bdec = lr; hit = true; }
+      for (int l = 0; l < p.L; ++l) {
+        if (s == p.slot_Wih[l]) { p.lr_Wih[l] = lr; hit = true; }
+        if (s == p.slot_Whh[l]) { p.lr_Whh[l] = lr; hit = true; }
+        if (s == p.slot_b[l]) { p.lr_b[l] = lr; hit = true; }
+      }
+      if (!hit) { why = "SGD on a non-parameter slot"; return false; }
+    }
+    if (o.kind == JOP_STATE_WRITE) {
+      const int s = (int)o.iattr[0];
+      const int src = producer_origin(g, o.in_node[0]);
+      bool ok = false;
+      for (int l = 0; l < p.L; ++l)
+        if ((s == p.slot_h[l] || s == p.slot_c[l]) && g.ops[src].kind == JOP_STATE_READ &&
+            g.ops[src].iattr[0] == s) ok = true;
+      if (ok) p.write_h = true;
+      if (!ok && g.ops[src].kind == JOP_CONST && g.ops[src].fattr[0] == 1.0) {
+        p.slot_tag = s;
+        p.write_tag = true;
+        ok = true;
+      }
+      if (!ok) { why = "unrecognised state write"; return false; }
+    }
+  }
+  if (!has_output) { why = "loss is not output 0"; return false; }
+  // the tag Switch: SWITCH(h_0 state, EQ(STATE_READ tag, 1))
+  for (const auto &o : g.ops)
+    if (o.func == 0 && o.kind == JOP_SWITCH && producer_origin(g, o.in_node[0]) >= 0) {
+      int s;
+      if (slot_of(g, o.in_node[0], &s) && s == p.slot_h[0] && g.ops[o.in_node[1]].kind == JOP_EQ) {
+        int ts;
+        if (slot_of(g, g.ops[o.in_node[1]].in_node[0], &ts)) p.slot_tag = ts;
+      }
+    }
+  // assumptions -> specialisation + device guards
+  int trip = -1, width = -1;
+  for (const auto &a : g.asms) {
+    if (a.kind == JA_TRIP_COUNT && a.target == 2) trip = (int)a.value;
+    if (a.kind == JA_RANGE && a.target == 2) width = (int)a.hi;
+    if (a.kind == JA_SHAPE_MATCH && a.target == 0 && a.ndim == 2) {
+      if (a.dims[0] != -1 && a.dims[0] != p.B) { why = "token batch != state batch"; return false; }
+      if (a.dims[1] != -1 && width < 0) width = (int)a.dims[1];
+    }
+    if (a.kind == JA_TYPE_TAG && a.target == p.slot_tag && a.value == 1) p.tag_specialised = true;
+  }
+  if (trip > 0) { p.T = trip; p.while_mode = false; }
+  else if (width > 0) { p.T = width; p.while_mode = true; }
+  else { why = "no TRIP_COUNT or bounded RANGE assumption on lengths"; return false; }
+  if (!p.tag_specialised && p.slot_tag < 0) { why = "state tag slot"; return false; }
+  for (const auto &a : g.asms) {
+    if (a.mode != JANUS_MODE_RUNTIME) continue;
+    LmPlan::RG r{};
+    r.id = a.id;
+    r.value = a.value; r.lo = a.lo; r.hi = a.hi; r.ref_arg = a.ref_arg; r.ref_dim = a.ref_dim;
+    r.arg = a.target; r.slot = -1;
+    if (a.kind == JA_TRIP_COUNT) r.kind = G_ALL_EQ;
+    else if (a.kind == JA_RANGE) r.kind = G_RANGE;
+    else if (a.kind == JA_VALUE_EQ) r.kind = G_FIRST_EQ;
+    else if (a.kind == JA_TYPE_TAG) { r.kind = G_FIRST_EQ; r.slot = a.target; r.arg = -1; }
+    else { why = "unsupported runtime assumption for this graph"; return false; }
+    if (g.opts.strip_asserts) continue;
+    p.runtime_guards.push_back(r);
+  }
+  if (g.opts.fail_assert_id >= 0)
+    for (const auto &a : g.asms)
+      if ((int)a.id == g.opts.fail_assert_id && a.mode == JANUS_MODE_RUNTIME) {
+        LmPlan::RG r{};
+        r.kind = G_FORCED; r.id = a.id; r.arg = -1; r.slot = -1;
+        p.runtime_guards.push_back(r);
+      }
+  if ((int)p.runtime_guards.size() > MAX_GUARDS) { why = "too many runtime guards"; return false; }
+  p.bf16 = g.opts.gemm_dtype != JANUS_F32;
+  if (g.opts.world_size > 1 && !p.bf16) { why = "fp32 path is single-GPU"; return false; }
+  // ------------------------------------------------------------------ workspace layout
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
+  p.off.status = take(sizeof(DevStatus));
+  p.nbar = 8;
+  p.off.barriers = take(p.nbar * sizeof(unsigned));
+  p.off.stage_args = take(3ull * p.B * p.T * sizeof(int));
+  const int B = p.B, T = p.T, H = p.H, E = p.E, V = p.V, G4 = 4 * p.H;
+  if (!p.bf16) {
+    p.off.small_ws = take(small_lm_ws_floats(V, E, H, p.L, B, T) * sizeof(float));
+  } else {
+    if (B > 128) { why = "batch > 128 (one TMEM tile of batch rows)"; return false; }
+    if (H % 2) { why = "odd hidden size"; return false; }
+    if (T * B > 8192) { why = "T*B > 8192"; return false; }
+    p.Ep = r8(E + 1);
+    p.Hp = r8(H + 1);
+    const int Vp = r8(V);
+    const size_t TB = (size_t)T * B;
+    for (int l = 0; l < p.L; ++l) {
+      const int Inp = l ? p.Hp : p.Ep;
+      p.off.Wih_b[l] = take((size_t)G4 * Inp * 2);
+      p.off.Whh_b[l] = take((size_t)G4 * p.Hp * 2);
+      p.off.WhhT_b[l] = take((size_t)H * G4 * 2);
+      p.off.bil[l] = take((size_t)G4 * 4);
+      p.off.Hs[l] = take((TB + B) * p.Hp * 2);
+      p.off.Cs[l] = take((TB + B) * p.Hp * 4);
+      p.off.G[l] = take(TB * G4 * 4);
+      p.off.DZ[l] = take(TB * G4 * 2);
+      p.off.dX[l] = take(TB * Inp * 4);
+      p.off.hT[l] = take((size_t)B * H * 4);
+      p.off.cT[l] = take((size_t)B * H * 4);
+      p.off.gWih[l] = take((size_t)G4 * Inp * 4);
+      p.off.gWhh[l] = take((size_t)G4 * p.Hp * 4);
+    }
+    p.off.Wdec_b = take((size_t)V * p.Hp * 2);
+    p.off.X = take(TB * p.Ep * 2);
+    p.off.logits = take(TB * Vp * 4);
+    p.off.dy = take(TB * Vp * 2);
+    p.off.rowloss = take(TB * 4);
+    p.off.dHtop = take(TB * p.Hp * 4);
+    p.off.gWdec = take((size_t)V * p.Hp * 4);
+    p.off.seg_word = take(TB * 4);
+    p.off.seg_start = take((TB + 1) * 4);
+    p.off.seg_grad = take(TB * p.Ep * 4);
+    p.off.nseg = take(16);
+    p.off.keys = take(TB * 8);
+  }
+  p.ws_bytes = o;
+  char buf[512];
+  snprintf(buf, sizeof buf,
+           "lstm_lm: L=%d V=%d E=%d H=%d B=%d %s=%d tag=%s path=%s guards=%zu "
+           "phases=[init,%sguards,cast,gather,{gemm_in,rec_fwd}xL,gemm_dec,xent,gemm_dWdec,"
+           "gemm_dh,{rec_bwd,gemm_dWhh,gemm_dWih,gemm_dx}xL,embed_grad,finalize,commit]",
+           p.L, p.V, p.E, p.H, p.B, p.while_mode ? "while_width" : "unrolled_T", p.T,
+           p.tag_specialised ? "specialised" : "device_switch", p.bf16 ? "tcgen05_bf16" : "fp32_single_cta",
+           p.runtime_guards.size(), p.while_mode ? "trip," : "");
+  g.describe = buf;
+  return true;
+}
+
+// ---------------------------------------------------------------------------------- run
+struct LmPtrs {
+  const int *tok, *tgt, *lens;
+  int W;
+  float *E, *Wih[4], *Whh[4], *b[4], *Wdec, *bdec, *h[4], *c[4];
+  int *tag;
+};
+
+static bool tensor_ok(const janus_tensor &t, int dtype, int64_t numel) {
+  if (!t.data || t.dtype != dtype) return false;
+  int64_t n = 1;
+  for (int k = 0; k < t.ndim; ++k) n *= t.shape[k];
+  return n == numel;
+}
+
+static GuardList make_guards(const LmPlan &p, const std::vector<LmPlan::RG> &rgs,
+                             const janus_tensor *args, const int *const *argp,
+                             const janus_tensor *state) {
+  GuardList gl{};
+  for (const auto &r : rgs) {
+    GuardDesc d{};
+    d.kind = r.kind;
+    d.id = r.id;
+    d.value = r.value; d.lo = r.lo; d.hi = r.hi;
+    if (r.kind == G_FORCED) { d.data = nullptr; d.n = 0; }
+    else if (r.slot >= 0) { d.data = static_cast<const int *>(state[r.slot].data); d.n = 1; }
+    else {
+      d.data = argp[r.arg];
+      int64_t n = 1;
+      for (int k = 0; k < args[r.arg].ndim; ++k) n *= args[r.arg].shape[k];
+      d.n = n;
+      if (r.kind == G_RANGE && r.ref_arg >= 0)
+        d.hi = std::min<int64_t>(d.hi, args[r.ref_arg].shape[r.ref_dim]);
+    }
+    gl.g[gl.n++] = d;
+  }
+  (void)p;
+  return gl;
+}
+
+janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_outs,
+                    cudaStream_t st, janus_failure *fail) {
+  if (!g.h_status && cudaMallocHost(&g.h_status, sizeof(DevStatus)) != cudaSuccess) return JANUS_ERR_CUDA;
+  if (n_outs > 0 && outs[0].data && is_device_ptr(outs[0].data))
+    if (cudaMemcpyAsync(outs[0].data, &dst->loss, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return JANUS_ERR_CUDA;
+  if (cudaMemcpyAsync(g.h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return JANUS_ERR_CUDA;
+  cudaError_t e = cudaStreamSynchronize(st);
+  g.host_syncs++;
+  if (e != cudaSuccess) return JANUS_ERR_CUDA;
+  const DevStatus &h = *g.h_status;
+  if (n_outs > 0 && outs[0].data && !is_device_ptr(outs[0].data))
+    *static_cast<float *>(outs[0].data) = h.loss;
+  if (h.status == JANUS_ASSUMPTION_FAILED) {
+    if (fail) {
+      fail->assumption_id = (uint32_t)(h.key >> IDX_BITS);
+      fail->rank = g.opts.rank;
+      const unsigned long long idx = h.key & ((1ull << IDX_BITS) - 1);
+      fail->index = idx == (1ull << IDX_BITS) - 1 ? -1 : (int64_t)idx;
+      fail->observed = h.observed;
+    }
+    return JANUS_ASSUMPTION_FAILED;
+  }
+  return h.status == 0 ? JANUS_OK : (janus_status)h.status;
+}
+
+#define LCHK(x)                                   \
+  do {                                            \
+    cudaError_t e_ = (x);                         \
+    g.launches++;                                 \
+    if (e_ != cudaSuccess) return JANUS_ERR_CUDA; \
+  } while (0)
+
+janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *state,
+                    const janus_tensor *outs, int n_outs, const janus_tensor &ws, cudaStream_t st,
+                    janus_failure *fail) {
+  const LmPlan &p = g.lm;
+  if (!ws.data || (size_t)ws.shape[0] * (ws.dtype == JANUS_U8 ? 1 : 4) < p.ws_bytes) return JANUS_ERR_INVALID;
+  uint8_t *W = static_cast<uint8_t *>(ws.data);
+  const int B = p.B, H = p.H, E = p.E, V = p.V, G4 = 4 * p.H, L = p.L;
+  // ---- arguments (stage host buffers into the workspace: the e2e path)
+  const int Wd = (int)args[0].shape[1];
+  if (args[0].ndim != 2 || args[0].shape[0] != B || Wd > p.T || (!p.while_mode && Wd != p.T))
+    return JANUS_ERR_INVALID;
+  const int *argp[3];
+  for (int a = 0; a < 3; ++a) {
+    const int64_t n = a < 2 ? (int64_t)B * Wd : B;
+    if (!tensor_ok(args[a], JANUS_I32, n)) return JANUS_ERR_INVALID;
+    if (is_device_ptr(args[a].data)) argp[a] = static_cast<const int *>(args[a].data);
+    else {
+      int *dstp = reinterpret_cast<int *>(W + p.off.stage_args) + (size_t)a * B * p.T;
+      if (cudaMemcpyAsync(dstp, args[a].data, n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return JANUS_ERR_CUDA;
+      argp[a] = dstp;
+    }
+  }
+  // ---- state slots
+  LmPtrs P{};
+  P.tok = argp[0]; P.tgt = argp[1]; P.lens = argp[2]; P.W = Wd;
+  auto sf = [&](int slot, int64_t n) -> float * {
+    if (slot < 0 || !tensor_ok(state[slot], JANUS_F32, n) || !is_device_ptr(state[slot].data)) return nullptr;
+    return static_cast<float *>(state[slot].data);
+  };
+  if (!(P.E = sf(p.slot_E, (int64_t)V * E))) return JANUS_ERR_INVALID;
+  for (int l = 0; l < L; ++l) {
+    const int In = l ? H : E;
+    if (!(P.Wih[l] = sf(p.slot_Wih[l], (int64_t)G4 * In)) || !(P.Whh[l] = sf(p.slot_Whh[l], (int64_t)G4 * H)) ||
+        !(P.b[l] = sf(p.slot_b[l], G4)) || !(P.h[l] = sf(p.slot_h[l], (int64_t)B * H)) ||
+        !(P.c[l] = sf(p.slot_c[l], (int64_t)B * H)))
+      return JANUS_ERR_INVALID;
+  }
+  if (!(P.Wdec = sf(p.slot_Wdec, (int64_t)V * H)) || !(P.bdec = sf(p.slot_bdec, V))) return JANUS_ERR_INVALID;
+  P.tag = p.slot_tag >= 0 ? static_cast<int *>(state[p.slot_tag].data) : nullptr;
+  DevStatus *dst = reinterpret_cast<DevStatus *>(W + p.off.status);
+  unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
+  GuardList gl = make_guards(p, p.runtime_guards, args, argp, state);
+
+  if (!p.bf16) {
+    // ------------------------------------------------------------ single-CTA fp32 program
+    SmallLmArgs a;
+    a.V = V; a.E = E; a.H = H; a.L = L; a.B = B; a.W = Wd; a.T = p.while_mode ? Wd : p.T;
+    a.tok = P.tok; a.tgt = P.tgt; a.lens = p.while_mode ? P.lens : nullptr;
+    a.Emb = P.E; a.Wdec = P.Wdec; a.bdec = P.bdec; a.tag = p.write_tag ? P.tag : nullptr;
+    a.tag_specialised = p.tag_specialised;
+    if (!p.tag_specialised) a.tag = P.tag;
+    for (int l = 0; l < L; ++l) {
+      a.Wih[l] = P.Wih[l]; a.Whh[l] = P.Whh[l]; a.bias[l] = P.b[l]; a.h[l] = P.h[l]; a.c[l] = P.c[l];
+      a.upd_Wih[l] = p.lr_Wih[l] != 0; a.upd_Whh[l] = p.lr_Whh[l] != 0; a.upd_b[l] = p.lr_b[l] != 0;
+    }
+    a.upd_E = p.lr_E != 0; a.upd_Wdec = p.lr_Wdec != 0; a.upd_bdec = p.lr_bdec != 0;
+    float lr = 0;
+    for (float v : {p.lr_E, p.lr_Wdec, p.lr_bdec, p.lr_Wih[0], p.lr_Whh[0], p.lr_b[0]}) if (v != 0) lr = v;
+    a.lr = lr;
+    a.gl = gl;
+    a.ws = reinterpret_cast<float *>(W + p.off.small_ws);
+    a.st = dst;
+    LCHK(launch_small_lm(a, st));
+    return finish(g, dst, outs, n_outs, st, fail);
+  }
+
+  // ------------------------------------------------------------ tcgen05 device program
+  const int T = p.T;              // unrolled T or max width W
+  const int Tw = p.while_mode ? Wd : T;  // width of this batch
+  const int TB = Tw * B;
+  const int Vp = r8(V), Ep = p.Ep, Hp = p.Hp;
+  const int *Tdev = p.while_mode ? &dst->trip : nullptr;
+  auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16 *>(W + off); };
+  auto fp = [&](size_t off) { return reinterpret_cast<float *>(W + off); };
+  LCHK(launch_step_init(dst, bars, p.nbar, st));
+  if (p.while_mode) LCHK(launch_trip(P.lens, B, Tw, dst, st));
+  if (gl.n) LCHK(launch_guards(gl, dst, st));
+  // operand copies (R1): interleaved / transposed bf16 working copies of the fp32 masters
+  for (int l = 0; l < L; ++l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    LCHK(launch_cast_rows(P.Wih[l], G4, In, In, bf(p.off.Wih_b[l]), Inp, H, st));
+    LCHK(launch_cast_rows(P.Whh[l], G4, H, H, bf(p.off.Whh_b[l]), Hp, H, st));
+    LCHK(launch_cast_transpose_interleaved(P.Whh[l], H, bf(p.off.WhhT_b[l]), G4, st));
+    LCHK(launch_bias_interleave(P.b[l], H, fp(p.off.bil[l]), st));
+    LCHK(launch_fill_col(bf(p.off.Hs[l]), TB + B, Hp, H, 1.f, Hp, st));
+  }
+  LCHK(launch_cast_rows(P.Wdec, V, H, H, bf(p.off.Wdec_b), Hp, 0, st));
+  LCHK(launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
+  // forward
+  for (int l = 0; l < L; ++l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    GemmOp op;
+    op.M = TB; op.N = G4; op.K = In;
+    op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
+    op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
+    op.ep.C = fp(p.off.G[l]); op.ep.ldc = G4; op.ep.bias_col = fp(p.off.bil[l]);
+    LCHK(gemm_bf16(op, st));
+    RecFwdArgs ra;
+    ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
+    ra.G = fp(p.off.G[l]); ra.Hs = bf(p.off.Hs[l]); ra.Cs = fp(p.off.Cs[l]); ra.ldh = Hp;
+    ra.h0 = P.h[l]; ra.c0 = P.c[l]; ra.hT = fp(p.off.hT[l]); ra.cT = fp(p.off.cT[l]);
+    ra.barrier = bars + l; ra.fail = nullptr;
+    ra.tag = p.tag_specialised ? nullptr : P.tag;
+    LCHK(lstm_rec_fwd(ra, bf(p.off.Whh_b[l]), Hp, p.while_mode, st));
+  }
+  {
+    GemmOp op;  // decoder logits
+    op.M = TB; op.N = V; op.K = H;
+    op.A = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.lda = Hp;
+    op.B = bf(p.off.Wdec_b); op.ldb = Hp;
+    op.ep.C = fp(p.off.logits); op.ep.ldc = Vp; op.ep.bias_col = P.bdec;
+    LCHK(gemm_bf16(op, st));
+  }
+  LCHK(launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
+                   (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
+  {
+    GemmOp op;  // dW_dec | db_dec = dy^T [h_top | 1]
+    op.M = V; op.N = H + 1; op.K = TB;
+    op.A = bf(p.off.dy); op.lda = Vp; op.a_mn = 1;
+    op.B = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.ldb = Hp; op.b_mn = 1;
+    op.ep.C = fp(p.off.gWdec); op.ep.ldc = Hp;
+    LCHK(gemm_bf16(op, st));
+    GemmOp o2;  // dh_top = dy W_dec
+    o2.M = TB; o2.N = H; o2.K = V;
+    o2.A = bf(p.off.dy); o2.lda = Vp;
+    o2.B = bf(p.off.Wdec_b); o2.ldb = Hp; o2.b_mn = 1;
+    o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
+    LCHK(gemm_bf16(o2, st));
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    RecBwdArgs rb;
+    rb.B = B; rb.H = H; rb.T = Tw; rb.T_dev = Tdev; rb.lens = p.while_mode ? P.lens : nullptr;
+    rb.G = fp(p.off.G[l]); rb.Cs = fp(p.off.Cs[l]); rb.ldh = Hp;
+    rb.dHin = l == L - 1 ? fp(p.off.dHtop) : fp(p.off.dX[l + 1]); rb.ldd = Hp;
+    rb.DZ = bf(p.off.DZ[l]); rb.barrier = bars + L + l;
+    LCHK(lstm_rec_bwd(rb, bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
+    const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
+    GemmOp a;  // dW_hh = dz^T h_{t-1}
+    a.M = G4; a.N = H; a.K = TB;
+    a.A = bf(p.off.DZ[l]); a.lda = G4; a.a_mn = 1;
+    a.B = bf(p.off.Hs[l]); a.ldb = Hp; a.b_mn = 1;
+    a.ep.C = fp(p.off.gWhh[l]); a.ep.ldc = Hp;
+    LCHK(gemm_bf16(a, st));
+    GemmOp b2;  // dW_ih | db = dz^T [x | 1]
+    b2.M = G4; b2.N = In + 1; b2.K = TB;
+    b2.A = bf(p.off.DZ[l]); b2.lda = G4; b2.a_mn = 1;
+    b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
+    b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
+    LCHK(gemm_bf16(b2, st));
+    if (l > 0 || p.lr_E != 0) {
+      GemmOp c2;  // dx = dz W_ih
+      c2.M = TB; c2.N = In; c2.K = G4;
+      c2.A = bf(p.off.DZ[l]); c2.lda = G4;
+      c2.B = bf(p.off.Wih_b[l]); c2.ldb = Inp; c2.b_mn = 1;
+      c2.ep.C = fp(p.off.dX[l]); c2.ep.ldc = Inp;
+      LCHK(gemm_bf16(c2, st));
+    }
+  }
+  int *seg_word = reinterpret_cast<int *>(W + p.off.seg_word);
+  int *nseg = reinterpret_cast<int *>(W + p.off.nseg);
+  if (p.lr_E != 0) {
+    LCHK(launch_embed_grad(P.tok, B, Wd, Tw, Tdev, fp(p.off.dX[0]), Ep, E, seg_word,
+                           reinterpret_cast<int *>(W + p.off.seg_start), fp(p.off.seg_grad), Ep,
+                           nseg, reinterpret_cast<unsigned long long *>(W + p.off.keys), st));
+    g.launches++;  // embed grad is two kernels
+  }
+  LCHK(launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
+  // ---- the all-or-nothing commit (P:164, P:266 (4))
+  CommitList cl{};
+  auto add = [&](CommitSeg s) { cl.s[cl.n++] = s; };
+  const float nr = (float)g.opts.world_size;
+  for (int l = 0; l < L; ++l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    CommitSeg s{};
+    if (p.lr_Wih[l] != 0) { s = {}; s.kind = C_DENSE_IL; s.dst = P.Wih[l]; s.grad = fp(p.off.gWih[l]); s.rows = G4; s.cols = In; s.ldg = Inp; s.H = H; s.lr = p.lr_Wih[l] / nr; add(s); }
+    if (p.lr_b[l] != 0) { s = {}; s.kind = C_BIAS_COL_IL; s.dst = P.b[l]; s.grad = fp(p.off.gWih[l]); s.rows = G4; s.cols = 1; s.ldg = Inp; s.col = In; s.H = H; s.lr = p.lr_b[l] / nr; add(s); }
+    if (p.lr_Whh[l] != 0) { s = {}; s.kind = C_DENSE_IL; s.dst = P.Whh[l]; s.grad = fp(p.off.gWhh[l]); s.rows = G4; s.cols = H; s.ldg = Hp; s.H = H; s.lr = p.lr_Whh[l] / nr; add(s); }
+    if (p.write_h) {
+      s = {}; s.kind = C_COPY; s.dst = P.h[l]; s.grad = fp(p.off.hT[l]); s.rows = B; s.cols = H; add(s);
+      s = {}; s.kind = C_COPY; s.dst = P.c[l]; s.grad = fp(p.off.cT[l]); s.rows = B; s.cols = H; add(s);
+    }
+  }
+  {
+    CommitSeg s{};
+    if (p.lr_Wdec != 0) { s = {}; s.kind = C_DENSE; s.dst = P.Wdec; s.grad = fp(p.off.gWdec); s.rows = V; s.cols = H; s.ldg = Hp; s.lr = p.lr_Wdec / nr; add(s); }
+    if (p.lr_bdec != 0) { s = {}; s.kind = C_BIAS_COL; s.dst = P.bdec; s.grad = fp(p.off.gWdec); s.rows = V; s.cols = 1; s.ldg = Hp; s.col = H; s.lr = p.lr_bdec / nr; add(s); }
+    if (p.lr_E != 0) { s = {}; s.kind = C_SPARSE_ROWS; s.dst = P.E; s.grad = fp(p.off.seg_grad); s.cols = E; s.ldg = Ep; s.rows_idx = seg_word; s.nrows = nseg; s.lr = p.lr_E / nr; add(s); }
+    if (p.write_tag && P.tag) { s = {}; s.kind = C_TAG; s.idst = P.tag; s.ival = 1; add(s); }
+  }
+  LCHK(launch_commit(cl, dst, st));
+  return finish(g, dst, outs, n_outs, st, fail);
+}
+
+}  // namespace jk

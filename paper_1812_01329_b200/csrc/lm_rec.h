@@ -1,0 +1,44 @@
+// lm_rec.h — persistent recurrent LSTM kernels (lm_rec.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace jk {
+
+struct RecFwdArgs {
+  int B = 0, H = 0, T = 0;       // T = steps (unrolled) or the max width (While mode)
+  const int *T_dev = nullptr;    // While mode: device-resident trip count (nullptr: use T)
+  const int *lens = nullptr;     // While mode: per-row lengths (rows t >= len carry h, c)
+  float *G = nullptr;            // [T*B][4H] input projection + bias (interleaved); overwritten
+                                 // with the gate activations (i, f, g, o) for backward
+  __nv_bfloat16 *Hs = nullptr;   // [(T+1)*B][ldh] h (bf16); row block 0 = h0
+  float *Cs = nullptr;           // [(T+1)*B][ldh] c (fp32); row block 0 = c0
+  int ldh = 0;
+  const float *h0 = nullptr, *c0 = nullptr;  // [B][H] initial state (fp32)
+  float *hT = nullptr, *cT = nullptr;        // [B][H] final state (fp32)
+  unsigned int *barrier = nullptr;           // zeroed before the launch
+  const int *fail = nullptr;                 // nonzero: skip (cooperative cancellation)
+  const int *tag = nullptr;                  // state type tag; != 1 -> h0 = c0 = 0 (device Switch)
+};
+
+struct RecBwdArgs {
+  int B = 0, H = 0, T = 0;
+  const int *T_dev = nullptr;
+  const int *lens = nullptr;
+  const float *G = nullptr;       // gate activations from the forward kernel
+  const float *Cs = nullptr;      // c history
+  int ldh = 0;
+  const float *dHin = nullptr;    // [T*B][ldd] gradient into h_t from above (decoder / next layer)
+  int ldd = 0;
+  __nv_bfloat16 *DZ = nullptr;    // [T*B][4H] out: rb(dz), interleaved columns
+  unsigned int *barrier = nullptr;
+  const int *fail = nullptr;
+};
+
+int rec_grid(int H);
+cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw, bool masked,
+                         cudaStream_t st);
+cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
+                         cudaStream_t st);
+
+}  // namespace jk

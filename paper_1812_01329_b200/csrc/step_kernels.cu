@@ -1,0 +1,455 @@
+// step_kernels.cu — SIMT phases of the speculative training step (see step_kernels.h).
+// HBM-bound work: 128-bit / coalesced access, grids sized in multiples of the SM count.
+#include "common.cuh"
+#include "step_kernels.h"
+
+namespace jk {
+
+static constexpr int NSM = 148;
+
+// ------------------------------------------------------------------------------ init / guards
+__global__ void step_init_kernel(DevStatus *st, unsigned int *bar, int nbar) {
+  const int i = threadIdx.x;
+  if (i == 0) {
+    st->key = KEY_PASS;
+    st->observed = 0;
+    st->runtime_err = 0;
+    st->status = 0;
+    st->loss = 0.f;
+    st->trip = 0;
+    st->flags = 0;
+  }
+  for (int k = i; k < nbar; k += blockDim.x) bar[k] = 0;
+}
+
+cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s) {
+  step_init_kernel<<<1, 256, 0, s>>>(st, barriers, nbar);
+  return cudaGetLastError();
+}
+
+// One block per assumption; each failing element proposes (id << 40 | index) to an atomicMin,
+// so the reported failure is the minimum id and, within it, the first element (reading Q9).
+__global__ void guards_kernel(GuardList gl, DevStatus *st) {
+  const GuardDesc g = gl.g[blockIdx.x];
+  const unsigned long long mask = (1ull << IDX_BITS) - 1;
+  if (g.kind == G_FORCED) {
+    if (threadIdx.x == 0) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | mask);
+    return;
+  }
+  const long long n = g.kind == G_FIRST_EQ ? 1 : g.n;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const long long v = g.data[i];
+    bool bad = false;
+    if (g.kind == G_ALL_EQ || g.kind == G_FIRST_EQ) bad = v != g.value;
+    else if (g.kind == G_RANGE) bad = v < g.lo || v > g.hi;
+    if (bad) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | (unsigned long long)i);
+  }
+}
+
+cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s) {
+  if (gl.n <= 0) return cudaSuccess;
+  guards_kernel<<<gl.n, 128, 0, s>>>(gl, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ gather
+// one warp per row; X[t*B+b][k] = rb(E[id][k]); ones column at k = Edim.
+__global__ void gather_kernel(const float *__restrict__ E, int V, int Edim, const int *__restrict__ tok,
+                              int B, int W, int T, const int *T_dev, __nv_bfloat16 *X, int ldx,
+                              DevStatus *st) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int rows = T * B;
+  const int Tb = T_dev ? *T_dev : T;
+  for (int r = warp; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const int t = r / B, b = r - t * B;
+    int id = tok[(size_t)b * W + t];
+    if (id < 0 || id >= V) {
+      if (lane == 0 && t < Tb) atomicOr(reinterpret_cast<unsigned int *>(&st->runtime_err), 1u);
+      id = 0;
+    }
+    const float *src = E + (size_t)id * Edim;
+    __nv_bfloat16 *dst = X + (size_t)r * ldx;
+    if ((Edim & 3) == 0) {
+      for (int k = lane * 4; k < Edim; k += 128) {
+        const float4 v = *reinterpret_cast<const float4 *>(src + k);
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), c = __floats2bfloat162_rn(v.z, v.w);
+        *reinterpret_cast<__nv_bfloat162 *>(dst + k) = a;
+        *reinterpret_cast<__nv_bfloat162 *>(dst + k + 2) = c;
+      }
+    } else {
+      for (int k = lane; k < Edim; k += 32) dst[k] = __float2bfloat16_rn(src[k]);
+    }
+    for (int k = Edim + lane; k < ldx; k += 32) dst[k] = __float2bfloat16_rn(k == Edim ? 1.f : 0.f);
+  }
+}
+
+cudaError_t launch_gather(const float *E, int V, int Edim, const int *tok, int B, int W, int T,
+                          const int *T_dev, __nv_bfloat16 *X, int ldx, DevStatus *st,
+                          cudaStream_t s) {
+  const int rows = T * B;
+  int blocks = (rows * 32 + 255) / 256;
+  blocks = blocks < 4 * NSM ? blocks : 4 * NSM;
+  gather_kernel<<<blocks, 256, 0, s>>>(E, V, Edim, tok, B, W, T, T_dev, X, ldx, st);
+  return cudaGetLastError();
+}
+
+__global__ void trip_kernel(const int *lens, int B, int W, DevStatus *st) {
+  if (threadIdx.x == 0) {
+    int T = 0;
+    for (int b = 0; b < B; ++b) T = max(T, lens[b]);
+    st->trip = min(max(T, 0), W);
+  }
+}
+cudaError_t launch_trip(const int *lens, int B, int W, DevStatus *st, cudaStream_t s) {
+  trip_kernel<<<1, 32, 0, s>>>(lens, B, W, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ casts
+__global__ void cast_rows_kernel(const float *__restrict__ src, int R, int Cc, int ld_src,
+                                 __nv_bfloat16 *dst, int ld_dst, int H) {
+  const long long n = (long long)R * ld_dst;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / ld_dst), k = (int)(e - (long long)r * ld_dst);
+    const int rs = H > 0 ? (r & 3) * H + (r >> 2) : r;  // interleaved row 4u+g <- g*H+u
+    dst[e] = __float2bfloat16_rn(k < Cc ? src[(size_t)rs * ld_src + k] : 0.f);
+  }
+}
+
+cudaError_t launch_cast_rows(const float *src, int R, int Cc, int ld_src, __nv_bfloat16 *dst,
+                             int ld_dst, int interleave_H, cudaStream_t s) {
+  cast_rows_kernel<<<8 * NSM, 256, 0, s>>>(src, R, Cc, ld_src, dst, ld_dst, interleave_H);
+  return cudaGetLastError();
+}
+
+// WT[u][ri] = rb(W[rc][u]),  ri = 4u'+g <-> rc = g*H+u'.  32x32 smem tiles.
+__global__ void cast_transpose_il_kernel(const float *__restrict__ W, int H, __nv_bfloat16 *WT,
+                                         int ldwt) {
+  __shared__ float tile[32][33];
+  const int ri0 = blockIdx.x * 32, u0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int ri = ri0 + i, u = u0 + tx;
+    float v = 0.f;
+    if (ri < 4 * H && u < H) v = W[(size_t)((ri & 3) * H + (ri >> 2)) * H + u];
+    tile[i][tx] = v;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int u = u0 + i, ri = ri0 + tx;
+    if (u < H && ri < 4 * H) WT[(size_t)u * ldwt + ri] = __float2bfloat16_rn(tile[tx][i]);
+  }
+}
+
+cudaError_t launch_cast_transpose_interleaved(const float *W, int H, __nv_bfloat16 *WT, int ldwt,
+                                              cudaStream_t s) {
+  dim3 grid((4 * H + 31) / 32, (H + 31) / 32);
+  cast_transpose_il_kernel<<<grid, dim3(32, 8), 0, s>>>(W, H, WT, ldwt);
+  return cudaGetLastError();
+}
+
+__global__ void bias_il_kernel(const float *b, int H, float *out) {
+  for (int ri = blockIdx.x * blockDim.x + threadIdx.x; ri < 4 * H; ri += gridDim.x * blockDim.x)
+    out[ri] = b[(ri & 3) * H + (ri >> 2)];
+}
+cudaError_t launch_bias_interleave(const float *b, int H, float *out, cudaStream_t s) {
+  bias_il_kernel<<<(4 * H + 255) / 256, 256, 0, s>>>(b, H, out);
+  return cudaGetLastError();
+}
+
+__global__ void fill_col_kernel(__nv_bfloat16 *X, int rows, int ld, int col, float v, int zero_to) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    X[(size_t)r * ld + col] = __float2bfloat16_rn(v);
+    for (int k = col + 1; k < zero_to; ++k) X[(size_t)r * ld + k] = __float2bfloat16_rn(0.f);
+  }
+}
+cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v, int zero_to,
+                            cudaStream_t s) {
+  fill_col_kernel<<<(rows + 255) / 256, 256, 0, s>>>(X, rows, ld, col, v, zero_to);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ xent
+template <int NT>
+__device__ float block_reduce(float v, float *sh, bool is_max) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float x = __shfl_xor_sync(0xffffffff, v, o);
+    v = is_max ? fmaxf(v, x) : v + x;
+  }
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < NT / 32 ? sh[lane] : (is_max ? -INFINITY : 0.f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float x = __shfl_xor_sync(0xffffffff, v, o);
+      v = is_max ? fmaxf(v, x) : v + x;
+    }
+    if (lane == 0) sh[32] = v;
+  }
+  __syncthreads();
+  const float r = sh[32];
+  __syncthreads();
+  return r;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) xent_kernel(const float *__restrict__ logits, int V, int ldl, int rows,
+                                                  const int *__restrict__ tgt, int B, int W,
+                                                  const int *lens, const int *T_dev, float n_valid,
+                                                  __nv_bfloat16 *dy, int lddy, float *rowloss,
+                                                  DevStatus *st) {
+  __shared__ float sh[33];
+  __shared__ float s_nv;
+  const int Tb = T_dev ? *T_dev : rows / B;
+  if (lens && threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < B; ++b) acc += min(lens[b], Tb);
+    s_nv = (float)max(acc, 1);
+  }
+  __syncthreads();
+  const float nv = lens ? s_nv : n_valid;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int t = r / B, b = r - t * B;
+    const bool valid = t < Tb && (!lens || t < lens[b]);
+    const float *y = logits + (size_t)r * ldl;
+    __nv_bfloat16 *d = dy + (size_t)r * lddy;
+    if (!valid) {
+      for (int k = threadIdx.x; k < V; k += NT) d[k] = __float2bfloat16_rn(0.f);
+      if (threadIdx.x == 0) rowloss[r] = 0.f;
+      continue;
+    }
+    int tg = tgt[(size_t)b * W + t];
+    if (tg < 0 || tg >= V) {
+      if (threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned int *>(&st->runtime_err), 2u);
+      tg = 0;
+    }
+    float m = -INFINITY;
+    for (int k = threadIdx.x; k < V; k += NT) m = fmaxf(m, y[k]);
+    m = block_reduce<NT>(m, sh, true);
+    float sum = 0.f;
+    for (int k = threadIdx.x; k < V; k += NT) sum += expf(y[k] - m);
+    sum = block_reduce<NT>(sum, sh, false);
+    const float lse = m + logf(sum);
+    const float inv = 1.f / nv;
+    for (int k = threadIdx.x; k < V; k += NT) {
+      const float p = expf(y[k] - lse) - (k == tg ? 1.f : 0.f);
+      d[k] = __float2bfloat16_rn(p * inv);
+    }
+    if (threadIdx.x == 0) rowloss[r] = (lse - y[tg]) * inv;
+  }
+}
+
+cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
+                        const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
+                        int lddy, float *rowloss, DevStatus *st, cudaStream_t s) {
+  int blocks = rows < 8 * NSM ? rows : 8 * NSM;
+  xent_kernel<256><<<blocks, 256, 0, s>>>(logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
+                                          lddy, rowloss, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ embedding grad
+// Single block: bitonic sort of (id << 32 | r) over r < Tb*B (time-major rows), then segment
+// starts by a block scan. Deterministic (no atomics in the accumulation order).
+constexpr int EG_MAX = 8192;
+__global__ void __launch_bounds__(1024) embed_sort_kernel(const int *tok, int B, int W, int T,
+                                                          const int *T_dev, int *seg_word,
+                                                          int *seg_start, int *nseg,
+                                                          unsigned long long *keys) {
+  extern __shared__ unsigned long long sk[];
+  __shared__ int warp_sums[32];
+  const int Tb = T_dev ? *T_dev : T;
+  const int n = Tb * B;
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    if (i < n) {
+      const int t = i / B, b = i - t * B;
+      sk[i] = ((unsigned long long)(unsigned)tok[(size_t)b * W + t] << 32) | (unsigned)i;
+    } else {
+      sk[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long a = sk[i], c = sk[ixj];
+          if ((a > c) == up) { sk[i] = c; sk[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // segment starts: flag, then exclusive scan (chunked per thread, block-wide)
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = min(n, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i)
+    cnt += (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) ? 1 : 0;
+  // block exclusive scan of cnt
+  int v = cnt;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffff, v, o);
+    if (lane >= o) v += x;
+  }
+  if (lane == 31) warp_sums[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int x = __shfl_up_sync(0xffffffff, ws, o);
+      if (lane >= o) ws += x;
+    }
+    warp_sums[lane] = ws;
+  }
+  __syncthreads();
+  int base = v - cnt + (w > 0 ? warp_sums[w - 1] : 0);
+  for (int i = lo; i < hi; ++i) {
+    if (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) {
+      seg_word[base] = (int)(sk[i] >> 32);
+      seg_start[base] = i;
+      ++base;
+    }
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    *nseg = base;
+    seg_start[base] = n;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = sk[i];
+}
+
+__global__ void embed_segsum_kernel(const unsigned long long *keys, const int *seg_start,
+                                    const int *nseg, const float *__restrict__ dX, int ldx, int Edim,
+                                    float *seg_grad, int ldg) {
+  const int ns = *nseg;
+  for (int sgi = blockIdx.x; sgi < ns; sgi += gridDim.x) {
+    const int a = seg_start[sgi], e = seg_start[sgi + 1];
+    for (int k = threadIdx.x; k < Edim; k += blockDim.x) {
+      float acc = 0.f;
+      for (int i = a; i < e; ++i) acc += dX[(size_t)(keys[i] & 0xffffffffu) * ldx + k];
+      seg_grad[(size_t)sgi * ldg + k] = acc;
+    }
+  }
+}
+
+cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev,
+                              const float *dX, int ldx, int Edim, int *seg_word, int *seg_start,
+                              float *seg_grad, int ldg, int *nseg,
+                              unsigned long long *keys_scratch, cudaStream_t s) {
+  int np = 1;
+  while (np < T * B) np <<= 1;
+  if (np > EG_MAX) return cudaErrorInvalidValue;
+  const int smem = np * 8;
+  cudaError_t e = cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  embed_sort_kernel<<<1, 1024, smem, s>>>(tok, B, W, T, T_dev, seg_word, seg_start, nseg, keys_scratch);
+  embed_segsum_kernel<<<4 * NSM, 256, 0, s>>>(keys_scratch, seg_start, nseg, dX, ldx, Edim, seg_grad, ldg);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ finalize
+__global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, DevStatus *st) {
+  __shared__ float sh[1024];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) acc += rowloss[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->loss = sh[0];
+    const unsigned long long key = st->key;
+    if (key != KEY_PASS) {
+      st->status = 1;  // JANUS_ASSUMPTION_FAILED
+      const unsigned id = (unsigned)(key >> IDX_BITS);
+      const unsigned long long idx = key & ((1ull << IDX_BITS) - 1);
+      long long obs = -1;
+      if (idx != (1ull << IDX_BITS) - 1)
+        for (int k = 0; k < gl.n; ++k)
+          if (gl.g[k].id == id && gl.g[k].kind != G_FORCED) obs = gl.g[k].data[idx];
+      st->observed = obs;
+    } else if (st->runtime_err) {
+      st->status = 4;  // JANUS_ERR_RUNTIME
+    } else {
+      st->status = 0;
+    }
+  }
+}
+
+cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
+                            int world_size, cudaStream_t s) {
+  (void)world_size;
+  finalize_kernel<<<1, 1024, 0, s>>>(rowloss, rows, gl, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ commit
+// Predicated on the device status: with any failure nothing is written (all-or-nothing).
+__global__ void commit_kernel(CommitList cl, const DevStatus *st) {
+  if (st->status != 0) return;
+  const CommitSeg sg = cl.s[blockIdx.y];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  switch (sg.kind) {
+    case C_DENSE: {
+      const long long n = (long long)sg.rows * sg.cols;
+      for (long long e = tid; e < n; e += stride) {
+        const int r = (int)(e / sg.cols), k = (int)(e - (long long)r * sg.cols);
+        sg.dst[e] -= sg.lr * sg.grad[(size_t)r * sg.ldg + k];
+      }
+    } break;
+    case C_DENSE_IL: {
+      const long long n = (long long)sg.rows * sg.cols;
+      for (long long e = tid; e < n; e += stride) {
+        const int rc = (int)(e / sg.cols), k = (int)(e - (long long)rc * sg.cols);
+        const int ri = 4 * (rc % sg.H) + rc / sg.H;
+        sg.dst[e] -= sg.lr * sg.grad[(size_t)ri * sg.ldg + k];
+      }
+    } break;
+    case C_BIAS_COL:
+      for (long long e = tid; e < sg.rows; e += stride)
+        sg.dst[e] -= sg.lr * sg.grad[(size_t)e * sg.ldg + sg.col];
+      break;
+    case C_BIAS_COL_IL:
+      for (long long e = tid; e < sg.rows; e += stride) {
+        const int rc = (int)e, ri = 4 * (rc % sg.H) + rc / sg.H;
+        sg.dst[e] -= sg.lr * sg.grad[(size_t)ri * sg.ldg + sg.col];
+      }
+      break;
+    case C_COPY: {
+      const long long n = (long long)sg.rows * sg.cols;
+      for (long long e = tid; e < n; e += stride) sg.dst[e] = sg.grad[e];
+    } break;
+    case C_TAG:
+      if (tid == 0) *sg.idst = sg.ival;
+      break;
+    case C_SPARSE_ROWS: {
+      const long long n = (long long)(*sg.nrows) * sg.cols;
+      for (long long e = tid; e < n; e += stride) {
+        const int k = (int)(e / sg.cols), j = (int)(e - (long long)k * sg.cols);
+        sg.dst[(size_t)sg.rows_idx[k] * sg.cols + j] -= sg.lr * sg.grad[(size_t)k * sg.ldg + j];
+      }
+    } break;
+  }
+}
+
+cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s) {
+  if (cl.n <= 0) return cudaSuccess;
+  commit_kernel<<<dim3(2 * NSM, cl.n), 256, 0, s>>>(cl, st);
+  return cudaGetLastError();
+}
+
+}  // namespace jk

@@ -1,0 +1,104 @@
+// step_kernels.h — SIMT kernels of the speculative step: status/guards (AssertOps), operand
+// preparation, embedding gather, softmax cross-entropy, embedding-gradient segmented sum,
+// loss/status finalisation and the predicated all-or-nothing commit.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace jk {
+
+// Device status word (16-byte aligned; copied to the host once per step).
+struct DevStatus {
+  unsigned long long key;  // min over failing (assumption_id << 40 | element index); ~0 = pass
+  long long observed;      // value of the failing element (filled by finalize)
+  int runtime_err;         // nonzero: runtime error in a node (bad id) -> ERR_RUNTIME
+  int status;              // janus_status computed on the device (OK / ASSUMPTION_FAILED / RUNTIME)
+  float loss;
+  int trip;                // device trip count of the While loop (diagnostic)
+  unsigned int flags;
+  int pad[3];
+};
+static_assert(sizeof(DevStatus) == 48, "DevStatus layout");
+
+constexpr unsigned long long KEY_PASS = ~0ull;
+constexpr int IDX_BITS = 40;
+
+// A RUNTIME assumption evaluated on the device (AssertOp).
+enum GuardKind { G_ALL_EQ = 0, G_FIRST_EQ = 1, G_RANGE = 2, G_FORCED = 3 };
+struct GuardDesc {
+  int kind;
+  unsigned int id;
+  const int *data;
+  long long n;
+  long long value, lo, hi;
+};
+constexpr int MAX_GUARDS = 8;
+struct GuardList {
+  int n;
+  GuardDesc g[MAX_GUARDS];
+};
+
+cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s);
+cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s);
+
+// gather X[t*B+b] = rb(E[tok[b][t]]) (bf16, ld) with X[:, E] = 1 (ones column for bias grads);
+// ids outside [0,V) set runtime_err and read row 0.
+cudaError_t launch_gather(const float *E, int V, int Edim, const int *tok, int B, int W, int T,
+                          const int *T_dev, __nv_bfloat16 *X, int ldx, DevStatus *st,
+                          cudaStream_t s);
+// While mode: device trip count st->trip = min(max(lens), W) (the LoopCond bound).
+cudaError_t launch_trip(const int *lens, int B, int W, DevStatus *st, cudaStream_t s);
+
+// x (fp32, canonical rows) -> bf16 copies: interleaved rows (4u+g <- g*H+u) and/or transposed.
+cudaError_t launch_cast_rows(const float *src, int R, int Cc, int ld_src, __nv_bfloat16 *dst,
+                             int ld_dst, int interleave_H, cudaStream_t s);
+cudaError_t launch_cast_transpose_interleaved(const float *W, int H, __nv_bfloat16 *WT, int ldwt,
+                                              cudaStream_t s);
+cudaError_t launch_bias_interleave(const float *b, int H, float *out, cudaStream_t s);
+cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v, int zero_to,
+                            cudaStream_t s);
+
+// per-row softmax cross-entropy: rowloss[r], dy = mask (softmax - onehot) / n_valid (bf16).
+// Row r = t*B + b targets tgt[b][t]; in While mode rows with t >= len_b (or t >= *T_dev) are
+// masked. n_valid: host constant, or computed from lens on the device when lens != nullptr.
+cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
+                        const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
+                        int lddy, float *rowloss, DevStatus *st, cudaStream_t s);
+
+// embedding gradient: sort (id, r) keys, segment sums of dX rows in ascending r.
+// seg_word[k], seg_grad[k][ldg] for k < *nseg.
+cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev,
+                              const float *dX, int ldx, int Edim, int *seg_word, int *seg_start,
+                              float *seg_grad, int ldg, int *nseg,
+                              unsigned long long *keys_scratch, cudaStream_t s);
+
+// loss = sum(rowloss) / n_valid... rowloss already carries the 1/n_valid scale; status decode.
+cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
+                            int world_size, cudaStream_t s);
+
+// commit segments (P:164 all-or-nothing, P:282 deferred update)
+enum CommitKind { C_DENSE = 0, C_DENSE_IL = 1, C_BIAS_COL = 2, C_BIAS_COL_IL = 3, C_COPY = 4,
+                  C_TAG = 5, C_SPARSE_ROWS = 6 };
+struct CommitSeg {
+  int kind;
+  float *dst;          // master (fp32) or state destination
+  const float *grad;   // gradient / copy source
+  int rows, cols;      // master shape (canonical)
+  int ldg;             // gradient row pitch
+  int col;             // C_BIAS_COL*: gradient column holding the bias gradient
+  int H;               // interleave H (C_*_IL)
+  float lr;            // learning rate / n_ranks
+  const int *rows_idx; // C_SPARSE_ROWS: word id per gradient row
+  const int *nrows;    // C_SPARSE_ROWS: device count of rows
+  int *idst;           // C_TAG
+  int ival;
+};
+constexpr int MAX_COMMIT = 24;
+struct CommitList {
+  int n;
+  CommitSeg s[MAX_COMMIT];
+};
+cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s);
+
+}  // namespace jk

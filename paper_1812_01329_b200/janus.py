@@ -1,0 +1,251 @@
+"""Thin ctypes binding of libjanus (include/janus.h, include/janus_dev.h).
+
+Argument marshalling only: every step of the path runs inside libjanus's CUDA kernels. PyTorch
+supplies device memory and streams. There is no CPU fallback: if the shared library is missing
+the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from workloads import programs as pg
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libjanus.so")
+
+OK, ASSUMPTION_FAILED, ERR_INVALID, ERR_UNSUPPORTED, ERR_RUNTIME, ERR_CUDA, ERR_NCCL = range(7)
+STATUS_NAMES = ["OK", "ASSUMPTION_FAILED", "ERR_INVALID", "ERR_UNSUPPORTED", "ERR_RUNTIME",
+                "ERR_CUDA", "ERR_NCCL"]
+F32, BF16, I32, I64, U8 = range(5)
+
+
+class JanusTensor(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("dtype", C.c_int32), ("ndim", C.c_int32),
+                ("shape", C.c_int64 * 4), ("stride", C.c_int64 * 4)]
+
+
+class JanusOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("func", C.c_int32), ("n_in", C.c_int32),
+                ("in_node", C.c_int32 * 12), ("in_port", C.c_int32 * 12),
+                ("iattr", C.c_int64 * 8), ("fattr", C.c_double * 2)]
+
+
+class JanusAssumption(C.Structure):
+    _fields_ = [("id", C.c_uint32), ("kind", C.c_int32), ("mode", C.c_int32), ("target", C.c_int32),
+                ("dtype", C.c_int32), ("ndim", C.c_int32), ("dims", C.c_int64 * 4),
+                ("lo", C.c_int64), ("hi", C.c_int64), ("value", C.c_int64),
+                ("ref_arg", C.c_int32), ("ref_dim", C.c_int32)]
+
+
+class JanusFailure(C.Structure):
+    _fields_ = [("assumption_id", C.c_uint32), ("rank", C.c_int32), ("index", C.c_int64),
+                ("observed", C.c_int64)]
+
+
+class JanusBuildOpts(C.Structure):
+    _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_uint8 * 128),
+                ("gemm_dtype", C.c_int32), ("strip_asserts", C.c_int32),
+                ("fail_assert_id", C.c_int32), ("reserved", C.c_int32 * 5)]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libjanus.so not built ({LIB_PATH}); run __graft_entry__.build()")
+lib = C.CDLL(LIB_PATH)
+
+EXPORTS = ["janus_graph_build", "janus_workspace_bytes", "janus_run", "janus_run_imperative",
+           "janus_counters", "janus_describe", "janus_graph_destroy", "janus_status_str",
+           "janus_abi_version"]
+DEV_EXPORTS = ["janus_dev_gemm_bf16"]
+
+_P = C.c_void_p
+for _name, _res, _args in [
+    ("janus_dev_gemm_bf16", C.c_int32, [C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P,
+                                        C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, C.c_int32, _P]),
+]:
+    if hasattr(lib, _name):
+        f = getattr(lib, _name)
+        f.restype, f.argtypes = _res, _args
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def dev_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, Cout, ldc, bias_col=None, bias_row=None,
+                  accumulate=False, stream=None):
+    r = lib.janus_dev_gemm_bf16(M, N, K, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn), _ptr(Cout),
+                                ldc, _ptr(bias_col), _ptr(bias_row), int(accumulate), _stream(stream))
+    if r != 0:
+        raise RuntimeError(f"janus_dev_gemm_bf16 failed with cuda error {r}")
+
+
+# ----------------------------------------------------------------------------------- step ABI
+_sigs = {
+    "janus_graph_build": (C.c_int, [C.POINTER(JanusOp), C.c_int32, C.POINTER(JanusAssumption), C.c_int32,
+                                    C.POINTER(JanusBuildOpts), C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
+    "janus_workspace_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "janus_run": (C.c_int, [C.c_void_p, C.POINTER(JanusTensor), C.c_int32, C.POINTER(JanusTensor), C.c_int32,
+                            C.POINTER(JanusTensor), C.c_int32, JanusTensor, C.c_void_p, C.POINTER(JanusFailure)]),
+    "janus_run_imperative": (C.c_int, [C.c_void_p, C.POINTER(JanusTensor), C.c_int32, C.POINTER(JanusTensor),
+                                       C.c_int32, C.POINTER(JanusTensor), C.c_int32, JanusTensor, C.c_void_p]),
+    "janus_counters": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "janus_describe": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "janus_graph_destroy": (None, [C.c_void_p]),
+    "janus_status_str": (C.c_char_p, [C.c_int]),
+    "janus_abi_version": (C.c_int32, []),
+}
+for _n, (_r, _a) in _sigs.items():
+    _f = getattr(lib, _n)
+    _f.restype, _f.argtypes = _r, _a
+
+_TORCH_DT = None
+
+
+def _dtcode(t):
+    global _TORCH_DT
+    import torch
+    if _TORCH_DT is None:
+        _TORCH_DT = {torch.float32: F32, torch.bfloat16: BF16, torch.int32: I32, torch.int64: I64,
+                     torch.uint8: U8}
+    return _TORCH_DT[t.dtype]
+
+
+def to_jt(t):
+    """torch tensor (cuda or pinned cpu) or numpy array -> JanusTensor (borrowed pointer)."""
+    jt = JanusTensor()
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        jt.data = t.ctypes.data
+        jt.dtype = {np.dtype(np.float32): F32, np.dtype(np.int32): I32, np.dtype(np.int64): I64,
+                    np.dtype(np.uint8): U8}[t.dtype]
+        shape, strides = t.shape, [s // t.itemsize for s in t.strides]
+    else:
+        assert t.is_contiguous()
+        jt.data = t.data_ptr()
+        jt.dtype = _dtcode(t)
+        shape, strides = tuple(t.shape), t.stride()
+    jt.ndim = len(shape)
+    for k, (s, st) in enumerate(zip(shape, strides)):
+        jt.shape[k] = s
+        jt.stride[k] = st
+    return jt
+
+
+def _jt_array(ts):
+    arr = (JanusTensor * max(1, len(ts)))()
+    for k, t in enumerate(ts):
+        arr[k] = to_jt(t)
+    return arr
+
+
+def marshal_ops(program):
+    ops = (JanusOp * len(program.ops))()
+    for k, o in enumerate(program.ops):
+        j = ops[k]
+        j.kind = pg.OP_CODE[o.kind]
+        j.func = o.func
+        j.n_in = len(o.ins)
+        for m, (n, p) in enumerate(o.ins):
+            j.in_node[m] = n
+            j.in_port[m] = p
+        for m, v in enumerate(o.i):
+            j.iattr[m] = int(v)
+        for m, v in enumerate(o.f):
+            j.fattr[m] = float(v)
+    return ops
+
+
+def marshal_assumptions(program):
+    arr = (JanusAssumption * max(1, len(program.assumptions)))()
+    for k, a in enumerate(program.assumptions):
+        j = arr[k]
+        j.id = a.id
+        j.kind = pg.ASM_CODE[a.kind]
+        j.mode = a.mode
+        j.target = a.target
+        j.dtype = a.dtype
+        j.ndim = len(a.dims)
+        for m, d in enumerate(a.dims):
+            j.dims[m] = d
+        j.lo, j.hi, j.value = a.lo, a.hi, a.value
+        j.ref_arg, j.ref_dim = a.ref_arg, a.ref_dim
+    return arr
+
+
+class JanusError(RuntimeError):
+    pass
+
+
+class Graph:
+    """A speculatively specialised graph (janus_graph_build) for one Program."""
+
+    def __init__(self, program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False,
+                 fail_assert_id=-1):
+        self.program = program
+        opts = JanusBuildOpts()
+        opts.world_size, opts.rank = world_size, rank
+        if nccl_id is not None:
+            for k, b in enumerate(bytes(nccl_id)[:128]):
+                opts.nccl_id[k] = b
+        gemm = gemm or program.meta.get("gemm", "bf16")
+        opts.gemm_dtype = F32 if gemm == "f32" else BF16
+        opts.strip_asserts = int(strip_asserts)
+        opts.fail_assert_id = fail_assert_id
+        self._ops = marshal_ops(program)
+        self._asms = marshal_assumptions(program)
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        r = lib.janus_graph_build(self._ops, len(program.ops), self._asms, len(program.assumptions),
+                                  C.byref(opts), C.byref(h), err, 1024)
+        if r not in (OK, ERR_UNSUPPORTED) or not h.value:
+            raise JanusError(f"janus_graph_build: {STATUS_NAMES[r]}: {err.value.decode()}")
+        self.h = h
+        self.device_path = r == OK
+        self.build_message = err.value.decode()
+        n = C.c_size_t()
+        lib.janus_workspace_bytes(self.h, C.byref(n))
+        self.workspace_bytes = n.value
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.janus_graph_destroy(self.h)
+            self.h = None
+
+    def new_workspace(self, device="cuda"):
+        import torch
+        return torch.zeros(max(16, self.workspace_bytes), dtype=torch.uint8, device=device)
+
+    def run(self, args, state, workspace, outs=(), stream=None):
+        """janus_run: returns (status, failure dict or None)."""
+        a, s, o = _jt_array(args), _jt_array(state), _jt_array(outs)
+        f = JanusFailure()
+        r = lib.janus_run(self.h, a, len(args), s, len(state), o, len(outs), to_jt(workspace),
+                          _stream(stream), C.byref(f))
+        fail = None
+        if r == ASSUMPTION_FAILED:
+            fail = dict(assumption_id=f.assumption_id, rank=f.rank, index=f.index, observed=f.observed)
+        return r, fail
+
+    def run_imperative(self, args, state, workspace, outs=(), stream=None):
+        a, s, o = _jt_array(args), _jt_array(state), _jt_array(outs)
+        return lib.janus_run_imperative(self.h, a, len(args), s, len(state), o, len(outs),
+                                        to_jt(workspace), _stream(stream))
+
+    def counters(self):
+        l, h, a = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib.janus_counters(self.h, C.byref(l), C.byref(h), C.byref(a))
+        return dict(launches=l.value, host_syncs=h.value, aborts=a.value)
+
+    def describe(self):
+        buf = C.create_string_buffer(4096)
+        lib.janus_describe(self.h, buf, 4096)
+        return buf.value.decode()

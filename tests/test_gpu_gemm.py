@@ -1,0 +1,58 @@
+"""tcgen05 GEMM vs the oracle's contraction (fp64 of the same bf16-rounded operands)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.numerics import rb  # noqa: E402
+
+
+def _run(M, N, K, a_mn, b_mn, bias=None, acc=False, seed=0):
+    from paper_1812_01329_b200 import janus as J
+    g = np.random.default_rng(seed)
+    A = rb(g.uniform(-1, 1, (M, K)))
+    B = rb(g.uniform(-1, 1, (N, K)))
+    r8 = lambda x: (x + 7) // 8 * 8
+    lda = r8(M) if a_mn else r8(K) + 8
+    ldb = r8(N) if b_mn else r8(K) + 8
+    At = np.zeros((K, lda) if a_mn else (M, lda))
+    Bt = np.zeros((K, ldb) if b_mn else (N, ldb))
+    if a_mn:
+        At[:, :M] = A.T
+    else:
+        At[:, :K] = A
+    if b_mn:
+        Bt[:, :N] = B.T
+    else:
+        Bt[:, :K] = B
+    dA = torch.tensor(At, dtype=torch.bfloat16, device="cuda")
+    dB = torch.tensor(Bt, dtype=torch.bfloat16, device="cuda")
+    ldc = (N + 3) // 4 * 4
+    C0 = g.uniform(-1, 1, (M, ldc)) if acc else np.zeros((M, ldc))
+    dC = torch.tensor(C0, dtype=torch.float32, device="cuda")
+    bcol = torch.tensor(g.uniform(-1, 1, N), dtype=torch.float32, device="cuda") if bias == "col" else None
+    brow = torch.tensor(g.uniform(-1, 1, M), dtype=torch.float32, device="cuda") if bias == "row" else None
+    J.dev_gemm_bf16(M, N, K, dA, lda, a_mn, dB, ldb, b_mn, dC, ldc, bcol, brow, acc)
+    torch.cuda.synchronize()
+    ref = A @ B.T
+    if bcol is not None:
+        ref += bcol.cpu().double().numpy()[None, :]
+    if brow is not None:
+        ref += brow.cpu().double().numpy()[:, None]
+    if acc:
+        ref += np.asarray(C0, np.float32)[:, :N]
+    got = dC.cpu().double().numpy()[:, :N]
+    err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
+    return err
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (200, 136, 650), (2240, 2600, 650), (300, 1100, 2240)])
+def test_gemm_layouts(M, N, K, a_mn, b_mn):
+    assert _run(M, N, K, a_mn, b_mn) < 1e-5
+
+
+def test_gemm_bias_and_accumulate():
+    assert _run(333, 260, 130, 0, 0, bias="col") < 1e-5
+    assert _run(333, 260, 130, 0, 1, bias="row", acc=True) < 1e-5

@@ -323,7 +323,7 @@ def treelstm_program(V, E, H, C, B, lr, *, max_nodes=127, speculate="levels", ge
     for s in slots:
         if s.param:
             g.op("SGD_APPLY", [loss], i=[sid[s.name], g.effect_seq()], f=[lr])
-    asms = [Assumption(0, "DTYPE_EQ", DISPATCH, a, dtype=I32) for a in range(6)]
+    asms = [Assumption(a, "DTYPE_EQ", DISPATCH, a, dtype=I32) for a in range(6)]
     asms += [Assumption(6, "SHAPE_MATCH", DISPATCH, 4, dims=(B + 1,)),
              Assumption(7, "SHAPE_MATCH", DISPATCH, 5, dims=(B,))]
     if speculate == "levels":
