@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark: LSTM-LM training step of the speculative graph on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4] [--impl janus|reference]
+
+One JSON line on rank 0. `value` = whole-job samples/s (a sample = one 35-token sequence) with
+inputs resident in HBM, timed with CUDA events on the launch stream, max over ranks. `e2e` = the
+same metric through janus_run with pinned HOST argument buffers (H2D inside the call) and the loss
+read back to the host every step. `roofline` is the dominant kernel of the step, timed live with
+per-phase CUDA events; `cpu_baseline` is the oracle on the host cores on a bounded sample.
+
+--impl reference times the oracle (oracle/, the plain CPU interpreter of the paper's semantics) on
+the host cores, each step a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import gen, programs as pg  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+BASELINE_METRIC = "LSTM/TreeLSTM train samples/s at 1/2/4/8 B200; tensor-pipe %; guard overhead"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+# ----------------------------------------------------------------------------- workloads
+def c2_program(B):
+    return pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=35, lr=1.0)
+
+
+WORKLOADS = {
+    "c2": dict(desc="C2 PTB-shaped LSTM LM: 2 layers, H=E=650, V=10000, T=35, B=64 per GPU, bf16 GEMM "
+                    "operands / fp32 accumulate, unrolled speculative graph (TRIP_COUNT=35)",
+               B=64, T=35),
+}
+
+
+def lm_flops_per_sample(V, E, H, L, T):
+    """Algorithmic training FLOPs of one sequence: 3x forward (fwd + dgrad + wgrad)."""
+    cell = sum(2 * 4 * H * ((E if l == 0 else H) + H) for l in range(L))
+    dec = 2 * H * V
+    return 3 * T * (cell + dec)
+
+
+def gemm_flops(name, V, E, H, TB):
+    G4 = 4 * H
+    table = {"gemm_in0": 2 * TB * G4 * E, "gemm_in1": 2 * TB * G4 * H, "gemm_dec": 2 * TB * V * H,
+             "gemm_dWdec": 2 * V * (H + 1) * TB, "gemm_dh": 2 * TB * H * V,
+             "gemm_dWhh0": 2 * G4 * H * TB, "gemm_dWhh1": 2 * G4 * H * TB,
+             "gemm_dWih0": 2 * G4 * (E + 1) * TB, "gemm_dWih1": 2 * G4 * (H + 1) * TB,
+             "gemm_dx0": 2 * TB * E * G4, "gemm_dx1": 2 * TB * H * G4}
+    return table.get(name)
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        self.rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if "Active" in v and "Not" not in v})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- CPU baselines
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return 1
+
+
+def oracle_sample(B, T):
+    """Time the oracle (as it stands) on one bounded sample: B sequences x T tokens of the C2 model."""
+    from oracle import interp as I
+    prog = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=T, lr=1.0)
+    state = gen.uniform_params(prog, 1, 0.05)
+    args = list(gen.lm_batches(gen.SEED_C2, B, T, 10000, 1))[0]
+    t0 = time.perf_counter()
+    r = I.run_graph_step(prog, list(args), state)
+    dt = time.perf_counter() - t0
+    assert r.status == I.OK
+    return dt
+
+
+def cpu_baseline():
+    B, T = 64, 35
+    dt = oracle_sample(B, T)
+    return {"value": B / dt, "unit": "samples/s", "cores": _blas_threads(), "kind": "oracle",
+            "sample": f"one C2 training step (B={B} sequences x T={T} tokens, full model) through "
+                      f"oracle.run_graph_step in {dt:.1f} s",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    B, T = 8, 5     # bounded per-step sample: 8 sequences x 5 tokens (sequence-equivalents below)
+    for _ in range(args.warmup):
+        oracle_sample(B, T)
+    times = [oracle_sample(B, T) for _ in range(args.steps)]
+    tot = sum(times)
+    v = args.steps * B * T / 35.0 / tot
+    cb = {"value": v, "unit": "samples/s", "cores": _blas_threads(), "kind": "oracle",
+          "sample": f"each step: oracle.run_graph_step on B={B} sequences x T={T} tokens of the C2 model; "
+                    f"value in 35-token sequence equivalents"}
+    print(json.dumps({"impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": "samples/s",
+                      "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": WORKLOADS["c2"]["desc"], "global_batch": 64, "seq_len": 35,
+                                 "parallelism": "none (host oracle)"},
+                      "cpu_baseline": cb,
+                      "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+# ----------------------------------------------------------------------------- main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--impl", default="janus", choices=["janus", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1812_01329_b200 import janus as J
+
+    wl = WORKLOADS[args.workload]
+    B, T = wl["B"], wl["T"]
+    prog = c2_program(B)
+    nccl_id = J.nccl_unique_id_bcast(rank, world) if world > 1 else None
+    g = J.Graph(prog, world_size=world, rank=rank, nccl_id=nccl_id)
+    assert g.device_path, g.build_message
+    ws = g.new_workspace()
+    state = [torch.tensor(x, device="cuda") for x in gen.uniform_params(prog, 1, 0.05)]
+    n_batches = 8
+    batches = list(gen.lm_batches(gen.SEED_C2, B, T, 10000, n_batches, ranks=world))
+    dev_batches = [[torch.tensor(a[rank * B:(rank + 1) * B], device="cuda") for a in b] for b in batches]
+    host_batches = [[torch.tensor(a[rank * B:(rank + 1) * B]).pin_memory() for a in b] for b in batches]
+    loss_d = torch.zeros(1, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(k, host=False, loss_out=None):
+        a = host_batches[k % n_batches] if host else dev_batches[k % n_batches]
+        st, fail = g.run(a, state, ws, outs=[loss_out if loss_out is not None else loss_d], stream=stream)
+        if st != J.OK:
+            raise RuntimeError(f"janus_run: {J.STATUS_NAMES[st]} {fail}")
+
+    def timed(fn, K):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(K):
+            fn(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for k in range(args.warmup):
+        step(k)
+    c0 = g.counters()
+    with Clocks(local) as clk:
+        ms = timed(lambda k: step(k), args.steps)
+    c1 = g.counters()
+    launches = (c1["launches"] - c0["launches"]) // args.steps
+    syncs = (c1["host_syncs"] - c0["host_syncs"]) / args.steps
+    ms_step = ms / args.steps
+    value = world * B * 1000.0 / ms_step
+
+    # e2e: pinned host buffers in, loss out to host memory, every step, through janus_run
+    loss_h = torch.zeros(1).pin_memory()
+    for k in range(2):
+        step(k, host=True, loss_out=loss_h)
+    ms_e2e = timed(lambda k: step(k, host=True, loss_out=loss_h), args.steps)
+    e2e = {"value": world * B * 1000.0 / (ms_e2e / args.steps), "unit": "samples/s",
+           "h2d_bytes_per_step": int(sum(a.numel() * 4 for a in host_batches[0])),
+           "d2h_bytes_per_step": 48}
+
+    # per-phase device timing (separate pass of the same steps, CUDA events on the launch stream)
+    J.dev_profile(g, True)
+    timed(lambda k: step(k), args.steps)
+    phases = J.dev_phase_report(g)
+    J.dev_profile(g, False)
+    pk = peaks()
+    TB = B * T
+    rows = []
+    step_ms = sum(v[0] for v in phases.values()) / args.steps
+    for name, (tot_ms, cnt) in phases.items():
+        fl = gemm_flops(name, 10000, 650, 650, TB)
+        rows.append((tot_ms / args.steps, name, cnt // args.steps, fl))
+    rows.sort(reverse=True)
+    gemms = [r for r in rows if r[3]]
+    top = gemms[0] if gemms else rows[0]
+    avg_ms = top[0] / max(1, top[2])
+    achieved = top[3] / (avg_ms * 1e-3) / 1e12 if top[3] else None
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    roofline = {"kernel": top[1], "bound": "tensor", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak if achieved else None, "traffic": None,
+                "flops_per_launch": top[3], "avg_launch_ms": avg_ms,
+                "peak_source": pk["source"] + " bf16_tflops_sustained (kernel timed inside the step)",
+                "share_of_step": top[0] / step_ms if step_ms else None}
+    flops = lm_flops_per_sample(10000, 650, 650, 2, T) * B
+    out = {
+        "metric": BASELINE_METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": wl["desc"], "global_batch": B * world, "seq_len": T,
+                   "parallelism": f"dp{world}",
+                   "l2": "no flush: the step's working set (~340 MB workspace + 79 MB params) exceeds the 126 MB L2"},
+        "words_per_s": value * T,
+        "step_tflops": flops * world / (ms_step * 1e-3) / 1e12 / world,
+        "step_flop_frac_of_sustained": flops / (ms_step * 1e-3) / 1e12 / peak,
+        "e2e": e2e, "gpu_launches": int(launches), "host_syncs_per_step": syncs,
+        "roofline": roofline,
+        "phases_ms_per_step": {r[1]: round(r[0], 4) for r in rows},
+        "paper_context": "JANUS LSTM (PTB, BS 20) 22.06k words/s on 1 TITAN Xp, fp32 (P:363) — other hardware/config",
+    }
+    out["clocks"] = clk.summary()
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline()
+    elif rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

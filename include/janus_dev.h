@@ -6,6 +6,7 @@
  */
 #ifndef JANUS_DEV_H
 #define JANUS_DEV_H
+#include <stddef.h>
 #include <stdint.h>
 #ifdef __cplusplus
 extern "C" {
@@ -17,6 +18,16 @@ int32_t janus_dev_gemm_bf16(int32_t M, int32_t N, int32_t K, const void *A, int3
                             int32_t a_mn, const void *B, int32_t ldb, int32_t b_mn, float *C,
                             int32_t ldc, const float *bias_col, const float *bias_row,
                             int32_t accumulate, void *stream);
+
+/* Per-phase device timing of janus_run (CUDA events on the launch stream, collected after the
+ * step's synchronisation). enable != 0 switches it on and clears the totals. The report is
+ * "name:total_ms:count;..." over the phases run since enabling. */
+struct janus_graph;
+int32_t janus_dev_profile(struct janus_graph *g, int32_t enable);
+/* Timeline probe of the layer-0 recurrent kernels (CTA 0): dev_buf (device, 16*T u64) receives
+ * %globaltimer stamps, 8 per step: forward at [0, 8T), backward at [8T, 16T). NULL disables. */
+int32_t janus_dev_set_probe(struct janus_graph *g, void *dev_buf);
+int32_t janus_dev_phase_report(const struct janus_graph *g, char *buf, size_t len);
 
 #ifdef __cplusplus
 }

@@ -189,6 +189,24 @@ bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t ou
   return r == CUDA_SUCCESS;
 }
 
+// 3-D view of a row-major bf16 matrix as {64 columns, rows, column chunks}: one TMA op then
+// fetches `box_chunks` consecutive 64-column chunks of `box_rows` rows, landing chunk-major in
+// shared memory (each chunk = box_rows x 128 B, 128-B swizzled) — the K-major UMMA layout.
+// Requires ld >= 64 * n_chunks (the chunk dimension never runs past the row pitch).
+bool make_tmap_bf16_chunks(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t ld,
+                           uint64_t n_chunks, uint32_t box_rows, uint32_t box_chunks) {
+  if (!get_encode() || ld < 64 * n_chunks) return false;
+  cuuint64_t dims[3] = {64, rows, n_chunks};
+  cuuint64_t strides[2] = {ld * 2, 128};
+  cuuint32_t box[3] = {64, box_rows, box_chunks};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), dims,
+                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int BN, int A_MN, int B_MN>
 static cudaError_t launch(const GemmOp &op, cudaStream_t st) {
   constexpr int STAGES = BN == 256 ? 4 : 5;

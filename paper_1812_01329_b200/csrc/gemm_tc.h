@@ -33,5 +33,7 @@ struct GemmOp {
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);
 bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_outer);
+bool make_tmap_bf16_chunks(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t ld,
+                           uint64_t n_chunks, uint32_t box_rows, uint32_t box_chunks);
 
 }  // namespace jk

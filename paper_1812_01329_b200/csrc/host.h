@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -39,7 +40,7 @@ struct LmPlan {
     size_t seg_word = 0, seg_start = 0, seg_grad = 0, nseg = 0, keys = 0;
     size_t small_ws = 0;
   } off;
-  int Ep = 0, Hp = 0;  // padded row pitches (elements)
+  int Ep = 0, Hp = 0, Gz = 0;  // padded row pitches (elements)
   int nbar = 0;
 };
 
@@ -55,7 +56,42 @@ struct TreePlan {
   size_t ws_bytes = 0;
 };
 
+// Optional per-phase device timing: a CUDA event is recorded on the launch stream before every
+// phase; after the step's single synchronisation the gaps are accumulated per phase name.
+struct PhaseProf {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::string> pending;  // phase name per recorded event ("" = end marker)
+  std::map<std::string, std::pair<double, long>> acc;  // name -> (total ms, launches)
+  void mark(const char *name, cudaStream_t st) {
+    if (!on) return;
+    if (pending.size() == pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) { on = false; return; }
+      pool.push_back(e);
+    }
+    cudaEventRecord(pool[pending.size()], st);
+    pending.push_back(name ? name : "");
+  }
+  void collect() {
+    if (!on) { pending.clear(); return; }
+    for (size_t i = 0; i + 1 < pending.size(); ++i) {
+      if (pending[i].empty()) continue;
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pool[i], pool[i + 1]);
+      auto &a = acc[pending[i]];
+      a.first += ms;
+      a.second += 1;
+    }
+    pending.clear();
+  }
+  ~PhaseProf() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 struct Graph {
+  PhaseProf prof;
   std::vector<janus_op> ops;
   std::vector<janus_assumption> asms;
   janus_build_opts opts{};
@@ -72,6 +108,7 @@ struct Graph {
   DevStatus *h_status = nullptr;
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
   std::string describe;
+  unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (16*T u64)
 };
 
 // host_graph.cpp

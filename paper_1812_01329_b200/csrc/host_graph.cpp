@@ -11,6 +11,7 @@
 #include <string>
 
 #include "host.h"
+#include "../../include/janus_dev.h"
 
 namespace jk {
 
@@ -325,6 +326,33 @@ janus_status janus_describe(const janus_graph *g, char *buf, size_t buf_len) {
   std::string d = g->kind.empty() ? "no device program: " + g->unsupported_reason : g->describe;
   set_err(buf, buf_len, d);
   return JANUS_OK;
+}
+
+/* dev hooks (include/janus_dev.h) */
+int32_t janus_dev_set_probe(janus_graph *g, void *dev_buf) {
+  if (!g) return -1;
+  g->probe = static_cast<unsigned long long *>(dev_buf);
+  return 0;
+}
+
+/* per-phase device timing */
+int32_t janus_dev_profile(janus_graph *g, int32_t enable) {
+  if (!g) return -1;
+  g->prof.on = enable != 0;
+  g->prof.acc.clear();
+  return 0;
+}
+
+int32_t janus_dev_phase_report(const janus_graph *g, char *buf, size_t len) {
+  if (!g || !buf || !len) return -1;
+  std::string r;
+  char tmp[160];
+  for (const auto &kv : g->prof.acc) {
+    snprintf(tmp, sizeof tmp, "%s:%.6f:%ld;", kv.first.c_str(), kv.second.first, kv.second.second);
+    r += tmp;
+  }
+  set_err(buf, len, r);
+  return (int32_t)g->prof.acc.size();
 }
 
 void janus_graph_destroy(janus_graph *g) {

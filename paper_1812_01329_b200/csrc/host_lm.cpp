@@ -187,7 +187,8 @@ bool lower_lm(Graph &g, std::string &why) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
   p.off.status = take(sizeof(DevStatus));
-  p.nbar = 8;
+  p.nbar = 256 * 8;  // per-CTA step flags: 256 CTAs x (L <= 4 layers) x 2 directions
+  if ((p.H + 15) / 16 > 256) { why = "hidden size > 4096"; return false; }
   p.off.barriers = take(p.nbar * sizeof(unsigned));
   p.off.stage_args = take(3ull * p.B * p.T * sizeof(int));
   const int B = p.B, T = p.T, H = p.H, E = p.E, V = p.V, G4 = 4 * p.H;
@@ -198,7 +199,9 @@ bool lower_lm(Graph &g, std::string &why) {
     if (H % 2) { why = "odd hidden size"; return false; }
     if (T * B > 8192) { why = "T*B > 8192"; return false; }
     p.Ep = r8(E + 1);
-    p.Hp = r8(H + 1);
+    // h rows are streamed by the recurrent kernels in whole 64-column chunks: pitch >= 64*ceil(H/64)
+    p.Hp = std::max(r8(H + 1), 64 * ((H + 63) / 64));
+    p.Gz = 64 * ((G4 + 63) / 64);  // dz pitch (chunked the same way)
     const int Vp = r8(V);
     const size_t TB = (size_t)T * B;
     for (int l = 0; l < p.L; ++l) {
@@ -210,7 +213,7 @@ bool lower_lm(Graph &g, std::string &why) {
       p.off.Hs[l] = take((TB + B) * p.Hp * 2);
       p.off.Cs[l] = take((TB + B) * p.Hp * 4);
       p.off.G[l] = take(TB * G4 * 4);
-      p.off.DZ[l] = take(TB * G4 * 2);
+      p.off.DZ[l] = take(TB * p.Gz * 2);
       p.off.dX[l] = take(TB * Inp * 4);
       p.off.hT[l] = take((size_t)B * H * 4);
       p.off.cT[l] = take((size_t)B * H * 4);
@@ -285,6 +288,8 @@ static GuardList make_guards(const LmPlan &p, const std::vector<LmPlan::RG> &rgs
 
 janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_outs,
                     cudaStream_t st, janus_failure *fail) {
+  g.prof.mark("readback", st);
+  g.prof.mark(nullptr, st);
   if (!g.h_status && cudaMallocHost(&g.h_status, sizeof(DevStatus)) != cudaSuccess) return JANUS_ERR_CUDA;
   if (n_outs > 0 && outs[0].data && is_device_ptr(outs[0].data))
     if (cudaMemcpyAsync(outs[0].data, &dst->loss, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -294,6 +299,7 @@ janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_ou
   cudaError_t e = cudaStreamSynchronize(st);
   g.host_syncs++;
   if (e != cudaSuccess) return JANUS_ERR_CUDA;
+  g.prof.collect();
   const DevStatus &h = *g.h_status;
   if (n_outs > 0 && outs[0].data && !is_device_ptr(outs[0].data))
     *static_cast<float *>(outs[0].data) = h.loss;
@@ -310,8 +316,9 @@ janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_ou
   return h.status == 0 ? JANUS_OK : (janus_status)h.status;
 }
 
-#define LCHK(x)                                   \
+#define LCHK(name, x)                             \
   do {                                            \
+    g.prof.mark(name, st);                        \
     cudaError_t e_ = (x);                         \
     g.launches++;                                 \
     if (e_ != cudaSuccess) return JANUS_ERR_CUDA; \
@@ -380,7 +387,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     a.gl = gl;
     a.ws = reinterpret_cast<float *>(W + p.off.small_ws);
     a.st = dst;
-    LCHK(launch_small_lm(a, st));
+    LCHK("lm_small_f32", launch_small_lm(a, st));
     return finish(g, dst, outs, n_outs, st, fail);
   }
 
@@ -392,20 +399,20 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   const int *Tdev = p.while_mode ? &dst->trip : nullptr;
   auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16 *>(W + off); };
   auto fp = [&](size_t off) { return reinterpret_cast<float *>(W + off); };
-  LCHK(launch_step_init(dst, bars, p.nbar, st));
-  if (p.while_mode) LCHK(launch_trip(P.lens, B, Tw, dst, st));
-  if (gl.n) LCHK(launch_guards(gl, dst, st));
+  LCHK("init", launch_step_init(dst, bars, p.nbar, st));
+  if (p.while_mode) LCHK("trip", launch_trip(P.lens, B, Tw, dst, st));
+  if (gl.n) LCHK("guards", launch_guards(gl, dst, st));
   // operand copies (R1): interleaved / transposed bf16 working copies of the fp32 masters
   for (int l = 0; l < L; ++l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
-    LCHK(launch_cast_rows(P.Wih[l], G4, In, In, bf(p.off.Wih_b[l]), Inp, H, st));
-    LCHK(launch_cast_rows(P.Whh[l], G4, H, H, bf(p.off.Whh_b[l]), Hp, H, st));
-    LCHK(launch_cast_transpose_interleaved(P.Whh[l], H, bf(p.off.WhhT_b[l]), G4, st));
-    LCHK(launch_bias_interleave(P.b[l], H, fp(p.off.bil[l]), st));
-    LCHK(launch_fill_col(bf(p.off.Hs[l]), TB + B, Hp, H, 1.f, Hp, st));
+    LCHK("cast", launch_cast_rows(P.Wih[l], G4, In, In, bf(p.off.Wih_b[l]), Inp, H, st));
+    LCHK("cast", launch_cast_rows(P.Whh[l], G4, H, H, bf(p.off.Whh_b[l]), Hp, H, st));
+    LCHK("cast", launch_cast_transpose_interleaved(P.Whh[l], H, bf(p.off.WhhT_b[l]), G4, st));
+    LCHK("cast", launch_bias_interleave(P.b[l], H, fp(p.off.bil[l]), st));
+    LCHK("cast", launch_fill_col(bf(p.off.Hs[l]), TB + B, Hp, H, 1.f, Hp, st));
   }
-  LCHK(launch_cast_rows(P.Wdec, V, H, H, bf(p.off.Wdec_b), Hp, 0, st));
-  LCHK(launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
+  LCHK("cast", launch_cast_rows(P.Wdec, V, H, H, bf(p.off.Wdec_b), Hp, 0, st));
+  LCHK("gather", launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
   // forward
   for (int l = 0; l < L; ++l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
@@ -414,14 +421,15 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
     op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
     op.ep.C = fp(p.off.G[l]); op.ep.ldc = G4; op.ep.bias_col = fp(p.off.bil[l]);
-    LCHK(gemm_bf16(op, st));
+    LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(op, st));
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
     ra.G = fp(p.off.G[l]); ra.Hs = bf(p.off.Hs[l]); ra.Cs = fp(p.off.Cs[l]); ra.ldh = Hp;
     ra.h0 = P.h[l]; ra.c0 = P.c[l]; ra.hT = fp(p.off.hT[l]); ra.cT = fp(p.off.cT[l]);
-    ra.barrier = bars + l; ra.fail = nullptr;
+    ra.barrier = bars + 256 * l; ra.fail = nullptr;
+    ra.dbg = l == 0 ? g.probe : nullptr;
     ra.tag = p.tag_specialised ? nullptr : P.tag;
-    LCHK(lstm_rec_fwd(ra, bf(p.off.Whh_b[l]), Hp, p.while_mode, st));
+    LCHK(l ? "rec_fwd1" : "rec_fwd0", lstm_rec_fwd(ra, bf(p.off.Whh_b[l]), Hp, p.while_mode, st));
   }
   {
     GemmOp op;  // decoder logits
@@ -429,9 +437,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.A = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.lda = Hp;
     op.B = bf(p.off.Wdec_b); op.ldb = Hp;
     op.ep.C = fp(p.off.logits); op.ep.ldc = Vp; op.ep.bias_col = P.bdec;
-    LCHK(gemm_bf16(op, st));
+    LCHK("gemm_dec", gemm_bf16(op, st));
   }
-  LCHK(launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
+  LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
                    (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
   {
     GemmOp op;  // dW_dec | db_dec = dy^T [h_top | 1]
@@ -439,13 +447,13 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.A = bf(p.off.dy); op.lda = Vp; op.a_mn = 1;
     op.B = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.ldb = Hp; op.b_mn = 1;
     op.ep.C = fp(p.off.gWdec); op.ep.ldc = Hp;
-    LCHK(gemm_bf16(op, st));
+    LCHK("gemm_dWdec", gemm_bf16(op, st));
     GemmOp o2;  // dh_top = dy W_dec
     o2.M = TB; o2.N = H; o2.K = V;
     o2.A = bf(p.off.dy); o2.lda = Vp;
     o2.B = bf(p.off.Wdec_b); o2.ldb = Hp; o2.b_mn = 1;
     o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
-    LCHK(gemm_bf16(o2, st));
+    LCHK("gemm_dh", gemm_bf16(o2, st));
   }
   for (int l = L - 1; l >= 0; --l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
@@ -453,39 +461,40 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     rb.B = B; rb.H = H; rb.T = Tw; rb.T_dev = Tdev; rb.lens = p.while_mode ? P.lens : nullptr;
     rb.G = fp(p.off.G[l]); rb.Cs = fp(p.off.Cs[l]); rb.ldh = Hp;
     rb.dHin = l == L - 1 ? fp(p.off.dHtop) : fp(p.off.dX[l + 1]); rb.ldd = Hp;
-    rb.DZ = bf(p.off.DZ[l]); rb.barrier = bars + L + l;
-    LCHK(lstm_rec_bwd(rb, bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
+    rb.DZ = bf(p.off.DZ[l]); rb.ldz = p.Gz; rb.barrier = bars + 256 * (L + l);
+    rb.dbg = (l == 0 && g.probe) ? g.probe + 8 * p.T : nullptr;
+    LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(rb, bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
     const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
     GemmOp a;  // dW_hh = dz^T h_{t-1}
     a.M = G4; a.N = H; a.K = TB;
-    a.A = bf(p.off.DZ[l]); a.lda = G4; a.a_mn = 1;
+    a.A = bf(p.off.DZ[l]); a.lda = p.Gz; a.a_mn = 1;
     a.B = bf(p.off.Hs[l]); a.ldb = Hp; a.b_mn = 1;
     a.ep.C = fp(p.off.gWhh[l]); a.ep.ldc = Hp;
-    LCHK(gemm_bf16(a, st));
+    LCHK(l ? "gemm_dWhh1" : "gemm_dWhh0", gemm_bf16(a, st));
     GemmOp b2;  // dW_ih | db = dz^T [x | 1]
     b2.M = G4; b2.N = In + 1; b2.K = TB;
-    b2.A = bf(p.off.DZ[l]); b2.lda = G4; b2.a_mn = 1;
+    b2.A = bf(p.off.DZ[l]); b2.lda = p.Gz; b2.a_mn = 1;
     b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
     b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
-    LCHK(gemm_bf16(b2, st));
+    LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(b2, st));
     if (l > 0 || p.lr_E != 0) {
       GemmOp c2;  // dx = dz W_ih
       c2.M = TB; c2.N = In; c2.K = G4;
-      c2.A = bf(p.off.DZ[l]); c2.lda = G4;
+      c2.A = bf(p.off.DZ[l]); c2.lda = p.Gz;
       c2.B = bf(p.off.Wih_b[l]); c2.ldb = Inp; c2.b_mn = 1;
       c2.ep.C = fp(p.off.dX[l]); c2.ep.ldc = Inp;
-      LCHK(gemm_bf16(c2, st));
+      LCHK(l ? "gemm_dx1" : "gemm_dx0", gemm_bf16(c2, st));
     }
   }
   int *seg_word = reinterpret_cast<int *>(W + p.off.seg_word);
   int *nseg = reinterpret_cast<int *>(W + p.off.nseg);
   if (p.lr_E != 0) {
-    LCHK(launch_embed_grad(P.tok, B, Wd, Tw, Tdev, fp(p.off.dX[0]), Ep, E, seg_word,
+    LCHK("embed_grad", launch_embed_grad(P.tok, B, Wd, Tw, Tdev, fp(p.off.dX[0]), Ep, E, seg_word,
                            reinterpret_cast<int *>(W + p.off.seg_start), fp(p.off.seg_grad), Ep,
                            nseg, reinterpret_cast<unsigned long long *>(W + p.off.keys), st));
     g.launches++;  // embed grad is two kernels
   }
-  LCHK(launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
+  LCHK("finalize", launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
   // ---- the all-or-nothing commit (P:164, P:266 (4))
   CommitList cl{};
   auto add = [&](CommitSeg s) { cl.s[cl.n++] = s; };
@@ -508,7 +517,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     if (p.lr_E != 0) { s = {}; s.kind = C_SPARSE_ROWS; s.dst = P.E; s.grad = fp(p.off.seg_grad); s.cols = E; s.ldg = Ep; s.rows_idx = seg_word; s.nrows = nseg; s.lr = p.lr_E / nr; add(s); }
     if (p.write_tag && P.tag) { s = {}; s.kind = C_TAG; s.idst = P.tag; s.ival = 1; add(s); }
   }
-  LCHK(launch_commit(cl, dst, st));
+  LCHK("commit", launch_commit(cl, dst, st));
   return finish(g, dst, outs, n_outs, st, fail);
 }
 

@@ -1,8 +1,7 @@
 // lm_rec.cu — the loop of the Figure 1 program (`for item in sequence: state =
 // rnn_cell(state, item)`) executed as ONE persistent launch per layer and direction: the loop
 // frame lives on the device — unrolled to the asserted trip count or, in While
-// mode, bounded by a trip count computed on the device — with a grid barrier per iteration and no
-// host round trip.
+// mode, bounded by a trip count computed on the device — with no host round trip.
 //
 // Weight-stationary tcgen05 design. CTA j owns hidden units [16j, 16j+16) (all 4 gates):
 //   forward : its 64 gate-interleaved rows of W_hh stay in shared memory for all T steps; per step
@@ -12,71 +11,162 @@
 //   backward: its 16 columns of W_hh (stored transposed, [units x 4H]) stay in shared memory;
 //             per step dz_{t+1} (bf16 [B x 4H]) streams in, D[b, u] = dz_{t+1} . W_hh[:, u] gives the
 //             recurrent dh, and the cell backward runs in registers (dc carried in registers).
+// Warp roles (192 threads): warps 0-3 epilogue (thread = batch row = TMEM lane), warp 4 producer
+// (polls the producers' step flags, then fetches many 64-column chunks per TMA op through a 3-D
+// tensor map), warp 5 MMA issuer. Each step is latency-bound, so every chunk of a step is in
+// flight at once when shared memory allows, and the step's other operands are loaded before the
+// MMA wait. Synchronisation is dataflow (per-CTA release flags), not a grid barrier.
 // Gate-interleaved order: row 4u+g of the working copies = canonical row g*H+u (g = i,f,g,o).
+#include <algorithm>
+
 #include "common.cuh"
 #include "gemm_tc.h"
 #include "lm_rec.h"
 
 namespace jk {
 
-constexpr int REC_THREADS = 128;
-constexpr int REC_UPC = 16;     // hidden units per CTA
-constexpr int REC_STAGES = 6;   // A-operand ring depth
+constexpr int REC_THREADS = 192;
+constexpr int REC_UPC = 16;      // hidden units per CTA
+constexpr int REC_MAX_SLOTS = 48;
+constexpr int SMEM_BUDGET = 232448 - 1024;
+constexpr int PAD = 16384;       // an M=128 MMA reads 128 rows from a chunk base
 
-struct RecSmem {
-  // laid out manually from a 1024-aligned base
-  static constexpr int A_STAGE = 128 * 128;  // 128 rows x 128 B (MMA reads 128 rows)
+// fp32-accurate activations on the fast exp path (|error| ~1e-7)
+JN_DEV float sig_f(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+JN_DEV float tanh_f(float x) {
+  const float e = __expf(-2.f * fabsf(x));
+  const float t = __fdividef(1.f - e, 1.f + e);
+  return copysignf(t, x);
+}
+
+// Dataflow synchronisation between the CTAs of a recurrent launch. Every step writes a fresh row
+// block (h_t / dz_t), so there are no write-after-read hazards — only read-after-write: a CTA
+// publishes "my slice of step t is written" with a release store of its per-CTA flag, and the
+// consumer's producer warp waits for the flags of all producers, then fences once.
+JN_DEV void publish_flag(unsigned int *flag, unsigned int v) {
+  __syncthreads();  // all of this CTA's stores of the step precede the release (bar.sync cumulativity)
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+// Executed by a whole warp: lanes poll the n producer flags in parallel (relaxed loads), then one
+// acquire fence and one generic->async proxy fence for the TMA loads lane 0 issues next.
+JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
+  const int lane = threadIdx.x & 31;
+  for (int c = lane; c < n; c += 32) {
+    unsigned int x;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
+    } while (x < v);
+  }
+  __syncwarp();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  fence_proxy_async_global();  // the TMA (async proxy) reads what the generic proxy wrote
+}
+
+struct RecLayout {
+  int nk;       // 64-column chunks of the streamed operand per step
+  int wbytes;   // resident weight slice bytes (1 KB aligned)
+  int cb;       // bytes per chunk in smem = Bp * 128 (Bp = B rounded up to 8)
+  int bp;       // rows per chunk fetched
+  int ch;       // chunks per TMA op
+  int nops;     // TMA ops per step
+  int nslots;   // ring slots (one op each)
+  int rot;      // ch == 1: CTA c fetches chunks starting at a CTA-dependent offset (spreads L2 load)
 };
 
-JN_DEV float tanh_acc(float x) { return tanhf(x); }
+JN_DEV int chunk_of(const RecLayout &ly, int k) {
+  return ly.rot ? (k + (int)blockIdx.x * 7) % ly.nk : k;
+}
+
+// optional timeline probe (CTA 0 only): dbg[8 t + k] = %globaltimer (ns)
+#define PROBE(t_, k_)                                                            \
+  do {                                                                           \
+    if (a.dbg && blockIdx.x == 0) {                                              \
+      unsigned long long ts_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_));                    \
+      a.dbg[8 * (t_) + (k_)] = ts_;                                              \
+    }                                                                            \
+  } while (0)
+
+// Producer (warp 4, lane 0): TMA op k of step `st` into ring slot (st*nops + k) % nslots.
+JN_DEV void issue_step(const CUtensorMap *tm, const RecLayout &ly, uint8_t *sA, uint64_t *full,
+                       uint64_t *empty, int st, int row0) {
+  for (int k = 0; k < ly.nops; ++k) {
+    const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
+    if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+    mbar_expect_tx(&full[s], ly.ch * ly.cb);
+    tma_load_3d(sA + (size_t)s * ly.ch * ly.cb, tm, &full[s], 0, row0,
+                ly.ch == 1 ? chunk_of(ly, k) : k * ly.ch);
+  }
+}
+
+// MMA issuer (warp 5, lane 0): D (TMEM) = sum over the step's chunks of A_chunk . W_chunk^T.
+template <int WCHUNK>
+JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *full, uint64_t *empty,
+                     uint64_t *tfull, uint32_t tmem, uint32_t idesc, int st) {
+  for (int k = 0; k < ly.nops; ++k) {
+    const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
+    mbar_wait(&full[s], r & 1);
+    tc_fence_after();
+    const uint32_t sa = smem_u32(sA + (size_t)s * ly.ch * ly.cb);
+    for (int c = 0; c < ly.ch; ++c) {
+      const int j = ly.ch == 1 ? chunk_of(ly, k) : k * ly.ch + c;
+      if (k * ly.ch + c >= ly.nk) break;
+      const uint32_t ca = sa + c * ly.cb, cw = smem_u32(sW + j * WCHUNK);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem, umma_desc_sw128(ca + kk * 32, 16, 1024), umma_desc_sw128(cw + kk * 32, 16, 1024),
+                  idesc, ((k * ly.ch + c) | kk) != 0);
+    }
+    umma_commit(&empty[s]);
+  }
+  umma_commit(tfull);
+}
 
 // ---------------------------------------------------------------------------------- forward
 template <bool MASKED>
 __global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmH,  // Hs [(T+1)B x H], box {64,B}
+    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmH,  // Hs chunks {64, (T+1)B, nk}
                         const __grid_constant__ CUtensorMap tmW,  // W_hh interleaved [4H x H], box {64,64}
-                        RecFwdArgs a) {
+                        RecFwdArgs a, RecLayout ly) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  const int nk = (a.H + 63) / 64;
-  uint8_t *sW = base;                                   // nk x 8 KB
-  uint8_t *sA = sW + nk * 8192;                         // REC_STAGES x 16 KB
-  uint64_t *full = reinterpret_cast<uint64_t *>(sA + REC_STAGES * RecSmem::A_STAGE);
-  uint64_t *empty = full + REC_STAGES;
-  uint64_t *tfull = empty + REC_STAGES;
+  const int nk = ly.nk, S = ly.nslots;
+  uint8_t *sW = base;
+  uint8_t *sA = sW + ly.wbytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sA + (size_t)S * ly.ch * ly.cb + PAD);
+  uint64_t *empty = full + S;
+  uint64_t *tfull = empty + S;
   uint64_t *wfull = tfull + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = threadIdx.x;  // batch row owned in the epilogue
+  const int warp = threadIdx.x >> 5;
+  const int b = threadIdx.x;  // batch row owned in the epilogue (warps 0-3)
   const int u0 = blockIdx.x * REC_UPC;
   const int B = a.B, H = a.H, G4 = 4 * a.H;
-  if (a.fail && *a.fail) return;  // cooperative cancellation: an earlier phase already failed
+  const int nu = min(REC_UPC, H - u0);
+  if (a.fail && *a.fail) return;
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 128) {
     tma_prefetch_desc(&tmH);
     tma_prefetch_desc(&tmW);
-    for (int s = 0; s < REC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(wfull, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 64);
+  if (warp == 5) tmem_alloc(tmem_slot, 64);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
-  // resident weight slice: 64 interleaved gate rows x H
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 128) {
     mbar_expect_tx(wfull, nk * 8192);
     for (int j = 0; j < nk; ++j) tma_load_2d(sW + j * 8192, &tmW, wfull, j * 64, blockIdx.x * 64);
   }
-
   // initial state -> registers and row block 0 of Hs / Cs (the local copies of P:266)
   float hreg[REC_UPC], creg[REC_UPC];
-  const bool row = b < B;
+  const bool row = warp < 4 && b < B;
   // `state = self.state` or zeros when it is still None: Switch/Merge on the device
   const bool is_tensor = a.tag == nullptr || *a.tag == 1;
 #pragma unroll
@@ -90,120 +180,126 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     }
   }
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
+  unsigned int *flags = a.barrier;  // flags[c] = 1 + last step whose h block CTA c has written
   fence_proxy_async_global();
-  unsigned int epoch = 1;
-  grid_arrive_wait(a.barrier, epoch * gridDim.x);
+  publish_flag(&flags[blockIdx.x], 1);
   const int T = a.T_dev ? *a.T_dev : a.T;
   constexpr uint32_t idesc = umma_idesc_bf16(128, 64, 0, 0);
-  mbar_wait(wfull, 0);
+  if (warp == 5) mbar_wait(wfull, 0);
 
   for (int t = 0; t < T; ++t) {
-    if (threadIdx.x == 0) {
-      fence_proxy_async_global();
-      for (int j = 0; j < nk; ++j) {
-        const int q = t * nk + j, s = q % REC_STAGES, r = q / REC_STAGES;
-        if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
-        mbar_expect_tx(&full[s], B * 128);
-        tma_load_2d(sA + s * RecSmem::A_STAGE, &tmH, &full[s], j * 64, t * B);
+    if (warp == 4) {
+      if (threadIdx.x == 128) PROBE(t, 0);
+      wait_flags_warp(flags, gridDim.x, (unsigned)t + 1);  // h_{t-1} fully written
+      if (threadIdx.x == 128) {
+        PROBE(t, 1);
+        issue_step(&tmH, ly, sA, full, empty, t, t * B);
+        PROBE(t, 2);
       }
-    } else if (threadIdx.x == 32) {
-      for (int j = 0; j < nk; ++j) {
-        const int q = t * nk + j, s = q % REC_STAGES, r = q / REC_STAGES;
-        mbar_wait(&full[s], r & 1);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(sA + s * RecSmem::A_STAGE), sw = smem_u32(sW + j * 8192);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_bf16(tmem, umma_desc_sw128(sa + k * 32, 16, 1024),
-                    umma_desc_sw128(sw + k * 32, 16, 1024), idesc, (j | k) != 0);
-        umma_commit(&empty[s]);
+      __syncwarp();
+    } else if (warp == 5) {
+      if (threadIdx.x == 160) {
+        mma_step<8192>(ly, sA, sW, full, empty, tfull, tmem, idesc, t);
+        PROBE(t, 4);
       }
-      umma_commit(tfull);
-    }
-    mbar_wait(tfull, t & 1);
-    __syncwarp();
-    tc_fence_after();
-    float z[64];
-    {
-      float lo[32], hi[32];
-      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-      tmem_ld32(ta, lo);
-      tmem_ld32(ta + 32, hi);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) { z[i] = lo[i]; z[32 + i] = hi[i]; }
-    }
-    if (row) {
-      float *g = a.G + (size_t)(t * B + b) * G4 + (size_t)blockIdx.x * 64;
-      const bool valid = !MASKED || t < len_b;
-      const int nu = min(REC_UPC, H - u0);
-      if (nu == REC_UPC) {
+      __syncwarp();
+    } else {
+      // input projection of this step (independent of h_{t-1}): load while the MMA runs
+      float z[64];
+      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * G4 + (size_t)blockIdx.x * 64;
+      if (row && nu == REC_UPC) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          float4 x = reinterpret_cast<const float4 *>(g)[q];
-          z[4 * q] += x.x; z[4 * q + 1] += x.y; z[4 * q + 2] += x.z; z[4 * q + 3] += x.w;
+          const float4 x = reinterpret_cast<const float4 *>(g)[q];
+          z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
         }
       } else {
-        for (int q = 0; q < 4 * nu; ++q) z[q] += g[q];
-      }
-      __nv_bfloat16 hb[REC_UPC];
 #pragma unroll
-      for (int u = 0; u < REC_UPC; ++u) {
-        const float ig = sigmoidf_(z[4 * u]), fg = sigmoidf_(z[4 * u + 1]);
-        const float gg = tanh_acc(z[4 * u + 2]), og = sigmoidf_(z[4 * u + 3]);
-        const float c2 = fg * creg[u] + ig * gg;
-        const float h2 = og * tanh_acc(c2);
-        z[4 * u] = ig; z[4 * u + 1] = fg; z[4 * u + 2] = gg; z[4 * u + 3] = og;
-        if (valid) { creg[u] = c2; hreg[u] = h2; }
-        hb[u] = __float2bfloat16_rn(hreg[u]);
+        for (int q = 0; q < 64; ++q) z[q] = (row && q < 4 * nu) ? g[q] : 0.f;
       }
-      // saved activations for the backward pass (in place of the projection)
-      if (nu == REC_UPC) {
+      mbar_wait(tfull, t & 1);
+      if (threadIdx.x == 0) PROBE(t, 5);
+      __syncwarp();
+      tc_fence_after();
+      {
+        float lo[32], hi[32];
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+        tmem_ld32(ta, lo);
+        tmem_ld32(ta + 32, hi);
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          reinterpret_cast<float4 *>(g)[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
-      } else {
-        for (int q = 0; q < 4 * nu; ++q) g[q] = z[q];
+        for (int i = 0; i < 32; ++i) { z[i] += lo[i]; z[32 + i] += hi[i]; }
       }
-      const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
-      for (int u = 0; u < nu; ++u) {
-        a.Cs[ro + u] = creg[u];
-        a.Hs[ro + u] = hb[u];
+      if (row) {
+        const bool valid = !MASKED || t < len_b;
+        __align__(16) __nv_bfloat16 hb[REC_UPC];
+#pragma unroll
+        for (int u = 0; u < REC_UPC; ++u) {
+          const float ig = sig_f(z[4 * u]), fg = sig_f(z[4 * u + 1]);
+          const float gg = tanh_f(z[4 * u + 2]), og = sig_f(z[4 * u + 3]);
+          const float c2 = fg * creg[u] + ig * gg;
+          const float h2 = og * tanh_f(c2);
+          z[4 * u] = ig; z[4 * u + 1] = fg; z[4 * u + 2] = gg; z[4 * u + 3] = og;
+          if (valid) { creg[u] = c2; hreg[u] = h2; }
+          hb[u] = __float2bfloat16_rn(hreg[u]);
+        }
+        const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
+        if (nu == REC_UPC) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            reinterpret_cast<float4 *>(g)[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
+          uint4 *hd = reinterpret_cast<uint4 *>(a.Hs + ro);
+          hd[0] = reinterpret_cast<const uint4 *>(hb)[0];
+          hd[1] = reinterpret_cast<const uint4 *>(hb)[1];
+          float4 *cd = reinterpret_cast<float4 *>(a.Cs + ro);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 64; ++q)
+            if (q < 4 * nu) g[q] = z[q];
+#pragma unroll
+          for (int u = 0; u < REC_UPC; ++u)
+            if (u < nu) { a.Cs[ro + u] = creg[u]; a.Hs[ro + u] = hb[u]; }
+        }
       }
+      if (threadIdx.x == 0) PROBE(t, 6);
+      fence_proxy_async_global();
     }
-    fence_proxy_async_global();
     tc_fence_before();
-    ++epoch;
-    grid_arrive_wait(a.barrier, epoch * gridDim.x);
+    publish_flag(&flags[blockIdx.x], (unsigned)t + 2);  // also the CTA's TMEM reuse boundary
     tc_fence_after();
+    if (threadIdx.x == 0) PROBE(t, 7);
   }
   // final state (committed by the commit phase only if every assumption held)
   if (row) {
-    for (int u = 0; u < REC_UPC && u0 + u < H; ++u) {
-      a.hT[(size_t)b * H + u0 + u] = hreg[u];
-      a.cT[(size_t)b * H + u0 + u] = creg[u];
-    }
+#pragma unroll
+    for (int u = 0; u < REC_UPC; ++u)
+      if (u < nu) {
+        a.hT[(size_t)b * H + u0 + u] = hreg[u];
+        a.cT[(size_t)b * H + u0 + u] = creg[u];
+      }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 64);
+  if (warp == 5) tmem_dealloc(tmem, 64);
 }
 
 // ---------------------------------------------------------------------------------- backward
 template <bool MASKED>
 __global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmDZ,  // DZ [T*B x 4H], box {64,B}
+    lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmDZ,  // DZ chunks {64, T*B, nk}
                         const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,16}
-                        RecBwdArgs a) {
+                        RecBwdArgs a, RecLayout ly) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   const int G4 = 4 * a.H;
-  const int nk = (G4 + 63) / 64;
-  uint8_t *sW = base;                                   // nk x 2 KB (16 rows x 128 B)
-  uint8_t *sA = sW + ((nk * 2048 + 1023) & ~1023);      // REC_STAGES x 16 KB
-  uint64_t *full = reinterpret_cast<uint64_t *>(sA + REC_STAGES * RecSmem::A_STAGE);
-  uint64_t *empty = full + REC_STAGES;
-  uint64_t *tfull = empty + REC_STAGES;
+  const int nk = ly.nk, S = ly.nslots;
+  uint8_t *sW = base;
+  uint8_t *sA = sW + ly.wbytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sA + (size_t)S * ly.ch * ly.cb + PAD);
+  uint64_t *empty = full + S;
+  uint64_t *tfull = empty + S;
   uint64_t *wfull = tfull + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
 
@@ -213,123 +309,173 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   const int B = a.B, H = a.H;
   if (a.fail && *a.fail) return;
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 128) {
     tma_prefetch_desc(&tmDZ);
     tma_prefetch_desc(&tmWT);
-    for (int s = 0; s < REC_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
     mbar_init(wfull, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 32);
+  if (warp == 5) tmem_alloc(tmem_slot, 32);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 128) {
     mbar_expect_tx(wfull, nk * 2048);
     for (int j = 0; j < nk; ++j) tma_load_2d(sW + j * 2048, &tmWT, wfull, j * 64, u0);
   }
   const int T = a.T_dev ? *a.T_dev : a.T;
-  const bool row = b < B;
+  const bool row = warp < 4 && b < B;
   const int nu = min(REC_UPC, H - u0);
   // While mode: dz rows of the steps beyond the device trip count must not contribute to wgrads
   if (MASKED && row) {
     for (int t = T; t < a.T; ++t)
       for (int q = 0; q < 4 * nu; ++q)
-        a.DZ[(size_t)(t * B + b) * G4 + (size_t)blockIdx.x * 64 + q] = __float2bfloat16_rn(0.f);
+        a.DZ[(size_t)(t * B + b) * a.ldz + (size_t)blockIdx.x * 64 + q] = __float2bfloat16_rn(0.f);
   }
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
   float dcreg[REC_UPC], carry[REC_UPC];
 #pragma unroll
   for (int u = 0; u < REC_UPC; ++u) { dcreg[u] = 0.f; carry[u] = 0.f; }
   constexpr uint32_t idesc = umma_idesc_bf16(128, 16, 0, 0);
-  mbar_wait(wfull, 0);
-  unsigned int epoch = 0;
-  int q = 0;  // global chunk counter (ring position)
+  if (warp == 5) mbar_wait(wfull, 0);
+  unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c has completed
+  int nmma = 0;                     // steps that issued MMAs (tfull phase)
 
   for (int t = T - 1; t >= 0; --t) {
     const bool has_next = t + 1 < T;  // dz_{t+1} exists
-    if (has_next) {
-      if (threadIdx.x == 0) {
-        fence_proxy_async_global();
-        for (int j = 0; j < nk; ++j) {
-          const int qq = q + j, s = qq % REC_STAGES, r = qq / REC_STAGES;
-          if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
-          mbar_expect_tx(&full[s], B * 128);
-          tma_load_2d(sA + s * RecSmem::A_STAGE, &tmDZ, &full[s], j * 64, (t + 1) * B);
+    const int ti = T - 1 - t;          // probe / ring index
+    if (warp == 4) {
+      if (has_next) {
+        if (threadIdx.x == 128) PROBE(ti, 0);
+        wait_flags_warp(flags, gridDim.x, (unsigned)(T - 1 - t));  // dz_{t+1} fully written
+        if (threadIdx.x == 128) {
+          PROBE(ti, 1);
+          issue_step(&tmDZ, ly, sA, full, empty, nmma, (t + 1) * B);
+          PROBE(ti, 2);
         }
-      } else if (threadIdx.x == 32) {
-        for (int j = 0; j < nk; ++j) {
-          const int qq = q + j, s = qq % REC_STAGES, r = qq / REC_STAGES;
-          mbar_wait(&full[s], r & 1);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(sA + s * RecSmem::A_STAGE), sw = smem_u32(sW + j * 2048);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(tmem, umma_desc_sw128(sa + k * 32, 16, 1024),
-                      umma_desc_sw128(sw + k * 32, 16, 1024), idesc, (j | k) != 0);
-          umma_commit(&empty[s]);
-        }
-        umma_commit(tfull);
       }
-      q += nk;
-    }
-    float dh[REC_UPC];
-    if (has_next) {
-      mbar_wait(tfull, epoch & 1);
-      ++epoch;
       __syncwarp();
-      tc_fence_after();
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), dh);
+    } else if (warp == 5) {
+      if (has_next && threadIdx.x == 160) {
+        mma_step<2048>(ly, sA, sW, full, empty, tfull, tmem, idesc, nmma);
+        PROBE(ti, 4);
+      }
+      __syncwarp();
     } else {
+      // per-step operands independent of dz_{t+1}: load while the MMA runs
+      const size_t r = (size_t)(t * B + (row ? b : 0));
+      float gt[64], ct[REC_UPC], cp[REC_UPC], din[REC_UPC];
+      {
+        const float *g = a.G + r * G4 + (size_t)blockIdx.x * 64;
+        const float *pc = a.Cs + (r + B) * a.ldh + u0;
+        const float *pp = a.Cs + r * a.ldh + u0;
+        const float *pd = a.dHin + r * a.ldd + u0;
+        if (row && nu == REC_UPC) {
 #pragma unroll
-      for (int u = 0; u < REC_UPC; ++u) dh[u] = 0.f;
-    }
-    if (row) {
-      const size_t r = (size_t)(t * B + b);
-      const float *din = a.dHin + r * a.ldd + u0;
-      const float *g = a.G + r * G4 + (size_t)blockIdx.x * 64;
-      const float *ct = a.Cs + (r + B) * a.ldh + u0;
-      const float *cp = a.Cs + r * a.ldh + u0;
-      __nv_bfloat16 *dz = a.DZ + r * G4 + (size_t)blockIdx.x * 64;
-      const bool valid = !MASKED || t < len_b;
-      for (int u = 0; u < nu; ++u) {
-        const float dhu = dh[u] + din[u] + carry[u];
-        const float ig = g[4 * u], fg = g[4 * u + 1], gg = g[4 * u + 2], og = g[4 * u + 3];
-        if (valid) {
-          const float tc = tanh_acc(ct[u]);
-          const float dout = dhu * tc;
-          const float dc = dcreg[u] + dhu * og * (1.f - tc * tc);
-          const float di = dc * gg, dg = dc * ig, df = dc * cp[u];
-          dcreg[u] = dc * fg;
-          carry[u] = 0.f;
-          dz[4 * u] = __float2bfloat16_rn(di * ig * (1.f - ig));
-          dz[4 * u + 1] = __float2bfloat16_rn(df * fg * (1.f - fg));
-          dz[4 * u + 2] = __float2bfloat16_rn(dg * (1.f - gg * gg));
-          dz[4 * u + 3] = __float2bfloat16_rn(dout * og * (1.f - og));
+          for (int k = 0; k < 16; ++k) {
+            const float4 x = reinterpret_cast<const float4 *>(g)[k];
+            gt[4 * k] = x.x; gt[4 * k + 1] = x.y; gt[4 * k + 2] = x.z; gt[4 * k + 3] = x.w;
+          }
+#pragma unroll
+          for (int u = 0; u < REC_UPC; ++u) { ct[u] = pc[u]; cp[u] = pp[u]; din[u] = pd[u]; }
         } else {
-          carry[u] = dhu;  // masked step: (h, c) passed through unchanged
-          dz[4 * u] = dz[4 * u + 1] = dz[4 * u + 2] = dz[4 * u + 3] = __float2bfloat16_rn(0.f);
+#pragma unroll
+          for (int k = 0; k < 64; ++k) gt[k] = (row && k < 4 * nu) ? g[k] : 0.f;
+#pragma unroll
+          for (int u = 0; u < REC_UPC; ++u) {
+            const bool ok = row && u < nu;
+            ct[u] = ok ? pc[u] : 0.f; cp[u] = ok ? pp[u] : 0.f; din[u] = ok ? pd[u] : 0.f;
+          }
         }
       }
+      float dh[REC_UPC];
+      if (has_next) {
+        mbar_wait(tfull, nmma & 1);
+        if (threadIdx.x == 0) PROBE(ti, 5);
+        __syncwarp();
+        tc_fence_after();
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), dh);
+      } else {
+#pragma unroll
+        for (int u = 0; u < REC_UPC; ++u) dh[u] = 0.f;
+      }
+      if (row) {
+        __nv_bfloat16 *dz = a.DZ + r * a.ldz + (size_t)blockIdx.x * 64;
+        const bool valid = !MASKED || t < len_b;
+        __align__(16) __nv_bfloat16 dzb[64];
+#pragma unroll
+        for (int u = 0; u < REC_UPC; ++u) {
+          const float dhu = dh[u] + din[u] + carry[u];
+          const float ig = gt[4 * u], fg = gt[4 * u + 1], gg = gt[4 * u + 2], og = gt[4 * u + 3];
+          if (valid) {
+            const float tc = tanh_f(ct[u]);
+            const float dout = dhu * tc;
+            const float dc = dcreg[u] + dhu * og * (1.f - tc * tc);
+            const float di = dc * gg, dg = dc * ig, df = dc * cp[u];
+            dcreg[u] = dc * fg;
+            carry[u] = 0.f;
+            dzb[4 * u] = __float2bfloat16_rn(di * ig * (1.f - ig));
+            dzb[4 * u + 1] = __float2bfloat16_rn(df * fg * (1.f - fg));
+            dzb[4 * u + 2] = __float2bfloat16_rn(dg * (1.f - gg * gg));
+            dzb[4 * u + 3] = __float2bfloat16_rn(dout * og * (1.f - og));
+          } else {
+            carry[u] = dhu;  // masked step: (h, c) passed through unchanged
+            dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
+          }
+        }
+        if (nu == REC_UPC) {
+          uint4 *d4 = reinterpret_cast<uint4 *>(dz);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 64; ++k)
+            if (k < 4 * nu) dz[k] = dzb[k];
+        }
+      }
+      if (threadIdx.x == 0) PROBE(ti, 6);
+      fence_proxy_async_global();
     }
-    fence_proxy_async_global();
+    if (has_next) ++nmma;
     tc_fence_before();
-    grid_arrive_wait(a.barrier, (unsigned)(T - t) * gridDim.x);
+    publish_flag(&flags[blockIdx.x], (unsigned)(T - t));
     tc_fence_after();
+    if (threadIdx.x == 0) PROBE(ti, 7);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 32);
+  if (warp == 5) tmem_dealloc(tmem, 32);
 }
 
 // ---------------------------------------------------------------------------------- host
-static int fwd_smem(int H) { return 1024 + ((H + 63) / 64) * 8192 + REC_STAGES * RecSmem::A_STAGE + 256; }
-static int bwd_smem(int H) {
-  const int nk = (4 * H + 63) / 64;
-  return 1024 + ((nk * 2048 + 1023) & ~1023) + REC_STAGES * RecSmem::A_STAGE + 256;
+static RecLayout layout(int wbytes, int nk, int B) {
+  RecLayout l;
+  l.nk = nk;
+  l.wbytes = (wbytes + 1023) & ~1023;
+  l.bp = (B + 7) & ~7;
+  l.cb = l.bp * 128;
+  const int avail = SMEM_BUDGET - l.wbytes - PAD - 1024 /*barriers*/;
+  const int max_chunks = avail / l.cb;  // chunks that fit in flight
+  // two ring slots (TMA of op k+1 overlaps the MMAs of op k); a whole step in flight if it fits
+  l.nslots = 2;
+  l.ch = std::min((nk + 1) / 2, max_chunks / 2);
+  l.ch = std::max(1, std::min(l.ch, 256));
+  l.rot = 0;
+  if (const char *e = getenv("JANUS_REC_CH")) {  // experiment knob: chunks per TMA op
+    const int ch = atoi(e);
+    if (ch >= 1) {
+      l.ch = std::min(ch, nk);
+      l.nslots = std::max(2, std::min(REC_MAX_SLOTS, max_chunks / l.ch));
+    }
+  }
+  if (const char *e = getenv("JANUS_REC_ROT")) l.rot = atoi(e) && l.ch == 1;
+  l.nops = (nk + l.ch - 1) / l.ch;
+  return l;
 }
+static int smem_of(const RecLayout &l) { return 1024 + l.wbytes + l.nslots * l.ch * l.cb + PAD + 1024; }
 
 int rec_grid(int H) { return (H + REC_UPC - 1) / REC_UPC; }
 
@@ -350,30 +496,38 @@ static cudaError_t coop_launch(const void *fn, int grid, int smem, void **args, 
 cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw, bool masked,
                          cudaStream_t st) {
   if (a.B > 128 || a.B < 1) return cudaErrorInvalidValue;
+  const int nk = (a.H + 63) / 64;
+  RecLayout ly = layout(nk * 8192, nk, a.B);
+  if (ly.ch < 1 || smem_of(ly) > 232448) return cudaErrorInvalidValue;
   CUtensorMap tmH, tmW;
-  if (!make_tmap_bf16(&tmH, a.Hs, a.H, (uint64_t)(a.T + 1) * a.B, a.ldh, a.B)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_chunks(&tmH, a.Hs, (uint64_t)(a.T + 1) * a.B, a.ldh, nk, ly.bp, ly.ch))
+    return cudaErrorInvalidValue;
   if (!make_tmap_bf16(&tmW, Whh, a.H, 4ull * a.H, ldw, 64)) return cudaErrorInvalidValue;
-  const int smem = fwd_smem(a.H);
+  const int smem = smem_of(ly);
   const void *fn = masked ? (const void *)lstm_rec_fwd_kernel<true> : (const void *)lstm_rec_fwd_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   RecFwdArgs aa = a;
-  void *args[] = {&tmH, &tmW, &aa};
+  void *args[] = {&tmH, &tmW, &aa, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
 
 cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
                          cudaStream_t st) {
   if (a.B > 128 || a.B < 1) return cudaErrorInvalidValue;
+  const int nk = (4 * a.H + 63) / 64;
+  RecLayout ly = layout(nk * 2048, nk, a.B);
+  if (ly.ch < 1 || smem_of(ly) > 232448) return cudaErrorInvalidValue;
   CUtensorMap tmDZ, tmWT;
-  if (!make_tmap_bf16(&tmDZ, a.DZ, 4ull * a.H, (uint64_t)a.T * a.B, 4ull * a.H, a.B)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_chunks(&tmDZ, a.DZ, (uint64_t)a.T * a.B, a.ldz, nk, ly.bp, ly.ch))
+    return cudaErrorInvalidValue;
   if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 16)) return cudaErrorInvalidValue;
-  const int smem = bwd_smem(a.H);
+  const int smem = smem_of(ly);
   const void *fn = masked ? (const void *)lstm_rec_bwd_kernel<true> : (const void *)lstm_rec_bwd_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   RecBwdArgs aa = a;
-  void *args[] = {&tmDZ, &tmWT, &aa};
+  void *args[] = {&tmDZ, &tmWT, &aa, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
 

@@ -19,6 +19,7 @@ struct RecFwdArgs {
   unsigned int *barrier = nullptr;           // zeroed before the launch
   const int *fail = nullptr;                 // nonzero: skip (cooperative cancellation)
   const int *tag = nullptr;                  // state type tag; != 1 -> h0 = c0 = 0 (device Switch)
+  unsigned long long *dbg = nullptr;         // optional %globaltimer probe of CTA 0 (8 per step)
 };
 
 struct RecBwdArgs {
@@ -30,9 +31,11 @@ struct RecBwdArgs {
   int ldh = 0;
   const float *dHin = nullptr;    // [T*B][ldd] gradient into h_t from above (decoder / next layer)
   int ldd = 0;
-  __nv_bfloat16 *DZ = nullptr;    // [T*B][4H] out: rb(dz), interleaved columns
+  __nv_bfloat16 *DZ = nullptr;    // [T*B][ldz] out: rb(dz), interleaved columns
+  int ldz = 0;                    // >= 64 * ceil(4H / 64), zero padding beyond 4H
   unsigned int *barrier = nullptr;
   const int *fail = nullptr;
+  unsigned long long *dbg = nullptr;
 };
 
 int rec_grid(int H);

@@ -249,3 +249,25 @@ class Graph:
         buf = C.create_string_buffer(4096)
         lib.janus_describe(self.h, buf, 4096)
         return buf.value.decode()
+
+
+# ----------------------------------------------------------------------------------- dev hooks
+lib.janus_dev_profile.restype, lib.janus_dev_profile.argtypes = C.c_int32, [C.c_void_p, C.c_int32]
+lib.janus_dev_phase_report.restype = C.c_int32
+lib.janus_dev_phase_report.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+
+
+def dev_profile(graph, enable):
+    lib.janus_dev_profile(graph.h, int(enable))
+
+
+def dev_phase_report(graph):
+    """{phase: (total_ms, launches)} since dev_profile(graph, True)."""
+    buf = C.create_string_buffer(1 << 16)
+    lib.janus_dev_phase_report(graph.h, buf, 1 << 16)
+    out = {}
+    for item in buf.value.decode().split(";"):
+        if item:
+            name, ms, cnt = item.rsplit(":", 2)
+            out[name] = (float(ms), int(cnt))
+    return out
