@@ -39,6 +39,7 @@ struct LmPlan {
     size_t gWih[4], gWhh[4], gWdec = 0;
     size_t seg_word = 0, seg_start = 0, seg_grad = 0, nseg = 0, keys = 0;
     size_t small_ws = 0;
+    size_t arena_begin = 0, arena_end = 0, dEd = 0, dp_scratch = 0;
   } off;
   int Ep = 0, Hp = 0, Gz = 0;  // padded row pitches (elements)
   int nbar = 0;
@@ -107,6 +108,7 @@ struct Graph {
   // pinned status readback
   DevStatus *h_status = nullptr;
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
+  bool dp = false;       // data-parallel collectives in the step (fixed at build)
   std::string describe;
   unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (16*T u64)
 };
@@ -132,6 +134,17 @@ size_t imperative_ws_bytes(const Graph &g);
 janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
                             const janus_tensor *state, int n_state, const janus_tensor *outs,
                             int n_outs, const janus_tensor &ws, cudaStream_t st);
+
+// host_dp.cpp: NCCL data parallelism
+bool dp_enabled(const Graph &g);
+bool dp_wanted(const janus_build_opts &o);  // decided once, at build time
+janus_status dp_init(Graph &g);
+void dp_destroy(Graph &g);
+janus_status dp_allreduce_sum(Graph &g, float *buf, size_t n, cudaStream_t st);
+janus_status dp_agree(Graph &g, DevStatus *st_dev, long long *scratch, cudaStream_t st);
+// a data-parallel rank whose DISPATCH guards failed still joins every collective (null step)
+janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,
+                         janus_failure *fail);
 
 // one D2H of the status word + stream sync; decodes the failure (host_lm.cpp)
 janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_outs,

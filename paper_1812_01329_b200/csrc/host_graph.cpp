@@ -260,6 +260,7 @@ janus_status janus_graph_build(const janus_op *ops, int32_t n_ops, const janus_a
     delete g;
     return s;
   }
+  g->dp = dp_wanted(g->opts);
   std::string why_lm, why_tree;
   if (lower_lm(*g, why_lm)) g->kind = "lstm_lm";
   else if (lower_tree(*g, why_tree)) g->kind = "treelstm";
@@ -289,13 +290,18 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
   if (g->kind.empty()) return JANUS_ERR_UNSUPPORTED;
   if (n_args < g->n_args || n_state < g->n_state) return JANUS_ERR_INVALID;
   janus_failure f{};
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   if (!check_dispatch(*g, args, n_args, &f)) {
+    g->aborts++;
+    if (dp_enabled(*g) && g->kind == "lstm_lm" && g->lm.bf16) {
+      // data parallel: still join the step's collectives (null step) so peers cannot block
+      janus_status r = run_lm_null(*g, f, workspace, st, fail);
+      return r == JANUS_OK ? JANUS_ASSUMPTION_FAILED : r;
+    }
     // cache miss: nothing is launched, nothing mutated
     if (fail) *fail = f;
-    g->aborts++;
     return JANUS_ASSUMPTION_FAILED;
   }
-  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
   janus_status r;
   if (g->kind == "lstm_lm") r = run_lm(*g, args, state, outs, n_outs, workspace, st, fail);
   else r = run_tree(*g, args, n_args, state, outs, n_outs, workspace, st, fail);
@@ -357,6 +363,7 @@ int32_t janus_dev_phase_report(const janus_graph *g, char *buf, size_t len) {
 
 void janus_graph_destroy(janus_graph *g) {
   if (!g) return;
+  dp_destroy(*g);
   if (g->h_status) cudaFreeHost(g->h_status);
   delete g;
 }

@@ -217,8 +217,6 @@ bool lower_lm(Graph &g, std::string &why) {
       p.off.dX[l] = take(TB * Inp * 4);
       p.off.hT[l] = take((size_t)B * H * 4);
       p.off.cT[l] = take((size_t)B * H * 4);
-      p.off.gWih[l] = take((size_t)G4 * Inp * 4);
-      p.off.gWhh[l] = take((size_t)G4 * p.Hp * 4);
     }
     p.off.Wdec_b = take((size_t)V * p.Hp * 2);
     p.off.X = take(TB * p.Ep * 2);
@@ -226,7 +224,17 @@ bool lower_lm(Graph &g, std::string &why) {
     p.off.dy = take(TB * Vp * 2);
     p.off.rowloss = take(TB * 4);
     p.off.dHtop = take(TB * p.Hp * 4);
+    // gradient arena: one contiguous fp32 block, allreduced in one NCCL call under DP
+    p.off.arena_begin = o;
+    for (int l = 0; l < p.L; ++l) {
+      const int Inp = l ? p.Hp : p.Ep;
+      p.off.gWih[l] = take((size_t)G4 * Inp * 4);
+      p.off.gWhh[l] = take((size_t)G4 * p.Hp * 4);
+    }
     p.off.gWdec = take((size_t)V * p.Hp * 4);
+    if (dp_enabled(g)) p.off.dEd = take((size_t)V * E * 4);  // dense embedding gradient
+    p.off.arena_end = o;
+    p.off.dp_scratch = take(64);
     p.off.seg_word = take(TB * 4);
     p.off.seg_start = take((TB + 1) * 4);
     p.off.seg_grad = take(TB * p.Ep * 4);
@@ -306,7 +314,7 @@ janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_ou
   if (h.status == JANUS_ASSUMPTION_FAILED) {
     if (fail) {
       fail->assumption_id = (uint32_t)(h.key >> IDX_BITS);
-      fail->rank = g.opts.rank;
+      fail->rank = g.nccl ? h.pad[0] : g.opts.rank;  // DP: the rank that failed (agreement)
       const unsigned long long idx = h.key & ((1ull << IDX_BITS) - 1);
       fail->index = idx == (1ull << IDX_BITS) - 1 ? -1 : (int64_t)idx;
       fail->observed = h.observed;
@@ -392,6 +400,10 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   }
 
   // ------------------------------------------------------------ tcgen05 device program
+  if (dp_enabled(g)) {
+    janus_status r = dp_init(g);
+    if (r != JANUS_OK) return r;
+  }
   const int T = p.T;              // unrolled T or max width W
   const int Tw = p.while_mode ? Wd : T;  // width of this batch
   const int TB = Tw * B;
@@ -494,7 +506,20 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
                            nseg, reinterpret_cast<unsigned long long *>(W + p.off.keys), st));
     g.launches++;  // embed grad is two kernels
   }
+  if (g.nccl) {
+    // DP: dense embedding gradient, one allreduce(sum) of the whole gradient arena
+    if (p.lr_E != 0)
+      LCHK("dp_scatter", launch_scatter_rows(fp(p.off.seg_grad), Ep, seg_word, nseg, fp(p.off.dEd), V, E, st));
+    g.prof.mark("dp_allreduce", st);
+    janus_status r = dp_allreduce_sum(g, fp(p.off.arena_begin), (p.off.arena_end - p.off.arena_begin) / 4, st);
+    if (r != JANUS_OK) return r;
+  }
   LCHK("finalize", launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
+  if (g.nccl) {  // every rank learns the same status before anything commits (reading Q12)
+    g.prof.mark("dp_agree", st);
+    janus_status r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
+    if (r != JANUS_OK) return r;
+  }
   // ---- the all-or-nothing commit (P:164, P:266 (4))
   CommitList cl{};
   auto add = [&](CommitSeg s) { cl.s[cl.n++] = s; };
@@ -514,11 +539,38 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     CommitSeg s{};
     if (p.lr_Wdec != 0) { s = {}; s.kind = C_DENSE; s.dst = P.Wdec; s.grad = fp(p.off.gWdec); s.rows = V; s.cols = H; s.ldg = Hp; s.lr = p.lr_Wdec / nr; add(s); }
     if (p.lr_bdec != 0) { s = {}; s.kind = C_BIAS_COL; s.dst = P.bdec; s.grad = fp(p.off.gWdec); s.rows = V; s.cols = 1; s.ldg = Hp; s.col = H; s.lr = p.lr_bdec / nr; add(s); }
-    if (p.lr_E != 0) { s = {}; s.kind = C_SPARSE_ROWS; s.dst = P.E; s.grad = fp(p.off.seg_grad); s.cols = E; s.ldg = Ep; s.rows_idx = seg_word; s.nrows = nseg; s.lr = p.lr_E / nr; add(s); }
+    if (p.lr_E != 0 && !g.nccl) { s = {}; s.kind = C_SPARSE_ROWS; s.dst = P.E; s.grad = fp(p.off.seg_grad); s.cols = E; s.ldg = Ep; s.rows_idx = seg_word; s.nrows = nseg; s.lr = p.lr_E / nr; add(s); }
+    if (p.lr_E != 0 && g.nccl) { s = {}; s.kind = C_DENSE; s.dst = P.E; s.grad = fp(p.off.dEd); s.rows = V; s.cols = E; s.ldg = E; s.lr = p.lr_E / nr; add(s); }
     if (p.write_tag && P.tag) { s = {}; s.kind = C_TAG; s.idst = P.tag; s.ival = 1; add(s); }
   }
   LCHK("commit", launch_commit(cl, dst, st));
   return finish(g, dst, outs, n_outs, st, fail);
+}
+
+}  // namespace jk
+
+namespace jk {
+
+// Null step of a data-parallel rank whose DISPATCH guards failed (P:162 cache miss): it launches no
+// compute, but joins the same collective sequence as a normal step so its peers cannot block, and
+// publishes its failure through the agreement so every rank aborts (reading Q12).
+janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,
+                         janus_failure *fail) {
+  const LmPlan &p = g.lm;
+  if (!ws.data || !p.bf16) return JANUS_ERR_INVALID;
+  janus_status r = dp_init(g);
+  if (r != JANUS_OK) return r;
+  uint8_t *W = static_cast<uint8_t *>(ws.data);
+  DevStatus *dst = reinterpret_cast<DevStatus *>(W + p.off.status);
+  unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
+  LCHK("init", launch_step_init(dst, bars, p.nbar, st));
+  LCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
+  r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + p.off.arena_begin),
+                       (p.off.arena_end - p.off.arena_begin) / 4, st);
+  if (r != JANUS_OK) return r;
+  r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
+  if (r != JANUS_OK) return r;
+  return finish(g, dst, nullptr, 0, st, fail);
 }
 
 }  // namespace jk

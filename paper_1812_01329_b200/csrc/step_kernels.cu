@@ -396,6 +396,78 @@ cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl,
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ data parallel
+__global__ void dp_pack_kernel(const DevStatus *st, long long *sc, int rank) {
+  const unsigned long long key = st->key;
+  unsigned long long p = KEY_PASS;
+  if (key != KEY_PASS)
+    p = ((key >> IDX_BITS) << 48) | ((unsigned long long)(rank & 0xff) << IDX_BITS) |
+        (key & ((1ull << IDX_BITS) - 1));
+  sc[0] = (long long)p;
+  sc[1] = st->runtime_err;
+  sc[3] = (long long)p;
+}
+cudaError_t launch_dp_pack(const DevStatus *st, long long *scratch, int rank, cudaStream_t s) {
+  dp_pack_kernel<<<1, 1, 0, s>>>(st, scratch, rank);
+  return cudaGetLastError();
+}
+__global__ void dp_observed_kernel(const DevStatus *st, long long *sc) {
+  const bool mine = sc[3] == sc[0] && (unsigned long long)sc[0] != KEY_PASS;
+  sc[2] = mine ? st->observed : (long long)(-9223372036854775807LL - 1);
+}
+cudaError_t launch_dp_observed(const DevStatus *st, long long *scratch, cudaStream_t s) {
+  dp_observed_kernel<<<1, 1, 0, s>>>(st, scratch);
+  return cudaGetLastError();
+}
+__global__ void dp_unpack_kernel(DevStatus *st, const long long *sc) {
+  const unsigned long long p = (unsigned long long)sc[0];
+  if (p != KEY_PASS) {
+    st->key = ((p >> 48) << IDX_BITS) | (p & ((1ull << IDX_BITS) - 1));
+    st->pad[0] = (int)((p >> IDX_BITS) & 0xff);
+    st->observed = sc[2];
+    st->status = 1;
+  } else {
+    st->key = KEY_PASS;
+    st->runtime_err = (int)sc[1];
+    st->status = sc[1] ? 4 : 0;
+  }
+}
+cudaError_t launch_dp_unpack(DevStatus *st, const long long *scratch, cudaStream_t s) {
+  dp_unpack_kernel<<<1, 1, 0, s>>>(st, scratch);
+  return cudaGetLastError();
+}
+__global__ void set_failure_kernel(DevStatus *st, unsigned id, long long index, long long observed) {
+  const unsigned long long idx = index < 0 ? (1ull << IDX_BITS) - 1 : (unsigned long long)index;
+  st->key = ((unsigned long long)id << IDX_BITS) | idx;
+  st->observed = observed;
+  st->status = 1;
+}
+cudaError_t launch_set_failure(DevStatus *st, unsigned id, long long index, long long observed,
+                               cudaStream_t s) {
+  set_failure_kernel<<<1, 1, 0, s>>>(st, id, index, observed);
+  return cudaGetLastError();
+}
+__global__ void scatter_rows_kernel(const float *seg_grad, int ldg, const int *seg_word,
+                                    const int *nseg, float *dense, int V, int cols) {
+  const long long n = (long long)V * cols;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += stride) dense[e] = 0.f;
+  // a grid-wide zero-then-scatter needs ordering: done by the second launch below
+}
+__global__ void scatter_rows2_kernel(const float *seg_grad, int ldg, const int *seg_word,
+                                     const int *nseg, float *dense, int cols) {
+  const int ns = *nseg;
+  for (int k = blockIdx.x; k < ns; k += gridDim.x)
+    for (int j = threadIdx.x; j < cols; j += blockDim.x)
+      dense[(size_t)seg_word[k] * cols + j] = seg_grad[(size_t)k * ldg + j];
+}
+cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_word, const int *nseg,
+                                float *dense, int V, int cols, cudaStream_t s) {
+  scatter_rows_kernel<<<4 * NSM, 256, 0, s>>>(seg_grad, ldg, seg_word, nseg, dense, V, cols);
+  scatter_rows2_kernel<<<4 * NSM, 256, 0, s>>>(seg_grad, ldg, seg_word, nseg, dense, cols);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ commit
 // Predicated on the device status: with any failure nothing is written (all-or-nothing).
 __global__ void commit_kernel(CommitList cl, const DevStatus *st) {

@@ -77,6 +77,19 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
 cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
                             int world_size, cudaStream_t s);
 
+// data-parallel abort agreement (host_dp.cpp): scratch[0] = packed key (MIN over ranks),
+// scratch[1] = runtime error (MAX), scratch[2] = observed of the winning rank (MAX), scratch[3] =
+// this rank's packed key. DevStatus.pad[0] receives the failing rank.
+cudaError_t launch_dp_pack(const DevStatus *st, long long *scratch, int rank, cudaStream_t s);
+cudaError_t launch_dp_observed(const DevStatus *st, long long *scratch, cudaStream_t s);
+cudaError_t launch_dp_unpack(DevStatus *st, const long long *scratch, cudaStream_t s);
+// a dispatch failure on this rank inside a data-parallel null step
+cudaError_t launch_set_failure(DevStatus *st, unsigned id, long long index, long long observed,
+                               cudaStream_t s);
+// dense embedding gradient for the data-parallel allreduce: zero + scatter the segment sums
+cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_word, const int *nseg,
+                                float *dense, int V, int cols, cudaStream_t s);
+
 // commit segments (P:164 all-or-nothing, P:282 deferred update)
 enum CommitKind { C_DENSE = 0, C_DENSE_IL = 1, C_BIAS_COL = 2, C_BIAS_COL_IL = 3, C_COPY = 4,
                   C_TAG = 5, C_SPARSE_ROWS = 6 };

@@ -257,6 +257,30 @@ lib.janus_dev_phase_report.restype = C.c_int32
 lib.janus_dev_phase_report.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
 
 
+lib.janus_nccl_unique_id.restype = C.c_int32
+lib.janus_nccl_unique_id.argtypes = [C.c_void_p]
+
+
+def nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    if lib.janus_nccl_unique_id(buf) != 0:
+        raise JanusError("ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def broadcast_bytes(data, rank, src=0):
+    """Broadcast a bytes object from `src` over the default torch.distributed group (any backend)."""
+    import torch.distributed as dist
+    obj = [data if rank == src else None]
+    dist.broadcast_object_list(obj, src=src)
+    return obj[0]
+
+
+def nccl_unique_id_bcast(rank, world):
+    """Rank 0 creates the NCCL unique id; torch.distributed carries it to every rank."""
+    return broadcast_bytes(nccl_unique_id() if rank == 0 else None, rank)
+
+
 def dev_profile(graph, enable):
     lib.janus_dev_profile(graph.h, int(enable))
 

@@ -161,6 +161,34 @@ def test_lm_guards_and_all_or_nothing():
     assert all(a.tobytes() == b.tobytes() for a, b in zip(to_host(dev), state))
 
 
+def test_lm_dp_collective_path_single_gpu(monkeypatch):
+    """The data-parallel step (NCCL allreduce of the gradient arena, dense embedding gradient,
+    abort agreement) on a 1-rank communicator equals the single-GPU step bit for bit; a dispatch
+    failure runs the null step and still reports the failure."""
+    B, T, V = 8, 6, 64
+    prog = pg.lstm_lm_program(V=V, E=40, H=48, L=2, B=B, T=T, lr=0.5)
+    janus = J()
+    g1 = janus.Graph(prog)
+    monkeypatch.setenv("JANUS_FORCE_DP", "1")
+    g2 = janus.Graph(prog)
+    monkeypatch.delenv("JANUS_FORCE_DP")
+    state = gen.uniform_params(prog, 9, 0.1)
+    args = _lm_batches(B, T, V, 1)[0]
+    d1, d2 = to_dev(state), to_dev(state)
+    s1, _, l1 = _step(g1, g1.new_workspace(), args, d1)
+    ws2 = g2.new_workspace()
+    s2, _, l2 = _step(g2, ws2, args, d2)
+    assert s1 == s2 == I.OK and l1 == l2
+    for a, b in zip(to_host(d1), to_host(d2)):
+        assert a.tobytes() == b.tobytes()
+    bad = ln = args[2].copy(); bad[3] = T - 1
+    st, fail, _ = _step(g2, ws2, (args[0], args[1], bad), d2)
+    assert st == I.ASSUMPTION_FAILED and fail == dict(assumption_id=2, rank=0, index=3, observed=T - 1)
+    st, fail, _ = _step(g2, ws2, (args[0][:B - 1], args[1][:B - 1], ln[:B - 1]), d2)   # null step
+    assert st == I.ASSUMPTION_FAILED and fail["assumption_id"] == 4 and fail["observed"] == B - 1
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(to_host(d1), to_host(d2)))
+
+
 def test_lm_host_buffers_e2e_equal_device_args():
     """janus_run with host (pinned) argument buffers stages them through the workspace."""
     B, T, V = 8, 6, 64
