@@ -27,6 +27,11 @@ int32_t janus_dev_profile(struct janus_graph *g, int32_t enable);
 /* Timeline probe of the layer-0 recurrent kernels (CTA 0): dev_buf (device, 16*T u64) receives
  * %globaltimer stamps, 8 per step: forward at [0, 8T), backward at [8T, 16T). NULL disables. */
 int32_t janus_dev_set_probe(struct janus_graph *g, void *dev_buf);
+/* Byte offset and size of a named region of the workspace after janus_run: "status",
+ * "tree.height", "tree.order", "tree.irank", "tree.pslot", "tree.lvl_off", "tree.meta"
+ * (int32 arrays of the device-built level schedule). Returns 0, or -1 if unknown. */
+int32_t janus_dev_workspace_region(const struct janus_graph *g, const char *name, size_t *offset,
+                                   size_t *bytes);
 int32_t janus_dev_phase_report(const struct janus_graph *g, char *buf, size_t len);
 
 #ifdef __cplusplus

@@ -27,7 +27,7 @@ template <int BN, int A_MN, int B_MN, int STAGES>
 __global__ void __launch_bounds__(128, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, GemmEpilogue ep, int M, int N,
-                        int K) {
+                        int K, const int *K_dev) {
   using C = GemmCfg<BN, A_MN, B_MN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(128, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * C::BM;
+  if (K_dev) K = min(K, *K_dev);  // reduction length known only on the device
   const int nk = (K + C::BK - 1) / C::BK;
 
   if (warp == 0 && lane == 0) {
@@ -113,6 +114,10 @@ __global__ void __launch_bounds__(128, 1)
     if (n >= N) break;  // warp-uniform
     float v[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c * 32, v);
+    if (nk == 0) {  // empty reduction: the TMEM accumulator was never written
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    }
     if (!row_ok) continue;
     if (ep.bias_row) {
       const float bv = ep.bias_row[m];
@@ -225,7 +230,7 @@ static cudaError_t launch(const GemmOp &op, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((op.N + BN - 1) / BN, (op.M + 127) / 128);
-  kern<<<grid, 128, C::SMEM, st>>>(ta, tb, op.ep, op.M, op.N, op.K);
+  kern<<<grid, 128, C::SMEM, st>>>(ta, tb, op.ep, op.M, op.N, op.K, op.K_dev);
   return cudaGetLastError();
 }
 

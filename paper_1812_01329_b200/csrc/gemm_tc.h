@@ -28,6 +28,7 @@ struct GemmOp {
   const __nv_bfloat16 *B = nullptr;
   int ldb = 0, b_mn = 0;
   GemmEpilogue ep;
+  const int *K_dev = nullptr;  // optional device-resident K (<= K): data-dependent reductions
 };
 
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);

@@ -13,6 +13,8 @@
 #include "host.h"
 #include "../../include/janus_dev.h"
 
+#define TREE_MAX_LEVELS_HOST 130  // tree.h TREE_MAX_LEVELS
+
 namespace jk {
 
 static int arity(int k) {
@@ -339,6 +341,31 @@ int32_t janus_dev_set_probe(janus_graph *g, void *dev_buf) {
   if (!g) return -1;
   g->probe = static_cast<unsigned long long *>(dev_buf);
   return 0;
+}
+
+/* named workspace regions (tests compare device-internal integer results bit-exactly) */
+int32_t janus_dev_workspace_region(const janus_graph *g, const char *name, size_t *offset,
+                                   size_t *bytes) {
+  if (!g || !name || !offset || !bytes) return -1;
+  const std::string n(name);
+  const TreePlan &t = g->tree;
+  const size_t N = (size_t)t.max_N * 4;
+  struct R { const char *k; size_t off, len; } rs[] = {
+      {"tree.height", t.off.height, N},   {"tree.order", t.off.order, N},
+      {"tree.irank", t.off.irank, N},     {"tree.pslot", t.off.pslot, N},
+      {"tree.lvl_off", t.off.lvl_off, (TREE_MAX_LEVELS_HOST + 2) * 4},
+      {"tree.meta", t.off.meta, 16},      {"status", g->kind == "treelstm" ? t.off.status : g->lm.off.status, sizeof(DevStatus)},
+      {"tree.dh_node", t.off.dh_node, (size_t)t.max_N * t.H * 4},
+      {"tree.dc_node", t.off.dc_node, (size_t)t.max_N * t.H * 4},
+      {"tree.root_h", t.off.root_h, (size_t)t.B * t.H * 4},
+  };
+  for (const auto &r : rs)
+    if (n == r.k && (g->kind == "treelstm" || n == "status")) {
+      *offset = r.off;
+      *bytes = r.len;
+      return 0;
+    }
+  return -1;
 }
 
 /* per-phase device timing */

@@ -32,6 +32,7 @@ cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cu
 __global__ void guards_kernel(GuardList gl, DevStatus *st) {
   const GuardDesc g = gl.g[blockIdx.x];
   const unsigned long long mask = (1ull << IDX_BITS) - 1;
+  if (g.kind == G_TREE) return;  // evaluated by tree_guard_kernel
   if (g.kind == G_FORCED) {
     if (threadIdx.x == 0) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | mask);
     return;
@@ -379,7 +380,9 @@ __global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, De
       long long obs = -1;
       if (idx != (1ull << IDX_BITS) - 1)
         for (int k = 0; k < gl.n; ++k)
-          if (gl.g[k].id == id && gl.g[k].kind != G_FORCED) obs = gl.g[k].data[idx];
+          if (gl.g[k].id == id && gl.g[k].kind != G_FORCED)
+            obs = (gl.g[k].kind == G_TREE && (long long)idx >= gl.g[k].n)
+                      ? gl.g[k].data2[idx - gl.g[k].n] : gl.g[k].data[idx];
       st->observed = obs;
     } else if (st->runtime_err) {
       st->status = 4;  // JANUS_ERR_RUNTIME
@@ -485,12 +488,26 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
     } break;
     case C_DENSE_IL: {
       const long long n = (long long)sg.rows * sg.cols;
+      const int ng = sg.ng ? sg.ng : 4;
       for (long long e = tid; e < n; e += stride) {
         const int rc = (int)(e / sg.cols), k = (int)(e - (long long)rc * sg.cols);
-        const int ri = 4 * (rc % sg.H) + rc / sg.H;
+        const int ri = ng * (rc % sg.H) + rc / sg.H;
         sg.dst[e] -= sg.lr * sg.grad[(size_t)ri * sg.ldg + k];
       }
     } break;
+    case C_TREE_BIAS:  // b blocks (i, f, o, u): internal gates (i, f_l, f_r, o, u), leaf (i, o, u)
+      for (long long e = tid; e < 4LL * sg.H; e += stride) {
+        const int q = (int)(e / sg.H), u = (int)(e % sg.H);
+        const float *gi = sg.grad + (size_t)5 * u * sg.ldg + sg.col;
+        const float *gl = sg.grad2 + (size_t)3 * u * sg.ldg2 + sg.col2;
+        float g = 0.f;
+        if (q == 0) g = gi[0] + gl[0];
+        else if (q == 1) g = gi[(size_t)sg.ldg] + gi[2 * (size_t)sg.ldg];
+        else if (q == 2) g = gi[3 * (size_t)sg.ldg] + gl[(size_t)sg.ldg2];
+        else g = gi[4 * (size_t)sg.ldg] + gl[2 * (size_t)sg.ldg2];
+        sg.dst[e] -= sg.lr * g;
+      }
+      break;
     case C_BIAS_COL:
       for (long long e = tid; e < sg.rows; e += stride)
         sg.dst[e] -= sg.lr * sg.grad[(size_t)e * sg.ldg + sg.col];

@@ -25,13 +25,15 @@ constexpr unsigned long long KEY_PASS = ~0ull;
 constexpr int IDX_BITS = 40;
 
 // A RUNTIME assumption evaluated on the device (AssertOp).
-enum GuardKind { G_ALL_EQ = 0, G_FIRST_EQ = 1, G_RANGE = 2, G_FORCED = 3 };
+enum GuardKind { G_ALL_EQ = 0, G_FIRST_EQ = 1, G_RANGE = 2, G_FORCED = 3,
+                 G_TREE = 4 /* evaluated by the forest guard; listed for the observed lookup */ };
 struct GuardDesc {
   int kind;
   unsigned int id;
   const int *data;
   long long n;
   long long value, lo, hi;
+  const int *data2;  // G_TREE: element i >= n is data2[i - n]
 };
 constexpr int MAX_GUARDS = 8;
 struct GuardList {
@@ -92,7 +94,7 @@ cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_w
 
 // commit segments (P:164 all-or-nothing, P:282 deferred update)
 enum CommitKind { C_DENSE = 0, C_DENSE_IL = 1, C_BIAS_COL = 2, C_BIAS_COL_IL = 3, C_COPY = 4,
-                  C_TAG = 5, C_SPARSE_ROWS = 6 };
+                  C_TAG = 5, C_SPARSE_ROWS = 6, C_TREE_BIAS = 7 };
 struct CommitSeg {
   int kind;
   float *dst;          // master (fp32) or state destination
@@ -106,6 +108,9 @@ struct CommitSeg {
   const int *nrows;    // C_SPARSE_ROWS: device count of rows
   int *idst;           // C_TAG
   int ival;
+  int ng;              // C_DENSE_IL: gates per unit (0 = 4)
+  const float *grad2;  // C_TREE_BIAS: leaf wgrad (bias column col2, pitch ldg2)
+  int ldg2, col2;
 };
 constexpr int MAX_COMMIT = 24;
 struct CommitList {

@@ -1,0 +1,659 @@
+// tree.cu — level-batched TreeLSTM training step (config C3).
+//
+// The TreeNN program recurses through InvokeOp (P:316 fn6: "recursion-based
+// implementation"). Under the TREE_BINARY assumption (every node a leaf or a binary node whose
+// children precede it in the same tree) the recursion is flattened into levels (reading Q8:
+// level = height, stable by node id) — exactly the parallelism +PARL exploits "in multiple
+// independent tree nodes" — and runs on the device:
+//   guard (AssertOp over the forest) -> schedule (stable counting sort by height) ->
+//   forward: one cooperative launch walks leaf level + internal levels with grid barriers; each
+//            level is a tcgen05 GEMM (rows = the level's nodes, gate-interleaved weight tiles) with
+//            the cell update fused in the TMEM epilogue, scattering h / c into the parent's
+//            staging row (each child has exactly one parent: no atomics) ->
+//   root classifier + xent -> backward: one cooperative launch walks the levels top-down.
+// Gate-interleaved rows: U_il row 5u+g = U row g*H+u (g = i, f_l, f_r, o, u); W_leaf_il row 3u+g
+// = W_leaf row g*H+u (g = i, o, u). Bias b has blocks (i, f, o, u) (reading Q5).
+#include "common.cuh"
+#include "gemm_tc.h"
+#include "tree.h"
+
+namespace jk {
+
+constexpr int TT = 192;          // threads: warps 0-3 epilogue, warp 4 TMA, warp 5 MMA
+constexpr int T_STAGES = 6;
+constexpr int T_ASTAGE = 128 * 128;  // A chunk: 128 rows x 64 bf16
+constexpr int T_BSTAGE = 80 * 128;   // B chunk: up to 80 rows x 64 bf16
+
+JN_DEV float sig_t(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+JN_DEV float tanh_t(float x) {
+  const float e = __expf(-2.f * fabsf(x));
+  return copysignf(__fdividef(1.f - e, 1.f + e), x);
+}
+
+JN_DEV void grid_sync(unsigned int *ctr, unsigned int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+  fence_proxy_async_global();
+}
+
+// =============================================================================== guard
+// TREE_BINARY (janus.h): elements 0..N-1 are nodes, N..N+B the tree_off entries; the minimum
+// failing element is reported (observed = off[t] for offsets, kind[n] for nodes).
+__global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d, TreeSched s,
+                                                          unsigned id, long long V, long long maxn,
+                                                          DevStatus *st) {
+  __shared__ int s_badoff;
+  __shared__ int s_badnode;
+  const int N = d.N, B = d.B;
+  if (threadIdx.x == 0) { s_badoff = 0x7fffffff; s_badnode = 0x7fffffff; }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= B; i += blockDim.x) {
+    bool ok;
+    if (i == 0) ok = t.off[0] == 0;
+    else {
+      const int sz = t.off[i] - t.off[i - 1];
+      ok = sz >= 1 && sz <= maxn && (i < B || t.off[B] == N);
+    }
+    if (!ok) atomicMin(&s_badoff, i);
+  }
+  __syncthreads();
+  const unsigned long long mask = (1ull << IDX_BITS) - 1;
+  if (s_badoff != 0x7fffffff) {
+    if (threadIdx.x == 0)
+      atomicMin(&st->key, ((unsigned long long)id << IDX_BITS) | (unsigned long long)(N + s_badoff));
+    return;
+  }
+  for (int n = threadIdx.x; n < N; n += blockDim.x) s.pcount[n] = 0;
+  __syncthreads();
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    int lo_t = 0, hi_t = B - 1;  // tree containing n: largest t with off[t] <= n
+    while (lo_t < hi_t) {
+      const int mid = (lo_t + hi_t + 1) >> 1;
+      if (t.off[mid] <= n) lo_t = mid; else hi_t = mid - 1;
+    }
+    s.tree_of[n] = lo_t;
+    const int lo = t.off[lo_t];
+    const int k = t.kind[n];
+    bool bad = false;
+    if (k == 0) bad = !(t.word[n] >= 0 && t.word[n] < V);
+    else if (k == 1) {
+      const int l = t.left[n], r = t.right[n];
+      if (l >= lo && l < n && r >= lo && r < n && l != r) {
+        atomicAdd(&s.pcount[l], 1);
+        atomicAdd(&s.pcount[r], 1);
+      } else bad = true;
+    } else bad = true;
+    if (bad) atomicMin(&s_badnode, n);
+  }
+  __syncthreads();
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    const bool root = n == t.off[s.tree_of[n] + 1] - 1;
+    if (root ? s.pcount[n] != 0 : s.pcount[n] != 1) atomicMin(&s_badnode, n);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_badnode != 0x7fffffff)
+    atomicMin(&st->key, ((unsigned long long)id << IDX_BITS) | (unsigned long long)s_badnode);
+  (void)mask;
+}
+
+cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
+                              long long V, long long max_nodes, DevStatus *st, cudaStream_t str) {
+  tree_guard_kernel<<<1, 1024, 0, str>>>(t, d, s, id, V, max_nodes, st);
+  return cudaGetLastError();
+}
+
+// =============================================================================== schedule
+// Single block. Heights by a per-tree scan in post-order (children precede parents); then a
+// stable counting sort by height in node-id order (warp match + per-level prefix over warps).
+__global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
+                                                             const DevStatus *st) {
+  __shared__ int hist[TREE_MAX_LEVELS + 1];
+  __shared__ int running[TREE_MAX_LEVELS + 1];
+  __shared__ unsigned short wcnt[32][TREE_MAX_LEVELS];
+  __shared__ int s_L;
+  const int N = d.N, B = d.B;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (st->key != KEY_PASS) {  // the forest failed its AssertOp: nothing downstream may run
+    if (tid == 0) { s.meta[0] = 0; s.meta[1] = 0; s.meta[2] = 0; s.meta[3] = 0; }
+    return;
+  }
+  for (int i = tid; i <= TREE_MAX_LEVELS; i += blockDim.x) { hist[i] = 0; running[i] = 0; }
+  if (tid == 0) s_L = 1;
+  __syncthreads();
+  // heights (robust to malformed input: the guard has already decided the commit)
+  for (int tr = tid; tr < B; tr += blockDim.x) {
+    const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
+    for (int n = lo; n < hi; ++n) {
+      int h = 0;
+      s.tree_of[n] = tr;
+      if (t.kind[n] == 1) {
+        const int l = t.left[n], r = t.right[n];
+        const int hl = (l >= lo && l < n) ? s.height[l] : 0;
+        const int hr = (r >= lo && r < n) ? s.height[r] : 0;
+        h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
+      }
+      s.height[n] = h;
+      s.pslot[n] = -1;
+    }
+  }
+  __syncthreads();
+  for (int n = tid; n < N; n += blockDim.x) {
+    atomicAdd(&hist[s.height[n]], 1);
+    atomicMax(&s_L, s.height[n] + 1);
+  }
+  __syncthreads();
+  const int L = s_L;
+  if (tid == 0) {
+    int acc = 0;
+    for (int l = 0; l <= L; ++l) {
+      s.lvl_off[l] = acc;
+      if (l < L) acc += hist[l];
+    }
+    s.meta[0] = L;
+    s.meta[1] = N;
+    s.meta[2] = hist[0];
+    s.meta[3] = N - hist[0];
+  }
+  __syncthreads();
+  // stable placement, chunk by chunk of 1024 ids
+  for (int c0 = 0; c0 < N; c0 += blockDim.x) {
+    for (int i = tid; i < 32 * TREE_MAX_LEVELS; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const int n = c0 + tid;
+    const bool live = n < N;
+    const int h = live ? s.height[n] : TREE_MAX_LEVELS - 1;
+    const unsigned same = __match_any_sync(0xffffffff, live ? h : -1 - lane);
+    const int rank_w = __popc(same & ((1u << lane) - 1));
+    if (live && rank_w == 0) wcnt[warp][h] = (unsigned short)__popc(same);
+    __syncthreads();
+    // per level: exclusive prefix over warps (in place), then advance the running count
+    for (int l = tid; l < L; l += blockDim.x) {
+      int acc = running[l];
+      for (int w = 0; w < 32; ++w) {
+        const int c = wcnt[w][l];
+        wcnt[w][l] = (unsigned short)(acc - running[l]);
+        acc += c;
+      }
+      hist[l] = running[l];  // base of this chunk for level l
+      running[l] = acc;
+    }
+    __syncthreads();
+    if (live) {
+      const int pos = s.lvl_off[h] + hist[h] + wcnt[warp][h] + rank_w;
+      s.order[pos] = n;
+      s.irank[n] = h > 0 ? pos - s.lvl_off[1] : -1;
+    }
+    __syncthreads();
+  }
+  // parent slots
+  for (int n = tid; n < N; n += blockDim.x) {
+    if (t.kind[n] == 1 && s.height[n] > 0) {
+      const int l = t.left[n], r = t.right[n];
+      if (l >= 0 && l < N) s.pslot[l] = (s.irank[n] << 1) | 0;
+      if (r >= 0 && r < N) s.pslot[r] = (s.irank[n] << 1) | 1;
+    }
+  }
+  (void)st;
+}
+
+cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
+                                 const DevStatus *st, cudaStream_t str) {
+  tree_schedule_kernel<<<1, 1024, 0, str>>>(t, d, s, st);
+  return cudaGetLastError();
+}
+
+// =============================================================================== GEMM tiles
+// Persistent tile loop shared by the forward and backward kernels: rows [row0, row0 + M) of the
+// A map times B rows [0, NTOT) in tiles of 128 x NT; the epilogue functor receives (row index,
+// tile column base, z[NT]) for rows < M.
+struct Ring {
+  uint64_t *full, *empty, *tfull;
+  uint8_t *sA, *sB;
+  uint32_t tmem;
+  int q;      // chunk counter (both producer and MMA advance it identically)
+  int tiles;  // tiles processed by this CTA (tfull phase)
+};
+
+template <int NT, typename Epi>
+JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, int row0, int M,
+                      int NTOT, int K, Epi epi) {
+  const int warp = threadIdx.x >> 5;
+  const int ntile_n = (NTOT + NT - 1) / NT;
+  const int tiles = ((M + 127) / 128) * ntile_n;
+  const int nk = (K + 63) / 64;
+  constexpr uint32_t idesc = umma_idesc_bf16(128, NT, 0, 0);
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int m = tile / ntile_n, nn = tile % ntile_n;
+    if (warp == 4) {
+      if ((threadIdx.x & 31) == 0)
+        for (int kc = 0; kc < nk; ++kc) {
+          const int q = rg.q + kc, s = q % T_STAGES, r = q / T_STAGES;
+          if (r > 0) mbar_wait(&rg.empty[s], (r - 1) & 1);
+          mbar_expect_tx(&rg.full[s], T_ASTAGE + NT * 128);
+          tma_load_2d(rg.sA + s * T_ASTAGE, tmA, &rg.full[s], kc * 64, row0 + m * 128);
+          tma_load_2d(rg.sB + s * T_BSTAGE, tmB, &rg.full[s], kc * 64, nn * NT);
+        }
+      __syncwarp();
+    } else if (warp == 5) {
+      if ((threadIdx.x & 31) == 0) {
+        for (int kc = 0; kc < nk; ++kc) {
+          const int q = rg.q + kc, s = q % T_STAGES, r = q / T_STAGES;
+          mbar_wait(&rg.full[s], r & 1);
+          tc_fence_after();
+          const uint32_t a = smem_u32(rg.sA + s * T_ASTAGE), b = smem_u32(rg.sB + s * T_BSTAGE);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_bf16(rg.tmem, umma_desc_sw128(a + k * 32, 16, 1024),
+                      umma_desc_sw128(b + k * 32, 16, 1024), idesc, (kc | k) != 0);
+          umma_commit(&rg.empty[s]);
+        }
+        umma_commit(rg.tfull);
+      }
+      __syncwarp();
+    } else {
+      mbar_wait(rg.tfull, rg.tiles & 1);
+      __syncwarp();
+      tc_fence_after();
+      float z[NT];
+      const uint32_t ta = rg.tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+      for (int c = 0; c + 32 <= NT; c += 32) {
+        float v[32];
+        tmem_ld32(ta + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) z[c + i] = v[i];
+      }
+      if (NT % 32) {
+        float v[16];
+        tmem_ld16(ta + (NT / 32) * 32, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z[(NT / 32) * 32 + i] = v[i];
+      }
+      const int row = m * 128 + threadIdx.x;
+      if (row < M) epi(row, nn * NT, z);
+    }
+    rg.q += nk;
+    rg.tiles += 1;
+    tc_fence_before();
+    __syncthreads();  // TMEM accumulator free for the next tile
+    tc_fence_after();
+  }
+}
+
+// =============================================================================== forward
+struct TreeFwdMaps {
+  CUtensorMap x_leaf, w_leaf, stage_h, u;
+};
+
+__global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__ TreeFwdMaps mp,
+                                                         TreeBufs t, TreeDims d, TreeSched s,
+                                                         const DevStatus *st) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  Ring rg;
+  rg.sA = base;
+  rg.sB = base + T_STAGES * T_ASTAGE;
+  rg.full = reinterpret_cast<uint64_t *>(rg.sB + T_STAGES * T_BSTAGE);
+  rg.empty = rg.full + T_STAGES;
+  rg.tfull = rg.empty + T_STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rg.tfull + 1);
+  const int warp = threadIdx.x >> 5;
+  const int H = d.H, E = d.E;
+  if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
+  if (threadIdx.x == 128) {
+    for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
+    mbar_init(rg.tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  rg.tmem = *tmem_slot;
+  rg.q = 0;
+  rg.tiles = 0;
+  const int L = s.meta[0], n0 = s.meta[2], nint = s.meta[3];
+  unsigned int ep = 0;
+  // ---- phase 0: leaf inputs in level-0 order (R1: rb(E[word])), ones columns for bias grads
+  {
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    for (long long e = gt; e < (long long)n0 * d.Ep; e += gs) {
+      const int pos = (int)(e / d.Ep), k = (int)(e % d.Ep);
+      int w = t.word[s.order[pos]];
+      w = (w >= 0 && w < d.V) ? w : 0;
+      const float v = k < E ? t.E[(size_t)w * E + k] : (k == E ? 1.f : 0.f);
+      t.x_leaf[(size_t)pos * d.Ep + k] = __float2bfloat16_rn(v);
+    }
+    for (int i = gt; i < nint; i += gs) t.stage_h[(size_t)i * d.P2 + 2 * H] = __float2bfloat16_rn(1.f);
+  }
+  fence_proxy_async_global();
+  grid_sync(t.barrier, ++ep * gridDim.x);
+  const float *b = t.b;
+  // ---- level 0: leaves. z = x W_leaf^T; i, o = sigmoid, u = tanh; c = i u; h = o tanh(c)
+  tile_loop<48>(rg, &mp.x_leaf, &mp.w_leaf, 0, n0, 3 * H, E, [&](int pos, int col0, float *z) {
+    const int n = s.order[pos];
+    const int ps = s.pslot[n];
+#pragma unroll
+    for (int uu = 0; uu < 16; ++uu) {
+      const int u = col0 / 3 + uu;
+      if (u >= H) break;
+      const float ig = sig_t(z[3 * uu] + b[u]);
+      const float og = sig_t(z[3 * uu + 1] + b[2 * H + u]);
+      const float ug = tanh_t(z[3 * uu + 2] + b[3 * H + u]);
+      const float c = ig * ug, h = og * tanh_t(c);
+      float *gl = t.gates_leaf + (size_t)pos * 3 * H + 3 * u;
+      gl[0] = ig; gl[1] = og; gl[2] = ug;
+      t.c_leaf[(size_t)pos * H + u] = c;
+      if (ps >= 0) {
+        const int pi = ps >> 1, side = ps & 1;
+        t.stage_h[(size_t)pi * d.P2 + side * H + u] = __float2bfloat16_rn(h);
+        t.stage_c[(size_t)pi * 2 * H + side * H + u] = c;
+      } else {
+        t.root_h[(size_t)s.tree_of[n] * H + u] = h;
+      }
+    }
+  });
+  fence_proxy_async_global();
+  grid_sync(t.barrier, ++ep * gridDim.x);
+  // ---- internal levels: z = [h_l; h_r] U^T; c = i u + f_l c_l + f_r c_r; h = o tanh(c)
+  for (int l = 1; l < L; ++l) {
+    const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
+    tile_loop<80>(rg, &mp.stage_h, &mp.u, r0, cnt, 5 * H, 2 * H, [&](int row, int col0, float *z) {
+      const int ir = r0 + row;
+      const int n = s.order[p0 + row];
+      const int ps = s.pslot[n];
+      const float *sc = t.stage_c + (size_t)ir * 2 * H;
+#pragma unroll
+      for (int uu = 0; uu < 16; ++uu) {
+        const int u = col0 / 5 + uu;
+        if (u >= H) break;
+        const float ig = sig_t(z[5 * uu] + b[u]);
+        const float fl = sig_t(z[5 * uu + 1] + b[H + u]);
+        const float fr = sig_t(z[5 * uu + 2] + b[H + u]);
+        const float og = sig_t(z[5 * uu + 3] + b[2 * H + u]);
+        const float ug = tanh_t(z[5 * uu + 4] + b[3 * H + u]);
+        const float c = ig * ug + fl * sc[u] + fr * sc[H + u];
+        const float h = og * tanh_t(c);
+        float *gi = t.gates_int + (size_t)ir * 5 * H + 5 * u;
+        gi[0] = ig; gi[1] = fl; gi[2] = fr; gi[3] = og; gi[4] = ug;
+        t.c_int[(size_t)ir * H + u] = c;
+        if (ps >= 0) {
+          const int pi = ps >> 1, side = ps & 1;
+          t.stage_h[(size_t)pi * d.P2 + side * H + u] = __float2bfloat16_rn(h);
+          t.stage_c[(size_t)pi * 2 * H + side * H + u] = c;
+        } else {
+          t.root_h[(size_t)s.tree_of[n] * H + u] = h;
+        }
+      }
+    });
+    fence_proxy_async_global();
+    grid_sync(t.barrier, ++ep * gridDim.x);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc(rg.tmem, 128);
+  (void)st;
+}
+
+static int tree_smem() { return 1024 + T_STAGES * (T_ASTAGE + T_BSTAGE) + 256; }
+
+static cudaError_t coop(const void *fn, int grid, int smem, void **args, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(TT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
+                            const __nv_bfloat16 *Wl_il, const __nv_bfloat16 *U_il, int grid,
+                            const DevStatus *st, cudaStream_t str) {
+  TreeFwdMaps mp;
+  bool ok = make_tmap_bf16(&mp.x_leaf, t.x_leaf, d.E, d.N, d.Ep, 128);
+  ok = ok && make_tmap_bf16(&mp.w_leaf, Wl_il, d.E, 3ull * d.H, d.Ep, 48);
+  ok = ok && make_tmap_bf16(&mp.stage_h, t.stage_h, 2ull * d.H, d.N, d.P2, 128);
+  ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
+  if (!ok) return cudaErrorInvalidValue;
+  const int smem = tree_smem();
+  cudaError_t e = cudaFuncSetAttribute(tree_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  TreeBufs tt = t;
+  TreeDims dd = d;
+  TreeSched ss = s;
+  void *args[] = {&mp, &tt, &dd, &ss, (void *)&st};
+  return coop((const void *)tree_fwd_kernel, grid, smem, args, str);
+}
+
+// =============================================================================== root classifier
+// y = rb(h_root) rb(W_c)^T + b_c; loss = mean over trees of xent(y, label) (reading Q6);
+// dy = (softmax - onehot) / B; dW_c = sum rb(dy)^T rb(h); db_c = sum rb(dy); dh_root = rb(dy) rb(W_c).
+__global__ void tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus *st) {
+  const int B = d.B, H = d.H, C = d.C;
+  extern __shared__ float sh[];
+  float *dyr = sh;  // [B][C] rounded dy
+  if (st->key != KEY_PASS) {
+    for (int tr = threadIdx.x; tr < B; tr += blockDim.x) t.rowloss[tr] = 0.f;
+    return;
+  }
+  for (int tr = threadIdx.x; tr < B; tr += blockDim.x) {
+    float y[8];
+    float m = -INFINITY;
+    for (int c = 0; c < C; ++c) {
+      float acc = t.bc[c];
+      for (int k = 0; k < H; ++k)
+        acc += bf16_round(t.root_h[(size_t)tr * H + k]) * bf16_round(t.Wc[(size_t)c * H + k]);
+      y[c] = acc;
+      m = fmaxf(m, acc);
+    }
+    float sum = 0.f;
+    for (int c = 0; c < C; ++c) sum += expf(y[c] - m);
+    const float lse = m + logf(sum);
+    int lab = t.label[tr];
+    if (lab < 0 || lab >= C) {
+      atomicOr(reinterpret_cast<unsigned int *>(&st->runtime_err), 2u);
+      lab = 0;
+    }
+    t.rowloss[tr] = (lse - y[lab]) / B;
+    for (int c = 0; c < C; ++c)
+      dyr[tr * C + c] = bf16_round((expf(y[c] - lse) - (c == lab ? 1.f : 0.f)) / B);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < C * H; e += blockDim.x) {
+    const int c = e / H, k = e % H;
+    float acc = 0.f;
+    for (int tr = 0; tr < B; ++tr) acc += dyr[tr * C + c] * bf16_round(t.root_h[(size_t)tr * H + k]);
+    t.gWc[e] = acc;
+  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float acc = 0.f;
+    for (int tr = 0; tr < B; ++tr) acc += dyr[tr * C + c];
+    t.gbc[c] = acc;
+  }
+  // dh of each root node (dc of a root = 0)
+  for (int e = threadIdx.x; e < B * H; e += blockDim.x) {
+    const int tr = e / H, k = e % H;
+    int root = t.off[tr + 1] - 1;
+    if (root < 0 || root >= d.N) continue;
+    float acc = 0.f;
+    for (int c = 0; c < C; ++c) acc += dyr[tr * C + c] * bf16_round(t.Wc[(size_t)c * H + k]);
+    t.dh_node[(size_t)root * H + k] = acc;
+    t.dc_node[(size_t)root * H + k] = 0.f;
+  }
+  (void)s;
+}
+
+cudaError_t launch_tree_root(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
+                             DevStatus *st, cudaStream_t str) {
+  if (d.C > 8) return cudaErrorInvalidValue;
+  tree_root_kernel<<<1, 1024, d.B * d.C * 4, str>>>(t, d, s, st);
+  return cudaGetLastError();
+}
+
+// =============================================================================== backward
+struct TreeBwdMaps {
+  CUtensorMap dz, ut;
+};
+
+__global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__ TreeBwdMaps mp,
+                                                         TreeBufs t, TreeDims d, TreeSched s,
+                                                         const DevStatus *st) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  Ring rg;
+  rg.sA = base;
+  rg.sB = base + T_STAGES * T_ASTAGE;
+  rg.full = reinterpret_cast<uint64_t *>(rg.sB + T_STAGES * T_BSTAGE);
+  rg.empty = rg.full + T_STAGES;
+  rg.tfull = rg.empty + T_STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rg.tfull + 1);
+  const int warp = threadIdx.x >> 5;
+  const int H = d.H;
+  if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
+  if (threadIdx.x == 128) {
+    for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
+    mbar_init(rg.tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  rg.tmem = *tmem_slot;
+  rg.q = 0;
+  rg.tiles = 0;
+  const int L = s.meta[0], n0 = s.meta[2], nint = s.meta[3];
+  unsigned int ep = 0;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int l = L - 1; l >= 1; --l) {
+    const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
+    // (a) cell backward of this level's nodes: their dh / dc were written by the parents
+    for (long long e = gt; e < (long long)cnt * H; e += gs) {
+      const int row = (int)(e / H), u = (int)(e % H);
+      const int ir = r0 + row, n = s.order[p0 + row];
+      const float dh = t.dh_node[(size_t)n * H + u];
+      const float *g = t.gates_int + (size_t)ir * 5 * H + 5 * u;
+      const float ig = g[0], fl = g[1], fr = g[2], og = g[3], ug = g[4];
+      const float tc = tanh_t(t.c_int[(size_t)ir * H + u]);
+      const float dout = dh * tc;
+      const float dc = t.dc_node[(size_t)n * H + u] + dh * og * (1.f - tc * tc);
+      const float cl = t.stage_c[(size_t)ir * 2 * H + u], cr = t.stage_c[(size_t)ir * 2 * H + H + u];
+      __nv_bfloat16 *dz = t.DZ_int + (size_t)ir * d.P5 + 5 * u;
+      dz[0] = __float2bfloat16_rn(dc * ug * ig * (1.f - ig));
+      dz[1] = __float2bfloat16_rn(dc * cl * fl * (1.f - fl));
+      dz[2] = __float2bfloat16_rn(dc * cr * fr * (1.f - fr));
+      dz[3] = __float2bfloat16_rn(dout * og * (1.f - og));
+      dz[4] = __float2bfloat16_rn(dc * ig * (1.f - ug * ug));
+      const int lc = t.left[n], rc = t.right[n];
+      t.dc_node[(size_t)lc * H + u] = dc * fl;
+      t.dc_node[(size_t)rc * H + u] = dc * fr;
+    }
+    fence_proxy_async_global();
+    grid_sync(t.barrier, ++ep * gridDim.x);
+    // (b) [dh_l ; dh_r] = rb(dz) U, scattered to the two children (each child has one parent)
+    tile_loop<64>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, 5 * H, [&](int row, int col0, float *z) {
+      const int n = s.order[p0 + row];
+      const int lc = t.left[n], rc = t.right[n];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int k = col0 + j;
+        if (k >= 2 * H) break;
+        if (k < H) t.dh_node[(size_t)lc * H + k] = z[j];
+        else t.dh_node[(size_t)rc * H + (k - H)] = z[j];
+      }
+    });
+    grid_sync(t.barrier, ++ep * gridDim.x);
+  }
+  // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]
+  for (long long e = gt; e < (long long)n0 * H; e += gs) {
+    const int pos = (int)(e / H), u = (int)(e % H);
+    const int n = s.order[pos];
+    const float dh = t.dh_node[(size_t)n * H + u];
+    const float *g = t.gates_leaf + (size_t)pos * 3 * H + 3 * u;
+    const float ig = g[0], og = g[1], ug = g[2];
+    const float tc = tanh_t(t.c_leaf[(size_t)pos * H + u]);
+    const float dc = t.dc_node[(size_t)n * H + u] + dh * og * (1.f - tc * tc);
+    __nv_bfloat16 *dz = t.DZ_leaf + (size_t)pos * d.P3 + 3 * u;
+    dz[0] = __float2bfloat16_rn(dc * ug * ig * (1.f - ig));
+    dz[1] = __float2bfloat16_rn(dh * tc * og * (1.f - og));
+    dz[2] = __float2bfloat16_rn(dc * ig * (1.f - ug * ug));
+  }
+  // zero the dz rows of the last partial 64-row K chunk of the wgrad GEMMs
+  for (long long e = gt; e < (long long)(((nint + 63) & ~63) - nint) * d.P5; e += gs)
+    t.DZ_int[(size_t)nint * d.P5 + e] = __float2bfloat16_rn(0.f);
+  for (long long e = gt; e < (long long)(((n0 + 63) & ~63) - n0) * d.P3; e += gs)
+    t.DZ_leaf[(size_t)n0 * d.P3 + e] = __float2bfloat16_rn(0.f);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc(rg.tmem, 128);
+  (void)st;
+}
+
+cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
+                            const __nv_bfloat16 *UT_il, int grid, const DevStatus *st,
+                            cudaStream_t str) {
+  TreeBwdMaps mp;
+  bool ok = make_tmap_bf16(&mp.dz, t.DZ_int, 5ull * d.H, d.N, d.P5, 128);
+  ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
+  if (!ok) return cudaErrorInvalidValue;
+  const int smem = tree_smem();
+  cudaError_t e = cudaFuncSetAttribute(tree_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  TreeBufs tt = t;
+  TreeDims dd = d;
+  TreeSched ss = s;
+  void *args[] = {&mp, &tt, &dd, &ss, (void *)&st};
+  return coop((const void *)tree_bwd_kernel, grid, smem, args, str);
+}
+
+// =============================================================================== casts
+__global__ void cast_il_kernel(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld) {
+  const long long n = (long long)ng * H * ld;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int ri = (int)(e / ld), k = (int)(e % ld);
+    const int rc = (ri % ng) * H + ri / ng;
+    dst[e] = __float2bfloat16_rn(k < cols ? src[(size_t)rc * cols + k] : 0.f);
+  }
+}
+cudaError_t launch_cast_il(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld,
+                           cudaStream_t s) {
+  cast_il_kernel<<<4 * 148, 256, 0, s>>>(src, H, ng, cols, dst, ld);
+  return cudaGetLastError();
+}
+// dst[k][ri] = rb(src[rc][k]),  ri = ng*u + g <-> rc = g*H + u
+__global__ void cast_il_T_kernel(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld) {
+  __shared__ float tile[32][33];
+  const int ri0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int R = ng * H;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int ri = ri0 + i, k = k0 + threadIdx.x;
+    tile[i][threadIdx.x] = (ri < R && k < cols) ? src[(size_t)((ri % ng) * H + ri / ng) * cols + k] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int k = k0 + i, ri = ri0 + threadIdx.x;
+    if (k < cols && ri < ld) dst[(size_t)k * ld + ri] = __float2bfloat16_rn(ri < R ? tile[threadIdx.x][i] : 0.f);
+  }
+}
+cudaError_t launch_cast_il_T(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld,
+                             cudaStream_t s) {
+  dim3 grid((ld + 31) / 32, (cols + 31) / 32);
+  cast_il_T_kernel<<<grid, dim3(32, 8), 0, s>>>(src, H, ng, cols, dst, ld);
+  return cudaGetLastError();
+}
+
+}  // namespace jk

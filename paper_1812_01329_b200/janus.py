@@ -281,6 +281,20 @@ def nccl_unique_id_bcast(rank, world):
     return broadcast_bytes(nccl_unique_id() if rank == 0 else None, rank)
 
 
+lib.janus_dev_workspace_region.restype = C.c_int32
+lib.janus_dev_workspace_region.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_size_t),
+                                           C.POINTER(C.c_size_t)]
+
+
+def dev_workspace_region(graph, workspace, name, dtype=np.int32):
+    """Copy a named workspace region (see janus_dev.h) to a numpy array."""
+    off, n = C.c_size_t(), C.c_size_t()
+    if lib.janus_dev_workspace_region(graph.h, name.encode(), C.byref(off), C.byref(n)) != 0:
+        raise KeyError(name)
+    raw = workspace[off.value:off.value + n.value].cpu().numpy()
+    return raw.view(dtype)
+
+
 def dev_profile(graph, enable):
     lib.janus_dev_profile(graph.h, int(enable))
 
