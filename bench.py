@@ -87,7 +87,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
@@ -151,7 +151,11 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    B, T = 8, 5     # bounded per-step sample: 8 sequences x 5 tokens (sequence-equivalents below)
+    # bounded per-step sample: B=8 sequences x T tokens of the C2 model, T sized (by timing a 1-token
+    # sample) so the whole --steps K --warmup W run takes about two minutes
+    B = 8
+    t1 = oracle_sample(B, 1)
+    T = int(max(1, min(35, 120.0 / max(1, args.steps + args.warmup) / max(t1, 1e-3))))
     for _ in range(args.warmup):
         oracle_sample(B, T)
     times = [oracle_sample(B, T) for _ in range(args.steps)]
@@ -170,15 +174,125 @@ def run_reference(args):
                       "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+# ----------------------------------------------------------------------------- extra measurements
+def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank, ms_step):
+    """TreeLSTM (C3) throughput, the imperative baseline (Table 3 "Imp."), assertion overhead
+    (strip_asserts A/B) and the C5 speculation-failure stress, all on this rank's GPU."""
+    out = {}
+    K = max(3, min(args.steps, 10))
+    B, T = 64, 35
+    prog = c2_program(B)
+    # --- guard overhead: same graph without RUNTIME AssertOps, interleaved A/B
+    g0 = J.Graph(prog, world_size=world, rank=rank, nccl_id=getattr(g, "_nccl_id", None)) if world == 1 else None
+    if g0 is not None:
+        gs = J.Graph(prog, strip_asserts=True)
+        ws_s = gs.new_workspace()
+        st_s = [s.clone() for s in state]
+        loss = torch.zeros(1, device="cuda")
+        ab = {"with": [], "without": []}
+        for rep in range(3):
+            for name, gg, w, s in (("with", g, ws, state), ("without", gs, ws_s, st_s)):
+                for k in range(2):
+                    gg.run(dev_batches[k], s, w, outs=[loss], stream=stream)
+                ab[name].append(timed(lambda k: gg.run(dev_batches[k % len(dev_batches)], s, w, outs=[loss],
+                                                       stream=stream), K) / K)
+        w_ms, wo_ms = statistics.median(ab["with"]), statistics.median(ab["without"])
+        out["guard_overhead"] = {"ms_with_asserts": w_ms, "ms_without": wo_ms, "overhead": w_ms / wo_ms - 1.0,
+                                 "method": "C2, strip_asserts A/B, interleaved, median of 3 x K steps"}
+    # --- imperative per-op executor on the same workload (the paper's "Imp." column)
+    if world == 1:
+        loss = torch.zeros(1, device="cuda")
+        st_i = [s.clone() for s in state]
+        c0 = g.counters()
+        g.run_imperative(dev_batches[0], st_i, ws_i := torch.zeros(g.workspace_bytes, dtype=torch.uint8, device="cuda"),
+                         outs=[loss], stream=stream)
+        c1 = g.counters()
+        KI = 3
+        ms_i = timed(lambda k: g.run_imperative(dev_batches[k % len(dev_batches)], st_i, ws_i, outs=[loss],
+                                                stream=stream), KI) / KI
+        c2 = g.counters()
+        out["imperative"] = {"samples_per_s": B * 1000.0 / ms_i, "ms_per_step": ms_i,
+                             "launches_per_step": (c2["launches"] - c1["launches"]) // KI,
+                             "host_syncs_per_step": (c2["host_syncs"] - c1["host_syncs"]) / KI,
+                             "graph_speedup": ms_i / ms_step}
+        del ws_i
+        # --- C5: 10% of batches violate an assumption and fall back to the imperative path
+        r = gen.rng(gen.SEED_C5)
+        nb = 40
+        viol = r.random(nb) < 0.10
+        viol[0] = True
+        kinds = ["dtype", "shape", "tag", "trip"]
+        st5 = [s.clone() for s in state]
+        tag_slot = prog.slot_index("tag")
+        ws5 = torch.zeros(g.workspace_bytes, dtype=torch.uint8, device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        aborts = {k: [] for k in kinds}
+        fb = {k: [] for k in kinds}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nv = 0
+        for k in range(nb):
+            tok, tgt, ln = dev_batches[k % len(dev_batches)]
+            if viol[k]:
+                kind = kinds[nv % 4]
+                nv += 1
+                if kind == "dtype":
+                    a = [tok.long(), tgt, ln]
+                elif kind == "shape":
+                    a = [tok[:B - 1].contiguous(), tgt[:B - 1].contiguous(), ln[:B - 1].contiguous()]
+                elif kind == "tag":
+                    st5[tag_slot].zero_()
+                    a = [tok, tgt, ln]
+                else:
+                    l2 = ln.clone(); l2[3] = T - 1
+                    a = [tok, tgt, l2]
+                ta = time.perf_counter()
+                s, f = g.run(a, st5, ws5, outs=[loss], stream=stream)
+                aborts[kind].append(1000 * (time.perf_counter() - ta))
+                if s == J.ASSUMPTION_FAILED:   # fallback to the imperative executor (P:160)
+                    fb[kind].append(J.STATUS_NAMES[g.run_imperative(a, st5, ws5, outs=[loss], stream=stream)])
+            else:
+                g.run([tok, tgt, ln], st5, ws5, outs=[loss], stream=stream)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["c5_stress"] = {"batches": nb, "violations": int(viol.sum()),
+                            "blended_samples_per_s": nb * B / dt,
+                            "abort_latency_ms": {k: (statistics.median(v) if v else None) for k, v in aborts.items()},
+                            "fallback_status": fb,
+                            "note": "wall clock incl. the host syncs of the imperative fallbacks"}
+        del ws5
+        # --- C3 TreeLSTM
+        for Bt in (25, 256):
+            tp = pg.treelstm_program(V=20000, E=300, H=300, C=2, B=Bt, lr=0.05)
+            gt = J.Graph(tp)
+            wst = gt.new_workspace()
+            stt = [torch.tensor(x, device="cuda") for x in gen.uniform_params(tp, 1, 0.05)]
+            forests = [[torch.tensor(a, device="cuda") for a in gen.sst_forest(gen.SEED_C3, k, Bt, 20000)]
+                       for k in range(4)]
+            for k in range(3):
+                gt.run(forests[k % 4], stt, wst, stream=stream)
+            ms_t = timed(lambda k: gt.run(forests[k % 4], stt, wst, stream=stream), K) / K
+            J.dev_profile(gt, True)
+            timed(lambda k: gt.run(forests[k % 4], stt, wst, stream=stream), K)
+            ph = J.dev_phase_report(gt)
+            J.dev_profile(gt, False)
+            out[f"treelstm_b{Bt}"] = {"sentences_per_s": Bt * 1000.0 / ms_t, "ms_per_step": ms_t,
+                                      "phases_ms_per_step": {n: round(v[0] / K, 4) for n, v in ph.items()},
+                                      "workload": f"C3 SST-shaped forests, B={Bt}, H=E=300, V=20000, <=64 leaves"}
+            del wst
+    return out
+
+
 # ----------------------------------------------------------------------------- main arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--impl", default="janus", choices=["janus", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip TreeLSTM / imperative / guard / C5 keys")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -292,9 +406,9 @@ def main():
         "paper_context": "JANUS LSTM (PTB, BS 20) 22.06k words/s on 1 TITAN Xp, fp32 (P:363) — other hardware/config",
     }
     out["clocks"] = clk.summary()
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline()
-    elif rank == 0 and not args.no_cpu_baseline:
+    if not args.no_extras:
+        out.update(extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank, ms_step))
+    if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(out))

@@ -309,6 +309,11 @@ struct Interp {
   float *fptr(int vid) { return static_cast<float *>(vals[vid].ptr); }
   int *iptr(int vid) { return static_cast<int *>(vals[vid].ptr); }
 
+  // shape mismatch inside a node: a runtime error (S:109 ShapeMismatch), commits nothing
+  void need(bool ok) {
+    if (!ok) throw Err{JANUS_ERR_RUNTIME, "shape mismatch"};
+  }
+
   // materialise a device float tensor (host scalars become 1-element tensors)
   int as_dev_f(int vid) {
     if (V(vid).kind == V_DEV) return vid;
@@ -334,12 +339,21 @@ struct Interp {
         IVal v;
         v.kind = V_DEV; v.dtype = t.dtype;
         for (int d = 0; d < t.ndim; ++d) v.shape.push_back(t.shape[d]);
-        const int64_t bytes = std::max<int64_t>(1, v.numel()) * 4;
+        const int64_t esz = t.dtype == JANUS_I64 ? 8 : 4;
+        const int64_t bytes = std::max<int64_t>(1, v.numel()) * esz;
         if (is_device_ptr(t.data)) v.ptr = t.data;
         else {
           v.ptr = alloc(bytes);
           if (cudaMemcpyAsync(v.ptr, t.data, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
             throw Err{JANUS_ERR_CUDA, "H2D"};
+        }
+        if (t.dtype == JANUS_I64) {  // an imperative program takes any integer type (no DtypeEq here)
+          void *p32 = alloc(std::max<int64_t>(1, v.numel()) * 4);
+          ck(imp::i64_to_i32(static_cast<int *>(p32), static_cast<const long long *>(v.ptr), v.numel(), st));
+          v.ptr = p32;
+          v.dtype = JANUS_I32;
+        } else if (t.dtype != JANUS_I32 && t.dtype != JANUS_F32) {
+          throw Err{JANUS_ERR_RUNTIME, "argument dtype"};
         }
         return {new_val(v), -2};
       }
@@ -474,6 +488,8 @@ struct Interp {
       }
       case JOP_LINEAR: {
         const IVal &x = V(in[0]), &W = V(in[1]);
+        need(x.shape.size() == 2 && W.shape.size() == 2 && x.shape[1] == W.shape[1] &&
+             V(in[2]).numel() == W.shape[0]);
         const int n = (int)x.shape[0], K = (int)x.shape[1], N = (int)W.shape[0];
         const int r = dev_f({n, N});
         ck(imp::gemm_nt(fptr(r), fptr(in[0]), fptr(in[1]), n, N, K, K, K, N, false, R, R, st));
@@ -484,6 +500,11 @@ struct Interp {
       }
       case JOP_LSTM_CELL: {
         const IVal &x = V(in[0]), &h = V(in[1]);
+        need(x.shape.size() == 2 && h.shape.size() == 2 && V(in[2]).shape == h.shape &&
+             x.shape[0] == h.shape[0] && V(in[6]).numel() == x.shape[0] &&
+             V(in[3]).shape == std::vector<int64_t>{4 * h.shape[1], x.shape[1]} &&
+             V(in[4]).shape == std::vector<int64_t>{4 * h.shape[1], h.shape[1]} &&
+             V(in[5]).numel() == 4 * h.shape[1]);
         const int B = (int)x.shape[0], E = (int)x.shape[1], H = (int)h.shape[1];
         const int Z = dev_f({B, 4 * H});
         ck(imp::gemm_nt(fptr(Z), fptr(in[0]), fptr(in[3]), B, 4 * H, E, E, E, 4 * H, false, R, R, st));
@@ -501,6 +522,8 @@ struct Interp {
       }
       case JOP_TREELSTM_LEAF: {
         const IVal &x = V(in[0]), &W = V(in[1]);
+        need(x.shape.size() == 2 && W.shape.size() == 2 && W.shape[1] == x.shape[1] &&
+             W.shape[0] % 3 == 0 && V(in[2]).numel() == 4 * (W.shape[0] / 3));
         const int n = (int)x.shape[0], E = (int)x.shape[1], H = (int)(W.shape[0] / 3);
         const int Z = dev_f({n, 3 * H}), bb = dev_f({3 * H});
         ck(imp::gemm_nt(fptr(Z), fptr(in[0]), fptr(in[1]), n, 3 * H, E, E, E, 3 * H, false, R, R, st));
@@ -515,6 +538,10 @@ struct Interp {
       }
       case JOP_TREELSTM_CELL: {
         const IVal &hl = V(in[0]);
+        need(hl.shape.size() == 2 && V(in[1]).shape == hl.shape && V(in[2]).shape == hl.shape &&
+             V(in[3]).shape == hl.shape &&
+             V(in[4]).shape == std::vector<int64_t>{5 * hl.shape[1], 2 * hl.shape[1]} &&
+             V(in[5]).numel() == 4 * hl.shape[1]);
         const int n = (int)hl.shape[0], H = (int)hl.shape[1];
         const int Z = dev_f({n, 5 * H}), bb = dev_f({5 * H});
         // z = [h_l ; h_r] U^T: the two halves of U's columns
@@ -535,6 +562,7 @@ struct Interp {
         const IVal &y = V(in[0]);
         const int n = (int)y.shape[0], C = (int)y.shape[1];
         const int tg = as_dev_i(in[1]), mk = as_dev_i(in[2]);
+        need(V(tg).numel() == n && V(mk).numel() == n);
         const int loss = dev_f({}), dy = dev_f({n, C});
         ck(imp::xent(fptr(loss), fptr(dy), fptr(in[0]), iptr(tg), iptr(mk), n, C, err_dev, st));
         vals[loss].rg = y.rg;

@@ -149,6 +149,16 @@ cudaError_t copy_i(int *y, const int *x, int64_t n, cudaStream_t s) {
   copy_i_k<<<blocks_for(n), 256, 0, s>>>(y, x, n);
   return cudaGetLastError();
 }
+__global__ void i64_to_i32_k(int *y, const long long *x, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = x[e];
+    y[e] = (v > 2147483647LL || v < -2147483647LL) ? -1 : (int)v;  // out of range -> invalid id
+  }
+}
+cudaError_t i64_to_i32(int *y, const long long *x, int64_t n, cudaStream_t s) {
+  i64_to_i32_k<<<blocks_for(n), 256, 0, s>>>(y, x, n);
+  return cudaGetLastError();
+}
 __global__ void embedding_k(float *X, const float *E, const int *ids, int n, int V, int Ed, bool r, int *err) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * Ed; e += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(e / Ed), k = (int)(e % Ed);

@@ -26,6 +26,7 @@ cudaError_t axpy(float *y, const float *x, float a, int64_t n, cudaStream_t s); 
 cudaError_t copy(float *y, const float *x, int64_t n, cudaStream_t s);
 cudaError_t round_copy(float *y, const float *x, int64_t n, bool r, cudaStream_t s);   // y = rb(x)
 cudaError_t copy_i(int *y, const int *x, int64_t n, cudaStream_t s);
+cudaError_t i64_to_i32(int *y, const long long *x, int64_t n, cudaStream_t s);
 // rows of E (optionally rounded); out-of-range ids set *err and read row 0
 cudaError_t embedding(float *X, const float *E, const int *ids, int n, int V, int Ed, bool r, int *err,
                       cudaStream_t s);
