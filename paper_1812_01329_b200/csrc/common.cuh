@@ -61,6 +61,17 @@ JN_DEV void tma_load_3d(void *smem_dst, const CUtensorMap *m, uint64_t *bar, int
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// plain bulk copy global -> shared (contiguous bytes, multiple of 16), completes on an mbarrier
+JN_DEV void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// byte offset of 16-B granule g of row r inside a 128-B-swizzled K-major tile (Swizzle<3,4,3>):
+// rows are 128 B, granule index XOR (row mod 8) — the layout TMA SWIZZLE_128B writes
+JN_DEV uint32_t sw128_off(uint32_t r, uint32_t g) { return r * 128u + ((g ^ (r & 7u)) << 4); }
 // generic-proxy writes (other CTAs, made visible by an acquire) -> async-proxy (TMA) reads
 JN_DEV void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");

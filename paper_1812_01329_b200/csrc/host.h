@@ -34,7 +34,7 @@ struct LmPlan {
   struct Off {
     size_t status = 0, barriers = 0, stage_args = 0;
     size_t Wih_b[4], Whh_b[4], WhhT_b[4], bil[4], Wdec_b = 0;
-    size_t X = 0, Hs[4], Cs[4], G[4], DZ[4], dX[4];
+    size_t X = 0, Hs[4], Cs[4], G[4], DZ[4], dX[4], Hsw[4], DZsw[4];
     size_t logits = 0, dy = 0, rowloss = 0, dHtop = 0, hT[4], cT[4];
     size_t gWih[4], gWhh[4], gWdec = 0;
     size_t seg_word = 0, seg_start = 0, seg_grad = 0, nseg = 0, keys = 0;
@@ -119,7 +119,7 @@ struct Graph {
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
   std::string describe;
-  unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (16*T u64)
+  unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*8*T u64)
 };
 
 // host_graph.cpp

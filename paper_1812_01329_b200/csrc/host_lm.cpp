@@ -214,6 +214,8 @@ bool lower_lm(Graph &g, std::string &why) {
       p.off.Cs[l] = take((TB + B) * p.Hp * 4);
       p.off.G[l] = take(TB * G4 * 4);
       p.off.DZ[l] = take(TB * p.Gz * 2);
+      p.off.Hsw[l] = take(rec_hsw_bytes(H, B, T));
+      p.off.DZsw[l] = take(rec_dzsw_bytes(H, B, T));
       p.off.dX[l] = take(TB * Inp * 4);
       p.off.hT[l] = take((size_t)B * H * 4);
       p.off.cT[l] = take((size_t)B * H * 4);
@@ -436,6 +438,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(op, st));
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
+    ra.Hsw = bf(p.off.Hsw[l]);
     ra.G = fp(p.off.G[l]); ra.Hs = bf(p.off.Hs[l]); ra.Cs = fp(p.off.Cs[l]); ra.ldh = Hp;
     ra.h0 = P.h[l]; ra.c0 = P.c[l]; ra.hT = fp(p.off.hT[l]); ra.cT = fp(p.off.cT[l]);
     ra.barrier = bars + 256 * l; ra.fail = nullptr;
@@ -473,8 +476,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     rb.B = B; rb.H = H; rb.T = Tw; rb.T_dev = Tdev; rb.lens = p.while_mode ? P.lens : nullptr;
     rb.G = fp(p.off.G[l]); rb.Cs = fp(p.off.Cs[l]); rb.ldh = Hp;
     rb.dHin = l == L - 1 ? fp(p.off.dHtop) : fp(p.off.dX[l + 1]); rb.ldd = Hp;
+    rb.DZsw = bf(p.off.DZsw[l]);
     rb.DZ = bf(p.off.DZ[l]); rb.ldz = p.Gz; rb.barrier = bars + 256 * (L + l);
-    rb.dbg = (l == 0 && g.probe) ? g.probe + 8 * p.T : nullptr;
+    rb.dbg = (l == 0 && g.probe) ? g.probe + (size_t)128 * 8 * p.T : nullptr;
     LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(rb, bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
     const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
     GemmOp a;  // dW_hh = dz^T h_{t-1}

@@ -70,32 +70,39 @@ struct RecLayout {
   int ch;       // chunks per TMA op
   int nops;     // TMA ops per step
   int nslots;   // ring slots (one op each)
-  int rot;      // ch == 1: CTA c fetches chunks starting at a CTA-dependent offset (spreads L2 load)
 };
 
-JN_DEV int chunk_of(const RecLayout &ly, int k) {
-  return ly.rot ? (k + (int)blockIdx.x * 7) % ly.nk : k;
-}
-
-// optional timeline probe (CTA 0 only): dbg[8 t + k] = %globaltimer (ns)
+// optional timeline probe (every CTA): dbg[(cta * T + t) * 8 + k] = %globaltimer (ns)
 #define PROBE(t_, k_)                                                            \
   do {                                                                           \
-    if (a.dbg && blockIdx.x == 0) {                                              \
+    if (a.dbg) {                                                                 \
       unsigned long long ts_;                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_));                    \
-      a.dbg[8 * (t_) + (k_)] = ts_;                                              \
+      a.dbg[((size_t)blockIdx.x * a.T + (t_)) * 8 + (k_)] = ts_;                 \
     }                                                                            \
   } while (0)
 
-// Producer (warp 4, lane 0): TMA op k of step `st` into ring slot (st*nops + k) % nslots.
-JN_DEV void issue_step(const CUtensorMap *tm, const RecLayout &ly, uint8_t *sA, uint64_t *full,
-                       uint64_t *empty, int st, int row0) {
+// Epilogue: this CTA's 16 units of batch row b (bf16) into exchange block `blk` — chunk u0/64,
+// two 16-B granules at their swizzled positions (the layout the consumer's MMA descriptors read).
+JN_DEV void write_xchg(uint8_t *xbuf, int blk, int nk, int cb, int u0, int b,
+                       const __nv_bfloat16 (&hb)[16]) {
+  uint8_t *chunk = xbuf + ((size_t)blk * nk + (u0 >> 6)) * cb;
+  const uint32_t g0 = (uint32_t)(u0 & 63) >> 3;
+  *reinterpret_cast<uint4 *>(chunk + sw128_off(b, g0)) = reinterpret_cast<const uint4 *>(hb)[0];
+  *reinterpret_cast<uint4 *>(chunk + sw128_off(b, g0 + 1)) = reinterpret_cast<const uint4 *>(hb)[1];
+}
+
+// Producer (warp 4, lane 0): op k of step `st` copies chunks [k*ch, k*ch + ch) of the step's
+// exchange block (already in the swizzled shared-memory layout, contiguous) into ring slot
+// (st*nops + k) % nslots with one bulk copy.
+JN_DEV void issue_step(const uint8_t *src, const RecLayout &ly, uint8_t *sA, uint64_t *full,
+                       uint64_t *empty, int st) {
   for (int k = 0; k < ly.nops; ++k) {
     const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
     if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
-    mbar_expect_tx(&full[s], ly.ch * ly.cb);
-    tma_load_3d(sA + (size_t)s * ly.ch * ly.cb, tm, &full[s], 0, row0,
-                ly.ch == 1 ? chunk_of(ly, k) : k * ly.ch);
+    const int nch = min(ly.ch, ly.nk - k * ly.ch);
+    mbar_expect_tx(&full[s], nch * ly.cb);
+    bulk_load(sA + (size_t)s * ly.ch * ly.cb, src + (size_t)k * ly.ch * ly.cb, nch * ly.cb, &full[s]);
   }
 }
 
@@ -109,7 +116,7 @@ JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *fu
     tc_fence_after();
     const uint32_t sa = smem_u32(sA + (size_t)s * ly.ch * ly.cb);
     for (int c = 0; c < ly.ch; ++c) {
-      const int j = ly.ch == 1 ? chunk_of(ly, k) : k * ly.ch + c;
+      const int j = k * ly.ch + c;
       if (k * ly.ch + c >= ly.nk) break;
       const uint32_t ca = sa + c * ly.cb, cw = smem_u32(sW + j * WCHUNK);
 #pragma unroll
@@ -125,8 +132,7 @@ JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *fu
 // ---------------------------------------------------------------------------------- forward
 template <bool MASKED>
 __global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmH,  // Hs chunks {64, (T+1)B, nk}
-                        const __grid_constant__ CUtensorMap tmW,  // W_hh interleaved [4H x H], box {64,64}
+    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmW,  // W_hh interleaved [4H x H], box {64,64}
                         RecFwdArgs a, RecLayout ly) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -148,7 +154,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   if (a.fail && *a.fail) return;
 
   if (threadIdx.x == 128) {
-    tma_prefetch_desc(&tmH);
     tma_prefetch_desc(&tmW);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
@@ -179,6 +184,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       a.Cs[(size_t)b * a.ldh + gu] = creg[u];
     }
   }
+  uint8_t *hsw = reinterpret_cast<uint8_t *>(a.Hsw);
+  if (row) {
+    __align__(16) __nv_bfloat16 h0b[REC_UPC];
+#pragma unroll
+    for (int u = 0; u < REC_UPC; ++u) h0b[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
+    write_xchg(hsw, 0, nk, ly.cb, u0, b, h0b);
+  }
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
   unsigned int *flags = a.barrier;  // flags[c] = 1 + last step whose h block CTA c has written
   fence_proxy_async_global();
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       wait_flags_warp(flags, gridDim.x, (unsigned)t + 1);  // h_{t-1} fully written
       if (threadIdx.x == 128) {
         PROBE(t, 1);
-        issue_step(&tmH, ly, sA, full, empty, t, t * B);
+        issue_step(hsw + (size_t)t * nk * ly.cb, ly, sA, full, empty, t);
         PROBE(t, 2);
       }
       __syncwarp();
@@ -240,8 +252,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
           const float h2 = og * tanh_f(c2);
           z[4 * u] = ig; z[4 * u + 1] = fg; z[4 * u + 2] = gg; z[4 * u + 3] = og;
           if (valid) { creg[u] = c2; hreg[u] = h2; }
-          hb[u] = __float2bfloat16_rn(hreg[u]);
+          hb[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
         }
+        write_xchg(hsw, t + 1, nk, ly.cb, u0, b, hb);  // first: it is on the other CTAs' critical path
         const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
         if (nu == REC_UPC) {
 #pragma unroll
@@ -287,8 +300,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // ---------------------------------------------------------------------------------- backward
 template <bool MASKED>
 __global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmDZ,  // DZ chunks {64, T*B, nk}
-                        const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,16}
+    lstm_rec_bwd_kernel(const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,16}
                         RecBwdArgs a, RecLayout ly) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -310,7 +322,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   if (a.fail && *a.fail) return;
 
   if (threadIdx.x == 128) {
-    tma_prefetch_desc(&tmDZ);
     tma_prefetch_desc(&tmWT);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(tfull, 1);
@@ -342,6 +353,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   constexpr uint32_t idesc = umma_idesc_bf16(128, 16, 0, 0);
   if (warp == 5) mbar_wait(wfull, 0);
   unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c has completed
+  uint8_t *dzsw = reinterpret_cast<uint8_t *>(a.DZsw);
   int nmma = 0;                     // steps that issued MMAs (tfull phase)
 
   for (int t = T - 1; t >= 0; --t) {
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         wait_flags_warp(flags, gridDim.x, (unsigned)(T - 1 - t));  // dz_{t+1} fully written
         if (threadIdx.x == 128) {
           PROBE(ti, 1);
-          issue_step(&tmDZ, ly, sA, full, empty, nmma, (t + 1) * B);
+          issue_step(dzsw + (size_t)(t + 1) * nk * ly.cb, ly, sA, full, empty, nmma);
           PROBE(ti, 2);
         }
       }
@@ -423,8 +435,15 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
             dzb[4 * u + 3] = __float2bfloat16_rn(dout * og * (1.f - og));
           } else {
             carry[u] = dhu;  // masked step: (h, c) passed through unchanged
-            dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
           }
+          if (!valid || u >= nu)
+            dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
+        }
+        {  // exchange copy first: it is on the other CTAs' critical path
+          uint8_t *chunk = dzsw + ((size_t)t * nk + blockIdx.x) * ly.cb;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4 *>(chunk + sw128_off(b, k)) = reinterpret_cast<const uint4 *>(dzb)[k];
         }
         if (nu == REC_UPC) {
           uint4 *d4 = reinterpret_cast<uint4 *>(dz);
@@ -463,7 +482,6 @@ static RecLayout layout(int wbytes, int nk, int B) {
   l.nslots = 2;
   l.ch = std::min((nk + 1) / 2, max_chunks / 2);
   l.ch = std::max(1, std::min(l.ch, 256));
-  l.rot = 0;
   if (const char *e = getenv("JANUS_REC_CH")) {  // experiment knob: chunks per TMA op
     const int ch = atoi(e);
     if (ch >= 1) {
@@ -471,11 +489,14 @@ static RecLayout layout(int wbytes, int nk, int B) {
       l.nslots = std::max(2, std::min(REC_MAX_SLOTS, max_chunks / l.ch));
     }
   }
-  if (const char *e = getenv("JANUS_REC_ROT")) l.rot = atoi(e) && l.ch == 1;
   l.nops = (nk + l.ch - 1) / l.ch;
   return l;
 }
 static int smem_of(const RecLayout &l) { return 1024 + l.wbytes + l.nslots * l.ch * l.cb + PAD + 1024; }
+
+static size_t xchg_block(int cols, int B) { return (size_t)((cols + 63) / 64) * ((B + 7) & ~7) * 128; }
+size_t rec_hsw_bytes(int H, int B, int T) { return (size_t)(T + 1) * xchg_block(H, B); }
+size_t rec_dzsw_bytes(int H, int B, int T) { return (size_t)T * xchg_block(4 * H, B); }
 
 int rec_grid(int H) { return (H + REC_UPC - 1) / REC_UPC; }
 
@@ -499,16 +520,15 @@ cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw,
   const int nk = (a.H + 63) / 64;
   RecLayout ly = layout(nk * 8192, nk, a.B);
   if (ly.ch < 1 || smem_of(ly) > 232448) return cudaErrorInvalidValue;
-  CUtensorMap tmH, tmW;
-  if (!make_tmap_bf16_chunks(&tmH, a.Hs, (uint64_t)(a.T + 1) * a.B, a.ldh, nk, ly.bp, ly.ch))
-    return cudaErrorInvalidValue;
+  if (!a.Hsw) return cudaErrorInvalidValue;
+  CUtensorMap tmW;
   if (!make_tmap_bf16(&tmW, Whh, a.H, 4ull * a.H, ldw, 64)) return cudaErrorInvalidValue;
   const int smem = smem_of(ly);
   const void *fn = masked ? (const void *)lstm_rec_fwd_kernel<true> : (const void *)lstm_rec_fwd_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   RecFwdArgs aa = a;
-  void *args[] = {&tmH, &tmW, &aa, &ly};
+  void *args[] = {&tmW, &aa, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
 
@@ -518,16 +538,15 @@ cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldw
   const int nk = (4 * a.H + 63) / 64;
   RecLayout ly = layout(nk * 2048, nk, a.B);
   if (ly.ch < 1 || smem_of(ly) > 232448) return cudaErrorInvalidValue;
-  CUtensorMap tmDZ, tmWT;
-  if (!make_tmap_bf16_chunks(&tmDZ, a.DZ, (uint64_t)a.T * a.B, a.ldz, nk, ly.bp, ly.ch))
-    return cudaErrorInvalidValue;
+  if (!a.DZsw) return cudaErrorInvalidValue;
+  CUtensorMap tmWT;
   if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 16)) return cudaErrorInvalidValue;
   const int smem = smem_of(ly);
   const void *fn = masked ? (const void *)lstm_rec_bwd_kernel<true> : (const void *)lstm_rec_bwd_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   RecBwdArgs aa = a;
-  void *args[] = {&tmDZ, &tmWT, &aa, &ly};
+  void *args[] = {&tmWT, &aa, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
 

@@ -20,6 +20,9 @@ struct RecFwdArgs {
   const int *fail = nullptr;                 // nonzero: skip (cooperative cancellation)
   const int *tag = nullptr;                  // state type tag; != 1 -> h0 = c0 = 0 (device Switch)
   unsigned long long *dbg = nullptr;         // optional %globaltimer probe of CTA 0 (8 per step)
+  // exchange copy of h in the consumers' shared-memory layout: [T+1][nk chunks][Bp rows][128 B],
+  // 128-B swizzled, so a step's operand is fetched with a few large bulk copies
+  __nv_bfloat16 *Hsw = nullptr;
 };
 
 struct RecBwdArgs {
@@ -36,7 +39,12 @@ struct RecBwdArgs {
   unsigned int *barrier = nullptr;
   const int *fail = nullptr;
   unsigned long long *dbg = nullptr;
+  __nv_bfloat16 *DZsw = nullptr;  // exchange copy of dz: [T][nk chunks][Bp rows][128 B] swizzled
 };
+
+// bytes of the swizzled exchange buffers
+size_t rec_hsw_bytes(int H, int B, int T);
+size_t rec_dzsw_bytes(int H, int B, int T);
 
 int rec_grid(int H);
 cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw, bool masked,

@@ -11,16 +11,27 @@ prog = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=T, lr=1.0)
 g = J.Graph(prog); ws = g.new_workspace()
 state = [torch.tensor(x, device="cuda") for x in gen.uniform_params(prog, 1, 0.05)]
 args = [torch.tensor(a, device="cuda") for a in list(gen.lm_batches(gen.SEED_C2, B, T, 10000, 1))[0]]
-buf = torch.zeros(16 * T, dtype=torch.int64, device="cuda")
+buf = torch.zeros(2 * 128 * 8 * T, dtype=torch.int64, device="cuda")
 for k in range(3):
     g.run(args, state, ws, outs=[torch.zeros(1, device="cuda")])
 J.lib.janus_dev_set_probe(g.h, buf.data_ptr())
 g.run(args, state, ws, outs=[torch.zeros(1, device="cuda")])
 torch.cuda.synchronize()
-d = buf.cpu().numpy().astype(np.float64).reshape(2, T, 8)
-names = ["start", "flags_ok", "tma_issued", "chunk0_landed", "mma_issued", "mma_done", "epi_done", "published"]
+NC = (650 + 15) // 16
+d = buf.cpu().numpy().astype(np.float64).reshape(2, 128, T, 8)[:, :NC]
+names = ["start", "flags_ok", "tma_issued", "-", "mma_issued", "mma_done", "epi_done", "published"]
 for dirn, a in (("fwd", d[0]), ("bwd", d[1])):
-    rel = a - a[:, :1]
-    print(f"== {dirn}: step period {np.median(np.diff(a[:, 0])):.0f} ns; median offsets from step start (ns):")
+    t0 = a[:, :, 0].min(axis=0)  # earliest CTA start of each step
+    per = np.median(np.diff(t0))
+    print(f"== {dirn}: step period {per:.0f} ns; offsets from the step's earliest start (ns): median / max over CTAs")
     for k, n in enumerate(names):
-        print(f"   {n:14s} {np.median(rel[1:-1, k]):8.0f}")
+        if n == "-": continue
+        rel = a[:, 1:-1, k] - t0[None, 1:-1]
+        print(f"   {n:12s} med {np.median(rel):7.0f}  p90 {np.percentile(rel, 90):7.0f}  max-cta-median {np.median(rel, axis=1).max():7.0f} (cta {np.median(rel, axis=1).argmax()})")
+    pub = a[:, 1:-1, 7] - t0[None, 1:-1]
+    last = pub.argmax(axis=0)
+    print("   last publisher histogram:", np.bincount(last, minlength=NC).tolist())
+    own = a[:, 1:-1, 7] - a[:, 1:-1, 1]
+    print(f"   own work flags_ok->published: med {np.median(own):.0f} max {own.max():.0f}")
+    print(f"   ld->mma: med {np.median(a[:, 1:-1, 4]-a[:, 1:-1, 2]):.0f}; mma->epi_done: {np.median(a[:, 1:-1, 6]-a[:, 1:-1, 5]):.0f}; epi->pub {np.median(a[:, 1:-1, 7]-a[:, 1:-1, 6]):.0f}")
+    print(f"   globaltimer granularity: min nonzero diff {np.min(np.diff(np.unique(a[:, :, 7])))}")
