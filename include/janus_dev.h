@@ -24,9 +24,9 @@ int32_t janus_dev_gemm_bf16(int32_t M, int32_t N, int32_t K, const void *A, int3
  * "name:total_ms:count;..." over the phases run since enabling. */
 struct janus_graph;
 int32_t janus_dev_profile(struct janus_graph *g, int32_t enable);
-/* Timeline probe of the layer-0 recurrent kernels (every CTA): dev_buf (device, 2*128*8*T u64)
- * receives %globaltimer stamps, 8 per step: forward CTA c step t at ((c*T)+t)*8, backward at
- * 128*8*T + the same index. NULL disables. */
+/* Timeline probe of the layer-0 recurrent kernels (every CTA): dev_buf (device, 2*128*16*T u64)
+ * receives %globaltimer stamps, 16 per step: forward CTA c step t at ((c*T)+t)*16, backward at
+ * 128*16*T + the same index. NULL disables. */
 int32_t janus_dev_set_probe(struct janus_graph *g, void *dev_buf);
 /* Byte offset and size of a named region of the workspace after janus_run: "status",
  * "tree.height", "tree.order", "tree.irank", "tree.pslot", "tree.lvl_off", "tree.meta"

@@ -119,7 +119,7 @@ struct Graph {
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
   std::string describe;
-  unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*8*T u64)
+  unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*16*T u64)
 };
 
 // host_graph.cpp

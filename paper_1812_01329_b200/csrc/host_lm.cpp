@@ -212,7 +212,7 @@ bool lower_lm(Graph &g, std::string &why) {
       p.off.bil[l] = take((size_t)G4 * 4);
       p.off.Hs[l] = take((TB + B) * p.Hp * 2);
       p.off.Cs[l] = take((TB + B) * p.Hp * 4);
-      p.off.G[l] = take(TB * G4 * 4);
+      p.off.G[l] = take(TB * p.Gz * 4);  // gate pitch padded to 64 per recurrent CTA
       p.off.DZ[l] = take(TB * p.Gz * 2);
       p.off.Hsw[l] = take(rec_hsw_bytes(H, B, T));
       p.off.DZsw[l] = take(rec_dzsw_bytes(H, B, T));
@@ -434,7 +434,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.M = TB; op.N = G4; op.K = In;
     op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
     op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
-    op.ep.C = fp(p.off.G[l]); op.ep.ldc = G4; op.ep.bias_col = fp(p.off.bil[l]);
+    op.ep.C = fp(p.off.G[l]); op.ep.ldc = p.Gz; op.ep.bias_col = fp(p.off.bil[l]);
     LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(op, st));
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
@@ -478,7 +478,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     rb.dHin = l == L - 1 ? fp(p.off.dHtop) : fp(p.off.dX[l + 1]); rb.ldd = Hp;
     rb.DZsw = bf(p.off.DZsw[l]);
     rb.DZ = bf(p.off.DZ[l]); rb.ldz = p.Gz; rb.barrier = bars + 256 * (L + l);
-    rb.dbg = (l == 0 && g.probe) ? g.probe + (size_t)128 * 8 * p.T : nullptr;
+    rb.dbg = (l == 0 && g.probe) ? g.probe + (size_t)128 * 16 * p.T : nullptr;
     LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(rb, bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
     const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
     GemmOp a;  // dW_hh = dz^T h_{t-1}

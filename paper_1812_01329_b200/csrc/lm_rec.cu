@@ -25,7 +25,8 @@
 
 namespace jk {
 
-constexpr int REC_THREADS = 192;
+constexpr int REC_NMW = 4;       // MMA-issuing warps (one tcgen05.mma stream each, own accumulator)
+constexpr int REC_THREADS = 160 + 32 * REC_NMW;
 constexpr int REC_UPC = 16;      // hidden units per CTA
 constexpr int REC_MAX_SLOTS = 48;
 constexpr int SMEM_BUDGET = 232448 - 1024;
@@ -72,13 +73,13 @@ struct RecLayout {
   int nslots;   // ring slots (one op each)
 };
 
-// optional timeline probe (every CTA): dbg[(cta * T + t) * 8 + k] = %globaltimer (ns)
+// optional timeline probe (every CTA): dbg[(cta * T + t) * 16 + k] = %globaltimer (ns)
 #define PROBE(t_, k_)                                                            \
   do {                                                                           \
     if (a.dbg) {                                                                 \
       unsigned long long ts_;                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_));                    \
-      a.dbg[((size_t)blockIdx.x * a.T + (t_)) * 8 + (k_)] = ts_;                 \
+      a.dbg[((size_t)blockIdx.x * a.T + (t_)) * 16 + (k_)] = ts_;                \
     }                                                                            \
   } while (0)
 
@@ -106,25 +107,34 @@ JN_DEV void issue_step(const uint8_t *src, const RecLayout &ly, uint8_t *sA, uin
   }
 }
 
-// MMA issuer (warp 5, lane 0): D (TMEM) = sum over the step's chunks of A_chunk . W_chunk^T.
-template <int WCHUNK>
+// MMA issuers (warps 5 .. 5+REC_NMW-1, lane 0 each). A single issuing warp sustains only about
+// one tcgen05.mma per ~130 cycles whatever N is (measured: scripts/bench_mma.cu), and the
+// recurrent MMAs are small (N = 64 / 16), so the step's K chunks are dealt round-robin to REC_NMW
+// warps, each accumulating into its own TMEM tile (columns w * NCOL); the epilogue sums the tiles.
+// Warp w: D_w = sum over chunks j = w (mod REC_NMW) of A_j . W_j^T.
+template <int WCHUNK, int NCOL>
 JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *full, uint64_t *empty,
-                     uint64_t *tfull, uint32_t tmem, uint32_t idesc, int st) {
+                     uint64_t *tfull, uint32_t tmem, uint32_t idesc, int st, int w,
+                     unsigned long long *pr) {
+  const uint32_t acc = tmem + (uint32_t)(w * NCOL);
   for (int k = 0; k < ly.nops; ++k) {
     const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
     mbar_wait(&full[s], r & 1);
+    if (pr && k < 4) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pr[8 + 2 * k]));
     tc_fence_after();
     const uint32_t sa = smem_u32(sA + (size_t)s * ly.ch * ly.cb);
     for (int c = 0; c < ly.ch; ++c) {
       const int j = k * ly.ch + c;
-      if (k * ly.ch + c >= ly.nk) break;
+      if (j >= ly.nk) break;
+      if (j % REC_NMW != w) continue;
       const uint32_t ca = sa + c * ly.cb, cw = smem_u32(sW + j * WCHUNK);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem, umma_desc_sw128(ca + kk * 32, 16, 1024), umma_desc_sw128(cw + kk * 32, 16, 1024),
-                  idesc, ((k * ly.ch + c) | kk) != 0);
+        umma_bf16(acc, umma_desc_sw128(ca + kk * 32, 16, 1024), umma_desc_sw128(cw + kk * 32, 16, 1024),
+                  idesc, (j != w || kk != 0) ? 1u : 0u);
     }
-    umma_commit(&empty[s]);
+    umma_commit(&empty[s]);  // the slot is free once every issuing warp's MMAs on it completed
+    if (pr && k < 4) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pr[9 + 2 * k]));
   }
   umma_commit(tfull);
 }
@@ -149,18 +159,19 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int b = threadIdx.x;  // batch row owned in the epilogue (warps 0-3)
   const int u0 = blockIdx.x * REC_UPC;
-  const int B = a.B, H = a.H, G4 = 4 * a.H;
+  const int B = a.B, H = a.H;
+  const int ldg = 64 * gridDim.x;  // G pitch
   const int nu = min(REC_UPC, H - u0);
   if (a.fail && *a.fail) return;
 
   if (threadIdx.x == 128) {
     tma_prefetch_desc(&tmW);
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tfull, 1);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
+    mbar_init(tfull, REC_NMW);
     mbar_init(wfull, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 64);
+  if (warp == 5) tmem_alloc(tmem_slot, 64 * REC_NMW);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -197,7 +208,8 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   publish_flag(&flags[blockIdx.x], 1);
   const int T = a.T_dev ? *a.T_dev : a.T;
   constexpr uint32_t idesc = umma_idesc_bf16(128, 64, 0, 0);
-  if (warp == 5) mbar_wait(wfull, 0);
+  const int nacc = min(REC_NMW, nk);  // accumulator tiles in use
+  if (warp >= 5) mbar_wait(wfull, 0);
 
   for (int t = 0; t < T; ++t) {
     if (warp == 4) {
@@ -209,25 +221,23 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         PROBE(t, 2);
       }
       __syncwarp();
-    } else if (warp == 5) {
-      if (threadIdx.x == 160) {
-        mma_step<8192>(ly, sA, sW, full, empty, tfull, tmem, idesc, t);
-        PROBE(t, 4);
+    } else if (warp >= 5) {
+      if ((threadIdx.x & 31) == 0) {
+        mma_step<8192, 64>(ly, sA, sW, full, empty, tfull, tmem, idesc, t, warp - 5,
+                           (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + t) * 16 : nullptr);
+        if (warp == 5) PROBE(t, 4);
       }
       __syncwarp();
     } else {
       // input projection of this step (independent of h_{t-1}): load while the MMA runs
+      // G rows are padded to 64 columns per CTA (ldg = 64 * grid), so every CTA moves whole
+      // 256-B rows; the padding units compute junk that is never published (hb = 0 there)
       float z[64];
-      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * G4 + (size_t)blockIdx.x * 64;
-      if (row && nu == REC_UPC) {
+      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * ldg + (size_t)blockIdx.x * 64;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float4 x = reinterpret_cast<const float4 *>(g)[q];
-          z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 64; ++q) z[q] = (row && q < 4 * nu) ? g[q] : 0.f;
+      for (int q = 0; q < 16; ++q) {
+        const float4 x = row ? reinterpret_cast<const float4 *>(g)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
       }
       mbar_wait(tfull, t & 1);
       if (threadIdx.x == 0) PROBE(t, 5);
@@ -236,10 +246,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       {
         float lo[32], hi[32];
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-        tmem_ld32(ta, lo);
-        tmem_ld32(ta + 32, hi);
+        for (int w = 0; w < nacc; ++w) {
+          tmem_ld32(ta + w * 64, lo);
+          tmem_ld32(ta + w * 64 + 32, hi);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) { z[i] += lo[i]; z[32 + i] += hi[i]; }
+          for (int i = 0; i < 32; ++i) { z[i] += lo[i]; z[32 + i] += hi[i]; }
+        }
       }
       if (row) {
         const bool valid = !MASKED || t < len_b;
@@ -256,24 +268,18 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         }
         write_xchg(hsw, t + 1, nk, ly.cb, u0, b, hb);  // first: it is on the other CTAs' critical path
         const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
-        if (nu == REC_UPC) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            reinterpret_cast<float4 *>(g)[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
-          uint4 *hd = reinterpret_cast<uint4 *>(a.Hs + ro);
-          hd[0] = reinterpret_cast<const uint4 *>(hb)[0];
-          hd[1] = reinterpret_cast<const uint4 *>(hb)[1];
-          float4 *cd = reinterpret_cast<float4 *>(a.Cs + ro);
+        for (int q = 0; q < 16; ++q)
+          reinterpret_cast<float4 *>(g)[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
+        float4 *cd = reinterpret_cast<float4 *>(a.Cs + ro);  // ldh >= 64 * ceil(H / 64)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
-        } else {
+        for (int q = 0; q < 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
 #pragma unroll
-          for (int q = 0; q < 64; ++q)
-            if (q < 4 * nu) g[q] = z[q];
-#pragma unroll
-          for (int u = 0; u < REC_UPC; ++u)
-            if (u < nu) { a.Cs[ro + u] = creg[u]; a.Hs[ro + u] = hb[u]; }
-        }
+        for (int u = 0; u < REC_UPC; ++u)  // column H of Hs is the GEMMs' ones column
+          if (u == nu) hb[u] = __float2bfloat16_rn(1.f);
+        uint4 *hd = reinterpret_cast<uint4 *>(a.Hs + ro);
+        hd[0] = reinterpret_cast<const uint4 *>(hb)[0];
+        hd[1] = reinterpret_cast<const uint4 *>(hb)[1];
       }
       if (threadIdx.x == 0) PROBE(t, 6);
       fence_proxy_async_global();
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tmem, 64);
+  if (warp == 5) tmem_dealloc(tmem, 64 * REC_NMW);
 }
 
 // ---------------------------------------------------------------------------------- backward
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
-  const int G4 = 4 * a.H;
+  const int ldg = 64 * gridDim.x;  // G pitch
   const int nk = ly.nk, S = ly.nslots;
   uint8_t *sW = base;
   uint8_t *sA = sW + ly.wbytes;
@@ -323,12 +329,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 
   if (threadIdx.x == 128) {
     tma_prefetch_desc(&tmWT);
-    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(tfull, 1);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
+    mbar_init(tfull, REC_NMW);
     mbar_init(wfull, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 32);
+  if (warp == 5) tmem_alloc(tmem_slot, 16 * REC_NMW < 32 ? 32 : 16 * REC_NMW);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -351,7 +357,8 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 #pragma unroll
   for (int u = 0; u < REC_UPC; ++u) { dcreg[u] = 0.f; carry[u] = 0.f; }
   constexpr uint32_t idesc = umma_idesc_bf16(128, 16, 0, 0);
-  if (warp == 5) mbar_wait(wfull, 0);
+  const int nacc = min(REC_NMW, nk);
+  if (warp >= 5) mbar_wait(wfull, 0);
   unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c has completed
   uint8_t *dzsw = reinterpret_cast<uint8_t *>(a.DZsw);
   int nmma = 0;                     // steps that issued MMAs (tfull phase)
@@ -370,10 +377,11 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         }
       }
       __syncwarp();
-    } else if (warp == 5) {
-      if (has_next && threadIdx.x == 160) {
-        mma_step<2048>(ly, sA, sW, full, empty, tfull, tmem, idesc, nmma);
-        PROBE(ti, 4);
+    } else if (warp >= 5) {
+      if (has_next && (threadIdx.x & 31) == 0) {
+        mma_step<2048, 16>(ly, sA, sW, full, empty, tfull, tmem, idesc, nmma, warp - 5,
+                           (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
+        if (warp == 5) PROBE(ti, 4);
       }
       __syncwarp();
     } else {
@@ -381,26 +389,25 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       const size_t r = (size_t)(t * B + (row ? b : 0));
       float gt[64], ct[REC_UPC], cp[REC_UPC], din[REC_UPC];
       {
-        const float *g = a.G + r * G4 + (size_t)blockIdx.x * 64;
+        // padded pitches (G: 64 per CTA, Cs / dHin: >= 64 * ceil(H / 64)): whole-row vector loads
+        const float *g = a.G + r * ldg + (size_t)blockIdx.x * 64;
         const float *pc = a.Cs + (r + B) * a.ldh + u0;
         const float *pp = a.Cs + r * a.ldh + u0;
         const float *pd = a.dHin + r * a.ldd + u0;
-        if (row && nu == REC_UPC) {
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float4 x = reinterpret_cast<const float4 *>(g)[k];
-            gt[4 * k] = x.x; gt[4 * k + 1] = x.y; gt[4 * k + 2] = x.z; gt[4 * k + 3] = x.w;
-          }
+        for (int k = 0; k < 16; ++k) {
+          const float4 x = row ? reinterpret_cast<const float4 *>(g)[k] : zero4;
+          gt[4 * k] = x.x; gt[4 * k + 1] = x.y; gt[4 * k + 2] = x.z; gt[4 * k + 3] = x.w;
+        }
 #pragma unroll
-          for (int u = 0; u < REC_UPC; ++u) { ct[u] = pc[u]; cp[u] = pp[u]; din[u] = pd[u]; }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 64; ++k) gt[k] = (row && k < 4 * nu) ? g[k] : 0.f;
-#pragma unroll
-          for (int u = 0; u < REC_UPC; ++u) {
-            const bool ok = row && u < nu;
-            ct[u] = ok ? pc[u] : 0.f; cp[u] = ok ? pp[u] : 0.f; din[u] = ok ? pd[u] : 0.f;
-          }
+        for (int k = 0; k < 4; ++k) {
+          const float4 x = row ? reinterpret_cast<const float4 *>(pc)[k] : zero4;
+          const float4 y = row ? reinterpret_cast<const float4 *>(pp)[k] : zero4;
+          const float4 w = row ? reinterpret_cast<const float4 *>(pd)[k] : zero4;
+          ct[4 * k] = x.x; ct[4 * k + 1] = x.y; ct[4 * k + 2] = x.z; ct[4 * k + 3] = x.w;
+          cp[4 * k] = y.x; cp[4 * k + 1] = y.y; cp[4 * k + 2] = y.z; cp[4 * k + 3] = y.w;
+          din[4 * k] = w.x; din[4 * k + 1] = w.y; din[4 * k + 2] = w.z; din[4 * k + 3] = w.w;
         }
       }
       float dh[REC_UPC];
@@ -410,6 +417,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         __syncwarp();
         tc_fence_after();
         tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), dh);
+        for (int w = 1; w < nacc; ++w) {
+          float d2[REC_UPC];
+          tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + w * 16, d2);
+#pragma unroll
+          for (int u = 0; u < REC_UPC; ++u) dh[u] += d2[u];
+        }
       } else {
 #pragma unroll
         for (int u = 0; u < REC_UPC; ++u) dh[u] = 0.f;
@@ -445,14 +458,10 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
           for (int k = 0; k < 8; ++k)
             *reinterpret_cast<uint4 *>(chunk + sw128_off(b, k)) = reinterpret_cast<const uint4 *>(dzb)[k];
         }
-        if (nu == REC_UPC) {
+        {  // ldz >= 64 * grid: padding columns get the zeros computed for the padding units
           uint4 *d4 = reinterpret_cast<uint4 *>(dz);
 #pragma unroll
           for (int k = 0; k < 8; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
-        } else {
-#pragma unroll
-          for (int k = 0; k < 64; ++k)
-            if (k < 4 * nu) dz[k] = dzb[k];
         }
       }
       if (threadIdx.x == 0) PROBE(ti, 6);
@@ -466,7 +475,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(tmem, 32);
+  if (warp == 5) tmem_dealloc(tmem, 16 * REC_NMW < 32 ? 32 : 16 * REC_NMW);
 }
 
 // ---------------------------------------------------------------------------------- host
