@@ -238,10 +238,9 @@ bool lower_lm(Graph &g, std::string &why) {
     p.off.arena_end = o;
     p.off.dp_scratch = take(64);
     p.off.seg_word = take(TB * 4);
-    p.off.seg_start = take((TB + 1) * 4);
     p.off.seg_grad = take(TB * p.Ep * 4);
     p.off.nseg = take(16);
-    p.off.keys = take(TB * 8);
+    p.off.ehist = take((size_t)V * 4);
   }
   p.ws_bytes = o;
   char buf[512];
@@ -505,9 +504,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   int *seg_word = reinterpret_cast<int *>(W + p.off.seg_word);
   int *nseg = reinterpret_cast<int *>(W + p.off.nseg);
   if (p.lr_E != 0) {
-    LCHK("embed_grad", launch_embed_grad(P.tok, B, Wd, Tw, Tdev, fp(p.off.dX[0]), Ep, E, seg_word,
-                           reinterpret_cast<int *>(W + p.off.seg_start), fp(p.off.seg_grad), Ep,
-                           nseg, reinterpret_cast<unsigned long long *>(W + p.off.keys), st));
+    LCHK("embed_grad", launch_embed_grad(P.tok, B, Wd, Tw, Tdev, V, fp(p.off.dX[0]), Ep, E, seg_word,
+                                         reinterpret_cast<int *>(W + p.off.ehist), fp(p.off.seg_grad),
+                                         Ep, nseg, st));
     g.launches++;  // embed grad is two kernels
   }
   if (g.nccl) {

@@ -1,5 +1,7 @@
 // step_kernels.cu — SIMT phases of the speculative training step (see step_kernels.h).
 // HBM-bound work: 128-bit / coalesced access, grids sized in multiples of the SM count.
+#include <algorithm>
+
 #include "common.cuh"
 #include "step_kernels.h"
 
@@ -107,20 +109,42 @@ cudaError_t launch_trip(const int *lens, int B, int W, DevStatus *st, cudaStream
 }
 
 // ------------------------------------------------------------------------------ casts
-__global__ void cast_rows_kernel(const float *__restrict__ src, int R, int Cc, int ld_src,
-                                 __nv_bfloat16 *dst, int ld_dst, int H) {
-  const long long n = (long long)R * ld_dst;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e / ld_dst), k = (int)(e - (long long)r * ld_dst);
-    const int rs = H > 0 ? (r & 3) * H + (r >> 2) : r;  // interleaved row 4u+g <- g*H+u
-    dst[e] = __float2bfloat16_rn(k < Cc ? src[(size_t)rs * ld_src + k] : 0.f);
+// Block: 4 destination rows at a time, each thread 2 columns per row per 512-column chunk, all
+// four rows' loads issued before the stores (memory-level parallelism for an HBM-bound copy).
+constexpr int CR_ROWS = 4;
+__global__ void __launch_bounds__(256) cast_rows_kernel(const float *__restrict__ src, int R, int Cc,
+                                                        int ld_src, __nv_bfloat16 *__restrict__ dst,
+                                                        int ld_dst, int H) {
+  const bool pairs = ((ld_src | Cc) & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 7) == 0;
+  for (int r0 = blockIdx.x * CR_ROWS; r0 < R; r0 += gridDim.x * CR_ROWS) {
+    for (int k0 = 0; k0 < ld_dst; k0 += 512) {
+      const int k = k0 + 2 * threadIdx.x;
+      float2 v[CR_ROWS];
+#pragma unroll
+      for (int q = 0; q < CR_ROWS; ++q) {
+        const int r = r0 + q;
+        v[q] = make_float2(0.f, 0.f);
+        if (r < R && k < Cc) {
+          const int rs = H > 0 ? (r & 3) * H + (r >> 2) : r;  // interleaved row 4u+g <- g*H+u
+          const float *sr = src + (size_t)rs * ld_src;
+          if (pairs) v[q] = *reinterpret_cast<const float2 *>(sr + k);
+          else { v[q].x = sr[k]; if (k + 1 < Cc) v[q].y = sr[k + 1]; }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CR_ROWS; ++q)
+        if (r0 + q < R && k < ld_dst)  // ld_dst is even
+          reinterpret_cast<__nv_bfloat162 *>(dst + (size_t)(r0 + q) * ld_dst)[k >> 1] =
+              __floats2bfloat162_rn(v[q].x, v[q].y);
+    }
   }
 }
 
 cudaError_t launch_cast_rows(const float *src, int R, int Cc, int ld_src, __nv_bfloat16 *dst,
                              int ld_dst, int interleave_H, cudaStream_t s) {
-  cast_rows_kernel<<<8 * NSM, 256, 0, s>>>(src, R, Cc, ld_src, dst, ld_dst, interleave_H);
+  if (ld_dst & 1) return cudaErrorInvalidValue;
+  const int blocks = std::min((R + CR_ROWS - 1) / CR_ROWS, 16 * NSM);
+  cast_rows_kernel<<<blocks, 256, 0, s>>>(src, R, Cc, ld_src, dst, ld_dst, interleave_H);
   return cudaGetLastError();
 }
 
@@ -159,15 +183,21 @@ cudaError_t launch_bias_interleave(const float *b, int H, float *out, cudaStream
   return cudaGetLastError();
 }
 
+// X[r][col] = v, X[r][col+1 .. zero_to) = 0: one thread per element.
 __global__ void fill_col_kernel(__nv_bfloat16 *X, int rows, int ld, int col, float v, int zero_to) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-    X[(size_t)r * ld + col] = __float2bfloat16_rn(v);
-    for (int k = col + 1; k < zero_to; ++k) X[(size_t)r * ld + k] = __float2bfloat16_rn(0.f);
+  const int w = zero_to > col ? zero_to - col : 1;
+  const long long n = (long long)rows * w;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / w), k = (int)(e - (long long)r * w);
+    X[(size_t)r * ld + col + k] = __float2bfloat16_rn(k == 0 ? v : 0.f);
   }
 }
 cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v, int zero_to,
                             cudaStream_t s) {
-  fill_col_kernel<<<(rows + 255) / 256, 256, 0, s>>>(X, rows, ld, col, v, zero_to);
+  const long long n = (long long)rows * (zero_to > col ? zero_to - col : 1);
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 8 * NSM);
+  fill_col_kernel<<<blocks, 256, 0, s>>>(X, rows, ld, col, v, zero_to);
   return cudaGetLastError();
 }
 
@@ -254,108 +284,85 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
 }
 
 // ------------------------------------------------------------------------------ embedding grad
-// Single block: bitonic sort of (id << 32 | r) over r < Tb*B (time-major rows), then segment
-// starts by a block scan. Deterministic (no atomics in the accumulation order).
+// dE[w] = sum of the dX rows r with tok(r) = w (the VJP of the embedding lookup). No sort:
+//   1. claim (grid over rows): the first thread to CAS owner[w] from -1 allocates slot k for w
+//      (seg_word[k] = w). Slot order is scheduling dependent; the set of slots is not.
+//   2. segsum (block per slot): the block lists the rows of its word IN ROW ORDER (block ballots
+//      over the time-major rows), warp j sums list entries j, j+EG_WARPS, ..., and the EG_WARPS
+//      partials are combined in warp order — a fixed order, so every dE row is deterministic.
 constexpr int EG_MAX = 8192;
-__global__ void __launch_bounds__(1024) embed_sort_kernel(const int *tok, int B, int W, int T,
-                                                          const int *T_dev, int *seg_word,
-                                                          int *seg_start, int *nseg,
-                                                          unsigned long long *keys) {
-  extern __shared__ unsigned long long sk[];
-  __shared__ int warp_sums[32];
-  const int Tb = T_dev ? *T_dev : T;
-  const int n = Tb * B;
-  int np = 1;
-  while (np < n) np <<= 1;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) {
-    if (i < n) {
-      const int t = i / B, b = i - t * B;
-      sk[i] = ((unsigned long long)(unsigned)tok[(size_t)b * W + t] << 32) | (unsigned)i;
-    } else {
-      sk[i] = ~0ull;
-    }
+constexpr int EG_WARPS = 16;
+JN_DEV int tok_of(const int *tok, int B, int W, int r) {
+  const int t = r / B, b = r - t * B;
+  return tok[(size_t)b * W + t];
+}
+
+__global__ void embed_claim_kernel(const int *tok, int B, int W, int T, const int *T_dev, int *owner,
+                                   int *seg_word, int *nseg) {
+  const int n = (T_dev ? *T_dev : T) * B;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int w = tok_of(tok, B, W, r);
+    if (atomicCAS(&owner[w], -1, r) == -1) seg_word[atomicAdd(nseg, 1)] = w;
   }
-  __syncthreads();
-  for (int k = 2; k <= np; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const unsigned long long a = sk[i], c = sk[ixj];
-          if ((a > c) == up) { sk[i] = c; sk[ixj] = a; }
-        }
+}
+
+__global__ void __launch_bounds__(EG_WARPS * 32) embed_segsum_kernel(
+    const int *tok, int B, int W, int T, const int *T_dev, const int *seg_word, const int *nseg,
+    const float *__restrict__ dX, int ldx, int Edim, float *seg_grad, int ldg) {
+  __shared__ int rows[EG_MAX];
+  __shared__ int wcount[EG_WARPS];
+  __shared__ float part[EG_WARPS][128];
+  const int n = (T_dev ? *T_dev : T) * B;
+  const int ns = *nseg;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int sgi = blockIdx.x; sgi < ns; sgi += gridDim.x) {
+    const int word = seg_word[sgi];
+    // ordered list of this word's rows
+    int cnt = 0;
+    for (int r0 = 0; r0 < n; r0 += blockDim.x) {
+      const int r = r0 + threadIdx.x;
+      const bool hit = r < n && tok_of(tok, B, W, r) == word;
+      const unsigned m = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) wcount[w] = __popc(m);
+      __syncthreads();
+      int before = cnt;
+      for (int j = 0; j < w; ++j) before += wcount[j];
+      if (hit) rows[before + __popc(m & ((1u << lane) - 1u))] = r;
+      for (int j = 0; j < EG_WARPS; ++j) cnt += wcount[j];
+      __syncthreads();
+    }
+    for (int c0 = 0; c0 < Edim; c0 += 128) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int i = w; i < cnt; i += EG_WARPS) {
+        const float *row = dX + (size_t)rows[i] * ldx + c0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (c0 + lane + 32 * q < Edim) acc[q] += row[lane + 32 * q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) part[w][lane + 32 * q] = acc[q];
+      __syncthreads();
+      if (w < 4) {
+        const int k = lane + 32 * w;
+        float sum = part[0][k];
+        for (int j = 1; j < EG_WARPS && j < cnt; ++j) sum += part[j][k];
+        if (c0 + k < Edim) seg_grad[(size_t)sgi * ldg + c0 + k] = sum;
       }
       __syncthreads();
     }
   }
-  // segment starts: flag, then exclusive scan (chunked per thread, block-wide)
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  const int lo = threadIdx.x * per, hi = min(n, lo + per);
-  int cnt = 0;
-  for (int i = lo; i < hi; ++i)
-    cnt += (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) ? 1 : 0;
-  // block exclusive scan of cnt
-  int v = cnt;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int x = __shfl_up_sync(0xffffffff, v, o);
-    if (lane >= o) v += x;
-  }
-  if (lane == 31) warp_sums[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    int ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int x = __shfl_up_sync(0xffffffff, ws, o);
-      if (lane >= o) ws += x;
-    }
-    warp_sums[lane] = ws;
-  }
-  __syncthreads();
-  int base = v - cnt + (w > 0 ? warp_sums[w - 1] : 0);
-  for (int i = lo; i < hi; ++i) {
-    if (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) {
-      seg_word[base] = (int)(sk[i] >> 32);
-      seg_start[base] = i;
-      ++base;
-    }
-  }
-  if (threadIdx.x == blockDim.x - 1) {
-    *nseg = base;
-    seg_start[base] = n;
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = sk[i];
 }
 
-__global__ void embed_segsum_kernel(const unsigned long long *keys, const int *seg_start,
-                                    const int *nseg, const float *__restrict__ dX, int ldx, int Edim,
-                                    float *seg_grad, int ldg) {
-  const int ns = *nseg;
-  for (int sgi = blockIdx.x; sgi < ns; sgi += gridDim.x) {
-    const int a = seg_start[sgi], e = seg_start[sgi + 1];
-    for (int k = threadIdx.x; k < Edim; k += blockDim.x) {
-      float acc = 0.f;
-      for (int i = a; i < e; ++i) acc += dX[(size_t)(keys[i] & 0xffffffffu) * ldx + k];
-      seg_grad[(size_t)sgi * ldg + k] = acc;
-    }
-  }
-}
-
-cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev,
-                              const float *dX, int ldx, int Edim, int *seg_word, int *seg_start,
-                              float *seg_grad, int ldg, int *nseg,
-                              unsigned long long *keys_scratch, cudaStream_t s) {
-  int np = 1;
-  while (np < T * B) np <<= 1;
-  if (np > EG_MAX) return cudaErrorInvalidValue;
-  const int smem = np * 8;
-  cudaError_t e = cudaFuncSetAttribute(embed_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev, int V,
+                              const float *dX, int ldx, int Edim, int *seg_word, int *owner,
+                              float *seg_grad, int ldg, int *nseg, cudaStream_t s) {
+  if (T * B > EG_MAX) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(owner, 0xff, (size_t)V * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(nseg, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
-  embed_sort_kernel<<<1, 1024, smem, s>>>(tok, B, W, T, T_dev, seg_word, seg_start, nseg, keys_scratch);
-  embed_segsum_kernel<<<4 * NSM, 256, 0, s>>>(keys_scratch, seg_start, nseg, dX, ldx, Edim, seg_grad, ldg);
+  embed_claim_kernel<<<(T * B + 255) / 256, 256, 0, s>>>(tok, B, W, T, T_dev, owner, seg_word, nseg);
+  embed_segsum_kernel<<<8 * NSM, EG_WARPS * 32, 0, s>>>(tok, B, W, T, T_dev, seg_word, nseg, dX, ldx,
+                                                        Edim, seg_grad, ldg);
   return cudaGetLastError();
 }
 
@@ -479,20 +486,38 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   switch (sg.kind) {
-    case C_DENSE: {
-      const long long n = (long long)sg.rows * sg.cols;
-      for (long long e = tid; e < n; e += stride) {
-        const int r = (int)(e / sg.cols), k = (int)(e - (long long)r * sg.cols);
-        sg.dst[e] -= sg.lr * sg.grad[(size_t)r * sg.ldg + k];
-      }
-    } break;
+    case C_DENSE:  // 4 rows per block iteration, 2 columns per thread, loads before stores
     case C_DENSE_IL: {
-      const long long n = (long long)sg.rows * sg.cols;
       const int ng = sg.ng ? sg.ng : 4;
-      for (long long e = tid; e < n; e += stride) {
-        const int rc = (int)(e / sg.cols), k = (int)(e - (long long)rc * sg.cols);
-        const int ri = ng * (rc % sg.H) + rc / sg.H;
-        sg.dst[e] -= sg.lr * sg.grad[(size_t)ri * sg.ldg + k];
+      const bool pairs = ((sg.cols | sg.ldg) & 1) == 0 &&
+                         ((reinterpret_cast<uintptr_t>(sg.dst) | reinterpret_cast<uintptr_t>(sg.grad)) & 7) == 0;
+      for (int r0 = blockIdx.x * CR_ROWS; r0 < sg.rows; r0 += gridDim.x * CR_ROWS) {
+        for (int k0 = 0; k0 < sg.cols; k0 += 512) {
+          const int k = k0 + 2 * threadIdx.x;
+          float2 dv[CR_ROWS], gv[CR_ROWS];
+#pragma unroll
+          for (int q = 0; q < CR_ROWS; ++q) {
+            const int rc = r0 + q;
+            dv[q] = gv[q] = make_float2(0.f, 0.f);
+            if (rc < sg.rows && k < sg.cols) {
+              const int ri = sg.kind == C_DENSE ? rc : ng * (rc % sg.H) + rc / sg.H;
+              const float *d = sg.dst + (size_t)rc * sg.cols + k;
+              const float *g = sg.grad + (size_t)ri * sg.ldg + k;
+              if (pairs) { dv[q] = *reinterpret_cast<const float2 *>(d); gv[q] = *reinterpret_cast<const float2 *>(g); }
+              else { dv[q].x = d[0]; gv[q].x = g[0]; if (k + 1 < sg.cols) { dv[q].y = d[1]; gv[q].y = g[1]; } }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < CR_ROWS; ++q) {
+            const int rc = r0 + q;
+            if (rc < sg.rows && k < sg.cols) {
+              float *d = sg.dst + (size_t)rc * sg.cols + k;
+              const float2 o = make_float2(dv[q].x - sg.lr * gv[q].x, dv[q].y - sg.lr * gv[q].y);
+              if (pairs) *reinterpret_cast<float2 *>(d) = o;
+              else { d[0] = o.x; if (k + 1 < sg.cols) d[1] = o.y; }
+            }
+          }
+        }
       }
     } break;
     case C_TREE_BIAS:  // b blocks (i, f, o, u): internal gates (i, f_l, f_r, o, u), leaf (i, o, u)
@@ -537,7 +562,7 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
 
 cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s) {
   if (cl.n <= 0) return cudaSuccess;
-  commit_kernel<<<dim3(2 * NSM, cl.n), 256, 0, s>>>(cl, st);
+  commit_kernel<<<dim3(4 * NSM, cl.n), 256, 0, s>>>(cl, st);
   return cudaGetLastError();
 }
 

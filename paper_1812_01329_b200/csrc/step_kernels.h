@@ -68,12 +68,12 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
                         const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
                         int lddy, float *rowloss, DevStatus *st, cudaStream_t s);
 
-// embedding gradient: sort (id, r) keys, segment sums of dX rows in ascending r.
-// seg_word[k], seg_grad[k][ldg] for k < *nseg.
-cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev,
-                              const float *dX, int ldx, int Edim, int *seg_word, int *seg_start,
-                              float *seg_grad, int ldg, int *nseg,
-                              unsigned long long *keys_scratch, cudaStream_t s);
+// embedding gradient: seg_word[k] (k < *nseg, slot order unspecified) lists the distinct ids of
+// the step; seg_grad[k][ldg] = sum of the dX rows of that id, summed in a fixed order
+// (deterministic). owner: V ints of scratch.
+cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev, int V,
+                              const float *dX, int ldx, int Edim, int *seg_word, int *owner,
+                              float *seg_grad, int ldg, int *nseg, cudaStream_t s);
 
 // loss = sum(rowloss) / n_valid... rowloss already carries the 1/n_valid scale; status decode.
 cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
