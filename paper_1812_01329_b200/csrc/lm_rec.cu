@@ -30,7 +30,6 @@ constexpr int REC_THREADS = 160 + 32 * REC_NMW;
 constexpr int REC_UPC = 16;      // hidden units per CTA
 constexpr int REC_MAX_SLOTS = 48;
 constexpr int SMEM_BUDGET = 232448 - 1024;
-constexpr int PAD = 16384;       // an M=128 MMA reads 128 rows from a chunk base
 
 // fp32-accurate activations on the fast exp path (|error| ~1e-7)
 JN_DEV float sig_f(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
@@ -48,19 +47,38 @@ JN_DEV void publish_flag(unsigned int *flag, unsigned int v) {
   __syncthreads();  // all of this CTA's stores of the step precede the release (bar.sync cumulativity)
   if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
 }
-// Executed by a whole warp: lanes poll the n producer flags in parallel (relaxed loads), then one
-// acquire fence and one generic->async proxy fence for the TMA loads lane 0 issues next.
+// Executed by a whole warp: lanes poll the n producer flags in parallel, two per 8-B relaxed load
+// (flags must be 8-B aligned), then one acquire fence and one generic->async proxy fence for the
+// bulk copies lane 0 issues next.
 JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
   const int lane = threadIdx.x & 31;
-  for (int c = lane; c < n; c += 32) {
-    unsigned int x;
+  for (int c = 2 * lane; c < n; c += 64) {
+    unsigned long long x;
+    unsigned lo, hi;
     do {
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
-    } while (x < v);
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(flags + c) : "memory");
+      lo = (unsigned)x;
+      hi = c + 1 < n ? (unsigned)(x >> 32) : v;
+    } while (lo < v || hi < v);
   }
   __syncwarp();
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
-  fence_proxy_async_global();  // the TMA (async proxy) reads what the generic proxy wrote
+  fence_proxy_async_global();  // the bulk copies (async proxy) read what the generic proxy wrote
+}
+
+// Named barrier of the four epilogue warps (threads 0-127) — the other warps run ahead.
+JN_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// Epilogue: this step's exchange-block writes are done (fenced for the async proxy by the caller);
+// thread 0 releases the CTA's step flag once all four epilogue warps got here.
+JN_DEV void epi_publish(unsigned int *flag, unsigned int v) {
+  epi_bar();
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+// Epilogue warp: its TMEM reads of this step completed -> the MMA warps may overwrite the tiles.
+JN_DEV void epi_tmem_release(uint64_t *tempty) {
+  tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(tempty);
 }
 
 struct RecLayout {
@@ -71,6 +89,7 @@ struct RecLayout {
   int ch;       // chunks per TMA op
   int nops;     // TMA ops per step
   int nslots;   // ring slots (one op each)
+  int pad;      // bytes after the ring: an M=128 MMA reads 128 rows from a chunk base
 };
 
 // optional timeline probe (every CTA): dbg[(cta * T + t) * 16 + k] = %globaltimer (ns)
@@ -114,11 +133,12 @@ JN_DEV void issue_step(const uint8_t *src, const RecLayout &ly, uint8_t *sA, uin
 // Warp w: D_w = sum over chunks j = w (mod REC_NMW) of A_j . W_j^T.
 template <int WCHUNK, int NCOL>
 JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *full, uint64_t *empty,
-                     uint64_t *tfull, uint32_t tmem, uint32_t idesc, int st, int w,
+                     uint64_t *tfull, uint64_t *tempty, uint32_t tmem, uint32_t idesc, int st, int w,
                      unsigned long long *pr) {
   const uint32_t acc = tmem + (uint32_t)(w * NCOL);
   for (int k = 0; k < ly.nops; ++k) {
     const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
+    if (k == 0 && st > 0) mbar_wait(tempty, (st - 1) & 1);  // the epilogue drained step st-1's tiles
     mbar_wait(&full[s], r & 1);
     if (pr && k < 4) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pr[8 + 2 * k]));
     tc_fence_after();
@@ -150,11 +170,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   const int nk = ly.nk, S = ly.nslots;
   uint8_t *sW = base;
   uint8_t *sA = sW + ly.wbytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sA + (size_t)S * ly.ch * ly.cb + PAD);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sA + (size_t)S * ly.ch * ly.cb + ly.pad);
   uint64_t *empty = full + S;
   uint64_t *tfull = empty + S;
   uint64_t *wfull = tfull + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
+  uint64_t *tempty = wfull + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int b = threadIdx.x;  // batch row owned in the epilogue (warps 0-3)
@@ -169,6 +190,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
     mbar_init(tfull, REC_NMW);
     mbar_init(wfull, 1);
+    mbar_init(tempty, 4);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc(tmem_slot, 64 * REC_NMW);
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       __syncwarp();
     } else if (warp >= 5) {
       if ((threadIdx.x & 31) == 0) {
-        mma_step<8192, 64>(ly, sA, sW, full, empty, tfull, tmem, idesc, t, warp - 5,
+        mma_step<8192, 64>(ly, sA, sW, full, empty, tfull, tempty, tmem, idesc, t, warp - 5,
                            (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + t) * 16 : nullptr);
         if (warp == 5) PROBE(t, 4);
       }
@@ -253,20 +275,26 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
           for (int i = 0; i < 32; ++i) { z[i] += lo[i]; z[32 + i] += hi[i]; }
         }
       }
-      if (row) {
-        const bool valid = !MASKED || t < len_b;
-        __align__(16) __nv_bfloat16 hb[REC_UPC];
+      epi_tmem_release(tempty);
+      const bool valid = !MASKED || t < len_b;
+      __align__(16) __nv_bfloat16 hb[REC_UPC];
 #pragma unroll
-        for (int u = 0; u < REC_UPC; ++u) {
-          const float ig = sig_f(z[4 * u]), fg = sig_f(z[4 * u + 1]);
-          const float gg = tanh_f(z[4 * u + 2]), og = sig_f(z[4 * u + 3]);
-          const float c2 = fg * creg[u] + ig * gg;
-          const float h2 = og * tanh_f(c2);
-          z[4 * u] = ig; z[4 * u + 1] = fg; z[4 * u + 2] = gg; z[4 * u + 3] = og;
-          if (valid) { creg[u] = c2; hreg[u] = h2; }
-          hb[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
-        }
-        write_xchg(hsw, t + 1, nk, ly.cb, u0, b, hb);  // first: it is on the other CTAs' critical path
+      for (int u = 0; u < REC_UPC; ++u) {
+        const float ig = sig_f(z[4 * u]), fg = sig_f(z[4 * u + 1]);
+        const float gg = tanh_f(z[4 * u + 2]), og = sig_f(z[4 * u + 3]);
+        const float c2 = fg * creg[u] + ig * gg;
+        const float h2 = og * tanh_f(c2);
+        z[4 * u] = ig; z[4 * u + 1] = fg; z[4 * u + 2] = gg; z[4 * u + 3] = og;
+        if (valid) { creg[u] = c2; hreg[u] = h2; }
+        hb[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
+      }
+      // critical path first: the exchange copy of h_t, then the step flag; the rest after
+      if (row) write_xchg(hsw, t + 1, nk, ly.cb, u0, b, hb);
+      fence_proxy_async_global();
+      if (threadIdx.x == 0) PROBE(t, 6);
+      epi_publish(&flags[blockIdx.x], (unsigned)t + 2);
+      if (threadIdx.x == 0) PROBE(t, 7);
+      if (row) {
         const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
 #pragma unroll
         for (int q = 0; q < 16; ++q)
@@ -281,13 +309,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         hd[0] = reinterpret_cast<const uint4 *>(hb)[0];
         hd[1] = reinterpret_cast<const uint4 *>(hb)[1];
       }
-      if (threadIdx.x == 0) PROBE(t, 6);
-      fence_proxy_async_global();
     }
-    tc_fence_before();
-    publish_flag(&flags[blockIdx.x], (unsigned)t + 2);  // also the CTA's TMEM reuse boundary
-    tc_fence_after();
-    if (threadIdx.x == 0) PROBE(t, 7);
   }
   // final state (committed by the commit phase only if every assumption held)
   if (row) {
@@ -315,11 +337,12 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   const int nk = ly.nk, S = ly.nslots;
   uint8_t *sW = base;
   uint8_t *sA = sW + ly.wbytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sA + (size_t)S * ly.ch * ly.cb + PAD);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sA + (size_t)S * ly.ch * ly.cb + ly.pad);
   uint64_t *empty = full + S;
   uint64_t *tfull = empty + S;
   uint64_t *wfull = tfull + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wfull + 1);
+  uint64_t *tempty = wfull + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
 
   const int warp = threadIdx.x >> 5;
   const int b = threadIdx.x;
@@ -332,6 +355,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
     mbar_init(tfull, REC_NMW);
     mbar_init(wfull, 1);
+    mbar_init(tempty, 4);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc(tmem_slot, 16 * REC_NMW < 32 ? 32 : 16 * REC_NMW);
@@ -379,7 +403,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       __syncwarp();
     } else if (warp >= 5) {
       if (has_next && (threadIdx.x & 31) == 0) {
-        mma_step<2048, 16>(ly, sA, sW, full, empty, tfull, tmem, idesc, nmma, warp - 5,
+        mma_step<2048, 16>(ly, sA, sW, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
                            (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
         if (warp == 5) PROBE(ti, 4);
       }
@@ -423,69 +447,321 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 #pragma unroll
           for (int u = 0; u < REC_UPC; ++u) dh[u] += d2[u];
         }
+        epi_tmem_release(tempty);
       } else {
 #pragma unroll
         for (int u = 0; u < REC_UPC; ++u) dh[u] = 0.f;
       }
-      if (row) {
-        __nv_bfloat16 *dz = a.DZ + r * a.ldz + (size_t)blockIdx.x * 64;
-        const bool valid = !MASKED || t < len_b;
-        __align__(16) __nv_bfloat16 dzb[64];
+      const bool valid = !MASKED || t < len_b;
+      __align__(16) __nv_bfloat16 dzb[64];
 #pragma unroll
-        for (int u = 0; u < REC_UPC; ++u) {
-          const float dhu = dh[u] + din[u] + carry[u];
-          const float ig = gt[4 * u], fg = gt[4 * u + 1], gg = gt[4 * u + 2], og = gt[4 * u + 3];
-          if (valid) {
-            const float tc = tanh_f(ct[u]);
-            const float dout = dhu * tc;
-            const float dc = dcreg[u] + dhu * og * (1.f - tc * tc);
-            const float di = dc * gg, dg = dc * ig, df = dc * cp[u];
-            dcreg[u] = dc * fg;
-            carry[u] = 0.f;
-            dzb[4 * u] = __float2bfloat16_rn(di * ig * (1.f - ig));
-            dzb[4 * u + 1] = __float2bfloat16_rn(df * fg * (1.f - fg));
-            dzb[4 * u + 2] = __float2bfloat16_rn(dg * (1.f - gg * gg));
-            dzb[4 * u + 3] = __float2bfloat16_rn(dout * og * (1.f - og));
-          } else {
-            carry[u] = dhu;  // masked step: (h, c) passed through unchanged
-          }
-          if (!valid || u >= nu)
-            dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
+      for (int u = 0; u < REC_UPC; ++u) {
+        const float dhu = dh[u] + din[u] + carry[u];
+        const float ig = gt[4 * u], fg = gt[4 * u + 1], gg = gt[4 * u + 2], og = gt[4 * u + 3];
+        if (valid) {
+          const float tc = tanh_f(ct[u]);
+          const float dout = dhu * tc;
+          const float dc = dcreg[u] + dhu * og * (1.f - tc * tc);
+          const float di = dc * gg, dg = dc * ig, df = dc * cp[u];
+          dcreg[u] = dc * fg;
+          carry[u] = 0.f;
+          dzb[4 * u] = __float2bfloat16_rn(di * ig * (1.f - ig));
+          dzb[4 * u + 1] = __float2bfloat16_rn(df * fg * (1.f - fg));
+          dzb[4 * u + 2] = __float2bfloat16_rn(dg * (1.f - gg * gg));
+          dzb[4 * u + 3] = __float2bfloat16_rn(dout * og * (1.f - og));
+        } else {
+          carry[u] = dhu;  // masked step: (h, c) passed through unchanged
         }
-        {  // exchange copy first: it is on the other CTAs' critical path
-          uint8_t *chunk = dzsw + ((size_t)t * nk + blockIdx.x) * ly.cb;
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            *reinterpret_cast<uint4 *>(chunk + sw128_off(b, k)) = reinterpret_cast<const uint4 *>(dzb)[k];
-        }
-        {  // ldz >= 64 * grid: padding columns get the zeros computed for the padding units
-          uint4 *d4 = reinterpret_cast<uint4 *>(dz);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
-        }
+        if (!valid || u >= nu)
+          dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
       }
-      if (threadIdx.x == 0) PROBE(ti, 6);
+      if (row) {  // critical path first: the exchange copy of dz_t, then the step flag
+        uint8_t *chunk = dzsw + ((size_t)t * nk + blockIdx.x) * ly.cb;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<uint4 *>(chunk + sw128_off(b, k)) = reinterpret_cast<const uint4 *>(dzb)[k];
+      }
       fence_proxy_async_global();
+      if (threadIdx.x == 0) PROBE(ti, 6);
+      epi_publish(&flags[blockIdx.x], (unsigned)(T - t));
+      if (threadIdx.x == 0) PROBE(ti, 7);
+      if (row) {  // ldz >= 64 * grid: padding columns get the zeros computed for the padding units
+        uint4 *d4 = reinterpret_cast<uint4 *>(a.DZ + r * a.ldz + (size_t)blockIdx.x * 64);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
+      }
     }
     if (has_next) ++nmma;
-    tc_fence_before();
-    publish_flag(&flags[blockIdx.x], (unsigned)(T - t));
-    tc_fence_after();
-    if (threadIdx.x == 0) PROBE(ti, 7);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc(tmem, 16 * REC_NMW < 32 ? 32 : 16 * REC_NMW);
 }
 
+// ------------------------------------------------------------------ backward, K-split clusters
+// dh_t = W_hh^T dz_{t+1} has K = 4H: every CTA of the plain backward kernel streams the WHOLE of
+// dz_{t+1} (B x 4H bf16, 328 KB at C2) through shared memory each step and issues 4H/16 MMAs —
+// the step is bound by that stream and by the MMA issue rate. Here a cluster of KS_CL CTAs owns
+// KS_UPC = 64 units; CTA r of the cluster holds W_hh^T[units x K-slice r] and streams only dz
+// columns of K-slice r (1/KS_CL of the data, 1/KS_CL of the MMAs, N = 64). The KS_CL partial dh
+// tiles are exchanged through distributed shared memory: CTA r keeps the 16 units it owns
+// (u0 = 16 * blockIdx.x, the same ownership, dz exchange layout and flags as the plain kernel)
+// and receives their partials from its KS_CL-1 peers, summed in a fixed order (deterministic).
+constexpr int KS_CL = 4;
+constexpr int KS_UPC = 16 * KS_CL;
+constexpr int KS_TILE_BYTES = 64 * REC_UPC * 4;  // one 16-unit tile of partial dh: [row < 64][16] fp32
+// red[parity][sender slot] (peers' tiles) + stage[group] (this CTA's 4 tiles, own one included)
+constexpr int KS_RED_BYTES = (2 * (KS_CL - 1) + KS_CL) * KS_TILE_BYTES;
+
+// Epilogue thread mapping (B <= 64, 128 epilogue threads): thread q owns batch row q % 64 and the
+// 8 units 8 (q / 64) .. +7 of the CTA's 16, so all four epilogue warps share the cell backward
+// (only warps 0-1 can read the TMEM lanes of rows 0-63; they stage the tiles through smem).
+template <bool MASKED>
+__global__ void __launch_bounds__(REC_THREADS, 1)
+    lstm_rec_bwd_ks_kernel(const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,64}
+                           RecBwdArgs a, RecLayout ly, int nk_all) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                              ~uintptr_t(1023));
+  const int nkr = ly.nk, S = ly.nslots;
+  uint8_t *sW = base;
+  uint8_t *sA = sW + ly.wbytes;
+  float *red = reinterpret_cast<float *>(sA + (size_t)S * ly.ch * ly.cb + ly.pad);
+  float *stage = red + 2 * (KS_CL - 1) * 64 * REC_UPC;
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) + KS_RED_BYTES);
+  uint64_t *empty = full + S;
+  uint64_t *tfull = empty + S;
+  uint64_t *wfull = tfull + 1;
+  uint64_t *tempty = wfull + 1;
+  uint64_t *redfull = tempty + 1;  // [2], one per parity
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(redfull + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank(), cl = blockIdx.x / KS_CL;
+  const int s0 = rank * nkr, nks = max(0, min(nkr, nk_all - s0));  // my K-slice of dz chunks
+  RecLayout lyl = ly;
+  lyl.nk = nks;
+  lyl.nops = (nks + ly.ch - 1) / ly.ch;
+  const bool active = (int)blockIdx.x < nk_all;  // owns real units (chunk blockIdx.x exists)
+  const int B = a.B, H = a.H;
+  const int u0 = REC_UPC * blockIdx.x;
+  const int nu = max(0, min(REC_UPC, H - u0));
+  const int ldg = 64 * nk_all;  // G pitch (64 gate columns per 16 units)
+  // epilogue mapping
+  const int eb = threadIdx.x & 63, eh = (threadIdx.x >> 6) & 1;  // row, unit half
+  const int nuh = max(0, min(8, nu - 8 * eh));                     // real units of my half
+  if (a.fail && *a.fail) return;  // uniform: every CTA reads the same flag
+
+  if (threadIdx.x == 128) {
+    tma_prefetch_desc(&tmWT);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
+    mbar_init(tfull, REC_NMW);
+    mbar_init(wfull, 1);
+    mbar_init(tempty, 4);
+    mbar_init(&redfull[0], 1);  // the owner's arrive.expect_tx; the peers' bulk copies complete_tx
+    mbar_init(&redfull[1], 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, 64 * REC_NMW);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync_all();  // peers' barriers are initialised before any bulk copy targets them
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 128 && nks > 0) {
+    mbar_expect_tx(wfull, nks * 8192);
+    for (int j = 0; j < nks; ++j) tma_load_2d(sW + j * 8192, &tmWT, wfull, (s0 + j) * 64, KS_UPC * cl);
+  }
+  const int T = a.T_dev ? *a.T_dev : a.T;
+  const bool row = warp < 4 && eb < B && active;
+  if (MASKED && row) {  // While mode: dz rows beyond the device trip count stay out of the wgrads
+    for (int t = T; t < a.T; ++t)
+      for (int q = 0; q < 4 * nuh; ++q)
+        a.DZ[(size_t)(t * B + eb) * a.ldz + (size_t)blockIdx.x * 64 + 32 * eh + q] = __float2bfloat16_rn(0.f);
+  }
+  const int len_b = (MASKED && row) ? a.lens[eb] : 0;
+  float dcreg[8], carry[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) { dcreg[u] = 0.f; carry[u] = 0.f; }
+  constexpr uint32_t idesc = umma_idesc_bf16(128, 64, 0, 0);
+  const int nacc = min(REC_NMW, nks);
+  if (warp >= 5 && nks > 0) mbar_wait(wfull, 0);
+  unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c has completed
+  uint8_t *dzsw = reinterpret_cast<uint8_t *>(a.DZsw);
+  int nmma = 0;  // steps with a dz_{t+1} operand (tfull / tempty / redfull phase)
+
+  for (int t = T - 1; t >= 0; --t) {
+    const bool has_next = t + 1 < T;
+    const int ti = T - 1 - t;
+    if (warp == 4) {
+      if (has_next && nks > 0) {
+        if (threadIdx.x == 128) PROBE(ti, 0);
+        for (int c = s0 + lane; c < s0 + nks; c += 32) {  // only my K-slice's producers
+          unsigned x;
+          do {
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
+          } while (x < (unsigned)(T - 1 - t));
+        }
+        __syncwarp();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        fence_proxy_async_global();
+        if (threadIdx.x == 128) {
+          PROBE(ti, 1);
+          issue_step(dzsw + ((size_t)(t + 1) * nk_all + s0) * ly.cb, lyl, sA, full, empty, nmma);
+          PROBE(ti, 2);
+        }
+      }
+      __syncwarp();
+    } else if (warp >= 5) {
+      if (has_next && nks > 0 && lane == 0) {
+        mma_step<8192, 64>(lyl, sA, sW, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
+                           (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
+        if (warp == 5) PROBE(ti, 4);
+      }
+      __syncwarp();
+    } else {
+      // per-step operands of my (row, 8 units), independent of dz_{t+1}: load while the MMA runs
+      const size_t r = (size_t)(t * B + (row ? eb : 0));
+      float gt[32], ct[8], cp[8], din[8];
+      {
+        const float *g = a.G + r * ldg + (size_t)blockIdx.x * 64 + 32 * eh;
+        const float *pc = a.Cs + (r + B) * a.ldh + u0 + 8 * eh;
+        const float *pp = a.Cs + r * a.ldh + u0 + 8 * eh;
+        const float *pd = a.dHin + r * a.ldd + u0 + 8 * eh;
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 x = row ? reinterpret_cast<const float4 *>(g)[k] : zero4;
+          gt[4 * k] = x.x; gt[4 * k + 1] = x.y; gt[4 * k + 2] = x.z; gt[4 * k + 3] = x.w;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float4 x = row ? reinterpret_cast<const float4 *>(pc)[k] : zero4;
+          const float4 y = row ? reinterpret_cast<const float4 *>(pp)[k] : zero4;
+          const float4 w = row ? reinterpret_cast<const float4 *>(pd)[k] : zero4;
+          ct[4 * k] = x.x; ct[4 * k + 1] = x.y; ct[4 * k + 2] = x.z; ct[4 * k + 3] = x.w;
+          cp[4 * k] = y.x; cp[4 * k + 1] = y.y; cp[4 * k + 2] = y.z; cp[4 * k + 3] = y.w;
+          din[4 * k] = w.x; din[4 * k + 1] = w.y; din[4 * k + 2] = w.z; din[4 * k + 3] = w.w;
+        }
+      }
+      float dh[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dh[u] = 0.f;
+      if (has_next) {
+        const int par = nmma & 1;
+        if (threadIdx.x == 0) {
+          bulk_wait_group_read0();  // the previous step's stage has been read out by the copies
+          mbar_expect_tx(&redfull[par], (KS_CL - 1) * KS_TILE_BYTES);
+        }
+        if (nks > 0) {
+          mbar_wait(tfull, nmma & 1);
+          if (threadIdx.x == 0) PROBE(ti, 5);
+          __syncwarp();
+          tc_fence_after();
+        }
+        epi_bar();  // stage free
+        if (warp < 2) {  // rows 0-63: sum the accumulator tiles, 16 columns (one group) at a time
+          const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+          for (int p = 0; p < KS_CL; ++p) {
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            for (int w = 0; w < nacc; ++w) {
+              float x[16];
+              tmem_ld16(ta + w * 64 + 16 * p, x);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] += x[i];
+            }
+            float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + threadIdx.x) * REC_UPC);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        }
+        if (nks > 0) epi_tmem_release(tempty);
+        if (threadIdx.x == 0) PROBE(ti, 3);
+        fence_proxy_async_shared();
+        epi_bar();
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int p = 0; p < KS_CL; ++p) {
+            if (p == rank) continue;
+            const int slot = rank < p ? rank : rank - 1;  // my sender slot inside peer p
+            const uint32_t dst = mapa_shared(smem_u32(red + (size_t)(par * (KS_CL - 1) + slot) * 64 * REC_UPC), p);
+            bulk_s2cluster(dst, stage + (size_t)p * 64 * REC_UPC, KS_TILE_BYTES, mapa_shared(smem_u32(&redfull[par]), p));
+          }
+          bulk_commit_group();
+          PROBE(ti, 14);
+        }
+        mbar_wait(&redfull[par], (nmma >> 1) & 1);
+        if (threadIdx.x == 0) PROBE(ti, 15);
+#pragma unroll
+        for (int p = 0; p < KS_CL; ++p) {  // fixed order over the K-slices: deterministic
+          const float *src = p == rank ? stage + (size_t)rank * 64 * REC_UPC
+                                       : red + (size_t)(par * (KS_CL - 1) + (p < rank ? p : p - 1)) * 64 * REC_UPC;
+          const float4 *s4 = reinterpret_cast<const float4 *>(src + (size_t)eb * REC_UPC + 8 * eh);
+          const float4 v0 = s4[0], v1 = s4[1];
+          dh[0] += v0.x; dh[1] += v0.y; dh[2] += v0.z; dh[3] += v0.w;
+          dh[4] += v1.x; dh[5] += v1.y; dh[6] += v1.z; dh[7] += v1.w;
+        }
+      }
+      const bool valid = !MASKED || t < len_b;
+      __align__(16) __nv_bfloat16 dzb[32];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float dhu = dh[u] + din[u] + carry[u];
+        const float ig = gt[4 * u], fg = gt[4 * u + 1], gg = gt[4 * u + 2], og = gt[4 * u + 3];
+        if (valid) {
+          const float tc = tanh_f(ct[u]);
+          const float dout = dhu * tc;
+          const float dc = dcreg[u] + dhu * og * (1.f - tc * tc);
+          const float di = dc * gg, dg = dc * ig, df = dc * cp[u];
+          dcreg[u] = dc * fg;
+          carry[u] = 0.f;
+          dzb[4 * u] = __float2bfloat16_rn(di * ig * (1.f - ig));
+          dzb[4 * u + 1] = __float2bfloat16_rn(df * fg * (1.f - fg));
+          dzb[4 * u + 2] = __float2bfloat16_rn(dg * (1.f - gg * gg));
+          dzb[4 * u + 3] = __float2bfloat16_rn(dout * og * (1.f - og));
+        } else {
+          carry[u] = dhu;
+        }
+        if (!valid || u >= nuh)
+          dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
+      }
+      if (row) {  // exchange copy: row eb, granules 4 eh .. 4 eh + 3 of chunk blockIdx.x
+        uint8_t *chunk = dzsw + ((size_t)t * nk_all + blockIdx.x) * ly.cb;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          *reinterpret_cast<uint4 *>(chunk + sw128_off(eb, 4 * eh + k)) = reinterpret_cast<const uint4 *>(dzb)[k];
+      }
+      fence_proxy_async_global();
+      if (threadIdx.x == 0) PROBE(ti, 6);
+      if (active) epi_publish(&flags[blockIdx.x], (unsigned)(T - t));
+      if (threadIdx.x == 0) PROBE(ti, 7);
+      if (row) {
+        uint4 *d4 = reinterpret_cast<uint4 *>(a.DZ + r * a.ldz + (size_t)blockIdx.x * 64 + 32 * eh);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
+      }
+    }
+    if (has_next) ++nmma;
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer may still address its shared memory
+  if (warp == 5) tmem_dealloc(tmem, 64 * REC_NMW);
+}
+
 // ---------------------------------------------------------------------------------- host
-static RecLayout layout(int wbytes, int nk, int B) {
+static RecLayout layout(int wbytes, int nk, int B, int extra = 0) {
   RecLayout l;
   l.nk = nk;
   l.wbytes = (wbytes + 1023) & ~1023;
   l.bp = (B + 7) & ~7;
   l.cb = l.bp * 128;
-  const int avail = SMEM_BUDGET - l.wbytes - PAD - 1024 /*barriers*/;
+  l.pad = (128 - l.bp) * 128;
+  const int avail = SMEM_BUDGET - l.wbytes - l.pad - extra - 1024 /*barriers*/;
   const int max_chunks = avail / l.cb;  // chunks that fit in flight
   // two ring slots (TMA of op k+1 overlaps the MMAs of op k); a whole step in flight if it fits
   l.nslots = 2;
@@ -501,7 +777,9 @@ static RecLayout layout(int wbytes, int nk, int B) {
   l.nops = (nk + l.ch - 1) / l.ch;
   return l;
 }
-static int smem_of(const RecLayout &l) { return 1024 + l.wbytes + l.nslots * l.ch * l.cb + PAD + 1024; }
+static int smem_of(const RecLayout &l, int extra = 0) {
+  return 1024 + l.wbytes + l.nslots * l.ch * l.cb + l.pad + extra + 1024;
+}
 
 static size_t xchg_block(int cols, int B) { return (size_t)((cols + 63) / 64) * ((B + 7) & ~7) * 128; }
 size_t rec_hsw_bytes(int H, int B, int T) { return (size_t)(T + 1) * xchg_block(H, B); }
@@ -541,13 +819,11 @@ cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw,
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
 
-cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
-                         cudaStream_t st) {
-  if (a.B > 128 || a.B < 1) return cudaErrorInvalidValue;
+static cudaError_t lstm_rec_bwd_plain(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt,
+                                      bool masked, cudaStream_t st) {
   const int nk = (4 * a.H + 63) / 64;
   RecLayout ly = layout(nk * 2048, nk, a.B);
   if (ly.ch < 1 || smem_of(ly) > 232448) return cudaErrorInvalidValue;
-  if (!a.DZsw) return cudaErrorInvalidValue;
   CUtensorMap tmWT;
   if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 16)) return cudaErrorInvalidValue;
   const int smem = smem_of(ly);
@@ -557,6 +833,51 @@ cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldw
   RecBwdArgs aa = a;
   void *args[] = {&tmWT, &aa, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
+}
+
+static cudaError_t lstm_rec_bwd_ks(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
+                                   cudaStream_t st) {
+  const int nk_all = (4 * a.H + 63) / 64;
+  const int nkr = (nk_all + KS_CL - 1) / KS_CL;
+  RecLayout ly = layout(nkr * 8192, nkr, a.B, KS_RED_BYTES);
+  if (ly.ch < 1 || smem_of(ly, KS_RED_BYTES) > 232448) return cudaErrorInvalidValue;
+  CUtensorMap tmWT;
+  if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 64)) return cudaErrorInvalidValue;
+  const int smem = smem_of(ly, KS_RED_BYTES);
+  const void *fn = masked ? (const void *)lstm_rec_bwd_ks_kernel<true> : (const void *)lstm_rec_bwd_ks_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  RecBwdArgs aa = a;
+  int nka = nk_all;
+  void *args[] = {&tmWT, &aa, &ly, &nka};
+  const int grid = KS_CL * ((a.H + KS_UPC - 1) / KS_UPC);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(REC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = KS_CL;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
+                         cudaStream_t st) {
+  if (a.B > 128 || a.B < 1) return cudaErrorInvalidValue;
+  if (!a.DZsw) return cudaErrorInvalidValue;
+  const char *e = getenv("JANUS_REC_BWD");
+  // the K-split kernel exchanges partial tiles of at most 64 batch rows
+  if ((e && e[0] == 'p') || a.B > 64) return lstm_rec_bwd_plain(a, WhhT, ldwt, masked, st);
+  return lstm_rec_bwd_ks(a, WhhT, ldwt, masked, st);
 }
 
 }  // namespace jk

@@ -33,7 +33,7 @@ __global__ void k_mma(int nmma, int reps, int nacc, long long *out) {
   long long t0 = 0, t1 = 0;
   if (UNI && NACC > 100) {  // NACC-100 warps issue concurrently, each into its own accumulator
     const int nw = NACC - 100, w = threadIdx.x >> 5;
-    __shared__ __align__(8) uint64_t bars[4];
+    __shared__ __align__(8) uint64_t bars[8];
     if (threadIdx.x < nw) { mbar_init(&bars[threadIdx.x], 1); }
     fence_barrier_init();
     __syncthreads();
@@ -130,7 +130,8 @@ int main(int argc, char **argv) {
   if (ts == 2) {  // uniform-warp issue variants
     if (N == 256) { run<128, 256, false, true, 1>("US", 1); run<64, 256, false, true, 1>("US", 1); run<128, 256, true, true, 1>("UT", 1); }
     if (N == 64) { run<128, 64, false, true, 101>("MW1", 1); run<128, 64, false, true, 102>("MW2", 2); run<128, 64, false, true, 104>("MW4", 4); }
-    if (N == 16) { run<128, 16, false, true, 101>("MW1", 1); run<128, 16, false, true, 102>("MW2", 2); run<128, 16, false, true, 104>("MW4", 4); }
+    if (N == 16) { run<128, 16, false, true, 104>("MW4", 4); run<64, 16, false, true, 104>("MW4", 4); run<64, 16, false, true, 102>("MW2", 2); }
+    if (N == 32) { run<128, 32, false, true, 104>("MW4", 4); run<64, 32, false, true, 104>("MW4", 4); }
     if (N == 8) { run<64, 8, false, true, 1>("US", 1); run<64, 64, false, true, 1>("US", 1); run<64, 64, true, true, 1>("UT", 1); run<128, 32, false, true, 1>("US", 1); run<128, 128, false, true, 1>("US", 1);}
   }
   return 0;

@@ -10,9 +10,9 @@ from paper_1812_01329_b200 import janus as J
 J.lib.janus_dev_set_probe.restype = C.c_int32
 J.lib.janus_dev_set_probe.argtypes = [C.c_void_p, C.c_void_p]
 B, T, H = 64, 35, 650
-NC = (H + 15) // 16
-NAMES = ["start", "flags_ok", "tma_issued", "-", "mma_issued", "mma_done", "epi_done", "published",
-         "op0_land", "op0_mma", "op1_land", "op1_mma", "op2_land", "op2_mma", "op3_land", "op3_mma"]
+NC = 4 * ((H + 63) // 64)
+NAMES = ["start", "flags_ok", "tma_issued", "tmem_read", "mma_issued", "mma_done", "epi_done", "published",
+         "op0_land", "op0_mma", "op1_land", "op1_mma", "op2_land", "op2_mma", "sent/op3_land", "peers_ok/op3_mma"]
 
 
 def report(buf):
