@@ -18,6 +18,13 @@ int32_t janus_dev_gemm_bf16(int32_t M, int32_t N, int32_t K, const void *A, int3
                             int32_t a_mn, const void *B, int32_t ldb, int32_t b_mn, float *C,
                             int32_t ldc, const float *bias_col, const float *bias_row,
                             int32_t accumulate, void *stream);
+/* Same, with the K dimension split `splits` ways (0 = the library's automatic choice, as in the
+ * step path; 1 = no split). Split partial sums are added in split order (deterministic). Uses a
+ * library-owned device flag buffer: calls must not run concurrently on different streams. */
+int32_t janus_dev_gemm_bf16_splitk(int32_t M, int32_t N, int32_t K, const void *A, int32_t lda,
+                                   int32_t a_mn, const void *B, int32_t ldb, int32_t b_mn, float *C,
+                                   int32_t ldc, const float *bias_col, const float *bias_row,
+                                   int32_t accumulate, int32_t splits, void *stream);
 
 /* Per-phase device timing of janus_run (CUDA events on the launch stream, collected after the
  * step's synchronisation). enable != 0 switches it on and clears the totals. The report is

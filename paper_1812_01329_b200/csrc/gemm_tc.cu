@@ -6,29 +6,88 @@
 //   Either operand may be K-major (K contiguous) or MN-major (M/N contiguous), so wgrad GEMMs
 //   (reduction over the token dimension, dW = dz^T x) read the activations in place.
 //
-// One CTA per 128 x BN output tile, 4 warps: warp0/lane0 issues TMA into a STAGES-deep smem ring
-// (128-B swizzle), warp1/lane0 issues tcgen05.mma (M=128, N=BN, K=16) into a TMEM accumulator,
-// then all 4 warps drain TMEM (tcgen05.ld 32x32b) and store with the fused epilogue.
+// Persistent, warp-specialised kernel, one CTA per SM (grid <= 148), 6 warps:
+//   warp 0 / lane 0 : TMA producer, STAGES-deep smem ring (128-B swizzle), runs across tiles;
+//   warp 1 / lane 0 : tcgen05.mma issuer (M=128, N=BN, K=16) into one of TWO TMEM accumulators,
+//                     so the epilogue of tile i overlaps the mainloop of tile i+1;
+//   warps 2-5       : epilogue, TMEM lanes 32 (w % 4) .. +31 (tcgen05.ld 32x32b) -> fused store.
+// Tiles are 128 x BN output blocks, optionally split along K ("splits") when there are too few
+// tiles to fill the GPU: each split parks its partial tile in scratch, and the LAST split to
+// finish (atomicInc counter, wraps back to 0) adds the partials in split order 0..splits-1 and
+// runs the epilogue — deterministic, and no CTA ever waits for another.
+// Tile t -> (split = t % splits, m-block fastest), CTA c takes t = c, c + grid, ...
+#include <algorithm>
+
 #include "common.cuh"
 #include "gemm_tc.h"
 
 namespace jk {
 
-template <int BN, int A_MN, int B_MN, int STAGES>
+template <int BN, int STAGES>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int THREADS = 192;
 };
 
+struct TileMap {
+  int Mb, Nb, splits, total;
+  JN_DEV void of(int t, int &m_blk, int &n_blk, int &s) const {
+    s = t % splits;
+    const int mn = t / splits;
+    m_blk = mn % Mb;
+    n_blk = mn / Mb;
+  }
+};
+
+// Fused epilogue of 32 consecutive outputs D[m][n .. n+32) of one row (n < N):
+// + bias_row[m] + bias_col[n] (+ old C when accumulating), fp32 and / or bf16 stores.
+JN_DEV void store_row32(const GemmEpilogue &ep, int m, int n, int N, float (&v)[32], const float *, int) {
+  if (ep.bias_row) {
+    const float bv = ep.bias_row[m];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += bv;
+  }
+  if (ep.C) {
+    float *dst = ep.C + (size_t)m * ep.ldc + n;
+    if (n + 32 <= N && (ep.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (ep.bias_col) {
+          const float4 bb = *reinterpret_cast<const float4 *>(ep.bias_col + n + j);
+          o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+        }
+        if (ep.accumulate) {
+          const float4 old = *reinterpret_cast<const float4 *>(dst + j);
+          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        *reinterpret_cast<float4 *>(dst + j) = o;
+      }
+    } else {
+      for (int j = 0; j < 32 && n + j < N; ++j) {
+        float o = v[j] + (ep.bias_col ? ep.bias_col[n + j] : 0.f);
+        if (ep.accumulate) o += dst[j];
+        dst[j] = o;
+      }
+    }
+  }
+  if (ep.Cb) {
+    __nv_bfloat16 *dst = ep.Cb + (size_t)m * ep.ldcb + n;
+    for (int j = 0; j < 32 && n + j < N; ++j)
+      dst[j] = __float2bfloat16_rn(v[j] + (ep.bias_col ? ep.bias_col[n + j] : 0.f));
+  }
+}
+
 template <int BN, int A_MN, int B_MN, int STAGES>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(192, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB, GemmEpilogue ep, int M, int N,
-                        int K, const int *K_dev) {
-  using C = GemmCfg<BN, A_MN, B_MN, STAGES>;
+                        int K, const int *K_dev, TileMap tm, unsigned *counters, float *partials) {
+  using C = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -36,11 +95,11 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t *sB = smem + STAGES * C::A_BYTES;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + STAGES;
-  uint64_t *tfull = empty + STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfull + 1);
+  uint64_t *tfull = empty + STAGES;  // [2]
+  uint64_t *tempty = tfull + 2;      // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * C::BM;
   if (K_dev) K = min(K, *K_dev);  // reduction length known only on the device
   const int nk = (K + C::BK - 1) / C::BK;
 
@@ -51,112 +110,165 @@ __global__ void __launch_bounds__(128, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, BN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES, r = kb / STAGES;
-      if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
-      mbar_expect_tx(&full[s], C::STAGE_BYTES);
-      const int k0 = kb * C::BK;
-      uint8_t *a = sA + s * C::A_BYTES, *b = sB + s * C::B_BYTES;
-      if (!A_MN) {
-        tma_load_2d(a, &tmA, &full[s], k0, m0);
-      } else {
-        tma_load_2d(a, &tmA, &full[s], m0, k0);
-        tma_load_2d(a + 8192, &tmA, &full[s], m0 + 64, k0);
-      }
-      if (!B_MN) {
-        tma_load_2d(b, &tmB, &full[s], k0, n0);
-      } else {
+  if (warp == 0) {  // ---------------- TMA producer (the warp loops together, lane 0 issues)
+    int q = 0;       // ring position, continuous across tiles
+    for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
+      int mb, nb, sp;
+      tm.of(t, mb, nb, sp);
+      const int m0 = mb * C::BM, n0 = nb * BN;
+      const int kb0 = (int)((long long)nk * sp / tm.splits), kb1 = (int)((long long)nk * (sp + 1) / tm.splits);
+      for (int kb = kb0; kb < kb1; ++kb, ++q) {
+        const int s = q % STAGES, r = q / STAGES;
+        if (lane == 0) {
+          if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          const int k0 = kb * C::BK;
+          uint8_t *a = sA + s * C::A_BYTES, *b = sB + s * C::B_BYTES;
+          if (!A_MN) {
+            tma_load_2d(a, &tmA, &full[s], k0, m0);
+          } else {
+            tma_load_2d(a, &tmA, &full[s], m0, k0);
+            tma_load_2d(a + 8192, &tmA, &full[s], m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &tmB, &full[s], k0, n0);
+          } else {
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[s], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[s], n0 + 64 * j, k0);
+          }
+        }
+        __syncwarp();
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
+  } else if (warp == 1) {  // ---------------- MMA issuer (the warp loops together, lane 0 issues)
     constexpr uint32_t idesc = umma_idesc_bf16(128, BN, A_MN, B_MN);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES, r = kb / STAGES;
-      mbar_wait(&full[s], r & 1);
+    int q = 0, i = 0;
+    for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++i) {
+      int mb, nb, sp;
+      tm.of(t, mb, nb, sp);
+      const int kb0 = (int)((long long)nk * sp / tm.splits), kb1 = (int)((long long)nk * (sp + 1) / tm.splits);
+      const int buf = i & 1;
+      if (i >= 2) mbar_wait(&tempty[buf], ((i >> 1) - 1) & 1);  // epilogue drained this buffer
       tc_fence_after();
-      const uint32_t a = smem_u32(sA + s * C::A_BYTES), b = smem_u32(sB + s * C::B_BYTES);
+      const uint32_t acc = tmem + (uint32_t)(buf * BN);
+      for (int kb = kb0; kb < kb1; ++kb, ++q) {
+        const int s = q % STAGES, r = q / STAGES;
+        mbar_wait(&full[s], r & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a = smem_u32(sA + s * C::A_BYTES), b = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
-      for (int j = 0; j < C::BK / 16; ++j) {
-        const uint64_t ad = A_MN ? umma_desc_sw128(a + j * 2048, 8192, 1024)
-                                 : umma_desc_sw128(a + j * 32, 16, 1024);
-        const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
-                                 : umma_desc_sw128(b + j * 32, 16, 1024);
-        umma_bf16(tmem, ad, bd, idesc, (kb | j) != 0);
+          for (int j = 0; j < C::BK / 16; ++j) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a + j * 2048, 8192, 1024)
+                                     : umma_desc_sw128(a + j * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
+                                     : umma_desc_sw128(b + j * 32, 16, 1024);
+            umma_bf16(acc, ad, bd, idesc, (kb != kb0 || j != 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
       }
-      umma_commit(&empty[s]);
+      if (lane == 0) umma_commit(&tfull[buf]);
+      __syncwarp();
     }
-    umma_commit(tfull);
-  }
-
-  // ---------------- epilogue: TMEM -> registers -> global
-  mbar_wait(tfull, 0);
-  __syncwarp();
-  tc_fence_after();
-  const int m = m0 + warp * 32 + lane;
-  const bool row_ok = m < M;
+  } else {
+    // ---------------- epilogue: TMEM -> registers -> global (warps 2-5)
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int i = 0;
+    for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++i) {
+      int mb, nb, sp;
+      tm.of(t, mb, nb, sp);
+      const int m0 = mb * C::BM, n0 = nb * BN;
+      const int kb0 = (int)((long long)nk * sp / tm.splits), kb1 = (int)((long long)nk * (sp + 1) / tm.splits);
+      const bool empty_k = kb1 <= kb0;  // no MMA wrote the accumulator
+      const int buf = i & 1;
+      const int tile = mb + tm.Mb * nb;
+      mbar_wait(&tfull[buf], (i >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      const int m = m0 + quad * 32 + lane;
+      const bool row_ok = m < M;
+      if (tm.splits == 1) {
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
-    const int n = n0 + c * 32;
-    if (n >= N) break;  // warp-uniform
-    float v[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c * 32, v);
-    if (nk == 0) {  // empty reduction: the TMEM accumulator was never written
+        for (int c = 0; c < BN / 32; ++c) {
+          const int n = n0 + c * 32;
+          if (n >= N) break;  // warp-uniform
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * BN + c * 32, v);
+          if (empty_k) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = 0.f;
-    }
-    if (!row_ok) continue;
-    if (ep.bias_row) {
-      const float bv = ep.bias_row[m];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += bv;
-    }
-    if (ep.C) {
-      float *dst = ep.C + (size_t)m * ep.ldc + n;
-      if (n + 32 <= N && (ep.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          if (ep.bias_col) {
-            const float4 bb = *reinterpret_cast<const float4 *>(ep.bias_col + n + j);
-            o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
           }
-          if (ep.accumulate) {
-            const float4 old = *reinterpret_cast<const float4 *>(dst + j);
-            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-          }
-          *reinterpret_cast<float4 *>(dst + j) = o;
+          if (row_ok) store_row32(ep, m, n, N, v, nullptr, 0);
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
       } else {
-        for (int j = 0; j < 32 && n + j < N; ++j) {
-          float o = v[j] + (ep.bias_col ? ep.bias_col[n + j] : 0.f);
-          if (ep.accumulate) o += dst[j];
-          dst[j] = o;
+        // split-K: park this split's partial tile; the last split to arrive adds the splits in
+        // order 0 .. splits-1 (deterministic) and runs the epilogue
+        float *pt = partials + ((size_t)tile * tm.splits + sp) * (128 * BN);
+        const int rl = quad * 32 + lane;  // tile-local row
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * BN + c * 32, v);
+          if (empty_k) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          }
+          float4 *d4 = reinterpret_cast<float4 *>(pt + (size_t)rl * BN + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        __shared__ unsigned s_last;
+        if (warp == 2 && lane == 0) s_last = atomicInc(&counters[tile], (unsigned)tm.splits - 1) == (unsigned)tm.splits - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          const float *p0 = partials + (size_t)tile * tm.splits * (128 * BN) + (size_t)rl * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            const int n = n0 + c * 32;
+            if (n >= N) break;
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            for (int q = 0; q < tm.splits; ++q) {
+              const float4 *s4 = reinterpret_cast<const float4 *>(p0 + (size_t)q * (128 * BN) + c * 32);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 x = __ldcg(s4 + j);
+                v[4 * j] += x.x; v[4 * j + 1] += x.y; v[4 * j + 2] += x.z; v[4 * j + 3] += x.w;
+              }
+            }
+            if (row_ok) store_row32(ep, m, n, N, v, nullptr, 0);
+          }
         }
       }
-    }
-    if (ep.Cb) {
-      __nv_bfloat16 *dst = ep.Cb + (size_t)m * ep.ldcb + n;
-      for (int j = 0; j < 32 && n + j < N; ++j)
-        dst[j] = __float2bfloat16_rn(v[j] + (ep.bias_col ? ep.bias_col[n + j] : 0.f));
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, BN);
+  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -212,10 +324,26 @@ bool make_tmap_bf16_chunks(CUtensorMap *m, const void *ptr, uint64_t rows, uint6
   return r == CUDA_SUCCESS;
 }
 
+static int g_num_sms = 0;
+
+// K splits: the fewest persistent rounds per unit of work, each split >= 4 k-blocks, and the
+// partial tiles must fit the caller's scratch
+static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
+  // partial tiles cost a write + read of 128 x BN fp32 each: only long reductions gain
+  if (tiles >= nsm || nk < 64) return 1;
+  int best = 1;
+  double best_cost = (double)((tiles + nsm - 1) / nsm);
+  for (int s = 2; s <= 8 && nk / s >= 4 && (size_t)tiles * s <= cap_tiles; ++s) {
+    const double cost = (double)((tiles * s + nsm - 1) / nsm) / s + 0.08 * s;  // + partial traffic
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = s; }
+  }
+  return best;
+}
+
 template <int BN, int A_MN, int B_MN>
 static cudaError_t launch(const GemmOp &op, cudaStream_t st) {
-  constexpr int STAGES = BN == 256 ? 4 : 5;
-  using C = GemmCfg<BN, A_MN, B_MN, STAGES>;
+  constexpr int STAGES = BN == 256 ? 4 : 6;
+  using C = GemmCfg<BN, STAGES>;
   CUtensorMap ta, tb;
   bool ok = A_MN ? make_tmap_bf16(&ta, op.A, op.M, op.K, op.lda, 64)
                  : make_tmap_bf16(&ta, op.A, op.K, op.M, op.lda, 128);
@@ -229,8 +357,27 @@ static cudaError_t launch(const GemmOp &op, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((op.N + BN - 1) / BN, (op.M + 127) / 128);
-  kern<<<grid, 128, C::SMEM, st>>>(ta, tb, op.ep, op.M, op.N, op.K, op.K_dev);
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  TileMap tm;
+  tm.Mb = (op.M + 127) / 128;
+  tm.Nb = (op.N + BN - 1) / BN;
+  const int nk = (op.K + 63) / 64;
+  const size_t cap_tiles = op.partials ? op.partials_cap / (128 * BN) : 0;
+  int splits = 1;
+  if (op.flags && op.partials) {
+    splits = op.splits > 0 ? op.splits : choose_splits(tm.Mb * tm.Nb, nk, g_num_sms, cap_tiles);
+    splits = std::max(1, std::min(splits, 64));
+    if ((size_t)tm.Mb * tm.Nb * splits > cap_tiles) splits = 1;
+  }
+  tm.splits = splits;
+  tm.total = tm.Mb * tm.Nb * splits;
+  const int grid = std::min(tm.total, g_num_sms);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, op.ep, op.M, op.N, op.K, op.K_dev, tm, op.flags, op.partials);
   return cudaGetLastError();
 }
 
@@ -239,7 +386,10 @@ cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st) {
   if ((op.lda & 7) || (op.ldb & 7) || (reinterpret_cast<uintptr_t>(op.A) & 15) ||
       (reinterpret_cast<uintptr_t>(op.B) & 15))
     return cudaErrorInvalidValue;
-  const bool wide = op.N >= 1024;  // BN = 256 for wide outputs (decoder), 128 otherwise
+  // BN = 256 for wide outputs (one tcgen05.mma issue costs ~130 cycles whatever N is, see
+  // scripts/bench_mma.cu, so wide tiles keep the tensor pipe busiest); narrow outputs (N ~ H)
+  // take BN = 128 for twice the tiles
+  const bool wide = op.N >= 1024;
 #define JN_G(BN_, AM, BMJ) return launch<BN_, AM, BMJ>(op, st)
   if (wide) {
     if (!op.a_mn && !op.b_mn) JN_G(256, 0, 0);
@@ -254,5 +404,7 @@ cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st) {
   }
 #undef JN_G
 }
+
+size_t gemm_flags_count(int M, int N) { return (size_t)((M + 127) / 128) * ((N + 127) / 128); }
 
 }  // namespace jk

@@ -29,9 +29,18 @@ struct GemmOp {
   int ldb = 0, b_mn = 0;
   GemmEpilogue ep;
   const int *K_dev = nullptr;  // optional device-resident K (<= K): data-dependent reductions
+  // split-K (deterministic: partials added in split order): `flags` = gemm_flags_count(M, N)
+  // ZERO-INITIALISED counters (every launch leaves them zero again) and `partials` = fp32
+  // scratch of partials_cap floats, both private to the stream; null disables splitting.
+  // splits: 0 = automatic, >= 1 forces the count (capped by the scratch).
+  unsigned *flags = nullptr;
+  float *partials = nullptr;
+  size_t partials_cap = 0;
+  int splits = 0;
 };
 
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);
+size_t gemm_flags_count(int M, int N);  // flags needed by a split-K launch of an M x N GEMM
 bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_outer);
 bool make_tmap_bf16_chunks(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t ld,

@@ -37,7 +37,7 @@ struct LmPlan {
     size_t X = 0, Hs[4], Cs[4], G[4], DZ[4], dX[4], Hsw[4], DZsw[4];
     size_t logits = 0, dy = 0, rowloss = 0, dHtop = 0, hT[4], cT[4];
     size_t gWih[4], gWhh[4], gWdec = 0;
-    size_t seg_word = 0, seg_grad = 0, nseg = 0, ehist = 0;
+    size_t seg_word = 0, seg_grad = 0, nseg = 0, ehist = 0, gflags = 0, gpart = 0;
     size_t small_ws = 0;
     size_t arena_begin = 0, arena_end = 0, dEd = 0, dp_scratch = 0;
   } off;
@@ -119,6 +119,7 @@ struct Graph {
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
   std::string describe;
+  const void *gflags_ws = nullptr;        // workspace whose split-K counters were zeroed
   unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*16*T u64)
 };
 

@@ -26,6 +26,8 @@
 
 namespace jk {
 
+static constexpr int GEMM_PART_TILES = 320;  // split-K scratch: 320 partial 128 x 256 fp32 tiles
+
 static int r8(int x) { return (x + 7) & ~7; }
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -241,6 +243,11 @@ bool lower_lm(Graph &g, std::string &why) {
     p.off.seg_grad = take(TB * p.Ep * 4);
     p.off.nseg = take(16);
     p.off.ehist = take((size_t)V * 4);
+    {  // split-K GEMM flags (one region: the step's GEMMs run in stream order)
+      const int mx = std::max({(int)TB, V, G4, p.Ep, p.Hp + 1});
+      p.off.gflags = take(gemm_flags_count(mx, mx) * 4);
+      p.off.gpart = take((size_t)GEMM_PART_TILES * 128 * 256 * 4);
+    }
   }
   p.ws_bytes = o;
   char buf[512];
@@ -412,6 +419,19 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   const int *Tdev = p.while_mode ? &dst->trip : nullptr;
   auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16 *>(W + off); };
   auto fp = [&](size_t off) { return reinterpret_cast<float *>(W + off); };
+  unsigned *gflags = reinterpret_cast<unsigned *>(W + p.off.gflags);
+  if (g.gflags_ws != W) {  // counters start at zero; every GEMM launch leaves them at zero
+    const int mx = std::max({B * p.T, V, 4 * H, p.Ep, p.Hp + 1});
+    if (cudaMemsetAsync(gflags, 0, gemm_flags_count(mx, mx) * 4, st) != cudaSuccess) return JANUS_ERR_CUDA;
+    g.gflags_ws = W;
+  }
+  float *gpart = reinterpret_cast<float *>(W + p.off.gpart);
+  auto with_flags = [&](GemmOp o) {
+    o.flags = gflags;
+    o.partials = gpart;
+    o.partials_cap = (size_t)GEMM_PART_TILES * 128 * 256;
+    return o;
+  };
   LCHK("init", launch_step_init(dst, bars, p.nbar, st));
   if (p.while_mode) LCHK("trip", launch_trip(P.lens, B, Tw, dst, st));
   if (gl.n) LCHK("guards", launch_guards(gl, dst, st));
@@ -434,7 +454,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
     op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
     op.ep.C = fp(p.off.G[l]); op.ep.ldc = p.Gz; op.ep.bias_col = fp(p.off.bil[l]);
-    LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(op, st));
+    LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(with_flags(op), st));
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
     ra.Hsw = bf(p.off.Hsw[l]);
@@ -451,7 +471,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.A = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.lda = Hp;
     op.B = bf(p.off.Wdec_b); op.ldb = Hp;
     op.ep.C = fp(p.off.logits); op.ep.ldc = Vp; op.ep.bias_col = P.bdec;
-    LCHK("gemm_dec", gemm_bf16(op, st));
+    LCHK("gemm_dec", gemm_bf16(with_flags(op), st));
   }
   LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
                    (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
@@ -461,13 +481,13 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.A = bf(p.off.dy); op.lda = Vp; op.a_mn = 1;
     op.B = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.ldb = Hp; op.b_mn = 1;
     op.ep.C = fp(p.off.gWdec); op.ep.ldc = Hp;
-    LCHK("gemm_dWdec", gemm_bf16(op, st));
+    LCHK("gemm_dWdec", gemm_bf16(with_flags(op), st));
     GemmOp o2;  // dh_top = dy W_dec
     o2.M = TB; o2.N = H; o2.K = V;
     o2.A = bf(p.off.dy); o2.lda = Vp;
     o2.B = bf(p.off.Wdec_b); o2.ldb = Hp; o2.b_mn = 1;
     o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
-    LCHK("gemm_dh", gemm_bf16(o2, st));
+    LCHK("gemm_dh", gemm_bf16(with_flags(o2), st));
   }
   for (int l = L - 1; l >= 0; --l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
@@ -485,20 +505,20 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     a.A = bf(p.off.DZ[l]); a.lda = p.Gz; a.a_mn = 1;
     a.B = bf(p.off.Hs[l]); a.ldb = Hp; a.b_mn = 1;
     a.ep.C = fp(p.off.gWhh[l]); a.ep.ldc = Hp;
-    LCHK(l ? "gemm_dWhh1" : "gemm_dWhh0", gemm_bf16(a, st));
+    LCHK(l ? "gemm_dWhh1" : "gemm_dWhh0", gemm_bf16(with_flags(a), st));
     GemmOp b2;  // dW_ih | db = dz^T [x | 1]
     b2.M = G4; b2.N = In + 1; b2.K = TB;
     b2.A = bf(p.off.DZ[l]); b2.lda = p.Gz; b2.a_mn = 1;
     b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
     b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
-    LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(b2, st));
+    LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(with_flags(b2), st));
     if (l > 0 || p.lr_E != 0) {
       GemmOp c2;  // dx = dz W_ih
       c2.M = TB; c2.N = In; c2.K = G4;
       c2.A = bf(p.off.DZ[l]); c2.lda = p.Gz;
       c2.B = bf(p.off.Wih_b[l]); c2.ldb = Inp; c2.b_mn = 1;
       c2.ep.C = fp(p.off.dX[l]); c2.ep.ldc = Inp;
-      LCHK(l ? "gemm_dx1" : "gemm_dx0", gemm_bf16(c2, st));
+      LCHK(l ? "gemm_dx1" : "gemm_dx0", gemm_bf16(with_flags(c2), st));
     }
   }
   int *seg_word = reinterpret_cast<int *>(W + p.off.seg_word);

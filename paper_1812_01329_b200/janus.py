@@ -58,12 +58,15 @@ lib = C.CDLL(LIB_PATH)
 EXPORTS = ["janus_graph_build", "janus_workspace_bytes", "janus_run", "janus_run_imperative",
            "janus_counters", "janus_describe", "janus_graph_destroy", "janus_status_str",
            "janus_abi_version"]
-DEV_EXPORTS = ["janus_dev_gemm_bf16"]
+DEV_EXPORTS = ["janus_dev_gemm_bf16", "janus_dev_gemm_bf16_splitk"]
 
 _P = C.c_void_p
 for _name, _res, _args in [
     ("janus_dev_gemm_bf16", C.c_int32, [C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P,
                                         C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, C.c_int32, _P]),
+    ("janus_dev_gemm_bf16_splitk", C.c_int32, [C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P,
+                                               C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, C.c_int32,
+                                               C.c_int32, _P]),
 ]:
     if hasattr(lib, _name):
         f = getattr(lib, _name)
@@ -86,6 +89,15 @@ def dev_gemm_bf16(M, N, K, A, lda, a_mn, B, ldb, b_mn, Cout, ldc, bias_col=None,
                                 ldc, _ptr(bias_col), _ptr(bias_row), int(accumulate), _stream(stream))
     if r != 0:
         raise RuntimeError(f"janus_dev_gemm_bf16 failed with cuda error {r}")
+
+
+def dev_gemm_bf16_splitk(M, N, K, A, lda, a_mn, B, ldb, b_mn, Cout, ldc, bias_col=None, bias_row=None,
+                         accumulate=False, splits=0, stream=None):
+    r = lib.janus_dev_gemm_bf16_splitk(M, N, K, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn), _ptr(Cout),
+                                       ldc, _ptr(bias_col), _ptr(bias_row), int(accumulate), int(splits),
+                                       _stream(stream))
+    if r != 0:
+        raise RuntimeError(f"janus_dev_gemm_bf16_splitk failed with cuda error {r}")
 
 
 # ----------------------------------------------------------------------------------- step ABI

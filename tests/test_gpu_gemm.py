@@ -8,7 +8,7 @@ pytestmark = pytest.mark.gpu
 from oracle.numerics import rb  # noqa: E402
 
 
-def _run(M, N, K, a_mn, b_mn, bias=None, acc=False, seed=0):
+def _run(M, N, K, a_mn, b_mn, bias=None, acc=False, seed=0, splits=None, ret_out=False):
     from paper_1812_01329_b200 import janus as J
     g = np.random.default_rng(seed)
     A = rb(g.uniform(-1, 1, (M, K)))
@@ -33,7 +33,10 @@ def _run(M, N, K, a_mn, b_mn, bias=None, acc=False, seed=0):
     dC = torch.tensor(C0, dtype=torch.float32, device="cuda")
     bcol = torch.tensor(g.uniform(-1, 1, N), dtype=torch.float32, device="cuda") if bias == "col" else None
     brow = torch.tensor(g.uniform(-1, 1, M), dtype=torch.float32, device="cuda") if bias == "row" else None
-    J.dev_gemm_bf16(M, N, K, dA, lda, a_mn, dB, ldb, b_mn, dC, ldc, bcol, brow, acc)
+    if splits is None:
+        J.dev_gemm_bf16(M, N, K, dA, lda, a_mn, dB, ldb, b_mn, dC, ldc, bcol, brow, acc)
+    else:
+        J.dev_gemm_bf16_splitk(M, N, K, dA, lda, a_mn, dB, ldb, b_mn, dC, ldc, bcol, brow, acc, splits)
     torch.cuda.synchronize()
     ref = A @ B.T
     if bcol is not None:
@@ -44,7 +47,7 @@ def _run(M, N, K, a_mn, b_mn, bias=None, acc=False, seed=0):
         ref += np.asarray(C0, np.float32)[:, :N]
     got = dC.cpu().double().numpy()[:, :N]
     err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
-    return err
+    return (err, got) if ret_out else err
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
@@ -56,3 +59,24 @@ def test_gemm_layouts(M, N, K, a_mn, b_mn):
 def test_gemm_bias_and_accumulate():
     assert _run(333, 260, 130, 0, 0, bias="col") < 1e-5
     assert _run(333, 260, 130, 0, 1, bias="row", acc=True) < 1e-5
+
+
+@pytest.mark.parametrize("splits", [0, 1, 2, 3, 5])
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [(2240, 650, 10000, 0, 1), (2600, 651, 2240, 1, 1), (200, 136, 650, 0, 0)])
+def test_gemm_splitk(M, N, K, a_mn, b_mn, splits):
+    """K split across CTAs, partial sums added in split order (SURVEY §8(a) H10 dgrad/wgrad)."""
+    # fp32 accumulation over K = 10^4 terms: the error bound grows with K
+    assert _run(M, N, K, a_mn, b_mn, splits=splits) < 1e-5 * max(1.0, K / 4096)
+
+
+def test_gemm_splitk_bias_accumulate_and_empty_splits():
+    # bias and the old C enter exactly once; more splits than k-blocks leaves empty splits
+    assert _run(333, 260, 130, 0, 0, bias="col", acc=True, splits=4) < 1e-5
+    assert _run(333, 260, 130, 0, 1, bias="row", acc=True, splits=3) < 1e-5
+    assert _run(130, 300, 64, 0, 0, bias="col", splits=4) < 1e-5
+
+
+def test_gemm_splitk_deterministic():
+    e1, o1 = _run(2240, 650, 10000, 0, 1, splits=4, ret_out=True)
+    e2, o2 = _run(2240, 650, 10000, 0, 1, splits=4, ret_out=True)
+    assert e1 < 1e-5 and np.array_equal(o1, o2)
