@@ -379,16 +379,45 @@ def main():
         fl = gemm_flops(name, 10000, 650, 650, TB)
         rows.append((tot_ms / args.steps, name, cnt // args.steps, fl))
     rows.sort(reverse=True)
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    peak_src = pk["source"] + " bf16_tflops_sustained (kernels timed inside the step)"
+    ncu = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            ncu = json.load(f)
+    except (OSError, ValueError):
+        pass
+
+    def traffic(key):
+        d = ncu.get(key)
+        return None if not d else d["dram_read_bytes"] + d["dram_write_bytes"]
+
+    # the dominant kernel of the step: the backward recurrence (two launches, one per layer).
+    # Algorithmic tensor work per launch: the (T-1) recurrent products dh_t = W_hh^T dz_{t+1},
+    # 2 * B * 4H * H flops each; the launch is latency-bound (T dependent steps), see DESIGN.md.
+    rec = [r for r in rows if r[1].startswith("rec_bwd")]
+    rec_ms = sum(r[0] for r in rec)
+    rec_n = sum(r[2] for r in rec)
+    rec_avg = rec_ms / max(1, rec_n)
+    rec_fl = 2.0 * B * 4 * 650 * 650 * (T - 1)
+    rec_ach = rec_fl / (rec_avg * 1e-3) / 1e12 if rec_avg else None
+    roofline = {"kernel": "rec_bwd (lstm_rec_bwd_ks_kernel, K-split clusters)", "bound": "tensor",
+                "achieved": rec_ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": rec_ach / peak if rec_ach else None, "traffic": traffic("rec_bwd"),
+                "flops_per_launch": rec_fl, "avg_launch_ms": rec_avg,
+                "step_period_us": rec_avg * 1000.0 / T,
+                "peak_source": peak_src, "share_of_step": rec_ms / step_ms if step_ms else None,
+                "traffic_source": "profiles/r1_ncu_traffic.json (ncu --set full, dram read+write per launch)",
+                "note": "latency-bound: T=35 dependent steps per launch; the step period is the bound, not the tensor pipe"}
     gemms = [r for r in rows if r[3]]
     top = gemms[0] if gemms else rows[0]
     avg_ms = top[0] / max(1, top[2])
     achieved = top[3] / (avg_ms * 1e-3) / 1e12 if top[3] else None
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    roofline = {"kernel": top[1], "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak if achieved else None, "traffic": None,
-                "flops_per_launch": top[3], "avg_launch_ms": avg_ms,
-                "peak_source": pk["source"] + " bf16_tflops_sustained (kernel timed inside the step)",
-                "share_of_step": top[0] / step_ms if step_ms else None}
+    roofline_gemm = {"kernel": top[1], "bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak if achieved else None,
+                     "traffic": traffic("gemm_dec") if top[1] == "gemm_dec" else None,
+                     "flops_per_launch": top[3], "avg_launch_ms": avg_ms, "peak_source": peak_src,
+                     "share_of_step": top[0] / step_ms if step_ms else None}
     flops = lm_flops_per_sample(10000, 650, 650, 2, T) * B
     out = {
         "metric": BASELINE_METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
@@ -401,7 +430,7 @@ def main():
         "step_tflops": flops * world / (ms_step * 1e-3) / 1e12 / world,
         "step_flop_frac_of_sustained": flops / (ms_step * 1e-3) / 1e12 / peak,
         "e2e": e2e, "gpu_launches": int(launches), "host_syncs_per_step": syncs,
-        "roofline": roofline,
+        "roofline": roofline, "roofline_gemm": roofline_gemm,
         "phases_ms_per_step": {r[1]: round(r[0], 4) for r in rows},
         "paper_context": "JANUS LSTM (PTB, BS 20) 22.06k words/s on 1 TITAN Xp, fp32 (P:363) — other hardware/config",
     }
