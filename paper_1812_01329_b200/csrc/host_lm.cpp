@@ -447,23 +447,36 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   LCHK("cast", launch_cast_rows(P.Wdec, V, H, H, bf(p.off.Wdec_b), Hp, 0, st));
   LCHK("gather", launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
   // forward
-  for (int l = 0; l < L; ++l) {
-    const int In = l ? H : E, Inp = l ? Hp : Ep;
-    GemmOp op;
-    op.M = TB; op.N = G4; op.K = In;
-    op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
-    op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
-    op.ep.C = fp(p.off.G[l]); op.ep.ldc = p.Gz; op.ep.bias_col = fp(p.off.bil[l]);
-    LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(with_flags(op), st));
+  // two layers: one wavefront launch (layer 1 one step behind layer 0, its input projection
+  // fused into the recurrent MMA) unless disabled or too wide for one CTA per SM
+  const char *wf_env = getenv("JANUS_REC_WF");
+  const bool wavefront = L == 2 && !(wf_env && wf_env[0] == '0') && rec_fwd_wf_grid(H) <= 148;
+  auto rec_args = [&](int l) {
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
     ra.Hsw = bf(p.off.Hsw[l]);
     ra.G = fp(p.off.G[l]); ra.Hs = bf(p.off.Hs[l]); ra.Cs = fp(p.off.Cs[l]); ra.ldh = Hp;
     ra.h0 = P.h[l]; ra.c0 = P.c[l]; ra.hT = fp(p.off.hT[l]); ra.cT = fp(p.off.cT[l]);
     ra.barrier = bars + 256 * l; ra.fail = nullptr;
-    ra.dbg = l == 0 ? g.probe : nullptr;
+    ra.dbg = (l == 0 || wavefront) ? g.probe : nullptr;  // indexed by the launch's CTA index
     ra.tag = p.tag_specialised ? nullptr : P.tag;
-    LCHK(l ? "rec_fwd1" : "rec_fwd0", lstm_rec_fwd(ra, bf(p.off.Whh_b[l]), Hp, p.while_mode, st));
+    return ra;
+  };
+  for (int l = 0; l < L; ++l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    if (wavefront && l == 1) break;
+    GemmOp op;
+    op.M = TB; op.N = G4; op.K = In;
+    op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
+    op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
+    op.ep.C = fp(p.off.G[l]); op.ep.ldc = p.Gz; op.ep.bias_col = fp(p.off.bil[l]);
+    LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(with_flags(op), st));
+    if (wavefront) {
+      LCHK("rec_fwd01", lstm_rec_fwd_wavefront(rec_args(0), rec_args(1), bf(p.off.Whh_b[0]), bf(p.off.Wih_b[1]),
+                                               bf(p.off.Whh_b[1]), Hp, fp(p.off.bil[1]), p.while_mode, st));
+    } else {
+      LCHK(l ? "rec_fwd1" : "rec_fwd0", lstm_rec_fwd(rec_args(l), bf(p.off.Whh_b[l]), Hp, p.while_mode, st));
+    }
   }
   {
     GemmOp op;  // decoder logits

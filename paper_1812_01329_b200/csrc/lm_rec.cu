@@ -82,7 +82,8 @@ JN_DEV void epi_tmem_release(uint64_t *tempty) {
 }
 
 struct RecLayout {
-  int nk;       // 64-column chunks of the streamed operand per step
+  int nk;       // 64-column chunks of the streamed operand per step (run A, then run B)
+  int nka;      // chunks of run A (the wavefront kernel's layer-1 CTAs stream two exchange blocks)
   int wbytes;   // resident weight slice bytes (1 KB aligned)
   int cb;       // bytes per chunk in smem = Bp * 128 (Bp = B rounded up to 8)
   int bp;       // rows per chunk fetched
@@ -112,29 +113,45 @@ JN_DEV void write_xchg(uint8_t *xbuf, int blk, int nk, int cb, int u0, int b,
   *reinterpret_cast<uint4 *>(chunk + sw128_off(b, g0 + 1)) = reinterpret_cast<const uint4 *>(hb)[1];
 }
 
-// Producer (warp 4, lane 0): op k of step `st` copies chunks [k*ch, k*ch + ch) of the step's
-// exchange block (already in the swizzled shared-memory layout, contiguous) into ring slot
-// (st*nops + k) % nslots with one bulk copy.
-JN_DEV void issue_step(const uint8_t *src, const RecLayout &ly, uint8_t *sA, uint64_t *full,
-                       uint64_t *empty, int st) {
+// Ops of a step: run A's chunks [0, nka) in ops of up to ch chunks, then run B's [nka, nk).
+JN_DEV int ops_a(const RecLayout &ly) { return (ly.nka + ly.ch - 1) / ly.ch; }
+JN_DEV void op_range(const RecLayout &ly, int k, int &first, int &n) {
+  const int oa = ops_a(ly);
+  if (k < oa) {
+    first = k * ly.ch;
+    n = min(ly.ch, ly.nka - first);
+  } else {
+    first = ly.nka + (k - oa) * ly.ch;
+    n = min(ly.ch, ly.nk - first);
+  }
+}
+
+// Producer (warp 4, lane 0): op k of step `st` copies its chunks of the step's exchange block(s)
+// (already in the swizzled shared-memory layout, contiguous) into ring slot (st*nops + k) %
+// nslots with one bulk copy. srcA holds chunks [0, nka), srcB chunks [nka, nk).
+JN_DEV void issue_step(const uint8_t *srcA, const uint8_t *srcB, const RecLayout &ly, uint8_t *sA,
+                       uint64_t *full, uint64_t *empty, int st) {
   for (int k = 0; k < ly.nops; ++k) {
     const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
     if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
-    const int nch = min(ly.ch, ly.nk - k * ly.ch);
+    int first, nch;
+    op_range(ly, k, first, nch);
+    const uint8_t *src = first < ly.nka ? srcA + (size_t)first * ly.cb : srcB + (size_t)(first - ly.nka) * ly.cb;
     mbar_expect_tx(&full[s], nch * ly.cb);
-    bulk_load(sA + (size_t)s * ly.ch * ly.cb, src + (size_t)k * ly.ch * ly.cb, nch * ly.cb, &full[s]);
+    bulk_load(sA + (size_t)s * ly.ch * ly.cb, src, nch * ly.cb, &full[s]);
   }
 }
 
 // MMA issuers (warps 5 .. 5+REC_NMW-1, lane 0 each). A single issuing warp sustains only about
 // one tcgen05.mma per ~130 cycles whatever N is (measured: scripts/bench_mma.cu), and the
-// recurrent MMAs are small (N = 64 / 16), so the step's K chunks are dealt round-robin to REC_NMW
-// warps, each accumulating into its own TMEM tile (columns w * NCOL); the epilogue sums the tiles.
-// Warp w: D_w = sum over chunks j = w (mod REC_NMW) of A_j . W_j^T.
-template <int WCHUNK, int NCOL>
-JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *full, uint64_t *empty,
-                     uint64_t *tfull, uint64_t *tempty, uint32_t tmem, uint32_t idesc, int st, int w,
-                     unsigned long long *pr) {
+// recurrent MMAs are small (N = 64 / 32 / 16), so the step's K chunks are dealt round-robin to
+// REC_NMW warps, each accumulating into its own TMEM tile (columns w * NCOL); the epilogue sums
+// the tiles. Warp w: D_w = sum over chunks j = w (mod REC_NMW) of A_j . W_j^T (W chunk j at
+// sW + j * wchunk bytes).
+template <int NCOL>
+JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, int wchunk, uint64_t *full,
+                     uint64_t *empty, uint64_t *tfull, uint64_t *tempty, uint32_t tmem, uint32_t idesc,
+                     int st, int w, unsigned long long *pr) {
   const uint32_t acc = tmem + (uint32_t)(w * NCOL);
   for (int k = 0; k < ly.nops; ++k) {
     const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
@@ -142,12 +159,13 @@ JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *fu
     mbar_wait(&full[s], r & 1);
     if (pr && k < 4) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pr[8 + 2 * k]));
     tc_fence_after();
+    int first, nch;
+    op_range(ly, k, first, nch);
     const uint32_t sa = smem_u32(sA + (size_t)s * ly.ch * ly.cb);
-    for (int c = 0; c < ly.ch; ++c) {
-      const int j = k * ly.ch + c;
-      if (j >= ly.nk) break;
+    for (int c = 0; c < nch; ++c) {
+      const int j = first + c;
       if (j % REC_NMW != w) continue;
-      const uint32_t ca = sa + c * ly.cb, cw = smem_u32(sW + j * WCHUNK);
+      const uint32_t ca = sa + c * ly.cb, cw = smem_u32(sW + (size_t)j * wchunk);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         umma_bf16(acc, umma_desc_sw128(ca + kk * 32, 16, 1024), umma_desc_sw128(cw + kk * 32, 16, 1024),
@@ -160,10 +178,42 @@ JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, uint64_t *fu
 }
 
 // ---------------------------------------------------------------------------------- forward
-template <bool MASKED>
-__global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmW,  // W_hh interleaved [4H x H], box {64,64}
-                        RecFwdArgs a, RecLayout ly) {
+// One forward recurrence role: a CTA owning UPC units (4 UPC gate-interleaved rows) of one layer.
+// Single-layer launch: every CTA streams its own layer's h_{t-1} (run A). Wavefront launch (two
+// layers in one kernel): layer-1 CTAs compute W_ih1 h0_t + W_hh1 h1_{t-1} in one accumulation —
+// run A = layer 0's exchange block t+1 (h0_t), run B = their own block t (h1_{t-1}) — so layer 1's
+// step t runs concurrently with layer 0's step t+1 and no input-projection GEMM is needed.
+struct FwdCtx {
+  RecFwdArgs a;                  // this layer's buffers; a.barrier = this layer's step flags
+  const __nv_bfloat16 *hswA;     // run-A exchange buffer (own Hsw, or the layer below's)
+  int blkA_off;                  // run-A block = t + blkA_off
+  const unsigned int *flagsA;    // producers of run A: wait flagsA[i] >= t + 1 + blkA_off
+  int nflagsA;
+  const unsigned int *flagsB;    // producers of run B (own layer): wait flagsB[i] >= t + 1
+  int nflagsB;
+  const float *bias;             // gate-interleaved bias (z init) when G is not pre-filled
+  int cta;                       // CTA index within the layer
+};
+
+JN_DEV void wait_flag_set(const unsigned int *flags, int n, unsigned int v) {
+  const int lane = threadIdx.x & 31;
+  for (int c = lane; c < n; c += 32) {
+    unsigned x;
+    do {
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
+    } while (x < v);
+  }
+}
+
+// M64 (B <= 64): M = 64 MMAs — half the A-operand shared-memory reads of M = 128, whose upper 64
+// rows would be padding. The accumulator row i then sits in TMEM lane (i % 16) + 32 (i / 16):
+// epilogue warp w, lanes 0-15 own batch rows 16 w .. 16 w + 15.
+template <int UPC, bool MASKED, bool M64>
+JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMap *tmWb,
+                     const RecLayout &ly) {
+  constexpr int NG = 4 * UPC;           // gate rows / MMA N / TMEM columns per accumulator
+  constexpr int WCH = NG * 128;         // bytes per weight chunk
+  const RecFwdArgs &a = cx.a;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -177,16 +227,19 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   uint64_t *tempty = wfull + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
 
-  const int warp = threadIdx.x >> 5;
-  const int b = threadIdx.x;  // batch row owned in the epilogue (warps 0-3)
-  const int u0 = blockIdx.x * REC_UPC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // batch row owned in the epilogue (warps 0-3)
+  const int b = M64 ? (lane < 16 ? 16 * warp + lane : (1 << 20)) : (int)threadIdx.x;
+  const int u0 = cx.cta * UPC;
   const int B = a.B, H = a.H;
-  const int ldg = 64 * gridDim.x;  // G pitch
-  const int nu = min(REC_UPC, H - u0);
+  const int nkh = (H + 63) / 64;             // chunks of one h block
+  const int ldg = 64 * ((4 * H + 63) / 64);  // G pitch (whole 64-column groups)
+  const int nu = max(0, min(UPC, H - u0));
   if (a.fail && *a.fail) return;
 
   if (threadIdx.x == 128) {
-    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(tmWa);
+    if (tmWb != tmWa) tma_prefetch_desc(tmWb);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
     mbar_init(tfull, REC_NMW);
     mbar_init(wfull, 1);
@@ -199,16 +252,19 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 128) {
-    mbar_expect_tx(wfull, nk * 8192);
-    for (int j = 0; j < nk; ++j) tma_load_2d(sW + j * 8192, &tmW, wfull, j * 64, blockIdx.x * 64);
+    mbar_expect_tx(wfull, nk * WCH);
+    for (int j = 0; j < nk; ++j) {
+      if (j < ly.nka) tma_load_2d(sW + j * WCH, tmWa, wfull, j * 64, NG * cx.cta);
+      else tma_load_2d(sW + j * WCH, tmWb, wfull, (j - ly.nka) * 64, NG * cx.cta);
+    }
   }
-  // initial state -> registers and row block 0 of Hs / Cs (the local copies of P:266)
-  float hreg[REC_UPC], creg[REC_UPC];
+  // initial state -> registers, row block 0 of Hs / Cs and exchange block 0
+  float hreg[UPC], creg[UPC];
   const bool row = warp < 4 && b < B;
   // `state = self.state` or zeros when it is still None: Switch/Merge on the device
   const bool is_tensor = a.tag == nullptr || *a.tag == 1;
 #pragma unroll
-  for (int u = 0; u < REC_UPC; ++u) {
+  for (int u = 0; u < UPC; ++u) {
     const int gu = u0 + u;
     hreg[u] = (row && gu < H && is_tensor) ? a.h0[(size_t)b * H + gu] : 0.f;
     creg[u] = (row && gu < H && is_tensor) ? a.c0[(size_t)b * H + gu] : 0.f;
@@ -218,68 +274,90 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     }
   }
   uint8_t *hsw = reinterpret_cast<uint8_t *>(a.Hsw);
-  if (row) {
-    __align__(16) __nv_bfloat16 h0b[REC_UPC];
+  const uint8_t *hswA = reinterpret_cast<const uint8_t *>(cx.hswA);
+  // exchange copy: this CTA's UPC units of row b = UPC / 8 granules of chunk u0 / 64
+  auto write_x = [&](int blk, const __nv_bfloat16 *hb) {
+    uint8_t *chunk = hsw + ((size_t)blk * nkh + (u0 >> 6)) * ly.cb;
+    const uint32_t g0 = (uint32_t)(u0 & 63) >> 3;
 #pragma unroll
-    for (int u = 0; u < REC_UPC; ++u) h0b[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
-    write_xchg(hsw, 0, nk, ly.cb, u0, b, h0b);
+    for (int q = 0; q < UPC / 8; ++q)
+      *reinterpret_cast<uint4 *>(chunk + sw128_off(b, g0 + q)) = reinterpret_cast<const uint4 *>(hb)[q];
+  };
+  if (row) {
+    __align__(16) __nv_bfloat16 h0b[UPC];
+#pragma unroll
+    for (int u = 0; u < UPC; ++u) h0b[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
+    write_x(0, h0b);
   }
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
   unsigned int *flags = a.barrier;  // flags[c] = 1 + last step whose h block CTA c has written
   fence_proxy_async_global();
-  publish_flag(&flags[blockIdx.x], 1);
+  publish_flag(&flags[cx.cta], 1);
   const int T = a.T_dev ? *a.T_dev : a.T;
-  constexpr uint32_t idesc = umma_idesc_bf16(128, 64, 0, 0);
+  constexpr uint32_t idesc = umma_idesc_bf16(M64 ? 64 : 128, NG, 0, 0);
   const int nacc = min(REC_NMW, nk);  // accumulator tiles in use
   if (warp >= 5) mbar_wait(wfull, 0);
 
   for (int t = 0; t < T; ++t) {
     if (warp == 4) {
       if (threadIdx.x == 128) PROBE(t, 0);
-      wait_flags_warp(flags, gridDim.x, (unsigned)t + 1);  // h_{t-1} fully written
+      // run A's producers (h_{t-1} of this layer, or h_t of the layer below), then run B's
+      wait_flag_set(cx.flagsA, cx.nflagsA, (unsigned)(t + 1 + cx.blkA_off));
+      if (cx.flagsB) wait_flag_set(cx.flagsB, cx.nflagsB, (unsigned)t + 1);
+      __syncwarp();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      fence_proxy_async_global();
       if (threadIdx.x == 128) {
         PROBE(t, 1);
-        issue_step(hsw + (size_t)t * nk * ly.cb, ly, sA, full, empty, t);
+        issue_step(hswA + (size_t)(t + cx.blkA_off) * nkh * ly.cb, hsw + (size_t)t * nkh * ly.cb, ly, sA,
+                   full, empty, t);
         PROBE(t, 2);
       }
       __syncwarp();
     } else if (warp >= 5) {
       if ((threadIdx.x & 31) == 0) {
-        mma_step<8192, 64>(ly, sA, sW, full, empty, tfull, tempty, tmem, idesc, t, warp - 5,
-                           (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + t) * 16 : nullptr);
+        mma_step<NG>(ly, sA, sW, WCH, full, empty, tfull, tempty, tmem, idesc, t, warp - 5,
+                     (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + t) * 16 : nullptr);
         if (warp == 5) PROBE(t, 4);
       }
       __syncwarp();
     } else {
-      // input projection of this step (independent of h_{t-1}): load while the MMA runs
-      // G rows are padded to 64 columns per CTA (ldg = 64 * grid), so every CTA moves whole
-      // 256-B rows; the padding units compute junk that is never published (hb = 0 there)
-      float z[64];
-      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * ldg + (size_t)blockIdx.x * 64;
+      // input projection of this step (independent of h_{t-1}): load while the MMA runs. G rows
+      // are padded to whole 64-column groups, so every CTA moves whole rows; padding units
+      // compute junk that is never published (hb = 0 there)
+      float z[NG];
+      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * ldg + (size_t)NG * cx.cta;
+      if (cx.bias) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const float4 x = row ? reinterpret_cast<const float4 *>(g)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
-        z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
+        for (int q = 0; q < NG; ++q) z[q] = cx.bias[min(NG * cx.cta + q, 4 * H - 1)];
+      } else {
+#pragma unroll
+        for (int q = 0; q < NG / 4; ++q) {
+          const float4 x = row ? reinterpret_cast<const float4 *>(g)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
+        }
       }
       mbar_wait(tfull, t & 1);
       if (threadIdx.x == 0) PROBE(t, 5);
       __syncwarp();
       tc_fence_after();
       {
-        float lo[32], hi[32];
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
         for (int w = 0; w < nacc; ++w) {
-          tmem_ld32(ta + w * 64, lo);
-          tmem_ld32(ta + w * 64 + 32, hi);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) { z[i] += lo[i]; z[32 + i] += hi[i]; }
+          for (int h = 0; h < NG / 32; ++h) {
+            float v[32];
+            tmem_ld32(ta + w * NG + 32 * h, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) z[32 * h + i] += v[i];
+          }
         }
       }
       epi_tmem_release(tempty);
       const bool valid = !MASKED || t < len_b;
-      __align__(16) __nv_bfloat16 hb[REC_UPC];
+      __align__(16) __nv_bfloat16 hb[UPC];
 #pragma unroll
-      for (int u = 0; u < REC_UPC; ++u) {
+      for (int u = 0; u < UPC; ++u) {
         const float ig = sig_f(z[4 * u]), fg = sig_f(z[4 * u + 1]);
         const float gg = tanh_f(z[4 * u + 2]), og = sig_f(z[4 * u + 3]);
         const float c2 = fg * creg[u] + ig * gg;
@@ -289,32 +367,32 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         hb[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
       }
       // critical path first: the exchange copy of h_t, then the step flag; the rest after
-      if (row) write_xchg(hsw, t + 1, nk, ly.cb, u0, b, hb);
+      if (row) write_x(t + 1, hb);
       fence_proxy_async_global();
       if (threadIdx.x == 0) PROBE(t, 6);
-      epi_publish(&flags[blockIdx.x], (unsigned)t + 2);
+      epi_publish(&flags[cx.cta], (unsigned)t + 2);
       if (threadIdx.x == 0) PROBE(t, 7);
       if (row) {
         const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
+        for (int q = 0; q < NG / 4; ++q)
           reinterpret_cast<float4 *>(g)[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
         float4 *cd = reinterpret_cast<float4 *>(a.Cs + ro);  // ldh >= 64 * ceil(H / 64)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
+        for (int q = 0; q < UPC / 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
 #pragma unroll
-        for (int u = 0; u < REC_UPC; ++u)  // column H of Hs is the GEMMs' ones column
+        for (int u = 0; u < UPC; ++u)  // column H of Hs is the GEMMs' ones column
           if (u == nu) hb[u] = __float2bfloat16_rn(1.f);
         uint4 *hd = reinterpret_cast<uint4 *>(a.Hs + ro);
-        hd[0] = reinterpret_cast<const uint4 *>(hb)[0];
-        hd[1] = reinterpret_cast<const uint4 *>(hb)[1];
+#pragma unroll
+        for (int q = 0; q < UPC / 8; ++q) hd[q] = reinterpret_cast<const uint4 *>(hb)[q];
       }
     }
   }
   // final state (committed by the commit phase only if every assumption held)
   if (row) {
 #pragma unroll
-    for (int u = 0; u < REC_UPC; ++u)
+    for (int u = 0; u < UPC; ++u)
       if (u < nu) {
         a.hT[(size_t)b * H + u0 + u] = hreg[u];
         a.cT[(size_t)b * H + u0 + u] = creg[u];
@@ -323,6 +401,30 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc(tmem, 64 * REC_NMW);
+}
+
+template <bool MASKED, bool M64>
+__global__ void __launch_bounds__(REC_THREADS, 1)
+    lstm_rec_fwd_kernel(const __grid_constant__ CUtensorMap tmW,  // W_hh interleaved [4H x H], box {64,64}
+                        FwdCtx cx, RecLayout ly) {
+  cx.cta = blockIdx.x;
+  fwd_body<REC_UPC, MASKED, M64>(cx, &tmW, &tmW, ly);
+}
+
+// Wavefront: CTAs [0, g0) run layer 0 (16 units each), CTAs [g0, g0 + g1) run layer 1 (8 units).
+template <bool MASKED, bool M64>
+__global__ void __launch_bounds__(REC_THREADS, 1)
+    lstm_rec_fwd_wf_kernel(const __grid_constant__ CUtensorMap tmW0,    // W_hh0, box {64,64}
+                           const __grid_constant__ CUtensorMap tmWih1,  // W_ih1, box {64,32}
+                           const __grid_constant__ CUtensorMap tmWhh1,  // W_hh1, box {64,32}
+                           FwdCtx c0, FwdCtx c1, RecLayout ly0, RecLayout ly1, int g0) {
+  if ((int)blockIdx.x < g0) {
+    c0.cta = blockIdx.x;
+    fwd_body<REC_UPC, MASKED, M64>(c0, &tmW0, &tmW0, ly0);
+  } else {
+    c1.cta = blockIdx.x - g0;
+    fwd_body<REC_UPC / 2, MASKED, M64>(c1, &tmWih1, &tmWhh1, ly1);
+  }
 }
 
 // ---------------------------------------------------------------------------------- backward
@@ -396,14 +498,14 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         wait_flags_warp(flags, gridDim.x, (unsigned)(T - 1 - t));  // dz_{t+1} fully written
         if (threadIdx.x == 128) {
           PROBE(ti, 1);
-          issue_step(dzsw + (size_t)(t + 1) * nk * ly.cb, ly, sA, full, empty, nmma);
+          issue_step(dzsw + (size_t)(t + 1) * nk * ly.cb, nullptr, ly, sA, full, empty, nmma);
           PROBE(ti, 2);
         }
       }
       __syncwarp();
     } else if (warp >= 5) {
       if (has_next && (threadIdx.x & 31) == 0) {
-        mma_step<2048, 16>(ly, sA, sW, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
+        mma_step<16>(ly, sA, sW, 2048, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
                            (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
         if (warp == 5) PROBE(ti, 4);
       }
@@ -516,7 +618,7 @@ constexpr int KS_RED_BYTES = (2 * (KS_CL - 1) + KS_CL) * KS_TILE_BYTES;
 // Epilogue thread mapping (B <= 64, 128 epilogue threads): thread q owns batch row q % 64 and the
 // 8 units 8 (q / 64) .. +7 of the CTA's 16, so all four epilogue warps share the cell backward
 // (only warps 0-1 can read the TMEM lanes of rows 0-63; they stage the tiles through smem).
-template <bool MASKED>
+template <bool MASKED, bool M64>
 __global__ void __launch_bounds__(REC_THREADS, 1)
     lstm_rec_bwd_ks_kernel(const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,64}
                            RecBwdArgs a, RecLayout ly, int nk_all) {
@@ -541,6 +643,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   const int s0 = rank * nkr, nks = max(0, min(nkr, nk_all - s0));  // my K-slice of dz chunks
   RecLayout lyl = ly;
   lyl.nk = nks;
+  lyl.nka = nks;
   lyl.nops = (nks + ly.ch - 1) / ly.ch;
   const bool active = (int)blockIdx.x < nk_all;  // owns real units (chunk blockIdx.x exists)
   const int B = a.B, H = a.H;
@@ -583,7 +686,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   float dcreg[8], carry[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) { dcreg[u] = 0.f; carry[u] = 0.f; }
-  constexpr uint32_t idesc = umma_idesc_bf16(128, 64, 0, 0);
+  constexpr uint32_t idesc = umma_idesc_bf16(M64 ? 64 : 128, 64, 0, 0);
   const int nacc = min(REC_NMW, nks);
   if (warp >= 5 && nks > 0) mbar_wait(wfull, 0);
   unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c has completed
@@ -607,14 +710,14 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         fence_proxy_async_global();
         if (threadIdx.x == 128) {
           PROBE(ti, 1);
-          issue_step(dzsw + ((size_t)(t + 1) * nk_all + s0) * ly.cb, lyl, sA, full, empty, nmma);
+          issue_step(dzsw + ((size_t)(t + 1) * nk_all + s0) * ly.cb, nullptr, lyl, sA, full, empty, nmma);
           PROBE(ti, 2);
         }
       }
       __syncwarp();
     } else if (warp >= 5) {
       if (has_next && nks > 0 && lane == 0) {
-        mma_step<8192, 64>(lyl, sA, sW, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
+        mma_step<64>(lyl, sA, sW, 8192, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
                            (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
         if (warp == 5) PROBE(ti, 4);
       }
@@ -660,7 +763,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
           tc_fence_after();
         }
         epi_bar();  // stage free
-        if (warp < 2) {  // rows 0-63: sum the accumulator tiles, 16 columns (one group) at a time
+        // rows 0-63: sum the accumulator tiles, 16 columns (one group) at a time. M = 128: rows sit
+        // in lanes 0-63 (warps 0-1); M = 64: row i in lane (i % 16) + 32 (i / 16) (lanes 0-15 of
+        // every epilogue warp)
+        // (tcgen05.ld is .sync.aligned: the condition must be warp-uniform; lanes 16-31 of an M = 64
+        // warp load junk lanes and skip the store)
+        const int srow = M64 ? 16 * warp + lane : (int)threadIdx.x;
+        if (M64 || warp < 2) {
           const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
           for (int p = 0; p < KS_CL; ++p) {
@@ -673,9 +782,11 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 #pragma unroll
               for (int i = 0; i < 16; ++i) v[i] += x[i];
             }
-            float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + threadIdx.x) * REC_UPC);
+            if (!M64 || lane < 16) {
+              float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + srow) * REC_UPC);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
           }
         }
         if (nks > 0) epi_tmem_release(tempty);
@@ -754,13 +865,13 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------------- host
-static RecLayout layout(int wbytes, int nk, int B, int extra = 0) {
+static RecLayout layout(int wbytes, int nk, int B, int extra = 0, bool m64 = false) {
   RecLayout l;
   l.nk = nk;
   l.wbytes = (wbytes + 1023) & ~1023;
   l.bp = (B + 7) & ~7;
   l.cb = l.bp * 128;
-  l.pad = (128 - l.bp) * 128;
+  l.pad = std::max(0, (m64 ? 64 : 128) - l.bp) * 128;  // rows an MMA reads past the last chunk
   const int avail = SMEM_BUDGET - l.wbytes - l.pad - extra - 1024 /*barriers*/;
   const int max_chunks = avail / l.cb;  // chunks that fit in flight
   // two ring slots (TMA of op k+1 overlaps the MMAs of op k); a whole step in flight if it fits
@@ -774,6 +885,7 @@ static RecLayout layout(int wbytes, int nk, int B, int extra = 0) {
       l.nslots = std::max(2, std::min(REC_MAX_SLOTS, max_chunks / l.ch));
     }
   }
+  l.nka = nk;
   l.nops = (nk + l.ch - 1) / l.ch;
   return l;
 }
@@ -805,18 +917,66 @@ cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw,
                          cudaStream_t st) {
   if (a.B > 128 || a.B < 1) return cudaErrorInvalidValue;
   const int nk = (a.H + 63) / 64;
-  RecLayout ly = layout(nk * 8192, nk, a.B);
+  RecLayout ly = layout(nk * 8192, nk, a.B, 0, a.B <= 64);
   if (ly.ch < 1 || smem_of(ly) > 232448) return cudaErrorInvalidValue;
   if (!a.Hsw) return cudaErrorInvalidValue;
   CUtensorMap tmW;
   if (!make_tmap_bf16(&tmW, Whh, a.H, 4ull * a.H, ldw, 64)) return cudaErrorInvalidValue;
   const int smem = smem_of(ly);
-  const void *fn = masked ? (const void *)lstm_rec_fwd_kernel<true> : (const void *)lstm_rec_fwd_kernel<false>;
+  const bool m64 = a.B <= 64;
+  const void *fn = masked ? (m64 ? (const void *)lstm_rec_fwd_kernel<true, true> : (const void *)lstm_rec_fwd_kernel<true, false>)
+                          : (m64 ? (const void *)lstm_rec_fwd_kernel<false, true> : (const void *)lstm_rec_fwd_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  RecFwdArgs aa = a;
-  void *args[] = {&tmW, &aa, &ly};
+  FwdCtx cx = {};
+  cx.a = a;
+  cx.hswA = a.Hsw;
+  cx.blkA_off = 0;
+  cx.flagsA = a.barrier;
+  cx.nflagsA = rec_grid(a.H);
+  void *args[] = {&tmW, &cx, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
+}
+
+int rec_fwd_wf_grid(int H) { return rec_grid(H) + (H + REC_UPC / 2 - 1) / (REC_UPC / 2); }
+
+cudaError_t lstm_rec_fwd_wavefront(const RecFwdArgs &a0, const RecFwdArgs &a1, const __nv_bfloat16 *Whh0,
+                                   const __nv_bfloat16 *Wih1, const __nv_bfloat16 *Whh1, int ldw,
+                                   const float *bias1_il, bool masked, cudaStream_t st) {
+  if (a0.B > 128 || a0.B < 1 || a0.H != a1.H || !a0.Hsw || !a1.Hsw) return cudaErrorInvalidValue;
+  const int H = a0.H, nkh = (H + 63) / 64;
+  RecLayout ly0 = layout(nkh * 8192, nkh, a0.B, 0, a0.B <= 64);
+  RecLayout ly1 = layout(2 * nkh * 4096, 2 * nkh, a0.B, 0, a0.B <= 64);
+  ly1.nka = nkh;
+  ly1.nops = (nkh + ly1.ch - 1) / ly1.ch * 2;
+  const int smem = std::max(smem_of(ly0), smem_of(ly1));
+  if (ly0.ch < 1 || ly1.ch < 1 || smem > 232448) return cudaErrorInvalidValue;
+  CUtensorMap tm0, tmi, tmh;
+  if (!make_tmap_bf16(&tm0, Whh0, H, 4ull * H, ldw, 64) || !make_tmap_bf16(&tmi, Wih1, H, 4ull * H, ldw, 32) ||
+      !make_tmap_bf16(&tmh, Whh1, H, 4ull * H, ldw, 32))
+    return cudaErrorInvalidValue;
+  const bool m64 = a0.B <= 64;
+  const void *fn = masked ? (m64 ? (const void *)lstm_rec_fwd_wf_kernel<true, true> : (const void *)lstm_rec_fwd_wf_kernel<true, false>)
+                          : (m64 ? (const void *)lstm_rec_fwd_wf_kernel<false, true> : (const void *)lstm_rec_fwd_wf_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int g0 = rec_grid(H), g1 = rec_fwd_wf_grid(H) - g0;
+  FwdCtx c0 = {}, c1 = {};
+  c0.a = a0;
+  c0.hswA = a0.Hsw;
+  c0.flagsA = a0.barrier;
+  c0.nflagsA = g0;
+  c1.a = a1;
+  c1.hswA = a0.Hsw;  // h0_t = layer 0's exchange block t + 1
+  c1.blkA_off = 1;
+  c1.flagsA = a0.barrier;
+  c1.nflagsA = g0;
+  c1.flagsB = a1.barrier;
+  c1.nflagsB = g1;
+  c1.bias = bias1_il;
+  int g0_ = g0;
+  void *args[] = {&tm0, &tmi, &tmh, &c0, &c1, &ly0, &ly1, &g0_};
+  return coop_launch(fn, g0 + g1, smem, args, st);
 }
 
 static cudaError_t lstm_rec_bwd_plain(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt,
@@ -839,12 +999,12 @@ static cudaError_t lstm_rec_bwd_ks(const RecBwdArgs &a, const __nv_bfloat16 *Whh
                                    cudaStream_t st) {
   const int nk_all = (4 * a.H + 63) / 64;
   const int nkr = (nk_all + KS_CL - 1) / KS_CL;
-  RecLayout ly = layout(nkr * 8192, nkr, a.B, KS_RED_BYTES);
+  RecLayout ly = layout(nkr * 8192, nkr, a.B, KS_RED_BYTES, true);  // B <= 64 here: M = 64 MMAs
   if (ly.ch < 1 || smem_of(ly, KS_RED_BYTES) > 232448) return cudaErrorInvalidValue;
   CUtensorMap tmWT;
   if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 64)) return cudaErrorInvalidValue;
   const int smem = smem_of(ly, KS_RED_BYTES);
-  const void *fn = masked ? (const void *)lstm_rec_bwd_ks_kernel<true> : (const void *)lstm_rec_bwd_ks_kernel<false>;
+  const void *fn = masked ? (const void *)lstm_rec_bwd_ks_kernel<true, true> : (const void *)lstm_rec_bwd_ks_kernel<false, true>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -858,15 +1018,22 @@ static cudaError_t lstm_rec_bwd_ks(const RecBwdArgs &a, const __nv_bfloat16 *Whh
   cfg.blockDim = dim3(REC_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = KS_CL;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = KS_CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
+  // The CTAs wait on each other's step flags, so all clusters must be resident at once. A
+  // cooperative launch would guarantee it but cannot be combined with clusters under the
+  // profiler's replay; check instead that the device can hold every cluster simultaneously
+  // (one CTA per SM; the launch runs alone on the stream).
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg) != cudaSuccess) max_clusters = 0;
+  }
+  if (grid / KS_CL > max_clusters) return cudaErrorCooperativeLaunchTooLarge;
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
@@ -877,7 +1044,12 @@ cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldw
   const char *e = getenv("JANUS_REC_BWD");
   // the K-split kernel exchanges partial tiles of at most 64 batch rows
   if ((e && e[0] == 'p') || a.B > 64) return lstm_rec_bwd_plain(a, WhhT, ldwt, masked, st);
-  return lstm_rec_bwd_ks(a, WhhT, ldwt, masked, st);
+  const cudaError_t r = lstm_rec_bwd_ks(a, WhhT, ldwt, masked, st);
+  if (r == cudaErrorCooperativeLaunchTooLarge) {
+    (void)cudaGetLastError();
+    return lstm_rec_bwd_plain(a, WhhT, ldwt, masked, st);
+  }
+  return r;
 }
 
 }  // namespace jk

@@ -49,6 +49,13 @@ size_t rec_dzsw_bytes(int H, int B, int T);
 int rec_grid(int H);
 cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw, bool masked,
                          cudaStream_t st);
+// Both layers of a 2-layer stack in one launch (wavefront: layer 1's step t runs with layer 0's
+// step t+1). Layer 1's input projection is computed in-kernel (its G buffer receives the gate
+// activations only); Wih1 / Whh1 interleaved [4H x ldw] bf16, bias1_il interleaved fp32 [4H].
+int rec_fwd_wf_grid(int H);
+cudaError_t lstm_rec_fwd_wavefront(const RecFwdArgs &a0, const RecFwdArgs &a1, const __nv_bfloat16 *Whh0,
+                                   const __nv_bfloat16 *Wih1, const __nv_bfloat16 *Whh1, int ldw,
+                                   const float *bias1_il, bool masked, cudaStream_t st);
 cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
                          cudaStream_t st);
 

@@ -16,8 +16,13 @@ NAMES = ["start", "flags_ok", "tma_issued", "tmem_read", "mma_issued", "mma_done
 
 
 def report(buf):
-    d = buf.cpu().numpy().astype(np.float64).reshape(2, 128, T, 16)[:, :NC]
-    for dirn, a in (("fwd", d[0]), ("bwd", d[1])):
+    full = buf.cpu().numpy().astype(np.float64).reshape(2, 128, T, 16)
+    g0 = (H + 15) // 16
+    parts = [("fwd layer0", full[0, :g0])]
+    if full[0, g0:, 1:-1, 7].any():  # wavefront launch: layer-1 CTAs follow
+        parts.append(("fwd layer1 (wavefront)", full[0, g0:g0 + (H + 7) // 8]))
+    parts.append(("bwd", full[1, :NC]))
+    for dirn, a in parts:
         t0 = a[:, :, 0].min(axis=0)  # earliest CTA start of each step
         per = np.median(np.diff(t0))
         print(f"== {dirn}: step period {per:.0f} ns; offsets from the step's earliest start (ns)")
