@@ -130,8 +130,8 @@ JN_DEV void op_range(const RecLayout &ly, int k, int &first, int &n) {
 // (already in the swizzled shared-memory layout, contiguous) into ring slot (st*nops + k) %
 // nslots with one bulk copy. srcA holds chunks [0, nka), srcB chunks [nka, nk).
 JN_DEV void issue_step(const uint8_t *srcA, const uint8_t *srcB, const RecLayout &ly, uint8_t *sA,
-                       uint64_t *full, uint64_t *empty, int st) {
-  for (int k = 0; k < ly.nops; ++k) {
+                       uint64_t *full, uint64_t *empty, int st, int k_begin = 0, int k_end = 1 << 30) {
+  for (int k = k_begin; k < min(ly.nops, k_end); ++k) {
     const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
     if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
     int first, nch;
@@ -301,18 +301,28 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   for (int t = 0; t < T; ++t) {
     if (warp == 4) {
       if (threadIdx.x == 128) PROBE(t, 0);
-      // run A's producers (h_{t-1} of this layer, or h_t of the layer below), then run B's
+      // run A's producers (h_{t-1} of this layer, or h_t of the layer below) -> run A's ops; then
+      // run B's (this layer's h_{t-1}) -> run B's ops. In the wavefront, run A (the layer below,
+      // which runs ahead) is usually ready first, so its MMAs overlap the wait for run B.
+      const uint8_t *srcA = hswA + (size_t)(t + cx.blkA_off) * nkh * ly.cb;
+      const uint8_t *srcB = hsw + (size_t)t * nkh * ly.cb;
       wait_flag_set(cx.flagsA, cx.nflagsA, (unsigned)(t + 1 + cx.blkA_off));
-      if (cx.flagsB) wait_flag_set(cx.flagsB, cx.nflagsB, (unsigned)t + 1);
       __syncwarp();
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
       fence_proxy_async_global();
       if (threadIdx.x == 128) {
         PROBE(t, 1);
-        issue_step(hswA + (size_t)(t + cx.blkA_off) * nkh * ly.cb, hsw + (size_t)t * nkh * ly.cb, ly, sA,
-                   full, empty, t);
-        PROBE(t, 2);
+        issue_step(srcA, srcB, ly, sA, full, empty, t, 0, ops_a(ly));
       }
+      __syncwarp();
+      if (cx.flagsB) {
+        wait_flag_set(cx.flagsB, cx.nflagsB, (unsigned)t + 1);
+        __syncwarp();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        fence_proxy_async_global();
+        if (threadIdx.x == 128) issue_step(srcA, srcB, ly, sA, full, empty, t, ops_a(ly));
+      }
+      if (threadIdx.x == 128) PROBE(t, 2);
       __syncwarp();
     } else if (warp >= 5) {
       if ((threadIdx.x & 31) == 0) {
