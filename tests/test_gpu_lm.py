@@ -98,6 +98,22 @@ def test_lm_bf16_batch128_one_layer():
     _run_parity(prog, "bf16", 2e-2, _lm_batches(128, 4, 200, 1), scale=0.2)
 
 
+def test_lm_bf16_three_layers_per_layer_kernels():
+    """L=3 does not take the two-layer wavefront: one forward launch per layer (M=64 MMAs)."""
+    prog = pg.lstm_lm_program(V=120, E=40, H=48, L=3, B=16, T=7, lr=0.5)
+    _run_parity(prog, "bf16", 2e-2, _lm_batches(16, 7, 120, 2), scale=0.2)
+
+
+@pytest.mark.parametrize("env", [{"JANUS_REC_WF": "0"}, {"JANUS_REC_BWD": "plain"},
+                                 {"JANUS_REC_WF": "0", "JANUS_REC_BWD": "plain"}])
+def test_lm_bf16_kernel_variants(monkeypatch, env):
+    """The per-layer forward and the plain (non-K-split) backward give the same parity."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    prog = pg.lstm_lm_program(V=300, E=72, H=100, L=2, B=33, T=9, lr=0.5)
+    _run_parity(prog, "bf16", 2e-2, _lm_batches(33, 9, 300, 1), scale=0.2)
+
+
 def test_lm_bf16_c2_full_size():
     """BASELINE config C2 at full size: 2x650, T35, B64, V10000 — one step, every output."""
     prog = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=64, T=35, lr=1.0)
