@@ -179,7 +179,7 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
     """TreeLSTM (C3) throughput, the imperative baseline (Table 3 "Imp."), assertion overhead
     (strip_asserts A/B) and the C5 speculation-failure stress, all on this rank's GPU."""
     out = {}
-    K = max(3, min(args.steps, 10))
+    K = max(3, min(args.steps, 40))
     B, T = 64, 35
     prog = c2_program(B)
     # --- guard overhead: same graph without RUNTIME AssertOps, interleaved A/B
@@ -190,7 +190,7 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         st_s = [s.clone() for s in state]
         loss = torch.zeros(1, device="cuda")
         ab = {"with": [], "without": []}
-        for rep in range(3):
+        for rep in range(5):
             for name, gg, w, s in (("with", g, ws, state), ("without", gs, ws_s, st_s)):
                 for k in range(2):
                     gg.run(dev_batches[k], s, w, outs=[loss], stream=stream)
@@ -198,7 +198,8 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
                                                        stream=stream), K) / K)
         w_ms, wo_ms = statistics.median(ab["with"]), statistics.median(ab["without"])
         out["guard_overhead"] = {"ms_with_asserts": w_ms, "ms_without": wo_ms, "overhead": w_ms / wo_ms - 1.0,
-                                 "method": "C2, strip_asserts A/B, interleaved, median of 3 x K steps"}
+                                 "method": f"C2, strip_asserts A/B, interleaved, median of 5 x {K} steps "
+                                           "(noise ~ +-2%; the guard kernel's own share is phases_ms_per_step['guards'])"}
     # --- imperative per-op executor on the same workload (the paper's "Imp." column)
     if world == 1:
         loss = torch.zeros(1, device="cuda")
