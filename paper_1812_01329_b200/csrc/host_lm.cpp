@@ -435,16 +435,27 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   LCHK("init", launch_step_init(dst, bars, p.nbar, st));
   if (p.while_mode) LCHK("trip", launch_trip(P.lens, B, Tw, dst, st));
   if (gl.n) LCHK("guards", launch_guards(gl, dst, st));
-  // operand copies (R1): interleaved / transposed bf16 working copies of the fp32 masters
-  for (int l = 0; l < L; ++l) {
-    const int In = l ? H : E, Inp = l ? Hp : Ep;
-    LCHK("cast", launch_cast_rows(P.Wih[l], G4, In, In, bf(p.off.Wih_b[l]), Inp, H, st));
-    LCHK("cast", launch_cast_rows(P.Whh[l], G4, H, H, bf(p.off.Whh_b[l]), Hp, H, st));
-    LCHK("cast", launch_cast_transpose_interleaved(P.Whh[l], H, bf(p.off.WhhT_b[l]), G4, st));
-    LCHK("cast", launch_bias_interleave(P.b[l], H, fp(p.off.bil[l]), st));
-    LCHK("cast", launch_fill_col(bf(p.off.Hs[l]), TB + B, Hp, H, 1.f, Hp, st));
+  // operand copies (R1): interleaved / transposed bf16 working copies of the fp32 masters, the
+  // interleaved biases and the ones columns — one fused launch
+  {
+    PrepList pl = {};
+    auto add = [&](PrepSeg sg) { pl.s[pl.n++] = sg; };
+    for (int l = 0; l < L; ++l) {
+      const int In = l ? H : E, Inp = l ? Hp : Ep;
+      PrepSeg sg = {};
+      sg.kind = P_CAST_ROWS; sg.src = P.Wih[l]; sg.dst = bf(p.off.Wih_b[l]); sg.rows = G4; sg.cols = In;
+      sg.ld_src = In; sg.ld_dst = Inp; sg.H = H; add(sg);
+      sg = {}; sg.kind = P_CAST_ROWS; sg.src = P.Whh[l]; sg.dst = bf(p.off.Whh_b[l]); sg.rows = G4; sg.cols = H;
+      sg.ld_src = H; sg.ld_dst = Hp; sg.H = H; add(sg);
+      sg = {}; sg.kind = P_CAST_T_IL; sg.src = P.Whh[l]; sg.dst = bf(p.off.WhhT_b[l]); sg.ld_dst = G4; sg.H = H; add(sg);
+      sg = {}; sg.kind = P_BIAS_IL; sg.src = P.b[l]; sg.fdst = fp(p.off.bil[l]); sg.H = H; add(sg);
+      sg = {}; sg.kind = P_FILL_COL; sg.dst = bf(p.off.Hs[l]); sg.rows = TB + B; sg.cols = H; sg.ld_dst = Hp; add(sg);
+    }
+    PrepSeg sg = {};
+    sg.kind = P_CAST_ROWS; sg.src = P.Wdec; sg.dst = bf(p.off.Wdec_b); sg.rows = V; sg.cols = H;
+    sg.ld_src = H; sg.ld_dst = Hp; sg.H = 0; add(sg);
+    LCHK("cast", launch_prep(pl, st));
   }
-  LCHK("cast", launch_cast_rows(P.Wdec, V, H, H, bf(p.off.Wdec_b), Hp, 0, st));
   LCHK("gather", launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
   // forward
   // two layers: one wavefront launch (layer 1 one step behind layer 0, its input projection

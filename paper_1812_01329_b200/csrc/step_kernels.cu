@@ -201,6 +201,79 @@ cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ fused prep
+// Every per-step operand copy of the LM step in ONE launch (blockIdx.y = segment): row casts
+// (optionally gate-interleaving), the interleaved transpose of W_hh, bias interleave, ones-column
+// fill. Each segment strides its own work units over blockIdx.x.
+__global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
+  const PrepSeg sg = pl.s[blockIdx.y];
+  switch (sg.kind) {
+    case P_CAST_ROWS: {
+      const bool pairs = ((sg.ld_src | sg.cols) & 1) == 0 && (reinterpret_cast<uintptr_t>(sg.src) & 7) == 0;
+      for (int r0 = blockIdx.x * CR_ROWS; r0 < sg.rows; r0 += gridDim.x * CR_ROWS) {
+        for (int k0 = 0; k0 < sg.ld_dst; k0 += 512) {
+          const int k = k0 + 2 * threadIdx.x;
+          float2 v[CR_ROWS];
+#pragma unroll
+          for (int q = 0; q < CR_ROWS; ++q) {
+            const int r = r0 + q;
+            v[q] = make_float2(0.f, 0.f);
+            if (r < sg.rows && k < sg.cols) {
+              const int rs = sg.H > 0 ? (r & 3) * sg.H + (r >> 2) : r;
+              const float *sr = sg.src + (size_t)rs * sg.ld_src;
+              if (pairs) v[q] = *reinterpret_cast<const float2 *>(sr + k);
+              else { v[q].x = sr[k]; if (k + 1 < sg.cols) v[q].y = sr[k + 1]; }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < CR_ROWS; ++q)
+            if (r0 + q < sg.rows && k < sg.ld_dst)
+              reinterpret_cast<__nv_bfloat162 *>(sg.dst + (size_t)(r0 + q) * sg.ld_dst)[k >> 1] =
+                  __floats2bfloat162_rn(v[q].x, v[q].y);
+        }
+      }
+    } break;
+    case P_CAST_T_IL: {  // WT[u][ri] = rb(W[rc][u]), 32 x 32 tiles, threads as 32 x 8
+      __shared__ float tile[32][33];
+      const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+      const int H = sg.H, nti = (4 * H + 31) / 32, ntu = (H + 31) / 32;
+      for (int tb = blockIdx.x; tb < nti * ntu; tb += gridDim.x) {
+        const int ri0 = (tb % nti) * 32, u0 = (tb / nti) * 32;
+        for (int i = ty; i < 32; i += 8) {
+          const int ri = ri0 + i, u = u0 + tx;
+          float v = 0.f;
+          if (ri < 4 * H && u < H) v = sg.src[(size_t)((ri & 3) * H + (ri >> 2)) * H + u];
+          tile[i][tx] = v;
+        }
+        __syncthreads();
+        for (int i = ty; i < 32; i += 8) {
+          const int u = u0 + i, ri = ri0 + tx;
+          if (u < H && ri < 4 * H) sg.dst[(size_t)u * sg.ld_dst + ri] = __float2bfloat16_rn(tile[tx][i]);
+        }
+        __syncthreads();
+      }
+    } break;
+    case P_BIAS_IL:
+      for (int ri = blockIdx.x * blockDim.x + threadIdx.x; ri < 4 * sg.H; ri += gridDim.x * blockDim.x)
+        sg.fdst[ri] = sg.src[(ri & 3) * sg.H + (ri >> 2)];
+      break;
+    case P_FILL_COL: {  // dst[r][col] = 1, dst[r][col+1 .. ld_dst) = 0
+      const int w = max(1, sg.ld_dst - sg.cols);
+      const long long n = (long long)sg.rows * w;
+      for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(e / w), k = (int)(e - (long long)r * w);
+        sg.dst[(size_t)r * sg.ld_dst + sg.cols + k] = __float2bfloat16_rn(k == 0 ? 1.f : 0.f);
+      }
+    } break;
+  }
+}
+
+cudaError_t launch_prep(const PrepList &pl, cudaStream_t s) {
+  if (pl.n <= 0) return cudaSuccess;
+  prep_kernel<<<dim3(2 * NSM, pl.n), 256, 0, s>>>(pl);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ xent
 template <int NT>
 __device__ float block_reduce(float v, float *sh, bool is_max) {
@@ -274,12 +347,106 @@ __global__ void __launch_bounds__(NT) xent_kernel(const float *__restrict__ logi
   }
 }
 
+// Single-read variant: the row lives in registers (NV4 float4 per thread), so logits are read from
+// HBM once and dy is written with 8-B stores. Same arithmetic as xent_kernel (max, sum of exp,
+// lse, dy = rb((softmax - onehot) / n_valid)); used when V <= NT * 4 * NV4 and rows are 16-B aligned.
+template <int NT, int NV4>
+__global__ void __launch_bounds__(NT) xent_reg_kernel(const float *__restrict__ logits, int V, int ldl, int rows,
+                                                      const int *__restrict__ tgt, int B, int W,
+                                                      const int *lens, const int *T_dev, float n_valid,
+                                                      __nv_bfloat16 *dy, int lddy, float *rowloss,
+                                                      DevStatus *st) {
+  __shared__ float sh[33];
+  __shared__ float s_nv;
+  const int Tb = T_dev ? *T_dev : rows / B;
+  if (lens && threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < B; ++b) acc += min(lens[b], Tb);
+    s_nv = (float)max(acc, 1);
+  }
+  __syncthreads();
+  const float nv = lens ? s_nv : n_valid;
+  const float inv = 1.f / nv;
+  const int V4 = (V + 3) >> 2;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int t = r / B, b = r - t * B;
+    const bool valid = t < Tb && (!lens || t < lens[b]);
+    const float4 *y4 = reinterpret_cast<const float4 *>(logits + (size_t)r * ldl);
+    uint2 *d2 = reinterpret_cast<uint2 *>(dy + (size_t)r * lddy);
+    if (!valid) {
+      for (int k = threadIdx.x; k < V4; k += NT) d2[k] = make_uint2(0u, 0u);
+      if (threadIdx.x == 0) rowloss[r] = 0.f;
+      continue;
+    }
+    int tg = tgt[(size_t)b * W + t];
+    if (tg < 0 || tg >= V) {
+      if (threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned int *>(&st->runtime_err), 2u);
+      tg = 0;
+    }
+    float4 v[NV4];
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NV4; ++i) {
+      const int k4 = threadIdx.x + i * NT;
+      v[i] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (k4 < V4) {
+        v[i] = __ldcs(y4 + k4);  // streamed: read once
+        const int k = 4 * k4;
+        if (k + 1 >= V) v[i].y = -INFINITY;
+        if (k + 2 >= V) v[i].z = -INFINITY;
+        if (k + 3 >= V) v[i].w = -INFINITY;
+      }
+      m = fmaxf(m, fmaxf(fmaxf(v[i].x, v[i].y), fmaxf(v[i].z, v[i].w)));
+    }
+    m = block_reduce<NT>(m, sh, true);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV4; ++i) {  // e = exp(y - m), kept in registers (one exp per logit)
+      v[i].x = __expf(v[i].x - m); v[i].y = __expf(v[i].y - m);
+      v[i].z = __expf(v[i].z - m); v[i].w = __expf(v[i].w - m);
+      sum += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+    sum = block_reduce<NT>(sum, sh, false);
+    const float lse = m + logf(sum);
+    const float sc = inv / sum;  // softmax / n_valid = e * sc
+#pragma unroll
+    for (int i = 0; i < NV4; ++i) {
+      const int k4 = threadIdx.x + i * NT;
+      if (k4 >= V4) continue;
+      const int k = 4 * k4;
+      const float p0 = v[i].x * sc - (k == tg ? inv : 0.f);
+      const float p1 = v[i].y * sc - (k + 1 == tg ? inv : 0.f);
+      const float p2 = v[i].z * sc - (k + 2 == tg ? inv : 0.f);
+      const float p3 = v[i].w * sc - (k + 3 == tg ? inv : 0.f);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(p0, p1);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(p2, p3);
+      if (k + 3 < V) {
+        d2[k4] = make_uint2(*reinterpret_cast<unsigned *>(&lo), *reinterpret_cast<unsigned *>(&hi));
+      } else {  // ragged tail of the row
+        __nv_bfloat16 *d = dy + (size_t)r * lddy + k;
+        d[0] = lo.x;
+        if (k + 1 < V) d[1] = lo.y;
+        if (k + 2 < V) d[2] = hi.x;
+      }
+    }
+    if (threadIdx.x == 0) rowloss[r] = (lse - logits[(size_t)r * ldl + tg]) * inv;
+  }
+}
+
 cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
                         const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
                         int lddy, float *rowloss, DevStatus *st, cudaStream_t s) {
   int blocks = rows < 8 * NSM ? rows : 8 * NSM;
-  xent_kernel<256><<<blocks, 256, 0, s>>>(logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
-                                          lddy, rowloss, st);
+  constexpr int NT = 128, NV4 = 20;  // 4 rows in flight per SM (register-limited)
+  const bool aligned = (ldl % 4) == 0 && (lddy % 4) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                       (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
+  if (aligned && V <= NT * 4 * NV4) {
+    xent_reg_kernel<NT, NV4><<<blocks, NT, 0, s>>>(logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
+                                                   lddy, rowloss, st);
+  } else {
+    xent_kernel<256><<<blocks, 256, 0, s>>>(logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
+                                            lddy, rowloss, st);
+  }
   return cudaGetLastError();
 }
 

@@ -53,6 +53,23 @@ cudaError_t launch_gather(const float *E, int V, int Edim, const int *tok, int B
 cudaError_t launch_trip(const int *lens, int B, int W, DevStatus *st, cudaStream_t s);
 
 // x (fp32, canonical rows) -> bf16 copies: interleaved rows (4u+g <- g*H+u) and/or transposed.
+// Fused per-step operand preparation (one launch): see prep_kernel in step_kernels.cu.
+enum PrepKind { P_CAST_ROWS = 0, P_CAST_T_IL = 1, P_BIAS_IL = 2, P_FILL_COL = 3 };
+struct PrepSeg {
+  int kind;
+  const float *src;      // fp32 source (CAST_ROWS, CAST_T_IL, BIAS_IL)
+  __nv_bfloat16 *dst;    // bf16 destination (CAST_ROWS, CAST_T_IL, FILL_COL)
+  float *fdst;           // fp32 destination (BIAS_IL)
+  int rows, cols;        // CAST_ROWS: dst rows, valid source columns; FILL_COL: rows, ones column
+  int ld_src, ld_dst;    // pitches (elements); FILL_COL zeroes (cols, ld_dst)
+  int H;                 // CAST_ROWS: > 0 gate-interleaves rows; CAST_T_IL / BIAS_IL: hidden size
+};
+constexpr int MAX_PREP = 24;
+struct PrepList {
+  int n;
+  PrepSeg s[MAX_PREP];
+};
+cudaError_t launch_prep(const PrepList &pl, cudaStream_t s);
 cudaError_t launch_cast_rows(const float *src, int R, int Cc, int ld_src, __nv_bfloat16 *dst,
                              int ld_dst, int interleave_H, cudaStream_t s);
 cudaError_t launch_cast_transpose_interleaved(const float *W, int H, __nv_bfloat16 *WT, int ldwt,
