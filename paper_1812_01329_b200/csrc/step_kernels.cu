@@ -465,20 +465,24 @@ JN_DEV int tok_of(const int *tok, int B, int W, int r) {
 }
 
 __global__ void embed_claim_kernel(const int *tok, int B, int W, int T, const int *T_dev, int *owner,
-                                   int *seg_word, int *nseg) {
+                                   int *seg_word, int *nseg, int *tokr) {
   const int n = (T_dev ? *T_dev : T) * B;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int w = tok_of(tok, B, W, r);
+    tokr[r] = w;  // time-major copy: the segment sums scan it coalesced
     if (atomicCAS(&owner[w], -1, r) == -1) seg_word[atomicAdd(nseg, 1)] = w;
   }
 }
 
+// dynamic smem: rows[EG_MAX] ints, then part[EG_WARPS][NQ * 32] floats
+template <int NQ>
 __global__ void __launch_bounds__(EG_WARPS * 32) embed_segsum_kernel(
-    const int *tok, int B, int W, int T, const int *T_dev, const int *seg_word, const int *nseg,
+    const int *tokr, int B, int T, const int *T_dev, const int *seg_word, const int *nseg,
     const float *__restrict__ dX, int ldx, int Edim, float *seg_grad, int ldg) {
-  __shared__ int rows[EG_MAX];
+  extern __shared__ int eg_smem[];
+  int *rows = eg_smem;
+  float *part = reinterpret_cast<float *>(eg_smem + EG_MAX);  // [EG_WARPS][NQ * 32]
   __shared__ int wcount[EG_WARPS];
-  __shared__ float part[EG_WARPS][128];
   const int n = (T_dev ? *T_dev : T) * B;
   const int ns = *nseg;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -488,7 +492,7 @@ __global__ void __launch_bounds__(EG_WARPS * 32) embed_segsum_kernel(
     int cnt = 0;
     for (int r0 = 0; r0 < n; r0 += blockDim.x) {
       const int r = r0 + threadIdx.x;
-      const bool hit = r < n && tok_of(tok, B, W, r) == word;
+      const bool hit = r < n && tokr[r] == word;
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (lane == 0) wcount[w] = __popc(m);
       __syncthreads();
@@ -498,25 +502,43 @@ __global__ void __launch_bounds__(EG_WARPS * 32) embed_segsum_kernel(
       for (int j = 0; j < EG_WARPS; ++j) cnt += wcount[j];
       __syncthreads();
     }
-    for (int c0 = 0; c0 < Edim; c0 += 128) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int i = w; i < cnt; i += EG_WARPS) {
-        const float *row = dX + (size_t)rows[i] * ldx + c0;
+    // warp w sums list entries w, w + EG_WARPS, ... over ALL columns at once (lane: columns
+    // lane + 32 q), two rows per iteration: up to 2 NQ independent loads in flight per lane
+    float acc[NQ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (c0 + lane + 32 * q < Edim) acc[q] += row[lane + 32 * q];
+    for (int q = 0; q < NQ; ++q) acc[q] = 0.f;
+    int i = w;
+    for (; i + EG_WARPS < cnt; i += 2 * EG_WARPS) {
+      const float *r0p = dX + (size_t)rows[i] * ldx;
+      const float *r1p = dX + (size_t)rows[i + EG_WARPS] * ldx;
+      float x0[NQ], x1[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int c = lane + 32 * q;
+        x0[q] = c < Edim ? r0p[c] : 0.f;
+        x1[q] = c < Edim ? r1p[c] : 0.f;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) part[w][lane + 32 * q] = acc[q];
-      __syncthreads();
-      if (w < 4) {
-        const int k = lane + 32 * w;
-        float sum = part[0][k];
-        for (int j = 1; j < EG_WARPS && j < cnt; ++j) sum += part[j][k];
-        if (c0 + k < Edim) seg_grad[(size_t)sgi * ldg + c0 + k] = sum;
-      }
-      __syncthreads();
+      for (int q = 0; q < NQ; ++q) { acc[q] += x0[q]; acc[q] += x1[q]; }
     }
+    if (i < cnt) {
+      const float *r0p = dX + (size_t)rows[i] * ldx;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int c = lane + 32 * q;
+        acc[q] += c < Edim ? r0p[c] : 0.f;
+      }
+    }
+    // combine the warps' partial sums in warp order (deterministic)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) part[w * NQ * 32 + lane + 32 * q] = acc[q];
+    __syncthreads();
+    for (int c = threadIdx.x; c < Edim; c += blockDim.x) {
+      float sum = part[c];
+      for (int j = 1; j < EG_WARPS && j < cnt; ++j) sum += part[j * NQ * 32 + c];
+      seg_grad[(size_t)sgi * ldg + c] = sum;
+    }
+    __syncthreads();
   }
 }
 
@@ -527,10 +549,19 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
   cudaError_t e = cudaMemsetAsync(owner, 0xff, (size_t)V * sizeof(int), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(nseg, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
-  embed_claim_kernel<<<(T * B + 255) / 256, 256, 0, s>>>(tok, B, W, T, T_dev, owner, seg_word, nseg);
-  embed_segsum_kernel<<<8 * NSM, EG_WARPS * 32, 0, s>>>(tok, B, W, T, T_dev, seg_word, nseg, dX, ldx,
-                                                        Edim, seg_grad, ldg);
-  return cudaGetLastError();
+  int *tokr = owner + V;  // scratch: T*B ints after the owner table
+  embed_claim_kernel<<<(T * B + 255) / 256, 256, 0, s>>>(tok, B, W, T, T_dev, owner, seg_word, nseg, tokr);
+  auto go = [&](auto kern, int nq) {
+    const int smem = EG_MAX * 4 + EG_WARPS * nq * 32 * 4;
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (r != cudaSuccess) return r;
+    kern<<<4 * NSM, EG_WARPS * 32, smem, s>>>(tokr, B, T, T_dev, seg_word, nseg, dX, ldx, Edim, seg_grad, ldg);
+    return cudaGetLastError();
+  };
+  if (Edim <= 8 * 32) return go(embed_segsum_kernel<8>, 8);
+  if (Edim <= 24 * 32) return go(embed_segsum_kernel<24>, 24);
+  if (Edim <= 48 * 32) return go(embed_segsum_kernel<48>, 48);
+  return cudaErrorInvalidValue;
 }
 
 // ------------------------------------------------------------------------------ finalize
