@@ -210,6 +210,17 @@ JN_DEV void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+JN_DEV void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // ------------------------------------------------------------------------------ grid sync
 // Monotonic counter barrier for co-resident (cooperatively launched) CTAs. `target` grows by
 // gridDim each use, so the counter never needs a reset inside a launch.

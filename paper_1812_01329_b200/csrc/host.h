@@ -33,7 +33,7 @@ struct LmPlan {
   size_t ws_bytes = 0;
   struct Off {
     size_t status = 0, barriers = 0, stage_args = 0;
-    size_t Wih_b[4], Whh_b[4], WhhT_b[4], bil[4], Wdec_b = 0;
+    size_t Wih_b[4], Whh_b[4], WhhT_b[4], bil[4], Wdec_b = 0, WihT_b1 = 0;
     size_t X = 0, Hs[4], Cs[4], G[4], DZ[4], dX[4], Hsw[4], DZsw[4];
     size_t logits = 0, dy = 0, rowloss = 0, dHtop = 0, hT[4], cT[4];
     size_t gWih[4], gWhh[4], gWdec = 0;

@@ -223,6 +223,7 @@ bool lower_lm(Graph &g, std::string &why) {
       p.off.cT[l] = take((size_t)B * H * 4);
     }
     p.off.Wdec_b = take((size_t)V * p.Hp * 2);
+    if (p.L == 2) p.off.WihT_b1 = take((size_t)H * G4 * 2);  // W_ih1^T for the backward wavefront
     p.off.X = take(TB * p.Ep * 2);
     p.off.logits = take(TB * Vp * 4);
     p.off.dy = take(TB * Vp * 2);
@@ -451,6 +452,10 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       sg = {}; sg.kind = P_BIAS_IL; sg.src = P.b[l]; sg.fdst = fp(p.off.bil[l]); sg.H = H; add(sg);
       sg = {}; sg.kind = P_FILL_COL; sg.dst = bf(p.off.Hs[l]); sg.rows = TB + B; sg.cols = H; sg.ld_dst = Hp; add(sg);
     }
+    if (L == 2) {  // W_ih1^T (interleaved) for the backward wavefront
+      PrepSeg sg = {};
+      sg.kind = P_CAST_T_IL; sg.src = P.Wih[1]; sg.dst = bf(p.off.WihT_b1); sg.ld_dst = G4; sg.H = H; add(sg);
+    }
     PrepSeg sg = {};
     sg.kind = P_CAST_ROWS; sg.src = P.Wdec; sg.dst = bf(p.off.Wdec_b); sg.rows = V; sg.cols = H;
     sg.ld_src = H; sg.ld_dst = Hp; sg.H = 0; add(sg);
@@ -513,16 +518,32 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
     LCHK("gemm_dh", gemm_bf16(with_flags(o2), st));
   }
-  for (int l = L - 1; l >= 0; --l) {
-    const int In = l ? H : E, Inp = l ? Hp : Ep;
+  // two layers, B <= 64: one backward wavefront launch (layer 0 one step behind layer 1, the
+  // dgrad of layer 1's input W_ih1^T dz1_t folded into layer 0's recurrent MMA)
+  const char *bwf_env = getenv("JANUS_REC_BWD_WF");
+  const char *bk_env = getenv("JANUS_REC_BWD");
+  const bool bwd_wave = L == 2 && B <= 64 && !(bwf_env && bwf_env[0] == '0') && !(bk_env && bk_env[0] == 'p') &&
+                        rec_bwd_wf_grid(H) <= 148;
+  auto bwd_args = [&](int l) {
     RecBwdArgs rb;
     rb.B = B; rb.H = H; rb.T = Tw; rb.T_dev = Tdev; rb.lens = p.while_mode ? P.lens : nullptr;
     rb.G = fp(p.off.G[l]); rb.Cs = fp(p.off.Cs[l]); rb.ldh = Hp;
     rb.dHin = l == L - 1 ? fp(p.off.dHtop) : fp(p.off.dX[l + 1]); rb.ldd = Hp;
     rb.DZsw = bf(p.off.DZsw[l]);
     rb.DZ = bf(p.off.DZ[l]); rb.ldz = p.Gz; rb.barrier = bars + 256 * (L + l);
-    rb.dbg = (l == 0 && g.probe) ? g.probe + (size_t)128 * 16 * p.T : nullptr;
-    LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(rb, bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
+    rb.dbg = ((l == 0 || bwd_wave) && g.probe) ? g.probe + (size_t)128 * 16 * p.T : nullptr;
+    return rb;
+  };
+  if (bwd_wave) {
+    RecBwdArgs r0 = bwd_args(0);
+    r0.dHin = nullptr;  // layer 1's input dgrad arrives through the fused MMA
+    LCHK("rec_bwd01", lstm_rec_bwd_wavefront(bwd_args(1), r0, bf(p.off.WhhT_b[1]), bf(p.off.WihT_b1),
+                                             bf(p.off.WhhT_b[0]), G4, p.while_mode, st));
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    if (!bwd_wave)
+      LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(bwd_args(l), bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
     const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
     GemmOp a;  // dW_hh = dz^T h_{t-1}
     a.M = G4; a.N = H; a.K = TB;
@@ -536,7 +557,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
     b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
     LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(with_flags(b2), st));
-    if (l > 0 || p.lr_E != 0) {
+    if ((l > 0 && !bwd_wave) || (l == 0 && p.lr_E != 0)) {
       GemmOp c2;  // dx = dz W_ih
       c2.M = TB; c2.N = In; c2.K = G4;
       c2.A = bf(p.off.DZ[l]); c2.lda = p.Gz;

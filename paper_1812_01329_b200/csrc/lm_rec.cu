@@ -129,10 +129,12 @@ JN_DEV void op_range(const RecLayout &ly, int k, int &first, int &n) {
 // Producer (warp 4, lane 0): op k of step `st` copies its chunks of the step's exchange block(s)
 // (already in the swizzled shared-memory layout, contiguous) into ring slot (st*nops + k) %
 // nslots with one bulk copy. srcA holds chunks [0, nka), srcB chunks [nka, nk).
+// q0 >= 0: ring position of the step's first op (steps with varying op counts); else st * nops.
 JN_DEV void issue_step(const uint8_t *srcA, const uint8_t *srcB, const RecLayout &ly, uint8_t *sA,
-                       uint64_t *full, uint64_t *empty, int st, int k_begin = 0, int k_end = 1 << 30) {
+                       uint64_t *full, uint64_t *empty, int st, int k_begin = 0, int k_end = 1 << 30,
+                       int q0 = -1) {
   for (int k = k_begin; k < min(ly.nops, k_end); ++k) {
-    const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
+    const int q = (q0 >= 0 ? q0 : st * ly.nops) + k, s = q % ly.nslots, r = q / ly.nslots;
     if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
     int first, nch;
     op_range(ly, k, first, nch);
@@ -151,10 +153,10 @@ JN_DEV void issue_step(const uint8_t *srcA, const uint8_t *srcB, const RecLayout
 template <int NCOL>
 JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, int wchunk, uint64_t *full,
                      uint64_t *empty, uint64_t *tfull, uint64_t *tempty, uint32_t tmem, uint32_t idesc,
-                     int st, int w, unsigned long long *pr) {
+                     int st, int w, unsigned long long *pr, int q0 = -1) {
   const uint32_t acc = tmem + (uint32_t)(w * NCOL);
   for (int k = 0; k < ly.nops; ++k) {
-    const int q = st * ly.nops + k, s = q % ly.nslots, r = q / ly.nslots;
+    const int q = (q0 >= 0 ? q0 : st * ly.nops) + k, s = q % ly.nslots, r = q / ly.nslots;
     if (k == 0 && st > 0) mbar_wait(tempty, (st - 1) & 1);  // the epilogue drained step st-1's tiles
     mbar_wait(&full[s], r & 1);
     if (pr && k < 4) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pr[8 + 2 * k]));
@@ -620,27 +622,41 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // (u0 = 16 * blockIdx.x, the same ownership, dz exchange layout and flags as the plain kernel)
 // and receives their partials from its KS_CL-1 peers, summed in a fixed order (deterministic).
 constexpr int KS_CL = 4;
-constexpr int KS_UPC = 16 * KS_CL;
-constexpr int KS_TILE_BYTES = 64 * REC_UPC * 4;  // one 16-unit tile of partial dh: [row < 64][16] fp32
-// red[parity][sender slot] (peers' tiles) + stage[group] (this CTA's 4 tiles, own one included)
-constexpr int KS_RED_BYTES = (2 * (KS_CL - 1) + KS_CL) * KS_TILE_BYTES;
+template <int UPC>
+struct KsCfg {
+  static constexpr int CUNITS = KS_CL * UPC;              // units per cluster = MMA N
+  static constexpr int WCH = CUNITS * 128;                 // bytes per resident weight chunk
+  static constexpr int TILE = 64 * UPC * 4;                // one peer's partial tile [row < 64][UPC] fp32
+  static constexpr int RED = (2 * (KS_CL - 1) + KS_CL) * TILE;  // red[parity][sender] + stage[group]
+  static constexpr int HU = UPC / 2;                       // units per epilogue thread
+};
 
-// Epilogue thread mapping (B <= 64, 128 epilogue threads): thread q owns batch row q % 64 and the
-// 8 units 8 (q / 64) .. +7 of the CTA's 16, so all four epilogue warps share the cell backward
-// (only warps 0-1 can read the TMEM lanes of rows 0-63; they stage the tiles through smem).
-template <bool MASKED, bool M64>
-__global__ void __launch_bounds__(REC_THREADS, 1)
-    lstm_rec_bwd_ks_kernel(const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,64}
-                           RecBwdArgs a, RecLayout ly, int nk_all) {
+// One backward-recurrence role (a layer). K space of a step: run A = the layer above's dz_t
+// (wavefront layer 0 only: dX_t = W_ih^T dz_t of the layer above, folded into this layer's dh
+// instead of a separate dgrad GEMM), then run B = this layer's dz_{t+1}.
+struct KsCtx {
+  RecBwdArgs a;                  // this layer; a.barrier = its step flags, a.DZsw its exchange buffer
+  int base;                      // first CTA of this layer in the launch (multiple of KS_CL)
+  int nk_all;                    // chunks of one dz block = ceil(4H / 64)
+  const __nv_bfloat16 *dzswA;    // run A: the layer above's exchange buffer (block t)
+  const unsigned int *flagsA;    // its step flags (16 units = one chunk per producer CTA)
+  int nkA;                       // chunks of run A (0: none)
+};
+
+template <int UPC, bool MASKED>
+JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap *tmWb, const RecLayout &ly) {
+  using C = KsCfg<UPC>;
+  constexpr int HU = C::HU;
+  const RecBwdArgs &a = cx.a;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
   const int nkr = ly.nk, S = ly.nslots;
   uint8_t *sW = base;
   uint8_t *sA = sW + ly.wbytes;
-  float *red = reinterpret_cast<float *>(sA + (size_t)S * ly.ch * ly.cb + ly.pad);
-  float *stage = red + 2 * (KS_CL - 1) * 64 * REC_UPC;
-  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) + KS_RED_BYTES);
+  float *red = reinterpret_cast<float *>(sA + (size_t)S * ly.ch * ly.cb + ly.pad);  // [2][CL-1][64][UPC]
+  float *stage = red + 2 * (KS_CL - 1) * 64 * UPC;                                // [CL][64][UPC]
+  uint64_t *full = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(red) + C::RED);
   uint64_t *empty = full + S;
   uint64_t *tfull = empty + S;
   uint64_t *wfull = tfull + 1;
@@ -649,24 +665,27 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(redfull + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = (int)cluster_ctarank(), cl = blockIdx.x / KS_CL;
-  const int s0 = rank * nkr, nks = max(0, min(nkr, nk_all - s0));  // my K-slice of dz chunks
-  RecLayout lyl = ly;
-  lyl.nk = nks;
-  lyl.nka = nks;
-  lyl.nops = (nks + ly.ch - 1) / ly.ch;
-  const bool active = (int)blockIdx.x < nk_all;  // owns real units (chunk blockIdx.x exists)
+  const int lcta = blockIdx.x - cx.base;  // CTA index within the layer
+  const int rank = (int)cluster_ctarank(), cl = lcta / KS_CL;
+  const int nkA = cx.nkA, nk_all = cx.nk_all, nkt = nkA + nk_all;
+  const int s0 = rank * nkr, nks = max(0, min(nkr, nkt - s0));  // my K-slice
+  const int na = max(0, min(s0 + nks, nkA) - s0);               // ... of which run A
+  const int nb = nks - na, b0 = max(0, s0 - nkA);               // ... and run B (from chunk b0)
   const int B = a.B, H = a.H;
-  const int u0 = REC_UPC * blockIdx.x;
-  const int nu = max(0, min(REC_UPC, H - u0));
-  const int ldg = 64 * nk_all;  // G pitch (64 gate columns per 16 units)
-  // epilogue mapping
-  const int eb = threadIdx.x & 63, eh = (threadIdx.x >> 6) & 1;  // row, unit half
-  const int nuh = max(0, min(8, nu - 8 * eh));                     // real units of my half
+  const int u0 = UPC * lcta;
+  // a CTA whose gate columns lie inside the dz chunk grid publishes its slice every step (zeros
+  // for units >= H): consumers wait on every producer of a chunk
+  const bool active = 4 * u0 < 64 * nk_all;
+  const int ldg = 64 * nk_all;  // G pitch
+  // epilogue mapping: thread q owns batch row q % 64 and units HU (q / 64) .. + HU - 1
+  const int eb = threadIdx.x & 63, eh = (threadIdx.x >> 6) & 1;
+  const int ue = u0 + HU * eh;                    // first unit of my epilogue share
+  const int nuh = max(0, min(HU, H - ue));        // real units of my share
   if (a.fail && *a.fail) return;  // uniform: every CTA reads the same flag
 
   if (threadIdx.x == 128) {
-    tma_prefetch_desc(&tmWT);
+    if (nkA) tma_prefetch_desc(tmWa);
+    tma_prefetch_desc(tmWb);
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], REC_NMW); }
     mbar_init(tfull, REC_NMW);
     mbar_init(wfull, 1);
@@ -682,124 +701,151 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
   cluster_sync_all();  // peers' barriers are initialised before any bulk copy targets them
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 128 && nks > 0) {
-    mbar_expect_tx(wfull, nks * 8192);
-    for (int j = 0; j < nks; ++j) tma_load_2d(sW + j * 8192, &tmWT, wfull, (s0 + j) * 64, KS_UPC * cl);
+    mbar_expect_tx(wfull, nks * C::WCH);
+    for (int j = 0; j < nks; ++j) {
+      const int g = s0 + j;
+      if (g < nkA) tma_load_2d(sW + j * C::WCH, tmWa, wfull, g * 64, C::CUNITS * cl);
+      else tma_load_2d(sW + j * C::WCH, tmWb, wfull, (g - nkA) * 64, C::CUNITS * cl);
+    }
   }
   const int T = a.T_dev ? *a.T_dev : a.T;
   const bool row = warp < 4 && eb < B && active;
   if (MASKED && row) {  // While mode: dz rows beyond the device trip count stay out of the wgrads
     for (int t = T; t < a.T; ++t)
       for (int q = 0; q < 4 * nuh; ++q)
-        a.DZ[(size_t)(t * B + eb) * a.ldz + (size_t)blockIdx.x * 64 + 32 * eh + q] = __float2bfloat16_rn(0.f);
+        a.DZ[(size_t)(t * B + eb) * a.ldz + 4 * (size_t)ue + q] = __float2bfloat16_rn(0.f);
   }
   const int len_b = (MASKED && row) ? a.lens[eb] : 0;
-  float dcreg[8], carry[8];
+  float dcreg[HU], carry[HU];
 #pragma unroll
-  for (int u = 0; u < 8; ++u) { dcreg[u] = 0.f; carry[u] = 0.f; }
-  constexpr uint32_t idesc = umma_idesc_bf16(M64 ? 64 : 128, 64, 0, 0);
-  const int nacc = min(REC_NMW, nks);
+  for (int u = 0; u < HU; ++u) { dcreg[u] = 0.f; carry[u] = 0.f; }
+  constexpr uint32_t idesc = umma_idesc_bf16(64, C::CUNITS, 0, 0);  // B <= 64: M = 64
   if (warp >= 5 && nks > 0) mbar_wait(wfull, 0);
-  unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c has completed
+  unsigned int *flags = a.barrier;  // flags[c] = number of steps CTA c of this layer has completed
   uint8_t *dzsw = reinterpret_cast<uint8_t *>(a.DZsw);
-  int nmma = 0;  // steps with a dz_{t+1} operand (tfull / tempty / redfull phase)
+  const uint8_t *dzswA = reinterpret_cast<const uint8_t *>(cx.dzswA);
+  int q_ring = 0;  // ring position (ops), producer and MMA warps advance it identically
+  int nm = 0;      // steps in which this CTA issued MMAs (tfull / tempty phase)
+  int nx = 0;      // exchange steps (redfull phase; uniform across the cluster)
 
   for (int t = T - 1; t >= 0; --t) {
-    const bool has_next = t + 1 < T;
     const int ti = T - 1 - t;
+    const bool has_b = t + 1 < T;                 // dz_{t+1} of this layer exists
+    const int nbs = has_b ? nb : 0;               // run-B chunks of my slice this step
+    const int nstep = na + nbs;                   // chunks I multiply this step
+    const bool has_x = nkA > 0 || has_b;          // the cluster exchanges partials this step
+    RecLayout lys = ly;
+    lys.nk = nstep;
+    lys.nka = na;
+    lys.nops = (na + ly.ch - 1) / ly.ch + (nbs + ly.ch - 1) / ly.ch;
     if (warp == 4) {
-      if (has_next && nks > 0) {
+      if (nstep > 0) {
         if (threadIdx.x == 128) PROBE(ti, 0);
-        for (int c = s0 + lane; c < s0 + nks; c += 32) {  // only my K-slice's producers
-          unsigned x;
-          do {
-            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
-          } while (x < (unsigned)(T - 1 - t));
+        const uint8_t *srcA = dzswA ? dzswA + ((size_t)t * nk_all + s0) * ly.cb : nullptr;
+        const uint8_t *srcB = dzsw + ((size_t)(t + 1) * nk_all + b0) * ly.cb;
+        const int opsA = (na + ly.ch - 1) / ly.ch;
+        if (na > 0) {  // the layer above's dz_t: producer CTA g of that layer per chunk g
+          for (int c = s0 + lane; c < s0 + na; c += 32) {
+            unsigned x;
+            do {
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(cx.flagsA + c) : "memory");
+            } while (x < (unsigned)(T - t));
+          }
+          __syncwarp();
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          fence_proxy_async_global();
+          if (threadIdx.x == 128) issue_step(srcA, srcB, lys, sA, full, empty, 0, 0, opsA, q_ring);
         }
-        __syncwarp();
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        fence_proxy_async_global();
-        if (threadIdx.x == 128) {
-          PROBE(ti, 1);
-          issue_step(dzsw + ((size_t)(t + 1) * nk_all + s0) * ly.cb, nullptr, lyl, sA, full, empty, nmma);
-          PROBE(ti, 2);
+        if (nbs > 0) {  // this layer's dz_{t+1}: chunk j is produced by CTAs [16 j / UPC, 16 (j + 1) / UPC)
+          const int p0 = b0 * 16 / UPC, p1 = (b0 + nbs) * 16 / UPC;
+          for (int c = p0 + lane; c < p1; c += 32) {
+            unsigned x;
+            do {
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
+            } while (x < (unsigned)(T - 1 - t));
+          }
+          __syncwarp();
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          fence_proxy_async_global();
+          if (threadIdx.x == 128) issue_step(srcA, srcB, lys, sA, full, empty, 0, opsA, 1 << 30, q_ring);
         }
+        if (threadIdx.x == 128) PROBE(ti, 2);
       }
       __syncwarp();
     } else if (warp >= 5) {
-      if (has_next && nks > 0 && lane == 0) {
-        mma_step<64>(lyl, sA, sW, 8192, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
-                           (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
+      if (nstep > 0 && lane == 0) {
+        mma_step<C::CUNITS>(lys, sA, sW, C::WCH, full, empty, tfull, tempty, tmem, idesc, nm, warp - 5,
+                            (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr,
+                            q_ring);
         if (warp == 5) PROBE(ti, 4);
       }
       __syncwarp();
     } else {
-      // per-step operands of my (row, 8 units), independent of dz_{t+1}: load while the MMA runs
+      // per-step operands of my (row, HU units), independent of the dz's: load while the MMA runs
       const size_t r = (size_t)(t * B + (row ? eb : 0));
-      float gt[32], ct[8], cp[8], din[8];
+      float gt[4 * HU], ct[HU], cp[HU], din[HU];
       {
-        const float *g = a.G + r * ldg + (size_t)blockIdx.x * 64 + 32 * eh;
-        const float *pc = a.Cs + (r + B) * a.ldh + u0 + 8 * eh;
-        const float *pp = a.Cs + r * a.ldh + u0 + 8 * eh;
-        const float *pd = a.dHin + r * a.ldd + u0 + 8 * eh;
+        const float *g = a.G + r * ldg + 4 * (size_t)ue;
+        const float *pc = a.Cs + (r + B) * a.ldh + ue;
+        const float *pp = a.Cs + r * a.ldh + ue;
+        const float *pd = a.dHin ? a.dHin + r * a.ldd + ue : nullptr;
         const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < HU; ++k) {
           const float4 x = row ? reinterpret_cast<const float4 *>(g)[k] : zero4;
           gt[4 * k] = x.x; gt[4 * k + 1] = x.y; gt[4 * k + 2] = x.z; gt[4 * k + 3] = x.w;
         }
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < HU / 4; ++k) {
           const float4 x = row ? reinterpret_cast<const float4 *>(pc)[k] : zero4;
           const float4 y = row ? reinterpret_cast<const float4 *>(pp)[k] : zero4;
-          const float4 w = row ? reinterpret_cast<const float4 *>(pd)[k] : zero4;
+          const float4 w = (row && pd) ? reinterpret_cast<const float4 *>(pd)[k] : zero4;
           ct[4 * k] = x.x; ct[4 * k + 1] = x.y; ct[4 * k + 2] = x.z; ct[4 * k + 3] = x.w;
           cp[4 * k] = y.x; cp[4 * k + 1] = y.y; cp[4 * k + 2] = y.z; cp[4 * k + 3] = y.w;
           din[4 * k] = w.x; din[4 * k + 1] = w.y; din[4 * k + 2] = w.z; din[4 * k + 3] = w.w;
         }
       }
-      float dh[8];
+      float dh[HU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dh[u] = 0.f;
-      if (has_next) {
-        const int par = nmma & 1;
+      for (int u = 0; u < HU; ++u) dh[u] = 0.f;
+      if (has_x) {
+        const int par = nx & 1;
         if (threadIdx.x == 0) {
           bulk_wait_group_read0();  // the previous step's stage has been read out by the copies
-          mbar_expect_tx(&redfull[par], (KS_CL - 1) * KS_TILE_BYTES);
+          mbar_expect_tx(&redfull[par], (KS_CL - 1) * C::TILE);
         }
-        if (nks > 0) {
-          mbar_wait(tfull, nmma & 1);
+        if (nstep > 0) {
+          mbar_wait(tfull, nm & 1);
           if (threadIdx.x == 0) PROBE(ti, 5);
           __syncwarp();
           tc_fence_after();
         }
         epi_bar();  // stage free
-        // rows 0-63: sum the accumulator tiles, 16 columns (one group) at a time. M = 128: rows sit
-        // in lanes 0-63 (warps 0-1); M = 64: row i in lane (i % 16) + 32 (i / 16) (lanes 0-15 of
-        // every epilogue warp)
-        // (tcgen05.ld is .sync.aligned: the condition must be warp-uniform; lanes 16-31 of an M = 64
-        // warp load junk lanes and skip the store)
-        const int srow = M64 ? 16 * warp + lane : (int)threadIdx.x;
-        if (M64 || warp < 2) {
+        {  // M = 64: accumulator row i in TMEM lane (i % 16) + 32 (i / 16); tcgen05.ld is
+           // .sync.aligned, so every lane of the warp loads and lanes 16-31 skip the store
+          const int srow = 16 * warp + lane;
           const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+          const int nacc = min(REC_NMW, nstep);
 #pragma unroll
           for (int p = 0; p < KS_CL; ++p) {
-            float v[16];
+            float v[UPC];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            for (int i = 0; i < UPC; ++i) v[i] = 0.f;
             for (int w = 0; w < nacc; ++w) {
-              float x[16];
-              tmem_ld16(ta + w * 64 + 16 * p, x);
+              float x[UPC];
+              if constexpr (UPC == 16) tmem_ld16(ta + w * C::CUNITS + UPC * p, x);
+              else tmem_ld8(ta + w * C::CUNITS + UPC * p, x);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] += x[i];
+              for (int i = 0; i < UPC; ++i) v[i] += x[i];
             }
-            if (!M64 || lane < 16) {
-              float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + srow) * REC_UPC);
+            if (lane < 16) {
+              float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + srow) * UPC);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              for (int q = 0; q < UPC / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             }
           }
         }
-        if (nks > 0) epi_tmem_release(tempty);
+        if (nstep > 0) epi_tmem_release(tempty);
         if (threadIdx.x == 0) PROBE(ti, 3);
         fence_proxy_async_shared();
         epi_bar();
@@ -808,28 +854,30 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
           for (int p = 0; p < KS_CL; ++p) {
             if (p == rank) continue;
             const int slot = rank < p ? rank : rank - 1;  // my sender slot inside peer p
-            const uint32_t dst = mapa_shared(smem_u32(red + (size_t)(par * (KS_CL - 1) + slot) * 64 * REC_UPC), p);
-            bulk_s2cluster(dst, stage + (size_t)p * 64 * REC_UPC, KS_TILE_BYTES, mapa_shared(smem_u32(&redfull[par]), p));
+            const uint32_t dst = mapa_shared(smem_u32(red + (size_t)(par * (KS_CL - 1) + slot) * 64 * UPC), p);
+            bulk_s2cluster(dst, stage + (size_t)p * 64 * UPC, C::TILE, mapa_shared(smem_u32(&redfull[par]), p));
           }
           bulk_commit_group();
           PROBE(ti, 14);
         }
-        mbar_wait(&redfull[par], (nmma >> 1) & 1);
+        mbar_wait(&redfull[par], (nx >> 1) & 1);
         if (threadIdx.x == 0) PROBE(ti, 15);
 #pragma unroll
         for (int p = 0; p < KS_CL; ++p) {  // fixed order over the K-slices: deterministic
-          const float *src = p == rank ? stage + (size_t)rank * 64 * REC_UPC
-                                       : red + (size_t)(par * (KS_CL - 1) + (p < rank ? p : p - 1)) * 64 * REC_UPC;
-          const float4 *s4 = reinterpret_cast<const float4 *>(src + (size_t)eb * REC_UPC + 8 * eh);
-          const float4 v0 = s4[0], v1 = s4[1];
-          dh[0] += v0.x; dh[1] += v0.y; dh[2] += v0.z; dh[3] += v0.w;
-          dh[4] += v1.x; dh[5] += v1.y; dh[6] += v1.z; dh[7] += v1.w;
+          const float *src = p == rank ? stage + (size_t)rank * 64 * UPC
+                                       : red + (size_t)(par * (KS_CL - 1) + (p < rank ? p : p - 1)) * 64 * UPC;
+          const float4 *s4 = reinterpret_cast<const float4 *>(src + (size_t)eb * UPC + HU * eh);
+#pragma unroll
+          for (int q = 0; q < HU / 4; ++q) {
+            const float4 v = s4[q];
+            dh[4 * q] += v.x; dh[4 * q + 1] += v.y; dh[4 * q + 2] += v.z; dh[4 * q + 3] += v.w;
+          }
         }
       }
       const bool valid = !MASKED || t < len_b;
-      __align__(16) __nv_bfloat16 dzb[32];
+      __align__(16) __nv_bfloat16 dzb[4 * HU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < HU; ++u) {
         const float dhu = dh[u] + din[u] + carry[u];
         const float ig = gt[4 * u], fg = gt[4 * u + 1], gg = gt[4 * u + 2], og = gt[4 * u + 3];
         if (valid) {
@@ -849,29 +897,52 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         if (!valid || u >= nuh)
           dzb[4 * u] = dzb[4 * u + 1] = dzb[4 * u + 2] = dzb[4 * u + 3] = __float2bfloat16_rn(0.f);
       }
-      if (row) {  // exchange copy: row eb, granules 4 eh .. 4 eh + 3 of chunk blockIdx.x
-        uint8_t *chunk = dzsw + ((size_t)t * nk_all + blockIdx.x) * ly.cb;
+      if (row) {  // exchange copy: gate columns 4 ue .. 4 ue + 4 HU of row eb
+        const int col = 4 * ue;
+        uint8_t *chunk = dzsw + ((size_t)t * nk_all + (col >> 6)) * ly.cb;
+        const int g0 = (col & 63) >> 3;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          *reinterpret_cast<uint4 *>(chunk + sw128_off(eb, 4 * eh + k)) = reinterpret_cast<const uint4 *>(dzb)[k];
+        for (int k = 0; k < HU / 2; ++k)
+          *reinterpret_cast<uint4 *>(chunk + sw128_off(eb, g0 + k)) = reinterpret_cast<const uint4 *>(dzb)[k];
       }
       fence_proxy_async_global();
       if (threadIdx.x == 0) PROBE(ti, 6);
-      if (active) epi_publish(&flags[blockIdx.x], (unsigned)(T - t));
+      if (active) epi_publish(&flags[lcta], (unsigned)(T - t));
       if (threadIdx.x == 0) PROBE(ti, 7);
       if (row) {
-        uint4 *d4 = reinterpret_cast<uint4 *>(a.DZ + r * a.ldz + (size_t)blockIdx.x * 64 + 32 * eh);
+        uint4 *d4 = reinterpret_cast<uint4 *>(a.DZ + r * a.ldz + 4 * (size_t)ue);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
+        for (int k = 0; k < HU / 2; ++k) d4[k] = reinterpret_cast<const uint4 *>(dzb)[k];
       }
     }
-    if (has_next) ++nmma;
+    if (nstep > 0) ++nm;
+    if (has_x) ++nx;
+    q_ring += lys.nops;
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while a peer may still address its shared memory
   if (warp == 5) tmem_dealloc(tmem, 64 * REC_NMW);
+}
+
+template <bool MASKED>
+__global__ void __launch_bounds__(REC_THREADS, 1)
+    lstm_rec_bwd_ks_kernel(const __grid_constant__ CUtensorMap tmWT,  // W_hh^T [H x 4H], box {64,64}
+                           KsCtx cx, RecLayout ly) {
+  ks_body<REC_UPC, MASKED>(cx, &tmWT, &tmWT, ly);
+}
+
+// Backward wavefront of a 2-layer stack: CTAs [0, g1) run layer 1 (16 units), CTAs [g1, g1 + g0)
+// layer 0 (8 units), whose K space starts with layer 1's dz_t (W_ih1^T fused, no dgrad GEMM).
+template <bool MASKED>
+__global__ void __launch_bounds__(REC_THREADS, 1)
+    lstm_rec_bwd_wf_kernel(const __grid_constant__ CUtensorMap tmWT1,   // W_hh1^T, box {64,64}
+                           const __grid_constant__ CUtensorMap tmWihT1, // W_ih1^T, box {64,32}
+                           const __grid_constant__ CUtensorMap tmWT0,   // W_hh0^T, box {64,32}
+                           KsCtx c1, KsCtx c0, RecLayout ly1, RecLayout ly0) {
+  if ((int)blockIdx.x < c0.base) ks_body<REC_UPC, MASKED>(c1, &tmWT1, &tmWT1, ly1);
+  else ks_body<REC_UPC / 2, MASKED>(c0, &tmWihT1, &tmWT0, ly0);
 }
 
 // ---------------------------------------------------------------------------------- host
@@ -1005,24 +1076,9 @@ static cudaError_t lstm_rec_bwd_plain(const RecBwdArgs &a, const __nv_bfloat16 *
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
 
-static cudaError_t lstm_rec_bwd_ks(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
-                                   cudaStream_t st) {
-  const int nk_all = (4 * a.H + 63) / 64;
-  const int nkr = (nk_all + KS_CL - 1) / KS_CL;
-  RecLayout ly = layout(nkr * 8192, nkr, a.B, KS_RED_BYTES, true);  // B <= 64 here: M = 64 MMAs
-  if (ly.ch < 1 || smem_of(ly, KS_RED_BYTES) > 232448) return cudaErrorInvalidValue;
-  CUtensorMap tmWT;
-  if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 64)) return cudaErrorInvalidValue;
-  const int smem = smem_of(ly, KS_RED_BYTES);
-  const void *fn = masked ? (const void *)lstm_rec_bwd_ks_kernel<true, true> : (const void *)lstm_rec_bwd_ks_kernel<false, true>;
+static cudaError_t cluster_launch(const void *fn, int grid, int smem, void **args, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  if (e != cudaSuccess) return e;
-  RecBwdArgs aa = a;
-  int nka = nk_all;
-  void *args[] = {&tmWT, &aa, &ly, &nka};
-  const int grid = KS_CL * ((a.H + KS_UPC - 1) / KS_UPC);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(REC_THREADS);
@@ -1039,12 +1095,65 @@ static cudaError_t lstm_rec_bwd_ks(const RecBwdArgs &a, const __nv_bfloat16 *Whh
   // cooperative launch would guarantee it but cannot be combined with clusters under the
   // profiler's replay; check instead that the device can hold every cluster simultaneously
   // (one CTA per SM; the launch runs alone on the stream).
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg) != cudaSuccess) max_clusters = 0;
-  }
+  int max_clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg) != cudaSuccess) max_clusters = 0;
   if (grid / KS_CL > max_clusters) return cudaErrorCooperativeLaunchTooLarge;
   return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+template <int UPC>
+static RecLayout ks_layout(int nkt, int B) {
+  const int nkr = (nkt + KS_CL - 1) / KS_CL;
+  return layout(nkr * KsCfg<UPC>::WCH, nkr, B, KsCfg<UPC>::RED, true);  // B <= 64: M = 64 MMAs
+}
+
+static int ks_grid(int H, int upc) { return KS_CL * ((H + KS_CL * upc - 1) / (KS_CL * upc)); }
+
+static cudaError_t lstm_rec_bwd_ks(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
+                                   cudaStream_t st) {
+  const int nk_all = (4 * a.H + 63) / 64;
+  RecLayout ly = ks_layout<REC_UPC>(nk_all, a.B);
+  const int smem = smem_of(ly, KsCfg<REC_UPC>::RED);
+  if (ly.ch < 1 || smem > 232448) return cudaErrorInvalidValue;
+  CUtensorMap tmWT;
+  if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 64)) return cudaErrorInvalidValue;
+  const void *fn = masked ? (const void *)lstm_rec_bwd_ks_kernel<true> : (const void *)lstm_rec_bwd_ks_kernel<false>;
+  KsCtx cx = {};
+  cx.a = a;
+  cx.base = 0;
+  cx.nk_all = nk_all;
+  void *args[] = {&tmWT, &cx, &ly};
+  return cluster_launch(fn, ks_grid(a.H, REC_UPC), smem, args, st);
+}
+
+int rec_bwd_wf_grid(int H) { return ks_grid(H, REC_UPC) + ks_grid(H, REC_UPC / 2); }
+
+cudaError_t lstm_rec_bwd_wavefront(const RecBwdArgs &a1, const RecBwdArgs &a0, const __nv_bfloat16 *WhhT1,
+                                   const __nv_bfloat16 *WihT1, const __nv_bfloat16 *WhhT0, int ldwt,
+                                   bool masked, cudaStream_t st) {
+  if (a1.B > 64 || a1.B < 1 || a1.H != a0.H || !a1.DZsw || !a0.DZsw) return cudaErrorInvalidValue;
+  const int H = a1.H, nk_all = (4 * H + 63) / 64;
+  RecLayout ly1 = ks_layout<REC_UPC>(nk_all, a1.B);
+  RecLayout ly0 = ks_layout<REC_UPC / 2>(2 * nk_all, a1.B);
+  const int smem = std::max(smem_of(ly1, KsCfg<REC_UPC>::RED), smem_of(ly0, KsCfg<REC_UPC / 2>::RED));
+  if (ly1.ch < 1 || ly0.ch < 1 || smem > 232448) return cudaErrorInvalidValue;
+  CUtensorMap t1, ti, t0;
+  if (!make_tmap_bf16(&t1, WhhT1, 4ull * H, H, ldwt, 64) || !make_tmap_bf16(&ti, WihT1, 4ull * H, H, ldwt, 32) ||
+      !make_tmap_bf16(&t0, WhhT0, 4ull * H, H, ldwt, 32))
+    return cudaErrorInvalidValue;
+  const void *fn = masked ? (const void *)lstm_rec_bwd_wf_kernel<true> : (const void *)lstm_rec_bwd_wf_kernel<false>;
+  KsCtx c1 = {}, c0 = {};
+  c1.a = a1;
+  c1.base = 0;
+  c1.nk_all = nk_all;
+  c0.a = a0;
+  c0.base = ks_grid(H, REC_UPC);
+  c0.nk_all = nk_all;
+  c0.dzswA = a1.DZsw;
+  c0.flagsA = a1.barrier;
+  c0.nkA = nk_all;
+  void *args[] = {&t1, &ti, &t0, &c1, &c0, &ly1, &ly0};
+  return cluster_launch(fn, rec_bwd_wf_grid(H), smem, args, st);
 }
 
 cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,

@@ -56,6 +56,13 @@ int rec_fwd_wf_grid(int H);
 cudaError_t lstm_rec_fwd_wavefront(const RecFwdArgs &a0, const RecFwdArgs &a1, const __nv_bfloat16 *Whh0,
                                    const __nv_bfloat16 *Wih1, const __nv_bfloat16 *Whh1, int ldw,
                                    const float *bias1_il, bool masked, cudaStream_t st);
+// Backward of a 2-layer stack in one launch (wavefront: layer 0's step t runs with layer 1's step
+// t-1; W_ih1^T dz1_t, the dgrad of layer 1's input, is folded into layer 0's recurrent MMA, so
+// a0.dHin must be null). B <= 64. WihT1: W_ih1 transposed, gate-interleaved [H x ldwt] bf16.
+int rec_bwd_wf_grid(int H);
+cudaError_t lstm_rec_bwd_wavefront(const RecBwdArgs &a1, const RecBwdArgs &a0, const __nv_bfloat16 *WhhT1,
+                                   const __nv_bfloat16 *WihT1, const __nv_bfloat16 *WhhT0, int ldwt,
+                                   bool masked, cudaStream_t st);
 cudaError_t lstm_rec_bwd(const RecBwdArgs &a, const __nv_bfloat16 *WhhT, int ldwt, bool masked,
                          cudaStream_t st);
 
