@@ -400,9 +400,15 @@ def main():
     rec_ms = sum(r[0] for r in rec)
     rec_n = sum(r[2] for r in rec)
     rec_avg = rec_ms / max(1, rec_n)
-    rec_fl = 2.0 * B * 4 * 650 * 650 * (T - 1)
+    wave = any(r[1] == "rec_bwd01" for r in rec)
+    Hh = 650
+    # per launch: the recurrent products dh_t = W_hh^T dz_{t+1} (T-1 per layer) and, in the
+    # two-layer wavefront, the fused input dgrad W_ih1^T dz1_t (T of them), 2*B*4H*H flops each
+    rec_fl = 2.0 * B * 4 * Hh * Hh * ((T - 1) * 2 + T if wave else (T - 1))
     rec_ach = rec_fl / (rec_avg * 1e-3) / 1e12 if rec_avg else None
-    roofline = {"kernel": "rec_bwd (lstm_rec_bwd_ks_kernel, K-split clusters)", "bound": "tensor",
+    roofline = {"kernel": ("rec_bwd01 (lstm_rec_bwd_wf_kernel: both layers, K-split clusters)" if wave
+                           else "rec_bwd (lstm_rec_bwd_ks_kernel, K-split clusters)"),
+                "bound": "tensor",
                 "achieved": rec_ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": rec_ach / peak if rec_ach else None, "traffic": traffic("rec_bwd"),
                 "flops_per_launch": rec_fl, "avg_launch_ms": rec_avg,

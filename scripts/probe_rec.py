@@ -21,7 +21,10 @@ def report(buf):
     parts = [("fwd layer0", full[0, :g0])]
     if full[0, g0:, 1:-1, 7].any():  # wavefront launch: layer-1 CTAs follow
         parts.append(("fwd layer1 (wavefront)", full[0, g0:g0 + (H + 7) // 8]))
-    parts.append(("bwd", full[1, :NC]))
+    nb1 = 4 * ((H + 63) // 64)  # K-split clusters of layer 1 (or of the only layer)
+    parts.append(("bwd layer1 (or single layer)", full[1, :nb1]))
+    if full[1, nb1:, 1:-1, 7].any():  # backward wavefront: layer-0 CTAs follow
+        parts.append(("bwd layer0 (wavefront)", full[1, nb1:nb1 + 4 * ((H + 31) // 32)]))
     for dirn, a in parts:
         t0 = a[:, :, 0].min(axis=0)  # earliest CTA start of each step
         per = np.median(np.diff(t0))
