@@ -17,6 +17,7 @@
 // runs the epilogue — deterministic, and no CTA ever waits for another.
 // Tile t -> (split = t % splits, m-block fastest), CTA c takes t = c, c + grid, ...
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 #include "gemm_tc.h"
@@ -82,11 +83,43 @@ JN_DEV void store_row32(const GemmEpilogue &ep, int m, int n, int N, float (&v)[
   }
 }
 
+// Up to GB_MAX GEMMs with the same operand majors and tile width in one persistent launch
+// (grouped): their tiles are concatenated, so small GEMMs fill the machine together.
+constexpr int GB_MAX = 4;
+struct GemmBatch {
+  CUtensorMap ta[GB_MAX], tb[GB_MAX];
+  GemmEpilogue ep[GB_MAX];
+  int M[GB_MAX], N[GB_MAX], K[GB_MAX];
+  const int *K_dev[GB_MAX];
+  TileMap tm[GB_MAX];
+  unsigned *counters[GB_MAX];
+  float *partials[GB_MAX];
+  int tile_start[GB_MAX + 1];
+  int n;
+};
+
+struct TileRef {
+  int g, mb, nb, sp, kb0, kb1, tile;
+};
+
+template <int BN, int STAGES>
+JN_DEV TileRef tile_ref(const GemmBatch &gb, int t) {
+  TileRef r;
+  r.g = 0;
+  while (r.g + 1 < gb.n && t >= gb.tile_start[r.g + 1]) ++r.g;
+  const TileMap &tm = gb.tm[r.g];
+  tm.of(t - gb.tile_start[r.g], r.mb, r.nb, r.sp);
+  int K = gb.K[r.g];
+  if (gb.K_dev[r.g]) K = min(K, *gb.K_dev[r.g]);  // reduction length known only on the device
+  const int nk = (K + 63) / 64;
+  r.kb0 = (int)((long long)nk * r.sp / tm.splits);
+  r.kb1 = (int)((long long)nk * (r.sp + 1) / tm.splits);
+  r.tile = r.mb + tm.Mb * r.nb;
+  return r;
+}
+
 template <int BN, int A_MN, int B_MN, int STAGES>
-__global__ void __launch_bounds__(192, 1)
-    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, GemmEpilogue ep, int M, int N,
-                        int K, const int *K_dev, TileMap tm, unsigned *counters, float *partials) {
+__global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
   using C = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -100,12 +133,13 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (K_dev) K = min(K, *K_dev);  // reduction length known only on the device
-  const int nk = (K + C::BK - 1) / C::BK;
+  const int total = gb.tile_start[gb.n];
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    for (int g = 0; g < gb.n; ++g) {
+      tma_prefetch_desc(&gb.ta[g]);
+      tma_prefetch_desc(&gb.tb[g]);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -124,12 +158,11 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {  // ---------------- TMA producer (the warp loops together, lane 0 issues)
     int q = 0;       // ring position, continuous across tiles
-    for (int t = blockIdx.x; t < tm.total; t += gridDim.x) {
-      int mb, nb, sp;
-      tm.of(t, mb, nb, sp);
-      const int m0 = mb * C::BM, n0 = nb * BN;
-      const int kb0 = (int)((long long)nk * sp / tm.splits), kb1 = (int)((long long)nk * (sp + 1) / tm.splits);
-      for (int kb = kb0; kb < kb1; ++kb, ++q) {
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+      const CUtensorMap *tmA = &gb.ta[tr.g], *tmB = &gb.tb[tr.g];
+      const int m0 = tr.mb * C::BM, n0 = tr.nb * BN;
+      for (int kb = tr.kb0; kb < tr.kb1; ++kb, ++q) {
         const int s = q % STAGES, r = q / STAGES;
         if (lane == 0) {
           if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
@@ -137,16 +170,16 @@ __global__ void __launch_bounds__(192, 1)
           const int k0 = kb * C::BK;
           uint8_t *a = sA + s * C::A_BYTES, *b = sB + s * C::B_BYTES;
           if (!A_MN) {
-            tma_load_2d(a, &tmA, &full[s], k0, m0);
+            tma_load_2d(a, tmA, &full[s], k0, m0);
           } else {
-            tma_load_2d(a, &tmA, &full[s], m0, k0);
-            tma_load_2d(a + 8192, &tmA, &full[s], m0 + 64, k0);
+            tma_load_2d(a, tmA, &full[s], m0, k0);
+            tma_load_2d(a + 8192, tmA, &full[s], m0 + 64, k0);
           }
           if (!B_MN) {
-            tma_load_2d(b, &tmB, &full[s], k0, n0);
+            tma_load_2d(b, tmB, &full[s], k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[s], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, tmB, &full[s], n0 + 64 * j, k0);
           }
         }
         __syncwarp();
@@ -155,15 +188,13 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {  // ---------------- MMA issuer (the warp loops together, lane 0 issues)
     constexpr uint32_t idesc = umma_idesc_bf16(128, BN, A_MN, B_MN);
     int q = 0, i = 0;
-    for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++i) {
-      int mb, nb, sp;
-      tm.of(t, mb, nb, sp);
-      const int kb0 = (int)((long long)nk * sp / tm.splits), kb1 = (int)((long long)nk * (sp + 1) / tm.splits);
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+      const TileRef tr = tile_ref<BN, STAGES>(gb, t);
       const int buf = i & 1;
       if (i >= 2) mbar_wait(&tempty[buf], ((i >> 1) - 1) & 1);  // epilogue drained this buffer
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(buf * BN);
-      for (int kb = kb0; kb < kb1; ++kb, ++q) {
+      for (int kb = tr.kb0; kb < tr.kb1; ++kb, ++q) {
         const int s = q % STAGES, r = q / STAGES;
         mbar_wait(&full[s], r & 1);
         tc_fence_after();
@@ -175,7 +206,7 @@ __global__ void __launch_bounds__(192, 1)
                                      : umma_desc_sw128(a + j * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
                                      : umma_desc_sw128(b + j * 32, 16, 1024);
-            umma_bf16(acc, ad, bd, idesc, (kb != kb0 || j != 0) ? 1u : 0u);
+            umma_bf16(acc, ad, bd, idesc, (kb != tr.kb0 || j != 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
@@ -188,20 +219,20 @@ __global__ void __launch_bounds__(192, 1)
     // ---------------- epilogue: TMEM -> registers -> global (warps 2-5)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     int i = 0;
-    for (int t = blockIdx.x; t < tm.total; t += gridDim.x, ++i) {
-      int mb, nb, sp;
-      tm.of(t, mb, nb, sp);
-      const int m0 = mb * C::BM, n0 = nb * BN;
-      const int kb0 = (int)((long long)nk * sp / tm.splits), kb1 = (int)((long long)nk * (sp + 1) / tm.splits);
-      const bool empty_k = kb1 <= kb0;  // no MMA wrote the accumulator
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+      const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+      const GemmEpilogue &ep = gb.ep[tr.g];
+      const int M = gb.M[tr.g], N = gb.N[tr.g];
+      const int splits = gb.tm[tr.g].splits;
+      const int m0 = tr.mb * C::BM, n0 = tr.nb * BN;
+      const bool empty_k = tr.kb1 <= tr.kb0;  // no MMA wrote the accumulator
       const int buf = i & 1;
-      const int tile = mb + tm.Mb * nb;
       mbar_wait(&tfull[buf], (i >> 1) & 1);
       __syncwarp();
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const bool row_ok = m < M;
-      if (tm.splits == 1) {
+      if (splits == 1) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           const int n = n0 + c * 32;
@@ -220,7 +251,8 @@ __global__ void __launch_bounds__(192, 1)
       } else {
         // split-K: park this split's partial tile; the last split to arrive adds the splits in
         // order 0 .. splits-1 (deterministic) and runs the epilogue
-        float *pt = partials + ((size_t)tile * tm.splits + sp) * (128 * BN);
+        float *partials = gb.partials[tr.g];
+        float *pt = partials + ((size_t)tr.tile * splits + tr.sp) * (128 * BN);
         const int rl = quad * 32 + lane;  // tile-local row
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -240,11 +272,12 @@ __global__ void __launch_bounds__(192, 1)
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         __shared__ unsigned s_last;
-        if (warp == 2 && lane == 0) s_last = atomicInc(&counters[tile], (unsigned)tm.splits - 1) == (unsigned)tm.splits - 1;
+        if (warp == 2 && lane == 0)
+          s_last = atomicInc(&gb.counters[tr.g][tr.tile], (unsigned)splits - 1) == (unsigned)splits - 1;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (s_last) {
           __threadfence();
-          const float *p0 = partials + (size_t)tile * tm.splits * (128 * BN) + (size_t)rl * BN;
+          const float *p0 = partials + (size_t)tr.tile * splits * (128 * BN) + (size_t)rl * BN;
 #pragma unroll 1
           for (int c = 0; c < BN / 32; ++c) {
             const int n = n0 + c * 32;
@@ -252,8 +285,8 @@ __global__ void __launch_bounds__(192, 1)
             float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
-            for (int q = 0; q < tm.splits; ++q) {
-              const float4 *s4 = reinterpret_cast<const float4 *>(p0 + (size_t)q * (128 * BN) + c * 32);
+            for (int qq = 0; qq < splits; ++qq) {
+              const float4 *s4 = reinterpret_cast<const float4 *>(p0 + (size_t)qq * (128 * BN) + c * 32);
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const float4 x = __ldcg(s4 + j);
@@ -341,15 +374,9 @@ static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
 }
 
 template <int BN, int A_MN, int B_MN>
-static cudaError_t launch(const GemmOp &op, cudaStream_t st) {
+static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   constexpr int STAGES = BN == 256 ? 4 : 6;
   using C = GemmCfg<BN, STAGES>;
-  CUtensorMap ta, tb;
-  bool ok = A_MN ? make_tmap_bf16(&ta, op.A, op.M, op.K, op.lda, 64)
-                 : make_tmap_bf16(&ta, op.A, op.K, op.M, op.lda, 128);
-  ok = ok && (B_MN ? make_tmap_bf16(&tb, op.B, op.N, op.K, op.ldb, 64)
-                   : make_tmap_bf16(&tb, op.B, op.K, op.N, op.ldb, BN));
-  if (!ok) return cudaErrorInvalidValue;
   auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -363,47 +390,95 @@ static cudaError_t launch(const GemmOp &op, cudaStream_t st) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  TileMap tm;
-  tm.Mb = (op.M + 127) / 128;
-  tm.Nb = (op.N + BN - 1) / BN;
-  const int nk = (op.K + 63) / 64;
-  const size_t cap_tiles = op.partials ? op.partials_cap / (128 * BN) : 0;
-  int splits = 1;
-  if (op.flags && op.partials) {
-    splits = op.splits > 0 ? op.splits : choose_splits(tm.Mb * tm.Nb, nk, g_num_sms, cap_tiles);
-    splits = std::max(1, std::min(splits, 64));
-    if ((size_t)tm.Mb * tm.Nb * splits > cap_tiles) splits = 1;
+  GemmBatch gb;  // ~1.5 KB of kernel parameters (copied at launch)
+  memset(&gb, 0, sizeof(gb));
+  gb.n = n;
+  int total = 0;
+  for (int g = 0; g < n; ++g) {
+    const GemmOp &op = ops[g];
+    bool ok = A_MN ? make_tmap_bf16(&gb.ta[g], op.A, op.M, op.K, op.lda, 64)
+                   : make_tmap_bf16(&gb.ta[g], op.A, op.K, op.M, op.lda, 128);
+    ok = ok && (B_MN ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, 64)
+                     : make_tmap_bf16(&gb.tb[g], op.B, op.K, op.N, op.ldb, BN));
+    if (!ok) return cudaErrorInvalidValue;
+    TileMap &tm = gb.tm[g];
+    tm.Mb = (op.M + 127) / 128;
+    tm.Nb = (op.N + BN - 1) / BN;
+    const int nk = (op.K + 63) / 64;
+    const size_t cap_tiles = op.partials ? op.partials_cap / (128 * BN) : 0;
+    int splits = 1;
+    if (n == 1 && op.flags && op.partials) {  // split-K only for single launches (own scratch)
+      splits = op.splits > 0 ? op.splits : choose_splits(tm.Mb * tm.Nb, nk, g_num_sms, cap_tiles);
+      splits = std::max(1, std::min(splits, 64));
+      if ((size_t)tm.Mb * tm.Nb * splits > cap_tiles) splits = 1;
+    }
+    tm.splits = splits;
+    tm.total = tm.Mb * tm.Nb * splits;
+    gb.ep[g] = op.ep;
+    gb.M[g] = op.M; gb.N[g] = op.N; gb.K[g] = op.K;
+    gb.K_dev[g] = op.K_dev;
+    gb.counters[g] = op.flags;
+    gb.partials[g] = op.partials;
+    gb.tile_start[g] = total;
+    total += tm.total;
   }
-  tm.splits = splits;
-  tm.total = tm.Mb * tm.Nb * splits;
-  const int grid = std::min(tm.total, g_num_sms);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, op.ep, op.M, op.N, op.K, op.K_dev, tm, op.flags, op.partials);
+  gb.tile_start[n] = total;
+  if (total == 0) return cudaSuccess;
+  const int grid = std::min(total, g_num_sms);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(gb);
   return cudaGetLastError();
 }
 
-cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st) {
-  if (op.M <= 0 || op.N <= 0) return cudaSuccess;
+static cudaError_t check_op(const GemmOp &op) {
   if ((op.lda & 7) || (op.ldb & 7) || (reinterpret_cast<uintptr_t>(op.A) & 15) ||
       (reinterpret_cast<uintptr_t>(op.B) & 15))
     return cudaErrorInvalidValue;
-  // BN = 256 for wide outputs (one tcgen05.mma issue costs ~130 cycles whatever N is, see
-  // scripts/bench_mma.cu, so wide tiles keep the tensor pipe busiest); narrow outputs (N ~ H)
-  // take BN = 128 for twice the tiles
-  const bool wide = op.N >= 1024;
-#define JN_G(BN_, AM, BMJ) return launch<BN_, AM, BMJ>(op, st)
+  return cudaSuccess;
+}
+
+// BN = 256 for wide outputs (one tcgen05.mma issue costs ~130 cycles whatever N is, see
+// scripts/bench_mma.cu, so wide tiles keep the tensor pipe busiest); narrow outputs (N ~ H) take
+// BN = 128 for twice the tiles
+static bool wide_of(const GemmOp &op) { return op.N >= 1024; }
+
+cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st) {
+  GemmOp live[GB_MAX];
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    if (ops[i].M <= 0 || ops[i].N <= 0) continue;
+    const cudaError_t e = check_op(ops[i]);
+    if (e != cudaSuccess) return e;
+    live[m++] = ops[i];
+  }
+  if (m == 0) return cudaSuccess;
+  if (m > GB_MAX) return cudaErrorInvalidValue;
+  const bool wide = wide_of(live[0]);
+  const int am = live[0].a_mn, bm = live[0].b_mn;
+  bool same = true;
+  for (int i = 1; i < m; ++i) same = same && wide_of(live[i]) == wide && live[i].a_mn == am && live[i].b_mn == bm;
+  if (!same) {  // different kernel configurations: one launch each
+    for (int i = 0; i < m; ++i) {
+      const cudaError_t e = gemm_bf16_group(&live[i], 1, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+#define JN_G(BN_, AM, BMJ) return launch<BN_, AM, BMJ>(live, m, st)
   if (wide) {
-    if (!op.a_mn && !op.b_mn) JN_G(256, 0, 0);
-    if (!op.a_mn && op.b_mn) JN_G(256, 0, 1);
-    if (op.a_mn && !op.b_mn) JN_G(256, 1, 0);
+    if (!am && !bm) JN_G(256, 0, 0);
+    if (!am && bm) JN_G(256, 0, 1);
+    if (am && !bm) JN_G(256, 1, 0);
     JN_G(256, 1, 1);
   } else {
-    if (!op.a_mn && !op.b_mn) JN_G(128, 0, 0);
-    if (!op.a_mn && op.b_mn) JN_G(128, 0, 1);
-    if (op.a_mn && !op.b_mn) JN_G(128, 1, 0);
+    if (!am && !bm) JN_G(128, 0, 0);
+    if (!am && bm) JN_G(128, 0, 1);
+    if (am && !bm) JN_G(128, 1, 0);
     JN_G(128, 1, 1);
   }
 #undef JN_G
 }
+
+cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st) { return gemm_bf16_group(&op, 1, st); }
 
 size_t gemm_flags_count(int M, int N) { return (size_t)((M + 127) / 128) * ((N + 127) / 128); }
 

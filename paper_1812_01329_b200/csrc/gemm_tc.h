@@ -40,6 +40,9 @@ struct GemmOp {
 };
 
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);
+// Several GEMMs in one persistent launch (tiles concatenated; <= 4 ops). Ops sharing the kernel
+// configuration (operand majors, tile width) are grouped; split-K applies to single launches only.
+cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st);
 size_t gemm_flags_count(int M, int N);  // flags needed by a split-K launch of an M x N GEMM
 bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_outer);

@@ -540,23 +540,35 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     LCHK("rec_bwd01", lstm_rec_bwd_wavefront(bwd_args(1), r0, bf(p.off.WhhT_b[1]), bf(p.off.WihT_b1),
                                              bf(p.off.WhhT_b[0]), G4, p.while_mode, st));
   }
-  for (int l = L - 1; l >= 0; --l) {
+  auto wgrad_ops = [&](int l, GemmOp &a, GemmOp &b2) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
-    if (!bwd_wave)
-      LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(bwd_args(l), bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
     const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
-    GemmOp a;  // dW_hh = dz^T h_{t-1}
+    a = GemmOp();  // dW_hh = dz^T h_{t-1}
     a.M = G4; a.N = H; a.K = TB;
     a.A = bf(p.off.DZ[l]); a.lda = p.Gz; a.a_mn = 1;
     a.B = bf(p.off.Hs[l]); a.ldb = Hp; a.b_mn = 1;
     a.ep.C = fp(p.off.gWhh[l]); a.ep.ldc = Hp;
-    LCHK(l ? "gemm_dWhh1" : "gemm_dWhh0", gemm_bf16(with_flags(a), st));
-    GemmOp b2;  // dW_ih | db = dz^T [x | 1]
+    b2 = GemmOp();  // dW_ih | db = dz^T [x | 1]
     b2.M = G4; b2.N = In + 1; b2.K = TB;
     b2.A = bf(p.off.DZ[l]); b2.lda = p.Gz; b2.a_mn = 1;
     b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
     b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
-    LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(with_flags(b2), st));
+  };
+  if (bwd_wave) {  // the four weight-gradient GEMMs of both layers in one grouped launch
+    GemmOp ops[4];
+    wgrad_ops(1, ops[0], ops[1]);
+    wgrad_ops(0, ops[2], ops[3]);
+    LCHK("gemm_dW", gemm_bf16_group(ops, 4, st));
+  }
+  for (int l = L - 1; l >= 0; --l) {
+    const int In = l ? H : E, Inp = l ? Hp : Ep;
+    if (!bwd_wave) {
+      LCHK(l ? "rec_bwd1" : "rec_bwd0", lstm_rec_bwd(bwd_args(l), bf(p.off.WhhT_b[l]), G4, p.while_mode, st));
+      GemmOp a, b2;
+      wgrad_ops(l, a, b2);
+      LCHK(l ? "gemm_dWhh1" : "gemm_dWhh0", gemm_bf16(with_flags(a), st));
+      LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(with_flags(b2), st));
+    }
     if ((l > 0 && !bwd_wave) || (l == 0 && p.lr_E != 0)) {
       GemmOp c2;  // dx = dz W_ih
       c2.M = TB; c2.N = In; c2.K = G4;
