@@ -85,9 +85,10 @@ JN_DEV void store_row32(const GemmEpilogue &ep, int m, int n, int N, float (&v)[
 
 // Up to GB_MAX GEMMs with the same operand majors and tile width in one persistent launch
 // (grouped): their tiles are concatenated, so small GEMMs fill the machine together.
-constexpr int GB_MAX = 4;
+constexpr int GB_MAX = 8;
 struct GemmBatch {
   CUtensorMap ta[GB_MAX], tb[GB_MAX];
+  int amn[GB_MAX], bmn[GB_MAX];  // operand majors per GEMM (runtime: one kernel serves all four)
   GemmEpilogue ep[GB_MAX];
   int M[GB_MAX], N[GB_MAX], K[GB_MAX];
   const int *K_dev[GB_MAX];
@@ -118,7 +119,7 @@ JN_DEV TileRef tile_ref(const GemmBatch &gb, int t) {
   return r;
 }
 
-template <int BN, int A_MN, int B_MN, int STAGES>
+template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
   using C = GemmCfg<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const TileRef tr = tile_ref<BN, STAGES>(gb, t);
       const CUtensorMap *tmA = &gb.ta[tr.g], *tmB = &gb.tb[tr.g];
+      const bool A_MN = gb.amn[tr.g], B_MN = gb.bmn[tr.g];
       const int m0 = tr.mb * C::BM, n0 = tr.nb * BN;
       for (int kb = tr.kb0; kb < tr.kb1; ++kb, ++q) {
         const int s = q % STAGES, r = q / STAGES;
@@ -186,10 +188,11 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
       }
     }
   } else if (warp == 1) {  // ---------------- MMA issuer (the warp loops together, lane 0 issues)
-    constexpr uint32_t idesc = umma_idesc_bf16(128, BN, A_MN, B_MN);
     int q = 0, i = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
       const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+      const int A_MN = gb.amn[tr.g], B_MN = gb.bmn[tr.g];
+      const uint32_t idesc = umma_idesc_bf16(128, BN, A_MN, B_MN);
       const int buf = i & 1;
       if (i >= 2) mbar_wait(&tempty[buf], ((i >> 1) - 1) & 1);  // epilogue drained this buffer
       tc_fence_after();
@@ -373,11 +376,11 @@ static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
   return best;
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN>
 static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   constexpr int STAGES = BN == 256 ? 4 : 6;
   using C = GemmCfg<BN, STAGES>;
-  auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, STAGES>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -396,10 +399,12 @@ static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   int total = 0;
   for (int g = 0; g < n; ++g) {
     const GemmOp &op = ops[g];
-    bool ok = A_MN ? make_tmap_bf16(&gb.ta[g], op.A, op.M, op.K, op.lda, 64)
-                   : make_tmap_bf16(&gb.ta[g], op.A, op.K, op.M, op.lda, 128);
-    ok = ok && (B_MN ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, 64)
-                     : make_tmap_bf16(&gb.tb[g], op.B, op.K, op.N, op.ldb, BN));
+    bool ok = op.a_mn ? make_tmap_bf16(&gb.ta[g], op.A, op.M, op.K, op.lda, 64)
+                      : make_tmap_bf16(&gb.ta[g], op.A, op.K, op.M, op.lda, 128);
+    ok = ok && (op.b_mn ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, 64)
+                        : make_tmap_bf16(&gb.tb[g], op.B, op.K, op.N, op.ldb, BN));
+    gb.amn[g] = op.a_mn ? 1 : 0;
+    gb.bmn[g] = op.b_mn ? 1 : 0;
     if (!ok) return cudaErrorInvalidValue;
     TileMap &tm = gb.tm[g];
     tm.Mb = (op.M + 127) / 128;
@@ -452,30 +457,19 @@ cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st) {
   }
   if (m == 0) return cudaSuccess;
   if (m > GB_MAX) return cudaErrorInvalidValue;
-  const bool wide = wide_of(live[0]);
-  const int am = live[0].a_mn, bm = live[0].b_mn;
-  bool same = true;
-  for (int i = 1; i < m; ++i) same = same && wide_of(live[i]) == wide && live[i].a_mn == am && live[i].b_mn == bm;
-  if (!same) {  // different kernel configurations: one launch each
-    for (int i = 0; i < m; ++i) {
-      const cudaError_t e = gemm_bf16_group(&live[i], 1, st);
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+  // group by tile width (the operand majors are per-GEMM runtime properties of the kernel)
+  GemmOp wide[GB_MAX], narrow[GB_MAX];
+  int nw = 0, nn = 0;
+  for (int i = 0; i < m; ++i) {
+    if (wide_of(live[i])) wide[nw++] = live[i];
+    else narrow[nn++] = live[i];
   }
-#define JN_G(BN_, AM, BMJ) return launch<BN_, AM, BMJ>(live, m, st)
-  if (wide) {
-    if (!am && !bm) JN_G(256, 0, 0);
-    if (!am && bm) JN_G(256, 0, 1);
-    if (am && !bm) JN_G(256, 1, 0);
-    JN_G(256, 1, 1);
-  } else {
-    if (!am && !bm) JN_G(128, 0, 0);
-    if (!am && bm) JN_G(128, 0, 1);
-    if (am && !bm) JN_G(128, 1, 0);
-    JN_G(128, 1, 1);
+  if (nw) {
+    const cudaError_t e = launch<256>(wide, nw, st);
+    if (e != cudaSuccess) return e;
   }
-#undef JN_G
+  if (nn) return launch<128>(narrow, nn, st);
+  return cudaSuccess;
 }
 
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st) { return gemm_bf16_group(&op, 1, st); }

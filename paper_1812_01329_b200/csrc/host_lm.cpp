@@ -502,15 +502,21 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.ep.C = fp(p.off.logits); op.ep.ldc = Vp; op.ep.bias_col = P.bdec;
     LCHK("gemm_dec", gemm_bf16(with_flags(op), st));
   }
+  // two layers, B <= 64: one backward wavefront launch (layer 0 one step behind layer 1, the
+  // dgrad of layer 1's input W_ih1^T dz1_t folded into layer 0's recurrent MMA)
+  const char *bwf_env = getenv("JANUS_REC_BWD_WF");
+  const char *bk_env = getenv("JANUS_REC_BWD");
+  const bool bwd_wave = L == 2 && B <= 64 && !(bwf_env && bwf_env[0] == '0') && !(bk_env && bk_env[0] == 'p') &&
+                        rec_bwd_wf_grid(H) <= 148;
+  GemmOp dwdec;  // dW_dec | db_dec = dy^T [h_top | 1]
+  dwdec.M = V; dwdec.N = H + 1; dwdec.K = TB;
+  dwdec.A = bf(p.off.dy); dwdec.lda = Vp; dwdec.a_mn = 1;
+  dwdec.B = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; dwdec.ldb = Hp; dwdec.b_mn = 1;
+  dwdec.ep.C = fp(p.off.gWdec); dwdec.ep.ldc = Hp;
   LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
                    (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
   {
-    GemmOp op;  // dW_dec | db_dec = dy^T [h_top | 1]
-    op.M = V; op.N = H + 1; op.K = TB;
-    op.A = bf(p.off.dy); op.lda = Vp; op.a_mn = 1;
-    op.B = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.ldb = Hp; op.b_mn = 1;
-    op.ep.C = fp(p.off.gWdec); op.ep.ldc = Hp;
-    LCHK("gemm_dWdec", gemm_bf16(with_flags(op), st));
+    if (!bwd_wave) LCHK("gemm_dWdec", gemm_bf16(with_flags(dwdec), st));  // else grouped below
     GemmOp o2;  // dh_top = dy W_dec
     o2.M = TB; o2.N = H; o2.K = V;
     o2.A = bf(p.off.dy); o2.lda = Vp;
@@ -518,12 +524,6 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
     LCHK("gemm_dh", gemm_bf16(with_flags(o2), st));
   }
-  // two layers, B <= 64: one backward wavefront launch (layer 0 one step behind layer 1, the
-  // dgrad of layer 1's input W_ih1^T dz1_t folded into layer 0's recurrent MMA)
-  const char *bwf_env = getenv("JANUS_REC_BWD_WF");
-  const char *bk_env = getenv("JANUS_REC_BWD");
-  const bool bwd_wave = L == 2 && B <= 64 && !(bwf_env && bwf_env[0] == '0') && !(bk_env && bk_env[0] == 'p') &&
-                        rec_bwd_wf_grid(H) <= 148;
   auto bwd_args = [&](int l) {
     RecBwdArgs rb;
     rb.B = B; rb.H = H; rb.T = Tw; rb.T_dev = Tdev; rb.lens = p.while_mode ? P.lens : nullptr;
@@ -554,11 +554,23 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
     b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
   };
-  if (bwd_wave) {  // the four weight-gradient GEMMs of both layers in one grouped launch
-    GemmOp ops[4];
-    wgrad_ops(1, ops[0], ops[1]);
-    wgrad_ops(0, ops[2], ops[3]);
-    LCHK("gemm_dW", gemm_bf16_group(ops, 4, st));
+  if (bwd_wave) {  // every weight gradient + the embedding dgrad in one grouped launch
+    GemmOp ops[6];
+    int n = 0;
+    ops[n++] = dwdec;
+    wgrad_ops(1, ops[n], ops[n + 1]);
+    n += 2;
+    wgrad_ops(0, ops[n], ops[n + 1]);
+    n += 2;
+    if (p.lr_E != 0) {
+      GemmOp &c2 = ops[n++];  // dx0 = dz0 W_ih0 (embedding gradient rows)
+      c2 = GemmOp();
+      c2.M = TB; c2.N = E; c2.K = G4;
+      c2.A = bf(p.off.DZ[0]); c2.lda = p.Gz;
+      c2.B = bf(p.off.Wih_b[0]); c2.ldb = Ep; c2.b_mn = 1;
+      c2.ep.C = fp(p.off.dX[0]); c2.ep.ldc = Ep;
+    }
+    LCHK("gemm_wgrad", gemm_bf16_group(ops, n, st));
   }
   for (int l = L - 1; l >= 0; --l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
@@ -569,7 +581,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       LCHK(l ? "gemm_dWhh1" : "gemm_dWhh0", gemm_bf16(with_flags(a), st));
       LCHK(l ? "gemm_dWih1" : "gemm_dWih0", gemm_bf16(with_flags(b2), st));
     }
-    if ((l > 0 && !bwd_wave) || (l == 0 && p.lr_E != 0)) {
+    if (!bwd_wave && (l > 0 || p.lr_E != 0)) {
       GemmOp c2;  // dx = dz W_ih
       c2.M = TB; c2.N = In; c2.K = G4;
       c2.A = bf(p.off.DZ[l]); c2.lda = p.Gz;
