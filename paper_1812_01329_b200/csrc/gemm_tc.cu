@@ -55,19 +55,30 @@ JN_DEV void store_row32(const GemmEpilogue &ep, int m, int n, int N, float (&v)[
   if (ep.C) {
     float *dst = ep.C + (size_t)m * ep.ldc + n;
     if (n + 32 <= N && (ep.ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      // every load (bias, old C) is issued before the first store: the stores may alias them in
+      // the compiler's view, and interleaving would serialise eight load latencies per call
+      float4 add[8];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        if (ep.bias_col) {
-          const float4 bb = *reinterpret_cast<const float4 *>(ep.bias_col + n + j);
-          o.x += bb.x; o.y += bb.y; o.z += bb.z; o.w += bb.w;
-        }
-        if (ep.accumulate) {
-          const float4 old = *reinterpret_cast<const float4 *>(dst + j);
-          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-        }
-        *reinterpret_cast<float4 *>(dst + j) = o;
+      for (int j = 0; j < 8; ++j) add[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ep.bias_col) {
+        const float4 *b4 = reinterpret_cast<const float4 *>(ep.bias_col + n);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) add[j] = __ldg(b4 + j);
       }
+      if (ep.accumulate) {
+        const float4 *o4 = reinterpret_cast<const float4 *>(dst);
+        float4 old[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) old[j] = o4[j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          add[j].x += old[j].x; add[j].y += old[j].y; add[j].z += old[j].z; add[j].w += old[j].w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        reinterpret_cast<float4 *>(dst)[j] = make_float4(v[4 * j] + add[j].x, v[4 * j + 1] + add[j].y,
+                                                         v[4 * j + 2] + add[j].z, v[4 * j + 3] + add[j].w);
     } else {
       for (int j = 0; j < 32 && n + j < N; ++j) {
         float o = v[j] + (ep.bias_col ? ep.bias_col[n + j] : 0.f);
