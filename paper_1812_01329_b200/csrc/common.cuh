@@ -70,6 +70,20 @@ JN_DEV void tma_load_2d_mc(void *smem_dst, const CUtensorMap *m, uint64_t *bar, 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
+// 2-D tile store / reduce-add from shared memory (bulk async group: commit + wait_group.read
+// before the staging buffer is rewritten)
+JN_DEV void tma_store_2d(const CUtensorMap *m, const void *smem_src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+JN_DEV void tma_reduce_add_2d(const CUtensorMap *m, const void *smem_src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 // plain bulk copy global -> shared (contiguous bytes, multiple of 16), completes on an mbarrier
 JN_DEV void bulk_load(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -212,6 +226,7 @@ JN_DEV void bulk_s2cluster(uint32_t dst_caddr, const void *src, uint32_t bytes, 
       : "memory");
 }
 JN_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+JN_DEV void bulk_wait_group_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 JN_DEV void bulk_wait_group_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // arrive (release, cluster scope) on an mbarrier given by its shared::cluster address
 JN_DEV void mbar_arrive_cluster(uint32_t cbar) {

@@ -24,13 +24,17 @@
 
 namespace jk {
 
+bool make_tmap_f32_box32(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t ld);
+
 template <int BN, int STAGES>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // epilogue staging for TMA stores: per epilogue warp two 32 x 32 fp32 boxes (double buffer)
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 192;
 };
 
@@ -99,6 +103,8 @@ JN_DEV void store_row32(const GemmEpilogue &ep, int m, int n, int N, float (&v)[
 constexpr int GB_MAX = 8;
 struct GemmBatch {
   CUtensorMap ta[GB_MAX], tb[GB_MAX];
+  CUtensorMap tc[GB_MAX];        // fp32 D, box {32, 32}, 128-B swizzle (TMA-store epilogue)
+  int tma_store[GB_MAX];         // 1: epilogue through tc (fp32 D only, no bf16 copy)
   int amn[GB_MAX], bmn[GB_MAX];  // operand majors per GEMM (runtime: one kernel serves all four)
   GemmEpilogue ep[GB_MAX];
   int M[GB_MAX], N[GB_MAX], K[GB_MAX];
@@ -138,7 +144,8 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
                                               ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + STAGES * C::A_BYTES;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t *epi_stage = smem + STAGES * C::STAGE_BYTES;  // [4 warps][2][32 rows][128 B], swizzled
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE_BYTES + C::EPI_BYTES);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;  // [2]
   uint64_t *tempty = tfull + 2;      // [2]
@@ -151,6 +158,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
     for (int g = 0; g < gb.n; ++g) {
       tma_prefetch_desc(&gb.ta[g]);
       tma_prefetch_desc(&gb.tb[g]);
+      if (gb.tma_store[g]) tma_prefetch_desc(&gb.tc[g]);
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -246,7 +254,61 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const bool row_ok = m < M;
-      if (splits == 1) {
+      if (splits == 1 && gb.tma_store[tr.g]) {
+        // TMA-store epilogue: each 32 x 32 block of this warp's rows goes registers -> swizzled
+        // smem box -> one bulk tensor store (or reduce-add when accumulating), asynchronously;
+        // two boxes per warp alternate (wait_group.read 1 before a box is rewritten)
+        uint8_t *stg0 = epi_stage + (size_t)(warp - 2) * 2 * 4096;
+        const int mrow0 = m0 + quad * 32;
+        const float bv = (ep.bias_row && row_ok) ? ep.bias_row[m] : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int n = n0 + c * 32;
+          if (n >= N) break;  // warp-uniform
+          float v[32];
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * BN + c * 32, v);
+          if (empty_k) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          }
+          if (ep.bias_col) {
+            float4 bb[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              bb[j] = n + 4 * j + 3 < N ? __ldg(reinterpret_cast<const float4 *>(ep.bias_col + n) + j)
+                                        : make_float4(n + 4 * j < N ? ep.bias_col[n + 4 * j] : 0.f,
+                                                      n + 4 * j + 1 < N ? ep.bias_col[n + 4 * j + 1] : 0.f,
+                                                      n + 4 * j + 2 < N ? ep.bias_col[n + 4 * j + 2] : 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              v[4 * j] += bb[j].x; v[4 * j + 1] += bb[j].y; v[4 * j + 2] += bb[j].z; v[4 * j + 3] += bb[j].w;
+            }
+          }
+          if (ep.bias_row) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += bv;
+          }
+          uint8_t *stg = stg0 + (c & 1) * 4096;
+          if (lane == 0 && c >= 2) bulk_wait_group_read1();  // this box's previous store has read it
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)  // row `lane`, 16-B granule j at its 128-B-swizzled slot
+            *reinterpret_cast<float4 *>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            if (ep.accumulate) tma_reduce_add_2d(&gb.tc[tr.g], stg, n, mrow0);
+            else tma_store_2d(&gb.tc[tr.g], stg, n, mrow0);
+            bulk_commit_group();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) bulk_wait_group_read0();  // both boxes free before the next tile
+        __syncwarp();
+      } else if (splits == 1) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           const int n = n0 + c * 32;
@@ -313,6 +375,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
       }
     }
   }
+  if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 2 * BN);
@@ -353,6 +416,20 @@ bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t ou
   return r == CUDA_SUCCESS;
 }
 
+// 2-D fp32 tensor map for the TMA-store epilogue: box {32 columns, 32 rows}, 128-B swizzle
+// (a 32-float row is exactly one 128-B swizzle row). Out-of-bounds box parts are not written.
+bool make_tmap_f32_box32(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t ld) {
+  if (!get_encode()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 3-D view of a row-major bf16 matrix as {64 columns, rows, column chunks}: one TMA op then
 // fetches `box_chunks` consecutive 64-column chunks of `box_rows` rows, landing chunk-major in
 // shared memory (each chunk = box_rows x 128 B, 128-B swizzled) — the K-major UMMA layout.
@@ -372,6 +449,7 @@ bool make_tmap_bf16_chunks(CUtensorMap *m, const void *ptr, uint64_t rows, uint6
 }
 
 static int g_num_sms = 0;
+static bool g_tma_store_ok = getenv("JANUS_GEMM_TMA_STORE") == nullptr || getenv("JANUS_GEMM_TMA_STORE")[0] != '0';
 
 // K splits: the fewest persistent rounds per unit of work, each split >= 4 k-blocks, and the
 // partial tiles must fit the caller's scratch
@@ -417,6 +495,10 @@ static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
     gb.amn[g] = op.a_mn ? 1 : 0;
     gb.bmn[g] = op.b_mn ? 1 : 0;
     if (!ok) return cudaErrorInvalidValue;
+    gb.tma_store[g] = 0;
+    if (op.ep.C && !op.ep.Cb && (op.ep.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(op.ep.C) & 15) == 0 &&
+        g_tma_store_ok)
+      gb.tma_store[g] = make_tmap_f32_box32(&gb.tc[g], op.ep.C, op.N, op.M, op.ep.ldc) ? 1 : 0;
     TileMap &tm = gb.tm[g];
     tm.Mb = (op.M + 127) / 128;
     tm.Nb = (op.N + BN - 1) / BN;
