@@ -534,10 +534,18 @@ static cudaError_t check_op(const GemmOp &op) {
   return cudaSuccess;
 }
 
-// BN = 256 for wide outputs (one tcgen05.mma issue costs ~130 cycles whatever N is, see
-// scripts/bench_mma.cu, so wide tiles keep the tensor pipe busiest); narrow outputs (N ~ H) take
-// BN = 128 for twice the tiles
-static bool wide_of(const GemmOp &op) { return op.N >= 1024; }
+// Tile width: one tcgen05.mma issue costs ~130 cycles whatever N is (scripts/bench_mma.cu), so
+// BN = 256 tiles keep the tensor pipe busiest — as long as the launch still has enough tiles to
+// occupy the SMs (else BN = 128 for twice the tiles). Decided per launch (grouped GEMMs together).
+static bool wide_of(const GemmOp &op) { return op.N > 128; }
+static bool use_bn256(const GemmOp *ops, int n) {
+  long tiles = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!wide_of(ops[i])) return false;
+    tiles += (long)((ops[i].M + 127) / 128) * ((ops[i].N + 255) / 256);
+  }
+  return tiles >= 100;
+}
 
 cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st) {
   GemmOp live[GB_MAX];
@@ -550,19 +558,9 @@ cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st) {
   }
   if (m == 0) return cudaSuccess;
   if (m > GB_MAX) return cudaErrorInvalidValue;
-  // group by tile width (the operand majors are per-GEMM runtime properties of the kernel)
-  GemmOp wide[GB_MAX], narrow[GB_MAX];
-  int nw = 0, nn = 0;
-  for (int i = 0; i < m; ++i) {
-    if (wide_of(live[i])) wide[nw++] = live[i];
-    else narrow[nn++] = live[i];
-  }
-  if (nw) {
-    const cudaError_t e = launch<256>(wide, nw, st);
-    if (e != cudaSuccess) return e;
-  }
-  if (nn) return launch<128>(narrow, nn, st);
-  return cudaSuccess;
+  // one launch for the whole group (the operand majors are per-GEMM runtime properties)
+  if (use_bn256(live, m)) return launch<256>(live, m, st);
+  return launch<128>(live, m, st);
 }
 
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st) { return gemm_bf16_group(&op, 1, st); }
