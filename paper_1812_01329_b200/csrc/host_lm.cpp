@@ -189,7 +189,7 @@ bool lower_lm(Graph &g, std::string &why) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
   p.off.status = take(sizeof(DevStatus));
-  p.nbar = 256 * 8;  // per-CTA step flags: 256 CTAs x (L <= 4 layers) x 2 directions
+  p.nbar = rec_flag_words(256) * 8;  // per-CTA step flags: 256 CTAs x (L <= 4 layers) x 2 directions
   if ((p.H + 15) / 16 > 256) { why = "hidden size > 4096"; return false; }
   p.off.barriers = take(p.nbar * sizeof(unsigned));
   p.off.stage_args = take(3ull * p.B * p.T * sizeof(int));
@@ -433,7 +433,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     o.partials_cap = (size_t)GEMM_PART_TILES * 128 * 256;
     return o;
   };
-  LCHK("init", launch_step_init(dst, bars, p.nbar, st));
+  LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
   if (p.while_mode) LCHK("trip", launch_trip(P.lens, B, Tw, dst, st));
   if (gl.n) LCHK("guards", launch_guards(gl, dst, st));
   // operand copies (R1): interleaved / transposed bf16 working copies of the fp32 masters, the
@@ -473,7 +473,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     ra.Hsw = bf(p.off.Hsw[l]);
     ra.G = fp(p.off.G[l]); ra.Hs = bf(p.off.Hs[l]); ra.Cs = fp(p.off.Cs[l]); ra.ldh = Hp;
     ra.h0 = P.h[l]; ra.c0 = P.c[l]; ra.hT = fp(p.off.hT[l]); ra.cT = fp(p.off.cT[l]);
-    ra.barrier = bars + 256 * l; ra.fail = nullptr;
+    ra.barrier = bars + rec_flag_words(256) * l; ra.fail = nullptr;
     ra.dbg = (l == 0 || wavefront) ? g.probe : nullptr;  // indexed by the launch's CTA index
     ra.tag = p.tag_specialised ? nullptr : P.tag;
     return ra;
@@ -530,7 +530,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     rb.G = fp(p.off.G[l]); rb.Cs = fp(p.off.Cs[l]); rb.ldh = Hp;
     rb.dHin = l == L - 1 ? fp(p.off.dHtop) : fp(p.off.dX[l + 1]); rb.ldd = Hp;
     rb.DZsw = bf(p.off.DZsw[l]);
-    rb.DZ = bf(p.off.DZ[l]); rb.ldz = p.Gz; rb.barrier = bars + 256 * (L + l);
+    rb.DZ = bf(p.off.DZ[l]); rb.ldz = p.Gz; rb.barrier = bars + rec_flag_words(256) * (L + l);
     rb.dbg = ((l == 0 || bwd_wave) && g.probe) ? g.probe + (size_t)128 * 16 * p.T : nullptr;
     return rb;
   };
@@ -655,7 +655,7 @@ janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &w
   uint8_t *W = static_cast<uint8_t *>(ws.data);
   DevStatus *dst = reinterpret_cast<DevStatus *>(W + p.off.status);
   unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
-  LCHK("init", launch_step_init(dst, bars, p.nbar, st));
+  LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
   LCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
   r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + p.off.arena_begin),
                        (p.off.arena_end - p.off.arena_begin) / 4, st);

@@ -39,6 +39,10 @@ JN_DEV float tanh_f(float x) {
   return copysignf(t, x);
 }
 
+// Step flags are REC_FS words apart (one 128-B line each): a CTA's release store then shares its
+// line with no other producer while ~100 consumers poll.
+constexpr int REC_FS = 32;
+
 // Dataflow synchronisation between the CTAs of a recurrent launch. Every step writes a fresh row
 // block (h_t / dz_t), so there are no write-after-read hazards — only read-after-write: a CTA
 // publishes "my slice of step t is written" with a release store of its per-CTA flag, and the
@@ -52,14 +56,11 @@ JN_DEV void publish_flag(unsigned int *flag, unsigned int v) {
 // bulk copies lane 0 issues next.
 JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
   const int lane = threadIdx.x & 31;
-  for (int c = 2 * lane; c < n; c += 64) {
-    unsigned long long x;
-    unsigned lo, hi;
+  for (int c = lane; c < n; c += 32) {
+    unsigned x;
     do {
-      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(x) : "l"(flags + c) : "memory");
-      lo = (unsigned)x;
-      hi = c + 1 < n ? (unsigned)(x >> 32) : v;
-    } while (lo < v || hi < v);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
+    } while (x < v);
   }
   __syncwarp();
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -202,7 +203,7 @@ JN_DEV void wait_flag_set(const unsigned int *flags, int n, unsigned int v) {
   for (int c = lane; c < n; c += 32) {
     unsigned x;
     do {
-      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
     } while (x < v);
   }
 }
@@ -294,7 +295,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
   unsigned int *flags = a.barrier;  // flags[c] = 1 + last step whose h block CTA c has written
   fence_proxy_async_global();
-  publish_flag(&flags[cx.cta], 1);
+  publish_flag(&flags[cx.cta * REC_FS], 1);
   const int T = a.T_dev ? *a.T_dev : a.T;
   constexpr uint32_t idesc = umma_idesc_bf16(M64 ? 64 : 128, NG, 0, 0);
   const int nacc = min(REC_NMW, nk);  // accumulator tiles in use
@@ -382,7 +383,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       if (row) write_x(t + 1, hb);
       fence_proxy_async_global();
       if (threadIdx.x == 0) PROBE(t, 6);
-      epi_publish(&flags[cx.cta], (unsigned)t + 2);
+      epi_publish(&flags[cx.cta * REC_FS], (unsigned)t + 2);
       if (threadIdx.x == 0) PROBE(t, 7);
       if (row) {
         const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       }
       fence_proxy_async_global();
       if (threadIdx.x == 0) PROBE(ti, 6);
-      epi_publish(&flags[blockIdx.x], (unsigned)(T - t));
+      epi_publish(&flags[blockIdx.x * REC_FS], (unsigned)(T - t));
       if (threadIdx.x == 0) PROBE(ti, 7);
       if (row) {  // ldz >= 64 * grid: padding columns get the zeros computed for the padding units
         uint4 *d4 = reinterpret_cast<uint4 *>(a.DZ + r * a.ldz + (size_t)blockIdx.x * 64);
@@ -748,7 +749,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
           for (int c = s0 + lane; c < s0 + na; c += 32) {
             unsigned x;
             do {
-              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(cx.flagsA + c) : "memory");
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(cx.flagsA + c * REC_FS) : "memory");
             } while (x < (unsigned)(T - t));
           }
           __syncwarp();
@@ -761,7 +762,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
           for (int c = p0 + lane; c < p1; c += 32) {
             unsigned x;
             do {
-              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c) : "memory");
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
             } while (x < (unsigned)(T - 1 - t));
           }
           __syncwarp();
@@ -907,7 +908,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
       }
       fence_proxy_async_global();
       if (threadIdx.x == 0) PROBE(ti, 6);
-      if (active) epi_publish(&flags[lcta], (unsigned)(T - t));
+      if (active) epi_publish(&flags[lcta * REC_FS], (unsigned)(T - t));
       if (threadIdx.x == 0) PROBE(ti, 7);
       if (row) {
         uint4 *d4 = reinterpret_cast<uint4 *>(a.DZ + r * a.ldz + 4 * (size_t)ue);

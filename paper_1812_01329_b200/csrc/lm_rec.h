@@ -16,7 +16,7 @@ struct RecFwdArgs {
   int ldh = 0;
   const float *h0 = nullptr, *c0 = nullptr;  // [B][H] initial state (fp32)
   float *hT = nullptr, *cT = nullptr;        // [B][H] final state (fp32)
-  unsigned int *barrier = nullptr;           // zeroed before the launch
+  unsigned int *barrier = nullptr;           // zeroed before the launch: rec_flag_words(grid) u32
   const int *fail = nullptr;                 // nonzero: skip (cooperative cancellation)
   const int *tag = nullptr;                  // state type tag; != 1 -> h0 = c0 = 0 (device Switch)
   unsigned long long *dbg = nullptr;         // optional %globaltimer probe of CTA 0 (8 per step)
@@ -41,6 +41,9 @@ struct RecBwdArgs {
   unsigned long long *dbg = nullptr;
   __nv_bfloat16 *DZsw = nullptr;  // exchange copy of dz: [T][nk chunks][Bp rows][128 B] swizzled
 };
+
+// step-flag words a launch of `ctas` CTAs needs (one 128-B line per CTA)
+constexpr int rec_flag_words(int ctas) { return ctas * 32; }
 
 // bytes of the swizzled exchange buffers
 size_t rec_hsw_bytes(int H, int B, int T);

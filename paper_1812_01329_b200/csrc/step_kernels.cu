@@ -10,8 +10,8 @@ namespace jk {
 static constexpr int NSM = 148;
 
 // ------------------------------------------------------------------------------ init / guards
-__global__ void step_init_kernel(DevStatus *st, unsigned int *bar, int nbar) {
-  const int i = threadIdx.x;
+__global__ void step_init_kernel(DevStatus *st, unsigned int *bar, int nbar, int stride) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
     st->key = KEY_PASS;
     st->observed = 0;
@@ -21,11 +21,12 @@ __global__ void step_init_kernel(DevStatus *st, unsigned int *bar, int nbar) {
     st->trip = 0;
     st->flags = 0;
   }
-  for (int k = i; k < nbar; k += blockDim.x) bar[k] = 0;
+  for (int k = i; k * stride < nbar; k += gridDim.x * blockDim.x) bar[(size_t)k * stride] = 0;
 }
 
-cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s) {
-  step_init_kernel<<<1, 256, 0, s>>>(st, barriers, nbar);
+cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s, int stride) {
+  const int n = (nbar + stride - 1) / stride;
+  step_init_kernel<<<std::max(1, std::min((n + 255) / 256, 8)), 256, 0, s>>>(st, barriers, nbar, stride);
   return cudaGetLastError();
 }
 

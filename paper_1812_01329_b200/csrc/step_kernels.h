@@ -41,7 +41,8 @@ struct GuardList {
   GuardDesc g[MAX_GUARDS];
 };
 
-cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s);
+// status word := PASS; zeroes words 0, stride, 2 stride, ... < nbar of the step-flag area
+cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s, int stride = 1);
 cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s);
 
 // gather X[t*B+b] = rb(E[tok[b][t]]) (bf16, ld) with X[:, E] = 1 (ones column for bias grads);
