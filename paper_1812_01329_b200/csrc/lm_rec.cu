@@ -832,12 +832,26 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
             float v[UPC];
 #pragma unroll
             for (int i = 0; i < UPC; ++i) v[i] = 0.f;
-            for (int w = 0; w < nacc; ++w) {
-              float x[UPC];
-              if constexpr (UPC == 16) tmem_ld16(ta + w * C::CUNITS + UPC * p, x);
-              else tmem_ld8(ta + w * C::CUNITS + UPC * p, x);
+            if (nacc > 0) {  // every tile's load in flight, one wait
+              uint32_t r0[UPC], r1[UPC], r2[UPC], r3[UPC];
+              auto ld = [&](int w, uint32_t (&r)[UPC]) {
+                if constexpr (UPC == 16) tmem_ld16_nw(ta + w * C::CUNITS + UPC * p, r);
+                else tmem_ld8_nw(ta + w * C::CUNITS + UPC * p, r);
+              };
+              ld(0, r0);
+              if (nacc > 1) ld(1, r1);
+              if (nacc > 2) ld(2, r2);
+              if (nacc > 3) ld(3, r3);
+              tmem_ld_wait();
+              tmem_pin(r0); tmem_pin(r1); tmem_pin(r2); tmem_pin(r3);
 #pragma unroll
-              for (int i = 0; i < UPC; ++i) v[i] += x[i];
+              for (int i = 0; i < UPC; ++i) {
+                float acc = __uint_as_float(r0[i]);
+                if (nacc > 1) acc += __uint_as_float(r1[i]);
+                if (nacc > 2) acc += __uint_as_float(r2[i]);
+                if (nacc > 3) acc += __uint_as_float(r3[i]);
+                v[i] = acc;
+              }
             }
             if (lane < 16) {
               float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + srow) * UPC);
