@@ -243,7 +243,7 @@ bool lower_lm(Graph &g, std::string &why) {
     p.off.seg_word = take(TB * 4);
     p.off.seg_grad = take(TB * p.Ep * 4);
     p.off.nseg = take(16);
-    p.off.ehist = take(((size_t)V + TB) * 4);
+    p.off.ehist = take(((size_t)V + 2 * TB + 1) * 4);
     {  // split-K GEMM flags (one region: the step's GEMMs run in stream order)
       const int mx = std::max({(int)TB, V, G4, p.Ep, p.Hp + 1});
       p.off.gflags = take(gemm_flags_count(mx, mx) * 4);

@@ -452,92 +452,171 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
 }
 
 // ------------------------------------------------------------------------------ embedding grad
-// dE[w] = sum of the dX rows r with tok(r) = w (the VJP of the embedding lookup). No sort:
-//   1. claim (grid over rows): the first thread to CAS owner[w] from -1 allocates slot k for w
-//      (seg_word[k] = w). Slot order is scheduling dependent; the set of slots is not.
-//   2. segsum (block per slot): the block lists the rows of its word IN ROW ORDER (block ballots
-//      over the time-major rows), warp j sums list entries j, j+EG_WARPS, ..., and the EG_WARPS
-//      partials are combined in warp order — a fixed order, so every dE row is deterministic.
+// dE[w] = sum of the dX rows r with tok(r) = w (the VJP of the embedding lookup):
+//   1. bucket (one block): the first occurrence of each word in row order gets the next slot
+//      (atomicMin of the row into owner[w], then a block scan of "is first") — the slot order is
+//      deterministic; rows are counted per slot, offsets scanned, and every row appended to its
+//      slot's list (append order arbitrary);
+//   2. segsum (block per slot): the slot's rows are sorted ascending, warp j sums rows j,
+//      j + EG_WARPS, ... over all columns, and the warps' partials are combined in warp order —
+//      a fixed summation order, so every dE row is deterministic.
 constexpr int EG_MAX = 8192;
-constexpr int EG_WARPS = 16;
+constexpr int EG_WARPS = 8;  // 256-thread blocks: several blocks per SM
 JN_DEV int tok_of(const int *tok, int B, int W, int r) {
   const int t = r / B, b = r - t * B;
   return tok[(size_t)b * W + t];
 }
 
-__global__ void embed_claim_kernel(const int *tok, int B, int W, int T, const int *T_dev, int *owner,
-                                   int *seg_word, int *nseg, int *tokr) {
-  const int n = (T_dev ? *T_dev : T) * B;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    const int w = tok_of(tok, B, W, r);
-    tokr[r] = w;  // time-major copy: the segment sums scan it coalesced
-    if (atomicCAS(&owner[w], -1, r) == -1) seg_word[atomicAdd(nseg, 1)] = w;
+JN_DEV int block_excl_scan(int v, int *warp_sums, int *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ws, o);
+      if (lane >= o) ws += y;
+    }
+    warp_sums[lane] = ws;
+  }
+  __syncthreads();
+  const int r = x - v + (w > 0 ? warp_sums[w - 1] : 0);
+  if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return r;
+}
+
+// owner: V ints preset to INT_MAX; seg_start: n + 1 ints; list: n ints
+__global__ void __launch_bounds__(1024) embed_bucket_kernel(const int *tok, int B, int W, int T, const int *T_dev,
+                                                            int *owner, int *seg_word, int *seg_start, int *nseg,
+                                                            int *list) {
+  extern __shared__ int eb_smem[];
+  int *s_word = eb_smem;             // [EG_MAX] word of row r, later its slot
+  int *s_slot = eb_smem + EG_MAX;    // [EG_MAX] slot of a first-occurrence row
+  int *s_cnt = eb_smem + 2 * EG_MAX; // [EG_MAX] rows per slot, then append cursors
+  __shared__ int warp_sums[32];
+  const int n = (T_dev ? *T_dev : T) * B;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const int w = tok_of(tok, B, W, r);
+    s_word[r] = w;
+    atomicMin(&owner[w], r);
+    s_cnt[r] = 0;
+  }
+  __syncthreads();
+  __threadfence_block();
+  // slots in order of first occurrence: scan of is_first over the rows, chunk per thread
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = min(n, (int)threadIdx.x * per), hi = min(n, lo + per);
+  int nf = 0;
+  for (int r = lo; r < hi; ++r) nf += owner[s_word[r]] == r;
+  int total = 0;
+  int slot = block_excl_scan(nf, warp_sums, &total);
+  for (int r = lo; r < hi; ++r)
+    if (owner[s_word[r]] == r) {
+      s_slot[r] = slot;  // provisional: first rows know their slot
+      seg_word[slot] = s_word[r];
+      ++slot;
+    }
+  __syncthreads();
+  // every row: slot of its word (through the first row), count per slot
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const int sl = s_slot[owner[s_word[r]]];
+    atomicAdd(&s_cnt[sl], 1);
+    s_word[r] = sl;  // s_word now holds the row's slot
+  }
+  __syncthreads();
+  // offsets
+  const int per2 = (total + blockDim.x - 1) / blockDim.x;
+  const int lo2 = min(total, (int)threadIdx.x * per2), hi2 = min(total, lo2 + per2);
+  int c = 0;
+  for (int k = lo2; k < hi2; ++k) c += s_cnt[k];
+  int off = block_excl_scan(c, warp_sums, nullptr);
+  for (int k = lo2; k < hi2; ++k) {
+    const int ck = s_cnt[k];
+    seg_start[k] = off;
+    s_cnt[k] = off;  // append cursor
+    off += ck;
+  }
+  if (threadIdx.x == 0) {
+    *nseg = total;
+    seg_start[total] = n;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < n; r += blockDim.x) list[atomicAdd(&s_cnt[s_word[r]], 1)] = r;
 }
 
 // dynamic smem: rows[EG_MAX] ints, then part[EG_WARPS][NQ * 32] floats
 template <int NQ>
-__global__ void __launch_bounds__(EG_WARPS * 32) embed_segsum_kernel(
-    const int *tokr, int B, int T, const int *T_dev, const int *seg_word, const int *nseg,
-    const float *__restrict__ dX, int ldx, int Edim, float *seg_grad, int ldg) {
+__global__ void __launch_bounds__(EG_WARPS * 32, 2) embed_segsum_kernel(
+    const int *seg_start, const int *list, const int *nseg, const float *__restrict__ dX, int ldx, int Edim,
+    float *seg_grad, int ldg) {
   extern __shared__ int eg_smem[];
   int *rows = eg_smem;
   float *part = reinterpret_cast<float *>(eg_smem + EG_MAX);  // [EG_WARPS][NQ * 32]
-  __shared__ int wcount[EG_WARPS];
-  const int n = (T_dev ? *T_dev : T) * B;
   const int ns = *nseg;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int sgi = blockIdx.x; sgi < ns; sgi += gridDim.x) {
-    const int word = seg_word[sgi];
-    // ordered list of this word's rows
-    int cnt = 0;
-    for (int r0 = 0; r0 < n; r0 += blockDim.x) {
-      const int r = r0 + threadIdx.x;
-      const bool hit = r < n && tokr[r] == word;
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) wcount[w] = __popc(m);
-      __syncthreads();
-      int before = cnt;
-      for (int j = 0; j < w; ++j) before += wcount[j];
-      if (hit) rows[before + __popc(m & ((1u << lane) - 1u))] = r;
-      for (int j = 0; j < EG_WARPS; ++j) cnt += wcount[j];
-      __syncthreads();
-    }
-    // warp w sums list entries w, w + EG_WARPS, ... over ALL columns at once (lane: columns
+    const int a = seg_start[sgi], cnt = seg_start[sgi + 1] - a;
+    // the slot's rows, sorted ascending (bitonic over the next power of two; pads = INT_MAX)
+    int np = 1;
+    while (np < cnt) np <<= 1;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) rows[i] = i < cnt ? list[a + i] : 0x7fffffff;
+    __syncthreads();
+    for (int k = 2; k <= np; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int x = rows[i], y = rows[ixj];
+            if ((x > y) == ((i & k) == 0)) { rows[i] = y; rows[ixj] = x; }
+          }
+        }
+        __syncthreads();
+      }
+    // warp w sums entries w, w + EG_WARPS, ... over ALL columns at once (lane: columns
     // lane + 32 q), two rows per iteration: up to 2 NQ independent loads in flight per lane
     float acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.f;
     int i = w;
-    for (; i + EG_WARPS < cnt; i += 2 * EG_WARPS) {
-      const float *r0p = dX + (size_t)rows[i] * ldx;
-      const float *r1p = dX + (size_t)rows[i + EG_WARPS] * ldx;
-      float x0[NQ], x1[NQ];
+    for (; i + 3 * EG_WARPS < cnt; i += 4 * EG_WARPS) {  // four rows in flight per iteration
+      const float *rp[4];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int c = lane + 32 * q;
-        x0[q] = c < Edim ? r0p[c] : 0.f;
-        x1[q] = c < Edim ? r1p[c] : 0.f;
-      }
+      for (int u = 0; u < 4; ++u) rp[u] = dX + (size_t)rows[i + u * EG_WARPS] * ldx;
+      float x[4][NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) { acc[q] += x0[q]; acc[q] += x1[q]; }
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int cc = lane + 32 * q;
+          x[u][q] = cc < Edim ? rp[u][cc] : 0.f;
+        }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) { acc[q] += x[0][q]; acc[q] += x[1][q]; acc[q] += x[2][q]; acc[q] += x[3][q]; }
     }
-    if (i < cnt) {
+    for (; i < cnt; i += EG_WARPS) {
       const float *r0p = dX + (size_t)rows[i] * ldx;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const int c = lane + 32 * q;
-        acc[q] += c < Edim ? r0p[c] : 0.f;
+        const int cc = lane + 32 * q;
+        acc[q] += cc < Edim ? r0p[cc] : 0.f;
       }
     }
     // combine the warps' partial sums in warp order (deterministic)
 #pragma unroll
     for (int q = 0; q < NQ; ++q) part[w * NQ * 32 + lane + 32 * q] = acc[q];
     __syncthreads();
-    for (int c = threadIdx.x; c < Edim; c += blockDim.x) {
-      float sum = part[c];
-      for (int j = 1; j < EG_WARPS && j < cnt; ++j) sum += part[j * NQ * 32 + c];
-      seg_grad[(size_t)sgi * ldg + c] = sum;
+    for (int cc = threadIdx.x; cc < Edim; cc += blockDim.x) {
+      float sum = part[cc];
+      for (int j = 1; j < EG_WARPS && j < cnt; ++j) sum += part[j * NQ * 32 + cc];
+      seg_grad[(size_t)sgi * ldg + cc] = sum;
     }
     __syncthreads();
   }
@@ -547,16 +626,18 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
                               const float *dX, int ldx, int Edim, int *seg_word, int *owner,
                               float *seg_grad, int ldg, int *nseg, cudaStream_t s) {
   if (T * B > EG_MAX) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(owner, 0xff, (size_t)V * sizeof(int), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(nseg, 0, sizeof(int), s);
+  cudaError_t e = cudaMemsetAsync(owner, 0x7f, (size_t)V * sizeof(int), s);  // INT_MAX-ish
   if (e != cudaSuccess) return e;
-  int *tokr = owner + V;  // scratch: T*B ints after the owner table
-  embed_claim_kernel<<<(T * B + 255) / 256, 256, 0, s>>>(tok, B, W, T, T_dev, owner, seg_word, nseg, tokr);
+  int *seg_start = owner + V;                 // scratch: T*B + 1 ints
+  int *list = seg_start + (size_t)T * B + 1;  // scratch: T*B ints
+  e = cudaFuncSetAttribute(embed_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * EG_MAX * 4);
+  if (e != cudaSuccess) return e;
+  embed_bucket_kernel<<<1, 1024, 3 * EG_MAX * 4, s>>>(tok, B, W, T, T_dev, owner, seg_word, seg_start, nseg, list);
   auto go = [&](auto kern, int nq) {
     const int smem = EG_MAX * 4 + EG_WARPS * nq * 32 * 4;
     cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (r != cudaSuccess) return r;
-    kern<<<4 * NSM, EG_WARPS * 32, smem, s>>>(tokr, B, T, T_dev, seg_word, nseg, dX, ldx, Edim, seg_grad, ldg);
+    kern<<<8 * NSM, EG_WARPS * 32, smem, s>>>(seg_start, list, nseg, dX, ldx, Edim, seg_grad, ldg);
     return cudaGetLastError();
   };
   if (Edim <= 8 * 32) return go(embed_segsum_kernel<8>, 8);

@@ -88,7 +88,8 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
 
 // embedding gradient: seg_word[k] (k < *nseg, slot order unspecified) lists the distinct ids of
 // the step; seg_grad[k][ldg] = sum of the dX rows of that id, summed in a fixed order
-// (deterministic). owner: V + T*B ints of scratch.
+// (deterministic). owner: V + 2 T*B + 1 ints of scratch. seg_word slots are in order of first
+// occurrence (deterministic).
 cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev, int V,
                               const float *dX, int ldx, int Edim, int *seg_word, int *owner,
                               float *seg_grad, int ldg, int *nseg, cudaStream_t s);
