@@ -454,7 +454,10 @@ static bool g_tma_store_ok = getenv("JANUS_GEMM_TMA_STORE") == nullptr || getenv
 // K splits: the fewest persistent rounds per unit of work, each split >= 4 k-blocks, and the
 // partial tiles must fit the caller's scratch
 static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
-  // partial tiles cost a write + read of 128 x BN fp32 each: only long reductions gain
+  // Automatic split-K is off: the last-arriver reduction of the partial tiles measured slower
+  // than the unsplit GEMM for every shape of the step (scripts/gemm_check.py); explicit
+  // GemmOp::splits still selects it (tests/test_gpu_gemm.py::test_gemm_splitk*).
+  if (getenv("JANUS_GEMM_AUTOSPLIT") == nullptr) return 1;
   if (tiles >= nsm || nk < 64) return 1;
   int best = 1;
   double best_cost = (double)((tiles + nsm - 1) / nsm);
