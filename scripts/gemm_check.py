@@ -29,8 +29,9 @@ def run(M, N, K, a_mn, b_mn, splits, reps=20):
     tf = 2.0 * M * N * K / ms / 1e9
     print(f"M={M:5d} N={N:5d} K={K:5d} a_mn={a_mn} b_mn={b_mn} splits={splits}: err {err:.2e}  {ms*1000:8.1f} us  {tf:7.1f} TFLOP/s", flush=True)
 
-shapes = [(2240, 10000, 704, 0, 0), (2240, 2600, 656, 0, 0), (10000, 651, 2240, 1, 1), (2240, 650, 10000, 0, 1),
-          (2600, 651, 2240, 1, 1), (2240, 650, 2600, 0, 1)]
-for sh in shapes:
-    for s in (1, 0, 2):
-        run(*sh, s)
+if __name__ == "__main__":
+    shapes = [(2240, 10000, 704, 0, 0), (2240, 2600, 656, 0, 0), (10000, 651, 2240, 1, 1), (2240, 650, 10000, 0, 1),
+              (2600, 651, 2240, 1, 1), (2240, 650, 2600, 0, 1)]
+    for sh in shapes:
+        for s in (1, 0, 2):
+            run(*sh, s)
