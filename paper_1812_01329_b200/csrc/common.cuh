@@ -297,6 +297,26 @@ JN_DEV void grid_arrive_wait(unsigned int *counter, unsigned int target) {
 
 }  // namespace jk
 
+namespace jk {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size: the call costs host
+// time on every launch otherwise (host-side cache; the library's launches come from one thread)
+inline cudaError_t set_smem_once(const void *fn, int bytes) {
+  static const void *fns[64];
+  static int sizes[64];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (fns[i] == fn) {
+      if (sizes[i] >= bytes) return cudaSuccess;
+      const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) sizes[i] = bytes;
+      return e;
+    }
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && n < 64) { fns[n] = fn; sizes[n] = bytes; ++n; }
+  return e;
+}
+}  // namespace jk
+
 #define JN_CUDA(x)                                                      \
   do {                                                                  \
     cudaError_t e_ = (x);                                               \

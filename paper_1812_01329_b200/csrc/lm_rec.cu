@@ -1022,7 +1022,7 @@ cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw,
   const bool m64 = a.B <= 64;
   const void *fn = masked ? (m64 ? (const void *)lstm_rec_fwd_kernel<true, true> : (const void *)lstm_rec_fwd_kernel<true, false>)
                           : (m64 ? (const void *)lstm_rec_fwd_kernel<false, true> : (const void *)lstm_rec_fwd_kernel<false, false>);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_once((const void *)fn, smem);
   if (e != cudaSuccess) return e;
   FwdCtx cx = {};
   cx.a = a;
@@ -1054,7 +1054,7 @@ cudaError_t lstm_rec_fwd_wavefront(const RecFwdArgs &a0, const RecFwdArgs &a1, c
   const bool m64 = a0.B <= 64;
   const void *fn = masked ? (m64 ? (const void *)lstm_rec_fwd_wf_kernel<true, true> : (const void *)lstm_rec_fwd_wf_kernel<true, false>)
                           : (m64 ? (const void *)lstm_rec_fwd_wf_kernel<false, true> : (const void *)lstm_rec_fwd_wf_kernel<false, false>);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_once((const void *)fn, smem);
   if (e != cudaSuccess) return e;
   const int g0 = rec_grid(H), g1 = rec_fwd_wf_grid(H) - g0;
   FwdCtx c0 = {}, c1 = {};
@@ -1084,7 +1084,7 @@ static cudaError_t lstm_rec_bwd_plain(const RecBwdArgs &a, const __nv_bfloat16 *
   if (!make_tmap_bf16(&tmWT, WhhT, 4ull * a.H, a.H, ldwt, 16)) return cudaErrorInvalidValue;
   const int smem = smem_of(ly);
   const void *fn = masked ? (const void *)lstm_rec_bwd_kernel<true> : (const void *)lstm_rec_bwd_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_once((const void *)fn, smem);
   if (e != cudaSuccess) return e;
   RecBwdArgs aa = a;
   void *args[] = {&tmWT, &aa, &ly};
@@ -1092,7 +1092,7 @@ static cudaError_t lstm_rec_bwd_plain(const RecBwdArgs &a, const __nv_bfloat16 *
 }
 
 static cudaError_t cluster_launch(const void *fn, int grid, int smem, void **args, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_once((const void *)fn, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1110,8 +1110,15 @@ static cudaError_t cluster_launch(const void *fn, int grid, int smem, void **arg
   // cooperative launch would guarantee it but cannot be combined with clusters under the
   // profiler's replay; check instead that the device can hold every cluster simultaneously
   // (one CTA per SM; the launch runs alone on the stream).
-  int max_clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg) != cudaSuccess) max_clusters = 0;
+  static const void *c_fn[8];
+  static int c_smem[8], c_max[8], c_n = 0;
+  int max_clusters = -1;
+  for (int i = 0; i < c_n; ++i)
+    if (c_fn[i] == fn && c_smem[i] == smem) max_clusters = c_max[i];
+  if (max_clusters < 0) {  // occupancy query once per kernel and size (host cost)
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg) != cudaSuccess) max_clusters = 0;
+    if (c_n < 8) { c_fn[c_n] = fn; c_smem[c_n] = smem; c_max[c_n] = max_clusters; ++c_n; }
+  }
   if (grid / KS_CL > max_clusters) return cudaErrorCooperativeLaunchTooLarge;
   return cudaLaunchKernelExC(&cfg, fn, args);
 }

@@ -630,12 +630,12 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
   if (e != cudaSuccess) return e;
   int *seg_start = owner + V;                 // scratch: T*B + 1 ints
   int *list = seg_start + (size_t)T * B + 1;  // scratch: T*B ints
-  e = cudaFuncSetAttribute(embed_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * EG_MAX * 4);
+  e = set_smem_once((const void *)embed_bucket_kernel, 3 * EG_MAX * 4);
   if (e != cudaSuccess) return e;
   embed_bucket_kernel<<<1, 1024, 3 * EG_MAX * 4, s>>>(tok, B, W, T, T_dev, owner, seg_word, seg_start, nseg, list);
   auto go = [&](auto kern, int nq) {
     const int smem = EG_MAX * 4 + EG_WARPS * nq * 32 * 4;
-    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t r = set_smem_once((const void *)kern, smem);
     if (r != cudaSuccess) return r;
     kern<<<8 * NSM, EG_WARPS * 32, smem, s>>>(seg_start, list, nseg, dX, ldx, Edim, seg_grad, ldg);
     return cudaGetLastError();

@@ -112,6 +112,8 @@ cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSc
 // =============================================================================== schedule
 // Single block. Heights by a per-tree scan in post-order (children precede parents); then a
 // stable counting sort by height in node-id order (warp match + per-level prefix over warps).
+constexpr int TREE_SCHED_SMEM_NODES = 40 * 1024;  // heights in shared memory up to 160 KB
+
 __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
                                                              const DevStatus *st) {
   __shared__ int hist[TREE_MAX_LEVELS + 1];
@@ -127,20 +129,31 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
   for (int i = tid; i <= TREE_MAX_LEVELS; i += blockDim.x) { hist[i] = 0; running[i] = 0; }
   if (tid == 0) s_L = 1;
   __syncthreads();
-  // heights (robust to malformed input: the guard has already decided the commit)
+  // heights (robust to malformed input: the guard has already decided the commit). One thread
+  // walks each tree in node order (children precede parents); the heights live in shared memory
+  // when the forest fits, so the walk is not a chain of global-memory round trips.
+  extern __shared__ int sh_height[];
+  int *hh = N <= TREE_SCHED_SMEM_NODES ? sh_height : s.height;
   for (int tr = tid; tr < B; tr += blockDim.x) {
     const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
     for (int n = lo; n < hi; ++n) {
       int h = 0;
-      s.tree_of[n] = tr;
       if (t.kind[n] == 1) {
         const int l = t.left[n], r = t.right[n];
-        const int hl = (l >= lo && l < n) ? s.height[l] : 0;
-        const int hr = (r >= lo && r < n) ? s.height[r] : 0;
+        const int hl = (l >= lo && l < n) ? hh[l] : 0;
+        const int hr = (r >= lo && r < n) ? hh[r] : 0;
         h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
       }
-      s.height[n] = h;
+      hh[n] = h;
+    }
+  }
+  __syncthreads();
+  for (int tr = 0; tr < B; ++tr) {  // tree_of, pslot, heights to global (parallel over nodes)
+    const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
+    for (int n = lo + tid; n < hi; n += blockDim.x) {
+      s.tree_of[n] = tr;
       s.pslot[n] = -1;
+      if (hh != s.height) s.height[n] = hh[n];
     }
   }
   __syncthreads();
@@ -205,7 +218,10 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
 
 cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                                  const DevStatus *st, cudaStream_t str) {
-  tree_schedule_kernel<<<1, 1024, 0, str>>>(t, d, s, st);
+  const int smem = d.N <= TREE_SCHED_SMEM_NODES ? d.N * 4 : 0;
+  cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, TREE_SCHED_SMEM_NODES * 4);
+  if (e != cudaSuccess) return e;
+  tree_schedule_kernel<<<1, 1024, smem, str>>>(t, d, s, st);
   return cudaGetLastError();
 }
 
@@ -429,7 +445,7 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
   if (!ok) return cudaErrorInvalidValue;
   const int smem = tree_smem();
-  cudaError_t e = cudaFuncSetAttribute(tree_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_once((const void *)tree_fwd_kernel, smem);
   if (e != cudaSuccess) return e;
   TreeBufs tt = t;
   TreeDims dd = d;
@@ -449,16 +465,23 @@ __global__ void tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus 
     for (int tr = threadIdx.x; tr < B; tr += blockDim.x) t.rowloss[tr] = 0.f;
     return;
   }
+  // logits: one warp per (tree, class) pair, lanes over the hidden units, warp reduction
+  float *ysh = dyr + B * C;  // [B][C] logits
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int p = wid; p < B * C; p += nw) {
+    const int tr = p / C, c = p - tr * C;
+    float acc = 0.f;
+    for (int k = lane; k < H; k += 32)
+      acc += bf16_round(t.root_h[(size_t)tr * H + k]) * bf16_round(t.Wc[(size_t)c * H + k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ysh[p] = acc + t.bc[c];
+  }
+  __syncthreads();
   for (int tr = threadIdx.x; tr < B; tr += blockDim.x) {
-    float y[8];
+    const float *y = ysh + tr * C;
     float m = -INFINITY;
-    for (int c = 0; c < C; ++c) {
-      float acc = t.bc[c];
-      for (int k = 0; k < H; ++k)
-        acc += bf16_round(t.root_h[(size_t)tr * H + k]) * bf16_round(t.Wc[(size_t)c * H + k]);
-      y[c] = acc;
-      m = fmaxf(m, acc);
-    }
+    for (int c = 0; c < C; ++c) m = fmaxf(m, y[c]);
     float sum = 0.f;
     for (int c = 0; c < C; ++c) sum += expf(y[c] - m);
     const float lse = m + logf(sum);
@@ -499,7 +522,7 @@ __global__ void tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus 
 cudaError_t launch_tree_root(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                              DevStatus *st, cudaStream_t str) {
   if (d.C > 8) return cudaErrorInvalidValue;
-  tree_root_kernel<<<1, 1024, d.B * d.C * 4, str>>>(t, d, s, st);
+  tree_root_kernel<<<1, 1024, 2 * d.B * d.C * 4, str>>>(t, d, s, st);
   return cudaGetLastError();
 }
 
@@ -611,7 +634,7 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
   if (!ok) return cudaErrorInvalidValue;
   const int smem = tree_smem();
-  cudaError_t e = cudaFuncSetAttribute(tree_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_smem_once((const void *)tree_bwd_kernel, smem);
   if (e != cudaSuccess) return e;
   TreeBufs tt = t;
   TreeDims dd = d;
