@@ -112,7 +112,7 @@ cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSc
 // =============================================================================== schedule
 // Single block. Heights by a per-tree scan in post-order (children precede parents); then a
 // stable counting sort by height in node-id order (warp match + per-level prefix over warps).
-constexpr int TREE_SCHED_SMEM_NODES = 40 * 1024;  // heights in shared memory up to 160 KB
+constexpr int TREE_SCHED_SMEM_NODES = 13 * 1024;  // heights + children in shared memory up to 156 KB
 
 __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
                                                              const DevStatus *st) {
@@ -133,13 +133,26 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
   // walks each tree in node order (children precede parents); the heights live in shared memory
   // when the forest fits, so the walk is not a chain of global-memory round trips.
   extern __shared__ int sh_height[];
-  int *hh = N <= TREE_SCHED_SMEM_NODES ? sh_height : s.height;
+  const bool in_smem = N <= TREE_SCHED_SMEM_NODES;
+  int *hh = in_smem ? sh_height : s.height;
+  // children of internal nodes (kl = INT_MIN marks a leaf) staged in shared memory first
+  int *kl = sh_height + N, *kr = sh_height + 2 * N;
+  constexpr int LEAF = -2147483647 - 1;
+  if (in_smem) {
+    for (int n = tid; n < N; n += blockDim.x) {
+      const bool in = t.kind[n] == 1;
+      kl[n] = in ? t.left[n] : LEAF;
+      kr[n] = in ? t.right[n] : LEAF;
+    }
+    __syncthreads();
+  }
   for (int tr = tid; tr < B; tr += blockDim.x) {
     const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
     for (int n = lo; n < hi; ++n) {
       int h = 0;
-      if (t.kind[n] == 1) {
-        const int l = t.left[n], r = t.right[n];
+      const bool internal = in_smem ? kl[n] != LEAF : t.kind[n] == 1;
+      if (internal) {
+        const int l = in_smem ? kl[n] : t.left[n], r = in_smem ? kr[n] : t.right[n];
         const int hl = (l >= lo && l < n) ? hh[l] : 0;
         const int hr = (r >= lo && r < n) ? hh[r] : 0;
         h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
@@ -218,8 +231,8 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
 
 cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                                  const DevStatus *st, cudaStream_t str) {
-  const int smem = d.N <= TREE_SCHED_SMEM_NODES ? d.N * 4 : 0;
-  cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, TREE_SCHED_SMEM_NODES * 4);
+  const int smem = d.N <= TREE_SCHED_SMEM_NODES ? 3 * d.N * 4 : 0;
+  cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, 3 * TREE_SCHED_SMEM_NODES * 4);
   if (e != cudaSuccess) return e;
   tree_schedule_kernel<<<1, 1024, smem, str>>>(t, d, s, st);
   return cudaGetLastError();
