@@ -19,8 +19,11 @@
 
 namespace jk {
 
-constexpr int TT = 192;          // threads: warps 0-3 epilogue, warp 4 TMA, warp 5 MMA
-constexpr int T_STAGES = 6;
+constexpr int T_NMW = 4;          // MMA-issuing warps (one accumulator each; ~130 cycles per issue)
+constexpr int TT = 160 + 32 * T_NMW;  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
+// ring stages: a multiple of T_NMW, so a stage is always consumed by the same MMA warp (it owns
+// chunks q = w mod T_NMW) and that warp can never wait on a stage two phases ahead of its loads
+constexpr int T_STAGES = 8;
 constexpr int T_ASTAGE = 128 * 128;  // A chunk: 128 rows x 64 bf16
 constexpr int T_BSTAGE = 80 * 128;   // B chunk: up to 80 rows x 64 bf16
 
@@ -252,7 +255,9 @@ struct Ring {
 
 template <int NT, typename Epi>
 JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, int row0, int M,
-                      int NTOT, int K, Epi epi) {
+                      int NTOT, int K, Epi epi, int nmw) {
+  // nmw in {1, 2, 4} MMA warps take part (T_STAGES % nmw == 0 keeps a fixed owner per stage):
+  // more warps for long reductions, fewer TMEM tiles for the epilogue to sum on short ones
   const int warp = threadIdx.x >> 5;
   const int ntile_n = (NTOT + NT - 1) / NT;
   const int tiles = ((M + 127) / 128) * ntile_n;
@@ -270,20 +275,25 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
           tma_load_2d(rg.sB + s * T_BSTAGE, tmB, &rg.full[s], kc * 64, nn * NT);
         }
       __syncwarp();
-    } else if (warp == 5) {
+    } else if (warp >= 5) {
+      // ring chunk q goes to MMA warp q % T_NMW (a fixed owner per stage), accumulating into
+      // its own TMEM tile
+      const int w = warp - 5;
       if ((threadIdx.x & 31) == 0) {
-        for (int kc = 0; kc < nk; ++kc) {
+        const uint32_t acc = rg.tmem + (uint32_t)(w * NT);
+        const int kc0 = w < nmw ? ((w - rg.q) % nmw + nmw) % nmw : nk;  // my first chunk of this tile
+        for (int kc = kc0; kc < nk; kc += nmw) {
           const int q = rg.q + kc, s = q % T_STAGES, r = q / T_STAGES;
           mbar_wait(&rg.full[s], r & 1);
           tc_fence_after();
           const uint32_t a = smem_u32(rg.sA + s * T_ASTAGE), b = smem_u32(rg.sB + s * T_BSTAGE);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_bf16(rg.tmem, umma_desc_sw128(a + k * 32, 16, 1024),
-                      umma_desc_sw128(b + k * 32, 16, 1024), idesc, (kc | k) != 0);
+            umma_bf16(acc, umma_desc_sw128(a + k * 32, 16, 1024),
+                      umma_desc_sw128(b + k * 32, 16, 1024), idesc, (kc != kc0 || k != 0) ? 1u : 0u);
           umma_commit(&rg.empty[s]);
         }
-        umma_commit(rg.tfull);
+        umma_commit(rg.tfull);  // arrives even with no chunk (nk < T_NMW)
       }
       __syncwarp();
     } else {
@@ -291,19 +301,25 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
       __syncwarp();
       tc_fence_after();
       float z[NT];
+#pragma unroll
+      for (int i = 0; i < NT; ++i) z[i] = 0.f;
       const uint32_t ta = rg.tmem + ((uint32_t)(warp * 32) << 16);
+      const int nacc = min(nmw, nk);  // the owners of chunks 0 .. nacc-1 of this tile
+      for (int i = 0; i < nacc; ++i) {
+        const int w = (rg.q + i) % nmw;
 #pragma unroll
-      for (int c = 0; c + 32 <= NT; c += 32) {
-        float v[32];
-        tmem_ld32(ta + c, v);
+        for (int c = 0; c + 32 <= NT; c += 32) {
+          float v[32];
+          tmem_ld32(ta + w * NT + c, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) z[c + i] = v[i];
-      }
-      if (NT % 32) {
-        float v[16];
-        tmem_ld16(ta + (NT / 32) * 32, v);
+          for (int i = 0; i < 32; ++i) z[c + i] += v[i];
+        }
+        if (NT % 32) {
+          float v[16];
+          tmem_ld16(ta + w * NT + (NT / 32) * 32, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) z[(NT / 32) * 32 + i] = v[i];
+          for (int i = 0; i < 16; ++i) z[(NT / 32) * 32 + i] += v[i];
+        }
       }
       const int row = m * 128 + threadIdx.x;
       if (row < M) epi(row, nn * NT, z);
@@ -339,10 +355,10 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
   if (threadIdx.x == 128) {
     for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
-    mbar_init(rg.tfull, 1);
+    mbar_init(rg.tfull, T_NMW);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 128);
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -389,7 +405,7 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
         t.root_h[(size_t)s.tree_of[n] * H + u] = h;
       }
     }
-  });
+  }, (E + 63) / 64 >= 8 ? 2 : 1);
   fence_proxy_async_global();
   grid_sync(t.barrier, ++ep * gridDim.x);
   // ---- internal levels: z = [h_l; h_r] U^T; c = i u + f_l c_l + f_r c_r; h = o tanh(c)
@@ -422,13 +438,13 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
           t.root_h[(size_t)s.tree_of[n] * H + u] = h;
         }
       }
-    });
+    }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1));
     fence_proxy_async_global();
     grid_sync(t.barrier, ++ep * gridDim.x);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(rg.tmem, 128);
+  if (warp == 5) tmem_dealloc(rg.tmem, 512);
   (void)st;
 }
 
@@ -562,10 +578,10 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
   if (threadIdx.x == 128) {
     for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
-    mbar_init(rg.tfull, 1);
+    mbar_init(rg.tfull, T_NMW);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 128);
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -611,7 +627,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
         if (k < H) t.dh_node[(size_t)lc * H + k] = z[j];
         else t.dh_node[(size_t)rc * H + (k - H)] = z[j];
       }
-    });
+    }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1));
     grid_sync(t.barrier, ++ep * gridDim.x);
   }
   // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]
@@ -635,7 +651,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
     t.DZ_leaf[(size_t)n0 * d.P3 + e] = __float2bfloat16_rn(0.f);
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc(rg.tmem, 128);
+  if (warp == 5) tmem_dealloc(rg.tmem, 512);
   (void)st;
 }
 
