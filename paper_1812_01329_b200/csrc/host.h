@@ -40,6 +40,7 @@ struct LmPlan {
     size_t seg_word = 0, seg_grad = 0, nseg = 0, ehist = 0, gflags = 0, gpart = 0;
     size_t small_ws = 0;
     size_t arena_begin = 0, arena_end = 0, dEd = 0, dp_scratch = 0;
+    size_t arena_early_end = 0;  // [arena_begin, arena_early_end): dW_dec, allreduced during the backward
   } off;
   int Ep = 0, Hp = 0, Gz = 0;  // padded row pitches (elements)
   int nbar = 0;
@@ -117,6 +118,9 @@ struct Graph {
   // pinned status readback
   DevStatus *h_status = nullptr;
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
+  void *nccl2 = nullptr; // second communicator (split) for the collective that overlaps the backward
+  cudaStream_t side = nullptr;             // stream of the overlapped collective
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
   std::string describe;
   const void *gflags_ws = nullptr;        // workspace whose split-K counters were zeroed
@@ -151,6 +155,10 @@ bool dp_wanted(const janus_build_opts &o);  // decided once, at build time
 janus_status dp_init(Graph &g);
 void dp_destroy(Graph &g);
 janus_status dp_allreduce_sum(Graph &g, float *buf, size_t n, cudaStream_t st);
+// the same on the second communicator (issued on the side stream by the step, on the launch
+// stream by a null step — the per-communicator order is the same on every rank)
+janus_status dp_allreduce_sum2(Graph &g, float *buf, size_t n, cudaStream_t st);
+bool dp_overlap(const Graph &g);  // the backward's early allreduce is in use
 janus_status dp_agree(Graph &g, DevStatus *st_dev, long long *scratch, cudaStream_t st);
 // a data-parallel rank whose DISPATCH guards failed still joins every collective (null step)
 janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,

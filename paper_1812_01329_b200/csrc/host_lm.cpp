@@ -231,12 +231,13 @@ bool lower_lm(Graph &g, std::string &why) {
     p.off.dHtop = take(TB * p.Hp * 4);
     // gradient arena: one contiguous fp32 block, allreduced in one NCCL call under DP
     p.off.arena_begin = o;
+    p.off.gWdec = take((size_t)V * p.Hp * 4);  // first: its allreduce may start during the backward
+    p.off.arena_early_end = o;
     for (int l = 0; l < p.L; ++l) {
       const int Inp = l ? p.Hp : p.Ep;
       p.off.gWih[l] = take((size_t)G4 * Inp * 4);
       p.off.gWhh[l] = take((size_t)G4 * p.Hp * 4);
     }
-    p.off.gWdec = take((size_t)V * p.Hp * 4);
     if (dp_enabled(g)) p.off.dEd = take((size_t)V * E * 4);  // dense embedding gradient
     p.off.arena_end = o;
     p.off.dp_scratch = take(64);
@@ -508,6 +509,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   const char *bk_env = getenv("JANUS_REC_BWD");
   const bool bwd_wave = L == 2 && B <= 64 && !(bwf_env && bwf_env[0] == '0') && !(bk_env && bk_env[0] == 'p') &&
                         rec_bwd_wf_grid(H) <= 148;
+  const bool overlap = g.nccl && g.nccl2 && g.side;  // dp_overlap() held at init
   GemmOp dwdec;  // dW_dec | db_dec = dy^T [h_top | 1]
   dwdec.M = V; dwdec.N = H + 1; dwdec.K = TB;
   dwdec.A = bf(p.off.dy); dwdec.lda = Vp; dwdec.a_mn = 1;
@@ -516,7 +518,16 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
                    (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
   {
-    if (!bwd_wave) LCHK("gemm_dWdec", gemm_bf16(with_flags(dwdec), st));  // else grouped below
+    if (!bwd_wave || overlap) LCHK("gemm_dWdec", gemm_bf16(with_flags(dwdec), st));  // else grouped below
+    if (overlap) {  // allreduce dW_dec on the side stream while the backward recurrence runs
+      g.prof.mark("dp_allreduce_early", st);
+      if (cudaEventRecord(g.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(g.side, g.ev_fork, 0) != cudaSuccess)
+        return JANUS_ERR_CUDA;
+      janus_status r = dp_allreduce_sum2(g, fp(p.off.arena_begin), (p.off.arena_early_end - p.off.arena_begin) / 4,
+                                         g.side);
+      if (r != JANUS_OK) return r;
+      if (cudaEventRecord(g.ev_join, g.side) != cudaSuccess) return JANUS_ERR_CUDA;
+    }
     GemmOp o2;  // dh_top = dy W_dec
     o2.M = TB; o2.N = H; o2.K = V;
     o2.A = bf(p.off.dy); o2.lda = Vp;
@@ -557,7 +568,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   if (bwd_wave) {  // every weight gradient + the embedding dgrad in one grouped launch
     GemmOp ops[6];
     int n = 0;
-    ops[n++] = dwdec;
+    if (!overlap) ops[n++] = dwdec;
     wgrad_ops(1, ops[n], ops[n + 1]);
     n += 2;
     wgrad_ops(0, ops[n], ops[n + 1]);
@@ -603,8 +614,10 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     if (p.lr_E != 0)
       LCHK("dp_scatter", launch_scatter_rows(fp(p.off.seg_grad), Ep, seg_word, nseg, fp(p.off.dEd), V, E, st));
     g.prof.mark("dp_allreduce", st);
-    janus_status r = dp_allreduce_sum(g, fp(p.off.arena_begin), (p.off.arena_end - p.off.arena_begin) / 4, st);
+    const size_t a0 = overlap ? p.off.arena_early_end : p.off.arena_begin;
+    janus_status r = dp_allreduce_sum(g, fp(a0), (p.off.arena_end - a0) / 4, st);
     if (r != JANUS_OK) return r;
+    if (overlap && cudaStreamWaitEvent(st, g.ev_join, 0) != cudaSuccess) return JANUS_ERR_CUDA;
   }
   LCHK("finalize", launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
   if (g.nccl) {  // every rank learns the same status before anything commits (reading Q12)
@@ -657,8 +670,14 @@ janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &w
   unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
   LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
   LCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
-  r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + p.off.arena_begin),
-                       (p.off.arena_end - p.off.arena_begin) / 4, st);
+  size_t a0 = p.off.arena_begin;
+  if (g.nccl2) {  // the same per-communicator sequence as a full step: early part, then the rest
+    r = dp_allreduce_sum2(g, reinterpret_cast<float *>(W + p.off.arena_begin),
+                          (p.off.arena_early_end - p.off.arena_begin) / 4, st);
+    if (r != JANUS_OK) return r;
+    a0 = p.off.arena_early_end;
+  }
+  r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + a0), (p.off.arena_end - a0) / 4, st);
   if (r != JANUS_OK) return r;
   r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
   if (r != JANUS_OK) return r;
