@@ -26,7 +26,7 @@ namespace jk {
 
 bool make_tmap_f32_box32(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t ld);
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int NMMA = 1>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
@@ -35,7 +35,7 @@ struct GemmCfg {
   // epilogue staging for TMA stores: per epilogue warp two 32 x 32 fp32 boxes (double buffer)
   static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int THREADS = 192;
+  static constexpr int THREADS = 192 + 32 * (NMMA - 1);  // warp 6: the second MMA warp
 };
 
 struct TileMap {
@@ -136,9 +136,13 @@ JN_DEV TileRef tile_ref(const GemmBatch &gb, int t) {
   return r;
 }
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
-  using C = GemmCfg<BN, STAGES>;
+// NMMA = 2 (BN = 128): a second MMA-issuing warp takes the odd ring stages into its own
+// accumulators — one warp issues a tcgen05.mma only every ~130 cycles, twice the N = 128 MMA time;
+// STAGES is even, so every stage has one fixed owner and no wait can alias a phase
+template <int BN, int STAGES, int NMMA>
+__global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
+  using C = GemmCfg<BN, STAGES, NMMA>;
+  static_assert(STAGES % NMMA == 0, "stage ownership");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -165,12 +169,12 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
+      mbar_init(&tfull[i], NMMA);
       mbar_init(&tempty[i], 4);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * NMMA * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -206,7 +210,8 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
         __syncwarp();
       }
     }
-  } else if (warp == 1) {  // ---------------- MMA issuer (the warp loops together, lane 0 issues)
+  } else if (warp == 1 || warp >= 6) {  // ---------------- MMA issuers (lane 0 issues)
+    const int mw = warp == 1 ? 0 : warp - 5;  // which of the NMMA issuing warps
     int q = 0, i = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
       const TileRef tr = tile_ref<BN, STAGES>(gb, t);
@@ -215,8 +220,10 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
       const int buf = i & 1;
       if (i >= 2) mbar_wait(&tempty[buf], ((i >> 1) - 1) & 1);  // epilogue drained this buffer
       tc_fence_after();
-      const uint32_t acc = tmem + (uint32_t)(buf * BN);
+      const uint32_t acc = tmem + (uint32_t)((buf * NMMA + mw) * BN);
+      bool first = true;
       for (int kb = tr.kb0; kb < tr.kb1; ++kb, ++q) {
+        if (q % NMMA != mw) continue;
         const int s = q % STAGES, r = q / STAGES;
         mbar_wait(&full[s], r & 1);
         tc_fence_after();
@@ -228,21 +235,36 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
                                      : umma_desc_sw128(a + j * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
                                      : umma_desc_sw128(b + j * 32, 16, 1024);
-            umma_bf16(acc, ad, bd, idesc, (kb != tr.kb0 || j != 0) ? 1u : 0u);
+            umma_bf16(acc, ad, bd, idesc, (!first || j != 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
+        first = false;
         __syncwarp();
       }
-      if (lane == 0) umma_commit(&tfull[buf]);
+      if (lane == 0) umma_commit(&tfull[buf]);  // arrives even without a k-block of its own
       __syncwarp();
     }
   } else {
     // ---------------- epilogue: TMEM -> registers -> global (warps 2-5)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    int i = 0;
+    int i = 0, qe = 0;          // qe: ring position of the tile's first k-block (as the MMA warps)
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
       const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+      const int nkt = tr.kb1 > tr.kb0 ? tr.kb1 - tr.kb0 : 0;
+      const int qt = qe;
+      qe += nkt;
+      // accumulator columns of chunk c: the owners of the tile's first min(NMMA, nkt) k-blocks
+      auto ld_acc = [&](int c, float (&v)[32]) {
+        const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(((i & 1) * NMMA) * BN) + c * 32;
+        tmem_ld32(base + (uint32_t)((qt % NMMA) * BN), v);
+        if (NMMA > 1 && nkt > 1) {
+          float w[32];
+          tmem_ld32(base + (uint32_t)(((qt + 1) % NMMA) * BN), w);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] += w[j];
+        }
+      };
       const GemmEpilogue &ep = gb.ep[tr.g];
       const int M = gb.M[tr.g], N = gb.N[tr.g];
       const int splits = gb.tm[tr.g].splits;
@@ -266,7 +288,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
           const int n = n0 + c * 32;
           if (n >= N) break;  // warp-uniform
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * BN + c * 32, v);
+          ld_acc(c, v);
           if (empty_k) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -314,7 +336,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
           const int n = n0 + c * 32;
           if (n >= N) break;  // warp-uniform
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * BN + c * 32, v);
+          ld_acc(c, v);
           if (empty_k) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -333,7 +355,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           float v[32];
-          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + buf * BN + c * 32, v);
+          ld_acc(c, v);
           if (empty_k) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -378,7 +400,7 @@ __global__ void __launch_bounds__(192, 1) gemm_bf16_tc_kernel(const __grid_const
   if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 2 * BN);
+  if (warp == 1) tmem_dealloc(tmem, 2 * NMMA * BN);
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -471,8 +493,9 @@ static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
 template <int BN>
 static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   constexpr int STAGES = BN == 256 ? 4 : 6;
-  using C = GemmCfg<BN, STAGES>;
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES>;
+  constexpr int NMMA = BN == 256 ? 1 : 2;
+  using C = GemmCfg<BN, STAGES, NMMA>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, NMMA>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
