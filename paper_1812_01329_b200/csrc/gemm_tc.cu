@@ -120,29 +120,35 @@ struct TileRef {
   int g, mb, nb, sp, kb0, kb1, tile;
 };
 
-template <int BN, int STAGES>
-JN_DEV TileRef tile_ref(const GemmBatch &gb, int t) {
+// t: cluster-tile index; with CM > 1 the CM CTAs of a cluster take m-blocks CM * mg + rank of the
+// same n-block and K range (they share the B tile through TMA multicast); tm.Mb counts m-groups
+template <int BN, int STAGES, int CM = 1>
+JN_DEV TileRef tile_ref(const GemmBatch &gb, int t, int rank = 0) {
   TileRef r;
   r.g = 0;
   while (r.g + 1 < gb.n && t >= gb.tile_start[r.g + 1]) ++r.g;
   const TileMap &tm = gb.tm[r.g];
   tm.of(t - gb.tile_start[r.g], r.mb, r.nb, r.sp);
+  if (CM > 1) r.mb = r.mb * CM + rank;
   int K = gb.K[r.g];
   if (gb.K_dev[r.g]) K = min(K, *gb.K_dev[r.g]);  // reduction length known only on the device
   const int nk = (K + 63) / 64;
   r.kb0 = (int)((long long)nk * r.sp / tm.splits);
   r.kb1 = (int)((long long)nk * (r.sp + 1) / tm.splits);
-  r.tile = r.mb + tm.Mb * r.nb;
+  r.tile = r.mb + tm.Mb * CM * r.nb;
   return r;
 }
 
 // NMMA = 2 (BN = 128): a second MMA-issuing warp takes the odd ring stages into its own
 // accumulators — one warp issues a tcgen05.mma only every ~130 cycles, twice the N = 128 MMA time;
 // STAGES is even, so every stage has one fixed owner and no wait can alias a phase
-template <int BN, int STAGES, int NMMA>
+template <int BN, int STAGES, int NMMA, int CM>
 __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
   using C = GemmCfg<BN, STAGES, NMMA>;
   static_assert(STAGES % NMMA == 0, "stage ownership");
+  // CM > 1: clusters of CM CTAs along M share each B tile; CTA r loads rows / k-rows slice r of it
+  // with a multicast TMA into every cluster CTA, and a stage is released only when the owning
+  // MMA warp of EVERY cluster CTA consumed it (multicast commit into each empty barrier)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
@@ -157,6 +163,9 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = gb.tile_start[gb.n];
+  const int rank = CM > 1 ? (int)cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CM, ncl = gridDim.x / CM;  // cluster index / count
+  constexpr uint16_t cmask = (uint16_t)((1u << CM) - 1);
 
   if (warp == 0 && lane == 0) {
     for (int g = 0; g < gb.n; ++g) {
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CM);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], NMMA);
@@ -178,12 +187,13 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (CM > 1) cluster_sync_all();  // peers' barriers exist before any multicast targets them
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {  // ---------------- TMA producer (the warp loops together, lane 0 issues)
     int q = 0;       // ring position, continuous across tiles
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+    for (int t = cid; t < total; t += ncl) {
+      const TileRef tr = tile_ref<BN, STAGES, CM>(gb, t, rank);
       const CUtensorMap *tmA = &gb.ta[tr.g], *tmB = &gb.tb[tr.g];
       const bool A_MN = gb.amn[tr.g], B_MN = gb.bmn[tr.g];
       const int m0 = tr.mb * C::BM, n0 = tr.nb * BN;
@@ -200,11 +210,21 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
             tma_load_2d(a, tmA, &full[s], m0, k0);
             tma_load_2d(a + 8192, tmA, &full[s], m0 + 64, k0);
           }
-          if (!B_MN) {
-            tma_load_2d(b, tmB, &full[s], k0, n0);
-          } else {
+          if (CM == 1) {
+            if (!B_MN) {
+              tma_load_2d(b, tmB, &full[s], k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, tmB, &full[s], n0 + 64 * j, k0);
+              for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, tmB, &full[s], n0 + 64 * j, k0);
+            }
+          } else if (!B_MN) {  // my slice of N rows, multicast to the cluster
+            constexpr int RS = BN / CM;
+            tma_load_2d_mc(b + rank * RS * 128, tmB, &full[s], k0, n0 + rank * RS, cmask);
+          } else {  // my slice of the K rows of every 64-column chunk, multicast
+            constexpr int KS = 64 / CM;
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d_mc(b + j * 8192 + rank * KS * 128, tmB, &full[s], n0 + 64 * j, k0 + rank * KS, cmask);
           }
         }
         __syncwarp();
@@ -213,8 +233,8 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
   } else if (warp == 1 || warp >= 6) {  // ---------------- MMA issuers (lane 0 issues)
     const int mw = warp == 1 ? 0 : warp - 5;  // which of the NMMA issuing warps
     int q = 0, i = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-      const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+    for (int t = cid; t < total; t += ncl, ++i) {
+      const TileRef tr = tile_ref<BN, STAGES, CM>(gb, t, rank);
       const int A_MN = gb.amn[tr.g], B_MN = gb.bmn[tr.g];
       const uint32_t idesc = umma_idesc_bf16(128, BN, A_MN, B_MN);
       const int buf = i & 1;
@@ -237,7 +257,8 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
                                      : umma_desc_sw128(b + j * 32, 16, 1024);
             umma_bf16(acc, ad, bd, idesc, (!first || j != 0) ? 1u : 0u);
           }
-          umma_commit(&empty[s]);
+          if (CM == 1) umma_commit(&empty[s]);
+          else umma_commit_mc(&empty[s], cmask);
         }
         first = false;
         __syncwarp();
@@ -249,8 +270,8 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
     // ---------------- epilogue: TMEM -> registers -> global (warps 2-5)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     int i = 0, qe = 0;          // qe: ring position of the tile's first k-block (as the MMA warps)
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-      const TileRef tr = tile_ref<BN, STAGES>(gb, t);
+    for (int t = cid; t < total; t += ncl, ++i) {
+      const TileRef tr = tile_ref<BN, STAGES, CM>(gb, t, rank);
       const int nkt = tr.kb1 > tr.kb0 ? tr.kb1 - tr.kb0 : 0;
       const int qt = qe;
       qe += nkt;
@@ -400,6 +421,7 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
   if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done
   tc_fence_before();
   __syncthreads();
+  if (CM > 1) cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
   if (warp == 1) tmem_dealloc(tmem, 2 * NMMA * BN);
 }
 
@@ -490,12 +512,17 @@ static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
   return best;
 }
 
-template <int BN>
-static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
+// may this op run split-K (single launch with scratch, explicit or automatic splits)?
+static bool op_wants_split(const GemmOp &op) {
+  return op.flags && op.partials && (op.splits > 1 || (op.splits <= 0 && getenv("JANUS_GEMM_AUTOSPLIT")));
+}
+
+template <int BN, int CM>
+static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
   constexpr int STAGES = BN == 256 ? 4 : 6;
   constexpr int NMMA = BN == 256 ? 1 : 2;
   using C = GemmCfg<BN, STAGES, NMMA>;
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES, NMMA>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, NMMA, CM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -516,8 +543,8 @@ static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
     const GemmOp &op = ops[g];
     bool ok = op.a_mn ? make_tmap_bf16(&gb.ta[g], op.A, op.M, op.K, op.lda, 64)
                       : make_tmap_bf16(&gb.ta[g], op.A, op.K, op.M, op.lda, 128);
-    ok = ok && (op.b_mn ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, 64)
-                        : make_tmap_bf16(&gb.tb[g], op.B, op.K, op.N, op.ldb, BN));
+    ok = ok && (op.b_mn ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, 64 / CM)
+                        : make_tmap_bf16(&gb.tb[g], op.B, op.K, op.N, op.ldb, BN / CM));
     gb.amn[g] = op.a_mn ? 1 : 0;
     gb.bmn[g] = op.b_mn ? 1 : 0;
     if (!ok) return cudaErrorInvalidValue;
@@ -526,12 +553,12 @@ static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
         g_tma_store_ok)
       gb.tma_store[g] = make_tmap_f32_box32(&gb.tc[g], op.ep.C, op.N, op.M, op.ep.ldc) ? 1 : 0;
     TileMap &tm = gb.tm[g];
-    tm.Mb = (op.M + 127) / 128;
+    tm.Mb = ((op.M + 127) / 128 + CM - 1) / CM;  // m-groups of CM blocks (ghost blocks: OOB)
     tm.Nb = (op.N + BN - 1) / BN;
     const int nk = (op.K + 63) / 64;
     const size_t cap_tiles = op.partials ? op.partials_cap / (128 * BN) : 0;
     int splits = 1;
-    if (n == 1 && op.flags && op.partials) {  // split-K only for single launches (own scratch)
+    if (CM == 1 && n == 1 && op.flags && op.partials) {  // split-K only for single launches (own scratch)
       splits = op.splits > 0 ? op.splits : choose_splits(tm.Mb * tm.Nb, nk, g_num_sms, cap_tiles);
       splits = std::max(1, std::min(splits, 64));
       if ((size_t)tm.Mb * tm.Nb * splits > cap_tiles) splits = 1;
@@ -548,9 +575,37 @@ static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   }
   gb.tile_start[n] = total;
   if (total == 0) return cudaSuccess;
-  const int grid = std::min(total, g_num_sms);
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(gb);
-  return cudaGetLastError();
+  if (CM == 1) {
+    const int grid = std::min(total, g_num_sms);
+    kern<<<grid, C::THREADS, C::SMEM, st>>>(gb);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::min(total, g_num_sms / CM) * CM);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CM;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, gb);
+}
+
+// Clusters of two CTAs along M share the B tile (multicast TMA): the tensor pipe of these
+// GEMMs is fed at L2 -> smem rates, and halving B's share of that traffic is the lever.
+// JANUS_GEMM_CM=1 disables it.
+static int g_gemm_cm = getenv("JANUS_GEMM_CM") ? atoi(getenv("JANUS_GEMM_CM")) : 2;
+
+template <int BN>
+static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
+  bool split = false;
+  for (int g = 0; g < n; ++g) split = split || (op_wants_split(ops[g]) && n == 1);
+  if (g_gemm_cm == 2 && !split) return launch_cm<BN, 2>(ops, n, st);
+  return launch_cm<BN, 1>(ops, n, st);
 }
 
 static cudaError_t check_op(const GemmOp &op) {
