@@ -219,7 +219,7 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         del ws_i
         # --- C5: 10% of batches violate an assumption and fall back to the imperative path
         r = gen.rng(gen.SEED_C5)
-        nb = 40
+        nb = 200
         viol = r.random(nb) < 0.10
         viol[0] = True
         kinds = ["dtype", "shape", "tag", "trip"]
@@ -262,6 +262,42 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
                             "fallback_status": fb,
                             "note": "wall clock incl. the host syncs of the imperative fallbacks"}
         del ws5
+        # --- C5 through the graph cache + relaxation driver (NEXT-1): the same violation stream;
+        # assumptions that break twice are relaxed and their batches return to the device path
+        sess = J.Session(prog)
+        st5 = [s.clone() for s in state]
+        paths = {"graph": 0, "imperative": 0}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nv = 0
+        for k in range(nb):
+            tok, tgt, ln = dev_batches[k % len(dev_batches)]
+            a = [tok, tgt, ln]
+            if viol[k]:
+                kind = kinds[nv % 4]
+                nv += 1
+                if kind == "dtype":
+                    a = [tok.long(), tgt, ln]
+                elif kind == "shape":
+                    a = [tok[:B - 1].contiguous(), tgt[:B - 1].contiguous(), ln[:B - 1].contiguous()]
+                elif kind == "tag":
+                    st5[tag_slot].zero_()
+                else:
+                    l2 = ln.clone(); l2[3] = T - 1
+                    a = [tok, tgt, l2]
+            s, info = sess.step(a, st5, outs=[loss], stream=stream)
+            paths[info["path"]] += 1
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        sst = sess.stats()
+        out["c5_stress_session"] = {
+            "batches": nb, "violations": int(viol.sum()), "blended_samples_per_s": nb * B / dt,
+            "paths": paths, "misses": sst["misses"], "aborts": sst["aborts"], "generated": sst["generated"],
+            "entries": [{k: e[k] for k in ("id", "active", "device", "hits", "origin")} for e in sst["entries"]],
+            "note": "janus_session_step: cache lookup, imperative fallback in the same call, relax after 2 "
+                    "failures of one assumption (TRIP_COUNT -> device While, TYPE_TAG -> device Switch); "
+                    "the first relaxed graph's build and workspace allocation are inside the timed loop"}
+        del sess
         # --- C3 TreeLSTM
         for Bt in (25, 256):
             tp = pg.treelstm_program(V=20000, E=300, H=300, C=2, B=Bt, lr=0.05)

@@ -45,7 +45,9 @@ typedef enum {
   JANUS_ERR_UNSUPPORTED = 3,  /* graph valid but the device path cannot run it exactly       */
   JANUS_ERR_RUNTIME = 4,      /* runtime error in a node (bad token id, bad child id)         */
   JANUS_ERR_CUDA = 5,
-  JANUS_ERR_NCCL = 6
+  JANUS_ERR_NCCL = 6,
+  JANUS_ERR_WORKSPACE = 7     /* janus_session_step: workspace smaller than the dispatched
+                                 graph needs; nothing ran (required bytes in the step info) */
 } janus_status;
 
 typedef enum { JANUS_F32 = 0, JANUS_BF16 = 1, JANUS_I32 = 2, JANUS_I64 = 3, JANUS_U8 = 4 } janus_dtype;
@@ -81,6 +83,7 @@ typedef struct {
  *   OUTPUT         in0 = value; iattr0 = output index
  *   ADD, LESS, EQ  in0, in1 (scalar ∘ scalar, or scalar ∘ vector elementwise; LESS/EQ give int32)
  *   MAX_REDUCE     in0 int32 vector -> int32 scalar
+ *   LEN            in0 tensor -> int32 scalar = shape[0] (the whitelisted `len`)
  *   SUM            in0 f32 tensor -> f32 scalar (sum of all elements)
  *   ZEROS_LIKE     in0 -> zeros of the same dtype/shape
  *   COLUMN         in0 = matrix [B,T], in1 = scalar t -> vector [B] = in0[:, t]
@@ -122,8 +125,8 @@ typedef enum {
   JOP_TA_NEW = 21, JOP_TA_WRITE = 22, JOP_TA_STACK = 23,
   JOP_SWITCH = 24, JOP_MERGE = 25, JOP_ENTER = 26, JOP_EXIT = 27, JOP_NEXT_ITERATION = 28,
   JOP_LOOP_COND = 29, JOP_IDENTITY = 30, JOP_INVOKE = 31, JOP_RETURN = 32,
-  JOP_SGD_APPLY = 33,
-  JOP__COUNT = 34
+  JOP_SGD_APPLY = 33, JOP_LEN = 34,
+  JOP__COUNT = 35
 } janus_op_kind;
 
 #define JANUS_MAX_IN 12
@@ -215,7 +218,9 @@ janus_status janus_graph_build(const janus_op *ops, int32_t n_ops, const janus_a
                                char *err, size_t err_len);
 
 /* Device bytes the caller must allocate for `workspace` (graph path and imperative path). The
- * workspace must stay alive and unmodified between calls (it caches bf16 operand copies). */
+ * first janus_run on a workspace zero-fills it (the device program keeps zero pads and counters
+ * there across steps); later runs reuse it as left, so the caller must not modify it between
+ * calls. janus_run_imperative may write anywhere in it; the next janus_run re-initialises. */
 janus_status janus_workspace_bytes(const janus_graph *g, size_t *bytes);
 
 /* One speculative graph step. Enqueues on cuda_stream (a cudaStream_t; NULL = default)
@@ -249,6 +254,101 @@ janus_status janus_describe(const janus_graph *g, char *buf, size_t buf_len);
 void janus_graph_destroy(janus_graph *g); /* NULL-safe */
 const char *janus_status_str(janus_status s);
 int32_t janus_abi_version(void);
+
+/* ---------------------------------------------------------------------------------------------
+ * Graph cache + relaxation driver (Figure 2 of the paper).
+ *
+ * A session owns the generic op list and a cache of speculatively specialised graphs, each saved
+ * with the assumptions it was generated under ("the optimized graph and the assumption that
+ * were used to generate the graph are saved into the graph cache"). Every step:
+ *   1. Dispatch: the first active entry whose DISPATCH assumptions hold for the argument
+ *      metadata runs janus_run. No entry matches = cache miss: the step runs imperatively
+ *      (janus_run_imperative of a graph built without assumptions).
+ *   2. An AssertOp failure falls back to the imperative executor in the same call
+ *      ("falls back to the imperative executor"), so a step always returns the imperative
+ *      result when an assumption breaks.
+ *   3. Policy ("gives up further optimizations that rely on the assumptions that
+ *      repeatedly break"; SPEC S:516-524 threshold 2): once the SAME assumption of an entry has
+ *      failed `fail_threshold` times (only failures whose fallback committed count), the entry is
+ *      retired and regenerated with that assumption relaxed one level (janus_relax); once the
+ *      same dispatch key has missed `fail_threshold` times, a graph specialised to the observed
+ *      key is generated — a shape-only miss first tries the per-dim join of Figure 4 (P:246-248,
+ *      "(4, 8) and (3, 8)" -> "(?, 8)") and replaces the old entry if the joined graph still has
+ *      a device program; otherwise the new entry coexists with the old one (one specialised graph
+ *      per key, as the cache keys on argument types).
+ *   A generated graph without a device program (janus_graph_build ERR_UNSUPPORTED) is cached as
+ *   an imperative-only entry: its key dispatches straight to the imperative executor.
+ * Entries are never re-specialised once relaxed (relaxation is monotone; with at most 2 levels
+ * per assumption the number of aborts per assumption is bounded by 2 * fail_threshold).
+ * Single-GPU only (world_size must be 1): regeneration would need a fresh NCCL communicator.
+ * A session is not thread-safe; one step at a time (as janus_run).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct janus_session janus_session;
+
+typedef struct {
+  int32_t fail_threshold;  /* failures (misses) of one assumption (key) before regeneration; <=0 -> 2 */
+  int32_t cache_max;       /* active entries kept (least recently dispatched retired); <=0 -> unlimited */
+  int32_t reserved[6];
+} janus_session_opts;
+
+enum { JANUS_PATH_GRAPH = 0, JANUS_PATH_IMPERATIVE = 1 };
+enum {
+  JANUS_EV_HIT = 0,               /* dispatched, every assumption held: graph result       */
+  JANUS_EV_MISS = 1,              /* no entry matched: imperative (P:162 cache miss)       */
+  JANUS_EV_ABORT = 2,             /* dispatched, an AssertOp failed: imperative fallback   */
+  JANUS_EV_IMPERATIVE_ENTRY = 3   /* dispatched to an entry without a device program       */
+};
+
+typedef struct {
+  int32_t path;             /* JANUS_PATH_* that produced the returned result                */
+  int32_t event;            /* JANUS_EV_*                                                    */
+  int32_t entry;            /* id of the dispatched entry, -1 on a miss                      */
+  int32_t generated;        /* id of the entry generated by this step, -1 if none            */
+  janus_failure fail;       /* MISS: first failing DISPATCH assumption of the first active
+                               entry; ABORT: the AssertOp failure (zeroed on a HIT)          */
+  uint64_t workspace_bytes; /* bytes the step needs (always set; see JANUS_ERR_WORKSPACE)    */
+} janus_step_info;
+
+/* Copies the op list and assumptions, builds the initial entry (the caller's assumptions, i.e.
+ * the profiled context of P:150) and the assumption-free graph used for cache misses.
+ * Status as janus_graph_build for the op list; the initial entry may lack a device program.
+ * opts may be NULL (defaults); bopts as for janus_graph_build (world_size must be 1). */
+janus_status janus_session_create(const janus_op *ops, int32_t n_ops, const janus_assumption *asms,
+                                  int32_t n_asms, const janus_build_opts *bopts,
+                                  const janus_session_opts *opts, janus_session **out, char *err,
+                                  size_t err_len);
+
+/* Largest workspace any active entry (or the miss path) of the session currently needs. */
+janus_status janus_session_workspace_bytes(const janus_session *s, size_t *bytes);
+
+/* One step through the cache (see above). Arguments as janus_run. Returns the status of the
+ * result that was committed (JANUS_OK, or the imperative executor's ERR_RUNTIME / ERR_*); never
+ * JANUS_ASSUMPTION_FAILED. JANUS_ERR_WORKSPACE: nothing ran and no counter moved; grow the
+ * workspace to info->workspace_bytes and call again. info may be NULL. */
+janus_status janus_session_step(janus_session *s, const janus_tensor *args, int32_t n_args,
+                                const janus_tensor *state, int32_t n_state,
+                                const janus_tensor *outs, int32_t n_outs, janus_tensor workspace,
+                                void *cuda_stream, janus_step_info *info);
+
+/* JSON report (SPEC S:508-516 analogue): calls, graph/imperative calls, misses, aborts by
+ * assumption id, generated entries and every entry (id, active, device, hits, assumptions). */
+janus_status janus_session_stats(const janus_session *s, char *buf, size_t buf_len);
+
+void janus_session_destroy(janus_session *s); /* NULL-safe */
+
+/* Relax one failed assumption one level up the specialisation hierarchy (Figure 4, P:240-248;
+ * SPEC S:253-261 relax). `observed` = metadata of the offending argument (DISPATCH kinds; may be
+ * NULL otherwise; only dtype/ndim/shape are read, data is never touched).
+ *   DTYPE_EQ    -> DTYPE_EQ on the observed dtype (the cache keys on argument types)
+ *   SHAPE_MATCH -> per-dim join with the observed shape: dims that differ become -1 ('?');
+ *                  a rank mismatch drops the assumption (kind level)
+ *   TRIP_COUNT  -> RANGE [1, value] on the same argument: the loop is regenerated as a bounded
+ *                  device While (P:222 Enter/Exit/NextIteration) instead of unrolled
+ *   TYPE_TAG, VALUE_EQ, RANGE, TREE_BINARY -> dropped (the construct is evaluated on the
+ *                  device or the graph loses its device program)
+ * *out receives the relaxed assumption (same id) unless *dropped = 1. Pure host function. */
+janus_status janus_relax(const janus_assumption *a, const janus_tensor *observed,
+                         janus_assumption *out, int32_t *dropped);
 
 #ifdef __cplusplus
 }

@@ -432,6 +432,8 @@ class GraphExec:
             else:
                 out = Val((a == b).astype(np.int64))
             put(n, 0, tag, out)
+        elif k == "LEN":                               # whitelisted len
+            put(n, 0, tag, Val(np.array(len(d[0]), np.int64)))
         elif k == "MAX_REDUCE":
             put(n, 0, tag, Val(np.array(np.max(d[0]), np.int64)))
         elif k == "SUM":

@@ -124,6 +124,9 @@ struct Graph {
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
   std::string describe;
   const void *gflags_ws = nullptr;        // workspace whose split-K counters were zeroed
+  // workspace the device program last initialised (zero-filled on first use by janus_run; the
+  // imperative executor writes anywhere in it, so running it on the same buffer clears this)
+  const void *ws_ready = nullptr;
   unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*16*T u64)
 };
 
@@ -175,3 +178,6 @@ janus_status cuda_status(cudaError_t e);
 bool is_device_ptr(const void *p);
 
 }  // namespace jk
+
+// the opaque handle of janus.h is the host graph object
+struct janus_graph : public jk::Graph {};

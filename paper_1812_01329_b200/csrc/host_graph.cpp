@@ -20,7 +20,7 @@ namespace jk {
 static int arity(int k) {
   switch (k) {
     case JOP_ARG: case JOP_CONST: case JOP_STATE_READ: case JOP_TA_NEW: return 0;
-    case JOP_STATE_WRITE: case JOP_OUTPUT: case JOP_MAX_REDUCE: case JOP_SUM: case JOP_ZEROS_LIKE:
+    case JOP_STATE_WRITE: case JOP_OUTPUT: case JOP_MAX_REDUCE: case JOP_LEN: case JOP_SUM: case JOP_ZEROS_LIKE:
     case JOP_TA_STACK: case JOP_ENTER: case JOP_EXIT: case JOP_NEXT_ITERATION: case JOP_LOOP_COND:
     case JOP_IDENTITY: case JOP_SGD_APPLY: return 1;
     case JOP_ADD: case JOP_LESS: case JOP_EQ: case JOP_COLUMN: case JOP_ELEMENT: case JOP_EMBEDDING:
@@ -211,7 +211,6 @@ bool check_dispatch(const Graph &g, const janus_tensor *args, int n_args, janus_
 
 using namespace jk;
 
-struct janus_graph : public Graph {};
 
 extern "C" {
 
@@ -226,6 +225,7 @@ const char *janus_status_str(janus_status s) {
     case JANUS_ERR_RUNTIME: return "ERR_RUNTIME";
     case JANUS_ERR_CUDA: return "ERR_CUDA";
     case JANUS_ERR_NCCL: return "ERR_NCCL";
+    case JANUS_ERR_WORKSPACE: return "ERR_WORKSPACE";
   }
   return "UNKNOWN";
 }
@@ -293,18 +293,32 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
   if (n_args < g->n_args || n_state < g->n_state) return JANUS_ERR_INVALID;
   janus_failure f{};
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  // a workspace this graph has not initialised (new, or written by the imperative executor or
+  // another graph since) is zero-filled first: the device program relies on zero pads
+  auto ready = [&]() -> janus_status {
+    if (g->ws_ready == workspace.data) return JANUS_OK;
+    const size_t have = (size_t)workspace.shape[0] * (workspace.dtype == JANUS_U8 ? 1 : 4);
+    if (!workspace.data || have < g->ws_bytes) return JANUS_ERR_INVALID;
+    if (cudaMemsetAsync(workspace.data, 0, g->ws_bytes, st) != cudaSuccess) return JANUS_ERR_CUDA;
+    g->gflags_ws = nullptr;
+    g->ws_ready = workspace.data;
+    return JANUS_OK;
+  };
   if (!check_dispatch(*g, args, n_args, &f)) {
     g->aborts++;
     if (dp_enabled(*g) && g->kind == "lstm_lm" && g->lm.bf16) {
       // data parallel: still join the step's collectives (null step) so peers cannot block
-      janus_status r = run_lm_null(*g, f, workspace, st, fail);
+      janus_status r = ready();
+      if (r != JANUS_OK) return r;
+      r = run_lm_null(*g, f, workspace, st, fail);
       return r == JANUS_OK ? JANUS_ASSUMPTION_FAILED : r;
     }
     // cache miss: nothing is launched, nothing mutated
     if (fail) *fail = f;
     return JANUS_ASSUMPTION_FAILED;
   }
-  janus_status r;
+  janus_status r = ready();
+  if (r != JANUS_OK) return r;
   if (g->kind == "lstm_lm") r = run_lm(*g, args, state, outs, n_outs, workspace, st, fail);
   else r = run_tree(*g, args, n_args, state, outs, n_outs, workspace, st, fail);
   if (r == JANUS_ASSUMPTION_FAILED) g->aborts++;
@@ -316,6 +330,7 @@ janus_status janus_run_imperative(janus_graph *g, const janus_tensor *args, int3
                                   const janus_tensor *outs, int32_t n_outs,
                                   janus_tensor workspace, void *cuda_stream) {
   if (!g || (!args && n_args) || (!state && n_state)) return JANUS_ERR_INVALID;
+  if (g->ws_ready == workspace.data) g->ws_ready = nullptr;
   return run_imperative(*g, args, n_args, state, n_state, outs, n_outs, workspace,
                         static_cast<cudaStream_t>(cuda_stream));
 }

@@ -437,6 +437,9 @@ struct Interp {
         const int64_t x = as_host_int(in[0]), y = as_host_int(in[1]);
         return {host_i(op == 2 ? x == y : x < y), -2};
       }
+      case JOP_LEN:  // len(x): host metadata, no launch
+        need(!V(in[0]).shape.empty());
+        return {host_i(V(in[0]).shape[0]), -2};
       case JOP_MAX_REDUCE: {
         const int r = dev_i({});
         ck(imp::max_reduce(iptr(r), iptr(in[0]), (int)V(in[0]).numel(), st));

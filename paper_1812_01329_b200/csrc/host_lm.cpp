@@ -148,6 +148,11 @@ bool lower_lm(Graph &g, std::string &why) {
     }
   // assumptions -> specialisation + device guards
   int trip = -1, width = -1;
+  for (const auto &a : g.asms)
+    if (a.kind == JA_DTYPE_EQ && a.target >= 0 && a.target <= 2 && a.dtype != JANUS_I32) {
+      why = "device program takes int32 token / target / length arguments";
+      return false;
+    }
   for (const auto &a : g.asms) {
     if (a.kind == JA_TRIP_COUNT && a.target == 2) trip = (int)a.value;
     if (a.kind == JA_RANGE && a.target == 2) width = (int)a.hi;

@@ -48,6 +48,11 @@ bool lower_tree(Graph &g, std::string &why) {
     why = "not the recursive TreeLSTM pattern";
     return false;
   }
+  for (const auto &a : g.asms)
+    if (a.kind == JA_DTYPE_EQ && a.target >= 0 && a.target <= 5 && a.dtype != JANUS_I32) {
+      why = "device program takes int32 forest / label arguments";
+      return false;
+    }
   const janus_op &inv = g.ops[main_invoke];
   if (inv.n_in != 9) { why = "node() arity"; return false; }
   for (int k = 1; k <= 4; ++k) {

@@ -16,9 +16,12 @@ from workloads import programs as pg
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libjanus.so")
 
-OK, ASSUMPTION_FAILED, ERR_INVALID, ERR_UNSUPPORTED, ERR_RUNTIME, ERR_CUDA, ERR_NCCL = range(7)
+OK, ASSUMPTION_FAILED, ERR_INVALID, ERR_UNSUPPORTED, ERR_RUNTIME, ERR_CUDA, ERR_NCCL, ERR_WORKSPACE = range(8)
 STATUS_NAMES = ["OK", "ASSUMPTION_FAILED", "ERR_INVALID", "ERR_UNSUPPORTED", "ERR_RUNTIME",
-                "ERR_CUDA", "ERR_NCCL"]
+                "ERR_CUDA", "ERR_NCCL", "ERR_WORKSPACE"]
+PATH_GRAPH, PATH_IMPERATIVE = 0, 1
+EV_HIT, EV_MISS, EV_ABORT, EV_IMPERATIVE_ENTRY = range(4)
+EVENT_NAMES = ["HIT", "MISS", "ABORT", "IMPERATIVE_ENTRY"]
 F32, BF16, I32, I64, U8 = range(5)
 
 
@@ -51,13 +54,23 @@ class JanusBuildOpts(C.Structure):
                 ("fail_assert_id", C.c_int32), ("reserved", C.c_int32 * 5)]
 
 
+class JanusSessionOpts(C.Structure):
+    _fields_ = [("fail_threshold", C.c_int32), ("cache_max", C.c_int32), ("reserved", C.c_int32 * 6)]
+
+
+class JanusStepInfo(C.Structure):
+    _fields_ = [("path", C.c_int32), ("event", C.c_int32), ("entry", C.c_int32), ("generated", C.c_int32),
+                ("fail", JanusFailure), ("workspace_bytes", C.c_uint64)]
+
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libjanus.so not built ({LIB_PATH}); run __graft_entry__.build()")
 lib = C.CDLL(LIB_PATH)
 
 EXPORTS = ["janus_graph_build", "janus_workspace_bytes", "janus_run", "janus_run_imperative",
            "janus_counters", "janus_describe", "janus_graph_destroy", "janus_status_str",
-           "janus_abi_version"]
+           "janus_abi_version", "janus_session_create", "janus_session_workspace_bytes",
+           "janus_session_step", "janus_session_stats", "janus_session_destroy", "janus_relax"]
 DEV_EXPORTS = ["janus_dev_gemm_bf16", "janus_dev_gemm_bf16_splitk"]
 
 _P = C.c_void_p
@@ -114,6 +127,17 @@ _sigs = {
     "janus_graph_destroy": (None, [C.c_void_p]),
     "janus_status_str": (C.c_char_p, [C.c_int]),
     "janus_abi_version": (C.c_int32, []),
+    "janus_session_create": (C.c_int, [C.POINTER(JanusOp), C.c_int32, C.POINTER(JanusAssumption), C.c_int32,
+                                       C.POINTER(JanusBuildOpts), C.POINTER(JanusSessionOpts),
+                                       C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
+    "janus_session_workspace_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "janus_session_step": (C.c_int, [C.c_void_p, C.POINTER(JanusTensor), C.c_int32, C.POINTER(JanusTensor),
+                                     C.c_int32, C.POINTER(JanusTensor), C.c_int32, JanusTensor, C.c_void_p,
+                                     C.POINTER(JanusStepInfo)]),
+    "janus_session_stats": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "janus_session_destroy": (None, [C.c_void_p]),
+    "janus_relax": (C.c_int, [C.POINTER(JanusAssumption), C.POINTER(JanusTensor), C.POINTER(JanusAssumption),
+                              C.POINTER(C.c_int32)]),
 }
 for _n, (_r, _a) in _sigs.items():
     _f = getattr(lib, _n)
@@ -203,15 +227,7 @@ class Graph:
     def __init__(self, program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False,
                  fail_assert_id=-1):
         self.program = program
-        opts = JanusBuildOpts()
-        opts.world_size, opts.rank = world_size, rank
-        if nccl_id is not None:
-            for k, b in enumerate(bytes(nccl_id)[:128]):
-                opts.nccl_id[k] = b
-        gemm = gemm or program.meta.get("gemm", "bf16")
-        opts.gemm_dtype = F32 if gemm == "f32" else BF16
-        opts.strip_asserts = int(strip_asserts)
-        opts.fail_assert_id = fail_assert_id
+        opts = _build_opts(program, gemm, world_size, rank, nccl_id, strip_asserts, fail_assert_id)
         self._ops = marshal_ops(program)
         self._asms = marshal_assumptions(program)
         h = C.c_void_p()
@@ -271,6 +287,100 @@ lib.janus_dev_phase_report.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
 
 lib.janus_nccl_unique_id.restype = C.c_int32
 lib.janus_nccl_unique_id.argtypes = [C.c_void_p]
+
+
+def _build_opts(program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False, fail_assert_id=-1):
+    opts = JanusBuildOpts()
+    opts.world_size, opts.rank = world_size, rank
+    if nccl_id is not None:
+        for k, b in enumerate(bytes(nccl_id)[:128]):
+            opts.nccl_id[k] = b
+    gemm = gemm or program.meta.get("gemm", "bf16")
+    opts.gemm_dtype = F32 if gemm == "f32" else BF16
+    opts.strip_asserts = int(strip_asserts)
+    opts.fail_assert_id = fail_assert_id
+    return opts
+
+
+class Session:
+    """Graph cache + relaxation driver (janus_session_*): every step dispatches to a cached
+    specialised graph, falls back to the imperative executor on a miss or an AssertOp failure, and
+    regenerates graphs whose assumptions repeatedly break. Owns a device workspace (torch) that
+    grows when the library asks for more (JANUS_ERR_WORKSPACE)."""
+
+    def __init__(self, program, gemm=None, fail_threshold=2, cache_max=0, strip_asserts=False,
+                 fail_assert_id=-1, device="cuda"):
+        self.program = program
+        opts = _build_opts(program, gemm, strip_asserts=strip_asserts, fail_assert_id=fail_assert_id)
+        so = JanusSessionOpts()
+        so.fail_threshold, so.cache_max = fail_threshold, cache_max
+        self._ops = marshal_ops(program)
+        self._asms = marshal_assumptions(program)
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        r = lib.janus_session_create(self._ops, len(program.ops), self._asms, len(program.assumptions),
+                                     C.byref(opts), C.byref(so), C.byref(h), err, 1024)
+        if r not in (OK, ERR_UNSUPPORTED) or not h.value:
+            raise JanusError(f"janus_session_create: {STATUS_NAMES[r]}: {err.value.decode()}")
+        self.h = h
+        self.device = device
+        self.workspace = None
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.janus_session_destroy(self.h)
+            self.h = None
+
+    def workspace_bytes(self):
+        n = C.c_size_t()
+        lib.janus_session_workspace_bytes(self.h, C.byref(n))
+        return n.value
+
+    def step(self, args, state, outs=(), stream=None):
+        """janus_session_step: returns (status, info dict)."""
+        import torch
+        a, s, o = _jt_array(args), _jt_array(state), _jt_array(outs)
+        info = JanusStepInfo()
+        for _ in range(4):
+            if self.workspace is None:
+                self.workspace = torch.zeros(max(16, self.workspace_bytes()), dtype=torch.uint8, device=self.device)
+            r = lib.janus_session_step(self.h, a, len(args), s, len(state), o, len(outs), to_jt(self.workspace),
+                                       _stream(stream), C.byref(info))
+            if r != ERR_WORKSPACE:
+                break
+            self.workspace = None   # grow (the library asked for info.workspace_bytes)
+            self.workspace = torch.zeros(int(info.workspace_bytes), dtype=torch.uint8, device=self.device)
+        f = info.fail
+        return r, dict(path="graph" if info.path == PATH_GRAPH else "imperative", event=EVENT_NAMES[info.event],
+                       entry=info.entry, generated=info.generated,
+                       fail=dict(assumption_id=f.assumption_id, rank=f.rank, index=f.index, observed=f.observed),
+                       workspace_bytes=int(info.workspace_bytes))
+
+    def stats(self):
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        if lib.janus_session_stats(self.h, buf, 1 << 16) != OK:
+            raise JanusError("janus_session_stats")
+        return json.loads(buf.value.decode())
+
+
+def relax(assumption, observed=None):
+    """janus_relax on one programs.Assumption; observed = (dtype code, shape tuple) or None.
+    Returns the relaxed JanusAssumption, or None when the assumption is dropped."""
+    src = marshal_assumptions(type("P", (), {"assumptions": [assumption]}))
+    jt = None
+    if observed is not None:
+        jt = JanusTensor()
+        jt.dtype, shape = observed
+        jt.ndim = len(shape)
+        for k, d in enumerate(shape):
+            jt.shape[k] = d
+    out = JanusAssumption()
+    dropped = C.c_int32()
+    r = lib.janus_relax(src, C.byref(jt) if jt is not None else None, C.byref(out), C.byref(dropped))
+    if r != OK:
+        raise JanusError(f"janus_relax: {STATUS_NAMES[r]}")
+    return None if dropped.value else out
 
 
 def nccl_unique_id():

@@ -26,7 +26,7 @@ OP_KINDS = [
     "TA_NEW", "TA_WRITE", "TA_STACK",
     "SWITCH", "MERGE", "ENTER", "EXIT", "NEXT_ITERATION",
     "LOOP_COND", "IDENTITY", "INVOKE", "RETURN",
-    "SGD_APPLY",
+    "SGD_APPLY", "LEN",
 ]
 OP_CODE = {k: i for i, k in enumerate(OP_KINDS)}
 
@@ -254,7 +254,7 @@ def treelstm_program(V, E, H, C, B, lr, *, max_nodes=127, speculate="levels", ge
         def node(n):                                    # function 1, recursive (InvokeOp)
             if kind[n] == LEAF: return leaf(embedding(word[n]))        # Switch/Merge
             else: return cell(node(left[n]), node(right[n]))
-        for i < B: roots += [node(tree_off[i+1]-1)]                    # loop frame
+        for i < len(label): roots += [node(tree_off[i+1]-1)]           # loop frame
         loss = xent(linear(roots), labels); optimizer update
 
     Arguments: 0 kind i32[N], 1 left i32[N], 2 right i32[N], 3 word i32[N], 4 tree_off i32[B+1],
@@ -291,7 +291,7 @@ def treelstm_program(V, E, H, C, B, lr, *, max_nodes=127, speculate="levels", ge
     rd = {s.name: _state_read(g, k, s) for k, s in enumerate(slots)}
     zero = g.op("CONST", i=[I32], f=[0.0])
     one = g.op("CONST", i=[I32], f=[1.0])
-    nB = g.op("CONST", i=[I32], f=[float(B)])
+    nB = g.op("LEN", [label])                        # for i < len(labels): the batch of trees
     acc0 = g.op("TA_NEW")
     FR = 1
     e_i = g.op("ENTER", [zero], i=[FR, 0])
