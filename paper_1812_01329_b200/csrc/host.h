@@ -19,6 +19,9 @@ struct LmPlan {
   bool while_mode = false;
   bool tag_specialised = false;  // TYPE_TAG assumed; otherwise the tag Switch runs on the device
   bool bf16 = true;              // tcgen05 path; false = single-CTA fp32 SIMT path
+  // dtype of the index arguments (tokens, targets, lengths) fixed by DTYPE_EQ: JANUS_I32, or
+  // JANUS_I64 (the type-specialised graph narrows them on the device first, as R10)
+  int arg_dtype[3] = {JANUS_I32, JANUS_I32, JANUS_I32};
   // state slots
   int slot_E = -1, slot_Wih[4] = {-1, -1, -1, -1}, slot_Whh[4] = {-1, -1, -1, -1},
       slot_b[4] = {-1, -1, -1, -1}, slot_Wdec = -1, slot_bdec = -1;
@@ -50,6 +53,7 @@ struct LmPlan {
 struct TreePlan {
   int V = 0, E = 0, H = 0, C = 0, B = 0, max_nodes = 127, max_N = 0;
   bool bf16 = true;
+  int arg_dtype[6] = {JANUS_I32, JANUS_I32, JANUS_I32, JANUS_I32, JANUS_I32, JANUS_I32};
   int slot_E = -1, slot_Wleaf = -1, slot_U = -1, slot_b = -1, slot_Wc = -1, slot_bc = -1;
   float lr_Wleaf = 0, lr_U = 0, lr_b = 0, lr_Wc = 0, lr_bc = 0;
   uint32_t tree_guard_id = 0;

@@ -20,6 +20,7 @@
 
 #include "gemm_tc.h"
 #include "host.h"
+#include "imp_kernels.h"
 #include "lm_rec.h"
 #include "lm_small.h"
 #include "step_kernels.h"
@@ -149,9 +150,12 @@ bool lower_lm(Graph &g, std::string &why) {
   // assumptions -> specialisation + device guards
   int trip = -1, width = -1;
   for (const auto &a : g.asms)
-    if (a.kind == JA_DTYPE_EQ && a.target >= 0 && a.target <= 2 && a.dtype != JANUS_I32) {
-      why = "device program takes int32 token / target / length arguments";
-      return false;
+    if (a.kind == JA_DTYPE_EQ && a.target >= 0 && a.target <= 2) {
+      if (a.dtype != JANUS_I32 && a.dtype != JANUS_I64) {
+        why = "token / target / length arguments must be int32 or int64";
+        return false;
+      }
+      p.arg_dtype[a.target] = a.dtype;
     }
   for (const auto &a : g.asms) {
     if (a.kind == JA_TRIP_COUNT && a.target == 2) trip = (int)a.value;
@@ -361,8 +365,16 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   const int *argp[3];
   for (int a = 0; a < 3; ++a) {
     const int64_t n = a < 2 ? (int64_t)B * Wd : B;
-    if (!tensor_ok(args[a], JANUS_I32, n)) return JANUS_ERR_INVALID;
-    if (is_device_ptr(args[a].data)) argp[a] = static_cast<const int *>(args[a].data);
+    if (!tensor_ok(args[a], p.arg_dtype[a], n)) return JANUS_ERR_INVALID;
+    if (p.arg_dtype[a] == JANUS_I64) {
+      // type-specialised graph (the cache keys on argument types): narrow on the device
+      if (!is_device_ptr(args[a].data)) return JANUS_ERR_INVALID;
+      int *dstp = reinterpret_cast<int *>(W + p.off.stage_args) + (size_t)a * B * p.T;
+      if (imp::i64_to_i32(dstp, static_cast<const long long *>(args[a].data), n, st) != cudaSuccess)
+        return JANUS_ERR_CUDA;
+      g.launches++;
+      argp[a] = dstp;
+    } else if (is_device_ptr(args[a].data)) argp[a] = static_cast<const int *>(args[a].data);
     else {
       int *dstp = reinterpret_cast<int *>(W + p.off.stage_args) + (size_t)a * B * p.T;
       if (cudaMemcpyAsync(dstp, args[a].data, n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess)

@@ -15,6 +15,7 @@
 
 #include "gemm_tc.h"
 #include "host.h"
+#include "imp_kernels.h"
 #include "step_kernels.h"
 #include "tree.h"
 
@@ -49,9 +50,12 @@ bool lower_tree(Graph &g, std::string &why) {
     return false;
   }
   for (const auto &a : g.asms)
-    if (a.kind == JA_DTYPE_EQ && a.target >= 0 && a.target <= 5 && a.dtype != JANUS_I32) {
-      why = "device program takes int32 forest / label arguments";
-      return false;
+    if (a.kind == JA_DTYPE_EQ && a.target >= 0 && a.target <= 5) {
+      if (a.dtype != JANUS_I32 && a.dtype != JANUS_I64) {
+        why = "forest / label arguments must be int32 or int64";
+        return false;
+      }
+      p.arg_dtype[a.target] = a.dtype;
     }
   const janus_op &inv = g.ops[main_invoke];
   if (inv.n_in != 9) { why = "node() arity"; return false; }
@@ -187,13 +191,25 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   uint8_t *W = static_cast<uint8_t *>(ws.data);
   const int N = (int)args[0].shape[0], B = p.B, H = p.H, E = p.E;
   if (args[0].ndim != 1 || N < 1 || N > p.max_N) return JANUS_ERR_INVALID;
-  for (int a = 1; a < 4; ++a)
-    if (args[a].ndim != 1 || args[a].shape[0] != N || args[a].dtype != JANUS_I32) return JANUS_ERR_INVALID;
-  // arguments: device pointers, or host buffers staged through the workspace
+  for (int a = 0; a < 6; ++a) {
+    const int64_t n = a < 4 ? N : (a == 4 ? B + 1 : B);
+    if (args[a].ndim != 1 || args[a].shape[0] != n || args[a].dtype != p.arg_dtype[a]) return JANUS_ERR_INVALID;
+  }
+  // arguments: device pointers, or host buffers staged through the workspace; int64 arguments
+  // of a type-specialised graph are narrowed on the device into the same staging area
   const int *argp[6];
   int *stage = reinterpret_cast<int *>(W + p.off.stage_args);
   for (int a = 0; a < 6; ++a) {
     const int64_t n = a < 4 ? N : (a == 4 ? B + 1 : B);
+    if (p.arg_dtype[a] == JANUS_I64) {
+      if (!is_device_ptr(args[a].data)) return JANUS_ERR_INVALID;
+      if (imp::i64_to_i32(stage, static_cast<const long long *>(args[a].data), n, st) != cudaSuccess)
+        return JANUS_ERR_CUDA;
+      g.launches++;
+      argp[a] = stage;
+      stage += n;
+      continue;
+    }
     if (is_device_ptr(args[a].data)) { argp[a] = static_cast<const int *>(args[a].data); continue; }
     if (cudaMemcpyAsync(stage, args[a].data, n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess) return JANUS_ERR_CUDA;
     argp[a] = stage;

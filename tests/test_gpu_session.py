@@ -80,7 +80,9 @@ def test_session_type_tag_relaxed_to_device_switch():
     assert "3:TYPE_TAG" not in " ".join(sess.stats()["entries"][1]["assumptions"])
 
 
-def test_session_dtype_miss_generates_imperative_entry_and_keeps_int32_graph():
+def test_session_dtype_miss_generates_int64_graph_and_keeps_int32_graph():
+    """int64 tokens miss the int32 graph twice; the graph generated for the int64 key (the cache
+    keys on argument types) runs on the device beside the int32 one."""
     B, T, V = 8, 6, 64
     prog = pg.lstm_lm_program(V=V, E=40, H=48, L=2, B=B, T=T, lr=0.5)
     sess = J().Session(prog)
@@ -92,11 +94,12 @@ def test_session_dtype_miss_generates_imperative_entry_and_keeps_int32_graph():
         dev = to_dev(state)
         info, state = _check(prog, sess, args, state, dev, what=f"step {k}")
         seen.append((info["event"], info["path"], info["generated"]))
-    assert seen == [("MISS", "imperative", -1), ("MISS", "imperative", 1), ("IMPERATIVE_ENTRY", "imperative", -1),
-                    ("HIT", "graph", -1), ("IMPERATIVE_ENTRY", "imperative", -1)]
+    assert seen == [("MISS", "imperative", -1), ("MISS", "imperative", 1), ("HIT", "graph", -1),
+                    ("HIT", "graph", -1), ("HIT", "graph", -1)]
     st = sess.stats()
     assert st["misses"] == 2 and st["entries"][0]["active"] and st["entries"][0]["hits"] == 1
-    assert not st["entries"][1]["device"] and "0:DTYPE_EQ(arg0,dt3)" in st["entries"][1]["assumptions"]
+    assert st["entries"][1]["device"] and st["entries"][1]["hits"] == 2
+    assert "0:DTYPE_EQ(arg0,dt3)" in st["entries"][1]["assumptions"]
 
 
 def test_session_shape_errors_are_not_specialised():
@@ -134,3 +137,41 @@ def test_session_tree_partial_minibatch_gets_its_own_graph():
     ents = sess.stats()["entries"]
     assert [e["active"] for e in ents] == [True, False, True] and ents[2]["origin"] == "miss-key"
     assert "6:SHAPE_MATCH(arg4,(5))" in ents[2]["assumptions"]
+
+
+def test_int64_specialised_graphs_match_the_oracle():
+    """Type-specialised graphs for int64 index arguments (LM tokens/targets/lengths, every tree
+    array) run on the device and commit the imperative program's result."""
+    janus = J()
+    B, T, V = 8, 6, 64
+    prog = pg.lstm_lm_program(V=V, E=40, H=48, L=2, B=B, T=T, lr=0.5)
+    for a in prog.assumptions:
+        if a.kind == "DTYPE_EQ":
+            a.dtype = 3
+    g = janus.Graph(prog)
+    assert g.device_path, g.build_message
+    state = gen.uniform_params(prog, 17, 0.1)
+    ws = g.new_workspace()
+    for k, b in enumerate(gen.lm_batches(gen.SEED_C2, B, T, V, 2)):
+        args = [x.astype(np.int64) for x in b]
+        dev, loss = to_dev(state), torch.zeros(1, device="cuda")
+        st, _ = g.run(to_dev(args), dev, ws, outs=[loss])
+        ora = I.run_imperative_step(prog, args, state, mode="bf16")
+        assert st == I.OK == ora.status
+        assert rel_err(float(loss.item()), ora.outputs[0]) <= 2e-2
+        assert_state_parity(prog, state, to_host(dev), ora.state, 2e-2, what=f"lm i64 step {k}")
+        state = ora.state
+    tp = pg.treelstm_program(V=50, E=24, H=32, C=2, B=5, lr=0.1)
+    for a in tp.assumptions:
+        if a.kind == "DTYPE_EQ":
+            a.dtype = 3
+    gt = janus.Graph(tp)
+    assert gt.device_path, gt.build_message
+    state = gen.uniform_params(tp, 5, 0.1)
+    args = [x.astype(np.int64) for x in gen.sst_forest(gen.SEED_C3, 1, 5, 50, max_leaves=12)]
+    dev, loss = to_dev(state), torch.zeros(1, device="cuda")
+    st, _ = gt.run(to_dev(args), dev, gt.new_workspace(), outs=[loss])
+    ora = I.run_imperative_step(tp, args, state, mode="bf16")
+    assert st == I.OK == ora.status
+    assert rel_err(float(loss.item()), ora.outputs[0]) <= 2e-2
+    assert_state_parity(tp, state, to_host(dev), ora.state, 2e-2, what="tree i64")

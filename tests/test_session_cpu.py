@@ -70,19 +70,22 @@ def test_relax_is_a_least_upper_bound_brute_force():
                 assert _dims(janus.relax(Assumption(1, "SHAPE_MATCH", DISPATCH, 0, dims=new), (I32, obs))) == new
 
 
-def test_int64_arguments_have_no_device_program():
-    """The device programs take int32 indices: a graph specialised to int64 tokens is an
-    imperative-only graph (ERR_UNSUPPORTED at build), never a device program reading int64 as int32."""
+def test_index_argument_dtypes_specialise_the_graph():
+    """A graph specialised to int64 index arguments keeps its device program (it narrows them on
+    the device, R10); any other index dtype has none (ERR_UNSUPPORTED: imperative only)."""
     janus = J()
-    prog = pg.lstm_lm_program(V=20, E=8, H=8, L=1, B=2, T=3, lr=0.1)
-    for a in prog.assumptions:
-        if a.kind == "DTYPE_EQ" and a.target == 0:
-            a.dtype = I64
-    g = janus.Graph(prog)
-    assert not g.device_path and "int32" in g.build_message
-    tp = pg.treelstm_program(V=20, E=8, H=8, C=2, B=2, lr=0.1)
-    tp.assumptions[1].dtype = I64
-    assert not janus.Graph(tp).device_path
+    for dt, device in ((I64, True), (0, False)):
+        prog = pg.lstm_lm_program(V=20, E=8, H=8, L=1, B=2, T=3, lr=0.1)
+        for a in prog.assumptions:
+            if a.kind == "DTYPE_EQ" and a.target == 0:
+                a.dtype = dt
+        g = janus.Graph(prog)
+        assert g.device_path == device, g.build_message
+        if not device:
+            assert "int32 or int64" in g.build_message
+        tp = pg.treelstm_program(V=20, E=8, H=8, C=2, B=2, lr=0.1)
+        tp.assumptions[1].dtype = dt
+        assert janus.Graph(tp).device_path == device
 
 
 def test_session_create_and_stats_on_cpu():
