@@ -68,6 +68,7 @@ bool lower_tree(Graph &g, std::string &why) {
   p.V = (int)d[0]; p.E = (int)d[1];
   if (!slot_dims(g, inv.in_node[6], &p.slot_Wleaf, d)) { why = "W_leaf slot"; return false; }
   p.H = (int)(d[0] / 3);
+  if (p.H > 1024) { why = "hidden size > 1024 (the forward keeps the bias in shared memory)"; return false; }
   if (d[0] != 3 * p.H || d[1] != p.E) { why = "W_leaf shape"; return false; }
   if (!slot_dims(g, inv.in_node[7], &p.slot_U, d) || d[0] != 5 * p.H || d[1] != 2 * p.H) { why = "U shape"; return false; }
   if (!slot_dims(g, inv.in_node[8], &p.slot_b, d) || d[0] != 4 * p.H) { why = "b shape"; return false; }
@@ -246,6 +247,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   t.c_leaf = fp(p.off.c_leaf); t.root_h = fp(p.off.root_h); t.dh_node = fp(p.off.dh_node);
   t.dc_node = fp(p.off.dc_node); t.DZ_int = bf(p.off.DZ_int); t.DZ_leaf = bf(p.off.DZ_leaf);
   t.gWc = fp(p.off.gWc); t.gbc = fp(p.off.gbc); t.rowloss = fp(p.off.rowloss); t.barrier = bars;
+  t.dbg = g.probe;
 
   // guards (AssertOps): forest structure + any other runtime assumption
   GuardList gl{};

@@ -23,7 +23,7 @@ constexpr int T_NMW = 4;          // MMA-issuing warps (one accumulator each; ~1
 constexpr int TT = 160 + 32 * T_NMW;  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
 // ring stages: a multiple of T_NMW, so a stage is always consumed by the same MMA warp (it owns
 // chunks q = w mod T_NMW) and that warp can never wait on a stage two phases ahead of its loads
-constexpr int T_STAGES = 8;
+constexpr int T_STAGES = 8;  // backward ring; the forward uses 6 (or 4) to fit its staging buffers
 constexpr int T_ASTAGE = 128 * 128;  // A chunk: 128 rows x 64 bf16
 constexpr int T_BSTAGE = 80 * 128;   // B chunk: up to 80 rows x 64 bf16
 
@@ -33,14 +33,86 @@ JN_DEV float tanh_t(float x) {
   return copysignf(__fdividef(1.f - e, 1.f + e), x);
 }
 
-JN_DEV void grid_sync(unsigned int *ctr, unsigned int target) {
+JN_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Epilogue row helpers: a thread owns one node row and up to 16 consecutive units of it. Every
+// global load of the row is issued before the TMEM accumulator is ready (tile_loop's `pre`), so the
+// epilogue proper has no load behind a store to a possibly aliasing pointer; runs of 4 values move
+// as 16-byte vectors (vec: H % 4 == 0 keeps every row and unit group 16-B aligned), the tail of a
+// run that ends inside a group moves element by element.
+JN_DEV void ld_run(const float *p, bool vec, int n, float *o) {  // 16 values
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (vec && n >= 4 * g + 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(p + 4 * g);
+      o[4 * g] = v.x; o[4 * g + 1] = v.y; o[4 * g + 2] = v.z; o[4 * g + 3] = v.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[4 * g + i] = 4 * g + i < n ? p[4 * g + i] : 0.f;
+    }
+  }
+}
+JN_DEV void ld4_s(const float *p, bool vec, int n, float *o) {  // shared memory, 4 values
+  if (vec && n >= 4) {
+    const float4 v = *reinterpret_cast<const float4 *>(p);
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = i < n ? p[i] : 0.f;
+  }
+}
+JN_DEV void ld4_nc(const float *p, bool vec, int n, float *o) {  // read-only data, 4 values
+  if (vec && n >= 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(p));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = i < n ? __ldg(p + i) : 0.f;
+  }
+}
+template <int NV>  // NV floats, a multiple of 4
+JN_DEV void st_run(float *p, bool vec, int n, const float *v) {
+#pragma unroll
+  for (int g = 0; g < NV / 4; ++g) {
+    if (vec && n >= 4 * g + 4) {
+      *reinterpret_cast<float4 *>(p + 4 * g) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * g + i < n) p[4 * g + i] = v[4 * g + i];
+    }
+  }
+}
+JN_DEV void st4_bf16(__nv_bfloat16 *p, bool vec, int n, const float *v) {  // 4 values, one 8-B store
+  if (vec && n >= 4) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 w;
+    w.x = *reinterpret_cast<uint32_t *>(&a);
+    w.y = *reinterpret_cast<uint32_t *>(&b);
+    *reinterpret_cast<uint2 *>(p) = w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < n) p[i] = __float2bfloat16_rn(v[i]);
+  }
+}
+
+JN_DEV void grid_sync(unsigned int *ctr, unsigned int target, unsigned long long *dbg = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    const unsigned int k = target / gridDim.x;
+    if (dbg && k < 256) dbg[((size_t)k * 256 + blockIdx.x) * 2] = gtimer();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
     unsigned int v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
     } while (v < target);
+    if (dbg && k < 256) dbg[((size_t)k * 256 + blockIdx.x) * 2 + 1] = gtimer();
   }
   __syncthreads();
   fence_proxy_async_global();
@@ -251,11 +323,17 @@ struct Ring {
   uint32_t tmem;
   int q;      // chunk counter (both producer and MMA advance it identically)
   int tiles;  // tiles processed by this CTA (tfull phase)
+  float *zst; // STAGED tile loops: the accumulator tile [128][NT + 1] in shared memory
 };
 
-template <int NT, typename Epi>
+// STAGED: the epilogue threads park the accumulator tile in shared memory and the epilogue
+// functor receives (first row of the tile, valid rows, tile column base) on all 128 threads, so
+// a level with few nodes spreads its (row, unit) work over the whole epilogue instead of one
+// thread per row; otherwise it receives (row, tile column base, z[NT], pre's context) per row.
+template <int NT, bool STAGED = false, int NS = T_STAGES, typename Pre, typename Epi>
 JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, int row0, int M,
-                      int NTOT, int K, Epi epi, int nmw) {
+                      int NTOT, int K, Pre pre, Epi epi, int nmw, unsigned long long *pr = nullptr) {
+  while (NS % nmw) nmw >>= 1;  // a fixed MMA warp per ring stage
   // nmw in {1, 2, 4} MMA warps take part (T_STAGES % nmw == 0 keeps a fixed owner per stage):
   // more warps for long reductions, fewer TMEM tiles for the epilogue to sum on short ones
   const int warp = threadIdx.x >> 5;
@@ -268,7 +346,7 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
     if (warp == 4) {
       if ((threadIdx.x & 31) == 0)
         for (int kc = 0; kc < nk; ++kc) {
-          const int q = rg.q + kc, s = q % T_STAGES, r = q / T_STAGES;
+          const int q = rg.q + kc, s = q % NS, r = q / NS;
           if (r > 0) mbar_wait(&rg.empty[s], (r - 1) & 1);
           mbar_expect_tx(&rg.full[s], T_ASTAGE + NT * 128);
           tma_load_2d(rg.sA + s * T_ASTAGE, tmA, &rg.full[s], kc * 64, row0 + m * 128);
@@ -283,7 +361,7 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
         const uint32_t acc = rg.tmem + (uint32_t)(w * NT);
         const int kc0 = w < nmw ? ((w - rg.q) % nmw + nmw) % nmw : nk;  // my first chunk of this tile
         for (int kc = kc0; kc < nk; kc += nmw) {
-          const int q = rg.q + kc, s = q % T_STAGES, r = q / T_STAGES;
+          const int q = rg.q + kc, s = q % NS, r = q / NS;
           mbar_wait(&rg.full[s], r & 1);
           tc_fence_after();
           const uint32_t a = smem_u32(rg.sA + s * T_ASTAGE), b = smem_u32(rg.sB + s * T_BSTAGE);
@@ -297,9 +375,12 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
       }
       __syncwarp();
     } else {
+      const int row = m * 128 + threadIdx.x;
+      const auto ctx = pre(row < M ? row : -1, nn * NT);  // row metadata while the MMAs run
       mbar_wait(rg.tfull, rg.tiles & 1);
       __syncwarp();
       tc_fence_after();
+      if (pr && threadIdx.x == 0) pr[0] = gtimer();
       float z[NT];
 #pragma unroll
       for (int i = 0; i < NT; ++i) z[i] = 0.f;
@@ -321,8 +402,25 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
           for (int i = 0; i < 16; ++i) z[(NT / 32) * 32 + i] += v[i];
         }
       }
-      const int row = m * 128 + threadIdx.x;
-      if (row < M) epi(row, nn * NT, z);
+      if (pr) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 0) pr[2] = gtimer();
+      }
+      if constexpr (STAGED) {
+        float *zr = rg.zst + threadIdx.x * (NT + 1);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) zr[i] = z[i];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        epi(m * 128, min(128, M - m * 128), nn * NT);
+        (void)ctx;
+      } else {
+        if (row < M) epi(row, nn * NT, z, ctx);
+      }
+      if (pr) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 0) pr[1] = gtimer();
+        if (threadIdx.x == 0) pr[3] = pr[1];
+      }
     }
     rg.q += nk;
     rg.tiles += 1;
@@ -337,6 +435,7 @@ struct TreeFwdMaps {
   CUtensorMap x_leaf, w_leaf, stage_h, u;
 };
 
+template <int NS>
 __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__ TreeFwdMaps mp,
                                                          TreeBufs t, TreeDims d, TreeSched s,
                                                          const DevStatus *st) {
@@ -345,16 +444,21 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
                                               ~uintptr_t(1023));
   Ring rg;
   rg.sA = base;
-  rg.sB = base + T_STAGES * T_ASTAGE;
-  rg.full = reinterpret_cast<uint64_t *>(rg.sB + T_STAGES * T_BSTAGE);
-  rg.empty = rg.full + T_STAGES;
-  rg.tfull = rg.empty + T_STAGES;
+  rg.sB = base + NS * T_ASTAGE;
+  rg.full = reinterpret_cast<uint64_t *>(rg.sB + NS * T_BSTAGE);
+  rg.empty = rg.full + NS;
+  rg.tfull = rg.empty + NS;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rg.tfull + 1);
-  const int warp = threadIdx.x >> 5;
+  float *sbias = reinterpret_cast<float *>(base + NS * (T_ASTAGE + T_BSTAGE) + 256);
   const int H = d.H, E = d.E;
+  rg.zst = sbias + ((4 * H + 3) & ~3);            // [128][NT + 1] accumulator tile
+  int *s_ps = reinterpret_cast<int *>(rg.zst + 128 * 81);  // per tile row: parent slot
+  int *s_tr = s_ps + 128;                          //               tree (roots)
+  float *s_cc = reinterpret_cast<float *>(s_tr + 128);  // [128][32] children c (c_l | c_r)
+  const int warp = threadIdx.x >> 5;
   if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
   if (threadIdx.x == 128) {
-    for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
     mbar_init(rg.tfull, T_NMW);
     fence_barrier_init();
   }
@@ -378,21 +482,45 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
       t.x_leaf[(size_t)pos * d.Ep + k] = __float2bfloat16_rn(v);
     }
     for (int i = gt; i < nint; i += gs) t.stage_h[(size_t)i * d.P2 + 2 * H] = __float2bfloat16_rn(1.f);
+    // the bias (4H floats) lives in shared memory for every epilogue of the launch
+    for (int i = threadIdx.x; i < 4 * H; i += blockDim.x) sbias[i] = t.b[i];
   }
   fence_proxy_async_global();
-  grid_sync(t.barrier, ++ep * gridDim.x);
-  const float *b = t.b;
+  grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
+  const float *b = sbias;
   // ---- level 0: leaves. z = x W_leaf^T; i, o = sigmoid, u = tanh; c = i u; h = o tanh(c)
-  tile_loop<48>(rg, &mp.x_leaf, &mp.w_leaf, 0, n0, 3 * H, E, [&](int pos, int col0, float *z) {
-    const int n = s.order[pos];
-    const int ps = s.pslot[n];
+  const bool vec = (H % 4) == 0;
+  tile_loop<48, true, NS>(rg, &mp.x_leaf, &mp.w_leaf, 0, n0, 3 * H, E, [&](int pos, int) {
+    if (pos >= 0) {  // row metadata into shared memory while the MMAs run
+      const int n = s.order[pos], ps = s.pslot[n];
+      s_ps[threadIdx.x] = ps;
+      s_tr[threadIdx.x] = ps < 0 ? s.tree_of[n] : 0;
+    }
+    return 0;
+  }, [&](int pbase, int nrows, int col0) {
+    const int u0 = col0 / 3, nu = min(16, H - u0);
+    for (int i0 = threadIdx.x; i0 < nrows * 16; i0 += 512) {  // item = (row, unit), 4 in flight
+      float zv[4][3], bv[4][3];
+      bool ok[4];
 #pragma unroll
-    for (int uu = 0; uu < 16; ++uu) {
-      const int u = col0 / 3 + uu;
-      if (u >= H) break;
-      const float ig = sig_t(z[3 * uu] + b[u]);
-      const float og = sig_t(z[3 * uu + 1] + b[2 * H + u]);
-      const float ug = tanh_t(z[3 * uu + 2] + b[3 * H + u]);
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + 128 * j;
+        ok[j] = i < nrows * 16 && (i & 15) < nu;
+        if (ok[j]) {
+          const float *zz = rg.zst + (i >> 4) * 49 + 3 * (i & 15);
+          const int u = u0 + (i & 15);
+#pragma unroll
+          for (int g = 0; g < 3; ++g) { zv[j][g] = zz[g]; bv[j][g] = b[(g == 0 ? 0 : g + 1) * H + u]; }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+      if (!ok[j]) continue;
+      const int i = i0 + 128 * j, r = i >> 4, uu = i & 15;
+      const int u = u0 + uu, pos = pbase + r, ps = s_ps[r];
+      const float ig = sig_t(zv[j][0] + bv[j][0]);
+      const float og = sig_t(zv[j][1] + bv[j][1]);
+      const float ug = tanh_t(zv[j][2] + bv[j][2]);
       const float c = ig * ug, h = og * tanh_t(c);
       float *gl = t.gates_leaf + (size_t)pos * 3 * H + 3 * u;
       gl[0] = ig; gl[1] = og; gl[2] = ug;
@@ -402,45 +530,83 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
         t.stage_h[(size_t)pi * d.P2 + side * H + u] = __float2bfloat16_rn(h);
         t.stage_c[(size_t)pi * 2 * H + side * H + u] = c;
       } else {
-        t.root_h[(size_t)s.tree_of[n] * H + u] = h;
+        t.root_h[(size_t)s_tr[r] * H + u] = h;
+      }
       }
     }
   }, (E + 63) / 64 >= 8 ? 2 : 1);
   fence_proxy_async_global();
-  grid_sync(t.barrier, ++ep * gridDim.x);
+  grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
   // ---- internal levels: z = [h_l; h_r] U^T; c = i u + f_l c_l + f_r c_r; h = o tanh(c)
   for (int l = 1; l < L; ++l) {
     const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
-    tile_loop<80>(rg, &mp.stage_h, &mp.u, r0, cnt, 5 * H, 2 * H, [&](int row, int col0, float *z) {
-      const int ir = r0 + row;
-      const int n = s.order[p0 + row];
-      const int ps = s.pslot[n];
-      const float *sc = t.stage_c + (size_t)ir * 2 * H;
+    tile_loop<80, true, NS>(rg, &mp.stage_h, &mp.u, r0, cnt, 5 * H, 2 * H, [&](int row, int col0) {
+      const int u0 = col0 / 5, nu = min(16, H - u0);
+      if (row >= 0 && nu > 0) {  // row metadata + children c into shared memory during the MMAs
+        const int n = s.order[p0 + row], ps = s.pslot[n];
+        s_ps[threadIdx.x] = ps;
+        s_tr[threadIdx.x] = ps < 0 ? s.tree_of[n] : 0;
+        const float *sc = t.stage_c + (size_t)(r0 + row) * 2 * H;
+        float cl[16], cr[16];
+        ld_run(sc + u0, vec, nu, cl);
+        ld_run(sc + H + u0, vec, nu, cr);
+        float *dst = s_cc + threadIdx.x * 32;
 #pragma unroll
-      for (int uu = 0; uu < 16; ++uu) {
-        const int u = col0 / 5 + uu;
-        if (u >= H) break;
-        const float ig = sig_t(z[5 * uu] + b[u]);
-        const float fl = sig_t(z[5 * uu + 1] + b[H + u]);
-        const float fr = sig_t(z[5 * uu + 2] + b[H + u]);
-        const float og = sig_t(z[5 * uu + 3] + b[2 * H + u]);
-        const float ug = tanh_t(z[5 * uu + 4] + b[3 * H + u]);
-        const float c = ig * ug + fl * sc[u] + fr * sc[H + u];
-        const float h = og * tanh_t(c);
-        float *gi = t.gates_int + (size_t)ir * 5 * H + 5 * u;
-        gi[0] = ig; gi[1] = fl; gi[2] = fr; gi[3] = og; gi[4] = ug;
-        t.c_int[(size_t)ir * H + u] = c;
-        if (ps >= 0) {
-          const int pi = ps >> 1, side = ps & 1;
-          t.stage_h[(size_t)pi * d.P2 + side * H + u] = __float2bfloat16_rn(h);
-          t.stage_c[(size_t)pi * 2 * H + side * H + u] = c;
-        } else {
-          t.root_h[(size_t)s.tree_of[n] * H + u] = h;
+        for (int k = 0; k < 16; ++k) { dst[k] = cl[k]; dst[16 + k] = cr[k]; }
+      }
+      return 0;
+    }, [&](int rbase, int nrows, int col0) {
+      const int u0 = col0 / 5, nu = min(16, H - u0);
+      // item = (row, unit), 16 per row; four items per thread in flight (all shared-memory reads
+      // first, then the math and the stores): one warp per SM sub-partition has no other latency
+      // hiding
+      for (int i0 = threadIdx.x; i0 < nrows * 16; i0 += 512) {
+        float zv[4][5], bv[4][4], cl[4], cr[4];
+        int rr[4], uu[4];
+        bool ok[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + 128 * j;
+          rr[j] = i >> 4; uu[j] = i & 15;
+          ok[j] = i < nrows * 16 && uu[j] < nu;
+          if (ok[j]) {
+            const float *zz = rg.zst + rr[j] * 81 + 5 * uu[j];
+            const int u = u0 + uu[j];
+#pragma unroll
+            for (int g = 0; g < 5; ++g) zv[j][g] = zz[g];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) bv[j][g] = b[g * H + u];
+            cl[j] = s_cc[rr[j] * 32 + uu[j]];
+            cr[j] = s_cc[rr[j] * 32 + 16 + uu[j]];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!ok[j]) continue;
+          const int r = rr[j], u = u0 + uu[j], ir = r0 + rbase + r, ps = s_ps[r];
+          const float ig = sig_t(zv[j][0] + bv[j][0]);
+          const float fl = sig_t(zv[j][1] + bv[j][1]);
+          const float fr = sig_t(zv[j][2] + bv[j][1]);
+          const float og = sig_t(zv[j][3] + bv[j][2]);
+          const float ug = tanh_t(zv[j][4] + bv[j][3]);
+          const float c = ig * ug + fl * cl[j] + fr * cr[j];
+          const float h = og * tanh_t(c);
+          float *gi = t.gates_int + (size_t)ir * 5 * H + 5 * u;
+          gi[0] = ig; gi[1] = fl; gi[2] = fr; gi[3] = og; gi[4] = ug;
+          t.c_int[(size_t)ir * H + u] = c;
+          if (ps >= 0) {
+            const int pi = ps >> 1, side = ps & 1;
+            t.stage_h[(size_t)pi * d.P2 + side * H + u] = __float2bfloat16_rn(h);
+            t.stage_c[(size_t)pi * 2 * H + side * H + u] = c;
+          } else {
+            t.root_h[(size_t)s_tr[r] * H + u] = h;
+          }
         }
       }
-    }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1));
+    }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1),
+       t.dbg ? t.dbg + 2 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr);
     fence_proxy_async_global();
-    grid_sync(t.barrier, ++ep * gridDim.x);
+    grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
   }
   tc_fence_before();
   __syncthreads();
@@ -448,7 +614,11 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   (void)st;
 }
 
-static int tree_smem() { return 1024 + T_STAGES * (T_ASTAGE + T_BSTAGE) + 256; }
+static int tree_smem(int ns = T_STAGES) { return 1024 + ns * (T_ASTAGE + T_BSTAGE) + 256; }
+// forward: + bias [4H] + accumulator tile [128][81] + row metadata [2][128] + children c [128][32]
+static int tree_smem_fwd(int ns, int H) {
+  return tree_smem(ns) + 4 * ((4 * H + 3) & ~3) + 4 * 128 * 81 + 8 * 128 + 4 * 128 * 32;
+}
 
 static cudaError_t coop(const void *fn, int grid, int smem, void **args, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
@@ -473,14 +643,16 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   ok = ok && make_tmap_bf16(&mp.stage_h, t.stage_h, 2ull * d.H, d.N, d.P2, 128);
   ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
   if (!ok) return cudaErrorInvalidValue;
-  const int smem = tree_smem();
-  cudaError_t e = set_smem_once((const void *)tree_fwd_kernel, smem);
+  const bool six = tree_smem_fwd(6, d.H) <= 227 * 1024;  // ring depth that fits beside the staging
+  const int smem = tree_smem_fwd(six ? 6 : 4, d.H);
+  const void *fn = six ? (const void *)tree_fwd_kernel<6> : (const void *)tree_fwd_kernel<4>;
+  cudaError_t e = set_smem_once(fn, smem);
   if (e != cudaSuccess) return e;
   TreeBufs tt = t;
   TreeDims dd = d;
   TreeSched ss = s;
   void *args[] = {&mp, &tt, &dd, &ss, (void *)&st};
-  return coop((const void *)tree_fwd_kernel, grid, smem, args, str);
+  return coop(fn, grid, smem, args, str);
 }
 
 // =============================================================================== root classifier
@@ -615,20 +787,37 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
       t.dc_node[(size_t)rc * H + u] = dc * fr;
     }
     fence_proxy_async_global();
-    grid_sync(t.barrier, ++ep * gridDim.x);
+    grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
     // (b) [dh_l ; dh_r] = rb(dz) U, scattered to the two children (each child has one parent)
-    tile_loop<64>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, 5 * H, [&](int row, int col0, float *z) {
-      const int n = s.order[p0 + row];
-      const int lc = t.left[n], rc = t.right[n];
+    tile_loop<64>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, 5 * H, [&](int row, int) {
+      int2 c = make_int2(0, 0);
+      if (row >= 0) {
+        const int n = s.order[p0 + row];
+        c = make_int2(t.left[n], t.right[n]);
+      }
+      return c;
+    }, [&](int row, int col0, float *z, int2 ch) {
+      const int lc = ch.x, rc = ch.y;
+      const bool vec = (H % 4) == 0;  // then a 4-column group never straddles the two children
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
+      for (int j = 0; j < 64; j += 4) {
         const int k = col0 + j;
         if (k >= 2 * H) break;
-        if (k < H) t.dh_node[(size_t)lc * H + k] = z[j];
-        else t.dh_node[(size_t)rc * H + (k - H)] = z[j];
+        float *dst = k < H ? t.dh_node + (size_t)lc * H + k : t.dh_node + (size_t)rc * H + (k - H);
+        if (vec) {
+          *reinterpret_cast<float4 *>(dst) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int ki = k + i;
+            if (ki >= 2 * H) break;
+            if (ki < H) t.dh_node[(size_t)lc * H + ki] = z[j + i];
+            else t.dh_node[(size_t)rc * H + (ki - H)] = z[j + i];
+          }
+        }
       }
     }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1));
-    grid_sync(t.barrier, ++ep * gridDim.x);
+    grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
   }
   // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]
   for (long long e = gt; e < (long long)n0 * H; e += gs) {

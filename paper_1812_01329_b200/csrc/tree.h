@@ -49,6 +49,8 @@ struct TreeBufs {
   float *gWc, *gbc;            // classifier gradients [C][H], [C]
   float *rowloss;              // [B]
   unsigned int *barrier;       // grid barrier counters (zeroed by step init)
+  unsigned long long *dbg;     // dev hook (janus_dev_set_probe): per-barrier arrival / release
+                               // %globaltimer of every CTA, [2 kernels][256 syncs][256 CTAs][2]
 };
 
 cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
