@@ -65,6 +65,7 @@ struct TreePlan {
     size_t status = 0, barriers = 0, stage_args = 0;
     size_t height = 0, order = 0, irank = 0, pslot = 0, tree_of = 0, pcount = 0, lvl_off = 0, meta = 0;
     size_t x_leaf = 0, stage_h = 0, stage_c = 0, gates_int = 0, c_int = 0, gates_leaf = 0, c_leaf = 0;
+    size_t root_part = 0;
     size_t root_h = 0, dh_node = 0, dc_node = 0, DZ_int = 0, DZ_leaf = 0, rowloss = 0;
     size_t U_il = 0, UT_il = 0, Wl_il = 0;
     size_t arena_begin = 0, arena_end = 0, gU = 0, gWl = 0, gWc = 0, gbc = 0, dp_scratch = 0;

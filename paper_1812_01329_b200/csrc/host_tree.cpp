@@ -147,6 +147,7 @@ bool lower_tree(Graph &g, std::string &why) {
   p.off.gates_leaf = take((size_t)N * 3 * H * 4);
   p.off.c_leaf = take((size_t)N * H * 4);
   p.off.root_h = take((size_t)p.B * H * 4);
+  p.off.root_part = take((size_t)((p.B + 7) / 8) * (p.C * H + p.C) * 4);  // root classifier partials
   p.off.dh_node = take((size_t)N * H * 4);
   p.off.dc_node = take((size_t)N * H * 4);
   p.off.DZ_int = take((size_t)(N + 64) * p.P5 * 2);
@@ -248,6 +249,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   t.dc_node = fp(p.off.dc_node); t.DZ_int = bf(p.off.DZ_int); t.DZ_leaf = bf(p.off.DZ_leaf);
   t.gWc = fp(p.off.gWc); t.gbc = fp(p.off.gbc); t.rowloss = fp(p.off.rowloss); t.barrier = bars;
   t.dbg = g.probe;
+  t.root_part = fp(p.off.root_part);
 
   // guards (AssertOps): forest structure + any other runtime assumption
   GuardList gl{};

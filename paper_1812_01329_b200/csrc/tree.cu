@@ -121,6 +121,8 @@ JN_DEV void grid_sync(unsigned int *ctr, unsigned int target, unsigned long long
 // =============================================================================== guard
 // TREE_BINARY (janus.h): elements 0..N-1 are nodes, N..N+B the tree_off entries; the minimum
 // failing element is reported (observed = off[t] for offsets, kind[n] for nodes).
+constexpr int TREE_GUARD_SMEM_INTS = 48 * 1024;  // offsets + parent counts in shared memory up to 192 KB
+
 __global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d, TreeSched s,
                                                           unsigned id, long long V, long long maxn,
                                                           DevStatus *st) {
@@ -145,32 +147,41 @@ __global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d
       atomicMin(&st->key, ((unsigned long long)id << IDX_BITS) | (unsigned long long)(N + s_badoff));
     return;
   }
-  for (int n = threadIdx.x; n < N; n += blockDim.x) s.pcount[n] = 0;
+  // tree offsets and parent counts in shared memory when they fit (binary searches and atomics
+  // on chip); otherwise in global memory
+  extern __shared__ int s_off[];
+  const bool sm = B + 1 + N <= TREE_GUARD_SMEM_INTS;
+  const int *offp = sm ? s_off : t.off;
+  int *pc = sm ? s_off + B + 1 : s.pcount;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) pc[n] = 0;
+  if (sm)
+    for (int i = threadIdx.x; i <= B; i += blockDim.x) s_off[i] = t.off[i];
   __syncthreads();
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
     int lo_t = 0, hi_t = B - 1;  // tree containing n: largest t with off[t] <= n
     while (lo_t < hi_t) {
       const int mid = (lo_t + hi_t + 1) >> 1;
-      if (t.off[mid] <= n) lo_t = mid; else hi_t = mid - 1;
+      if (offp[mid] <= n) lo_t = mid; else hi_t = mid - 1;
     }
     s.tree_of[n] = lo_t;
-    const int lo = t.off[lo_t];
-    const int k = t.kind[n];
+    const int lo = offp[lo_t];
+    // the forest arrays are read-only here: non-coherent loads may run ahead of the stores
+    const int k = __ldg(t.kind + n);
+    const int wd = __ldg(t.word + n), l = __ldg(t.left + n), r = __ldg(t.right + n);
     bool bad = false;
-    if (k == 0) bad = !(t.word[n] >= 0 && t.word[n] < V);
+    if (k == 0) bad = !(wd >= 0 && wd < V);
     else if (k == 1) {
-      const int l = t.left[n], r = t.right[n];
       if (l >= lo && l < n && r >= lo && r < n && l != r) {
-        atomicAdd(&s.pcount[l], 1);
-        atomicAdd(&s.pcount[r], 1);
+        atomicAdd(&pc[l], 1);
+        atomicAdd(&pc[r], 1);
       } else bad = true;
     } else bad = true;
     if (bad) atomicMin(&s_badnode, n);
   }
   __syncthreads();
   for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    const bool root = n == t.off[s.tree_of[n] + 1] - 1;
-    if (root ? s.pcount[n] != 0 : s.pcount[n] != 1) atomicMin(&s_badnode, n);
+    const bool root = n == offp[s.tree_of[n] + 1] - 1;
+    if (root ? pc[n] != 0 : pc[n] != 1) atomicMin(&s_badnode, n);
   }
   __syncthreads();
   if (threadIdx.x == 0 && s_badnode != 0x7fffffff)
@@ -180,7 +191,10 @@ __global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d
 
 cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
                               long long V, long long max_nodes, DevStatus *st, cudaStream_t str) {
-  tree_guard_kernel<<<1, 1024, 0, str>>>(t, d, s, id, V, max_nodes, st);
+  const int smem = d.B + 1 + d.N <= TREE_GUARD_SMEM_INTS ? (d.B + 1 + d.N) * 4 : 0;
+  cudaError_t e = set_smem_once((const void *)tree_guard_kernel, TREE_GUARD_SMEM_INTS * 4);
+  if (e != cudaSuccess) return e;
+  tree_guard_kernel<<<1, 1024, smem, str>>>(t, d, s, id, V, max_nodes, st);
   return cudaGetLastError();
 }
 
@@ -233,21 +247,16 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
         h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
       }
       hh[n] = h;
-    }
-  }
-  __syncthreads();
-  for (int tr = 0; tr < B; ++tr) {  // tree_of, pslot, heights to global (parallel over nodes)
-    const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
-    for (int n = lo + tid; n < hi; n += blockDim.x) {
+      // tree_of, pslot, heights to global by the walking thread (stores only: no round trips)
       s.tree_of[n] = tr;
       s.pslot[n] = -1;
-      if (hh != s.height) s.height[n] = hh[n];
+      if (hh != s.height) s.height[n] = h;
     }
   }
   __syncthreads();
   for (int n = tid; n < N; n += blockDim.x) {
-    atomicAdd(&hist[s.height[n]], 1);
-    atomicMax(&s_L, s.height[n] + 1);
+    atomicAdd(&hist[hh[n]], 1);
+    atomicMax(&s_L, hh[n] + 1);
   }
   __syncthreads();
   const int L = s_L;
@@ -269,7 +278,7 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
     __syncthreads();
     const int n = c0 + tid;
     const bool live = n < N;
-    const int h = live ? s.height[n] : TREE_MAX_LEVELS - 1;
+    const int h = live ? hh[n] : TREE_MAX_LEVELS - 1;
     const unsigned same = __match_any_sync(0xffffffff, live ? h : -1 - lane);
     const int rank_w = __popc(same & ((1u << lane) - 1));
     if (live && rank_w == 0) wcnt[warp][h] = (unsigned short)__popc(same);
@@ -295,7 +304,7 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
   }
   // parent slots
   for (int n = tid; n < N; n += blockDim.x) {
-    if (t.kind[n] == 1 && s.height[n] > 0) {
+    if (t.kind[n] == 1 && hh[n] > 0) {
       const int l = t.left[n], r = t.right[n];
       if (l >= 0 && l < N) s.pslot[l] = (s.irank[n] << 1) | 0;
       if (r >= 0 && r < N) s.pslot[r] = (s.irank[n] << 1) | 1;
@@ -330,9 +339,13 @@ struct Ring {
 // functor receives (first row of the tile, valid rows, tile column base) on all 128 threads, so
 // a level with few nodes spreads its (row, unit) work over the whole epilogue instead of one
 // thread per row; otherwise it receives (row, tile column base, z[NT], pre's context) per row.
+// tmA32 (optional): the A map with a 32-row box, used for tiles with <= 32 valid rows (the
+// upper levels of a forest): the MMA still reads 128 smem rows, but rows past the box only feed
+// accumulator rows the epilogue discards, and the level's A traffic drops 4x.
 template <int NT, bool STAGED = false, int NS = T_STAGES, typename Pre, typename Epi>
 JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, int row0, int M,
-                      int NTOT, int K, Pre pre, Epi epi, int nmw, unsigned long long *pr = nullptr) {
+                      int NTOT, int K, Pre pre, Epi epi, int nmw, unsigned long long *pr = nullptr,
+                      const CUtensorMap *tmA32 = nullptr) {
   while (NS % nmw) nmw >>= 1;  // a fixed MMA warp per ring stage
   // nmw in {1, 2, 4} MMA warps take part (T_STAGES % nmw == 0 keeps a fixed owner per stage):
   // more warps for long reductions, fewer TMEM tiles for the epilogue to sum on short ones
@@ -344,12 +357,14 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int m = tile / ntile_n, nn = tile % ntile_n;
     if (warp == 4) {
+      const bool small = tmA32 && M - m * 128 <= 32;
+      const CUtensorMap *ta = small ? tmA32 : tmA;
       if ((threadIdx.x & 31) == 0)
         for (int kc = 0; kc < nk; ++kc) {
           const int q = rg.q + kc, s = q % NS, r = q / NS;
           if (r > 0) mbar_wait(&rg.empty[s], (r - 1) & 1);
-          mbar_expect_tx(&rg.full[s], T_ASTAGE + NT * 128);
-          tma_load_2d(rg.sA + s * T_ASTAGE, tmA, &rg.full[s], kc * 64, row0 + m * 128);
+          mbar_expect_tx(&rg.full[s], (small ? 32 * 128 : T_ASTAGE) + NT * 128);
+          tma_load_2d(rg.sA + s * T_ASTAGE, ta, &rg.full[s], kc * 64, row0 + m * 128);
           tma_load_2d(rg.sB + s * T_BSTAGE, tmB, &rg.full[s], kc * 64, nn * NT);
         }
       __syncwarp();
@@ -432,7 +447,7 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
 
 // =============================================================================== forward
 struct TreeFwdMaps {
-  CUtensorMap x_leaf, w_leaf, stage_h, u;
+  CUtensorMap x_leaf, w_leaf, stage_h, u, stage_h32;
 };
 
 template <int NS>
@@ -604,7 +619,7 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
         }
       }
     }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1),
-       t.dbg ? t.dbg + 2 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr);
+       t.dbg ? t.dbg + 2 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.stage_h32);
     fence_proxy_async_global();
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
   }
@@ -642,6 +657,7 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   ok = ok && make_tmap_bf16(&mp.w_leaf, Wl_il, d.E, 3ull * d.H, d.Ep, 48);
   ok = ok && make_tmap_bf16(&mp.stage_h, t.stage_h, 2ull * d.H, d.N, d.P2, 128);
   ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
+  ok = ok && make_tmap_bf16(&mp.stage_h32, t.stage_h, 2ull * d.H, d.N, d.P2, 32);
   if (!ok) return cudaErrorInvalidValue;
   const bool six = tree_smem_fwd(6, d.H) <= 227 * 1024;  // ring depth that fits beside the staging
   const int smem = tree_smem_fwd(six ? 6 : 4, d.H);
@@ -658,64 +674,87 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
 // =============================================================================== root classifier
 // y = rb(h_root) rb(W_c)^T + b_c; loss = mean over trees of xent(y, label) (reading Q6);
 // dy = (softmax - onehot) / B; dW_c = sum rb(dy)^T rb(h); db_c = sum rb(dy); dh_root = rb(dy) rb(W_c).
-__global__ void tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus *st) {
+// Multi-block: block j owns trees [8j, 8j + 8) — their logits, softmax, loss rows and root dh —
+// and writes its share of dW_c / db_c to root_part[j]; the last block to finish (counter in
+// barrier word 32, zeroed by the step init) sums the shares in block order (deterministic).
+constexpr int ROOT_TPB = 8;  // trees per block
+
+__global__ void __launch_bounds__(256) tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus *st) {
   const int B = d.B, H = d.H, C = d.C;
-  extern __shared__ float sh[];
-  float *dyr = sh;  // [B][C] rounded dy
+  __shared__ float dyr[ROOT_TPB * 8];  // [tree][class] rounded dy (C <= 8)
+  __shared__ float ysh[ROOT_TPB * 8];  // logits
+  __shared__ int sroot[ROOT_TPB];
+  __shared__ bool s_last;
+  const int b0 = blockIdx.x * ROOT_TPB, nt = min(ROOT_TPB, B - b0);
   if (st->key != KEY_PASS) {
-    for (int tr = threadIdx.x; tr < B; tr += blockDim.x) t.rowloss[tr] = 0.f;
+    for (int tr = threadIdx.x; tr < nt; tr += blockDim.x) t.rowloss[b0 + tr] = 0.f;
     return;
   }
   // logits: one warp per (tree, class) pair, lanes over the hidden units, warp reduction
-  float *ysh = dyr + B * C;  // [B][C] logits
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int p = wid; p < B * C; p += nw) {
+  for (int p = wid; p < nt * C; p += nw) {
     const int tr = p / C, c = p - tr * C;
     float acc = 0.f;
     for (int k = lane; k < H; k += 32)
-      acc += bf16_round(t.root_h[(size_t)tr * H + k]) * bf16_round(t.Wc[(size_t)c * H + k]);
+      acc += bf16_round(__ldg(t.root_h + (size_t)(b0 + tr) * H + k)) * bf16_round(__ldg(t.Wc + (size_t)c * H + k));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) ysh[p] = acc + t.bc[c];
   }
   __syncthreads();
-  for (int tr = threadIdx.x; tr < B; tr += blockDim.x) {
+  for (int tr = threadIdx.x; tr < nt; tr += blockDim.x) {
     const float *y = ysh + tr * C;
     float m = -INFINITY;
     for (int c = 0; c < C; ++c) m = fmaxf(m, y[c]);
     float sum = 0.f;
     for (int c = 0; c < C; ++c) sum += expf(y[c] - m);
     const float lse = m + logf(sum);
-    int lab = t.label[tr];
+    int lab = t.label[b0 + tr];
     if (lab < 0 || lab >= C) {
       atomicOr(reinterpret_cast<unsigned int *>(&st->runtime_err), 2u);
       lab = 0;
     }
-    t.rowloss[tr] = (lse - y[lab]) / B;
+    t.rowloss[b0 + tr] = (lse - y[lab]) / B;
     for (int c = 0; c < C; ++c)
       dyr[tr * C + c] = bf16_round((expf(y[c] - lse) - (c == lab ? 1.f : 0.f)) / B);
+    sroot[tr] = t.off[b0 + tr + 1] - 1;
   }
   __syncthreads();
+  // this block's share of dW_c = sum_trees rb(dy)^T rb(h_root), db_c = sum_trees rb(dy)
+  float *part = t.root_part + (size_t)blockIdx.x * (C * H + C);
   for (int e = threadIdx.x; e < C * H; e += blockDim.x) {
-    const int c = e / H, k = e % H;
+    const int c = e / H, k = e - c * H;
     float acc = 0.f;
-    for (int tr = 0; tr < B; ++tr) acc += dyr[tr * C + c] * bf16_round(t.root_h[(size_t)tr * H + k]);
-    t.gWc[e] = acc;
+    for (int tr = 0; tr < nt; ++tr) acc += dyr[tr * C + c] * bf16_round(__ldg(t.root_h + (size_t)(b0 + tr) * H + k));
+    part[e] = acc;
   }
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     float acc = 0.f;
-    for (int tr = 0; tr < B; ++tr) acc += dyr[tr * C + c];
-    t.gbc[c] = acc;
+    for (int tr = 0; tr < nt; ++tr) acc += dyr[tr * C + c];
+    part[C * H + c] = acc;
   }
   // dh of each root node (dc of a root = 0)
-  for (int e = threadIdx.x; e < B * H; e += blockDim.x) {
-    const int tr = e / H, k = e % H;
-    int root = t.off[tr + 1] - 1;
+  for (int e = threadIdx.x; e < nt * H; e += blockDim.x) {
+    const int tr = e / H, k = e - tr * H;
+    const int root = sroot[tr];
     if (root < 0 || root >= d.N) continue;
     float acc = 0.f;
-    for (int c = 0; c < C; ++c) acc += dyr[tr * C + c] * bf16_round(t.Wc[(size_t)c * H + k]);
+    for (int c = 0; c < C; ++c) acc += dyr[tr * C + c] * bf16_round(__ldg(t.Wc + (size_t)c * H + k));
     t.dh_node[(size_t)root * H + k] = acc;
     t.dc_node[(size_t)root * H + k] = 0.f;
+  }
+  // the last block sums the shares in block order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(t.barrier + 32, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < C * H + C; e += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < (int)gridDim.x; ++j) acc += __ldcg(t.root_part + (size_t)j * (C * H + C) + e);
+    if (e < C * H) t.gWc[e] = acc;
+    else t.gbc[e - C * H] = acc;
   }
   (void)s;
 }
@@ -723,13 +762,13 @@ __global__ void tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus 
 cudaError_t launch_tree_root(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                              DevStatus *st, cudaStream_t str) {
   if (d.C > 8) return cudaErrorInvalidValue;
-  tree_root_kernel<<<1, 1024, 2 * d.B * d.C * 4, str>>>(t, d, s, st);
+  tree_root_kernel<<<(d.B + ROOT_TPB - 1) / ROOT_TPB, 256, 0, str>>>(t, d, s, st);
   return cudaGetLastError();
 }
 
 // =============================================================================== backward
 struct TreeBwdMaps {
-  CUtensorMap dz, ut;
+  CUtensorMap dz, ut, dz32;
 };
 
 __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__ TreeBwdMaps mp,
@@ -816,7 +855,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
           }
         }
       }
-    }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1));
+    }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1), nullptr, &mp.dz32);
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
   }
   // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]
@@ -850,6 +889,7 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   TreeBwdMaps mp;
   bool ok = make_tmap_bf16(&mp.dz, t.DZ_int, 5ull * d.H, d.N, d.P5, 128);
   ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
+  ok = ok && make_tmap_bf16(&mp.dz32, t.DZ_int, 5ull * d.H, d.N, d.P5, 32);
   if (!ok) return cudaErrorInvalidValue;
   const int smem = tree_smem();
   cudaError_t e = set_smem_once((const void *)tree_bwd_kernel, smem);
@@ -863,16 +903,18 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
 
 // =============================================================================== casts
 __global__ void cast_il_kernel(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld) {
-  const long long n = (long long)ng * H * ld;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const int ri = (int)(e / ld), k = (int)(e % ld);
+  // one block-stride loop per destination row (32-bit index math: a weight has < 2^31 elements)
+  const int R = ng * H;
+  for (int ri = blockIdx.x; ri < R; ri += gridDim.x) {
     const int rc = (ri % ng) * H + ri / ng;
-    dst[e] = __float2bfloat16_rn(k < cols ? src[(size_t)rc * cols + k] : 0.f);
+    const float *sr = src + (size_t)rc * cols;
+    __nv_bfloat16 *dr = dst + (size_t)ri * ld;
+    for (int k = threadIdx.x; k < ld; k += blockDim.x) dr[k] = __float2bfloat16_rn(k < cols ? sr[k] : 0.f);
   }
 }
 cudaError_t launch_cast_il(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld,
                            cudaStream_t s) {
-  cast_il_kernel<<<4 * 148, 256, 0, s>>>(src, H, ng, cols, dst, ld);
+  cast_il_kernel<<<min(ng * H, 16 * 148), 256, 0, s>>>(src, H, ng, cols, dst, ld);
   return cudaGetLastError();
 }
 // dst[k][ri] = rb(src[rc][k]),  ri = ng*u + g <-> rc = g*H + u

@@ -48,6 +48,7 @@ struct TreeBufs {
   __nv_bfloat16 *DZ_leaf;      // [n_leaf][P3] rb(dz), interleaved 3u+g
   float *gWc, *gbc;            // classifier gradients [C][H], [C]
   float *rowloss;              // [B]
+  float *root_part;            // [ceil(B/8)][C*H + C] per-block classifier-gradient partials
   unsigned int *barrier;       // grid barrier counters (zeroed by step init)
   unsigned long long *dbg;     // dev hook (janus_dev_set_probe): per-barrier arrival / release
                                // %globaltimer of every CTA, [2 kernels][256 syncs][256 CTAs][2]
