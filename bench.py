@@ -316,7 +316,32 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
             out[f"treelstm_b{Bt}"] = {"sentences_per_s": Bt * 1000.0 / ms_t, "ms_per_step": ms_t,
                                       "phases_ms_per_step": {n: round(v[0] / K, 4) for n, v in ph.items()},
                                       "workload": f"C3 SST-shaped forests, B={Bt}, H=E=300, V=20000, <=64 leaves"}
+            if Bt == 25:   # ablation (Figure 7): the imperative executor on the same forests
+                st_i = [x.clone() for x in stt]
+                gt.run_imperative(forests[0], st_i, wst, stream=stream)
+                ms_ti = timed(lambda k: gt.run_imperative(forests[k % 4], st_i, wst, stream=stream), 2) / 2
+                c3_abl = {"IMP": Bt * 1000.0 / ms_ti, "graph_level_batched": Bt * 1000.0 / ms_t}
             del wst
+        # --- Figure 7 ablation on B200: samples/s of the same C2 batches through the
+        # imperative executor (IMP), the graph with the loop kept as a device While (BASE: no
+        # unrolling; +SPCN shapes and types still specialised) and the unrolled graph (+UNRL)
+        pw = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=T, lr=1.0, speculate="while", max_T=T)
+        gw = J.Graph(pw)
+        ws_w = gw.new_workspace()
+        st_w = [s.clone() for s in state]
+        loss = torch.zeros(1, device="cuda")
+        for k in range(3):
+            gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream)
+        ms_w = timed(lambda k: gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream), K) / K
+        del ws_w
+        out["ablation_fig7"] = {
+            "c2_samples_per_s": {"IMP": out["imperative"]["samples_per_s"], "BASE_while": B * 1000.0 / ms_w,
+                                 "UNRL": B * 1000.0 / ms_step},
+            "c3_b25_sentences_per_s": c3_abl,
+            "note": "IMP = janus_run_imperative (one launch per op, host-side control flow); BASE_while = "
+                    "speculative graph with the loop as a device While (RANGE assumption); UNRL = unrolled "
+                    "graph (TRIP_COUNT). +SPCN and +PARL have no separate toggle: every device graph is "
+                    "shape-specialised and level/wavefront-parallel"}
     return out
 
 
