@@ -276,7 +276,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   TCHK("cast", launch_cast_il(Wl, H, 3, E, bf(p.off.Wl_il), p.Ep, st));
   TCHK("cast", launch_cast_il(U, H, 5, 2 * H, bf(p.off.U_il), p.P2, st));
   TCHK("cast", launch_cast_il_T(U, H, 5, 2 * H, bf(p.off.UT_il), p.P5, st));
-  const int grid = std::min(148, std::max(32, 3 * B));
+  const int grid = 148;  // one CTA per SM: the leaf level of a B=25 forest already has ~76 tiles
   TCHK("tree_fwd", launch_tree_fwd(t, d, s, bf(p.off.Wl_il), bf(p.off.U_il), grid, dst, st));
   TCHK("root_xent", launch_tree_root(t, d, s, dst, st));
   TreeBufs tb = t;

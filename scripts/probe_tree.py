@@ -34,7 +34,7 @@ print(f"B={B} levels={L} nodes/level={[int(lvl[l + 1] - lvl[l]) for l in range(L
 pp = buf.cpu().numpy()
 p = pp[:3 * 256 * 256 * 2].reshape(3, 256, 256, 2)
 q4 = pp[2 * 256 * 256 * 2:].reshape(256, 256, 4)
-grid = min(148, max(32, 3 * B))
+grid = 148  # host_tree.cpp: one CTA per SM
 for kern, name in ((0, "fwd"), (1, "bwd")):
     a, r = p[kern, :, :grid, 0], p[kern, :, :grid, 1]
     ks = [k for k in range(256) if (a[k] > 0).all()]
