@@ -175,3 +175,21 @@ def test_int64_specialised_graphs_match_the_oracle():
     assert st == I.OK == ora.status
     assert rel_err(float(loss.item()), ora.outputs[0]) <= 2e-2
     assert_state_parity(tp, state, to_host(dev), ora.state, 2e-2, what="tree i64")
+
+
+def test_session_cache_max_evicts_least_recently_dispatched():
+    """cache_max=1: the graph generated for int64 tokens evicts the int32 graph (least recently
+    dispatched); int32 batches then miss and are served imperatively, with identical results."""
+    B, T, V = 8, 6, 64
+    prog = pg.lstm_lm_program(V=V, E=40, H=48, L=2, B=B, T=T, lr=0.5)
+    sess = J().Session(prog, cache_max=1)
+    state = gen.uniform_params(prog, 19, 0.1)
+    seen = []
+    for k, (tok, tgt, ln) in enumerate(gen.lm_batches(gen.SEED_C2, B, T, V, 4)):
+        args = (tok.astype(np.int64), tgt, ln) if k < 3 else (tok, tgt, ln)
+        dev = to_dev(state)
+        info, state = _check(prog, sess, args, state, dev, what=f"step {k}")
+        seen.append((info["event"], info["path"]))
+    assert seen == [("MISS", "imperative"), ("MISS", "imperative"), ("HIT", "graph"), ("MISS", "imperative")]
+    ents = sess.stats()["entries"]
+    assert [e["active"] for e in ents] == [False, True]

@@ -71,6 +71,16 @@ def test_tree_ragged_units_and_chains():
     _check(prog, forests, scale=0.2)
 
 
+def test_tree_hidden_not_multiple_of_four_and_many_trees():
+    """H=30 (H % 4 != 0: the epilogues' scalar paths), odd E, B=40 trees (five root-classifier
+    blocks; the level schedule spans several 128-row tiles at the leaves)."""
+    V, B = 77, 40
+    prog = pg.treelstm_program(V=V, E=21, H=30, C=2, B=B, lr=0.2)
+    forests = [gen.sst_forest(gen.SEED_C3, 11, B, V, max_leaves=20),
+               gen.sst_forest(gen.SEED_C3, 12, B, V, max_leaves=20, chain=True)]
+    _check(prog, forests, scale=0.2)
+
+
 def test_tree_one_leaf_trees_and_all_shapes():
     """Degenerate cases: a lone root leaf, and every shape with <= 5 leaves in one forest."""
     V = 40
