@@ -333,6 +333,12 @@ struct Ring {
   int q;      // chunk counter (both producer and MMA advance it identically)
   int tiles;  // tiles processed by this CTA (tfull phase)
   float *zst; // STAGED tile loops: the accumulator tile [128][NT + 1] in shared memory
+  // resident B (optional): this CTA's NT-row slice of the B operand, all K chunks, loaded once
+  // per launch; the CTA then always takes tiles of column block bres_nn and only streams A
+  const uint8_t *sBres = nullptr;
+  uint64_t *bres_bar = nullptr;
+  int bres_nn = -1, bres_groups = 0;
+  bool bres_ready = false;  // (MMA thread) the resident slice has landed
 };
 
 // STAGED: the epilogue threads park the accumulator tile in shared memory and the epilogue
@@ -351,11 +357,17 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
   // more warps for long reductions, fewer TMEM tiles for the epilogue to sum on short ones
   const int warp = threadIdx.x >> 5;
   const int ntile_n = (NTOT + NT - 1) / NT;
-  const int tiles = ((M + 127) / 128) * ntile_n;
+  const int mtiles = (M + 127) / 128;
+  const int tiles = mtiles * ntile_n;
   const int nk = (K + 63) / 64;
+  const bool res = rg.sBres != nullptr;
   constexpr uint32_t idesc = umma_idesc_bf16(128, NT, 0, 0);
-  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int m = tile / ntile_n, nn = tile % ntile_n;
+  // tile sequence of this CTA: all tiles round robin, or (resident B) the M blocks of its column
+  const int t0 = res ? (rg.bres_nn < 0 ? tiles : blockIdx.x / ntile_n) : blockIdx.x;
+  const int tstep = res ? rg.bres_groups : gridDim.x;
+  const int tend = res ? mtiles : tiles;
+  for (int it = t0; it < tend; it += tstep) {
+    const int m = res ? it : it / ntile_n, nn = res ? rg.bres_nn : it % ntile_n;
     if (warp == 4) {
       const bool small = tmA32 && M - m * 128 <= 32;
       const CUtensorMap *ta = small ? tmA32 : tmA;
@@ -363,9 +375,9 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
         for (int kc = 0; kc < nk; ++kc) {
           const int q = rg.q + kc, s = q % NS, r = q / NS;
           if (r > 0) mbar_wait(&rg.empty[s], (r - 1) & 1);
-          mbar_expect_tx(&rg.full[s], (small ? 32 * 128 : T_ASTAGE) + NT * 128);
+          mbar_expect_tx(&rg.full[s], (small ? 32 * 128 : T_ASTAGE) + (res ? 0 : NT * 128));
           tma_load_2d(rg.sA + s * T_ASTAGE, ta, &rg.full[s], kc * 64, row0 + m * 128);
-          tma_load_2d(rg.sB + s * T_BSTAGE, tmB, &rg.full[s], kc * 64, nn * NT);
+          if (!res) tma_load_2d(rg.sB + s * T_BSTAGE, tmB, &rg.full[s], kc * 64, nn * NT);
         }
       __syncwarp();
     } else if (warp >= 5) {
@@ -373,13 +385,18 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
       // its own TMEM tile
       const int w = warp - 5;
       if ((threadIdx.x & 31) == 0) {
+        if (res && !rg.bres_ready) {
+          mbar_wait(rg.bres_bar, 0);
+          rg.bres_ready = true;
+        }
         const uint32_t acc = rg.tmem + (uint32_t)(w * NT);
         const int kc0 = w < nmw ? ((w - rg.q) % nmw + nmw) % nmw : nk;  // my first chunk of this tile
         for (int kc = kc0; kc < nk; kc += nmw) {
           const int q = rg.q + kc, s = q % NS, r = q / NS;
           mbar_wait(&rg.full[s], r & 1);
           tc_fence_after();
-          const uint32_t a = smem_u32(rg.sA + s * T_ASTAGE), b = smem_u32(rg.sB + s * T_BSTAGE);
+          const uint32_t a = smem_u32(rg.sA + s * T_ASTAGE);
+          const uint32_t b = res ? smem_u32(rg.sBres + kc * NT * 128) : smem_u32(rg.sB + s * T_BSTAGE);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             umma_bf16(acc, umma_desc_sw128(a + k * 32, 16, 1024),
@@ -768,9 +785,16 @@ cudaError_t launch_tree_root(const TreeBufs &t, const TreeDims &d, const TreeSch
 
 // =============================================================================== backward
 struct TreeBwdMaps {
-  CUtensorMap dz, ut, dz32;
+  CUtensorMap dz, ut, dz32, ut32;
 };
 
+// RES: the CTA keeps its 32-column slice of U^T (all K = 5H chunks, <= 96 KB) resident in shared
+// memory for the whole launch and only streams dz per level (the dgrad's B operand does not
+// change between levels); else both operands stream through the ring.
+constexpr int T_RES_CHUNKS = 24;  // resident K chunks (5H <= 1536)
+constexpr int T_RES_NT = 32;
+
+template <bool RES>
 __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__ TreeBwdMaps mp,
                                                          TreeBufs t, TreeDims d, TreeSched s,
                                                          const DevStatus *st) {
@@ -780,17 +804,34 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   Ring rg;
   rg.sA = base;
   rg.sB = base + T_STAGES * T_ASTAGE;
-  rg.full = reinterpret_cast<uint64_t *>(rg.sB + T_STAGES * T_BSTAGE);
+  uint8_t *after = RES ? rg.sB + T_RES_CHUNKS * T_RES_NT * 128 : rg.sB + T_STAGES * T_BSTAGE;
+  rg.full = reinterpret_cast<uint64_t *>(after);
   rg.empty = rg.full + T_STAGES;
   rg.tfull = rg.empty + T_STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rg.tfull + 1);
+  uint64_t *bres_bar = rg.tfull + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres_bar + 1);
   const int warp = threadIdx.x >> 5;
   const int H = d.H;
   if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
+  const int res_ntile = (2 * H + T_RES_NT - 1) / T_RES_NT;
+  const int res_groups = gridDim.x / res_ntile;
+  if (RES) {
+    rg.sBres = rg.sB;
+    rg.bres_bar = bres_bar;
+    rg.bres_groups = res_groups;
+    rg.bres_nn = (int)blockIdx.x < res_groups * res_ntile ? (int)blockIdx.x % res_ntile : -1;
+  }
   if (threadIdx.x == 128) {
     for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
     mbar_init(rg.tfull, T_NMW);
+    mbar_init(bres_bar, 1);
     fence_barrier_init();
+    if (RES && rg.bres_nn >= 0) {  // this CTA's slice of U^T, every K chunk, once
+      const int nk = (5 * H + 63) / 64;
+      mbar_expect_tx(bres_bar, nk * T_RES_NT * 128);
+      for (int c = 0; c < nk; ++c)
+        tma_load_2d(rg.sB + c * T_RES_NT * 128, &mp.ut32, bres_bar, c * 64, rg.bres_nn * T_RES_NT);
+    }
   }
   if (warp == 5) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -828,7 +869,8 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
     fence_proxy_async_global();
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
     // (b) [dh_l ; dh_r] = rb(dz) U, scattered to the two children (each child has one parent)
-    tile_loop<64>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, 5 * H, [&](int row, int) {
+    constexpr int BNT = RES ? T_RES_NT : 64;
+    tile_loop<BNT>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, 5 * H, [&](int row, int) {
       int2 c = make_int2(0, 0);
       if (row >= 0) {
         const int n = s.order[p0 + row];
@@ -839,7 +881,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
       const int lc = ch.x, rc = ch.y;
       const bool vec = (H % 4) == 0;  // then a 4-column group never straddles the two children
 #pragma unroll
-      for (int j = 0; j < 64; j += 4) {
+      for (int j = 0; j < BNT; j += 4) {
         const int k = col0 + j;
         if (k >= 2 * H) break;
         float *dst = k < H ? t.dh_node + (size_t)lc * H + k : t.dh_node + (size_t)rc * H + (k - H);
@@ -855,7 +897,8 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
           }
         }
       }
-    }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1), nullptr, &mp.dz32);
+    }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1),
+       t.dbg ? t.dbg + 3 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.dz32);
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
   }
   // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]
@@ -891,14 +934,18 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
   ok = ok && make_tmap_bf16(&mp.dz32, t.DZ_int, 5ull * d.H, d.N, d.P5, 32);
   if (!ok) return cudaErrorInvalidValue;
-  const int smem = tree_smem();
-  cudaError_t e = set_smem_once((const void *)tree_bwd_kernel, smem);
+  ok = ok && make_tmap_bf16(&mp.ut32, UT_il, 5ull * d.H, 2ull * d.H, d.P5, T_RES_NT);
+  if (!ok) return cudaErrorInvalidValue;
+  const bool res = (5 * d.H + 63) / 64 <= T_RES_CHUNKS && grid >= (2 * d.H + T_RES_NT - 1) / T_RES_NT;
+  const int smem = res ? 1024 + T_STAGES * T_ASTAGE + T_RES_CHUNKS * T_RES_NT * 128 + 256 : tree_smem();
+  const void *fn = res ? (const void *)tree_bwd_kernel<true> : (const void *)tree_bwd_kernel<false>;
+  cudaError_t e = set_smem_once(fn, smem);
   if (e != cudaSuccess) return e;
   TreeBufs tt = t;
   TreeDims dd = d;
   TreeSched ss = s;
   void *args[] = {&mp, &tt, &dd, &ss, (void *)&st};
-  return coop((const void *)tree_bwd_kernel, grid, smem, args, str);
+  return coop(fn, grid, smem, args, str);
 }
 
 // =============================================================================== casts

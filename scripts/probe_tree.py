@@ -22,7 +22,7 @@ st = [torch.tensor(x, device="cuda") for x in gen.uniform_params(tp, 1, 0.05)]
 f = [torch.tensor(a, device="cuda") for a in gen.sst_forest(gen.SEED_C3, 0, B, 20000)]
 for _ in range(3):
     g.run(f, st, ws)
-buf = torch.zeros(4 * 256 * 256 * 2, dtype=torch.int64, device="cuda")
+buf = torch.zeros(5 * 256 * 256 * 2, dtype=torch.int64, device="cuda")
 J.lib.janus_dev_set_probe(g.h, buf.data_ptr())
 g.run(f, st, ws)
 torch.cuda.synchronize()
@@ -33,7 +33,8 @@ L = int(meta[0])
 print(f"B={B} levels={L} nodes/level={[int(lvl[l + 1] - lvl[l]) for l in range(L)]}")
 pp = buf.cpu().numpy()
 p = pp[:3 * 256 * 256 * 2].reshape(3, 256, 256, 2)
-q4 = pp[2 * 256 * 256 * 2:].reshape(256, 256, 4)
+q4 = pp[2 * 256 * 256 * 2:4 * 256 * 256 * 2].reshape(256, 256, 4)
+q5 = pp[3 * 256 * 256 * 2:5 * 256 * 256 * 2].reshape(256, 256, 4)
 grid = 148  # host_tree.cpp: one CTA per SM
 for kern, name in ((0, "fwd"), (1, "bwd")):
     a, r = p[kern, :, :grid, 0], p[kern, :, :grid, 1]
@@ -66,5 +67,18 @@ for l in range(1, L):
     if not act.any():
         continue
     start = np.median(r[l + 1])
+    print(f"  level {l:2d} ({int(lvl[l + 1] - lvl[l]):4d} nodes, {int(act.sum())} CTAs): "
+          f"mainloop {(pr[act, 0].max() - start) / 1e3:5.2f} us  tmem {((pr[act, 2] - pr[act, 0]).max()) / 1e3:5.2f} us  epilogue {((pr[act, 1] - pr[act, 2]).max()) / 1e3:5.2f} us")
+
+# backward dgrad tile loops: level l runs after barrier 2 * (L - 1 - l) + 2 of the backward kernel
+print("-- backward dgrad levels")
+ab, rb = p[1, :, :grid, 0], p[1, :, :grid, 1]
+for l in range(L - 1, 0, -1):
+    pr = q5[l, :grid]
+    act = pr[:, 0] > 0
+    if not act.any():
+        continue
+    k = 2 * (L - 1 - l) + 1
+    start = np.median(rb[k])
     print(f"  level {l:2d} ({int(lvl[l + 1] - lvl[l]):4d} nodes, {int(act.sum())} CTAs): "
           f"mainloop {(pr[act, 0].max() - start) / 1e3:5.2f} us  tmem {((pr[act, 2] - pr[act, 0]).max()) / 1e3:5.2f} us  epilogue {((pr[act, 1] - pr[act, 2]).max()) / 1e3:5.2f} us")
