@@ -356,14 +356,15 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       tc_fence_after();
       {
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-        for (int w = 0; w < nacc; ++w) {
+        for (int w = 0; w < nacc; ++w) {  // an accumulator's loads in flight together, one wait
+          uint32_t v[NG / 32][32];
 #pragma unroll
-          for (int h = 0; h < NG / 32; ++h) {
-            float v[32];
-            tmem_ld32(ta + w * NG + 32 * h, v);
+          for (int h = 0; h < NG / 32; ++h) tmem_ld32_nw(ta + w * NG + 32 * h, v[h]);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) z[32 * h + i] += v[i];
-          }
+          for (int h = 0; h < NG / 32; ++h)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) z[32 * h + i] += __uint_as_float(v[h][i]);
         }
       }
       epi_tmem_release(tempty);
