@@ -461,7 +461,8 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
 //      j + EG_WARPS, ... over all columns, and the warps' partials are combined in warp order —
 //      a fixed summation order, so every dE row is deterministic.
 constexpr int EG_MAX = 8192;
-constexpr int EG_WARPS = 8;  // 256-thread blocks: several blocks per SM
+constexpr int EG_WARPS = 8;
+constexpr int EG_OWNER_SMEM = 24 * 1024;  // vocabulary sizes whose owner table lives in shared memory (96 KB)  // 256-thread blocks: several blocks per SM
 JN_DEV int tok_of(const int *tok, int B, int W, int r) {
   const int t = r / B, b = r - t * B;
   return tok[(size_t)b * W + t];
@@ -495,16 +496,24 @@ JN_DEV int block_excl_scan(int v, int *warp_sums, int *total) {
 
 // owner: V ints preset to INT_MAX; seg_start: n + 1 ints; list: n ints
 __global__ void __launch_bounds__(1024) embed_bucket_kernel(const int *tok, int B, int W, int T, const int *T_dev,
-                                                            int *owner, int *seg_word, int *seg_start, int *nseg,
-                                                            int *list) {
+                                                            int *owner_g, int V, int owner_sm, int *seg_word,
+                                                            int *seg_start, int *nseg, int *list) {
   extern __shared__ int eb_smem[];
   int *s_word = eb_smem;             // [EG_MAX] word of row r, later its slot
   int *s_slot = eb_smem + EG_MAX;    // [EG_MAX] slot of a first-occurrence row
   int *s_cnt = eb_smem + 2 * EG_MAX; // [EG_MAX] rows per slot, then append cursors
   __shared__ int warp_sums[32];
+  // first row of each word: in shared memory when the vocabulary fits (no global round trips),
+  // else the caller's INT_MAX-preset global array
+  int *owner = owner_sm ? eb_smem + 3 * EG_MAX : owner_g;
+  if (owner_sm) {
+    for (int w = threadIdx.x; w < V; w += blockDim.x) owner[w] = 0x7fffffff;
+    __syncthreads();
+  }
   const int n = (T_dev ? *T_dev : T) * B;
   for (int r = threadIdx.x; r < n; r += blockDim.x) {
-    const int w = tok_of(tok, B, W, r);
+    int w = tok_of(tok, B, W, r);
+    w = (w >= 0 && w < V) ? w : 0;  // a bad id is reported by the gather (ERR_RUNTIME: no commit)
     s_word[r] = w;
     atomicMin(&owner[w], r);
     s_cnt[r] = 0;
@@ -626,13 +635,19 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
                               const float *dX, int ldx, int Edim, int *seg_word, int *owner,
                               float *seg_grad, int ldg, int *nseg, cudaStream_t s) {
   if (T * B > EG_MAX) return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(owner, 0x7f, (size_t)V * sizeof(int), s);  // INT_MAX-ish
-  if (e != cudaSuccess) return e;
+  const int owner_sm = V <= EG_OWNER_SMEM;
+  cudaError_t e = cudaSuccess;
+  if (!owner_sm) {
+    e = cudaMemsetAsync(owner, 0x7f, (size_t)V * sizeof(int), s);  // INT_MAX-ish
+    if (e != cudaSuccess) return e;
+  }
   int *seg_start = owner + V;                 // scratch: T*B + 1 ints
   int *list = seg_start + (size_t)T * B + 1;  // scratch: T*B ints
-  e = set_smem_once((const void *)embed_bucket_kernel, 3 * EG_MAX * 4);
+  const int bsmem = (3 * EG_MAX + (owner_sm ? V : 0)) * 4;
+  e = set_smem_once((const void *)embed_bucket_kernel, (3 * EG_MAX + EG_OWNER_SMEM) * 4);
   if (e != cudaSuccess) return e;
-  embed_bucket_kernel<<<1, 1024, 3 * EG_MAX * 4, s>>>(tok, B, W, T, T_dev, owner, seg_word, seg_start, nseg, list);
+  embed_bucket_kernel<<<1, 1024, bsmem, s>>>(tok, B, W, T, T_dev, owner, V, owner_sm, seg_word, seg_start, nseg,
+                                             list);
   auto go = [&](auto kern, int nq) {
     const int smem = EG_MAX * 4 + EG_WARPS * nq * 32 * 4;
     cudaError_t r = set_smem_once((const void *)kern, smem);
