@@ -461,8 +461,8 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
 //      j + EG_WARPS, ... over all columns, and the warps' partials are combined in warp order —
 //      a fixed summation order, so every dE row is deterministic.
 constexpr int EG_MAX = 8192;
-constexpr int EG_WARPS = 8;
-constexpr int EG_OWNER_SMEM = 24 * 1024;  // vocabulary sizes whose owner table lives in shared memory (96 KB)  // 256-thread blocks: several blocks per SM
+constexpr int EG_WARPS = 8;  // 256-thread blocks: several blocks per SM
+constexpr int EG_OWNER_SMEM = 24 * 1024;  // vocabularies whose owner table lives in shared memory (96 KB)
 JN_DEV int tok_of(const int *tok, int B, int W, int r) {
   const int t = r / B, b = r - t * B;
   return tok[(size_t)b * W + t];
