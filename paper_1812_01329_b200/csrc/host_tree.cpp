@@ -273,9 +273,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   if (gl.n) TCHK("guards", launch_guards(gl, dst, st));
   if (p.tree_guard) TCHK("tree_guard", launch_tree_guard(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
   TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));
-  TCHK("cast", launch_cast_il(Wl, H, 3, E, bf(p.off.Wl_il), p.Ep, st));
-  TCHK("cast", launch_cast_il(U, H, 5, 2 * H, bf(p.off.U_il), p.P2, st));
-  TCHK("cast", launch_cast_il_T(U, H, 5, 2 * H, bf(p.off.UT_il), p.P5, st));
+  TCHK("cast", launch_tree_cast3(Wl, bf(p.off.Wl_il), p.Ep, U, bf(p.off.U_il), p.P2, bf(p.off.UT_il), p.P5, H, E, st));
   const int grid = 148;  // one CTA per SM: the leaf level of a B=25 forest already has ~76 tiles
   TCHK("tree_fwd", launch_tree_fwd(t, d, s, bf(p.off.Wl_il), bf(p.off.U_il), grid, dst, st));
   TCHK("root_xent", launch_tree_root(t, d, s, dst, st));

@@ -986,4 +986,44 @@ cudaError_t launch_cast_il_T(const float *src, int H, int ng, int cols, __nv_bfl
   return cudaGetLastError();
 }
 
+// The step's three operand copies in one launch: blocks [0, nl) cast W_leaf rows (interleaved by
+// 3), [nl, nl + nu) cast U rows (interleaved by 5), the rest transpose 32 x 32 tiles of U into U^T.
+__global__ void __launch_bounds__(256) tree_cast3_kernel(const float *Wl, __nv_bfloat16 *Wl_il, int ldw,
+                                                         const float *U, __nv_bfloat16 *U_il, int ldu,
+                                                         __nv_bfloat16 *UT_il, int ldut, int H, int E) {
+  __shared__ float tile[32][33];
+  const int nl = 3 * H, nu = 5 * H;
+  int bx = blockIdx.x;
+  if (bx < nl + nu) {  // one destination row per block
+    const bool leaf = bx < nl;
+    const int ng = leaf ? 3 : 5, cols = leaf ? E : 2 * H, ld = leaf ? ldw : ldu;
+    const int ri = leaf ? bx : bx - nl;
+    const int rc = (ri % ng) * H + ri / ng;
+    const float *sr = (leaf ? Wl : U) + (size_t)rc * cols;
+    __nv_bfloat16 *dr = (leaf ? Wl_il : U_il) + (size_t)ri * ld;
+    for (int k = threadIdx.x; k < ld; k += blockDim.x) dr[k] = __float2bfloat16_rn(k < cols ? sr[k] : 0.f);
+    return;
+  }
+  bx -= nl + nu;  // transpose tile: dst[k][ri] = rb(U[rc][k]), ri = 5u + g <-> rc = g H + u
+  const int ntr = (ldut + 31) / 32;
+  const int ri0 = (bx % ntr) * 32, k0 = (bx / ntr) * 32, cols = 2 * H;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8) {
+    const int ri = ri0 + i, k = k0 + tx;
+    tile[i][tx] = (ri < nu && k < cols) ? U[(size_t)((ri % 5) * H + ri / 5) * cols + k] : 0.f;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int k = k0 + i, ri = ri0 + tx;
+    if (k < cols && ri < ldut) UT_il[(size_t)k * ldut + ri] = __float2bfloat16_rn(ri < nu ? tile[tx][i] : 0.f);
+  }
+}
+cudaError_t launch_tree_cast3(const float *Wl, __nv_bfloat16 *Wl_il, int ldw, const float *U,
+                              __nv_bfloat16 *U_il, int ldu, __nv_bfloat16 *UT_il, int ldut, int H, int E,
+                              cudaStream_t s) {
+  const int tiles = ((ldut + 31) / 32) * ((2 * H + 31) / 32);
+  tree_cast3_kernel<<<8 * H + tiles, 256, 0, s>>>(Wl, Wl_il, ldw, U, U_il, ldu, UT_il, ldut, H, E);
+  return cudaGetLastError();
+}
+
 }  // namespace jk

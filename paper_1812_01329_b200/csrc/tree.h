@@ -73,6 +73,10 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
 // bf16 working copies: rows interleaved by `ng` gates (row ng*u+g <- g*H+u), optional transpose
 cudaError_t launch_cast_il(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld,
                            cudaStream_t s);
+// the three above for one TreeLSTM step in one launch (W_leaf rows, U rows, U^T tiles)
+cudaError_t launch_tree_cast3(const float *Wl, __nv_bfloat16 *Wl_il, int ldw, const float *U,
+                              __nv_bfloat16 *U_il, int ldu, __nv_bfloat16 *UT_il, int ldut, int H, int E,
+                              cudaStream_t s);
 cudaError_t launch_cast_il_T(const float *src, int H, int ng, int cols, __nv_bfloat16 *dst, int ld,
                              cudaStream_t s);
 
