@@ -237,7 +237,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     janus_status r = dp_init(g);
     if (r != JANUS_OK) return r;
   }
-  TreeDims d{N, B, p.V, E, H, p.C, p.Ep, p.P2, p.P5, p.P3};
+  TreeDims d{N, B, p.V, E, H, p.C, p.Ep, p.P2, p.P5, p.P3, p.max_N};
   TreeSched s{ip(p.off.height), ip(p.off.order), ip(p.off.irank), ip(p.off.pslot), ip(p.off.lvl_off),
               ip(p.off.meta), ip(p.off.tree_of), ip(p.off.pcount)};
   TreeBufs t{};

@@ -13,6 +13,8 @@
 //   root classifier + xent -> backward: one cooperative launch walks the levels top-down.
 // Gate-interleaved rows: U_il row 5u+g = U row g*H+u (g = i, f_l, f_r, o, u); W_leaf_il row 3u+g
 // = W_leaf row g*H+u (g = i, o, u). Bias b has blocks (i, f, o, u) (reading Q5).
+#include <string.h>
+
 #include "common.cuh"
 #include "gemm_tc.h"
 #include "tree.h"
@@ -669,13 +671,21 @@ static cudaError_t coop(const void *fn, int grid, int smem, void **args, cudaStr
 cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                             const __nv_bfloat16 *Wl_il, const __nv_bfloat16 *U_il, int grid,
                             const DevStatus *st, cudaStream_t str) {
-  TreeFwdMaps mp;
-  bool ok = make_tmap_bf16(&mp.x_leaf, t.x_leaf, d.E, d.N, d.Ep, 128);
-  ok = ok && make_tmap_bf16(&mp.w_leaf, Wl_il, d.E, 3ull * d.H, d.Ep, 48);
-  ok = ok && make_tmap_bf16(&mp.stage_h, t.stage_h, 2ull * d.H, d.N, d.P2, 128);
-  ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
-  ok = ok && make_tmap_bf16(&mp.stage_h32, t.stage_h, 2ull * d.H, d.N, d.P2, 32);
-  if (!ok) return cudaErrorInvalidValue;
+  // the maps span the allocated Nmax rows (rows past this step's N only feed discarded accumulator
+  // rows), so they depend on the workspace alone and are encoded once per workspace, not per step
+  struct Key { const void *a, *b, *c; long long E, H, Ep, P2, Nmax; };  // no padding: compared bytewise
+  thread_local Key key{};
+  thread_local TreeFwdMaps mp;
+  const Key k{t.x_leaf, Wl_il, U_il, d.E, d.H, d.Ep, d.P2, d.Nmax};
+  if (memcmp(&k, &key, sizeof k) != 0) {
+    bool ok = make_tmap_bf16(&mp.x_leaf, t.x_leaf, d.E, d.Nmax, d.Ep, 128);
+    ok = ok && make_tmap_bf16(&mp.w_leaf, Wl_il, d.E, 3ull * d.H, d.Ep, 48);
+    ok = ok && make_tmap_bf16(&mp.stage_h, t.stage_h, 2ull * d.H, d.Nmax, d.P2, 128);
+    ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
+    ok = ok && make_tmap_bf16(&mp.stage_h32, t.stage_h, 2ull * d.H, d.Nmax, d.P2, 32);
+    if (!ok) { key = Key{}; return cudaErrorInvalidValue; }
+    key = k;
+  }
   const bool six = tree_smem_fwd(6, d.H) <= 227 * 1024;  // ring depth that fits beside the staging
   const int smem = tree_smem_fwd(six ? 6 : 4, d.H);
   const void *fn = six ? (const void *)tree_fwd_kernel<6> : (const void *)tree_fwd_kernel<4>;
@@ -929,13 +939,18 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
 cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                             const __nv_bfloat16 *UT_il, int grid, const DevStatus *st,
                             cudaStream_t str) {
-  TreeBwdMaps mp;
-  bool ok = make_tmap_bf16(&mp.dz, t.DZ_int, 5ull * d.H, d.N, d.P5, 128);
-  ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
-  ok = ok && make_tmap_bf16(&mp.dz32, t.DZ_int, 5ull * d.H, d.N, d.P5, 32);
-  if (!ok) return cudaErrorInvalidValue;
-  ok = ok && make_tmap_bf16(&mp.ut32, UT_il, 5ull * d.H, 2ull * d.H, d.P5, T_RES_NT);
-  if (!ok) return cudaErrorInvalidValue;
+  struct Key { const void *a, *b; long long H, P5, Nmax; };  // once per workspace (see the forward)
+  thread_local Key key{};
+  thread_local TreeBwdMaps mp;
+  const Key k{t.DZ_int, UT_il, d.H, d.P5, d.Nmax};
+  if (memcmp(&k, &key, sizeof k) != 0) {
+    bool ok = make_tmap_bf16(&mp.dz, t.DZ_int, 5ull * d.H, d.Nmax, d.P5, 128);
+    ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
+    ok = ok && make_tmap_bf16(&mp.dz32, t.DZ_int, 5ull * d.H, d.Nmax, d.P5, 32);
+    ok = ok && make_tmap_bf16(&mp.ut32, UT_il, 5ull * d.H, 2ull * d.H, d.P5, T_RES_NT);
+    if (!ok) { key = Key{}; return cudaErrorInvalidValue; }
+    key = k;
+  }
   const bool res = (5 * d.H + 63) / 64 <= T_RES_CHUNKS && grid >= (2 * d.H + T_RES_NT - 1) / T_RES_NT;
   const int smem = res ? 1024 + T_STAGES * T_ASTAGE + T_RES_CHUNKS * T_RES_NT * 128 + 256 : tree_smem();
   const void *fn = res ? (const void *)tree_bwd_kernel<true> : (const void *)tree_bwd_kernel<false>;

@@ -28,6 +28,7 @@ struct TreeDims {
   int P2;   // stage_h pitch (bf16) >= 2H + 1, multiple of 64
   int P5;   // DZ_int pitch >= 5H, multiple of 64
   int P3;   // DZ_leaf pitch >= 3H, multiple of 64
+  int Nmax; // rows allocated for the node arrays (the tensor maps span Nmax rows: step-invariant)
 };
 
 struct TreeBufs {
