@@ -286,13 +286,15 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     a.A = bf(p.off.DZ_int); a.lda = p.P5; a.a_mn = 1;
     a.B = bf(p.off.stage_h); a.ldb = p.P2; a.b_mn = 1;
     a.ep.C = fp(p.off.gU); a.ep.ldc = p.ldgU;
-    TCHK("gemm_dU", gemm_bf16(a, st));
+
     GemmOp b2;  // dW_leaf | db_leaf = rb(dz_leaf)^T [x | 1]  (K = number of leaves)
     b2.M = 3 * H; b2.N = E + 1; b2.K = N; b2.K_dev = s.meta + 2;
     b2.A = bf(p.off.DZ_leaf); b2.lda = p.P3; b2.a_mn = 1;
     b2.B = bf(p.off.x_leaf); b2.ldb = p.Ep; b2.b_mn = 1;
     b2.ep.C = fp(p.off.gWl); b2.ep.ldc = p.ldgW;
-    TCHK("gemm_dWleaf", gemm_bf16(b2, st));
+    // one grouped launch: each GEMM alone has too few (long-K) tiles to occupy the GPU
+    const GemmOp both[2] = {a, b2};
+    TCHK("gemm_wgrad", gemm_bf16_group(both, 2, st));
   }
   if (g.nccl) {
     g.prof.mark("dp_allreduce", st);
