@@ -204,6 +204,7 @@ cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSc
 // Single block. Heights by a per-tree scan in post-order (children precede parents); then a
 // stable counting sort by height in node-id order (warp match + per-level prefix over warps).
 constexpr int TREE_SCHED_SMEM_NODES = 13 * 1024;  // heights + children in shared memory up to 156 KB
+constexpr int TREE_SCHED_SMEM_OFF = 4096;         // + the tree offsets (16 KB)
 
 __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
                                                              const DevStatus *st) {
@@ -217,6 +218,8 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
     if (tid == 0) { s.meta[0] = 0; s.meta[1] = 0; s.meta[2] = 0; s.meta[3] = 0; }
     return;
   }
+  unsigned long long *pb = t.dbg ? t.dbg + 4 * 256 * 256 * 2 : nullptr;  // dev probe: phase times
+  if (pb && tid == 0) pb[0] = gtimer();
   for (int i = tid; i <= TREE_MAX_LEVELS; i += blockDim.x) { hist[i] = 0; running[i] = 0; }
   if (tid == 0) s_L = 1;
   __syncthreads();
@@ -237,7 +240,34 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
     }
     __syncthreads();
   }
-  for (int tr = tid; tr < B; tr += blockDim.x) {
+  if (pb && tid == 0) pb[1] = gtimer();
+  // small forests (<= 2 nodes per thread): parallel relaxation; large ones: the per-tree walk (a
+  // sweep over 10 nodes per thread costs more than walking the largest tree)
+  const bool relax = in_smem && N <= 2 * (int)blockDim.x;
+  if (relax) {
+    // heights by parallel relaxation over all nodes: h = 1 + max(h_l, h_r) from h = 0 rises
+    // monotonically to the longest leaf path, one level per sweep (a sweep may read a value
+    // another thread has already raised: the fixpoint is the same), so max height + 1 sweeps,
+    // each one node per thread, instead of one thread walking each whole tree. Children with
+    // ids >= the node are ignored (the guard reports them), so no cycle can keep it rising.
+    for (int n = tid; n < N; n += blockDim.x) hh[n] = 0;
+    __syncthreads();
+    bool more = true;
+    while (more) {
+      bool changed = false;
+      for (int n = tid; n < N; n += blockDim.x) {
+        const int l = kl[n];
+        if (l == LEAF) continue;
+        const int r = kr[n];
+        const int hl = (l >= 0 && l < n) ? hh[l] : 0;
+        const int hr = (r >= 0 && r < n) ? hh[r] : 0;
+        const int h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
+        if (h != hh[n]) { hh[n] = h; changed = true; }
+      }
+      more = __syncthreads_or(changed);
+    }
+  }
+  for (int tr = relax ? B : tid; tr < B; tr += blockDim.x) {  // one thread walks each tree
     const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
     for (int n = lo; n < hi; ++n) {
       int h = 0;
@@ -249,13 +279,33 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
         h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
       }
       hh[n] = h;
-      // tree_of, pslot, heights to global by the walking thread (stores only: no round trips)
-      s.tree_of[n] = tr;
-      s.pslot[n] = -1;
-      if (hh != s.height) s.height[n] = h;
+      if (!in_smem) s.tree_of[n] = tr;  // (in shared memory: the parallel pass below)
     }
   }
   __syncthreads();
+  // tree_of, pslot, heights to global in parallel over nodes (the walk above is one thread per
+  // tree: it carries only the on-chip height chain); tree of a node by binary search in the
+  // offsets (shared memory)
+  if (in_smem) {
+    int *soff = sh_height + 3 * N;
+    const bool off_sm = B + 1 <= TREE_SCHED_SMEM_OFF;
+    if (off_sm)
+      for (int i = tid; i <= B; i += blockDim.x) soff[i] = t.off[i];
+    __syncthreads();
+    const int *offp = off_sm ? soff : t.off;
+    for (int n = tid; n < N; n += blockDim.x) {
+      int lo_t = 0, hi_t = B - 1;
+      while (lo_t < hi_t) {
+        const int mid = (lo_t + hi_t + 1) >> 1;
+        if (offp[mid] <= n) lo_t = mid; else hi_t = mid - 1;
+      }
+      s.tree_of[n] = lo_t;
+      s.height[n] = hh[n];
+    }
+  }
+  for (int n = tid; n < N; n += blockDim.x) s.pslot[n] = -1;
+  __syncthreads();
+  if (pb && tid == 0) pb[2] = gtimer();
   for (int n = tid; n < N; n += blockDim.x) {
     atomicAdd(&hist[hh[n]], 1);
     atomicMax(&s_L, hh[n] + 1);
@@ -274,6 +324,7 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
     s.meta[3] = N - hist[0];
   }
   __syncthreads();
+  if (pb && tid == 0) pb[3] = gtimer();
   // stable placement, chunk by chunk of 1024 ids
   for (int c0 = 0; c0 < N; c0 += blockDim.x) {
     for (int i = tid; i < 32 * TREE_MAX_LEVELS; i += blockDim.x) (&wcnt[0][0])[i] = 0;
@@ -304,6 +355,7 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
     }
     __syncthreads();
   }
+  if (pb && tid == 0) pb[4] = gtimer();
   // parent slots
   for (int n = tid; n < N; n += blockDim.x) {
     if (t.kind[n] == 1 && hh[n] > 0) {
@@ -312,13 +364,15 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
       if (r >= 0 && r < N) s.pslot[r] = (s.irank[n] << 1) | 1;
     }
   }
+  __syncthreads();
+  if (pb && tid == 0) pb[5] = gtimer();
   (void)st;
 }
 
 cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                                  const DevStatus *st, cudaStream_t str) {
-  const int smem = d.N <= TREE_SCHED_SMEM_NODES ? 3 * d.N * 4 : 0;
-  cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, 3 * TREE_SCHED_SMEM_NODES * 4);
+  const int smem = d.N <= TREE_SCHED_SMEM_NODES ? (3 * d.N + TREE_SCHED_SMEM_OFF) * 4 : 0;
+  cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, (3 * TREE_SCHED_SMEM_NODES + TREE_SCHED_SMEM_OFF) * 4);
   if (e != cudaSuccess) return e;
   tree_schedule_kernel<<<1, 1024, smem, str>>>(t, d, s, st);
   return cudaGetLastError();

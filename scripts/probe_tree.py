@@ -82,3 +82,8 @@ for l in range(L - 1, 0, -1):
     start = np.median(rb[k])
     print(f"  level {l:2d} ({int(lvl[l + 1] - lvl[l]):4d} nodes, {int(act.sum())} CTAs): "
           f"mainloop {(pr[act, 0].max() - start) / 1e3:5.2f} us  tmem {((pr[act, 2] - pr[act, 0]).max()) / 1e3:5.2f} us  epilogue {((pr[act, 1] - pr[act, 2]).max()) / 1e3:5.2f} us")
+
+sc = pp[4 * 256 * 256 * 2: 4 * 256 * 256 * 2 + 8]
+if sc[0] > 0:
+    names = ["init", "stage children", "height walk", "histogram+offsets", "stable placement", "parent slots"]
+    print("-- schedule kernel phases (us):", {names[i]: round((sc[i + 1] - sc[i]) / 1e3, 2) for i in range(5)})

@@ -81,6 +81,16 @@ def test_tree_hidden_not_multiple_of_four_and_many_trees():
     _check(prog, forests, scale=0.2)
 
 
+def test_tree_large_forest_small_cells():
+    """N > 2048 nodes (the schedule's per-tree walk instead of the parallel relaxation; several
+    128-row tiles per level; 17 root-classifier blocks) at a small H so the oracle stays fast."""
+    V, B = 50, 130
+    prog = pg.treelstm_program(V=V, E=8, H=16, C=2, B=B, lr=0.2)
+    f = gen.sst_forest(gen.SEED_C3, 21, B, V, max_leaves=40)
+    assert len(f[0]) > 2048
+    _check(prog, [f], scale=0.3)
+
+
 def test_tree_one_leaf_trees_and_all_shapes():
     """Degenerate cases: a lone root leaf, and every shape with <= 5 leaves in one forest."""
     V = 40
