@@ -1,6 +1,7 @@
 // common.cuh — sm_100a building blocks shared by the JANUS device kernels: error handling, bf16
 // helpers, mbarrier / TMA (cp.async.bulk.tensor) / tcgen05 (MMA, TMEM) inline-PTX wrappers.
 #pragma once
+#include <stdlib.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -327,6 +328,36 @@ inline cudaError_t set_smem_once(const void *fn, int bytes) {
   if (e == cudaSuccess && n < 64) { fns[n] = fn; sizes[n] = bytes; ++n; }
   return e;
 }
+
+// ------------------------------------------------------------------------------ PDL
+// Programmatic dependent launch: the step's short kernels are launched with programmatic stream
+// serialisation, so each one's CTAs are scheduled while its predecessor still runs; every such
+// kernel starts with griddepcontrol.wait (the predecessor grid has completed and its memory is
+// visible — so nothing is read or written early) and then lets its own successor launch.
+JN_DEV void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+inline bool pdl_on() {
+  static const bool on = !(getenv("JANUS_PDL") && getenv("JANUS_PDL")[0] == '0');
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 }  // namespace jk
 
 #define JN_CUDA(x)                                                      \

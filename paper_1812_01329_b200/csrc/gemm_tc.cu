@@ -144,6 +144,7 @@ JN_DEV TileRef tile_ref(const GemmBatch &gb, int t, int rank = 0) {
 // STAGES is even, so every stage has one fixed owner and no wait can alias a phase
 template <int BN, int STAGES, int NMMA, int CM>
 __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
+  pdl_enter();
   using C = GemmCfg<BN, STAGES, NMMA>;
   static_assert(STAGES % NMMA == 0, "stage ownership");
   // CM > 1: clusters of CM CTAs along M share each B tile; CTA r loads rows / k-rows slice r of it
@@ -577,21 +578,22 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
   if (total == 0) return cudaSuccess;
   if (CM == 1) {
     const int grid = std::min(total, g_num_sms);
-    kern<<<grid, C::THREADS, C::SMEM, st>>>(gb);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(grid), dim3(C::THREADS), C::SMEM, st, gb);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(std::min(total, g_num_sms / CM) * CM);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CM;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see pdl_enter (common.cuh)
+  at[1].val.programmaticStreamSerializationAllowed = pdl_on() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, gb);
 }
 

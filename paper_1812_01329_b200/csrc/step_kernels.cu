@@ -11,6 +11,7 @@ static constexpr int NSM = 148;
 
 // ------------------------------------------------------------------------------ init / guards
 __global__ void step_init_kernel(DevStatus *st, unsigned int *bar, int nbar, int stride) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
     st->key = KEY_PASS;
@@ -26,13 +27,17 @@ __global__ void step_init_kernel(DevStatus *st, unsigned int *bar, int nbar, int
 
 cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s, int stride) {
   const int n = (nbar + stride - 1) / stride;
-  step_init_kernel<<<std::max(1, std::min((n + 255) / 256, 8)), 256, 0, s>>>(st, barriers, nbar, stride);
+  {
+    const cudaError_t pe_ = launch_pdl(step_init_kernel, dim3(std::max(1, std::min((n + 255) / 256, 8))), dim3(256), 0, s, st, barriers, nbar, stride);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
 // One block per assumption; each failing element proposes (id << 40 | index) to an atomicMin,
 // so the reported failure is the minimum id and, within it, the first element (reading Q9).
 __global__ void guards_kernel(GuardList gl, DevStatus *st) {
+  pdl_enter();
   const GuardDesc g = gl.g[blockIdx.x];
   const unsigned long long mask = (1ull << IDX_BITS) - 1;
   if (g.kind == G_TREE) return;  // evaluated by tree_guard_kernel
@@ -52,7 +57,10 @@ __global__ void guards_kernel(GuardList gl, DevStatus *st) {
 
 cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s) {
   if (gl.n <= 0) return cudaSuccess;
-  guards_kernel<<<gl.n, 128, 0, s>>>(gl, st);
+  {
+    const cudaError_t pe_ = launch_pdl(guards_kernel, dim3(gl.n), dim3(128), 0, s, gl, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -61,6 +69,7 @@ cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s) {
 __global__ void gather_kernel(const float *__restrict__ E, int V, int Edim, const int *__restrict__ tok,
                               int B, int W, int T, const int *T_dev, __nv_bfloat16 *X, int ldx,
                               DevStatus *st) {
+  pdl_enter();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int rows = T * B;
   const int Tb = T_dev ? *T_dev : T;
@@ -93,11 +102,15 @@ cudaError_t launch_gather(const float *E, int V, int Edim, const int *tok, int B
   const int rows = T * B;
   int blocks = (rows * 32 + 255) / 256;
   blocks = blocks < 4 * NSM ? blocks : 4 * NSM;
-  gather_kernel<<<blocks, 256, 0, s>>>(E, V, Edim, tok, B, W, T, T_dev, X, ldx, st);
+  {
+    const cudaError_t pe_ = launch_pdl(gather_kernel, dim3(blocks), dim3(256), 0, s, E, V, Edim, tok, B, W, T, T_dev, X, ldx, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
 __global__ void trip_kernel(const int *lens, int B, int W, DevStatus *st) {
+  pdl_enter();
   if (threadIdx.x == 0) {
     int T = 0;
     for (int b = 0; b < B; ++b) T = max(T, lens[b]);
@@ -105,7 +118,10 @@ __global__ void trip_kernel(const int *lens, int B, int W, DevStatus *st) {
   }
 }
 cudaError_t launch_trip(const int *lens, int B, int W, DevStatus *st, cudaStream_t s) {
-  trip_kernel<<<1, 32, 0, s>>>(lens, B, W, st);
+  {
+    const cudaError_t pe_ = launch_pdl(trip_kernel, dim3(1), dim3(32), 0, s, lens, B, W, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -207,6 +223,7 @@ cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v
 // (optionally gate-interleaving), the interleaved transpose of W_hh, bias interleave, ones-column
 // fill. Each segment strides its own work units over blockIdx.x.
 __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
+  pdl_enter();
   const PrepSeg sg = pl.s[blockIdx.y];
   switch (sg.kind) {
     case P_CAST_ROWS: {
@@ -271,7 +288,10 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
 
 cudaError_t launch_prep(const PrepList &pl, cudaStream_t s) {
   if (pl.n <= 0) return cudaSuccess;
-  prep_kernel<<<dim3(2 * NSM, pl.n), 256, 0, s>>>(pl);
+  {
+    const cudaError_t pe_ = launch_pdl(prep_kernel, dim3(dim3(2 * NSM, pl.n)), dim3(256), 0, s, pl);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -307,6 +327,7 @@ __global__ void __launch_bounds__(NT) xent_kernel(const float *__restrict__ logi
                                                   const int *lens, const int *T_dev, float n_valid,
                                                   __nv_bfloat16 *dy, int lddy, float *rowloss,
                                                   DevStatus *st) {
+  pdl_enter();
   __shared__ float sh[33];
   __shared__ float s_nv;
   const int Tb = T_dev ? *T_dev : rows / B;
@@ -357,6 +378,7 @@ __global__ void __launch_bounds__(NT) xent_reg_kernel(const float *__restrict__ 
                                                       const int *lens, const int *T_dev, float n_valid,
                                                       __nv_bfloat16 *dy, int lddy, float *rowloss,
                                                       DevStatus *st) {
+  pdl_enter();
   __shared__ float sh[33];
   __shared__ float s_nv;
   const int Tb = T_dev ? *T_dev : rows / B;
@@ -442,11 +464,17 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
   const bool aligned = (ldl % 4) == 0 && (lddy % 4) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(dy) & 7) == 0;
   if (aligned && V <= NT * 4 * NV4) {
-    xent_reg_kernel<NT, NV4><<<blocks, NT, 0, s>>>(logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
+    {
+    const cudaError_t pe_ = launch_pdl(xent_reg_kernel<NT, NV4>, dim3(blocks), dim3(NT), 0, s, logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
                                                    lddy, rowloss, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   } else {
-    xent_kernel<256><<<blocks, 256, 0, s>>>(logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
+    {
+    const cudaError_t pe_ = launch_pdl(xent_kernel<256>, dim3(blocks), dim3(256), 0, s, logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
                                             lddy, rowloss, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   }
   return cudaGetLastError();
 }
@@ -498,6 +526,7 @@ JN_DEV int block_excl_scan(int v, int *warp_sums, int *total) {
 __global__ void __launch_bounds__(1024) embed_bucket_kernel(const int *tok, int B, int W, int T, const int *T_dev,
                                                             int *owner_g, int V, int owner_sm, int *seg_word,
                                                             int *seg_start, int *nseg, int *list) {
+  pdl_enter();
   extern __shared__ int eb_smem[];
   int *s_word = eb_smem;             // [EG_MAX] word of row r, later its slot
   int *s_slot = eb_smem + EG_MAX;    // [EG_MAX] slot of a first-occurrence row
@@ -566,6 +595,7 @@ template <int NQ>
 __global__ void __launch_bounds__(EG_WARPS * 32, 2) embed_segsum_kernel(
     const int *seg_start, const int *list, const int *nseg, const float *__restrict__ dX, int ldx, int Edim,
     float *seg_grad, int ldg) {
+  pdl_enter();
   extern __shared__ int eg_smem[];
   int *rows = eg_smem;
   float *part = reinterpret_cast<float *>(eg_smem + EG_MAX);  // [EG_WARPS][NQ * 32]
@@ -646,13 +676,19 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
   const int bsmem = (3 * EG_MAX + (owner_sm ? V : 0)) * 4;
   e = set_smem_once((const void *)embed_bucket_kernel, (3 * EG_MAX + EG_OWNER_SMEM) * 4);
   if (e != cudaSuccess) return e;
-  embed_bucket_kernel<<<1, 1024, bsmem, s>>>(tok, B, W, T, T_dev, owner, V, owner_sm, seg_word, seg_start, nseg,
+  {
+    const cudaError_t pe_ = launch_pdl(embed_bucket_kernel, dim3(1), dim3(1024), bsmem, s, tok, B, W, T, T_dev, owner, V, owner_sm, seg_word, seg_start, nseg,
                                              list);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   auto go = [&](auto kern, int nq) {
     const int smem = EG_MAX * 4 + EG_WARPS * nq * 32 * 4;
     cudaError_t r = set_smem_once((const void *)kern, smem);
     if (r != cudaSuccess) return r;
-    kern<<<8 * NSM, EG_WARPS * 32, smem, s>>>(seg_start, list, nseg, dX, ldx, Edim, seg_grad, ldg);
+    {
+    const cudaError_t pe_ = launch_pdl(kern, dim3(8 * NSM), dim3(EG_WARPS * 32), smem, s, seg_start, list, nseg, dX, ldx, Edim, seg_grad, ldg);
+    if (pe_ != cudaSuccess) return pe_;
+  }
     return cudaGetLastError();
   };
   if (Edim <= 8 * 32) return go(embed_segsum_kernel<8>, 8);
@@ -663,6 +699,7 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
 
 // ------------------------------------------------------------------------------ finalize
 __global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, DevStatus *st) {
+  pdl_enter();
   __shared__ float sh[1024];
   float acc = 0.f;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) acc += rowloss[i];
@@ -697,7 +734,10 @@ __global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, De
 cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
                             int world_size, cudaStream_t s) {
   (void)world_size;
-  finalize_kernel<<<1, 1024, 0, s>>>(rowloss, rows, gl, st);
+  {
+    const cudaError_t pe_ = launch_pdl(finalize_kernel, dim3(1), dim3(1024), 0, s, rowloss, rows, gl, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -776,6 +816,7 @@ cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_w
 // ------------------------------------------------------------------------------ commit
 // Predicated on the device status: with any failure nothing is written (all-or-nothing).
 __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
+  pdl_enter();
   if (st->status != 0) return;
   const CommitSeg sg = cl.s[blockIdx.y];
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -857,7 +898,10 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
 
 cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s) {
   if (cl.n <= 0) return cudaSuccess;
-  commit_kernel<<<dim3(4 * NSM, cl.n), 256, 0, s>>>(cl, st);
+  {
+    const cudaError_t pe_ = launch_pdl(commit_kernel, dim3(dim3(4 * NSM, cl.n)), dim3(256), 0, s, cl, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 

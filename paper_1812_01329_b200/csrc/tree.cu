@@ -128,6 +128,7 @@ constexpr int TREE_GUARD_SMEM_INTS = 48 * 1024;  // offsets + parent counts in s
 __global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d, TreeSched s,
                                                           unsigned id, long long V, long long maxn,
                                                           DevStatus *st) {
+  pdl_enter();
   __shared__ int s_badoff;
   __shared__ int s_badnode;
   const int N = d.N, B = d.B;
@@ -196,7 +197,10 @@ cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSc
   const int smem = d.B + 1 + d.N <= TREE_GUARD_SMEM_INTS ? (d.B + 1 + d.N) * 4 : 0;
   cudaError_t e = set_smem_once((const void *)tree_guard_kernel, TREE_GUARD_SMEM_INTS * 4);
   if (e != cudaSuccess) return e;
-  tree_guard_kernel<<<1, 1024, smem, str>>>(t, d, s, id, V, max_nodes, st);
+  {
+    const cudaError_t pe_ = launch_pdl(tree_guard_kernel, dim3(1), dim3(1024), smem, str, t, d, s, id, V, max_nodes, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -208,6 +212,7 @@ constexpr int TREE_SCHED_SMEM_OFF = 4096;         // + the tree offsets (16 KB)
 
 __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
                                                              const DevStatus *st) {
+  pdl_enter();
   __shared__ int hist[TREE_MAX_LEVELS + 1];
   __shared__ int running[TREE_MAX_LEVELS + 1];
   __shared__ unsigned short wcnt[32][TREE_MAX_LEVELS];
@@ -374,7 +379,10 @@ cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const Tre
   const int smem = d.N <= TREE_SCHED_SMEM_NODES ? (3 * d.N + TREE_SCHED_SMEM_OFF) * 4 : 0;
   cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, (3 * TREE_SCHED_SMEM_NODES + TREE_SCHED_SMEM_OFF) * 4);
   if (e != cudaSuccess) return e;
-  tree_schedule_kernel<<<1, 1024, smem, str>>>(t, d, s, st);
+  {
+    const cudaError_t pe_ = launch_pdl(tree_schedule_kernel, dim3(1), dim3(1024), smem, str, t, d, s, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -761,6 +769,7 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
 constexpr int ROOT_TPB = 8;  // trees per block
 
 __global__ void __launch_bounds__(256) tree_root_kernel(TreeBufs t, TreeDims d, TreeSched s, DevStatus *st) {
+  pdl_enter();
   const int B = d.B, H = d.H, C = d.C;
   __shared__ float dyr[ROOT_TPB * 8];  // [tree][class] rounded dy (C <= 8)
   __shared__ float ysh[ROOT_TPB * 8];  // logits
@@ -843,7 +852,10 @@ __global__ void __launch_bounds__(256) tree_root_kernel(TreeBufs t, TreeDims d, 
 cudaError_t launch_tree_root(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                              DevStatus *st, cudaStream_t str) {
   if (d.C > 8) return cudaErrorInvalidValue;
-  tree_root_kernel<<<(d.B + ROOT_TPB - 1) / ROOT_TPB, 256, 0, str>>>(t, d, s, st);
+  {
+    const cudaError_t pe_ = launch_pdl(tree_root_kernel, dim3((d.B + ROOT_TPB - 1) / ROOT_TPB), dim3(256), 0, str, t, d, s, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
@@ -1060,6 +1072,7 @@ cudaError_t launch_cast_il_T(const float *src, int H, int ng, int cols, __nv_bfl
 __global__ void __launch_bounds__(256) tree_cast3_kernel(const float *Wl, __nv_bfloat16 *Wl_il, int ldw,
                                                          const float *U, __nv_bfloat16 *U_il, int ldu,
                                                          __nv_bfloat16 *UT_il, int ldut, int H, int E) {
+  pdl_enter();
   __shared__ float tile[32][33];
   const int nl = 3 * H, nu = 5 * H;
   int bx = blockIdx.x;
@@ -1091,7 +1104,10 @@ cudaError_t launch_tree_cast3(const float *Wl, __nv_bfloat16 *Wl_il, int ldw, co
                               __nv_bfloat16 *U_il, int ldu, __nv_bfloat16 *UT_il, int ldut, int H, int E,
                               cudaStream_t s) {
   const int tiles = ((ldut + 31) / 32) * ((2 * H + 31) / 32);
-  tree_cast3_kernel<<<8 * H + tiles, 256, 0, s>>>(Wl, Wl_il, ldw, U, U_il, ldu, UT_il, ldut, H, E);
+  {
+    const cudaError_t pe_ = launch_pdl(tree_cast3_kernel, dim3(8 * H + tiles), dim3(256), 0, s, Wl, Wl_il, ldw, U, U_il, ldu, UT_il, ldut, H, E);
+    if (pe_ != cudaSuccess) return pe_;
+  }
   return cudaGetLastError();
 }
 
