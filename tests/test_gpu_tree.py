@@ -91,6 +91,16 @@ def test_tree_large_forest_small_cells():
     _check(prog, [f], scale=0.3)
 
 
+@pytest.mark.parametrize("H", [320, 800])
+def test_tree_wide_hidden_kernel_variants(H):
+    """H=320: 5H > 1536, so the backward streams U^T through its ring instead of keeping it
+    resident; H=800: the forward's 4-deep ring (the 6-deep one no longer fits beside the
+    epilogue staging)."""
+    V, B = 40, 3
+    prog = pg.treelstm_program(V=V, E=24, H=H, C=2, B=B, lr=0.2)
+    _check(prog, [gen.sst_forest(gen.SEED_C3, 5, B, V, max_leaves=6)], scale=0.1)
+
+
 def test_tree_one_leaf_trees_and_all_shapes():
     """Degenerate cases: a lone root leaf, and every shape with <= 5 leaves in one forest."""
     V = 40
