@@ -320,7 +320,16 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
                 st_i = [x.clone() for x in stt]
                 gt.run_imperative(forests[0], st_i, wst, stream=stream)
                 ms_ti = timed(lambda k: gt.run_imperative(forests[k % 4], st_i, wst, stream=stream), 2) / 2
-                c3_abl = {"IMP": Bt * 1000.0 / ms_ti, "graph_level_batched": Bt * 1000.0 / ms_t}
+                # -PARL: the same device program with the level loops on one CTA (no parallelism
+                # across the nodes of a level)
+                os.environ["JANUS_TREE_GRID"] = "1"
+                try:
+                    gt.run(forests[0], st_i, wst, stream=stream)
+                    ms_t1 = timed(lambda k: gt.run(forests[k % 4], st_i, wst, stream=stream), 3) / 3
+                finally:
+                    del os.environ["JANUS_TREE_GRID"]
+                c3_abl = {"IMP": Bt * 1000.0 / ms_ti, "graph_one_cta_per_level": Bt * 1000.0 / ms_t1,
+                          "graph_level_batched": Bt * 1000.0 / ms_t}
             del wst
         # --- Figure 7 ablation on B200: samples/s of the same C2 batches through the
         # imperative executor (IMP), the graph with the loop kept as a device While (BASE: no
@@ -340,8 +349,8 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
             "c3_b25_sentences_per_s": c3_abl,
             "note": "IMP = janus_run_imperative (one launch per op, host-side control flow); BASE_while = "
                     "speculative graph with the loop as a device While (RANGE assumption); UNRL = unrolled "
-                    "graph (TRIP_COUNT). +SPCN and +PARL have no separate toggle: every device graph is "
-                    "shape-specialised and level/wavefront-parallel"}
+                    "graph (TRIP_COUNT); C3 graph_one_cta_per_level = the level loops on one CTA (-PARL). +SPCN "
+                    "has no separate toggle: every device graph is shape-specialised"}
     return out
 
 

@@ -137,3 +137,12 @@ def test_tree_guard_failures():
     st, fail = gf.run(to_dev([kind, left, right, word, off, label]), dev, gf.new_workspace())
     assert st == I.ASSUMPTION_FAILED and fail["assumption_id"] == 8
     assert all(a.tobytes() == b.tobytes() for a, b in zip(to_host(dev), state))
+
+
+def test_tree_level_loops_on_one_cta(monkeypatch):
+    """The ablation's -PARL configuration (JANUS_TREE_GRID=1: every tile of a level on one CTA,
+    the backward streaming U^T) computes the same step."""
+    monkeypatch.setenv("JANUS_TREE_GRID", "1")
+    V, B = 50, 6
+    prog = pg.treelstm_program(V=V, E=24, H=32, C=2, B=B, lr=0.2)
+    _check(prog, [gen.sst_forest(gen.SEED_C3, 9, B, V, max_leaves=12)])
