@@ -343,13 +343,28 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
             gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream)
         ms_w = timed(lambda k: gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream), K) / K
         del ws_w
+        # the two layers one after the other (no layer wavefront forward or backward)
+        os.environ["JANUS_REC_WF"] = "0"
+        os.environ["JANUS_REC_BWD_WF"] = "0"
+        try:
+            gs2 = J.Graph(prog)
+            ws_s2 = gs2.new_workspace()
+            st_s2 = [s.clone() for s in state]
+            for k in range(3):
+                gs2.run(dev_batches[k % len(dev_batches)], st_s2, ws_s2, outs=[loss], stream=stream)
+            ms_s2 = timed(lambda k: gs2.run(dev_batches[k % len(dev_batches)], st_s2, ws_s2, outs=[loss],
+                                            stream=stream), K) / K
+            del ws_s2, gs2
+        finally:
+            del os.environ["JANUS_REC_WF"], os.environ["JANUS_REC_BWD_WF"]
         out["ablation_fig7"] = {
             "c2_samples_per_s": {"IMP": out["imperative"]["samples_per_s"], "BASE_while": B * 1000.0 / ms_w,
-                                 "UNRL": B * 1000.0 / ms_step},
+                                 "UNRL_layers_serial": B * 1000.0 / ms_s2, "UNRL": B * 1000.0 / ms_step},
             "c3_b25_sentences_per_s": c3_abl,
             "note": "IMP = janus_run_imperative (one launch per op, host-side control flow); BASE_while = "
                     "speculative graph with the loop as a device While (RANGE assumption); UNRL = unrolled "
-                    "graph (TRIP_COUNT); C3 graph_one_cta_per_level = the level loops on one CTA (-PARL). +SPCN "
+                    "graph (TRIP_COUNT); UNRL_layers_serial = the same without the two-layer wavefront (layer 1's "
+                    "recurrence after layer 0's, both directions); C3 graph_one_cta_per_level = the level loops on one CTA (-PARL). +SPCN "
                     "has no separate toggle: every device graph is shape-specialised"}
     return out
 
