@@ -135,7 +135,8 @@ bool lower_tree(Graph &g, std::string &why) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
   p.off.status = take(sizeof(DevStatus));
-  p.off.barriers = take(64 * sizeof(unsigned));
+  // 64 grid-barrier words, then one 128-B line per level: the forward's per-level arrival counters
+  p.off.barriers = take((64 + (size_t)TREE_MAX_LEVELS * 32) * sizeof(unsigned));
   p.off.stage_args = take((4ull * N + 2ull * (p.B + 1)) * sizeof(int));
   p.off.height = take((size_t)N * 4); p.off.order = take((size_t)N * 4); p.off.irank = take((size_t)N * 4);
   p.off.pslot = take((size_t)N * 4); p.off.tree_of = take((size_t)N * 4); p.off.pcount = take((size_t)N * 4);
@@ -270,7 +271,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     gd.kind = G_TREE; gd.id = p.tree_guard_id; gd.data = argp[0]; gd.n = N; gd.data2 = argp[4];
     gl.g[gl.n++] = gd;
   }
-  TCHK("init", launch_step_init(dst, bars, 64, st));
+  TCHK("init", launch_step_init(dst, bars, 64, st));  // (the forward zeroes its level counters)
   if (gl.n) TCHK("guards", launch_guards(gl, dst, st));
   if (p.tree_guard) TCHK("tree_guard", launch_tree_guard(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
   TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));

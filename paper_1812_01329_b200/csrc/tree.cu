@@ -580,6 +580,9 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
     for (int i = gt; i < nint; i += gs) t.stage_h[(size_t)i * d.P2 + 2 * H] = __float2bfloat16_rn(1.f);
     // the bias (4H floats) lives in shared memory for every epilogue of the launch
     for (int i = threadIdx.x; i < 4 * H; i += blockDim.x) sbias[i] = t.b[i];
+    // the per-level arrival counters (first used after the leaf level's grid barrier)
+    if (blockIdx.x == 0)
+      for (int l = threadIdx.x; l < TREE_MAX_LEVELS; l += blockDim.x) t.barrier[64 + l * 32] = 0;
   }
   fence_proxy_async_global();
   grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
@@ -634,8 +637,30 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   fence_proxy_async_global();
   grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
   // ---- internal levels: z = [h_l; h_r] U^T; c = i u + f_l c_l + f_r c_r; h = o tanh(c)
+  // Internal levels: only the CTAs with tiles at a level take part in it. A CTA waits for the
+  // previous level's workers (its arrival counter, one 128-B line per level) before its own tiles
+  // and then arrives on this level's counter — the chain of release/acquire pairs orders every
+  // earlier level too — instead of all CTAs meeting at a grid barrier per level.
+  unsigned int *lvl_ctr = t.barrier + 64;
+  const int ntn = (5 * H + 79) / 80;
+  auto workers = [&](int l) {
+    const int c = s.lvl_off[l + 1] - s.lvl_off[l];
+    return min((int)gridDim.x, ((c + 127) / 128) * ntn);
+  };
   for (int l = 1; l < L; ++l) {
     const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
+    if ((int)blockIdx.x >= workers(l)) continue;
+    if (l > 1) {
+      if (threadIdx.x == 0) {
+        const unsigned int target = (unsigned)workers(l - 1);
+        unsigned int v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(lvl_ctr + (l - 1) * 32) : "memory");
+        } while (v < target);
+      }
+      __syncthreads();
+      fence_proxy_async_global();
+    }
     tile_loop<80, true, NS>(rg, &mp.stage_h, &mp.u, r0, cnt, 5 * H, 2 * H, [&](int row, int col0) {
       const int u0 = col0 / 5, nu = min(16, H - u0);
       if (row >= 0 && nu > 0) {  // row metadata + children c into shared memory during the MMAs
@@ -702,7 +727,8 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
     }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1),
        t.dbg ? t.dbg + 2 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.stage_h32);
     fence_proxy_async_global();
-    grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(lvl_ctr + l * 32) : "memory");
   }
   tc_fence_before();
   __syncthreads();
