@@ -89,6 +89,12 @@ __global__ void gather_kernel(const float *__restrict__ E, int V, int Edim, cons
         *reinterpret_cast<__nv_bfloat162 *>(dst + k) = a;
         *reinterpret_cast<__nv_bfloat162 *>(dst + k + 2) = c;
       }
+    } else if ((Edim & 1) == 0) {  // e.g. E = 650: 8-B loads, 4-B stores, all issued before use
+#pragma unroll 4
+      for (int k = lane * 2; k < Edim; k += 64) {
+        const float2 v = *reinterpret_cast<const float2 *>(src + k);
+        *reinterpret_cast<__nv_bfloat162 *>(dst + k) = __floats2bfloat162_rn(v.x, v.y);
+      }
     } else {
       for (int k = lane; k < Edim; k += 32) dst[k] = __float2bfloat16_rn(src[k]);
     }
