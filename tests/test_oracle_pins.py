@@ -458,3 +458,32 @@ def test_runtime_error_commits_nothing():
     r = I.run_graph_step(prog, [tok, tok, np.array([2, 2], np.int32)], st)
     assert r.status == I.ERR_RUNTIME
     assert all(a.tobytes() == b.tobytes() for a, b in zip(r.state, st))
+
+
+def test_tree_program_batch_from_len_partial_minibatch():
+    """The TreeLSTM op list loops `for i < len(label)` (LEN, the whitelisted `len` of P:230): the
+    graph interpretation of a program written for B trees, run on a partial last minibatch of B-1
+    (P:314), equals the imperative program on the same forest — and a program whose loop bound
+    were the constant B would index past tree_off instead."""
+    V, B = 17, 5
+    prog = pg.treelstm_program(V=V, E=4, H=3, C=2, B=B, lr=0.3, speculate="none")
+    prog.assumptions = [a for a in prog.assumptions if a.kind != "SHAPE_MATCH"]   # any batch size
+    st = gen.uniform_params(prog, 7, 0.5)
+    f = list(gen.sst_forest(gen.SEED_C3, 3, B - 1, V, max_leaves=6))
+    g = I.run_graph_step(prog, f, st, mode="f32")
+    m = I.run_imperative_step(prog, f, st, mode="f32")
+    assert g.status == m.status == I.OK
+    assert abs(float(g.outputs[0]) - float(m.outputs[0])) <= 1e-6 * abs(float(m.outputs[0]))
+    for a, b in zip(g.state, m.state):
+        np.testing.assert_allclose(np.asarray(a, np.float64), np.asarray(b, np.float64), rtol=1e-5, atol=1e-7)
+    # the loop really ran over the 4 trees: the mean loss equals the mean of single-tree losses
+    offs = f[4]
+    per = []
+    for t in range(B - 1):
+        lo, hi = int(offs[t]), int(offs[t + 1])
+        sub = [np.asarray(x[lo:hi]) for x in f[:4]]
+        sub[1] = np.where(sub[0] == 1, sub[1] - lo, sub[1])
+        sub[2] = np.where(sub[0] == 1, sub[2] - lo, sub[2])
+        one = sub + [np.array([0, hi - lo], np.int32), np.asarray(f[5][t:t + 1])]
+        per.append(float(I.run_imperative_step(prog, one, st, mode="f32").outputs[0]))
+    assert abs(float(m.outputs[0]) - np.mean(per)) <= 1e-5 * abs(np.mean(per))
