@@ -46,14 +46,26 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- workloads
-def c2_program(B):
-    return pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=35, lr=1.0)
+def c2_program(B, speculate="unroll"):
+    """C2: the Figure 1 program with `if training: update` (training = 1, VALUE_EQ-speculated)."""
+    return pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=35, lr=1.0, speculate=speculate,
+                              max_T=35, training_flag=True)
+
+
+def c4_program(B):
+    """C4: the C2 model with data-dependent widths (device While, RANGE guard), SURVEY §8(d)."""
+    return pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=64, lr=1.0, speculate="while",
+                              training_flag=True)
 
 
 WORKLOADS = {
     "c2": dict(desc="C2 PTB-shaped LSTM LM: 2 layers, H=E=650, V=10000, T=35, B=64 per GPU, bf16 GEMM "
-                    "operands / fp32 accumulate, unrolled speculative graph (TRIP_COUNT=35)",
+                    "operands / fp32 accumulate, unrolled speculative graph (TRIP_COUNT=35, training "
+                    "flag speculated by VALUE_EQ)",
                B=64, T=35),
+    "c4": dict(desc="C4 variable-length RNN: the C2 model, per-batch width W ~ U{5..64}, ragged lengths "
+                    "U{1..W}, device While (RANGE guard), B=64 per GPU, bf16 / fp32 accumulate",
+               B=64, T=64),
 }
 
 
@@ -128,9 +140,9 @@ def _blas_threads():
 def oracle_sample(B, T):
     """Time the oracle (as it stands) on one bounded sample: B sequences x T tokens of the C2 model."""
     from oracle import interp as I
-    prog = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=T, lr=1.0)
+    prog = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=T, lr=1.0, training_flag=True)
     state = gen.uniform_params(prog, 1, 0.05)
-    args = list(gen.lm_batches(gen.SEED_C2, B, T, 10000, 1))[0]
+    args = list(list(gen.lm_batches(gen.SEED_C2, B, T, 10000, 1))[0]) + [np.ones(1, np.int32)]
     t0 = time.perf_counter()
     r = I.run_graph_step(prog, list(args), state)
     dt = time.perf_counter() - t0
@@ -175,6 +187,49 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- extra measurements
+def c4_extra(J, torch, stream, timed, K):
+    """C4 on one GPU: samples/s, valid tokens/s, padded fraction, and host syncs per step of the
+    graph path (1) against the imperative executor (one per control decision)."""
+    B = 64
+    prog = c4_program(B)
+    g = J.Graph(prog)
+    ws = g.new_workspace()
+    state = [torch.tensor(x, device="cuda") for x in gen.uniform_params(prog, 1, 0.05)]
+    one = np.ones(1, np.int32)
+    nb = 8
+    bs = [list(gen.c4_batch(gen.SEED_C4, k, B, 10000)) + [one] for k in range(nb)]
+    dev = [[torch.tensor(a, device="cuda") for a in b] for b in bs]
+    loss = torch.zeros(1, device="cuda")
+    for k in range(3):
+        g.run(dev[k], state, ws, outs=[loss], stream=stream)
+    Kc = max(nb, (K // nb) * nb)
+    c0 = g.counters()
+    ms = timed(lambda k: g.run(dev[k % nb], state, ws, outs=[loss], stream=stream), Kc) / Kc
+    c1 = g.counters()
+    valid = np.mean([int(b[2].sum()) for b in bs])
+    width = np.mean([b[0].shape[1] for b in bs])
+    st_i = [s.clone() for s in state]
+    ci0 = g.counters()
+    ms_i = timed(lambda k: g.run_imperative(dev[k], st_i, ws, outs=[loss], stream=stream), 2) / 2
+    ci1 = g.counters()
+    J.dev_profile(g, True)
+    timed(lambda k: g.run(dev[k % nb], state, ws, outs=[loss], stream=stream), nb)
+    ph = J.dev_phase_report(g)
+    J.dev_profile(g, False)
+    return {"samples_per_s": B * 1000.0 / ms, "valid_tokens_per_s": valid * 1000.0 / ms, "ms_per_step": ms,
+            "mean_width": float(width), "padded_fraction": float(1.0 - valid / (B * width)),
+            "graph_host_syncs_per_step": (c1["host_syncs"] - c0["host_syncs"]) / Kc,
+            "graph_launches_per_step": (c1["launches"] - c0["launches"]) / Kc,
+            "imperative_ms_per_step": ms_i,
+            "imperative_host_syncs_per_step": (ci1["host_syncs"] - ci0["host_syncs"]) / 2,
+            "imperative_launches_per_step": (ci1["launches"] - ci0["launches"]) / 2,
+            "phases_ms_per_step": {n: round(v[0] / nb, 4) for n, v in ph.items()},
+            "step_flop_frac_of_sustained": lm_flops_per_sample(10000, 650, 650, 2, 1) * valid /
+                                           (ms * 1e-3) / 1e12 / peaks().get("bf16_tflops_sustained", 1400.0),
+            "workload": "C4: C2 model, W ~ U{5..64}, lengths ~ U{1..W} (one row = W), B=64, seed 1815; "
+                        "8 batches cycled; FLOPs counted on valid tokens"}
+
+
 def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank, ms_step):
     """TreeLSTM (C3) throughput, the imperative baseline (Table 3 "Imp."), assertion overhead
     (strip_asserts A/B) and the C5 speculation-failure stress, all on this rank's GPU."""
@@ -233,27 +288,27 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         t0 = time.perf_counter()
         nv = 0
         for k in range(nb):
-            tok, tgt, ln = dev_batches[k % len(dev_batches)]
+            tok, tgt, ln, tr = dev_batches[k % len(dev_batches)]
             if viol[k]:
                 kind = kinds[nv % 4]
                 nv += 1
                 if kind == "dtype":
-                    a = [tok.long(), tgt, ln]
+                    a = [tok.long(), tgt, ln, tr]
                 elif kind == "shape":
-                    a = [tok[:B - 1].contiguous(), tgt[:B - 1].contiguous(), ln[:B - 1].contiguous()]
+                    a = [tok[:B - 1].contiguous(), tgt[:B - 1].contiguous(), ln[:B - 1].contiguous(), tr]
                 elif kind == "tag":
                     st5[tag_slot].zero_()
-                    a = [tok, tgt, ln]
+                    a = [tok, tgt, ln, tr]
                 else:
                     l2 = ln.clone(); l2[3] = T - 1
-                    a = [tok, tgt, l2]
+                    a = [tok, tgt, l2, tr]
                 ta = time.perf_counter()
                 s, f = g.run(a, st5, ws5, outs=[loss], stream=stream)
                 aborts[kind].append(1000 * (time.perf_counter() - ta))
                 if s == J.ASSUMPTION_FAILED:   # fallback to the imperative executor
                     fb[kind].append(J.STATUS_NAMES[g.run_imperative(a, st5, ws5, outs=[loss], stream=stream)])
             else:
-                g.run([tok, tgt, ln], st5, ws5, outs=[loss], stream=stream)
+                g.run([tok, tgt, ln, tr], st5, ws5, outs=[loss], stream=stream)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         out["c5_stress"] = {"batches": nb, "violations": int(viol.sum()),
@@ -271,20 +326,20 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         t0 = time.perf_counter()
         nv = 0
         for k in range(nb):
-            tok, tgt, ln = dev_batches[k % len(dev_batches)]
-            a = [tok, tgt, ln]
+            tok, tgt, ln, tr = dev_batches[k % len(dev_batches)]
+            a = [tok, tgt, ln, tr]
             if viol[k]:
                 kind = kinds[nv % 4]
                 nv += 1
                 if kind == "dtype":
-                    a = [tok.long(), tgt, ln]
+                    a = [tok.long(), tgt, ln, tr]
                 elif kind == "shape":
-                    a = [tok[:B - 1].contiguous(), tgt[:B - 1].contiguous(), ln[:B - 1].contiguous()]
+                    a = [tok[:B - 1].contiguous(), tgt[:B - 1].contiguous(), ln[:B - 1].contiguous(), tr]
                 elif kind == "tag":
                     st5[tag_slot].zero_()
                 else:
                     l2 = ln.clone(); l2[3] = T - 1
-                    a = [tok, tgt, l2]
+                    a = [tok, tgt, l2, tr]
             s, info = sess.step(a, st5, outs=[loss], stream=stream)
             paths[info["path"]] += 1
         torch.cuda.synchronize()
@@ -298,6 +353,8 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
                     "failures of one assumption (TRIP_COUNT -> device While, TYPE_TAG -> device Switch); "
                     "the first relaxed graph's build and workspace allocation are inside the timed loop"}
         del sess
+        # --- C4: data-dependent trip counts on the device (While + RANGE guard), SURVEY §8(d)
+        out["c4"] = c4_extra(J, torch, stream, timed, K)
         # --- C3 TreeLSTM
         for Bt in (25, 256):
             tp = pg.treelstm_program(V=20000, E=300, H=300, C=2, B=Bt, lr=0.05)
@@ -334,7 +391,7 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         # --- Figure 7 ablation on B200: samples/s of the same C2 batches through the
         # imperative executor (IMP), the graph with the loop kept as a device While (BASE: no
         # unrolling; +SPCN shapes and types still specialised) and the unrolled graph (+UNRL)
-        pw = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=T, lr=1.0, speculate="while", max_T=T)
+        pw = c2_program(B, speculate="while")
         gw = J.Graph(pw)
         ws_w = gw.new_workspace()
         st_w = [s.clone() for s in state]
@@ -396,16 +453,23 @@ def main():
 
     wl = WORKLOADS[args.workload]
     B, T = wl["B"], wl["T"]
-    prog = c2_program(B)
+    prog = c2_program(B) if args.workload == "c2" else c4_program(B)
     nccl_id = J.nccl_unique_id_bcast(rank, world) if world > 1 else None
     g = J.Graph(prog, world_size=world, rank=rank, nccl_id=nccl_id)
     assert g.device_path, g.build_message
     ws = g.new_workspace()
     state = [torch.tensor(x, device="cuda") for x in gen.uniform_params(prog, 1, 0.05)]
     n_batches = 8
-    batches = list(gen.lm_batches(gen.SEED_C2, B, T, 10000, n_batches, ranks=world))
-    dev_batches = [[torch.tensor(a[rank * B:(rank + 1) * B], device="cuda") for a in b] for b in batches]
-    host_batches = [[torch.tensor(a[rank * B:(rank + 1) * B]).pin_memory() for a in b] for b in batches]
+    one = np.ones(1, np.int32)   # training = 1 (the VALUE_EQ-speculated flag)
+    if args.workload == "c2":
+        batches = [[a[rank * B:(rank + 1) * B] for a in b] + [one]
+                   for b in gen.lm_batches(gen.SEED_C2, B, T, 10000, n_batches, ranks=world)]
+    else:   # every rank draws its own C4 batches (weak scaling)
+        batches = [list(gen.c4_batch(gen.SEED_C4, k * world + rank, B, 10000)) + [one] for k in range(n_batches)]
+    widths = [b[0].shape[1] for b in batches]
+    valid = [int(b[2].sum()) for b in batches]
+    dev_batches = [[torch.tensor(a, device="cuda") for a in b] for b in batches]
+    host_batches = [[torch.tensor(a).pin_memory() for a in b] for b in batches]
     loss_d = torch.zeros(1, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -449,7 +513,7 @@ def main():
         step(k, host=True, loss_out=loss_h)
     ms_e2e = timed(lambda k: step(k, host=True, loss_out=loss_h), args.steps)
     e2e = {"value": world * B * 1000.0 / (ms_e2e / args.steps), "unit": "samples/s",
-           "h2d_bytes_per_step": int(sum(a.numel() * 4 for a in host_batches[0])),
+           "h2d_bytes_per_step": int(np.mean([sum(a.numel() * 4 for a in hb) for hb in host_batches])),
            "d2h_bytes_per_step": 48}
 
     # per-phase device timing (separate pass of the same steps, CUDA events on the launch stream)
@@ -458,7 +522,8 @@ def main():
     phases = J.dev_phase_report(g)
     J.dev_profile(g, False)
     pk = peaks()
-    TB = B * T
+    T = float(np.mean([widths[k % n_batches] for k in range(args.steps)]))  # C2: 35; C4: mean width
+    TB = int(round(B * T))
     rows = []
     step_ms = sum(v[0] for v in phases.values()) / args.steps
     for name, (tot_ms, cnt) in phases.items():
@@ -510,7 +575,9 @@ def main():
                      "traffic": traffic("gemm_dec") if top[1] == "gemm_dec" else None,
                      "flops_per_launch": top[3], "avg_launch_ms": avg_ms, "peak_source": peak_src,
                      "share_of_step": top[0] / step_ms if step_ms else None}
-    flops = lm_flops_per_sample(10000, 650, 650, 2, T) * B
+    # algorithmic FLOPs of the step: per VALID token (C4's padded rows are work the method skips)
+    vtok = float(np.mean([valid[k % n_batches] for k in range(args.steps)]))
+    flops = lm_flops_per_sample(10000, 650, 650, 2, 1) * vtok
     out = {
         "metric": BASELINE_METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -518,7 +585,7 @@ def main():
         "config": {"workload": wl["desc"], "global_batch": B * world, "seq_len": T,
                    "parallelism": f"dp{world}",
                    "l2": "no flush: the step's working set (~340 MB workspace + 79 MB params) exceeds the 126 MB L2"},
-        "words_per_s": value * T,
+        "words_per_s": world * vtok * 1000.0 / ms_step,
         "step_tflops": flops * world / (ms_step * 1e-3) / 1e12 / world,
         "step_flop_frac_of_sustained": flops / (ms_step * 1e-3) / 1e12 / peak,
         "e2e": e2e, "gpu_launches": int(launches), "host_syncs_per_step": syncs,
@@ -526,8 +593,12 @@ def main():
         "phases_ms_per_step": {r[1]: round(r[0], 4) for r in rows},
         "paper_context": "JANUS LSTM (PTB, BS 20) 22.06k words/s on 1 TITAN Xp, fp32 (P:363) — other hardware/config",
     }
+    if args.workload == "c4":
+        out["c4"] = {"valid_tokens_per_s": world * vtok * 1000.0 / ms_step,
+                     "mean_width": T, "padded_fraction": 1.0 - vtok / (B * T),
+                     "host_syncs_per_step": syncs}
     out["clocks"] = clk.summary()
-    if not args.no_extras:
+    if not args.no_extras and args.workload == "c2":
         out.update(extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank, ms_step))
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()

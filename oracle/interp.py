@@ -611,9 +611,12 @@ def run_imperative_step(prog, args, state, mode="bf16"):
                  else np.asarray(s).astype(np.int64)) for k, s in enumerate(state)}
     sid = {s.name: k for k, s in enumerate(prog.slots)}
     writes = {}
+    update = True
     try:
         if model == "lstm_lm":
             loss = _imp_lstm_lm(prog, args, sv, sid, tape, P, writes)
+            if prog.meta.get("training_flag"):          # `if training:` around the update
+                update = int(np.asarray(args[3]).reshape(-1)[0]) != 0
         elif model == "treelstm":
             loss = _imp_treelstm(prog, args, sv, sid, tape, P)
         elif model == "running_sum":
@@ -637,7 +640,7 @@ def run_imperative_step(prog, args, state, mode="bf16"):
                       trace={"error": str(e)})
     effects = []
     grads = {}
-    params = [k for k, s in enumerate(prog.slots) if s.param]
+    params = [k for k, s in enumerate(prog.slots) if s.param] if update else []
     if params:
         g = tape.backward(loss)
         for k in params:
@@ -653,7 +656,7 @@ def run_imperative_step(prog, args, state, mode="bf16"):
 def _imp_lstm_lm(prog, args, sv, sid, tape, P, writes):
     m = prog.meta
     L = m["L"]
-    tok, tgt, lens = (np.asarray(a, np.int64) for a in args)
+    tok, tgt, lens = (np.asarray(a, np.int64) for a in args[:3])
     is_tensor = int(sv[sid["tag"]].data.reshape(-1)[0]) == 1
     h = [sv[sid[f"h{l}"]] if is_tensor else Val(np.zeros_like(sv[sid[f"h{l}"]].data)) for l in range(L)]
     c = [sv[sid[f"c{l}"]] if is_tensor else Val(np.zeros_like(sv[sid[f"c{l}"]].data)) for l in range(L)]

@@ -18,6 +18,10 @@ struct LmPlan {
   int T = 0;        // unrolled trip count (TRIP_COUNT) or maximum width W (While mode)
   bool while_mode = false;
   bool tag_specialised = false;  // TYPE_TAG assumed; otherwise the tag Switch runs on the device
+  // `if training:` around the optimizer update: argument index of the flag (-1 = no such branch);
+  // specialised by VALUE_EQ(training == 1), otherwise the commit reads the flag on the device
+  int train_arg = -1;
+  bool train_specialised = false;
   bool bf16 = true;              // tcgen05 path; false = single-CTA fp32 SIMT path
   // dtype of the index arguments (tokens, targets, lengths) fixed by DTYPE_EQ: JANUS_I32, or
   // JANUS_I64 (the type-specialised graph narrows them on the device first, as R10)
@@ -171,6 +175,9 @@ janus_status dp_agree(Graph &g, DevStatus *st_dev, long long *scratch, cudaStrea
 // a data-parallel rank whose DISPATCH guards failed still joins every collective (null step)
 janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,
                          janus_failure *fail);
+janus_status run_tree_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,
+                           janus_failure *fail);
+constexpr uint32_t NULL_STEP_INVALID_ARGS = 0xffffffffu;  // failure id of a rank with invalid arguments
 
 // one D2H of the status word + stream sync; decodes the failure (host_lm.cpp)
 janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_outs,

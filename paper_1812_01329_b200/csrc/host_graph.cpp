@@ -156,6 +156,16 @@ janus_status validate_graph(Graph &g, std::string &err) {
       err = buf;
       return JANUS_ERR_INVALID;
     }
+    if (a.id >= 0xffffu) {  // the data-parallel agreement packs the id into 16 bits
+      snprintf(buf, sizeof buf, "assumption id %u: ids must be < 65535", a.id);
+      err = buf;
+      return JANUS_ERR_INVALID;
+    }
+    if (a.kind == JA_SHAPE_MATCH && (a.ndim < 0 || a.ndim > 4)) {
+      snprintf(buf, sizeof buf, "assumption %u: SHAPE_MATCH ndim %d outside [0, 4]", a.id, a.ndim);
+      err = buf;
+      return JANUS_ERR_INVALID;
+    }
     if (a.mode == JANUS_MODE_DISPATCH && a.kind != JA_DTYPE_EQ && a.kind != JA_SHAPE_MATCH) {
       snprintf(buf, sizeof buf, "assumption %u: only DTYPE_EQ/SHAPE_MATCH are dispatch-checkable", a.id);
       err = buf;
@@ -304,13 +314,20 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
     g->ws_ready = workspace.data;
     return JANUS_OK;
   };
+  // data parallel: a rank that cannot run the step still joins its collectives (null step, the
+  // same sequence as a full step) so its peers cannot block; the failure reaches every rank
+  // through the agreement (reading Q12)
+  const bool dp_null = dp_enabled(*g) && (g->kind == "treelstm" || g->lm.bf16);
+  auto null_step = [&](const janus_failure &nf) -> janus_status {
+    janus_status r = ready();
+    if (r != JANUS_OK) return r;
+    return g->kind == "lstm_lm" ? run_lm_null(*g, nf, workspace, st, fail)
+                                : run_tree_null(*g, nf, workspace, st, fail);
+  };
   if (!check_dispatch(*g, args, n_args, &f)) {
     g->aborts++;
-    if (dp_enabled(*g) && g->kind == "lstm_lm" && g->lm.bf16) {
-      // data parallel: still join the step's collectives (null step) so peers cannot block
-      janus_status r = ready();
-      if (r != JANUS_OK) return r;
-      r = run_lm_null(*g, f, workspace, st, fail);
+    if (dp_null) {
+      const janus_status r = null_step(f);
       return r == JANUS_OK ? JANUS_ASSUMPTION_FAILED : r;
     }
     // cache miss: nothing is launched, nothing mutated
@@ -321,6 +338,12 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
   if (r != JANUS_OK) return r;
   if (g->kind == "lstm_lm") r = run_lm(*g, args, state, outs, n_outs, workspace, st, fail);
   else r = run_tree(*g, args, n_args, state, outs, n_outs, workspace, st, fail);
+  if (r == JANUS_ERR_INVALID && dp_null) {
+    // argument validation failed on this rank before any collective was issued
+    janus_failure nf{NULL_STEP_INVALID_ARGS, g->opts.rank, -1, -1};
+    const janus_status rn = null_step(nf);
+    return rn == JANUS_OK || rn == JANUS_ERR_RUNTIME ? JANUS_ERR_INVALID : rn;
+  }
   if (r == JANUS_ASSUMPTION_FAILED) g->aborts++;
   return r;
 }

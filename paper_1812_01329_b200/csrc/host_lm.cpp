@@ -107,7 +107,20 @@ bool lower_lm(Graph &g, std::string &why) {
     if (o.func != 0) continue;
     if (o.kind == JOP_OUTPUT && o.in_node[0] == xent && o.iattr[0] == 0) has_output = true;
     if (o.kind == JOP_SGD_APPLY) {
-      if (o.in_node[0] != xent) { why = "SGD of another loss"; return false; }
+      if (o.in_node[0] != xent) {
+        // `if training: update` (P:312 train / evaluate branch): SWITCH(loss, training[0]), arm 1
+        const janus_op &sw = g.ops[o.in_node[0]];
+        if (sw.kind != JOP_SWITCH || sw.in_node[0] != xent || o.in_port[0] != 1) { why = "SGD of another loss"; return false; }
+        const janus_op &el = g.ops[sw.in_node[1]];
+        const int ao = el.kind == JOP_ELEMENT ? producer_origin(g, el.in_node[0]) : -1;
+        const int ko = el.kind == JOP_ELEMENT ? producer_origin(g, el.in_node[1]) : -1;
+        if (ao < 0 || g.ops[ao].kind != JOP_ARG || g.ops[ao].iattr[0] != 3 || ko < 0 ||
+            g.ops[ko].kind != JOP_CONST || g.ops[ko].fattr[0] != 0.0) {
+          why = "update predicate is not training[0] (argument 3)";
+          return false;
+        }
+        p.train_arg = 3;
+      }
       const int s = (int)o.iattr[0];
       const float lr = (float)o.fattr[0];
       bool hit = false;
@@ -165,7 +178,18 @@ bool lower_lm(Graph &g, std::string &why) {
       if (a.dims[1] != -1 && width < 0) width = (int)a.dims[1];
     }
     if (a.kind == JA_TYPE_TAG && a.target == p.slot_tag && a.value == 1) p.tag_specialised = true;
+    // the training Switch with its value speculated (constant promotion): only the taken
+    // arm is kept and the VALUE_EQ AssertOp checks it
+    if (a.kind == JA_VALUE_EQ && a.mode == JANUS_MODE_RUNTIME && p.train_arg >= 0 && a.target == p.train_arg &&
+        a.value != 0)
+      p.train_specialised = true;
   }
+  for (const auto &a : g.asms)
+    if (a.mode == JANUS_MODE_RUNTIME && (a.kind == JA_VALUE_EQ || a.kind == JA_RANGE || a.kind == JA_TRIP_COUNT) &&
+        (a.target < 0 || a.target > (p.train_arg >= 0 ? 3 : 2))) {
+      why = "runtime assumption on an unknown argument";
+      return false;
+    }
   if (trip > 0) { p.T = trip; p.while_mode = false; }
   else if (width > 0) { p.T = width; p.while_mode = true; }
   else { why = "no TRIP_COUNT or bounded RANGE assumption on lengths"; return false; }
@@ -193,6 +217,10 @@ bool lower_lm(Graph &g, std::string &why) {
       }
   if ((int)p.runtime_guards.size() > MAX_GUARDS) { why = "too many runtime guards"; return false; }
   p.bf16 = g.opts.gemm_dtype != JANUS_F32;
+  if (!p.bf16 && p.train_arg >= 0 && !p.train_specialised) {
+    why = "fp32 single-CTA path: the training Switch must be speculated (VALUE_EQ)";
+    return false;
+  }
   if (g.opts.world_size > 1 && !p.bf16) { why = "fp32 path is single-GPU"; return false; }
   // ------------------------------------------------------------------ workspace layout
   size_t o = 0;
@@ -201,7 +229,7 @@ bool lower_lm(Graph &g, std::string &why) {
   p.nbar = rec_flag_words(256) * 8;  // per-CTA step flags: 256 CTAs x (L <= 4 layers) x 2 directions
   if ((p.H + 15) / 16 > 256) { why = "hidden size > 4096"; return false; }
   p.off.barriers = take(p.nbar * sizeof(unsigned));
-  p.off.stage_args = take(3ull * p.B * p.T * sizeof(int));
+  p.off.stage_args = take((3ull * p.B * p.T + 4) * sizeof(int));  // tokens, targets, lengths, training
   const int B = p.B, T = p.T, H = p.H, E = p.E, V = p.V, G4 = 4 * p.H;
   if (!p.bf16) {
     p.off.small_ws = take(small_lm_ws_floats(V, E, H, p.L, B, T) * sizeof(float));
@@ -263,11 +291,13 @@ bool lower_lm(Graph &g, std::string &why) {
   p.ws_bytes = o;
   char buf[512];
   snprintf(buf, sizeof buf,
-           "lstm_lm: L=%d V=%d E=%d H=%d B=%d %s=%d tag=%s path=%s guards=%zu "
+           "lstm_lm: L=%d V=%d E=%d H=%d B=%d %s=%d tag=%s train=%s path=%s guards=%zu "
            "phases=[init,%sguards,cast,gather,{gemm_in,rec_fwd}xL,gemm_dec,xent,gemm_dWdec,"
            "gemm_dh,{rec_bwd,gemm_dWhh,gemm_dWih,gemm_dx}xL,embed_grad,finalize,commit]",
            p.L, p.V, p.E, p.H, p.B, p.while_mode ? "while_width" : "unrolled_T", p.T,
-           p.tag_specialised ? "specialised" : "device_switch", p.bf16 ? "tcgen05_bf16" : "fp32_single_cta",
+           p.tag_specialised ? "specialised" : "device_switch",
+           p.train_arg < 0 ? "none" : p.train_specialised ? "specialised" : "device_switch",
+           p.bf16 ? "tcgen05_bf16" : "fp32_single_cta",
            p.runtime_guards.size(), p.while_mode ? "trip," : "");
   g.describe = buf;
   return true;
@@ -362,7 +392,16 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   const int Wd = (int)args[0].shape[1];
   if (args[0].ndim != 2 || args[0].shape[0] != B || Wd > p.T || (!p.while_mode && Wd != p.T))
     return JANUS_ERR_INVALID;
-  const int *argp[3];
+  const int *argp[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (p.train_arg >= 0) {  // training flag i32[1]
+    if (!tensor_ok(args[3], JANUS_I32, 1)) return JANUS_ERR_INVALID;
+    if (is_device_ptr(args[3].data)) argp[3] = static_cast<const int *>(args[3].data);
+    else {
+      int *dstp = reinterpret_cast<int *>(W + p.off.stage_args) + (size_t)3 * B * p.T;
+      if (cudaMemcpyAsync(dstp, args[3].data, 4, cudaMemcpyHostToDevice, st) != cudaSuccess) return JANUS_ERR_CUDA;
+      argp[3] = dstp;
+    }
+  }
   for (int a = 0; a < 3; ++a) {
     const int64_t n = a < 2 ? (int64_t)B * Wd : B;
     if (!tensor_ok(args[a], p.arg_dtype[a], n)) return JANUS_ERR_INVALID;
@@ -665,6 +704,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     if (p.lr_E != 0 && g.nccl) { s = {}; s.kind = C_DENSE; s.dst = P.E; s.grad = fp(p.off.dEd); s.rows = V; s.cols = E; s.ldg = E; s.lr = p.lr_E / nr; add(s); }
     if (p.write_tag && P.tag) { s = {}; s.kind = C_TAG; s.idst = P.tag; s.ival = 1; add(s); }
   }
+  if (p.train_arg >= 0 && !p.train_specialised)  // the training Switch evaluated on the device
+    for (int k = 0; k < cl.n; ++k)
+      if (cl.s[k].kind != C_COPY && cl.s[k].kind != C_TAG) cl.s[k].pred = argp[3];
   LCHK("commit", launch_commit(cl, dst, st));
   return finish(g, dst, outs, n_outs, st, fail);
 }
@@ -679,7 +721,8 @@ namespace jk {
 janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,
                          janus_failure *fail) {
   const LmPlan &p = g.lm;
-  if (!ws.data || !p.bf16) return JANUS_ERR_INVALID;
+  if (!ws.data || !p.bf16 || (size_t)ws.shape[0] * (ws.dtype == JANUS_U8 ? 1 : 4) < p.ws_bytes)
+    return JANUS_ERR_INVALID;
   janus_status r = dp_init(g);
   if (r != JANUS_OK) return r;
   uint8_t *W = static_cast<uint8_t *>(ws.data);

@@ -175,6 +175,22 @@ std::vector<janus_assumption> specialise(const std::vector<janus_assumption> &ba
       v.erase(p);
     }
   }
+  // A dim joined to '?' makes the batch width vary, so an exact trip count cannot hold for every
+  // key the joined graph serves: the loop is relaxed with it (TRIP_COUNT -> RANGE [1, n], a
+  // bounded device While, Figure 4 one level up) instead of staying unrolled to the old width.
+  bool widened = false;
+  for (const auto &a : v)
+    if (a.kind == JA_SHAPE_MATCH)
+      for (const auto &b0 : base)
+        if (b0.id == a.id)
+          for (int k = 0; k < a.ndim && k < 4; ++k) widened |= a.dims[k] < 0 && b0.dims[k] >= 0;
+  if (join && widened)
+    for (auto &a : v)
+      if (a.kind == JA_TRIP_COUNT) {
+        janus_assumption o{};
+        int32_t dropped = 0;
+        if (janus_relax(&a, nullptr, &o, &dropped) == JANUS_OK && !dropped) a = o;
+      }
   return v;
 }
 
@@ -315,20 +331,24 @@ janus_status janus_session_step(janus_session *s, const janus_tensor *args, int3
       int base = -1;
       for (int i = 0; i < (int)s->entries.size() && base < 0; ++i)
         if (s->entries[i].active) base = i;
-      for (const auto &x : s->entries[base].asms)
+      // every entry may have been evicted (cache_max): specialise the initial assumptions, whose
+      // record is kept after retirement
+      const std::vector<janus_assumption> base_asms = s->entries[base >= 0 ? base : 0].asms;
+      for (const auto &x : base_asms)
         if (x.id == miss.assumption_id) a = &x;
       if (a && a->target >= 0 && a->target < n_args &&
           ++s->miss_count[key_of(miss, args[a->target])] >= s->threshold) {
         bool dt = false;
-        const std::vector<janus_assumption> base_asms = s->entries[base].asms;
         std::vector<janus_assumption> joined = specialise(base_asms, args, n_args, true, &dt);
         int id = -1;
         if (!dt) {
-          // shapes only: the Figure 4 join covers both keys and replaces the old entry when the
-          // joined graph keeps its device program
+          // shapes only: the Figure 4 join ("(4,8) and (3,8)" -> "(?,8)") generates
+          // another graph that serves the new key; the older, more specialised entry stays in
+          // front of it in dispatch order and keeps serving its own key (it is never retired on
+          // the assumption that the joined plan can run it). A joined graph without a device
+          // program is dropped in favour of an exact-key graph.
           id = s->build(joined, "miss-join");
-          if (id >= 0 && s->entries[id].device) s->retire(s->entries[base]);
-          else if (id >= 0) { s->retire(s->entries[id]); id = -1; }
+          if (id >= 0 && !s->entries[id].device) { s->retire(s->entries[id]); id = -1; }
         }
         if (id < 0) id = s->build(specialise(base_asms, args, n_args, false, &dt), "miss-key");
         info->generated = id;
@@ -356,9 +376,9 @@ janus_status janus_session_step(janus_session *s, const janus_tensor *args, int3
     return r;
   }
   if (r == JANUS_ERR_INVALID || r == JANUS_ERR_UNSUPPORTED) {
-    // the device program cannot take these arguments (e.g. a joined '?' dim it does not
-    // support at this size): nothing ran; the entry keeps serving through the imperative path
-    e.device = false;
+    // the device program cannot take THESE arguments (e.g. a joined '?' dim beyond the width it
+    // was lowered for): nothing ran; this call is served imperatively, the entry keeps its
+    // device program for the keys it can run
     info->event = JANUS_EV_IMPERATIVE_ENTRY;
     return imperative(e.g);
   }

@@ -127,6 +127,7 @@ bool lower_tree(Graph &g, std::string &why) {
         p.runtime_guards.push_back(r);
       }
   if (g.opts.strip_asserts) p.tree_guard = false;
+  if ((int)p.runtime_guards.size() + (p.tree_guard ? 1 : 0) > MAX_GUARDS) { why = "too many runtime guards"; return false; }
   p.max_N = p.max_nodes * p.B;
   // ------------------------------------------------------------------ workspace layout
   const int N = p.max_N, H = p.H, E = p.E, V = p.V;
@@ -323,6 +324,28 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   if (p.lr_bc != 0) { sg = {}; sg.kind = C_DENSE; sg.dst = bc; sg.grad = fp(p.off.gbc); sg.rows = 1; sg.cols = p.C; sg.ldg = p.C; sg.lr = p.lr_bc / nr; add(sg); }
   TCHK("commit", launch_commit(cl, dst, st));
   return finish(g, dst, outs, n_outs, st, fail);
+}
+
+// Null step of a data-parallel TreeLSTM rank whose DISPATCH guards failed or whose arguments were
+// invalid: no compute, but the same collective sequence as a full step (arena allreduce, then the
+// agreement), so its peers cannot block; its failure reaches every rank through the agreement.
+janus_status run_tree_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,
+                           janus_failure *fail) {
+  const TreePlan &p = g.tree;
+  if (!ws.data || (size_t)ws.shape[0] * (ws.dtype == JANUS_U8 ? 1 : 4) < p.ws_bytes) return JANUS_ERR_INVALID;
+  janus_status r = dp_init(g);
+  if (r != JANUS_OK) return r;
+  uint8_t *W = static_cast<uint8_t *>(ws.data);
+  DevStatus *dst = reinterpret_cast<DevStatus *>(W + p.off.status);
+  unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
+  TCHK("init", launch_step_init(dst, bars, 64, st));
+  TCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
+  r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + p.off.arena_begin),
+                       (p.off.arena_end - p.off.arena_begin) / 4, st);
+  if (r != JANUS_OK) return r;
+  r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
+  if (r != JANUS_OK) return r;
+  return finish(g, dst, nullptr, 0, st, fail);
 }
 
 }  // namespace jk

@@ -196,6 +196,7 @@ struct FwdCtx {
   int nflagsB;
   const float *bias;             // gate-interleaved bias (z init) when G is not pre-filled
   int cta;                       // CTA index within the layer
+  int upcA, upcB;                // units per producer CTA of run A / run B (chunk -> flags)
 };
 
 JN_DEV void wait_flag_set(const unsigned int *flags, int n, unsigned int v) {
@@ -208,14 +209,55 @@ JN_DEV void wait_flag_set(const unsigned int *flags, int n, unsigned int v) {
   }
 }
 
+// tcgen05.ld .16x32bx2: lanes 0-15 of the warp's TMEM quadrant; threads 0-15 read N columns from
+// taddr, threads 16-31 the N columns from taddr + N (both halves of an M = 64 accumulator row).
+template <int N>
+JN_DEV void tmem_ld_16x2(uint32_t taddr, uint32_t (&r)[N]) {
+  static_assert(N == 16 || N == 32, "tmem_ld_16x2");
+  if constexpr (N == 32) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31}, [%32], 32;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+  } else {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16], 16;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+  }
+}
+
+// Producer warp: wait (every lane polls a share, acquire loads) until flags[p0, p1) >= v.
+JN_DEV void wait_flags_acq(const unsigned int *flags, int p0, int p1, unsigned int v) {
+  for (int c = p0 + (int)(threadIdx.x & 31); c < p1; c += 32) {
+    unsigned x;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
+    } while (x < v);
+  }
+  __syncwarp();  // bar.warp.sync orders every lane's acquire before lane 0's copy issue
+}
+
 // M64 (B <= 64): M = 64 MMAs — half the A-operand shared-memory reads of M = 128, whose upper 64
-// rows would be padding. The accumulator row i then sits in TMEM lane (i % 16) + 32 (i / 16):
-// epilogue warp w, lanes 0-15 own batch rows 16 w .. 16 w + 15.
+// rows would be padding. The accumulator row i then sits in TMEM lane (i % 16) + 32 (i / 16);
+// .16x32bx2 loads give epilogue warp w's lanes 0-15 AND 16-31 batch rows 16 w .. 16 w + 15, the
+// low and high half of the CTA's units respectively (all 128 epilogue threads busy).
 template <int UPC, bool MASKED, bool M64>
 JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMap *tmWb,
                      const RecLayout &ly) {
   constexpr int NG = 4 * UPC;           // gate rows / MMA N / TMEM columns per accumulator
   constexpr int WCH = NG * 128;         // bytes per weight chunk
+  constexpr int UH = M64 ? UPC / 2 : UPC;  // units per epilogue thread
+  constexpr int GH = 4 * UH;               // gate columns per epilogue thread
   const RecFwdArgs &a = cx.a;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -231,8 +273,9 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // batch row owned in the epilogue (warps 0-3)
-  const int b = M64 ? (lane < 16 ? 16 * warp + lane : (1 << 20)) : (int)threadIdx.x;
+  // batch row owned in the epilogue (warps 0-3) and the first of its UH units within the CTA
+  const int b = M64 ? 16 * warp + (lane & 15) : (int)threadIdx.x;
+  const int uoff = M64 ? (lane >> 4) * UH : 0;
   const int u0 = cx.cta * UPC;
   const int B = a.B, H = a.H;
   const int nkh = (H + 63) / 64;             // chunks of one h block
@@ -262,13 +305,13 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
     }
   }
   // initial state -> registers, row block 0 of Hs / Cs and exchange block 0
-  float hreg[UPC], creg[UPC];
+  float hreg[UH], creg[UH];
   const bool row = warp < 4 && b < B;
   // `state = self.state` or zeros when it is still None: Switch/Merge on the device
   const bool is_tensor = a.tag == nullptr || *a.tag == 1;
 #pragma unroll
-  for (int u = 0; u < UPC; ++u) {
-    const int gu = u0 + u;
+  for (int u = 0; u < UH; ++u) {
+    const int gu = u0 + uoff + u;
     hreg[u] = (row && gu < H && is_tensor) ? a.h0[(size_t)b * H + gu] : 0.f;
     creg[u] = (row && gu < H && is_tensor) ? a.c0[(size_t)b * H + gu] : 0.f;
     if (row && gu < H) {
@@ -278,18 +321,25 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   }
   uint8_t *hsw = reinterpret_cast<uint8_t *>(a.Hsw);
   const uint8_t *hswA = reinterpret_cast<const uint8_t *>(cx.hswA);
-  // exchange copy: this CTA's UPC units of row b = UPC / 8 granules of chunk u0 / 64
+  // exchange copy: this thread's UH units of row b (UH * 2 bytes, 16-B granule aligned for UH = 8,
+  // half a granule for UH = 4) at its swizzled position in chunk (u0 + uoff) / 64
   auto write_x = [&](int blk, const __nv_bfloat16 *hb) {
-    uint8_t *chunk = hsw + ((size_t)blk * nkh + (u0 >> 6)) * ly.cb;
-    const uint32_t g0 = (uint32_t)(u0 & 63) >> 3;
+    const int uc = u0 + uoff;
+    uint8_t *chunk = hsw + ((size_t)blk * nkh + (uc >> 6)) * ly.cb;
+    const uint32_t g0 = (uint32_t)(uc & 63) >> 3;
+    if constexpr (UH % 8 == 0) {
 #pragma unroll
-    for (int q = 0; q < UPC / 8; ++q)
-      *reinterpret_cast<uint4 *>(chunk + sw128_off(b, g0 + q)) = reinterpret_cast<const uint4 *>(hb)[q];
+      for (int q = 0; q < UH / 8; ++q)
+        *reinterpret_cast<uint4 *>(chunk + sw128_off(b, g0 + q)) = reinterpret_cast<const uint4 *>(hb)[q];
+    } else {
+      static_assert(UH == 4, "write_x");
+      *reinterpret_cast<uint2 *>(chunk + sw128_off(b, g0) + (uc & 7) * 2) = *reinterpret_cast<const uint2 *>(hb);
+    }
   };
   if (row) {
-    __align__(16) __nv_bfloat16 h0b[UPC];
+    __align__(16) __nv_bfloat16 h0b[UH];
 #pragma unroll
-    for (int u = 0; u < UPC; ++u) h0b[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
+    for (int u = 0; u < UH; ++u) h0b[u] = __float2bfloat16_rn(uoff + u < nu ? hreg[u] : 0.f);
     write_x(0, h0b);
   }
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
@@ -304,29 +354,29 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   for (int t = 0; t < T; ++t) {
     if (warp == 4) {
       if (threadIdx.x == 128) PROBE(t, 0);
-      // run A's producers (h_{t-1} of this layer, or h_t of the layer below) -> run A's ops; then
-      // run B's (this layer's h_{t-1}) -> run B's ops. In the wavefront, run A (the layer below,
-      // which runs ahead) is usually ready first, so its MMAs overlap the wait for run B.
+      // op by op: wait only for the producers of the op's chunks, then issue its copy, so the
+      // early chunks' copies and MMAs overlap the arrival of the later producers. Run A = h_{t-1}
+      // of this layer (or h_t of the layer below, which runs ahead), run B = this layer's h_{t-1}.
       const uint8_t *srcA = hswA + (size_t)(t + cx.blkA_off) * nkh * ly.cb;
       const uint8_t *srcB = hsw + (size_t)t * nkh * ly.cb;
-      wait_flag_set(cx.flagsA, cx.nflagsA, (unsigned)(t + 1 + cx.blkA_off));
-      __syncwarp();
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      fence_proxy_async_global();
-      if (threadIdx.x == 128) {
-        PROBE(t, 1);
-        issue_step(srcA, srcB, ly, sA, full, empty, t, 0, ops_a(ly));
-      }
-      __syncwarp();
-      if (cx.flagsB) {
-        wait_flag_set(cx.flagsB, cx.nflagsB, (unsigned)t + 1);
+      for (int k = 0; k < ly.nops; ++k) {
+        int first, nch;
+        op_range(ly, k, first, nch);
+        const bool run_a = first < ly.nka;
+        const int upc = run_a ? cx.upcA : cx.upcB;
+        const int c0 = (run_a ? first : first - ly.nka) * 64;  // first unit of the op
+        const int p0 = c0 / upc;
+        const int p1 = min(run_a ? cx.nflagsA : cx.nflagsB, (c0 + 64 * nch + upc - 1) / upc);
+        wait_flags_acq(run_a ? cx.flagsA : cx.flagsB, p0, p1,
+                       run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1);
+        if (threadIdx.x == 128) {
+          if (k == 0) PROBE(t, 1);
+          fence_proxy_async_global();  // generic-proxy writes of the producers -> async-proxy reads
+          issue_step(srcA, srcB, ly, sA, full, empty, t, k, k + 1);
+        }
         __syncwarp();
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        fence_proxy_async_global();
-        if (threadIdx.x == 128) issue_step(srcA, srcB, ly, sA, full, empty, t, ops_a(ly));
       }
       if (threadIdx.x == 128) PROBE(t, 2);
-      __syncwarp();
     } else if (warp >= 5) {
       if ((threadIdx.x & 31) == 0) {
         mma_step<NG>(ly, sA, sW, WCH, full, empty, tfull, tempty, tmem, idesc, t, warp - 5,
@@ -338,14 +388,14 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       // input projection of this step (independent of h_{t-1}): load while the MMA runs. G rows
       // are padded to whole 64-column groups, so every CTA moves whole rows; padding units
       // compute junk that is never published (hb = 0 there)
-      float z[NG];
-      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * ldg + (size_t)NG * cx.cta;
+      float z[GH];
+      float *g = a.G + (size_t)(t * B + (row ? b : 0)) * ldg + (size_t)NG * cx.cta + 4 * uoff;
       if (cx.bias) {
 #pragma unroll
-        for (int q = 0; q < NG; ++q) z[q] = cx.bias[min(NG * cx.cta + q, 4 * H - 1)];
+        for (int q = 0; q < GH; ++q) z[q] = cx.bias[min(NG * cx.cta + 4 * uoff + q, 4 * H - 1)];
       } else {
 #pragma unroll
-        for (int q = 0; q < NG / 4; ++q) {
+        for (int q = 0; q < GH / 4; ++q) {
           const float4 x = row ? reinterpret_cast<const float4 *>(g)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
           z[4 * q] = x.x; z[4 * q + 1] = x.y; z[4 * q + 2] = x.z; z[4 * q + 3] = x.w;
         }
@@ -357,28 +407,37 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       {
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
         for (int w = 0; w < nacc; ++w) {  // an accumulator's loads in flight together, one wait
-          uint32_t v[NG / 32][32];
+          if constexpr (M64) {
+            uint32_t v[GH];
+            tmem_ld_16x2<GH>(ta + w * NG, v);
+            tmem_ld_wait();
+            tmem_pin(v);
 #pragma unroll
-          for (int h = 0; h < NG / 32; ++h) tmem_ld32_nw(ta + w * NG + 32 * h, v[h]);
-          tmem_ld_wait();
+            for (int i = 0; i < GH; ++i) z[i] += __uint_as_float(v[i]);
+          } else {
+            uint32_t v[NG / 32][32];
 #pragma unroll
-          for (int h = 0; h < NG / 32; ++h)
+            for (int h = 0; h < NG / 32; ++h) tmem_ld32_nw(ta + w * NG + 32 * h, v[h]);
+            tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) z[32 * h + i] += __uint_as_float(v[h][i]);
+            for (int h = 0; h < NG / 32; ++h)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) z[32 * h + i] += __uint_as_float(v[h][i]);
+          }
         }
       }
       epi_tmem_release(tempty);
       const bool valid = !MASKED || t < len_b;
-      __align__(16) __nv_bfloat16 hb[UPC];
+      __align__(16) __nv_bfloat16 hb[UH];
 #pragma unroll
-      for (int u = 0; u < UPC; ++u) {
+      for (int u = 0; u < UH; ++u) {
         const float ig = sig_f(z[4 * u]), fg = sig_f(z[4 * u + 1]);
         const float gg = tanh_f(z[4 * u + 2]), og = sig_f(z[4 * u + 3]);
         const float c2 = fg * creg[u] + ig * gg;
         const float h2 = og * tanh_f(c2);
         z[4 * u] = ig; z[4 * u + 1] = fg; z[4 * u + 2] = gg; z[4 * u + 3] = og;
         if (valid) { creg[u] = c2; hreg[u] = h2; }
-        hb[u] = __float2bfloat16_rn(u < nu ? hreg[u] : 0.f);
+        hb[u] = __float2bfloat16_rn(uoff + u < nu ? hreg[u] : 0.f);
       }
       // critical path first: the exchange copy of h_t, then the step flag; the rest after
       if (row) write_x(t + 1, hb);
@@ -387,29 +446,33 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       epi_publish(&flags[cx.cta * REC_FS], (unsigned)t + 2);
       if (threadIdx.x == 0) PROBE(t, 7);
       if (row) {
-        const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0;
+        const size_t ro = (size_t)((t + 1) * B + b) * a.ldh + u0 + uoff;
 #pragma unroll
-        for (int q = 0; q < NG / 4; ++q)
+        for (int q = 0; q < GH / 4; ++q)
           reinterpret_cast<float4 *>(g)[q] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
         float4 *cd = reinterpret_cast<float4 *>(a.Cs + ro);  // ldh >= 64 * ceil(H / 64)
 #pragma unroll
-        for (int q = 0; q < UPC / 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
+        for (int q = 0; q < UH / 4; ++q) cd[q] = make_float4(creg[4 * q], creg[4 * q + 1], creg[4 * q + 2], creg[4 * q + 3]);
 #pragma unroll
-        for (int u = 0; u < UPC; ++u)  // column H of Hs is the GEMMs' ones column
-          if (u == nu) hb[u] = __float2bfloat16_rn(1.f);
-        uint4 *hd = reinterpret_cast<uint4 *>(a.Hs + ro);
+        for (int u = 0; u < UH; ++u)  // column H of Hs is the GEMMs' ones column
+          if (uoff + u == nu) hb[u] = __float2bfloat16_rn(1.f);
+        if constexpr (UH % 8 == 0) {
+          uint4 *hd = reinterpret_cast<uint4 *>(a.Hs + ro);
 #pragma unroll
-        for (int q = 0; q < UPC / 8; ++q) hd[q] = reinterpret_cast<const uint4 *>(hb)[q];
+          for (int q = 0; q < UH / 8; ++q) hd[q] = reinterpret_cast<const uint4 *>(hb)[q];
+        } else {
+          *reinterpret_cast<uint2 *>(a.Hs + ro) = *reinterpret_cast<const uint2 *>(hb);
+        }
       }
     }
   }
   // final state (committed by the commit phase only if every assumption held)
   if (row) {
 #pragma unroll
-    for (int u = 0; u < UPC; ++u)
-      if (u < nu) {
-        a.hT[(size_t)b * H + u0 + u] = hreg[u];
-        a.cT[(size_t)b * H + u0 + u] = creg[u];
+    for (int u = 0; u < UH; ++u)
+      if (uoff + u < nu) {
+        a.hT[(size_t)b * H + u0 + uoff + u] = hreg[u];
+        a.cT[(size_t)b * H + u0 + uoff + u] = creg[u];
       }
   }
   tc_fence_before();
@@ -1031,6 +1094,7 @@ cudaError_t lstm_rec_fwd(const RecFwdArgs &a, const __nv_bfloat16 *Whh, int ldw,
   cx.blkA_off = 0;
   cx.flagsA = a.barrier;
   cx.nflagsA = rec_grid(a.H);
+  cx.upcA = cx.upcB = REC_UPC;
   void *args[] = {&tmW, &cx, &ly};
   return coop_launch(fn, rec_grid(a.H), smem, args, st);
 }
@@ -1071,6 +1135,9 @@ cudaError_t lstm_rec_fwd_wavefront(const RecFwdArgs &a0, const RecFwdArgs &a1, c
   c1.flagsB = a1.barrier;
   c1.nflagsB = g1;
   c1.bias = bias1_il;
+  c0.upcA = c0.upcB = REC_UPC;
+  c1.upcA = REC_UPC;       // run A: layer 0's CTAs
+  c1.upcB = REC_UPC / 2;   // run B: layer 1's CTAs
   int g0_ = g0;
   void *args[] = {&tm0, &tmi, &tmh, &c0, &c1, &ly0, &ly1, &g0_};
   return coop_launch(fn, g0 + g1, smem, args, st);

@@ -788,6 +788,12 @@ cudaError_t launch_dp_unpack(DevStatus *st, const long long *scratch, cudaStream
   return cudaGetLastError();
 }
 __global__ void set_failure_kernel(DevStatus *st, unsigned id, long long index, long long observed) {
+  if (id == 0xffffffffu) {  // invalid arguments on this rank: agreed as a runtime error (no commit)
+    st->key = KEY_PASS;
+    st->runtime_err = 1;
+    st->status = 4;
+    return;
+  }
   const unsigned long long idx = index < 0 ? (1ull << IDX_BITS) - 1 : (unsigned long long)index;
   st->key = ((unsigned long long)id << IDX_BITS) | idx;
   st->observed = observed;
@@ -825,6 +831,7 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
   pdl_enter();
   if (st->status != 0) return;
   const CommitSeg sg = cl.s[blockIdx.y];
+  if (sg.pred && *sg.pred == 0) return;
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   switch (sg.kind) {

@@ -104,7 +104,8 @@ cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl,
 cudaError_t launch_dp_pack(const DevStatus *st, long long *scratch, int rank, cudaStream_t s);
 cudaError_t launch_dp_observed(const DevStatus *st, long long *scratch, cudaStream_t s);
 cudaError_t launch_dp_unpack(DevStatus *st, const long long *scratch, cudaStream_t s);
-// a dispatch failure on this rank inside a data-parallel null step
+// a dispatch failure on this rank inside a data-parallel null step (id 0xffffffff: this rank's
+// arguments were invalid; it joins the agreement as a runtime error)
 cudaError_t launch_set_failure(DevStatus *st, unsigned id, long long index, long long observed,
                                cudaStream_t s);
 // dense embedding gradient for the data-parallel allreduce: zero + scatter the segment sums
@@ -130,6 +131,7 @@ struct CommitSeg {
   int ng;              // C_DENSE_IL: gates per unit (0 = 4)
   const float *grad2;  // C_TREE_BIAS: leaf wgrad (bias column col2, pitch ldg2)
   int ldg2, col2;
+  const int *pred;     // device predicate (`if training:` Switch): skip the segment when *pred == 0
 };
 constexpr int MAX_COMMIT = 24;
 struct CommitList {

@@ -126,7 +126,8 @@ def lstm_lm_slots(V, E, H, L, B):
     return slots
 
 
-def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", max_T=None):
+def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", max_T=None,
+                    training_flag=False):
     """Generic graph of one truncated-BPTT step of the Figure 1 RNN model:
 
         state = self.state (zeros if it is still None)          # attribute read, P:266 (1)
@@ -136,7 +137,10 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
         self.state = state                                      # deferred write, P:266 (2),(4)
         loss = compute_loss(outputs); optimizer update           # P:154 inserted updates
 
-    Arguments: 0 tokens i32[B,W], 1 targets i32[B,W], 2 lengths i32[B].
+    Arguments: 0 tokens i32[B,W], 1 targets i32[B,W], 2 lengths i32[B]; with training_flag also
+    3 training i32[1]: the optimizer update runs only `if training:` (the train / evaluate branch
+    of P:312), speculated on its profiled value (constant promotion) by a RUNTIME VALUE_EQ
+    assumption (id 8): the single taken arm is kept and asserted.
     speculate: "unroll" — fixed trip count T (C1/C2: TRIP_COUNT assumption, unrolled graph);
                "while"  — variable trip count (C4: device-resident While, RANGE assumption);
                "none"   — no RUNTIME assumptions (imperative path only).
@@ -204,9 +208,14 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     logits = g.op("LINEAR", [outs, rd["W_dec"], rd["b_dec"]])
     loss = g.op("SOFTMAX_XENT", [logits, tgt_tm, mask])
     g.op("OUTPUT", [loss], i=[0])
+    upd = loss
+    if training_flag:                        # if training: optimizer.apply(...)  (Switch)
+        train = g.op("ARG", i=[3])
+        pred = g.op("ELEMENT", [train, zero])
+        upd = (g.op("SWITCH", [loss, pred]), 1)
     for s in slots:
         if s.param:
-            g.op("SGD_APPLY", [loss], i=[sid[s.name], g.effect_seq()], f=[lr])
+            g.op("SGD_APPLY", [upd], i=[sid[s.name], g.effect_seq()], f=[lr])
     for nm in init:
         g.op("STATE_WRITE", [x_state[nm]], i=[sid[nm], g.effect_seq()])
     g.op("STATE_WRITE", [tag_tensor], i=[sid["tag"], g.effect_seq()])
@@ -231,9 +240,14 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     elif speculate != "none":
         raise ValueError(speculate)
     args = [("tokens", I32, (B, T)), ("targets", I32, (B, T)), ("lengths", I32, (B,))]
+    if training_flag:
+        args.append(("training", I32, (1,)))
+        if speculate != "none":
+            asms += [Assumption(8, "VALUE_EQ", RUNTIME, 3, value=1),
+                     Assumption(9, "DTYPE_EQ", DISPATCH, 3, dtype=I32)]
     return Program(f"lstm_lm_L{L}_H{H}", g.ops, asms, slots, args, 1, lr,
                    meta=dict(model="lstm_lm", V=V, E=E, H=H, L=L, B=B, T=T, W=W, gemm=gemm,
-                             speculate=speculate))
+                             speculate=speculate, training_flag=training_flag))
 
 
 # ------------------------------------------------------------------------------------------------
