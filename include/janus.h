@@ -237,7 +237,12 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
 
 /* Imperative fallback (Figure 2 (E)): runs the generic op list op by op, one kernel
  * launch per op instance, control predicates read back to the host (TF-Eager analogue). No
- * assumptions; never returns ASSUMPTION_FAILED; commits unless ERR_RUNTIME. */
+ * assumptions; never returns ASSUMPTION_FAILED; commits unless ERR_RUNTIME.
+ * With world_size > 1 the call is collective: each rank runs its own shard, then ONE
+ * allreduce(sum) of [every SGD-updated slot's gradient, ascending slot | runtime-error count]
+ * over the graph's communicator; every rank returns ERR_RUNTIME if any rank hit one, otherwise
+ * every rank applies W -= (lr / world_size) * summed gradient. A rank that fails before the
+ * collective still joins it. Every SGD-updated state slot must be F32. */
 janus_status janus_run_imperative(janus_graph *g, const janus_tensor *args, int32_t n_args,
                                   const janus_tensor *state, int32_t n_state,
                                   const janus_tensor *outs, int32_t n_outs,

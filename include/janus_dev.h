@@ -8,6 +8,8 @@
 #define JANUS_DEV_H
 #include <stddef.h>
 #include <stdint.h>
+
+#include "janus.h"
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -41,6 +43,29 @@ int32_t janus_dev_set_probe(struct janus_graph *g, void *dev_buf);
 int32_t janus_dev_workspace_region(const struct janus_graph *g, const char *name, size_t *offset,
                                    size_t *bytes);
 int32_t janus_dev_phase_report(const struct janus_graph *g, char *buf, size_t len);
+
+/* ---- Data-parallel protocol test hooks (host memory only: they run without a GPU). ----
+ * P:298 §5 (gradient averaging by collectives inside the step) and reading Q12 / R7 (one
+ * failing rank aborts every rank; the minimum (id, rank) failure is reported everywhere).
+ * janus_allreduce_fn: in-place allreduce of `count` elements of `buf` (host memory) over the
+ * caller's process group; dtype JANUS_F32 or JANUS_I64; op 0 = sum, 1 = min, 2 = max; returns 0
+ * on success. Every rank must call the hooks below in the same order (they are collective). */
+typedef int32_t (*janus_allreduce_fn)(void *ctx, void *buf, int64_t count, int32_t dtype, int32_t op);
+/* Route this graph's protocol-test collectives through fn (graph built with world_size > 1 or
+ * JANUS_FORCE_DP=1; -1 otherwise). The device path keeps using NCCL. */
+int32_t janus_dev_dp_set_host_collective(struct janus_graph *g, janus_allreduce_fn fn, void *ctx);
+/* The step's gradient-arena allreduces in issue order, as janus_run and its null step issue them:
+ * out[3*i .. 3*i+2] = {communicator (1 main, 2 split/overlapped), byte offset in the workspace,
+ * bytes}. Returns the number of segments (writes at most cap), or -1. */
+int32_t janus_dev_dp_segments(const struct janus_graph *g, int64_t *out, int32_t cap);
+/* One step's collective protocol on a HOST copy of the workspace (ws_host, janus_workspace_bytes
+ * bytes): the arena allreduces (sum) of janus_dev_dp_segments in order, then the abort agreement
+ * with this rank's local outcome (local = the failure this rank observed, NULL = none;
+ * runtime_err != 0 = a runtime error on this rank). *status = the agreed janus_status, *out = the
+ * agreed failure (ASSUMPTION_FAILED only). Returns 0, -1 (bad arguments / no transport) or -2
+ * (the transport failed). */
+int32_t janus_dev_dp_host_step(struct janus_graph *g, void *ws_host, const janus_failure *local,
+                               int32_t runtime_err, janus_failure *out, int32_t *status);
 
 #ifdef __cplusplus
 }

@@ -199,6 +199,13 @@ def check_guards(prog, args, state, fail_assert_id=-1, strip_asserts=False):
     return f
 
 
+def _frozen(a):
+    """The step's view of a state slot: read-only (nothing in a step mutates its inputs; Prec
+    may then round a parameter once per step)."""
+    a.flags.writeable = False
+    return a
+
+
 # =============================================================================== tape autodiff
 class Tape:
     """Trace of executed differentiable op instances; reverse pass = the inserted autodiff
@@ -211,7 +218,9 @@ class Tape:
     def add(self, kind, ins, outs, saved=None, attrs=None):
         self.entries.append((kind, ins, outs, saved, attrs))
 
-    def backward(self, loss_val):
+    def backward(self, loss_val, skip=()):
+        """skip: ids of leaf Vals whose gradient is not wanted (state slots without an SGD
+        effect, e.g. C3's frozen word vectors): their VJP is not formed (nothing flows on)."""
         P = self.P
         g = {loss_val.id: np.float64(1.0)}
 
@@ -233,7 +242,8 @@ class Tape:
                 acc(x, dx); acc(W, dW); acc(b, db)
             elif kind == "EMBEDDING":
                 E, ids = ins
-                acc(E, nm.embedding_vjp(E.data.shape, ids.data, douts[0]))
+                if E.id not in skip:
+                    acc(E, nm.embedding_vjp(E.data.shape, ids.data, douts[0]))
             elif kind == "LSTM_CELL":
                 x, h, c, W_ih, W_hh, b = ins
                 dh2 = douts[0] if douts[0] is not None else np.zeros_like(h.data, dtype=np.float64)
@@ -411,7 +421,7 @@ class GraphExec:
                 v = self.local[slot]
             else:
                 raw = np.asarray(self.state[slot])
-                v = Val(raw.astype(np.float64) if raw.dtype.kind == "f" else raw.astype(np.int64))
+                v = Val(_frozen(raw.astype(np.float64) if raw.dtype.kind == "f" else raw.astype(np.int64)))
             self.state_vals[slot] = v
             put(n, 0, tag, v)
         elif k == "STATE_WRITE":
@@ -552,7 +562,7 @@ def _forward_backward(prog, args, state, P):
     grads = {}
     sgd_slots = [e[2] for e in ex.effects if e[1] == "sgd"]
     if sgd_slots:
-        g = ex.tape.backward(loss_val)
+        g = ex.tape.backward(loss_val, {v.id for s, v in ex.state_vals.items() if s not in sgd_slots})
         for s in sgd_slots:
             v = ex.state_vals.get(s)
             gd = g.get(v.id) if v is not None else None
@@ -607,8 +617,8 @@ def run_imperative_step(prog, args, state, mode="bf16"):
     P = nm.Prec(mode)
     model = prog.meta["model"]
     tape = Tape(P)
-    sv = {k: Val(np.asarray(s).astype(np.float64) if np.asarray(s).dtype.kind == "f"
-                 else np.asarray(s).astype(np.int64)) for k, s in enumerate(state)}
+    sv = {k: Val(_frozen(np.asarray(s).astype(np.float64) if np.asarray(s).dtype.kind == "f"
+                         else np.asarray(s).astype(np.int64))) for k, s in enumerate(state)}
     sid = {s.name: k for k, s in enumerate(prog.slots)}
     writes = {}
     update = True
@@ -642,7 +652,7 @@ def run_imperative_step(prog, args, state, mode="bf16"):
     grads = {}
     params = [k for k, s in enumerate(prog.slots) if s.param] if update else []
     if params:
-        g = tape.backward(loss)
+        g = tape.backward(loss, {sv[k].id for k in sv if k not in params})
         for k in params:
             gd = g.get(sv[k].id)
             grads[k] = np.zeros(np.shape(state[k])) if gd is None else np.asarray(gd).reshape(np.shape(state[k]))

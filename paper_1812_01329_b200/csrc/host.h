@@ -131,6 +131,9 @@ struct Graph {
   cudaStream_t side = nullptr;             // stream of the overlapped collective
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
+  // protocol-test transport (janus_dev_dp_set_host_collective): host buffers, caller's allreduce
+  int32_t (*host_coll)(void *ctx, void *buf, int64_t count, int32_t dtype, int32_t op) = nullptr;
+  void *host_coll_ctx = nullptr;
   std::string describe;
   const void *gflags_ws = nullptr;        // workspace whose split-K counters were zeroed
   // workspace the device program last initialised (zero-filled on first use by janus_run; the
@@ -171,6 +174,16 @@ janus_status dp_allreduce_sum(Graph &g, float *buf, size_t n, cudaStream_t st);
 // stream by a null step — the per-communicator order is the same on every rank)
 janus_status dp_allreduce_sum2(Graph &g, float *buf, size_t n, cudaStream_t st);
 bool dp_overlap(const Graph &g);  // the backward's early allreduce is in use
+// The step's gradient-arena allreduces in issue order (identical on every rank and for the null
+// step): comm 1 = the main communicator on the launch stream, comm 2 = the split communicator
+// (issued on the side stream, overlapping the backward, by a full step). Byte offsets into the
+// workspace.
+enum { DP_OP_SUM = 0, DP_OP_MIN = 1, DP_OP_MAX = 2 };  // janus_allreduce_fn ops
+struct DpSeg {
+  int comm;
+  size_t begin, end;
+};
+std::vector<DpSeg> dp_segments(const Graph &g);
 janus_status dp_agree(Graph &g, DevStatus *st_dev, long long *scratch, cudaStream_t st);
 // a data-parallel rank whose DISPATCH guards failed still joins every collective (null step)
 janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &ws, cudaStream_t st,

@@ -403,6 +403,26 @@ int32_t janus_dev_workspace_region(const janus_graph *g, const char *name, size_
       *bytes = r.len;
       return 0;
     }
+  if (g->kind == "treelstm") {  // gradient arena members (fp32, padded pitches)
+    struct R2 { const char *k; size_t off, len; } ts[] = {
+        {"tree.gU", t.off.gU, (size_t)5 * t.H * t.ldgU * 4}, {"tree.gWl", t.off.gWl, (size_t)3 * t.H * t.ldgW * 4},
+        {"tree.gWc", t.off.gWc, (size_t)t.C * t.H * 4},     {"tree.gbc", t.off.gbc, (size_t)t.C * 4},
+        {"arena", t.off.arena_begin, t.off.arena_end - t.off.arena_begin}};
+    for (const auto &r : ts)
+      if (n == r.k) { *offset = r.off; *bytes = r.len; return 0; }
+  }
+  if (g->kind == "lstm_lm" && g->lm.bf16) {
+    const LmPlan &p = g->lm;
+    const size_t G4 = (size_t)4 * p.H;
+    if (n == "arena") { *offset = p.off.arena_begin; *bytes = p.off.arena_end - p.off.arena_begin; return 0; }
+    if (n == "lm.gWdec") { *offset = p.off.gWdec; *bytes = (size_t)p.V * p.Hp * 4; return 0; }
+    if (n == "lm.dEd" && p.off.dEd) { *offset = p.off.dEd; *bytes = (size_t)p.V * p.E * 4; return 0; }
+    for (int l = 0; l < p.L; ++l) {
+      const std::string sl = std::to_string(l);
+      if (n == "lm.gWih" + sl) { *offset = p.off.gWih[l]; *bytes = G4 * (l ? p.Hp : p.Ep) * 4; return 0; }
+      if (n == "lm.gWhh" + sl) { *offset = p.off.gWhh[l]; *bytes = G4 * p.Hp * 4; return 0; }
+    }
+  }
   return -1;
 }
 

@@ -79,6 +79,7 @@ struct Interp {
   std::vector<std::pair<int64_t, std::pair<int, float>>> sgds;   // (seq, (slot, lr))
   int out_vid = -1;
   uint64_t launches = 0, syncs = 0;
+  bool dp_joined = false;  // this rank has issued the step's data-parallel collective
   // static analysis
   std::vector<std::vector<int>> path;      // frame path per node
   std::vector<std::vector<std::pair<int, int>>> consumers;
@@ -778,7 +779,6 @@ janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
                             const janus_tensor *state, int n_state, const janus_tensor *outs,
                             int n_outs, const janus_tensor &ws, cudaStream_t st) {
   if (n_args < g.n_args || n_state < g.n_state) return JANUS_ERR_INVALID;
-  if (g.opts.world_size > 1) return JANUS_ERR_UNSUPPORTED;  // single-GPU fallback in this round
   if (!ws.data) return JANUS_ERR_INVALID;
   const size_t cap = (size_t)ws.shape[0] * (ws.dtype == JANUS_U8 ? 1 : 4);
   if (cap < g.imp_ws_bytes) return JANUS_ERR_INVALID;
@@ -790,7 +790,40 @@ janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
   I.base = static_cast<uint8_t *>(ws.data);
   I.cap = cap;
   janus_status result = JANUS_OK;
+  // Data parallel: every rank runs its own shard imperatively, then ONE allreduce(sum) of
+  // a gradient arena = [grad of every SGD-updated slot, ascending slot | runtime-error count]. The
+  // arena is laid out from the program and the state shapes alone (identical on every rank) and
+  // allocated before anything runs, so a rank whose interpretation throws still joins the same
+  // collective (zero gradients, error count 1): every rank then returns ERR_RUNTIME and commits
+  // nothing, otherwise every rank applies W -= (lr / N) * sum of gradients (reading Q12).
+  const bool dp = dp_enabled(g);
+  std::vector<std::pair<int, int64_t>> dp_slots;  // (slot, arena offset in floats)
+  int64_t dp_n = 0;
+  float *arena = nullptr;
+  if (dp) {
+    const janus_status r = dp_init(g);
+    if (r != JANUS_OK) return r;
+    std::vector<int> slots;
+    for (const janus_op &o : g.ops)
+      if (o.kind == JOP_SGD_APPLY) slots.push_back((int)o.iattr[0]);
+    std::sort(slots.begin(), slots.end());
+    slots.erase(std::unique(slots.begin(), slots.end()), slots.end());
+    for (int sl : slots) {
+      if (sl < 0 || sl >= n_state || state[sl].dtype != JANUS_F32) return JANUS_ERR_INVALID;
+      int64_t n = 1;
+      for (int d = 0; d < state[sl].ndim; ++d) n *= state[sl].shape[d];
+      dp_slots.push_back({sl, dp_n});
+      dp_n += n;
+    }
+  }
+  auto dp_join = [&](bool failed) -> janus_status {  // the step's one collective
+    if (failed && imp::fill(arena, 0.f, dp_n, st) != cudaSuccess) return JANUS_ERR_CUDA;
+    if (imp::fill(arena + dp_n, failed ? 1.f : 0.f, 1, st) != cudaSuccess) return JANUS_ERR_CUDA;
+    I.launches += 1 + (failed ? 1 : 0);
+    return dp_allreduce_sum(g, arena, (size_t)dp_n + 1, st);
+  };
   try {
+    if (dp) arena = static_cast<float *>(I.alloc((size_t)(dp_n + 1) * 4));
     I.err_dev = static_cast<int *>(I.alloc(16));
     I.ck(imp::fill_i(I.err_dev, 0, 4, st));
     I.analyse();
@@ -806,13 +839,30 @@ janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
     // runtime errors are read back with the final sync; effects apply only without one
     int err = 0;
     float loss = 0.f;
+    float dp_err = 0.f;
+    if (dp) {
+      for (auto &sl : dp_slots) {
+        const int vid = I.state_vid.count(sl.first) ? I.state_vid[sl.first] : -1;
+        const float *gr = vid >= 0 ? I.gget(vid) : nullptr;
+        int64_t n = 1;
+        for (int d = 0; d < state[sl.first].ndim; ++d) n *= state[sl.first].shape[d];
+        I.ck(gr ? imp::copy(arena + sl.second, gr, n, st) : imp::fill(arena + sl.second, 0.f, n, st));
+      }
+      // this rank's runtime-error word joins the arena: the allreduce is also the agreement
+      I.ck(imp::err_to_float(arena + dp_n, I.err_dev, st));
+      const janus_status r = dp_allreduce_sum(g, arena, (size_t)dp_n + 1, st);
+      I.dp_joined = true;
+      if (r != JANUS_OK) throw Err{r, "allreduce"};
+      if (cudaMemcpyAsync(&dp_err, arena + dp_n, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        throw Err{JANUS_ERR_CUDA, "D2H"};
+    }
     if (cudaMemcpyAsync(&err, I.err_dev, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) throw Err{JANUS_ERR_CUDA, "D2H"};
     if (I.out_vid >= 0 && I.V(I.out_vid).kind == V_DEV)
       if (cudaMemcpyAsync(&loss, I.V(I.out_vid).ptr, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         throw Err{JANUS_ERR_CUDA, "D2H"};
     if (cudaStreamSynchronize(st) != cudaSuccess) throw Err{JANUS_ERR_CUDA, "sync"};
     ++I.syncs;
-    if (err) {
+    if (err || dp_err != 0.f) {
       result = JANUS_ERR_RUNTIME;
     } else {
       // commit: SGD on the masters, then state write-backs, in effect order (P:266 (4))
@@ -826,7 +876,14 @@ janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
           const float lr = I.sgds[e.second].second.second;
           const int vid = I.state_vid.count(slot) ? I.state_vid[slot] : -1;
           float *gr = vid >= 0 ? I.gget(vid) : nullptr;
-          if (gr) I.ck(imp::sgd(static_cast<float *>(state[slot].data), gr, lr, I.V(vid).numel(), st));
+          if (gr && dp) {  // the summed gradient, averaged over the ranks in the step size
+            for (auto &sl : dp_slots)
+              if (sl.first == slot) gr = arena + sl.second;
+            I.ck(imp::sgd(static_cast<float *>(state[slot].data), gr, lr / (float)g.opts.world_size,
+                          I.V(vid).numel(), st));
+          } else if (gr) {
+            I.ck(imp::sgd(static_cast<float *>(state[slot].data), gr, lr, I.V(vid).numel(), st));
+          }
         } else {
           const auto &w = I.writes[e.second - 1000000];
           const int slot = w.second.first, vid = w.second.second;
@@ -850,8 +907,13 @@ janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
       else *static_cast<float *>(outs[0].data) = loss;
     }
   } catch (const Err &e) {
-    cudaStreamSynchronize(st);
     result = e.st;
+    // a rank that failed before the collective still joins it (its peers would block otherwise)
+    if (dp && arena && !I.dp_joined && e.st != JANUS_ERR_CUDA && e.st != JANUS_ERR_NCCL) {
+      const janus_status r = dp_join(true);
+      if (r != JANUS_OK) result = r;
+    }
+    cudaStreamSynchronize(st);
   }
   g.launches += I.launches;
   g.host_syncs += I.syncs;

@@ -579,9 +579,11 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       g.prof.mark("dp_allreduce_early", st);
       if (cudaEventRecord(g.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(g.side, g.ev_fork, 0) != cudaSuccess)
         return JANUS_ERR_CUDA;
-      janus_status r = dp_allreduce_sum2(g, fp(p.off.arena_begin), (p.off.arena_early_end - p.off.arena_begin) / 4,
-                                         g.side);
-      if (r != JANUS_OK) return r;
+      for (const DpSeg &sg : dp_segments(g))  // the split communicator's segments (dW_dec | db_dec)
+        if (sg.comm == 2) {
+          janus_status r = dp_allreduce_sum2(g, fp(sg.begin), (sg.end - sg.begin) / 4, g.side);
+          if (r != JANUS_OK) return r;
+        }
       if (cudaEventRecord(g.ev_join, g.side) != cudaSuccess) return JANUS_ERR_CUDA;
     }
     GemmOp o2;  // dh_top = dy W_dec
@@ -670,9 +672,11 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     if (p.lr_E != 0)
       LCHK("dp_scatter", launch_scatter_rows(fp(p.off.seg_grad), Ep, seg_word, nseg, fp(p.off.dEd), V, E, st));
     g.prof.mark("dp_allreduce", st);
-    const size_t a0 = overlap ? p.off.arena_early_end : p.off.arena_begin;
-    janus_status r = dp_allreduce_sum(g, fp(a0), (p.off.arena_end - a0) / 4, st);
-    if (r != JANUS_OK) return r;
+    for (const DpSeg &sg : dp_segments(g))
+      if (sg.comm == 1) {
+        janus_status r = dp_allreduce_sum(g, fp(sg.begin), (sg.end - sg.begin) / 4, st);
+        if (r != JANUS_OK) return r;
+      }
     if (overlap && cudaStreamWaitEvent(st, g.ev_join, 0) != cudaSuccess) return JANUS_ERR_CUDA;
   }
   LCHK("finalize", launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
@@ -730,15 +734,13 @@ janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &w
   unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
   LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
   LCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
-  size_t a0 = p.off.arena_begin;
-  if (g.nccl2) {  // the same per-communicator sequence as a full step: early part, then the rest
-    r = dp_allreduce_sum2(g, reinterpret_cast<float *>(W + p.off.arena_begin),
-                          (p.off.arena_early_end - p.off.arena_begin) / 4, st);
+  // the same per-communicator sequence as a full step (dp_segments in order)
+  for (const DpSeg &sg : dp_segments(g)) {
+    float *b = reinterpret_cast<float *>(W + sg.begin);
+    r = sg.comm == 2 ? dp_allreduce_sum2(g, b, (sg.end - sg.begin) / 4, st)
+                     : dp_allreduce_sum(g, b, (sg.end - sg.begin) / 4, st);
     if (r != JANUS_OK) return r;
-    a0 = p.off.arena_early_end;
   }
-  r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + a0), (p.off.arena_end - a0) / 4, st);
-  if (r != JANUS_OK) return r;
   r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
   if (r != JANUS_OK) return r;
   return finish(g, dst, nullptr, 0, st, fail);

@@ -304,7 +304,9 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   }
   if (g.nccl) {
     g.prof.mark("dp_allreduce", st);
-    janus_status r = dp_allreduce_sum(g, fp(p.off.arena_begin), (p.off.arena_end - p.off.arena_begin) / 4, st);
+    janus_status r = JANUS_OK;
+    for (const DpSeg &sg : dp_segments(g))
+      if (r == JANUS_OK) r = dp_allreduce_sum(g, fp(sg.begin), (sg.end - sg.begin) / 4, st);
     if (r != JANUS_OK) return r;
   }
   TCHK("finalize", launch_finalize(fp(p.off.rowloss), B, gl, dst, g.opts.world_size, st));
@@ -340,9 +342,10 @@ janus_status run_tree_null(Graph &g, const janus_failure &f, const janus_tensor 
   unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
   TCHK("init", launch_step_init(dst, bars, 64, st));
   TCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
-  r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + p.off.arena_begin),
-                       (p.off.arena_end - p.off.arena_begin) / 4, st);
-  if (r != JANUS_OK) return r;
+  for (const DpSeg &sg : dp_segments(g)) {  // the same collective sequence as a full step
+    r = dp_allreduce_sum(g, reinterpret_cast<float *>(W + sg.begin), (sg.end - sg.begin) / 4, st);
+    if (r != JANUS_OK) return r;
+  }
   r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
   if (r != JANUS_OK) return r;
   return finish(g, dst, nullptr, 0, st, fail);

@@ -124,6 +124,11 @@ cudaError_t fill_i(int *p, int v, int64_t n, cudaStream_t s) {
   fill_i_k<<<blocks_for(n), 256, 0, s>>>(p, v, n);
   return cudaGetLastError();
 }
+__global__ void err_to_float_k(float *y, const int *err) { y[0] = err[0] != 0 ? 1.f : 0.f; }
+cudaError_t err_to_float(float *y, const int *err, cudaStream_t s) {
+  err_to_float_k<<<1, 1, 0, s>>>(y, err);
+  return cudaGetLastError();
+}
 __global__ void axpy_k(float *y, const float *x, float a, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) y[e] += a * x[e];
 }

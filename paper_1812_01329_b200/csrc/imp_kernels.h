@@ -22,6 +22,7 @@ cudaError_t add_bias(float *Y, const float *b, int n, int N, int ldy, cudaStream
 cudaError_t colsum(float *g, const float *D, int n, int N, int ldd, bool acc, bool rd, cudaStream_t s);
 cudaError_t fill(float *p, float v, int64_t n, cudaStream_t s);
 cudaError_t fill_i(int *p, int v, int64_t n, cudaStream_t s);
+cudaError_t err_to_float(float *y, const int *err, cudaStream_t s);  // y[0] = err[0] != 0 ? 1 : 0
 cudaError_t axpy(float *y, const float *x, float a, int64_t n, cudaStream_t s);        // y += a x
 cudaError_t copy(float *y, const float *x, int64_t n, cudaStream_t s);
 cudaError_t round_copy(float *y, const float *x, int64_t n, bool r, cudaStream_t s);   // y = rb(x)

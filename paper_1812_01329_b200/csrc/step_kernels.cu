@@ -748,56 +748,23 @@ cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl,
 }
 
 // ------------------------------------------------------------------------------ data parallel
-__global__ void dp_pack_kernel(const DevStatus *st, long long *sc, int rank) {
-  const unsigned long long key = st->key;
-  unsigned long long p = KEY_PASS;
-  if (key != KEY_PASS)
-    p = ((key >> IDX_BITS) << 48) | ((unsigned long long)(rank & 0xff) << IDX_BITS) |
-        (key & ((1ull << IDX_BITS) - 1));
-  sc[0] = (long long)p;
-  sc[1] = st->runtime_err;
-  sc[3] = (long long)p;
-}
+__global__ void dp_pack_kernel(const DevStatus *st, long long *sc, int rank) { dp_pack(*st, sc, rank); }
 cudaError_t launch_dp_pack(const DevStatus *st, long long *scratch, int rank, cudaStream_t s) {
   dp_pack_kernel<<<1, 1, 0, s>>>(st, scratch, rank);
   return cudaGetLastError();
 }
-__global__ void dp_observed_kernel(const DevStatus *st, long long *sc) {
-  const bool mine = sc[3] == sc[0] && (unsigned long long)sc[0] != KEY_PASS;
-  sc[2] = mine ? st->observed : (long long)(-9223372036854775807LL - 1);
-}
+__global__ void dp_observed_kernel(const DevStatus *st, long long *sc) { dp_observed(*st, sc); }
 cudaError_t launch_dp_observed(const DevStatus *st, long long *scratch, cudaStream_t s) {
   dp_observed_kernel<<<1, 1, 0, s>>>(st, scratch);
   return cudaGetLastError();
 }
-__global__ void dp_unpack_kernel(DevStatus *st, const long long *sc) {
-  const unsigned long long p = (unsigned long long)sc[0];
-  if (p != KEY_PASS) {
-    st->key = ((p >> 48) << IDX_BITS) | (p & ((1ull << IDX_BITS) - 1));
-    st->pad[0] = (int)((p >> IDX_BITS) & 0xff);
-    st->observed = sc[2];
-    st->status = 1;
-  } else {
-    st->key = KEY_PASS;
-    st->runtime_err = (int)sc[1];
-    st->status = sc[1] ? 4 : 0;
-  }
-}
+__global__ void dp_unpack_kernel(DevStatus *st, const long long *sc) { dp_unpack(*st, sc); }
 cudaError_t launch_dp_unpack(DevStatus *st, const long long *scratch, cudaStream_t s) {
   dp_unpack_kernel<<<1, 1, 0, s>>>(st, scratch);
   return cudaGetLastError();
 }
 __global__ void set_failure_kernel(DevStatus *st, unsigned id, long long index, long long observed) {
-  if (id == 0xffffffffu) {  // invalid arguments on this rank: agreed as a runtime error (no commit)
-    st->key = KEY_PASS;
-    st->runtime_err = 1;
-    st->status = 4;
-    return;
-  }
-  const unsigned long long idx = index < 0 ? (1ull << IDX_BITS) - 1 : (unsigned long long)index;
-  st->key = ((unsigned long long)id << IDX_BITS) | idx;
-  st->observed = observed;
-  st->status = 1;
+  dp_set_failure(*st, id, index, observed);
 }
 cudaError_t launch_set_failure(DevStatus *st, unsigned id, long long index, long long observed,
                                cudaStream_t s) {

@@ -101,6 +101,50 @@ cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl,
 // data-parallel abort agreement (host_dp.cpp): scratch[0] = packed key (MIN over ranks),
 // scratch[1] = runtime error (MAX), scratch[2] = observed of the winning rank (MAX), scratch[3] =
 // this rank's packed key. DevStatus.pad[0] receives the failing rank.
+// Global abort agreement (reading Q12 / R7), the arithmetic shared by the device kernels and
+// the host transport of the protocol test (host_dp.cpp). scratch: [0] packed key (MIN over
+// ranks), [1] runtime-error flag (MAX), [2] observed value of the winning rank (MAX), [3] this
+// rank's own packed key. Packed key = assumption id << 48 | rank << 40 | element index.
+__host__ __device__ inline void dp_pack(const DevStatus &st, long long *sc, int rank) {
+  unsigned long long p = KEY_PASS;
+  if (st.key != KEY_PASS)
+    p = ((st.key >> IDX_BITS) << 48) | ((unsigned long long)(rank & 0xff) << IDX_BITS) |
+        (st.key & ((1ull << IDX_BITS) - 1));
+  sc[0] = (long long)p;
+  sc[1] = st.runtime_err;
+  sc[3] = (long long)p;
+}
+__host__ __device__ inline void dp_observed(const DevStatus &st, long long *sc) {
+  const bool mine = sc[3] == sc[0] && (unsigned long long)sc[0] != KEY_PASS;
+  sc[2] = mine ? st.observed : (long long)(-9223372036854775807LL - 1);
+}
+__host__ __device__ inline void dp_unpack(DevStatus &st, const long long *sc) {
+  const unsigned long long p = (unsigned long long)sc[0];
+  if (p != KEY_PASS) {
+    st.key = ((p >> 48) << IDX_BITS) | (p & ((1ull << IDX_BITS) - 1));
+    st.pad[0] = (int)((p >> IDX_BITS) & 0xff);
+    st.observed = sc[2];
+    st.status = 1;
+  } else {
+    st.key = KEY_PASS;
+    st.runtime_err = (int)sc[1];
+    st.status = sc[1] ? 4 : 0;
+  }
+}
+// A failure decided on the host (dispatch guard of a null step); id ~0 = invalid arguments on
+// this rank, agreed as a runtime error (no commit).
+__host__ __device__ inline void dp_set_failure(DevStatus &st, unsigned id, long long index, long long observed) {
+  if (id == 0xffffffffu) {
+    st.key = KEY_PASS;
+    st.runtime_err = 1;
+    st.status = 4;
+    return;
+  }
+  const unsigned long long idx = index < 0 ? (1ull << IDX_BITS) - 1 : (unsigned long long)index;
+  st.key = ((unsigned long long)id << IDX_BITS) | idx;
+  st.observed = observed;
+  st.status = 1;
+}
 cudaError_t launch_dp_pack(const DevStatus *st, long long *scratch, int rank, cudaStream_t s);
 cudaError_t launch_dp_observed(const DevStatus *st, long long *scratch, cudaStream_t s);
 cudaError_t launch_dp_unpack(DevStatus *st, const long long *scratch, cudaStream_t s);

@@ -431,3 +431,65 @@ def dev_phase_report(graph):
             name, ms, cnt = item.rsplit(":", 2)
             out[name] = (float(ms), int(cnt))
     return out
+
+
+# ------------------------------------------------------------------ DP protocol test hooks (CPU)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32)
+lib.janus_dev_dp_set_host_collective.restype = C.c_int32
+lib.janus_dev_dp_set_host_collective.argtypes = [C.c_void_p, ALLREDUCE_FN, C.c_void_p]
+lib.janus_dev_dp_segments.restype = C.c_int32
+lib.janus_dev_dp_segments.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
+lib.janus_dev_dp_host_step.restype = C.c_int32
+lib.janus_dev_dp_host_step.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(JanusFailure), C.c_int32,
+                                       C.POINTER(JanusFailure), C.POINTER(C.c_int32)]
+
+
+def dev_dp_set_host_collective(graph, allreduce):
+    """Route the graph's protocol-test collectives through allreduce(ndarray, op) (in place; op
+    0 sum, 1 min, 2 max). Keeps the ctypes callback alive on the graph."""
+    def cb(ctx, buf, count, dtype, op):
+        try:
+            dt = {F32: np.float32, I64: np.int64}[dtype]
+            arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), (count,))
+            allreduce(arr, op)
+            return 0
+        except Exception:  # noqa: BLE001 — reported to the library as a transport failure
+            import traceback
+            traceback.print_exc()
+            return 1
+    graph._dp_cb = ALLREDUCE_FN(cb)
+    if lib.janus_dev_dp_set_host_collective(graph.h, graph._dp_cb, None) != 0:
+        raise JanusError("janus_dev_dp_set_host_collective: graph is not data-parallel")
+
+
+def dev_dp_segments(graph):
+    """[(communicator, byte offset, bytes)] of the step's arena allreduces, in issue order."""
+    buf = (C.c_int64 * 48)()
+    n = lib.janus_dev_dp_segments(graph.h, buf, 16)
+    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n)]
+
+
+def dev_dp_host_step(graph, ws_host, local=None, runtime_err=False):
+    """One step's collective protocol on a host workspace copy (np.uint8 array, modified in place).
+    local: None or (assumption_id, index, observed). Returns (status, failure dict or None)."""
+    lf = None
+    if local is not None:
+        lf = JanusFailure(assumption_id=local[0], rank=0, index=local[1], observed=local[2])
+    out, st = JanusFailure(), C.c_int32()
+    r = lib.janus_dev_dp_host_step(graph.h, ws_host.ctypes.data_as(C.c_void_p),
+                                   C.byref(lf) if lf is not None else None, int(runtime_err),
+                                   C.byref(out), C.byref(st))
+    if r != 0:
+        raise JanusError(f"janus_dev_dp_host_step: {r}")
+    f = None
+    if st.value == ASSUMPTION_FAILED:
+        f = dict(assumption_id=out.assumption_id, rank=out.rank, index=out.index, observed=out.observed)
+    return st.value, f
+
+
+def dev_workspace_region_bytes(graph, name):
+    """(byte offset, bytes) of a named workspace region (janus_dev.h), without a workspace."""
+    off, n = C.c_size_t(), C.c_size_t()
+    if lib.janus_dev_workspace_region(graph.h, name.encode(), C.byref(off), C.byref(n)) != 0:
+        raise KeyError(name)
+    return off.value, n.value

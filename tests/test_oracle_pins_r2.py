@@ -12,7 +12,14 @@ from oracle import numerics as nm
 from workloads import gen
 from workloads import programs as pg
 
-torch.set_default_dtype(torch.float64)
+
+@pytest.fixture(autouse=True)
+def _fp64_default():
+    """fp64 torch references for this module only (the GPU tests allocate fp32 by default)."""
+    old = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    yield
+    torch.set_default_dtype(old)
 
 
 # ----------------------------------------------------------------------------- torch references
