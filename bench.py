@@ -379,12 +379,10 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
                 ms_ti = timed(lambda k: gt.run_imperative(forests[k % 4], st_i, wst, stream=stream), 2) / 2
                 # -PARL: the same device program with the level loops on one CTA (no parallelism
                 # across the nodes of a level)
-                os.environ["JANUS_TREE_GRID"] = "1"
-                try:
-                    gt.run(forests[0], st_i, wst, stream=stream)
-                    ms_t1 = timed(lambda k: gt.run(forests[k % 4], st_i, wst, stream=stream), 3) / 3
-                finally:
-                    del os.environ["JANUS_TREE_GRID"]
+                gt1 = J.Graph(tp, tree_grid=1)
+                gt1.run(forests[0], st_i, wst, stream=stream)
+                ms_t1 = timed(lambda k: gt1.run(forests[k % 4], st_i, wst, stream=stream), 3) / 3
+                del gt1
                 c3_abl = {"IMP": Bt * 1000.0 / ms_ti, "graph_one_cta_per_level": Bt * 1000.0 / ms_t1,
                           "graph_level_batched": Bt * 1000.0 / ms_t}
             del wst
@@ -401,10 +399,8 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         ms_w = timed(lambda k: gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream), K) / K
         del ws_w
         # the two layers one after the other (no layer wavefront forward or backward)
-        os.environ["JANUS_REC_WF"] = "0"
-        os.environ["JANUS_REC_BWD_WF"] = "0"
-        try:
-            gs2 = J.Graph(prog)
+        if True:
+            gs2 = J.Graph(prog, serial_layers=True)
             ws_s2 = gs2.new_workspace()
             st_s2 = [s.clone() for s in state]
             for k in range(3):
@@ -412,8 +408,6 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
             ms_s2 = timed(lambda k: gs2.run(dev_batches[k % len(dev_batches)], st_s2, ws_s2, outs=[loss],
                                             stream=stream), K) / K
             del ws_s2, gs2
-        finally:
-            del os.environ["JANUS_REC_WF"], os.environ["JANUS_REC_BWD_WF"]
         out["ablation_fig7"] = {
             "c2_samples_per_s": {"IMP": out["imperative"]["samples_per_s"], "BASE_while": B * 1000.0 / ms_w,
                                  "UNRL_layers_serial": B * 1000.0 / ms_s2, "UNRL": B * 1000.0 / ms_step},

@@ -202,7 +202,15 @@ typedef struct {
                                 JANUS_F32: fp32 SIMT everywhere                             */
   int32_t strip_asserts;     /* test/ablation only: drop RUNTIME AssertOps (P:392 overhead) */
   int32_t fail_assert_id;    /* fault injection: force this assumption id to fail, -1 = off */
-  int32_t reserved[5];
+  /* Ablation / test switches; 0 = the default build (Figure 7 arms):              */
+  int32_t serial_layers;     /* 1: stacked LSTM layers one after the other, forward and backward
+                                (no layer wavefront: the layer-parallelism analogue of +PARL)   */
+  int32_t tree_grid;         /* CTAs of the level-batched tree kernels: 0 = one per SM; 1 = the
+                                -PARL arm (no parallelism across the nodes of a level)          */
+  int32_t force_dp;          /* 1 with world_size == 1: run the data-parallel collective path
+                                (arena allreduce, agreement, null step) on a 1-rank communicator */
+  int32_t no_dp_overlap;     /* 1: no early dW_dec allreduce on the split communicator          */
+  int32_t reserved[1];
 } janus_build_opts;
 
 typedef struct janus_graph janus_graph;

@@ -522,8 +522,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   // forward
   // two layers: one wavefront launch (layer 1 one step behind layer 0, its input projection
   // fused into the recurrent MMA) unless disabled or too wide for one CTA per SM
-  const char *wf_env = getenv("JANUS_REC_WF");
-  const bool wavefront = L == 2 && !(wf_env && wf_env[0] == '0') && rec_fwd_wf_grid(H) <= 148;
+  const bool wavefront = L == 2 && !g.opts.serial_layers && rec_fwd_wf_grid(H) <= 148;
   auto rec_args = [&](int l) {
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
@@ -561,9 +560,8 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   }
   // two layers, B <= 64: one backward wavefront launch (layer 0 one step behind layer 1, the
   // dgrad of layer 1's input W_ih1^T dz1_t folded into layer 0's recurrent MMA)
-  const char *bwf_env = getenv("JANUS_REC_BWD_WF");
-  const char *bk_env = getenv("JANUS_REC_BWD");
-  const bool bwd_wave = L == 2 && B <= 64 && !(bwf_env && bwf_env[0] == '0') && !(bk_env && bk_env[0] == 'p') &&
+  const char *bk_env = getenv("JANUS_REC_BWD");  // dev experiment knob: 'p' = plain (unsplit) kernel
+  const bool bwd_wave = L == 2 && B <= 64 && !g.opts.serial_layers && !(bk_env && bk_env[0] == 'p') &&
                         rec_bwd_wf_grid(H) <= 148;
   const bool overlap = g.nccl && g.nccl2 && g.side;  // dp_overlap() held at init
   GemmOp dwdec;  // dW_dec | db_dec = dy^T [h_top | 1]

@@ -277,10 +277,9 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   if (p.tree_guard) TCHK("tree_guard", launch_tree_guard(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
   TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));
   TCHK("cast", launch_tree_cast3(Wl, bf(p.off.Wl_il), p.Ep, U, bf(p.off.U_il), p.P2, bf(p.off.UT_il), p.P5, H, E, st));
-  // one CTA per SM: the leaf level of a B=25 forest already has ~76 tiles. JANUS_TREE_GRID=n
+  // one CTA per SM: the leaf level of a B=25 forest already has ~76 tiles. opts.tree_grid = n
   // (ablation only: the paper's +PARL) runs the level loops on n CTAs
-  int grid = 148;
-  if (const char *ge = getenv("JANUS_TREE_GRID")) grid = std::max(1, std::min(148, atoi(ge)));
+  const int grid = g.opts.tree_grid > 0 ? std::min(148, g.opts.tree_grid) : 148;
   TCHK("tree_fwd", launch_tree_fwd(t, d, s, bf(p.off.Wl_il), bf(p.off.U_il), grid, dst, st));
   TCHK("root_xent", launch_tree_root(t, d, s, dst, st));
   TreeBufs tb = t;

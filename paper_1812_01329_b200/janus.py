@@ -51,7 +51,8 @@ class JanusFailure(C.Structure):
 class JanusBuildOpts(C.Structure):
     _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_uint8 * 128),
                 ("gemm_dtype", C.c_int32), ("strip_asserts", C.c_int32),
-                ("fail_assert_id", C.c_int32), ("reserved", C.c_int32 * 5)]
+                ("fail_assert_id", C.c_int32), ("serial_layers", C.c_int32), ("tree_grid", C.c_int32),
+                ("force_dp", C.c_int32), ("no_dp_overlap", C.c_int32), ("reserved", C.c_int32 * 1)]
 
 
 class JanusSessionOpts(C.Structure):
@@ -225,9 +226,10 @@ class Graph:
     """A speculatively specialised graph (janus_graph_build) for one Program."""
 
     def __init__(self, program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False,
-                 fail_assert_id=-1):
+                 fail_assert_id=-1, **ablation):
+        """ablation: serial_layers, tree_grid, force_dp, no_dp_overlap (janus_build_opts)."""
         self.program = program
-        opts = _build_opts(program, gemm, world_size, rank, nccl_id, strip_asserts, fail_assert_id)
+        opts = _build_opts(program, gemm, world_size, rank, nccl_id, strip_asserts, fail_assert_id, **ablation)
         self._ops = marshal_ops(program)
         self._asms = marshal_assumptions(program)
         h = C.c_void_p()
@@ -289,8 +291,11 @@ lib.janus_nccl_unique_id.restype = C.c_int32
 lib.janus_nccl_unique_id.argtypes = [C.c_void_p]
 
 
-def _build_opts(program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False, fail_assert_id=-1):
+def _build_opts(program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False, fail_assert_id=-1,
+                serial_layers=False, tree_grid=0, force_dp=False, no_dp_overlap=False):
     opts = JanusBuildOpts()
+    opts.serial_layers, opts.tree_grid = int(serial_layers), int(tree_grid)
+    opts.force_dp, opts.no_dp_overlap = int(force_dp), int(no_dp_overlap)
     opts.world_size, opts.rank = world_size, rank
     if nccl_id is not None:
         for k, b in enumerate(bytes(nccl_id)[:128]):

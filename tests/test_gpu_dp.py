@@ -20,11 +20,7 @@ def J():
 
 
 def _graph(prog, monkeypatch, dp):
-    if dp:
-        monkeypatch.setenv("JANUS_FORCE_DP", "1")
-    g = J().Graph(prog)
-    monkeypatch.delenv("JANUS_FORCE_DP", raising=False)
-    return g
+    return J().Graph(prog, force_dp=dp)
 
 
 def _same(a, b):

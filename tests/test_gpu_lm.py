@@ -185,9 +185,7 @@ def test_lm_dp_collective_path_single_gpu(monkeypatch):
     prog = pg.lstm_lm_program(V=V, E=40, H=48, L=2, B=B, T=T, lr=0.5)
     janus = J()
     g1 = janus.Graph(prog)
-    monkeypatch.setenv("JANUS_FORCE_DP", "1")
-    g2 = janus.Graph(prog)
-    monkeypatch.delenv("JANUS_FORCE_DP")
+    g2 = janus.Graph(prog, force_dp=True)
     state = gen.uniform_params(prog, 9, 0.1)
     args = _lm_batches(B, T, V, 1)[0]
     d1, d2 = to_dev(state), to_dev(state)

@@ -16,9 +16,9 @@ def J():
     return janus
 
 
-def _check(prog, forests, seed=3, scale=0.3, tol=2e-2, check_sched=True):
+def _check(prog, forests, seed=3, scale=0.3, tol=2e-2, check_sched=True, **ablation):
     janus = J()
-    g = janus.Graph(prog)
+    g = janus.Graph(prog, **ablation)
     assert g.device_path, g.build_message
     ws = g.new_workspace()
     state = gen.uniform_params(prog, seed, scale)
@@ -139,10 +139,9 @@ def test_tree_guard_failures():
     assert all(a.tobytes() == b.tobytes() for a, b in zip(to_host(dev), state))
 
 
-def test_tree_level_loops_on_one_cta(monkeypatch):
-    """The ablation's -PARL configuration (JANUS_TREE_GRID=1: every tile of a level on one CTA,
-    the backward streaming U^T) computes the same step."""
-    monkeypatch.setenv("JANUS_TREE_GRID", "1")
+def test_tree_level_loops_on_one_cta():
+    """The ablation's -PARL configuration (tree_grid=1: every tile of a level on one CTA, the
+    backward streaming U^T) computes the same step."""
     V, B = 50, 6
     prog = pg.treelstm_program(V=V, E=24, H=32, C=2, B=B, lr=0.2)
-    _check(prog, [gen.sst_forest(gen.SEED_C3, 9, B, V, max_leaves=12)])
+    _check(prog, [gen.sst_forest(gen.SEED_C3, 9, B, V, max_leaves=12)], tree_grid=1)
