@@ -386,37 +386,45 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
                 c3_abl = {"IMP": Bt * 1000.0 / ms_ti, "graph_one_cta_per_level": Bt * 1000.0 / ms_t1,
                           "graph_level_batched": Bt * 1000.0 / ms_t}
             del wst
-        # --- Figure 7 ablation on B200: samples/s of the same C2 batches through the
-        # imperative executor (IMP), the graph with the loop kept as a device While (BASE: no
-        # unrolling; +SPCN shapes and types still specialised) and the unrolled graph (+UNRL)
-        pw = c2_program(B, speculate="while")
-        gw = J.Graph(pw)
-        ws_w = gw.new_workspace()
-        st_w = [s.clone() for s in state]
-        loss = torch.zeros(1, device="cuda")
-        for k in range(3):
-            gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream)
-        ms_w = timed(lambda k: gw.run(dev_batches[k % len(dev_batches)], st_w, ws_w, outs=[loss], stream=stream), K) / K
-        del ws_w
-        # the two layers one after the other (no layer wavefront forward or backward)
-        if True:
-            gs2 = J.Graph(prog, serial_layers=True)
-            ws_s2 = gs2.new_workspace()
-            st_s2 = [s.clone() for s in state]
+        # --- Figure 7 ablation on B200, stacked as in the paper: each arm adds one
+        # optimisation to the previous one. Same C2 batches, same state, samples/s.
+        #   BASE  : speculative graph, loop as a device While, runtime width (SHAPE_MATCH (B, ?),
+        #           RANGE lengths in [1, 64]: planned for any width <= 64), stacked layers serial
+        #   +SPCN : the same While graph specialised to the profiled shape (B, 35)
+        #   +UNRL : unrolled to the asserted trip count (TRIP_COUNT = 35), layers serial
+        #   +PARL : + the two-layer wavefront (layer 1's step t beside layer 0's step t+1, fwd and
+        #           bwd): the product graph
+        import copy
+        from workloads.programs import Assumption
+
+        def arm(program, serial):
+            g_ = J.Graph(program, serial_layers=serial)
+            ws_ = g_.new_workspace()
+            st_ = [s.clone() for s in state]
+            loss_ = torch.zeros(1, device="cuda")
             for k in range(3):
-                gs2.run(dev_batches[k % len(dev_batches)], st_s2, ws_s2, outs=[loss], stream=stream)
-            ms_s2 = timed(lambda k: gs2.run(dev_batches[k % len(dev_batches)], st_s2, ws_s2, outs=[loss],
-                                            stream=stream), K) / K
-            del ws_s2, gs2
+                st_r, _ = g_.run(dev_batches[k % len(dev_batches)], st_, ws_, outs=[loss_], stream=stream)
+                assert st_r == J.OK, (program.name, st_r)
+            ms_ = timed(lambda k: g_.run(dev_batches[k % len(dev_batches)], st_, ws_, outs=[loss_], stream=stream), K) / K
+            del ws_, g_
+            return B * 1000.0 / ms_
+
+        p_rt = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=64, lr=1.0, speculate="while",
+                                  training_flag=True)              # runtime width <= 64
+        p_sp = copy.deepcopy(c2_program(B, speculate="while"))     # width specialised to 35
+        p_sp.assumptions = [Assumption(a.id, a.kind, a.mode, a.target, dims=(B, 35))
+                            if a.kind == "SHAPE_MATCH" and a.target in (0, 1) else a for a in p_sp.assumptions]
+        c2_abl = {"IMP": out["imperative"]["samples_per_s"], "BASE": arm(p_rt, True), "+SPCN": arm(p_sp, True),
+                  "+UNRL": arm(prog, True), "+PARL": B * 1000.0 / ms_step}
         out["ablation_fig7"] = {
-            "c2_samples_per_s": {"IMP": out["imperative"]["samples_per_s"], "BASE_while": B * 1000.0 / ms_w,
-                                 "UNRL_layers_serial": B * 1000.0 / ms_s2, "UNRL": B * 1000.0 / ms_step},
+            "c2_samples_per_s": c2_abl,
+            "c2_while_runtime_width_wavefront": arm(p_rt, False),
             "c3_b25_sentences_per_s": c3_abl,
-            "note": "IMP = janus_run_imperative (one launch per op, host-side control flow); BASE_while = "
-                    "speculative graph with the loop as a device While (RANGE assumption); UNRL = unrolled "
-                    "graph (TRIP_COUNT); UNRL_layers_serial = the same without the two-layer wavefront (layer 1's "
-                    "recurrence after layer 0's, both directions); C3 graph_one_cta_per_level = the level loops on one CTA (-PARL). +SPCN "
-                    "has no separate toggle: every device graph is shape-specialised"}
+            "note": "stacked arms (P:384-390): IMP = janus_run_imperative (one launch per op, host-side "
+                    "control flow); BASE = device While, runtime width (B, ?) planned for W <= 64, layers "
+                    "serial; +SPCN = the While graph specialised to (B, 35); +UNRL = unrolled (TRIP_COUNT), "
+                    "layers serial; +PARL = + the two-layer wavefront (the product). C3: "
+                    "graph_one_cta_per_level = level loops on one CTA (-PARL)"}
     return out
 
 

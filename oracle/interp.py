@@ -267,6 +267,11 @@ class Tape:
                 dc = douts[1] if douts[1] is not None else np.zeros((1, H))
                 dhl, dcl, dhr, dcr, dU, db = nm.tree_cell_vjp(P, saved, U.data, dh, dc)
                 acc(hl, dhl); acc(cl, dcl); acc(hr, dhr); acc(cr, dcr); acc(U, dU); acc(b, db)
+            elif kind == "TREERNN_CELL":
+                hl, hr, W, b = ins
+                dh = douts[0] if douts[0] is not None else np.zeros((1, hl.data.shape[1]))
+                dhl, dhr, dW, db = nm.tree_rnn_vjp(P, saved, W.data, dh)
+                acc(hl, dhl); acc(hr, dhr); acc(W, dW); acc(b, db)
             elif kind == "TA_STACK":
                 # ins = element Vals in index order; each contributed `rows` rows
                 d = douts[0]
@@ -485,6 +490,11 @@ class GraphExec:
             oh, oc = Val(h), Val(c)
             self.tape.add("TREELSTM_CELL", vals, [oh, oc], saved)
             put(n, 0, tag, oh); put(n, 1, tag, oc)
+        elif k == "TREERNN_CELL":
+            h, saved = nm.tree_rnn_fwd(P, *d)
+            oh = Val(h)
+            self.tape.add("TREERNN_CELL", vals, [oh], saved)
+            put(n, 0, tag, oh)
         elif k == "SOFTMAX_XENT":
             loss, saved = nm.xent_fwd(*d)
             out = Val(np.array(loss))
@@ -629,6 +639,8 @@ def run_imperative_step(prog, args, state, mode="bf16"):
                 update = int(np.asarray(args[3]).reshape(-1)[0]) != 0
         elif model == "treelstm":
             loss = _imp_treelstm(prog, args, sv, sid, tape, P)
+        elif model == "treernn":
+            loss = _imp_treernn(prog, args, sv, sid, tape, P)
         elif model == "running_sum":
             seq = np.asarray(args[0], np.float64)
             s = sv[0]
@@ -731,6 +743,37 @@ def _imp_treelstm(prog, args, sv, sid, tape, P):
     W, bc = sv[sid["W_c"]], sv[sid["b_c"]]
     logits = Val(nm.linear_fwd(P, st.data, W.data, bc.data))
     tape.add("LINEAR", [st, W, bc], [logits])
+    lv, saved = nm.xent_fwd(logits.data, label, np.ones(len(label)))
+    loss = Val(np.array(lv))
+    tape.add("SOFTMAX_XENT", [logits, None, None], [loss], saved)
+    return loss
+
+
+def _imp_treernn(prog, args, sv, sid, tape, P):
+    kind, left, right, word, off, label = (np.asarray(a, np.int64) for a in args)
+    E, W, b = (sv[sid[k]] for k in ("E", "W", "b"))
+
+    def node(n):                                  # recursion = InvokeOp
+        if not 0 <= n < len(kind):
+            raise RuntimeFault("node id out of range")
+        if kind[n] == 0:                          # a leaf is its word vector
+            ids = Val(np.array([word[n]]))
+            x = Val(nm.embedding_fwd(P, E.data, ids.data))
+            tape.add("EMBEDDING", [E, ids], [x])
+            return x
+        hl = node(int(left[n]))
+        hr = node(int(right[n]))
+        h, saved = nm.tree_rnn_fwd(P, hl.data, hr.data, W.data, b.data)
+        oh = Val(h)
+        tape.add("TREERNN_CELL", [hl, hr, W, b], [oh], saved)
+        return oh
+
+    roots = [node(int(off[i + 1]) - 1) for i in range(len(off) - 1)]
+    st = Val(np.concatenate([v.data for v in roots], axis=0))
+    tape.add("TA_STACK", roots, [st])
+    Wc, bc = sv[sid["W_c"]], sv[sid["b_c"]]
+    logits = Val(nm.linear_fwd(P, st.data, Wc.data, bc.data))
+    tape.add("LINEAR", [st, Wc, bc], [logits])
     lv, saved = nm.xent_fwd(logits.data, label, np.ones(len(label)))
     loss = Val(np.array(lv))
     tape.add("SOFTMAX_XENT", [logits, None, None], [loss], saved)

@@ -198,6 +198,24 @@ def tree_cell_vjp(P, saved, U, dh, dc_in):
     return dhh[:, :H], dc * fl, dhh[:, H:], dc * fr, d.T @ P.g(hh), db
 
 
+def tree_rnn_fwd(P, hl, hr, W, b):
+    """TreeRNN cell (Socher et al. [37]; Table 2 TreeRNN on SST; reading R13): the parent of
+    two children is h = tanh([h_l; h_r] W^T + b), W [H, 2H], b [H]. Leaves are the word vectors."""
+    hh = np.concatenate([hl, hr], axis=1)
+    h = np.tanh(P.g(hh) @ P.g(W).T + b)
+    return h, (h, hh)
+
+
+def tree_rnn_vjp(P, saved, W, dh):
+    """dz = dh (1 - h^2); [dh_l; dh_r] = rb(dz) W; dW = rb(dz)^T rb([h_l; h_r]); db = sum rb(dz)
+    (R3 / R4 as for every affine op)."""
+    h, hh = saved
+    H = h.shape[1]
+    d = P.g(dh * (1.0 - h * h))
+    dhh = d @ P.g(W)
+    return dhh[:, :H], dhh[:, H:], d.T @ P.g(hh), d.sum(axis=0)
+
+
 # ------------------------------------------------------------------------ loss (KP4)
 def xent_fwd(logits, tgt, mask):
     """loss = sum_r mask_r (logsumexp(y_r) - y_r[tgt_r]) / max(1, sum_r mask_r)  (reading Q3).

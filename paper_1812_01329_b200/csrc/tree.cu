@@ -251,26 +251,35 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
   const bool relax = in_smem && N <= 2 * (int)blockDim.x;
   if (relax) {
     // heights by parallel relaxation over all nodes: h = 1 + max(h_l, h_r) from h = 0 rises
-    // monotonically to the longest leaf path, one level per sweep (a sweep may read a value
-    // another thread has already raised: the fixpoint is the same), so max height + 1 sweeps,
+    // monotonically to the longest leaf path, one level per sweep, so max height + 1 sweeps,
     // each one node per thread, instead of one thread walking each whole tree. Children with
     // ids >= the node are ignored (the guard reports them), so no cycle can keep it rising.
-    for (int n = tid; n < N; n += blockDim.x) hh[n] = 0;
+    // Jacobi sweeps (read one buffer, write the other): no thread reads a height another thread
+    // writes in the same sweep (race-free under compute-sanitizer racecheck).
+    int *h2 = sh_height + 3 * N + TREE_SCHED_SMEM_OFF;  // second buffer (relax: N <= 2048)
+    for (int n = tid; n < N; n += blockDim.x) { hh[n] = 0; h2[n] = 0; }
     __syncthreads();
+    int *cur = hh, *nxt = h2;
     bool more = true;
     while (more) {
       bool changed = false;
       for (int n = tid; n < N; n += blockDim.x) {
         const int l = kl[n];
-        if (l == LEAF) continue;
-        const int r = kr[n];
-        const int hl = (l >= 0 && l < n) ? hh[l] : 0;
-        const int hr = (r >= 0 && r < n) ? hh[r] : 0;
-        const int h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
-        if (h != hh[n]) { hh[n] = h; changed = true; }
+        int h = 0;
+        if (l != LEAF) {
+          const int r = kr[n];
+          const int hl = (l >= 0 && l < n) ? cur[l] : 0;
+          const int hr = (r >= 0 && r < n) ? cur[r] : 0;
+          h = min(1 + max(hl, hr), TREE_MAX_LEVELS - 1);
+        }
+        nxt[n] = h;
+        changed |= h != cur[n];
       }
       more = __syncthreads_or(changed);
+      int *tmp = cur; cur = nxt; nxt = tmp;
     }
+    if (cur != hh)  // the fixpoint is in h2: copy it back
+      for (int n = tid; n < N; n += blockDim.x) hh[n] = cur[n];
   }
   for (int tr = relax ? B : tid; tr < B; tr += blockDim.x) {  // one thread walks each tree
     const int lo = max(0, t.off[tr]), hi = min(N, t.off[tr + 1]);
@@ -376,7 +385,8 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
 
 cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                                  const DevStatus *st, cudaStream_t str) {
-  const int smem = d.N <= TREE_SCHED_SMEM_NODES ? (3 * d.N + TREE_SCHED_SMEM_OFF) * 4 : 0;
+  const int smem = d.N <= TREE_SCHED_SMEM_NODES
+                       ? (3 * d.N + TREE_SCHED_SMEM_OFF + (d.N <= 2048 ? d.N : 0)) * 4 : 0;
   cudaError_t e = set_smem_once((const void *)tree_schedule_kernel, (3 * TREE_SCHED_SMEM_NODES + TREE_SCHED_SMEM_OFF) * 4);
   if (e != cudaSuccess) return e;
   {

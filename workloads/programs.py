@@ -26,7 +26,7 @@ OP_KINDS = [
     "TA_NEW", "TA_WRITE", "TA_STACK",
     "SWITCH", "MERGE", "ENTER", "EXIT", "NEXT_ITERATION",
     "LOOP_COND", "IDENTITY", "INVOKE", "RETURN",
-    "SGD_APPLY", "LEN",
+    "SGD_APPLY", "LEN", "TREERNN_CELL",
 ]
 OP_CODE = {k: i for i, k in enumerate(OP_KINDS)}
 
