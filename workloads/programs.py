@@ -253,6 +253,95 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
 # ------------------------------------------------------------------------------------------------
 # TreeLSTM — recursive TreeNN of Table 2, recursion through InvokeOp (P:224, P:316 fn6).
 # ------------------------------------------------------------------------------------------------
+def treernn_slots(V, H, C):
+    return [Slot("E", F32, (V, H), False),          # frozen word vectors (leaves; E = H)
+            Slot("W", F32, (H, 2 * H), True),
+            Slot("b", F32, (H,), True),
+            Slot("W_c", F32, (C, H), True),
+            Slot("b_c", F32, (C,), True)]
+
+
+def treernn_program(V, H, C, B, lr, *, max_nodes=127, speculate="levels", gemm="bf16"):
+    """Generic graph of one TreeRNN training step (Socher et al. [37]; Table 2):
+
+        def node(n):                                    # function 1, recursive (InvokeOp)
+            if kind[n] == LEAF: return embedding(word[n])               # Switch/Merge
+            else: return tanh([node(left[n]); node(right[n])] W^T + b)  # TREERNN_CELL
+        for i < len(label): roots += [node(tree_off[i+1]-1)]           # loop frame
+        loss = xent(linear(roots), labels); optimizer update
+
+    Same arguments, assumptions and level lowering as treelstm_program; one output port per node.
+    """
+    slots = treernn_slots(V, H, C)
+    sid = {s.name: k for k, s in enumerate(slots)}
+    g = _G()
+    # ---- function 1: node(n, kind, left, right, word, E, W, b) -> h ----
+    g.func = 1
+    a = [g.op("ARG", i=[k]) for k in range(8)]
+    n, kind, left, right, word, Emb, W, b = a
+    k0 = g.op("CONST", i=[I32], f=[0.0])
+    kn = g.op("ELEMENT", [kind, n])
+    is_leaf = g.op("EQ", [kn, k0])
+    sw = g.op("SWITCH", [n, is_leaf])
+    w = g.op("ELEMENT", [word, (sw, 1)])             # leaf arm (port 1): the word vector
+    x = g.op("EMBEDDING", [Emb, w])
+    ln = g.op("ELEMENT", [left, (sw, 0)])            # internal arm (port 0)
+    rn = g.op("ELEMENT", [right, (sw, 0)])
+    rest = [kind, left, right, word, Emb, W, b]
+    hl = g.op("INVOKE", [ln] + rest, i=[1])
+    hr = g.op("INVOKE", [rn] + rest, i=[1])
+    cell = g.op("TREERNN_CELL", [(hl, 0), (hr, 0), W, b])
+    mh = g.op("MERGE", [x, cell])
+    g.op("RETURN", [mh])
+    # ---- main ----
+    g.func = 0
+    kind, left, right, word, off, label = [g.op("ARG", i=[k]) for k in range(6)]
+    rd = {s.name: _state_read(g, k, s) for k, s in enumerate(slots)}
+    zero = g.op("CONST", i=[I32], f=[0.0])
+    one = g.op("CONST", i=[I32], f=[1.0])
+    nB = g.op("LEN", [label])
+    acc0 = g.op("TA_NEW")
+    FR = 1
+    e_i = g.op("ENTER", [zero], i=[FR, 0])
+    e_acc = g.op("ENTER", [acc0], i=[FR, 0])
+    inv = {nm: g.op("ENTER", [src], i=[FR, 1]) for nm, src in
+           [("nB", nB), ("one", one), ("kind", kind), ("left", left), ("right", right),
+            ("word", word), ("off", off), ("E", rd["E"]), ("W", rd["W"]), ("b", rd["b"])]}
+    m_i = g.op("MERGE", [e_i, e_i])
+    m_acc = g.op("MERGE", [e_acc, e_acc])
+    cond = g.op("LESS", [m_i, inv["nB"]])
+    lc = g.op("LOOP_COND", [cond])
+    s_i = g.op("SWITCH", [m_i, lc])
+    s_acc = g.op("SWITCH", [m_acc, lc])
+    i1 = g.op("ADD", [(s_i, 1), inv["one"]])
+    end = g.op("ELEMENT", [inv["off"], i1])
+    root = g.op("ADD", [end, g.op("ENTER", [g.op("CONST", i=[I32], f=[-1.0])], i=[FR, 1])])
+    hroot = g.op("INVOKE", [root, inv["kind"], inv["left"], inv["right"], inv["word"], inv["E"],
+                            inv["W"], inv["b"]], i=[1])
+    acc1 = g.op("TA_WRITE", [(s_acc, 1), (s_i, 1), (hroot, 0)])
+    g.patch_input(m_i, 1, g.op("NEXT_ITERATION", [i1]))
+    g.patch_input(m_acc, 1, g.op("NEXT_ITERATION", [acc1]))
+    x_acc = g.op("EXIT", [(s_acc, 0)])
+    roots = g.op("TA_STACK", [x_acc])
+    logits = g.op("LINEAR", [roots, rd["W_c"], rd["b_c"]])
+    ones_mask = g.op("LESS", [g.op("CONST", i=[I32], f=[-1.0]), label])
+    loss = g.op("SOFTMAX_XENT", [logits, label, ones_mask])
+    g.op("OUTPUT", [loss], i=[0])
+    for s in slots:
+        if s.param:
+            g.op("SGD_APPLY", [loss], i=[sid[s.name], g.effect_seq()], f=[lr])
+    asms = [Assumption(a, "DTYPE_EQ", DISPATCH, a, dtype=I32) for a in range(6)]
+    asms += [Assumption(6, "SHAPE_MATCH", DISPATCH, 4, dims=(B + 1,)),
+             Assumption(7, "SHAPE_MATCH", DISPATCH, 5, dims=(B,))]
+    if speculate == "levels":
+        asms += [Assumption(8, "TREE_BINARY", RUNTIME, 0, hi=V, value=max_nodes)]
+    args = [("kind", I32, None), ("left", I32, None), ("right", I32, None), ("word", I32, None),
+            ("tree_off", I32, (B + 1,)), ("label", I32, (B,))]
+    return Program(f"treernn_H{H}", g.ops, asms, slots, args, 1, lr,
+                   meta=dict(model="treernn", V=V, E=H, H=H, C=C, B=B, gemm=gemm,
+                             max_nodes=max_nodes, speculate=speculate))
+
+
 def treelstm_slots(V, E, H, C):
     return [Slot("E", F32, (V, E), False),          # frozen word vectors (SURVEY Q5)
             Slot("W_leaf", F32, (3 * H, E), True),
