@@ -355,6 +355,25 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         del sess
         # --- C4: data-dependent trip counts on the device (While + RANGE guard), SURVEY §8(d)
         out["c4"] = c4_extra(J, torch, stream, timed, K)
+        # --- TreeRNN (Table 2) on the same SST-shaped forests, B=25, H=E=300
+        tp = pg.treernn_program(V=20000, H=300, C=2, B=25, lr=0.05)
+        gr = J.Graph(tp)
+        wsr = gr.new_workspace()
+        str_ = [torch.tensor(x, device="cuda") for x in gen.uniform_params(tp, 1, 0.05)]
+        forests = [[torch.tensor(a, device="cuda") for a in gen.sst_forest(gen.SEED_C3, k, 25, 20000)]
+                   for k in range(4)]
+        for k in range(3):
+            gr.run(forests[k % 4], str_, wsr, stream=stream)
+        ms_r = timed(lambda k: gr.run(forests[k % 4], str_, wsr, stream=stream), K) / K
+        st_i = [x.clone() for x in str_]
+        gr.run_imperative(forests[0], st_i, wsr, stream=stream)
+        ms_ri = timed(lambda k: gr.run_imperative(forests[k % 4], st_i, wsr, stream=stream), 2) / 2
+        out["treernn_b25"] = {"sentences_per_s": 25 * 1000.0 / ms_r, "ms_per_step": ms_r,
+                              "imperative_sentences_per_s": 25 * 1000.0 / ms_ri,
+                              "workload": "TreeRNN (Socher et al. [37]) on C3 SST-shaped forests, B=25, "
+                                          "H=E=300, V=20000, <=64 leaves",
+                              "paper_context": "JANUS TreeRNN 988.72 sentences/s on CPUs (P:365)"}
+        del wsr, gr
         # --- C3 TreeLSTM
         for Bt in (25, 256):
             tp = pg.treelstm_program(V=20000, E=300, H=300, C=2, B=Bt, lr=0.05)

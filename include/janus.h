@@ -67,7 +67,7 @@ typedef struct {
  *   STATE_READ/STATE_WRITE = PyGetAttrOp/PySetAttrOp with local copies (Figure 5);
  *   SWITCH/MERGE = `if`; ENTER/EXIT/NEXT_ITERATION/LOOP_COND = `while`/`for` frames
  *   (P:222); INVOKE = function call / recursion (InvokeOp); the whitelisted framework
- *   functions are EMBEDDING, LINEAR, LSTM_CELL, TREELSTM_LEAF, TREELSTM_CELL,
+ *   functions are EMBEDDING, LINEAR, LSTM_CELL, TREELSTM_LEAF, TREELSTM_CELL, TREERNN_CELL,
  *   SOFTMAX_XENT; SGD_APPLY is the automatically inserted differentiation + parameter update
  *    and, being a state mutation, is deferred until all assumptions hold.
  *
@@ -96,6 +96,8 @@ typedef struct {
  *   TREELSTM_LEAF  in0 = x [1,E], in1 = W_leaf [3H,E] (blocks i,o,u), in2 = b [4H] (blocks i,f,o,u)
  *   TREELSTM_CELL  in0 = h_l, in1 = c_l, in2 = h_r, in3 = c_r ([1,H] each), in4 = U [5H,2H]
  *                  (blocks i,f_l,f_r,o,u), in5 = b [4H]
+ *   TREERNN_CELL   in0 = h_l, in1 = h_r ([1,H] each), in2 = W [H,2H], in3 = b [H] -> h [1,H] =
+ *                  tanh([h_l; h_r] W^T + b) (TreeRNN [37], Table 2; one output port)
  *   SOFTMAX_XENT   in0 = logits [n,C], in1 = targets int32 [n], in2 = mask int32 [n] -> f32
  *                  scalar: mean over masked rows of (logsumexp(logits_r) - logits_r[target_r])
  *   SEQ_MASK       in0 = lengths [B], in1 = scalar T -> int32 [T*B], row t*B+b = (t < len_b)
@@ -125,8 +127,8 @@ typedef enum {
   JOP_TA_NEW = 21, JOP_TA_WRITE = 22, JOP_TA_STACK = 23,
   JOP_SWITCH = 24, JOP_MERGE = 25, JOP_ENTER = 26, JOP_EXIT = 27, JOP_NEXT_ITERATION = 28,
   JOP_LOOP_COND = 29, JOP_IDENTITY = 30, JOP_INVOKE = 31, JOP_RETURN = 32,
-  JOP_SGD_APPLY = 33, JOP_LEN = 34,
-  JOP__COUNT = 35
+  JOP_SGD_APPLY = 33, JOP_LEN = 34, JOP_TREERNN_CELL = 35,
+  JOP__COUNT = 36
 } janus_op_kind;
 
 #define JANUS_MAX_IN 12

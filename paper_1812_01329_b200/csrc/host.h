@@ -57,6 +57,7 @@ struct LmPlan {
 struct TreePlan {
   int V = 0, E = 0, H = 0, C = 0, B = 0, max_nodes = 127, max_N = 0;
   bool bf16 = true;
+  bool rnn = false;  // TreeRNN cell (TREERNN_CELL; slot_U = W [H, 2H], b [H], no W_leaf)
   int arg_dtype[6] = {JANUS_I32, JANUS_I32, JANUS_I32, JANUS_I32, JANUS_I32, JANUS_I32};
   int slot_E = -1, slot_Wleaf = -1, slot_U = -1, slot_b = -1, slot_Wc = -1, slot_bc = -1;
   float lr_Wleaf = 0, lr_U = 0, lr_b = 0, lr_Wc = 0, lr_bc = 0;

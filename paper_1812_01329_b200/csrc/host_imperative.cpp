@@ -562,6 +562,23 @@ struct Interp {
         tape.push_back(te);
         return {h, c};
       }
+      case JOP_TREERNN_CELL: {  // h = tanh([h_l ; h_r] W^T + b)  (TreeRNN [37])
+        const IVal &hl = V(in[0]);
+        need(hl.shape.size() == 2 && V(in[1]).shape == hl.shape &&
+             V(in[2]).shape == std::vector<int64_t>{hl.shape[1], 2 * hl.shape[1]} && V(in[3]).numel() == hl.shape[1]);
+        const int n = (int)hl.shape[0], H = (int)hl.shape[1];
+        const int h = dev_f({n, H});
+        ck(imp::gemm_nt(fptr(h), fptr(in[0]), fptr(in[2]), n, H, H, H, 2 * H, H, false, R, R, st));
+        ck(imp::gemm_nt(fptr(h), fptr(in[1]), fptr(in[2]) + H, n, H, H, H, 2 * H, H, true, R, R, st));
+        ck(imp::add_bias(fptr(h), fptr(in[3]), n, H, H, st));
+        ck(imp::tanh_inplace(fptr(h), (int64_t)n * H, st));
+        bool rg = false;
+        for (int k = 0; k < 4; ++k) rg |= V(in[k]).rg;
+        vals[h].rg = rg;
+        TapeE te{JOP_TREERNN_CELL, {in[0], in[1], in[2], in[3]}, {h}};
+        tape.push_back(te);
+        return {h};
+      }
       case JOP_SOFTMAX_XENT: {
         const IVal &y = V(in[0]);
         const int n = (int)y.shape[0], C = (int)y.shape[1];
@@ -736,6 +753,21 @@ struct Interp {
             ck(imp::colsum(fptr(gb), fptr(dz), n, 5 * H, 5 * H, false, R, st));
             ck(imp::tree_bias_bwd(gbuf(b), fptr(gb), H, 1, st));
           }
+        } break;
+        case JOP_TREERNN_CELL: {
+          const int hl = t.in[0], hr = t.in[1], W = t.in[2], b = t.in[3];
+          const int n = (int)V(hl).shape[0], H = (int)V(hl).shape[1];
+          const float *dh = gget(t.out[0]);
+          const int dz = dev_f({n, H});
+          ck(imp::tanh_bwd(fptr(dz), dh, fptr(t.out[0]), (int64_t)n * H, st));  // dz = dh (1 - h^2)
+          if (V(hl).rg) ck(imp::gemm_nn(gbuf(hl), fptr(dz), fptr(W), n, H, H, H, 2 * H, H, true, R, R, st));
+          if (V(hr).rg) ck(imp::gemm_nn(gbuf(hr), fptr(dz), fptr(W) + H, n, H, H, H, 2 * H, H, true, R, R, st));
+          if (V(W).rg) {
+            float *gW = gbuf(W);
+            ck(imp::gemm_tn(gW, fptr(dz), fptr(hl), n, H, H, H, H, 2 * H, true, R, R, st));
+            ck(imp::gemm_tn(gW + H, fptr(dz), fptr(hr), n, H, H, H, H, 2 * H, true, R, R, st));
+          }
+          if (V(b).rg) ck(imp::colsum(gbuf(b), fptr(dz), n, H, H, true, R, st));
         } break;
         case JOP_TA_STACK: {
           const float *d = gget(t.out[0]);

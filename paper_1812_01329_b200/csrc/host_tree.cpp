@@ -37,17 +37,21 @@ static bool slot_dims(const Graph &g, int node, int *slot, int64_t d[4]) {
 bool lower_tree(Graph &g, std::string &why) {
   TreePlan &p = g.tree;
   p = TreePlan();
-  int leaf = -1, cell = -1, self_invoke = 0, main_invoke = -1, xent = -1;
+  int leaf = -1, cell = -1, rcell = -1, self_invoke = 0, main_invoke = -1, xent = -1;
   for (int i = 0; i < (int)g.ops.size(); ++i) {
     const janus_op &o = g.ops[i];
     if (o.func == 1 && o.kind == JOP_TREELSTM_LEAF) leaf = i;
     if (o.func == 1 && o.kind == JOP_TREELSTM_CELL) cell = i;
+    if (o.func == 1 && o.kind == JOP_TREERNN_CELL) rcell = i;
     if (o.func == 1 && o.kind == JOP_INVOKE && o.iattr[0] == 1) ++self_invoke;
     if (o.func == 0 && o.kind == JOP_INVOKE && o.iattr[0] == 1) main_invoke = i;
     if (o.func == 0 && o.kind == JOP_SOFTMAX_XENT) xent = i;
   }
-  if (leaf < 0 || cell < 0 || self_invoke != 2 || main_invoke < 0 || xent < 0) {
-    why = "not the recursive TreeLSTM pattern";
+  // TreeRNN (Table 2): the leaf arm is the word vector itself, the internal arm a
+  // TREERNN_CELL; TreeLSTM: TREELSTM_LEAF / TREELSTM_CELL
+  p.rnn = rcell >= 0 && leaf < 0 && cell < 0;
+  if ((!p.rnn && (leaf < 0 || cell < 0)) || self_invoke != 2 || main_invoke < 0 || xent < 0) {
+    why = "not the recursive TreeLSTM / TreeRNN pattern";
     return false;
   }
   for (const auto &a : g.asms)
@@ -59,7 +63,7 @@ bool lower_tree(Graph &g, std::string &why) {
       p.arg_dtype[a.target] = a.dtype;
     }
   const janus_op &inv = g.ops[main_invoke];
-  if (inv.n_in != 9) { why = "node() arity"; return false; }
+  if (inv.n_in != (p.rnn ? 8 : 9)) { why = "node() arity"; return false; }
   for (int k = 1; k <= 4; ++k) {
     const int o = producer_origin(g, inv.in_node[k]);
     if (g.ops[o].kind != JOP_ARG || g.ops[o].iattr[0] != k - 1) { why = "forest arguments"; return false; }
@@ -67,12 +71,19 @@ bool lower_tree(Graph &g, std::string &why) {
   int64_t d[4];
   if (!slot_dims(g, inv.in_node[5], &p.slot_E, d)) { why = "embedding slot"; return false; }
   p.V = (int)d[0]; p.E = (int)d[1];
-  if (!slot_dims(g, inv.in_node[6], &p.slot_Wleaf, d)) { why = "W_leaf slot"; return false; }
-  p.H = (int)(d[0] / 3);
+  if (p.rnn) {
+    if (!slot_dims(g, inv.in_node[6], &p.slot_U, d)) { why = "W slot"; return false; }
+    p.H = (int)d[0];
+    if (d[1] != 2 * p.H || p.E != p.H) { why = "TreeRNN W must be [H, 2H] with E = H (leaves are word vectors)"; return false; }
+    if (!slot_dims(g, inv.in_node[7], &p.slot_b, d) || d[0] != p.H) { why = "b shape"; return false; }
+  } else {
+    if (!slot_dims(g, inv.in_node[6], &p.slot_Wleaf, d)) { why = "W_leaf slot"; return false; }
+    p.H = (int)(d[0] / 3);
+    if (d[0] != 3 * p.H || d[1] != p.E) { why = "W_leaf shape"; return false; }
+    if (!slot_dims(g, inv.in_node[7], &p.slot_U, d) || d[0] != 5 * p.H || d[1] != 2 * p.H) { why = "U shape"; return false; }
+    if (!slot_dims(g, inv.in_node[8], &p.slot_b, d) || d[0] != 4 * p.H) { why = "b shape"; return false; }
+  }
   if (p.H > 1024) { why = "hidden size > 1024 (the forward keeps the bias in shared memory)"; return false; }
-  if (d[0] != 3 * p.H || d[1] != p.E) { why = "W_leaf shape"; return false; }
-  if (!slot_dims(g, inv.in_node[7], &p.slot_U, d) || d[0] != 5 * p.H || d[1] != 2 * p.H) { why = "U shape"; return false; }
-  if (!slot_dims(g, inv.in_node[8], &p.slot_b, d) || d[0] != 4 * p.H) { why = "b shape"; return false; }
   const janus_op &x = g.ops[xent];
   const janus_op &lin = g.ops[x.in_node[0]];
   if (lin.kind != JOP_LINEAR) { why = "classifier"; return false; }
@@ -86,7 +97,7 @@ bool lower_tree(Graph &g, std::string &why) {
     if (o.kind == JOP_SGD_APPLY) {
       const int s = (int)o.iattr[0];
       const float lr = (float)o.fattr[0];
-      if (s == p.slot_Wleaf) p.lr_Wleaf = lr;
+      if (s == p.slot_Wleaf && s >= 0) p.lr_Wleaf = lr;
       else if (s == p.slot_U) p.lr_U = lr;
       else if (s == p.slot_b) p.lr_b = lr;
       else if (s == p.slot_Wc) p.lr_Wc = lr;
@@ -131,7 +142,9 @@ bool lower_tree(Graph &g, std::string &why) {
   p.max_N = p.max_nodes * p.B;
   // ------------------------------------------------------------------ workspace layout
   const int N = p.max_N, H = p.H, E = p.E, V = p.V;
-  p.Ep = r64(E + 1); p.P2 = r64(2 * H + 1); p.P5 = r64(5 * H); p.P3 = r64(3 * H);
+  const int NG = p.rnn ? 1 : 5;  // gates per unit of the internal cell
+  const size_t NL = p.rnn ? 0 : (size_t)N;  // rows of the leaf-GEMM buffers (none for the TreeRNN)
+  p.Ep = r64(E + 1); p.P2 = r64(2 * H + 1); p.P5 = r64(NG * H); p.P3 = r64(3 * H);
   p.ldgU = r8(2 * H + 1); p.ldgW = r8(E + 1);
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
@@ -142,26 +155,26 @@ bool lower_tree(Graph &g, std::string &why) {
   p.off.height = take((size_t)N * 4); p.off.order = take((size_t)N * 4); p.off.irank = take((size_t)N * 4);
   p.off.pslot = take((size_t)N * 4); p.off.tree_of = take((size_t)N * 4); p.off.pcount = take((size_t)N * 4);
   p.off.lvl_off = take((TREE_MAX_LEVELS + 2) * 4); p.off.meta = take(64);
-  p.off.x_leaf = take((size_t)N * p.Ep * 2);
+  p.off.x_leaf = take(NL * p.Ep * 2);
   p.off.stage_h = take((size_t)N * p.P2 * 2);
-  p.off.stage_c = take((size_t)N * 2 * H * 4);
-  p.off.gates_int = take((size_t)N * 5 * H * 4);
+  p.off.stage_c = take(NL * 2 * H * 4);
+  p.off.gates_int = take(NL * 5 * H * 4);
   p.off.c_int = take((size_t)N * H * 4);
-  p.off.gates_leaf = take((size_t)N * 3 * H * 4);
-  p.off.c_leaf = take((size_t)N * H * 4);
+  p.off.gates_leaf = take(NL * 3 * H * 4);
+  p.off.c_leaf = take(NL * H * 4);
   p.off.root_h = take((size_t)p.B * H * 4);
   p.off.root_part = take((size_t)((p.B + 7) / 8) * (p.C * H + p.C) * 4);  // root classifier partials
   p.off.dh_node = take((size_t)N * H * 4);
   p.off.dc_node = take((size_t)N * H * 4);
   p.off.DZ_int = take((size_t)(N + 64) * p.P5 * 2);
-  p.off.DZ_leaf = take((size_t)(N + 64) * p.P3 * 2);
+  p.off.DZ_leaf = take(p.rnn ? 0 : (size_t)(N + 64) * p.P3 * 2);
   p.off.rowloss = take((size_t)p.B * 4);
-  p.off.U_il = take((size_t)5 * H * p.P2 * 2);
+  p.off.U_il = take((size_t)NG * H * p.P2 * 2);
   p.off.UT_il = take((size_t)2 * H * p.P5 * 2);
-  p.off.Wl_il = take((size_t)3 * H * p.Ep * 2);
+  p.off.Wl_il = take(p.rnn ? 0 : (size_t)3 * H * p.Ep * 2);
   p.off.arena_begin = o;
-  p.off.gU = take((size_t)5 * H * p.ldgU * 4);
-  p.off.gWl = take((size_t)3 * H * p.ldgW * 4);
+  p.off.gU = take((size_t)NG * H * p.ldgU * 4);
+  p.off.gWl = take(p.rnn ? 0 : (size_t)3 * H * p.ldgW * 4);
   p.off.gWc = take((size_t)p.C * H * 4);
   p.off.gbc = take((size_t)p.C * 4);
   p.off.arena_end = o;
@@ -170,11 +183,11 @@ bool lower_tree(Graph &g, std::string &why) {
   (void)V;
   char buf[512];
   snprintf(buf, sizeof buf,
-           "treelstm: V=%d E=%d H=%d C=%d B=%d max_nodes/tree=%d guards=%zu+tree_binary "
+           "%s: V=%d E=%d H=%d C=%d B=%d max_nodes/tree=%d guards=%zu+tree_binary "
            "phases=[init,guards,tree_guard,schedule,cast,tree_fwd(leaf level + internal levels, "
            "cooperative),root_xent,tree_bwd(levels top-down, cooperative),gemm_dU,gemm_dWleaf,"
            "finalize,commit]",
-           p.V, p.E, p.H, p.C, p.B, p.max_nodes, p.runtime_guards.size());
+           p.rnn ? "treernn" : "treelstm", p.V, p.E, p.H, p.C, p.B, p.max_nodes, p.runtime_guards.size());
   g.describe = buf;
   return true;
 }
@@ -227,10 +240,11 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     if (t.dtype != JANUS_F32 || k != n || !is_device_ptr(t.data)) return nullptr;
     return static_cast<float *>(t.data);
   };
-  float *Emb = sf(p.slot_E, (int64_t)p.V * E), *Wl = sf(p.slot_Wleaf, 3LL * H * E),
-        *U = sf(p.slot_U, 10LL * H * H), *bb = sf(p.slot_b, 4LL * H), *Wc = sf(p.slot_Wc, (int64_t)p.C * H),
-        *bc = sf(p.slot_bc, p.C);
-  if (!Emb || !Wl || !U || !bb || !Wc || !bc) return JANUS_ERR_INVALID;
+  const int NG = p.rnn ? 1 : 5;
+  float *Emb = sf(p.slot_E, (int64_t)p.V * E), *Wl = p.rnn ? nullptr : sf(p.slot_Wleaf, 3LL * H * E),
+        *U = sf(p.slot_U, 2LL * NG * H * H), *bb = sf(p.slot_b, (p.rnn ? 1LL : 4LL) * H),
+        *Wc = sf(p.slot_Wc, (int64_t)p.C * H), *bc = sf(p.slot_bc, p.C);
+  if (!Emb || (!Wl && !p.rnn) || !U || !bb || !Wc || !bc) return JANUS_ERR_INVALID;
   auto bf = [&](size_t off) { return reinterpret_cast<__nv_bfloat16 *>(W + off); };
   auto fp = [&](size_t off) { return reinterpret_cast<float *>(W + off); };
   auto ip = [&](size_t off) { return reinterpret_cast<int *>(W + off); };
@@ -240,7 +254,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     janus_status r = dp_init(g);
     if (r != JANUS_OK) return r;
   }
-  TreeDims d{N, B, p.V, E, H, p.C, p.Ep, p.P2, p.P5, p.P3, p.max_N};
+  TreeDims d{N, B, p.V, E, H, p.C, p.Ep, p.P2, p.P5, p.P3, p.max_N, p.rnn ? 1 : 0};
   TreeSched s{ip(p.off.height), ip(p.off.order), ip(p.off.irank), ip(p.off.pslot), ip(p.off.lvl_off),
               ip(p.off.meta), ip(p.off.tree_of), ip(p.off.pcount)};
   TreeBufs t{};
@@ -276,7 +290,12 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   if (gl.n) TCHK("guards", launch_guards(gl, dst, st));
   if (p.tree_guard) TCHK("tree_guard", launch_tree_guard(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
   TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));
-  TCHK("cast", launch_tree_cast3(Wl, bf(p.off.Wl_il), p.Ep, U, bf(p.off.U_il), p.P2, bf(p.off.UT_il), p.P5, H, E, st));
+  if (p.rnn) {  // W rows and W^T (one gate: no interleave)
+    TCHK("cast", launch_cast_il(U, H, 1, 2 * H, bf(p.off.U_il), p.P2, st));
+    TCHK("cast_T", launch_cast_il_T(U, H, 1, 2 * H, bf(p.off.UT_il), p.P5, st));
+  } else {
+    TCHK("cast", launch_tree_cast3(Wl, bf(p.off.Wl_il), p.Ep, U, bf(p.off.U_il), p.P2, bf(p.off.UT_il), p.P5, H, E, st));
+  }
   // one CTA per SM: the leaf level of a B=25 forest already has ~76 tiles. opts.tree_grid = n
   // (ablation only: the paper's +PARL) runs the level loops on n CTAs
   const int grid = g.opts.tree_grid > 0 ? std::min(148, g.opts.tree_grid) : 148;
@@ -287,7 +306,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   TCHK("tree_bwd", launch_tree_bwd(tb, d, s, bf(p.off.UT_il), grid, dst, st));
   {
     GemmOp a;  // dU | db_int = rb(dz_int)^T [h_l h_r | 1]  (K = number of internal nodes, on device)
-    a.M = 5 * H; a.N = 2 * H + 1; a.K = N; a.K_dev = s.meta + 3;
+    a.M = NG * H; a.N = 2 * H + 1; a.K = N; a.K_dev = s.meta + 3;
     a.A = bf(p.off.DZ_int); a.lda = p.P5; a.a_mn = 1;
     a.B = bf(p.off.stage_h); a.ldb = p.P2; a.b_mn = 1;
     a.ep.C = fp(p.off.gU); a.ep.ldc = p.ldgU;
@@ -299,7 +318,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     b2.ep.C = fp(p.off.gWl); b2.ep.ldc = p.ldgW;
     // one grouped launch: each GEMM alone has too few (long-K) tiles to occupy the GPU
     const GemmOp both[2] = {a, b2};
-    TCHK("gemm_wgrad", gemm_bf16_group(both, 2, st));
+    TCHK("gemm_wgrad", gemm_bf16_group(both, p.rnn ? 1 : 2, st));  // TreeRNN: no leaf weights
   }
   if (g.nccl) {
     g.prof.mark("dp_allreduce", st);
@@ -319,8 +338,9 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   const float nr = (float)g.opts.world_size;
   CommitSeg sg{};
   if (p.lr_Wleaf != 0) { sg = {}; sg.kind = C_DENSE_IL; sg.ng = 3; sg.dst = Wl; sg.grad = fp(p.off.gWl); sg.rows = 3 * H; sg.cols = E; sg.ldg = p.ldgW; sg.H = H; sg.lr = p.lr_Wleaf / nr; add(sg); }
-  if (p.lr_U != 0) { sg = {}; sg.kind = C_DENSE_IL; sg.ng = 5; sg.dst = U; sg.grad = fp(p.off.gU); sg.rows = 5 * H; sg.cols = 2 * H; sg.ldg = p.ldgU; sg.H = H; sg.lr = p.lr_U / nr; add(sg); }
-  if (p.lr_b != 0) { sg = {}; sg.kind = C_TREE_BIAS; sg.dst = bb; sg.grad = fp(p.off.gU); sg.ldg = p.ldgU; sg.col = 2 * H; sg.grad2 = fp(p.off.gWl); sg.ldg2 = p.ldgW; sg.col2 = E; sg.H = H; sg.lr = p.lr_b / nr; add(sg); }
+  if (p.lr_U != 0) { sg = {}; sg.kind = C_DENSE_IL; sg.ng = NG; sg.dst = U; sg.grad = fp(p.off.gU); sg.rows = NG * H; sg.cols = 2 * H; sg.ldg = p.ldgU; sg.H = H; sg.lr = p.lr_U / nr; add(sg); }
+  if (p.lr_b != 0 && p.rnn) { sg = {}; sg.kind = C_BIAS_COL; sg.dst = bb; sg.grad = fp(p.off.gU); sg.rows = H; sg.cols = 1; sg.ldg = p.ldgU; sg.col = 2 * H; sg.lr = p.lr_b / nr; add(sg); }
+  if (p.lr_b != 0 && !p.rnn) { sg = {}; sg.kind = C_TREE_BIAS; sg.dst = bb; sg.grad = fp(p.off.gU); sg.ldg = p.ldgU; sg.col = 2 * H; sg.grad2 = fp(p.off.gWl); sg.ldg2 = p.ldgW; sg.col2 = E; sg.H = H; sg.lr = p.lr_b / nr; add(sg); }
   if (p.lr_Wc != 0) { sg = {}; sg.kind = C_DENSE; sg.dst = Wc; sg.grad = fp(p.off.gWc); sg.rows = p.C; sg.cols = H; sg.ldg = H; sg.lr = p.lr_Wc / nr; add(sg); }
   if (p.lr_bc != 0) { sg = {}; sg.kind = C_DENSE; sg.dst = bc; sg.grad = fp(p.off.gbc); sg.rows = 1; sg.cols = p.C; sg.ldg = p.C; sg.lr = p.lr_bc / nr; add(sg); }
   TCHK("commit", launch_commit(cl, dst, st));

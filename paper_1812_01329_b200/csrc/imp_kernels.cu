@@ -124,6 +124,22 @@ cudaError_t fill_i(int *p, int v, int64_t n, cudaStream_t s) {
   fill_i_k<<<blocks_for(n), 256, 0, s>>>(p, v, n);
   return cudaGetLastError();
 }
+__global__ void tanh_inplace_k(float *y, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = tanhf(y[e]);
+}
+cudaError_t tanh_inplace(float *y, int64_t n, cudaStream_t s) {
+  tanh_inplace_k<<<blocks_for(n), 256, 0, s>>>(y, n);
+  return cudaGetLastError();
+}
+__global__ void tanh_bwd_k(float *dz, const float *dh, const float *h, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dz[e] = dh[e] * (1.f - h[e] * h[e]);
+}
+cudaError_t tanh_bwd(float *dz, const float *dh, const float *h, int64_t n, cudaStream_t s) {
+  tanh_bwd_k<<<blocks_for(n), 256, 0, s>>>(dz, dh, h, n);
+  return cudaGetLastError();
+}
 __global__ void err_to_float_k(float *y, const int *err) { y[0] = err[0] != 0 ? 1.f : 0.f; }
 cudaError_t err_to_float(float *y, const int *err, cudaStream_t s) {
   err_to_float_k<<<1, 1, 0, s>>>(y, err);

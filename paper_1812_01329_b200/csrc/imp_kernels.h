@@ -70,6 +70,9 @@ cudaError_t tree_bias_bwd(float *db, const float *g, int H, int cell, cudaStream
 cudaError_t xent(float *loss, float *dy, const float *logits, const int *tgt, const int *mask, int n,
                  int C, int *err, cudaStream_t s);
 cudaError_t sgd(float *W, const float *g, float lr, int64_t n, cudaStream_t s);
+// TreeRNN cell activation: y = tanh(y); its backward dz = dh (1 - h^2)
+cudaError_t tanh_inplace(float *y, int64_t n, cudaStream_t s);
+cudaError_t tanh_bwd(float *dz, const float *dh, const float *h, int64_t n, cudaStream_t s);
 
 }  // namespace imp
 }  // namespace jk

@@ -541,7 +541,7 @@ struct TreeFwdMaps {
   CUtensorMap x_leaf, w_leaf, stage_h, u, stage_h32;
 };
 
-template <int NS>
+template <int NS, bool RNN>
 __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__ TreeFwdMaps mp,
                                                          TreeBufs t, TreeDims d, TreeSched s,
                                                          const DevStatus *st) {
@@ -580,16 +580,30 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   // ---- phase 0: leaf inputs in level-0 order (R1: rb(E[word])), ones columns for bias grads
   {
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
-    for (long long e = gt; e < (long long)n0 * d.Ep; e += gs) {
-      const int pos = (int)(e / d.Ep), k = (int)(e % d.Ep);
-      int w = t.word[s.order[pos]];
-      w = (w >= 0 && w < d.V) ? w : 0;
-      const float v = k < E ? t.E[(size_t)w * E + k] : (k == E ? 1.f : 0.f);
-      t.x_leaf[(size_t)pos * d.Ep + k] = __float2bfloat16_rn(v);
+    if constexpr (RNN) {
+      // TreeRNN: a leaf IS its word vector (E = H, R2: rounded where it feeds a GEMM), written
+      // straight into its parent's staging row (or the root features of a one-leaf tree)
+      for (long long e = gt; e < (long long)n0 * H; e += gs) {
+        const int pos = (int)(e / H), k = (int)(e % H);
+        const int n = s.order[pos], ps = s.pslot[n];
+        int w = t.word[n];
+        w = (w >= 0 && w < d.V) ? w : 0;
+        const __nv_bfloat16 hb = __float2bfloat16_rn(t.E[(size_t)w * E + k]);
+        if (ps >= 0) t.stage_h[(size_t)(ps >> 1) * d.P2 + (ps & 1) * H + k] = hb;
+        else t.root_h[(size_t)s.tree_of[n] * H + k] = __bfloat162float(hb);
+      }
+    } else {
+      for (long long e = gt; e < (long long)n0 * d.Ep; e += gs) {
+        const int pos = (int)(e / d.Ep), k = (int)(e % d.Ep);
+        int w = t.word[s.order[pos]];
+        w = (w >= 0 && w < d.V) ? w : 0;
+        const float v = k < E ? t.E[(size_t)w * E + k] : (k == E ? 1.f : 0.f);
+        t.x_leaf[(size_t)pos * d.Ep + k] = __float2bfloat16_rn(v);
+      }
     }
     for (int i = gt; i < nint; i += gs) t.stage_h[(size_t)i * d.P2 + 2 * H] = __float2bfloat16_rn(1.f);
-    // the bias (4H floats) lives in shared memory for every epilogue of the launch
-    for (int i = threadIdx.x; i < 4 * H; i += blockDim.x) sbias[i] = t.b[i];
+    // the bias (4H floats; TreeRNN: H) lives in shared memory for every epilogue of the launch
+    for (int i = threadIdx.x; i < (RNN ? H : 4 * H); i += blockDim.x) sbias[i] = t.b[i];
     // the per-level arrival counters (first used after the leaf level's grid barrier)
     if (blockIdx.x == 0)
       for (int l = threadIdx.x; l < TREE_MAX_LEVELS; l += blockDim.x) t.barrier[64 + l * 32] = 0;
@@ -599,6 +613,7 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   const float *b = sbias;
   // ---- level 0: leaves. z = x W_leaf^T; i, o = sigmoid, u = tanh; c = i u; h = o tanh(c)
   const bool vec = (H % 4) == 0;
+  if constexpr (!RNN) {
   tile_loop<48, true, NS>(rg, &mp.x_leaf, &mp.w_leaf, 0, n0, 3 * H, E, [&](int pos, int) {
     if (pos >= 0) {  // row metadata into shared memory while the MMAs run
       const int n = s.order[pos], ps = s.pslot[n];
@@ -646,13 +661,15 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   }, (E + 63) / 64 >= 8 ? 2 : 1);
   fence_proxy_async_global();
   grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
+  }  // !RNN (TreeRNN leaves were placed in phase 0)
   // ---- internal levels: z = [h_l; h_r] U^T; c = i u + f_l c_l + f_r c_r; h = o tanh(c)
   // Internal levels: only the CTAs with tiles at a level take part in it. A CTA waits for the
   // previous level's workers (its arrival counter, one 128-B line per level) before its own tiles
   // and then arrives on this level's counter — the chain of release/acquire pairs orders every
   // earlier level too — instead of all CTAs meeting at a grid barrier per level.
   unsigned int *lvl_ctr = t.barrier + 64;
-  const int ntn = (5 * H + 79) / 80;
+  const int NGH = RNN ? H : 5 * H;  // gate rows of the cell weight (U: 5H interleaved; W: H)
+  const int ntn = (NGH + 79) / 80;
   auto workers = [&](int l) {
     const int c = s.lvl_off[l + 1] - s.lvl_off[l];
     return min((int)gridDim.x, ((c + 127) / 128) * ntn);
@@ -671,6 +688,40 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
       __syncthreads();
       fence_proxy_async_global();
     }
+    if constexpr (RNN) {
+    // TreeRNN: z = [h_l; h_r] W^T + b, h = tanh(z); a tile = 80 units of 128 nodes
+    tile_loop<80, true, NS>(rg, &mp.stage_h, &mp.u, r0, cnt, H, 2 * H, [&](int row, int) {
+      if (row >= 0) {
+        const int n = s.order[p0 + row], ps = s.pslot[n];
+        s_ps[threadIdx.x] = ps;
+        s_tr[threadIdx.x] = ps < 0 ? s.tree_of[n] : 0;
+      }
+      return 0;
+    }, [&](int rbase, int nrows, int col0) {
+      const int nu = min(80, H - col0);
+      for (int i0 = threadIdx.x; i0 < nrows * 80; i0 += 512) {  // item = (row, unit), 4 in flight
+        float zv[4];
+        bool ok[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int i = i0 + 128 * j, r = i / 80, uu = i - 80 * r;
+          ok[j] = i < nrows * 80 && uu < nu;
+          zv[j] = ok[j] ? rg.zst[r * 81 + uu] + b[col0 + uu] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!ok[j]) continue;
+          const int i = i0 + 128 * j, r = i / 80, u = col0 + i - 80 * r;
+          const int ir = r0 + rbase + r, ps = s_ps[r];
+          const float h = tanh_t(zv[j]);
+          t.c_int[(size_t)ir * H + u] = h;
+          if (ps >= 0) t.stage_h[(size_t)(ps >> 1) * d.P2 + (ps & 1) * H + u] = __float2bfloat16_rn(h);
+          else t.root_h[(size_t)s_tr[r] * H + u] = h;
+        }
+      }
+    }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1),
+       t.dbg ? t.dbg + 2 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.stage_h32);
+    } else {
     tile_loop<80, true, NS>(rg, &mp.stage_h, &mp.u, r0, cnt, 5 * H, 2 * H, [&](int row, int col0) {
       const int u0 = col0 / 5, nu = min(16, H - u0);
       if (row >= 0 && nu > 0) {  // row metadata + children c into shared memory during the MMAs
@@ -736,6 +787,7 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
       }
     }, (2 * H + 63) / 64 >= 16 ? 4 : ((2 * H + 63) / 64 >= 8 ? 2 : 1),
        t.dbg ? t.dbg + 2 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.stage_h32);
+    }  // RNN / LSTM cell
     fence_proxy_async_global();
     __syncthreads();
     if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(lvl_ctr + l * 32) : "memory");
@@ -771,22 +823,27 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
                             const DevStatus *st, cudaStream_t str) {
   // the maps span the allocated Nmax rows (rows past this step's N only feed discarded accumulator
   // rows), so they depend on the workspace alone and are encoded once per workspace, not per step
-  struct Key { const void *a, *b, *c; long long E, H, Ep, P2, Nmax; };  // no padding: compared bytewise
+  struct Key { const void *a, *b, *c; long long E, H, Ep, P2, Nmax, rnn; };  // no padding: compared bytewise
   thread_local Key key{};
   thread_local TreeFwdMaps mp;
-  const Key k{t.x_leaf, Wl_il, U_il, d.E, d.H, d.Ep, d.P2, d.Nmax};
+  const Key k{t.x_leaf, Wl_il, U_il, d.E, d.H, d.Ep, d.P2, d.Nmax, d.rnn};
   if (memcmp(&k, &key, sizeof k) != 0) {
-    bool ok = make_tmap_bf16(&mp.x_leaf, t.x_leaf, d.E, d.Nmax, d.Ep, 128);
-    ok = ok && make_tmap_bf16(&mp.w_leaf, Wl_il, d.E, 3ull * d.H, d.Ep, 48);
+    const int ngh = d.rnn ? d.H : 5 * d.H;
+    bool ok = true;
+    if (!d.rnn) {  // the TreeRNN has no leaf GEMM
+      ok = make_tmap_bf16(&mp.x_leaf, t.x_leaf, d.E, d.Nmax, d.Ep, 128);
+      ok = ok && make_tmap_bf16(&mp.w_leaf, Wl_il, d.E, 3ull * d.H, d.Ep, 48);
+    }
     ok = ok && make_tmap_bf16(&mp.stage_h, t.stage_h, 2ull * d.H, d.Nmax, d.P2, 128);
-    ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, 5ull * d.H, d.P2, 80);
+    ok = ok && make_tmap_bf16(&mp.u, U_il, 2ull * d.H, (uint64_t)ngh, d.P2, 80);
     ok = ok && make_tmap_bf16(&mp.stage_h32, t.stage_h, 2ull * d.H, d.Nmax, d.P2, 32);
     if (!ok) { key = Key{}; return cudaErrorInvalidValue; }
     key = k;
   }
   const bool six = tree_smem_fwd(6, d.H) <= 227 * 1024;  // ring depth that fits beside the staging
   const int smem = tree_smem_fwd(six ? 6 : 4, d.H);
-  const void *fn = six ? (const void *)tree_fwd_kernel<6> : (const void *)tree_fwd_kernel<4>;
+  const void *fn = d.rnn ? (six ? (const void *)tree_fwd_kernel<6, true> : (const void *)tree_fwd_kernel<4, true>)
+                         : (six ? (const void *)tree_fwd_kernel<6, false> : (const void *)tree_fwd_kernel<4, false>);
   cudaError_t e = set_smem_once(fn, smem);
   if (e != cudaSuccess) return e;
   TreeBufs tt = t;
@@ -906,7 +963,7 @@ struct TreeBwdMaps {
 constexpr int T_RES_CHUNKS = 24;  // resident K chunks (5H <= 1536)
 constexpr int T_RES_NT = 32;
 
-template <bool RES>
+template <bool RES, bool RNN>
 __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__ TreeBwdMaps mp,
                                                          TreeBufs t, TreeDims d, TreeSched s,
                                                          const DevStatus *st) {
@@ -924,6 +981,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres_bar + 1);
   const int warp = threadIdx.x >> 5;
   const int H = d.H;
+  const int NGH = RNN ? H : 5 * H;  // K of the dgrad (dz width)
   if (st->key != KEY_PASS) return;  // assumption failed: skip (uniform across CTAs)
   const int res_ntile = (2 * H + T_RES_NT - 1) / T_RES_NT;
   const int res_groups = gridDim.x / res_ntile;
@@ -939,7 +997,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
     mbar_init(bres_bar, 1);
     fence_barrier_init();
     if (RES && rg.bres_nn >= 0) {  // this CTA's slice of U^T, every K chunk, once
-      const int nk = (5 * H + 63) / 64;
+      const int nk = (NGH + 63) / 64;
       mbar_expect_tx(bres_bar, nk * T_RES_NT * 128);
       for (int c = 0; c < nk; ++c)
         tma_load_2d(rg.sB + c * T_RES_NT * 128, &mp.ut32, bres_bar, c * 64, rg.bres_nn * T_RES_NT);
@@ -958,6 +1016,14 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   for (int l = L - 1; l >= 1; --l) {
     const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
     // (a) cell backward of this level's nodes: their dh / dc were written by the parents
+    if constexpr (RNN) {  // TreeRNN: dz = dh (1 - h^2)
+      for (long long e = gt; e < (long long)cnt * H; e += gs) {
+        const int row = (int)(e / H), u = (int)(e % H);
+        const int ir = r0 + row, n = s.order[p0 + row];
+        const float h = t.c_int[(size_t)ir * H + u];
+        t.DZ_int[(size_t)ir * d.P5 + u] = __float2bfloat16_rn(t.dh_node[(size_t)n * H + u] * (1.f - h * h));
+      }
+    } else
     for (long long e = gt; e < (long long)cnt * H; e += gs) {
       const int row = (int)(e / H), u = (int)(e % H);
       const int ir = r0 + row, n = s.order[p0 + row];
@@ -982,7 +1048,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
     // (b) [dh_l ; dh_r] = rb(dz) U, scattered to the two children (each child has one parent)
     constexpr int BNT = RES ? T_RES_NT : 64;
-    tile_loop<BNT>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, 5 * H, [&](int row, int) {
+    tile_loop<BNT>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, NGH, [&](int row, int) {
       int2 c = make_int2(0, 0);
       if (row >= 0) {
         const int n = s.order[p0 + row];
@@ -1009,11 +1075,12 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
           }
         }
       }
-    }, (5 * H + 63) / 64 >= 16 ? 4 : ((5 * H + 63) / 64 >= 8 ? 2 : 1),
+    }, (NGH + 63) / 64 >= 16 ? 4 : ((NGH + 63) / 64 >= 8 ? 2 : 1),
        t.dbg ? t.dbg + 3 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.dz32);
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
   }
-  // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]
+  // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]  (TreeRNN: frozen word vectors, nothing)
+  if constexpr (!RNN)
   for (long long e = gt; e < (long long)n0 * H; e += gs) {
     const int pos = (int)(e / H), u = (int)(e % H);
     const int n = s.order[pos];
@@ -1030,8 +1097,9 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   // zero the dz rows of the last partial 64-row K chunk of the wgrad GEMMs
   for (long long e = gt; e < (long long)(((nint + 63) & ~63) - nint) * d.P5; e += gs)
     t.DZ_int[(size_t)nint * d.P5 + e] = __float2bfloat16_rn(0.f);
-  for (long long e = gt; e < (long long)(((n0 + 63) & ~63) - n0) * d.P3; e += gs)
-    t.DZ_leaf[(size_t)n0 * d.P3 + e] = __float2bfloat16_rn(0.f);
+  if constexpr (!RNN)
+    for (long long e = gt; e < (long long)(((n0 + 63) & ~63) - n0) * d.P3; e += gs)
+      t.DZ_leaf[(size_t)n0 * d.P3 + e] = __float2bfloat16_rn(0.f);
   tc_fence_before();
   __syncthreads();
   if (warp == 5) tmem_dealloc(rg.tmem, 512);
@@ -1044,18 +1112,20 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   struct Key { const void *a, *b; long long H, P5, Nmax; };  // once per workspace (see the forward)
   thread_local Key key{};
   thread_local TreeBwdMaps mp;
-  const Key k{t.DZ_int, UT_il, d.H, d.P5, d.Nmax};
+  const uint64_t ngh = d.rnn ? (uint64_t)d.H : 5ull * d.H;
+  const Key k{t.DZ_int, UT_il, d.H, d.P5, d.Nmax + ((long long)d.rnn << 40)};
   if (memcmp(&k, &key, sizeof k) != 0) {
-    bool ok = make_tmap_bf16(&mp.dz, t.DZ_int, 5ull * d.H, d.Nmax, d.P5, 128);
-    ok = ok && make_tmap_bf16(&mp.ut, UT_il, 5ull * d.H, 2ull * d.H, d.P5, 64);
-    ok = ok && make_tmap_bf16(&mp.dz32, t.DZ_int, 5ull * d.H, d.Nmax, d.P5, 32);
-    ok = ok && make_tmap_bf16(&mp.ut32, UT_il, 5ull * d.H, 2ull * d.H, d.P5, T_RES_NT);
+    bool ok = make_tmap_bf16(&mp.dz, t.DZ_int, ngh, d.Nmax, d.P5, 128);
+    ok = ok && make_tmap_bf16(&mp.ut, UT_il, ngh, 2ull * d.H, d.P5, 64);
+    ok = ok && make_tmap_bf16(&mp.dz32, t.DZ_int, ngh, d.Nmax, d.P5, 32);
+    ok = ok && make_tmap_bf16(&mp.ut32, UT_il, ngh, 2ull * d.H, d.P5, T_RES_NT);
     if (!ok) { key = Key{}; return cudaErrorInvalidValue; }
     key = k;
   }
-  const bool res = (5 * d.H + 63) / 64 <= T_RES_CHUNKS && grid >= (2 * d.H + T_RES_NT - 1) / T_RES_NT;
+  const bool res = ((int)ngh + 63) / 64 <= T_RES_CHUNKS && grid >= (2 * d.H + T_RES_NT - 1) / T_RES_NT;
   const int smem = res ? 1024 + T_STAGES * T_ASTAGE + T_RES_CHUNKS * T_RES_NT * 128 + 256 : tree_smem();
-  const void *fn = res ? (const void *)tree_bwd_kernel<true> : (const void *)tree_bwd_kernel<false>;
+  const void *fn = d.rnn ? (res ? (const void *)tree_bwd_kernel<true, true> : (const void *)tree_bwd_kernel<false, true>)
+                         : (res ? (const void *)tree_bwd_kernel<true, false> : (const void *)tree_bwd_kernel<false, false>);
   cudaError_t e = set_smem_once(fn, smem);
   if (e != cudaSuccess) return e;
   TreeBufs tt = t;

@@ -29,6 +29,7 @@ struct TreeDims {
   int P5;   // DZ_int pitch >= 5H, multiple of 64
   int P3;   // DZ_leaf pitch >= 3H, multiple of 64
   int Nmax; // rows allocated for the node arrays (the tensor maps span Nmax rows: step-invariant)
+  int rnn;  // 1: TreeRNN cell (one tanh gate, leaves = word vectors), 0: TreeLSTM
 };
 
 struct TreeBufs {
@@ -40,7 +41,7 @@ struct TreeBufs {
   __nv_bfloat16 *stage_h;      // [N_int][P2] children h (h_l | h_r), ones column at 2H
   float *stage_c;              // [N_int][2H] children c
   float *gates_int;            // [N_int][5H] (i, f_l, f_r, o, u) per unit, interleaved 5u+g
-  float *c_int;                // [N_int][H]
+  float *c_int;                // [N_int][H] (TreeRNN: h of the internal nodes)
   float *gates_leaf;           // [n_leaf][3H] (i, o, u) interleaved 3u+g
   float *c_leaf;               // [n_leaf][H]
   float *root_h;               // [B][H]
