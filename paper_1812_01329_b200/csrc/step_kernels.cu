@@ -462,9 +462,110 @@ __global__ void __launch_bounds__(NT) xent_reg_kernel(const float *__restrict__ 
   }
 }
 
+// Streaming variant: persistent blocks (two per SM) each own rows r = blockIdx.x + i * gridDim.x;
+// row i + 1 is fetched into the other of two shared-memory buffers by one bulk copy while row i
+// is reduced, so the HBM stream never waits for a reduction (the register variant above has only
+// its own row in flight). Same arithmetic: max, sum of exp(y - m), lse, dy = rb(e * inv / sum -
+// onehot * inv), the exponentials recomputed in the second pass rather than stored.
+constexpr int XT_NT = 256;
+__global__ void __launch_bounds__(XT_NT) xent_tma_kernel(const float *__restrict__ logits, int V, int ldl, int rows,
+                                                         const int *__restrict__ tgt, int B, int W,
+                                                         const int *lens, const int *T_dev, float n_valid,
+                                                         __nv_bfloat16 *dy, int lddy, float *rowloss,
+                                                         DevStatus *st) {
+  extern __shared__ __align__(16) uint8_t xs_raw[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ float sh[33];
+  __shared__ float s_nv;
+  pdl_enter();
+  float *buf = reinterpret_cast<float *>(xs_raw);
+  const size_t rb = ((size_t)V * 4 + 15) & ~size_t(15);  // bytes per buffer
+  const int Tb = T_dev ? *T_dev : rows / B;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+    int acc = 0;
+    if (lens)
+      for (int b = 0; b < B; ++b) acc += min(lens[b], Tb);
+    s_nv = (float)max(acc, 1);
+  }
+  __syncthreads();
+  const float nv = lens ? s_nv : n_valid;
+  const float inv = 1.f / nv;
+  const int V4 = V >> 2;  // V % 4 == 0 on this path
+  auto valid_row = [&](int r) {
+    const int t = r / B, b = r - t * B;
+    return t < Tb && (!lens || t < lens[b]);
+  };
+  auto issue = [&](int r, int k) {  // thread 0: row r into buffer k
+    mbar_expect_tx(&bar[k], (uint32_t)V * 4);
+    bulk_load(reinterpret_cast<uint8_t *>(buf) + k * rb, logits + (size_t)r * ldl, (uint32_t)V * 4, &bar[k]);
+  };
+  unsigned ph[2] = {0u, 0u};  // completed loads per buffer (uniform over the block)
+  const int r0 = blockIdx.x;
+  if (threadIdx.x == 0 && r0 < rows && valid_row(r0)) issue(r0, 0);
+  for (int i = 0, r = r0; r < rows; ++i, r += gridDim.x) {
+    const int k = i & 1;
+    const int rn = r + gridDim.x;
+    if (threadIdx.x == 0 && rn < rows && valid_row(rn)) issue(rn, k ^ 1);
+    const int t = r / B, b = r - t * B;
+    uint2 *d2 = reinterpret_cast<uint2 *>(dy + (size_t)r * lddy);
+    if (!valid_row(r)) {
+      for (int q = threadIdx.x; q < V4; q += XT_NT) d2[q] = make_uint2(0u, 0u);
+      if (threadIdx.x == 0) rowloss[r] = 0.f;
+      continue;  // nothing was loaded into buffer k for this row
+    }
+    int tg = tgt[(size_t)b * W + t];
+    if (tg < 0 || tg >= V) {
+      if (threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned int *>(&st->runtime_err), 2u);
+      tg = 0;
+    }
+    mbar_wait(&bar[k], ph[k] & 1);
+    ++ph[k];
+    const float4 *y4 = reinterpret_cast<const float4 *>(reinterpret_cast<uint8_t *>(buf) + k * rb);
+    float m = -INFINITY;
+    for (int q = threadIdx.x; q < V4; q += XT_NT) {
+      const float4 v = y4[q];
+      m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+    m = block_reduce<XT_NT>(m, sh, true);
+    float sum = 0.f;
+    for (int q = threadIdx.x; q < V4; q += XT_NT) {
+      const float4 v = y4[q];
+      sum += (__expf(v.x - m) + __expf(v.y - m)) + (__expf(v.z - m) + __expf(v.w - m));
+    }
+    sum = block_reduce<XT_NT>(sum, sh, false);
+    const float lse = m + logf(sum);
+    const float sc = inv / sum;
+    for (int q = threadIdx.x; q < V4; q += XT_NT) {
+      const float4 v = y4[q];
+      const int c = 4 * q;
+      const float p0 = __expf(v.x - m) * sc - (c == tg ? inv : 0.f);
+      const float p1 = __expf(v.y - m) * sc - (c + 1 == tg ? inv : 0.f);
+      const float p2 = __expf(v.z - m) * sc - (c + 2 == tg ? inv : 0.f);
+      const float p3 = __expf(v.w - m) * sc - (c + 3 == tg ? inv : 0.f);
+      __nv_bfloat162 lo = __floats2bfloat162_rn(p0, p1);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(p2, p3);
+      d2[q] = make_uint2(*reinterpret_cast<unsigned *>(&lo), *reinterpret_cast<unsigned *>(&hi));
+    }
+    if (threadIdx.x == 0) rowloss[r] = (lse - reinterpret_cast<const float *>(y4)[tg]) * inv;
+    __syncthreads();  // every read of buffer k is done before it is refilled (iteration i + 2)
+  }
+}
+
 cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
                         const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
                         int lddy, float *rowloss, DevStatus *st, cudaStream_t s) {
+  const int xt_smem = 2 * (int)(((size_t)V * 4 + 15) & ~size_t(15));
+  if (V % 4 == 0 && (ldl % 4) == 0 && (lddy % 4) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(dy) & 7) == 0 && xt_smem <= 110 * 1024 && !getenv("JANUS_XENT_REG")) {
+    cudaError_t e = set_smem_once((const void *)xent_tma_kernel, xt_smem);
+    if (e != cudaSuccess) return e;
+    const int blocks = rows < 2 * NSM ? rows : 2 * NSM;
+    return launch_pdl(xent_tma_kernel, dim3(blocks), dim3(XT_NT), (size_t)xt_smem, s, logits, V, ldl, rows, tgt, B,
+                      W, lens, T_dev, n_valid, dy, lddy, rowloss, st);
+  }
   int blocks = rows < 8 * NSM ? rows : 8 * NSM;
   constexpr int NT = 128, NV4 = 20;  // 4 rows in flight per SM (register-limited)
   const bool aligned = (ldl % 4) == 0 && (lddy % 4) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
