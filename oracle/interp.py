@@ -267,6 +267,8 @@ class Tape:
                 dc = douts[1] if douts[1] is not None else np.zeros((1, H))
                 dhl, dcl, dhr, dcr, dU, db = nm.tree_cell_vjp(P, saved, U.data, dh, dc)
                 acc(hl, dhl); acc(cl, dcl); acc(hr, dhr); acc(cr, dcr); acc(U, dU); acc(b, db)
+            elif kind == "DROPOUT":
+                acc(ins[0], nm.dropout_vjp(saved, douts[0]))
             elif kind == "TREERNN_CELL":
                 hl, hr, W, b = ins
                 dh = douts[0] if douts[0] is not None else np.zeros((1, hl.data.shape[1]))
@@ -490,6 +492,13 @@ class GraphExec:
             oh, oc = Val(h), Val(c)
             self.tape.add("TREELSTM_CELL", vals, [oh, oc], saved)
             put(n, 0, tag, oh); put(n, 1, tag, oc)
+        elif k == "DROPOUT":  # in0 x [B, D], in1 key i32[2], in2 step t; rows t * B + b
+            x, key, t = d[0], d[1], int(d[2])
+            rows = t * x.shape[0] + np.arange(x.shape[0])
+            y, saved = nm.dropout_fwd(x, key, op.i[0], rows, op.f[0])
+            out = Val(y)
+            self.tape.add("DROPOUT", [vals[0]], [out], saved)
+            put(n, 0, tag, out)
         elif k == "TREERNN_CELL":
             h, saved = nm.tree_rnn_fwd(P, *d)
             oh = Val(h)
@@ -685,10 +694,23 @@ def _imp_lstm_lm(prog, args, sv, sid, tape, P, writes):
     T = int(lens.max())
     outs = []
     E = sv[sid["E"]]
+    pdrop = m.get("dropout", 0.0)
+    key = np.asarray(args[m["key_arg"]]).reshape(-1) if pdrop else None
+    B = tok.shape[0]
+
+    def drop(x, site, t):  # x = dropout(x) on a non-recurrent connection (Zaremba [51])
+        if not pdrop:
+            return x
+        y, saved = nm.dropout_fwd(x.data, key, site, t * B + np.arange(B), pdrop)
+        out = Val(y)
+        tape.add("DROPOUT", [x], [out], saved)
+        return out
+
     for t in range(T):
         ids = Val(tok[:, t])
         x = Val(nm.embedding_fwd(P, E.data, ids.data))
         tape.add("EMBEDDING", [E, ids], [x])
+        x = drop(x, 0, t)
         valid = (t < lens).astype(np.int64)
         for l in range(L):
             W_ih, W_hh, b = sv[sid[f"W_ih{l}"]], sv[sid[f"W_hh{l}"]], sv[sid[f"b{l}"]]
@@ -696,7 +718,7 @@ def _imp_lstm_lm(prog, args, sv, sid, tape, P, writes):
             oh, oc = Val(h2), Val(c2)
             tape.add("LSTM_CELL", [x, h[l], c[l], W_ih, W_hh, b], [oh, oc], saved)
             h[l], c[l] = oh, oc
-            x = oh
+            x = drop(oh, l + 1, t)
         outs.append(x)
     st = Val(np.concatenate([v.data for v in outs], axis=0))
     tape.add("TA_STACK", outs, [st])

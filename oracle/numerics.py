@@ -216,6 +216,59 @@ def tree_rnn_vjp(P, saved, W, dh):
     return dhh[:, :H], dhh[:, H:], d.T @ P.g(hh), d.sum(axis=0)
 
 
+# ------------------------------------------------------------------------ dropout (NEXT-4)
+_PHILOX_M0, _PHILOX_M1 = 0xD2511F53, 0xCD9E8D57
+_PHILOX_W0, _PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 (Salmon et al., SC'11), the counter-based generator the dropout masks are
+    drawn from: ctr uint32 [..., 4], key uint32 [..., 2] -> uint32 [..., 4]. Ten rounds; round i
+    uses the key bumped i times by (W0, W1); a round is
+    (hi0, lo0) = M0 * c0, (hi1, lo1) = M1 * c2, c <- (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0)."""
+    c = np.asarray(ctr, np.uint64) & 0xFFFFFFFF
+    k = np.asarray(key, np.uint64) & 0xFFFFFFFF
+    c0, c1, c2, c3 = (c[..., i] for i in range(4))
+    k0, k1 = k[..., 0], k[..., 1]
+    for r in range(10):
+        if r:
+            k0 = (k0 + _PHILOX_W0) & 0xFFFFFFFF
+            k1 = (k1 + _PHILOX_W1) & 0xFFFFFFFF
+        p0 = c0 * _PHILOX_M0
+        p1 = c2 * _PHILOX_M1
+        hi0, lo0 = p0 >> 32, p0 & 0xFFFFFFFF
+        hi1, lo1 = p1 >> 32, p1 & 0xFFFFFFFF
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+    return np.stack([c0, c1, c2, c3], axis=-1).astype(np.uint32)
+
+
+def dropout_mask(key, site, rows, cols, p):
+    """Keep mask of dropout site `site` (reading R14): element (r, j) draws word j mod 4 of
+    Philox4x32-10(counter = (j div 4, r, site, 0), key) and is kept iff word >= floor(p * 2^32).
+    rows: global row indices (time-major t * B + b)."""
+    rows = np.asarray(rows, np.uint64).reshape(-1)
+    j = np.arange(cols, dtype=np.uint64)
+    ctr = np.zeros((len(rows), cols, 4), np.uint64)
+    ctr[..., 0] = j[None, :] >> 2
+    ctr[..., 1] = rows[:, None]
+    ctr[..., 2] = site
+    k = np.broadcast_to(np.asarray(key, np.uint64).reshape(2), ctr.shape[:-1] + (2,))
+    words = philox4x32_10(ctr, k)
+    w = np.take_along_axis(words, (j & 3).astype(np.int64)[None, :, None].repeat(len(rows), 0), axis=-1)[..., 0]
+    thr = np.uint64(min(int(p * 4294967296.0), 4294967295))
+    return (w.astype(np.uint64) >= thr).astype(np.float64)
+
+
+def dropout_fwd(x, key, site, rows, p):
+    """Inverted dropout of the non-recurrent connections (Zaremba et al. [51]): y = x m / (1 - p)."""
+    m = dropout_mask(key, site, rows, x.shape[1], p) / (1.0 - p)
+    return x * m, m
+
+
+def dropout_vjp(saved, dy):
+    return dy * saved
+
+
 # ------------------------------------------------------------------------ loss (KP4)
 def xent_fwd(logits, tgt, mask):
     """loss = sum_r mask_r (logsumexp(y_r) - y_r[tgt_r]) / max(1, sum_r mask_r)  (reading Q3).

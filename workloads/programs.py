@@ -26,7 +26,7 @@ OP_KINDS = [
     "TA_NEW", "TA_WRITE", "TA_STACK",
     "SWITCH", "MERGE", "ENTER", "EXIT", "NEXT_ITERATION",
     "LOOP_COND", "IDENTITY", "INVOKE", "RETURN",
-    "SGD_APPLY", "LEN", "TREERNN_CELL",
+    "SGD_APPLY", "LEN", "TREERNN_CELL", "DROPOUT",
 ]
 OP_CODE = {k: i for i, k in enumerate(OP_KINDS)}
 
@@ -127,7 +127,7 @@ def lstm_lm_slots(V, E, H, L, B):
 
 
 def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", max_T=None,
-                    training_flag=False):
+                    training_flag=False, dropout=0.0):
     """Generic graph of one truncated-BPTT step of the Figure 1 RNN model:
 
         state = self.state (zeros if it is still None)          # attribute read, P:266 (1)
@@ -141,6 +141,10 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     3 training i32[1]: the optimizer update runs only `if training:` (the train / evaluate branch
     of P:312), speculated on its profiled value (constant promotion) by a RUNTIME VALUE_EQ
     assumption (id 8): the single taken arm is kept and asserted.
+    dropout = p > 0: the Zaremba et al. [51] regularised model (PTB medium: H = 650, p =
+    0.5): dropout on every non-recurrent connection — the embedding output, each layer's output
+    into the next layer and the top layer's output into the decoder (DROPOUT sites 0 .. L) — with
+    masks drawn by Philox4x32-10 from a per-step key argument i32[2] (the last argument).
     speculate: "unroll" — fixed trip count T (C1/C2: TRIP_COUNT assumption, unrolled graph);
                "while"  — variable trip count (C4: device-resident While, RANGE assumption);
                "none"   — no RUNTIME assumptions (imperative path only).
@@ -170,9 +174,14 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     e_state = {nm: g.op("ENTER", [init[nm]], i=[FR, 0]) for nm in init}
     e_acc = g.op("ENTER", [acc0], i=[FR, 0])
     inv = {}
-    for nm, src in [("T_b", T_b), ("tok", tok), ("lens", lens), ("one", one), ("E", rd["E"])] + \
+    key_arg = 4 if training_flag else 3
+    extra = [("key", g.op("ARG", i=[key_arg]))] if dropout else []
+    for nm, src in [("T_b", T_b), ("tok", tok), ("lens", lens), ("one", one), ("E", rd["E"])] + extra + \
             [(f"{p}{l}", rd[f"{p}{l}"]) for l in range(L) for p in ("W_ih", "W_hh", "b")]:
         inv[nm] = g.op("ENTER", [src], i=[FR, 1])
+
+    def drop(x, site):  # dropout on a non-recurrent connection, masks keyed by (site, t * B + b)
+        return (g.op("DROPOUT", [x, inv["key"], t], i=[site], f=[dropout]), 0) if dropout else x
     m_t = g.op("MERGE", [e_t, e_t])  # second input patched to the NextIteration below
     m_state = {nm: g.op("MERGE", [e_state[nm], e_state[nm]]) for nm in init}
     m_acc = g.op("MERGE", [e_acc, e_acc])
@@ -184,13 +193,13 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     t = (s_t, 1)
     tok_t = g.op("COLUMN", [inv["tok"], t])
     valid = g.op("LESS", [t, inv["lens"]])
-    x = (g.op("EMBEDDING", [inv["E"], tok_t]), 0)
+    x = drop((g.op("EMBEDDING", [inv["E"], tok_t]), 0), 0)
     new_state = {}
     for l in range(L):
         cell = g.op("LSTM_CELL", [x, (s_state[f"h{l}"], 1), (s_state[f"c{l}"], 1), inv[f"W_ih{l}"],
                                   inv[f"W_hh{l}"], inv[f"b{l}"], valid])
         new_state[f"h{l}"], new_state[f"c{l}"] = (cell, 0), (cell, 1)
-        x = (cell, 0)
+        x = drop((cell, 0), l + 1)
     acc1 = g.op("TA_WRITE", [(s_acc, 1), t, x])
     t1 = g.op("ADD", [t, inv["one"]])
     ni_t = g.op("NEXT_ITERATION", [t1])
@@ -245,9 +254,15 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
         if speculate != "none":
             asms += [Assumption(8, "VALUE_EQ", RUNTIME, 3, value=1),
                      Assumption(9, "DTYPE_EQ", DISPATCH, 3, dtype=I32)]
-    return Program(f"lstm_lm_L{L}_H{H}", g.ops, asms, slots, args, 1, lr,
+    if dropout:
+        args.append(("dropout_key", I32, (2,)))
+        if speculate != "none":
+            asms += [Assumption(10, "DTYPE_EQ", DISPATCH, key_arg, dtype=I32),
+                     Assumption(11, "SHAPE_MATCH", DISPATCH, key_arg, dims=(2,))]
+    return Program(f"lstm_lm_L{L}_H{H}" + (f"_drop{dropout:g}" if dropout else ""), g.ops, asms, slots, args, 1, lr,
                    meta=dict(model="lstm_lm", V=V, E=E, H=H, L=L, B=B, T=T, W=W, gemm=gemm,
-                             speculate=speculate, training_flag=training_flag))
+                             speculate=speculate, training_flag=training_flag, dropout=dropout,
+                             key_arg=key_arg if dropout else -1))
 
 
 # ------------------------------------------------------------------------------------------------
