@@ -355,6 +355,22 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         del sess
         # --- C4: data-dependent trip counts on the device (While + RANGE guard), SURVEY §8(d)
         out["c4"] = c4_extra(J, torch, stream, timed, K)
+        # --- the Zaremba regularised LM (NEXT-4; [51] via P:312, PTB medium = the C2 shape): dropout
+        # 0.5 on every non-recurrent connection, Philox masks keyed per step (layers run serially)
+        pd = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=35, lr=1.0, dropout=0.5, training_flag=True)
+        gd = J.Graph(pd)
+        wsd = gd.new_workspace()
+        std = [s.clone() for s in state]
+        loss = torch.zeros(1, device="cuda")
+        keys = [torch.tensor([k, 2024], dtype=torch.int32, device="cuda") for k in range(4)]
+        for k in range(3):
+            gd.run(dev_batches[k % len(dev_batches)] + [keys[k % 4]], std, wsd, outs=[loss], stream=stream)
+        ms_d = timed(lambda k: gd.run(dev_batches[k % len(dev_batches)] + [keys[k % 4]], std, wsd, outs=[loss],
+                                      stream=stream), K) / K
+        out["c2_dropout"] = {"samples_per_s": B * 1000.0 / ms_d, "ms_per_step": ms_d,
+                             "workload": "Zaremba medium LM (C2 shape: 2 x 650, V=10000, T=35, B=64), dropout "
+                                         "0.5 on the non-recurrent connections, Philox4x32-10 masks"}
+        del wsd, gd
         # --- TreeRNN (Table 2) on the same SST-shaped forests, B=25, H=E=300
         tp = pg.treernn_program(V=20000, H=300, C=2, B=25, lr=0.05)
         gr = J.Graph(tp)

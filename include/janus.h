@@ -98,6 +98,10 @@ typedef struct {
  *                  (blocks i,f_l,f_r,o,u), in5 = b [4H]
  *   TREERNN_CELL   in0 = h_l, in1 = h_r ([1,H] each), in2 = W [H,2H], in3 = b [H] -> h [1,H] =
  *                  tanh([h_l; h_r] W^T + b) (TreeRNN [37], Table 2; one output port)
+ *   DROPOUT        in0 = x [n,D] f32, in1 = key i32[2], in2 = scalar step t; iattr0 = site,
+ *                  fattr0 = p -> x * m / (1 - p): inverted dropout of a non-recurrent connection
+ *                  (Zaremba et al. [51]). m[r][j] = 1 iff word j mod 4 of Philox4x32-10
+ *                  (counter = (j / 4, t * n + r, site, 0), key) >= floor(p * 2^32).
  *   SOFTMAX_XENT   in0 = logits [n,C], in1 = targets int32 [n], in2 = mask int32 [n] -> f32
  *                  scalar: mean over masked rows of (logsumexp(logits_r) - logits_r[target_r])
  *   SEQ_MASK       in0 = lengths [B], in1 = scalar T -> int32 [T*B], row t*B+b = (t < len_b)
@@ -127,8 +131,8 @@ typedef enum {
   JOP_TA_NEW = 21, JOP_TA_WRITE = 22, JOP_TA_STACK = 23,
   JOP_SWITCH = 24, JOP_MERGE = 25, JOP_ENTER = 26, JOP_EXIT = 27, JOP_NEXT_ITERATION = 28,
   JOP_LOOP_COND = 29, JOP_IDENTITY = 30, JOP_INVOKE = 31, JOP_RETURN = 32,
-  JOP_SGD_APPLY = 33, JOP_LEN = 34, JOP_TREERNN_CELL = 35,
-  JOP__COUNT = 36
+  JOP_SGD_APPLY = 33, JOP_LEN = 34, JOP_TREERNN_CELL = 35, JOP_DROPOUT = 36,
+  JOP__COUNT = 37
 } janus_op_kind;
 
 #define JANUS_MAX_IN 12

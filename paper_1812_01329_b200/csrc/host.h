@@ -33,6 +33,10 @@ struct LmPlan {
   // learning rates (0 = parameter not updated / frozen)
   float lr_E = 0, lr_Wih[4] = {}, lr_Whh[4] = {}, lr_b[4] = {}, lr_Wdec = 0, lr_bdec = 0;
   bool write_h = false, write_tag = false;
+  // dropout on the non-recurrent connections (Zaremba [51]; DROPOUT sites 0 .. L, reading R14):
+  // keep probability 1 - dropout, masks from Philox4x32-10 keyed by argument key_arg (i32[2])
+  float dropout = 0.f;
+  int key_arg = -1;
   // device guards
   struct RG { int kind; uint32_t id; int arg; int slot; int64_t value, lo, hi; int ref_arg, ref_dim; };
   std::vector<RG> runtime_guards;
@@ -42,6 +46,7 @@ struct LmPlan {
     size_t status = 0, barriers = 0, stage_args = 0;
     size_t Wih_b[4], Whh_b[4], WhhT_b[4], bil[4], Wdec_b = 0, WihT_b1 = 0;
     size_t X = 0, Hs[4], Cs[4], G[4], DZ[4], dX[4], Hsw[4], DZsw[4];
+    size_t Xd[5] = {0, 0, 0, 0, 0};  // dropout: masked bf16 copy of the input of layer l (1..L-1) / the decoder (L)
     size_t logits = 0, dy = 0, rowloss = 0, dHtop = 0, hT[4], cT[4];
     size_t gWih[4], gWhh[4], gWdec = 0;
     size_t seg_word = 0, seg_grad = 0, nseg = 0, ehist = 0, gflags = 0, gpart = 0;

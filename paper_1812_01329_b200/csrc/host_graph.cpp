@@ -25,7 +25,7 @@ static int arity(int k) {
     case JOP_IDENTITY: case JOP_SGD_APPLY: return 1;
     case JOP_ADD: case JOP_LESS: case JOP_EQ: case JOP_COLUMN: case JOP_ELEMENT: case JOP_EMBEDDING:
     case JOP_SEQ_MASK: case JOP_TIME_MAJOR: case JOP_SWITCH: return 2;
-    case JOP_LINEAR: case JOP_TREELSTM_LEAF: case JOP_SOFTMAX_XENT: case JOP_TA_WRITE: return 3;
+    case JOP_LINEAR: case JOP_TREELSTM_LEAF: case JOP_SOFTMAX_XENT: case JOP_TA_WRITE: case JOP_DROPOUT: return 3;
     case JOP_TREERNN_CELL: return 4;
     case JOP_TREELSTM_CELL: return 6;
     case JOP_LSTM_CELL: return 7;

@@ -562,6 +562,22 @@ struct Interp {
         tape.push_back(te);
         return {h, c};
       }
+      case JOP_DROPOUT: {  // y = x m / (1 - p), Philox masks keyed by (site, t * n + r)  (Zaremba [51])
+        const IVal &x = V(in[0]);
+        need(x.shape.size() == 2 && V(in[1]).numel() == 2 && V(in[1]).dtype == JANUS_I32);
+        const int n = (int)x.shape[0], D = (int)x.shape[1];
+        const int t = (int)as_host_int(in[2]);
+        const int key = as_dev_i(in[1]);
+        const int y = dev_f({n, D});
+        ck(imp::copy(fptr(y), fptr(in[0]), (int64_t)n * D, st));
+        ck(launch_dropout_f32(fptr(y), n, D, D, iptr(key), (int)o.iattr[0], (float)o.fattr[0], st, t * n));
+        vals[y].rg = x.rg;
+        TapeE te{JOP_DROPOUT, {in[0], key}, {y}};
+        te.i0 = (int)o.iattr[0]; te.i1 = t;
+        te.saved = {const_cast<void *>(static_cast<const void *>(&o.fattr[0]))};
+        tape.push_back(te);
+        return {y};
+      }
       case JOP_TREERNN_CELL: {  // h = tanh([h_l ; h_r] W^T + b)  (TreeRNN [37])
         const IVal &hl = V(in[0]);
         need(hl.shape.size() == 2 && V(in[1]).shape == hl.shape &&
@@ -753,6 +769,16 @@ struct Interp {
             ck(imp::colsum(fptr(gb), fptr(dz), n, 5 * H, 5 * H, false, R, st));
             ck(imp::tree_bias_bwd(gbuf(b), fptr(gb), H, 1, st));
           }
+        } break;
+        case JOP_DROPOUT: {  // dx = dy m / (1 - p): the same mask, regenerated
+          const int x = t.in[0];
+          if (!V(x).rg) break;
+          const int n = (int)V(x).shape[0], D = (int)V(x).shape[1];
+          const int d = dev_f({n, D});
+          ck(imp::copy(fptr(d), gget(t.out[0]), (int64_t)n * D, st));
+          ck(launch_dropout_f32(fptr(d), n, D, D, iptr(t.in[1]), t.i0, (float)*static_cast<const double *>(t.saved[0]),
+                                st, t.i1 * n));
+          ck(imp::axpy(gbuf(x), fptr(d), 1.f, (int64_t)n * D, st));
         } break;
         case JOP_TREERNN_CELL: {
           const int hl = t.in[0], hr = t.in[1], W = t.in[2], b = t.in[3];

@@ -63,6 +63,24 @@ bool lower_lm(Graph &g, std::string &why) {
   if (p.L > 4) { why = "more than 4 layers"; return false; }
   int64_t d[4];
   int nd;
+  // dropout sites (Zaremba [51]): DROPOUT(x, key, t) with site s on the input of layer s (s < L)
+  // and on the decoder input (s = L); every site present, one p and one key argument
+  int drop_site_node[5] = {-1, -1, -1, -1, -1};
+  auto through_dropout = [&](int node, int port, int site, int *src, int *src_port) -> bool {
+    const janus_op &o = g.ops[node];
+    if (o.kind != JOP_DROPOUT) { *src = node; *src_port = port; return true; }
+    if (o.iattr[0] != site || site > 4) return false;
+    const int ko = producer_origin(g, o.in_node[1]);
+    if (ko < 0 || g.ops[ko].kind != JOP_ARG) return false;
+    const int ka = (int)g.ops[ko].iattr[0];
+    if ((p.key_arg >= 0 && p.key_arg != ka) || (p.dropout != 0.f && p.dropout != (float)o.fattr[0])) return false;
+    p.key_arg = ka;
+    p.dropout = (float)o.fattr[0];
+    drop_site_node[site] = node;
+    *src = o.in_node[0];
+    *src_port = o.in_port[0];
+    return true;
+  };
   for (int l = 0; l < p.L; ++l) {
     const janus_op &c = g.ops[cells[l]];
     if (!slot_of(g, c.in_node[3], &p.slot_Wih[l], d, &nd) || nd != 2) { why = "W_ih not a state slot"; return false; }
@@ -75,9 +93,11 @@ bool lower_lm(Graph &g, std::string &why) {
     if (l == 0) p.B = (int)d[0];
     else if (d[0] != p.B) { why = "h batch"; return false; }
     if (!slot_of(g, c.in_node[2], &p.slot_c[l], d, &nd) || d[0] != p.B || d[1] != p.H) { why = "c state"; return false; }
+    int xin = -1, xport = 0;
+    if (!through_dropout(c.in_node[0], c.in_port[0], l, &xin, &xport)) { why = "dropout site"; return false; }
     if (l == 0) {
-      if (c.in_node[0] != emb) { why = "layer-0 input is not the embedding"; return false; }
-    } else if (c.in_node[0] != cells[l - 1] || c.in_port[0] != 0) { why = "layer chain"; return false; }
+      if (xin != emb) { why = "layer-0 input is not the embedding"; return false; }
+    } else if (xin != cells[l - 1] || xport != 0) { why = "layer chain"; return false; }
     const janus_op &v = g.ops[c.in_node[6]];
     if (v.kind != JOP_LESS || !is_arg(g, v.in_node[1], 2)) { why = "valid mask"; return false; }
   }
@@ -95,6 +115,18 @@ bool lower_lm(Graph &g, std::string &why) {
     dec = x.in_node[0];
     const janus_op &lin = g.ops[dec];
     if (lin.kind != JOP_LINEAR || g.ops[lin.in_node[0]].kind != JOP_TA_STACK) { why = "decoder"; return false; }
+    for (const auto &o : g.ops)  // what the loop collects for the decoder: h_top or DROPOUT(h_top)
+      if (o.func == 0 && o.kind == JOP_TA_WRITE) {
+        int src = -1, sp = 0;
+        const int vn = o.in_node[2];
+        if (!through_dropout(vn, o.in_port[2], p.L, &src, &sp) || src != cells[p.L - 1] || sp != 0) {
+          why = "decoder input is not the top layer's h";
+          return false;
+        }
+      }
+    if (p.key_arg >= 0)
+      for (int s = 0; s <= p.L; ++s)
+        if (drop_site_node[s] < 0) { why = "dropout on some but not all non-recurrent connections"; return false; }
     if (!slot_of(g, lin.in_node[1], &p.slot_Wdec, d, &nd) || d[0] != p.V || d[1] != p.H) { why = "W_dec"; return false; }
     if (!slot_of(g, lin.in_node[2], &p.slot_bdec, d, &nd) || d[0] != p.V) { why = "b_dec"; return false; }
     const janus_op &tm = g.ops[x.in_node[1]];
@@ -222,6 +254,8 @@ bool lower_lm(Graph &g, std::string &why) {
     return false;
   }
   if (g.opts.world_size > 1 && !p.bf16) { why = "fp32 path is single-GPU"; return false; }
+  if (p.key_arg >= 0 && !p.bf16) { why = "dropout runs on the bf16 tensor-core path"; return false; }
+  if (p.key_arg >= 0 && (p.dropout <= 0.f || p.dropout >= 1.f)) { why = "dropout probability outside (0, 1)"; return false; }
   // ------------------------------------------------------------------ workspace layout
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
@@ -229,7 +263,7 @@ bool lower_lm(Graph &g, std::string &why) {
   p.nbar = rec_flag_words(256) * 8;  // per-CTA step flags: 256 CTAs x (L <= 4 layers) x 2 directions
   if ((p.H + 15) / 16 > 256) { why = "hidden size > 4096"; return false; }
   p.off.barriers = take(p.nbar * sizeof(unsigned));
-  p.off.stage_args = take((3ull * p.B * p.T + 4) * sizeof(int));  // tokens, targets, lengths, training
+  p.off.stage_args = take((3ull * p.B * p.T + 8) * sizeof(int));  // tokens, targets, lengths, training, key
   const int B = p.B, T = p.T, H = p.H, E = p.E, V = p.V, G4 = 4 * p.H;
   if (!p.bf16) {
     p.off.small_ws = take(small_lm_ws_floats(V, E, H, p.L, B, T) * sizeof(float));
@@ -259,6 +293,8 @@ bool lower_lm(Graph &g, std::string &why) {
       p.off.hT[l] = take((size_t)B * H * 4);
       p.off.cT[l] = take((size_t)B * H * 4);
     }
+    if (p.key_arg >= 0)  // dropout: masked bf16 input copies of layers 1 .. L-1 and of the decoder
+      for (int s = 1; s <= p.L; ++s) p.off.Xd[s] = take(TB * p.Hp * 2);
     p.off.Wdec_b = take((size_t)V * p.Hp * 2);
     if (p.L == 2) p.off.WihT_b1 = take((size_t)H * G4 * 2);  // W_ih1^T for the backward wavefront
     p.off.X = take(TB * p.Ep * 2);
@@ -291,13 +327,13 @@ bool lower_lm(Graph &g, std::string &why) {
   p.ws_bytes = o;
   char buf[512];
   snprintf(buf, sizeof buf,
-           "lstm_lm: L=%d V=%d E=%d H=%d B=%d %s=%d tag=%s train=%s path=%s guards=%zu "
+           "lstm_lm: L=%d V=%d E=%d H=%d B=%d %s=%d tag=%s train=%s dropout=%g path=%s guards=%zu "
            "phases=[init,%sguards,cast,gather,{gemm_in,rec_fwd}xL,gemm_dec,xent,gemm_dWdec,"
            "gemm_dh,{rec_bwd,gemm_dWhh,gemm_dWih,gemm_dx}xL,embed_grad,finalize,commit]",
            p.L, p.V, p.E, p.H, p.B, p.while_mode ? "while_width" : "unrolled_T", p.T,
            p.tag_specialised ? "specialised" : "device_switch",
            p.train_arg < 0 ? "none" : p.train_specialised ? "specialised" : "device_switch",
-           p.bf16 ? "tcgen05_bf16" : "fp32_single_cta",
+           (double)(p.key_arg >= 0 ? p.dropout : 0.f), p.bf16 ? "tcgen05_bf16" : "fp32_single_cta",
            p.runtime_guards.size(), p.while_mode ? "trip," : "");
   g.describe = buf;
   return true;
@@ -400,6 +436,16 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       int *dstp = reinterpret_cast<int *>(W + p.off.stage_args) + (size_t)3 * B * p.T;
       if (cudaMemcpyAsync(dstp, args[3].data, 4, cudaMemcpyHostToDevice, st) != cudaSuccess) return JANUS_ERR_CUDA;
       argp[3] = dstp;
+    }
+  }
+  const int *keyp = nullptr;  // dropout key (Philox), i32[2]
+  if (p.key_arg >= 0) {
+    if (!tensor_ok(args[p.key_arg], JANUS_I32, 2)) return JANUS_ERR_INVALID;
+    if (is_device_ptr(args[p.key_arg].data)) keyp = static_cast<const int *>(args[p.key_arg].data);
+    else {
+      int *dstp = reinterpret_cast<int *>(W + p.off.stage_args) + (size_t)3 * B * p.T + 4;
+      if (cudaMemcpyAsync(dstp, args[p.key_arg].data, 8, cudaMemcpyHostToDevice, st) != cudaSuccess) return JANUS_ERR_CUDA;
+      keyp = dstp;
     }
   }
   for (int a = 0; a < 3; ++a) {
@@ -519,10 +565,16 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     LCHK("cast", launch_prep(pl, st));
   }
   LCHK("gather", launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
+  const bool drop = p.key_arg >= 0;  // Zaremba dropout: site 0 on the embedding output (in place)
+  if (drop) LCHK("dropout", launch_dropout_bf16(bf(p.off.X), bf(p.off.X), TB, E, Ep, keyp, 0, p.dropout, st));
+  // input of layer l (l >= 1) and of the decoder: the layer below's h, or its dropped copy
+  auto layer_in = [&](int l) -> __nv_bfloat16 * {
+    return drop ? bf(p.off.Xd[l]) : bf(p.off.Hs[l - 1]) + (size_t)B * Hp;
+  };
   // forward
   // two layers: one wavefront launch (layer 1 one step behind layer 0, its input projection
   // fused into the recurrent MMA) unless disabled or too wide for one CTA per SM
-  const bool wavefront = L == 2 && !g.opts.serial_layers && rec_fwd_wf_grid(H) <= 148;
+  const bool wavefront = L == 2 && !g.opts.serial_layers && !drop && rec_fwd_wf_grid(H) <= 148;
   auto rec_args = [&](int l) {
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
@@ -537,9 +589,11 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   for (int l = 0; l < L; ++l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
     if (wavefront && l == 1) break;
+    if (drop && l) LCHK("dropout", launch_dropout_bf16(bf(p.off.Hs[l - 1]) + (size_t)B * Hp, bf(p.off.Xd[l]), TB, H, Hp,
+                                                     keyp, l, p.dropout, st));
     GemmOp op;
     op.M = TB; op.N = G4; op.K = In;
-    op.A = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X); op.lda = Inp;
+    op.A = l ? layer_in(l) : bf(p.off.X); op.lda = Inp;
     op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
     op.ep.C = fp(p.off.G[l]); op.ep.ldc = p.Gz; op.ep.bias_col = fp(p.off.bil[l]);
     LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(with_flags(op), st));
@@ -550,10 +604,12 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       LCHK(l ? "rec_fwd1" : "rec_fwd0", lstm_rec_fwd(rec_args(l), bf(p.off.Whh_b[l]), Hp, p.while_mode, st));
     }
   }
+  if (drop) LCHK("dropout", launch_dropout_bf16(bf(p.off.Hs[L - 1]) + (size_t)B * Hp, bf(p.off.Xd[L]), TB, H, Hp,
+                                               keyp, L, p.dropout, st));
   {
     GemmOp op;  // decoder logits
     op.M = TB; op.N = V; op.K = H;
-    op.A = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; op.lda = Hp;
+    op.A = layer_in(L); op.lda = Hp;
     op.B = bf(p.off.Wdec_b); op.ldb = Hp;
     op.ep.C = fp(p.off.logits); op.ep.ldc = Vp; op.ep.bias_col = P.bdec;
     LCHK("gemm_dec", gemm_bf16(with_flags(op), st));
@@ -561,13 +617,13 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   // two layers, B <= 64: one backward wavefront launch (layer 0 one step behind layer 1, the
   // dgrad of layer 1's input W_ih1^T dz1_t folded into layer 0's recurrent MMA)
   const char *bk_env = getenv("JANUS_REC_BWD");  // dev experiment knob: 'p' = plain (unsplit) kernel
-  const bool bwd_wave = L == 2 && B <= 64 && !g.opts.serial_layers && !(bk_env && bk_env[0] == 'p') &&
+  const bool bwd_wave = L == 2 && B <= 64 && !g.opts.serial_layers && !drop && !(bk_env && bk_env[0] == 'p') &&
                         rec_bwd_wf_grid(H) <= 148;
   const bool overlap = g.nccl && g.nccl2 && g.side;  // dp_overlap() held at init
   GemmOp dwdec;  // dW_dec | db_dec = dy^T [h_top | 1]
   dwdec.M = V; dwdec.N = H + 1; dwdec.K = TB;
   dwdec.A = bf(p.off.dy); dwdec.lda = Vp; dwdec.a_mn = 1;
-  dwdec.B = bf(p.off.Hs[L - 1]) + (size_t)B * Hp; dwdec.ldb = Hp; dwdec.b_mn = 1;
+  dwdec.B = layer_in(L); dwdec.ldb = Hp; dwdec.b_mn = 1;
   dwdec.ep.C = fp(p.off.gWdec); dwdec.ep.ldc = Hp;
   LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
                    (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
@@ -590,6 +646,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     o2.B = bf(p.off.Wdec_b); o2.ldb = Hp; o2.b_mn = 1;
     o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
     LCHK("gemm_dh", gemm_bf16(with_flags(o2), st));
+    if (drop) LCHK("dropout", launch_dropout_f32(fp(p.off.dHtop), TB, H, Hp, keyp, L, p.dropout, st));
   }
   auto bwd_args = [&](int l) {
     RecBwdArgs rb;
@@ -609,7 +666,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   }
   auto wgrad_ops = [&](int l, GemmOp &a, GemmOp &b2) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
-    const __nv_bfloat16 *xin = l ? bf(p.off.Hs[l - 1]) + (size_t)B * Hp : bf(p.off.X);
+    const __nv_bfloat16 *xin = l ? layer_in(l) : bf(p.off.X);
     a = GemmOp();  // dW_hh = dz^T h_{t-1}
     a.M = G4; a.N = H; a.K = TB;
     a.A = bf(p.off.DZ[l]); a.lda = p.Gz; a.a_mn = 1;
@@ -655,6 +712,8 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       c2.B = bf(p.off.Wih_b[l]); c2.ldb = Inp; c2.b_mn = 1;
       c2.ep.C = fp(p.off.dX[l]); c2.ep.ldc = Inp;
       LCHK(l ? "gemm_dx1" : "gemm_dx0", gemm_bf16(with_flags(c2), st));
+      // the VJP of the dropout on this layer's input (site l) before the layer below reads it
+      if (drop) LCHK("dropout", launch_dropout_f32(fp(p.off.dX[l]), TB, In, Inp, keyp, l, p.dropout, st));
     }
   }
   int *seg_word = reinterpret_cast<int *>(W + p.off.seg_word);

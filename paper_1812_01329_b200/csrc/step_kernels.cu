@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "philox.cuh"
 #include "step_kernels.h"
 
 namespace jk {
@@ -584,6 +585,67 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
   }
   }
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ dropout
+uint32_t dropout_threshold(float p) {
+  const double t = (double)p * 4294967296.0;
+  return t >= 4294967295.0 ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+// one thread per (row, group of 4 columns): one Philox call gives the group's four words
+__global__ void dropout_bf16_kernel(const __nv_bfloat16 *src, __nv_bfloat16 *dst, int rows, int cols, int ld,
+                                    const int *key, int site, uint32_t thr, float scale) {
+  pdl_enter();
+  const uint2 k = make_uint2((uint32_t)key[0], (uint32_t)key[1]);
+  const int gq = (ld + 3) >> 2;
+  const long long n = (long long)rows * gq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / gq), q = (int)(e - (long long)r * gq);
+    const uint4 w = dropout_words(k, site, r, q);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = 4 * q + i;
+      if (j >= ld) break;
+      const size_t o = (size_t)r * ld + j;
+      const float v = __bfloat162float(src[o]);
+      dst[o] = j < cols ? __float2bfloat16_rn(ws[i] >= thr ? v * scale : 0.f) : src[o];
+    }
+  }
+}
+__global__ void dropout_f32_kernel(float *x, int rows, int cols, int ld, const int *key, int site, uint32_t thr,
+                                   float scale, int row0) {
+  pdl_enter();
+  const uint2 k = make_uint2((uint32_t)key[0], (uint32_t)key[1]);
+  const int gq = (cols + 3) >> 2;
+  const long long n = (long long)rows * gq;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / gq), q = (int)(e - (long long)r * gq);
+    const uint4 w = dropout_words(k, site, row0 + r, q);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = 4 * q + i;
+      if (j >= cols) break;
+      float *p = x + (size_t)r * ld + j;
+      *p = ws[i] >= thr ? *p * scale : 0.f;
+    }
+  }
+}
+cudaError_t launch_dropout_bf16(const __nv_bfloat16 *src, __nv_bfloat16 *dst, int rows, int cols, int ld,
+                                const int *key, int site, float p, cudaStream_t s) {
+  const long long n = (long long)rows * ((ld + 3) / 4);
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 8 * NSM);
+  return launch_pdl(dropout_bf16_kernel, dim3(blocks), dim3(256), 0, s, src, dst, rows, cols, ld, key, site,
+                    dropout_threshold(p), 1.f / (1.f - p));
+}
+cudaError_t launch_dropout_f32(float *x, int rows, int cols, int ld, const int *key, int site, float p,
+                               cudaStream_t s, int row0) {
+  const long long n = (long long)rows * ((cols + 3) / 4);
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 8 * NSM);
+  return launch_pdl(dropout_f32_kernel, dim3(blocks), dim3(256), 0, s, x, rows, cols, ld, key, site,
+                    dropout_threshold(p), 1.f / (1.f - p), row0);
 }
 
 // ------------------------------------------------------------------------------ embedding grad

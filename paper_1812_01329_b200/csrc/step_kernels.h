@@ -82,6 +82,15 @@ cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v
 // per-row softmax cross-entropy: rowloss[r], dy = mask (softmax - onehot) / n_valid (bf16).
 // Row r = t*B + b targets tgt[b][t]; in While mode rows with t >= len_b (or t >= *T_dev) are
 // masked. n_valid: host constant, or computed from lens on the device when lens != nullptr.
+// Inverted dropout (Zaremba [51]; masks: philox.cuh, reading R14) of rows [0, rows) of a
+// time-major matrix (global row r = t * B + b), columns [0, cols): bf16 mode: dst = rb(src * m / (1 -
+// p)) with the columns cols .. ld copied unchanged (the ones column); f32 mode: x *= m / (1 - p) in
+// place. key: device i32[2].
+cudaError_t launch_dropout_bf16(const __nv_bfloat16 *src, __nv_bfloat16 *dst, int rows, int cols, int ld,
+                                const int *key, int site, float p, cudaStream_t s);
+cudaError_t launch_dropout_f32(float *x, int rows, int cols, int ld, const int *key, int site, float p,
+                               cudaStream_t s, int row0 = 0);  // row0: global index of row 0
+uint32_t dropout_threshold(float p);  // floor(p * 2^32), saturated
 cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
                         const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
                         int lddy, float *rowloss, DevStatus *st, cudaStream_t s);
