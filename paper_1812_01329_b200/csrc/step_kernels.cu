@@ -234,44 +234,60 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
   const PrepSeg sg = pl.s[blockIdx.y];
   switch (sg.kind) {
     case P_CAST_ROWS: {
+      // HBM-bound copy: every load of PR rows x (<= 2) 512-column chunks is issued before any
+      // store (up to 128 B in flight per thread; the Little's-law depth an SM needs at ~1 us of
+      // DRAM latency); wider rows fall back to one chunk at a time
+      constexpr int PR = 8;
       const bool pairs = ((sg.ld_src | sg.cols) & 1) == 0 && (reinterpret_cast<uintptr_t>(sg.src) & 7) == 0;
-      for (int r0 = blockIdx.x * CR_ROWS; r0 < sg.rows; r0 += gridDim.x * CR_ROWS) {
-        for (int k0 = 0; k0 < sg.ld_dst; k0 += 512) {
-          const int k = k0 + 2 * threadIdx.x;
-          float2 v[CR_ROWS];
+      const int nkc = (sg.ld_dst + 511) / 512;
+      for (int r0 = blockIdx.x * PR; r0 < sg.rows; r0 += gridDim.x * PR) {
+        for (int kc0 = 0; kc0 < nkc; kc0 += 2) {
+          float2 v[PR][2];
 #pragma unroll
-          for (int q = 0; q < CR_ROWS; ++q) {
-            const int r = r0 + q;
-            v[q] = make_float2(0.f, 0.f);
-            if (r < sg.rows && k < sg.cols) {
-              const int rs = sg.H > 0 ? (r & 3) * sg.H + (r >> 2) : r;
-              const float *sr = sg.src + (size_t)rs * sg.ld_src;
-              if (pairs) v[q] = *reinterpret_cast<const float2 *>(sr + k);
-              else { v[q].x = sr[k]; if (k + 1 < sg.cols) v[q].y = sr[k + 1]; }
+          for (int q = 0; q < PR; ++q)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int r = r0 + q, k = (kc0 + c) * 512 + 2 * threadIdx.x;
+              v[q][c] = make_float2(0.f, 0.f);
+              if (r < sg.rows && k < sg.cols) {
+                const int rs = sg.H > 0 ? (r & 3) * sg.H + (r >> 2) : r;
+                const float *sr = sg.src + (size_t)rs * sg.ld_src;
+                if (pairs) v[q][c] = __ldcs(reinterpret_cast<const float2 *>(sr + k));
+                else { v[q][c].x = sr[k]; if (k + 1 < sg.cols) v[q][c].y = sr[k + 1]; }
+              }
             }
-          }
 #pragma unroll
-          for (int q = 0; q < CR_ROWS; ++q)
-            if (r0 + q < sg.rows && k < sg.ld_dst)
-              reinterpret_cast<__nv_bfloat162 *>(sg.dst + (size_t)(r0 + q) * sg.ld_dst)[k >> 1] =
-                  __floats2bfloat162_rn(v[q].x, v[q].y);
+          for (int q = 0; q < PR; ++q)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int k = (kc0 + c) * 512 + 2 * threadIdx.x;
+              if (r0 + q < sg.rows && k < sg.ld_dst)  // ld_dst is even
+                reinterpret_cast<__nv_bfloat162 *>(sg.dst + (size_t)(r0 + q) * sg.ld_dst)[k >> 1] =
+                    __floats2bfloat162_rn(v[q][c].x, v[q][c].y);
+            }
         }
       }
     } break;
-    case P_CAST_T_IL: {  // WT[u][ri] = rb(W[rc][u]), 32 x 32 tiles, threads as 32 x 8
-      __shared__ float tile[32][33];
+    case P_CAST_T_IL: {  // WT[u][ri] = rb(W[rc][u]): panels of 32 ri x 128 u, threads as 32 x 8
+      __shared__ float tile[32][129];
       const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-      const int H = sg.H, nti = (4 * H + 31) / 32, ntu = (H + 31) / 32;
-      for (int tb = blockIdx.x; tb < nti * ntu; tb += gridDim.x) {
-        const int ri0 = (tb % nti) * 32, u0 = (tb / nti) * 32;
-        for (int i = ty; i < 32; i += 8) {
-          const int ri = ri0 + i, u = u0 + tx;
-          float v = 0.f;
-          if (ri < 4 * H && u < H) v = sg.src[(size_t)((ri & 3) * H + (ri >> 2)) * H + u];
-          tile[i][tx] = v;
-        }
+      const int H = sg.H, nti = (4 * H + 31) / 32, ntp = (H + 127) / 128;
+      for (int tb = blockIdx.x; tb < nti * ntp; tb += gridDim.x) {
+        const int ri0 = (tb % nti) * 32, u0 = (tb / nti) * 128;
+        float v[4][4];  // all 16 loads of the panel in flight before the shared-memory stores
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int ri = ri0 + ty + 8 * a, u = u0 + 32 * c + tx;
+            v[a][c] = (ri < 4 * H && u < H) ? __ldcs(sg.src + (size_t)((ri & 3) * H + (ri >> 2)) * H + u) : 0.f;
+          }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) tile[ty + 8 * a][32 * c + tx] = v[a][c];
         __syncthreads();
-        for (int i = ty; i < 32; i += 8) {
+        for (int i = ty; i < 128; i += 8) {
           const int u = u0 + i, ri = ri0 + tx;
           if (u < H && ri < 4 * H) sg.dst[(size_t)u * sg.ld_dst + ri] = __float2bfloat16_rn(tile[tx][i]);
         }
