@@ -176,14 +176,14 @@ def run_reference(args):
     cb = {"value": v, "unit": "samples/s", "cores": _blas_threads(), "kind": "oracle",
           "sample": f"each step: oracle.run_graph_step on B={B} sequences x T={T} tokens of the C2 model; "
                     f"value in 35-token sequence equivalents"}
-    print(json.dumps({"impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": "samples/s",
+    emit({"impl": "reference", "metric": BASELINE_METRIC, "value": v, "unit": "samples/s",
                       "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                       "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True,
                       "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                       "config": {"workload": WORKLOADS["c2"]["desc"], "global_batch": 64, "seq_len": 35,
                                  "parallelism": "none (host oracle)"},
                       "cpu_baseline": cb,
-                      "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+                      "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
 # ----------------------------------------------------------------------------- extra measurements
@@ -355,6 +355,21 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         del sess
         # --- C4: data-dependent trip counts on the device (While + RANGE guard), SURVEY §8(d)
         out["c4"] = c4_extra(J, torch, stream, timed, K)
+        # --- the data-parallel step on a 1-rank communicator (force_dp): NCCL allreduce of the
+        # gradient arena vs the reduction fused into the weight-gradient GEMM epilogue (NEXT-3)
+        dp1 = {}
+        for name, kw in (("nccl_allreduce", {}), ("fused_epilogue", {"fused_allreduce": True})):
+            gp = J.Graph(prog, force_dp=True, no_dp_overlap=True, **kw)
+            wsp = gp.new_workspace()
+            stp = [s.clone() for s in state]
+            lossp = torch.zeros(1, device="cuda")
+            for k in range(3):
+                gp.run(dev_batches[k % len(dev_batches)], stp, wsp, outs=[lossp], stream=stream)
+            msp = timed(lambda k: gp.run(dev_batches[k % len(dev_batches)], stp, wsp, outs=[lossp], stream=stream), K) / K
+            dp1[name] = {"samples_per_s": B * 1000.0 / msp, "ms_per_step": msp}
+            del wsp, gp
+        out["dp_1rank"] = dict(dp1, note="force_dp on one GPU: the collective sequence runs on a 1-rank "
+                                         "communicator (no NVLink traffic); measures the protocol's own cost")
         # --- the Zaremba regularised LM (NEXT-4; [51] via P:312, PTB medium = the C2 shape): dropout
         # 0.5 on every non-recurrent connection, Philox masks keyed per step (layers run serially)
         pd = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=B, T=35, lr=1.0, dropout=0.5, training_flag=True)
@@ -464,7 +479,26 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
 
 
 # ----------------------------------------------------------------------------- main arm
+_JSON_FD = None
+
+
+def emit(obj):
+    """The one JSON line of the run, on the process's original stdout."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
+
+
 def main():
+    # stdout carries exactly one JSON line: everything else written to file descriptor 1 — NCCL's
+    # version banner and NCCL_DEBUG output, any native print — is sent to stderr
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -640,7 +674,7 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()
     if rank == 0:
-        print(json.dumps(out))
+        emit(out)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

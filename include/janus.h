@@ -216,7 +216,10 @@ typedef struct {
   int32_t force_dp;          /* 1 with world_size == 1: run the data-parallel collective path
                                 (arena allreduce, agreement, null step) on a 1-rank communicator */
   int32_t no_dp_overlap;     /* 1: no early dW_dec allreduce on the split communicator          */
-  int32_t reserved[1];
+  int32_t fused_allreduce;   /* 1 (data parallel, 2-layer LM): the weight gradients are reduced
+                                across ranks inside the weight-gradient GEMM's epilogue over
+                                NVLink peer memory (NCCL symmetric windows, NCCL-owned), tile by
+                                tile as the tiles finish (NEXT-3); else one NCCL allreduce      */
 } janus_build_opts;
 
 typedef struct janus_graph janus_graph;

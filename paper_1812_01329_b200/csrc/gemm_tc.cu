@@ -20,6 +20,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "fused_ar.cuh"
 #include "gemm_tc.h"
 
 namespace jk {
@@ -350,8 +351,19 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
-        if (lane == 0) bulk_wait_group_read0();  // both boxes free before the next tile
-        __syncwarp();
+        if (ep.fr.win) {
+          // fused cross-rank reduction (NEXT-3): the tile's stores must have COMPLETED (not only
+          // read their boxes) before the owner may read it; then the per-tile protocol
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            fence_proxy_async_global();  // the tile's TMA (async-proxy) writes -> generic loads
+          }
+          __syncwarp();
+          fr_tile(ep.fr, tr.tile, m0, n0, BN, M, N, ep.ldc, quad * 32 + lane);
+        } else {
+          if (lane == 0) bulk_wait_group_read0();  // both boxes free before the next tile
+          __syncwarp();
+        }
       } else if (splits == 1) {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -559,7 +571,8 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
     const int nk = (op.K + 63) / 64;
     const size_t cap_tiles = op.partials ? op.partials_cap / (128 * BN) : 0;
     int splits = 1;
-    if (CM == 1 && n == 1 && op.flags && op.partials) {  // split-K only for single launches (own scratch)
+    if (op.ep.fr.win && !gb.tma_store[g]) return cudaErrorInvalidValue;  // fused reduction: TMA-store path
+    if (CM == 1 && n == 1 && op.flags && op.partials && !op.ep.fr.win) {  // split-K only for single launches (own scratch)
       splits = op.splits > 0 ? op.splits : choose_splits(tm.Mb * tm.Nb, nk, g_num_sms, cap_tiles);
       splits = std::max(1, std::min(splits, 64));
       if ((size_t)tm.Mb * tm.Nb * splits > cap_tiles) splits = 1;
@@ -621,6 +634,18 @@ static cudaError_t check_op(const GemmOp &op) {
 // BN = 256 tiles keep the tensor pipe busiest — as long as the launch still has enough tiles to
 // occupy the SMs (else BN = 128 for twice the tiles). Decided per launch (grouped GEMMs together).
 static bool wide_of(const GemmOp &op) { return op.N > 128; }
+static bool use_bn256(const GemmOp *ops, int n);
+void gemm_group_tiling(const GemmOp *ops, int n, int *bn, int *mblocks, int *nblocks) {
+  const int BN = use_bn256(ops, n) ? 256 : 128;
+  bool split = false;
+  for (int g = 0; g < n; ++g) split = split || (op_wants_split(ops[g]) && n == 1);
+  const int CM = (g_gemm_cm == 2 && !split) ? 2 : 1;
+  *bn = BN;
+  for (int g = 0; g < n; ++g) {
+    mblocks[g] = (((ops[g].M + 127) / 128 + CM - 1) / CM) * CM;
+    nblocks[g] = (ops[g].N + BN - 1) / BN;
+  }
+}
 static bool use_bn256(const GemmOp *ops, int n) {
   long tiles = 0;
   for (int i = 0; i < n; ++i) {

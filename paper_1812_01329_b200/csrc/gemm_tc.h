@@ -6,6 +6,22 @@
 
 namespace jk {
 
+// NEXT-3: gradient reduction fused into the weight-gradient GEMM's epilogue (P:298 — the
+// collective inside the step — done over NVLink peer memory, tile by tile, as the tiles finish).
+// C lives in an NCCL symmetric window (load/store accessible on every rank of the node); tile t
+// is owned by rank t mod nranks: every rank signals the owner when its tile t is written, the
+// owner sums the ranks' tiles in rank order (deterministic, bit-identical everywhere), writes
+// the sum into every rank's window and signals each rank. Flags are epoch counters: never reset.
+struct FusedReduce {
+  void *win = nullptr;   // ncclWindow_t of the arena (nullptr: no fused reduction)
+  size_t c_off = 0;      // byte offset of this GEMM's C inside the arena window
+  void *fwin = nullptr;  // ncclWindow_t of the tile flags
+  size_t flag_off = 0;   // byte offset of this GEMM's flags (2 x u32 per tile: ready, reduced)
+  int nranks = 1, rank = 0;
+  unsigned epoch = 0;    // this step's epoch (1, 2, ...): ready counts reach epoch * nranks
+  int force_pull = 0;    // test hook: run the owner's pull / sum / push even with one rank
+};
+
 struct GemmEpilogue {
   float *C = nullptr;               // fp32 output [M, ldc] (row-major), may be null
   int ldc = 0;
@@ -14,6 +30,7 @@ struct GemmEpilogue {
   const float *bias_col = nullptr;  // + bias[n]
   const float *bias_row = nullptr;  // + bias[m]
   int accumulate = 0;               // C += result
+  FusedReduce fr;                   // fused cross-rank reduction of C (TMA-store path only)
 };
 
 // D[M,N] = A[M,K] . B[N,K]^T.
@@ -44,6 +61,9 @@ cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);
 // configuration (operand majors, tile width) are grouped; split-K applies to single launches only.
 cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st);
 size_t gemm_flags_count(int M, int N);  // flags needed by a split-K launch of an M x N GEMM
+// Tile geometry a grouped launch uses for each op (BN, M blocks incl. cluster ghosts, N blocks):
+// the fused reduction's tile ids are mb + mblocks * nb.
+void gemm_group_tiling(const GemmOp *ops, int n, int *bn, int *mblocks, int *nblocks);
 bool make_tmap_bf16(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_outer);
 bool make_tmap_bf16_chunks(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t ld,

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/janus.h"
+#include "fused_ar.h"
 #include "step_kernels.h"
 
 namespace jk {
@@ -137,6 +138,8 @@ struct Graph {
   cudaStream_t side = nullptr;             // stream of the overlapped collective
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
+  bool fused_ar = false; // NEXT-3: weight gradients reduced in the wgrad GEMM epilogue (fixed at build)
+  FusedArena far;        // its NCCL symmetric windows (created with the communicator)
   // protocol-test transport (janus_dev_dp_set_host_collective): host buffers, caller's allreduce
   int32_t (*host_coll)(void *ctx, void *buf, int64_t count, int32_t dtype, int32_t op) = nullptr;
   void *host_coll_ctx = nullptr;

@@ -12,6 +12,7 @@
 
 #include "host.h"
 #include "../../include/janus_dev.h"
+#include "lm_rec.h"
 
 #define TREE_MAX_LEVELS_HOST 130  // tree.h TREE_MAX_LEVELS
 
@@ -275,7 +276,12 @@ janus_status janus_graph_build(const janus_op *ops, int32_t n_ops, const janus_a
   }
   g->dp = dp_wanted(g->opts);
   std::string why_lm, why_tree;
-  if (lower_lm(*g, why_lm)) g->kind = "lstm_lm";
+  if (lower_lm(*g, why_lm)) {
+    g->kind = "lstm_lm";
+    const LmPlan &p = g->lm;  // the fused reduction rides on the grouped weight-gradient launch
+    g->fused_ar = g->dp && g->opts.fused_allreduce && p.bf16 && p.L == 2 && p.B <= 64 && p.key_arg < 0 &&
+                  !g->opts.serial_layers && rec_bwd_wf_grid(p.H) <= 148;
+  }
   else if (lower_tree(*g, why_tree)) g->kind = "treelstm";
   else g->unsupported_reason = "lstm_lm: " + why_lm + "; treelstm: " + why_tree;
   g->imp_ws_bytes = imperative_ws_bytes(*g);

@@ -417,6 +417,48 @@ janus_status finish(Graph &g, DevStatus *dst, const janus_tensor *outs, int n_ou
     if (e_ != cudaSuccess) return JANUS_ERR_CUDA; \
   } while (0)
 
+// The grouped weight-gradient launch of the 2-layer backward wavefront, shapes only (the same list
+// for a step and for its null step, so both reduce the same tiles): [dW_dec | db_dec], dW_hh1,
+// [dW_ih1 | db1], dW_hh0, [dW_ih0 | db0] — gradients (c_off = arena byte offset of C) — and the
+// embedding dgrad dx0 (not a gradient, when E is trained).
+struct WgShape {
+  int M, N, K, ldc;
+  size_t c_off;
+  bool grad;
+};
+static int lm_wgrad_shapes(const LmPlan &p, bool with_dwdec, WgShape *w) {
+  const int TB = p.B * p.T, G4 = 4 * p.H, H = p.H, E = p.E;
+  const size_t a0 = p.off.arena_begin;
+  int n = 0;
+  if (with_dwdec) w[n++] = {p.V, H + 1, TB, p.Hp, p.off.gWdec - a0, true};
+  for (int l = 1; l >= 0; --l) {
+    w[n++] = {G4, H, TB, p.Hp, p.off.gWhh[l] - a0, true};
+    w[n++] = {G4, (l ? H : E) + 1, TB, l ? p.Hp : p.Ep, p.off.gWih[l] - a0, true};
+  }
+  if (p.lr_E != 0) w[n++] = {TB, E, G4, p.Ep, 0, false};
+  return n;
+}
+// Tile geometry and per-GEMM descriptors of the fused reduction for this step's epoch; returns the
+// number of fused tiles (their flags are 0 .. tiles-1 of the flag window).
+static int lm_fused_plan(const Graph &g, bool with_dwdec, unsigned epoch, FusedReduce *fr, FusedGeom *geo, int *ng) {
+  WgShape w[6];
+  const int n = lm_wgrad_shapes(g.lm, with_dwdec, w);
+  GemmOp ops[6];
+  for (int i = 0; i < n; ++i) { ops[i].M = w[i].M; ops[i].N = w[i].N; ops[i].K = w[i].K; }
+  int bn = 0, mb[6], nb[6];
+  gemm_group_tiling(ops, n, &bn, mb, nb);
+  int tiles = 0, k = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!w[i].grad) { fr[i] = FusedReduce(); continue; }
+    fr[i] = fused_descriptor(g.far, w[i].c_off, (size_t)tiles, epoch);
+    geo[k] = FusedGeom{w[i].M, w[i].N, w[i].ldc, mb[i], nb[i], bn};
+    ++k;
+    tiles += mb[i] * nb[i];
+  }
+  *ng = k;
+  return tiles;
+}
+
 janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *state,
                     const janus_tensor *outs, int n_outs, const janus_tensor &ws, cudaStream_t st,
                     janus_failure *fail) {
@@ -516,6 +558,11 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     janus_status r = dp_init(g);
     if (r != JANUS_OK) return r;
   }
+  // gradient arena: the workspace, or NCCL's symmetric window when reduced in the GEMM epilogue
+  auto ar = [&](size_t off) -> float * {
+    return g.far.arena ? reinterpret_cast<float *>(static_cast<uint8_t *>(g.far.arena) + (off - p.off.arena_begin))
+                       : reinterpret_cast<float *>(W + off);
+  };
   const int T = p.T;              // unrolled T or max width W
   const int Tw = p.while_mode ? Wd : T;  // width of this batch
   const int TB = Tw * B;
@@ -617,14 +664,17 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   // two layers, B <= 64: one backward wavefront launch (layer 0 one step behind layer 1, the
   // dgrad of layer 1's input W_ih1^T dz1_t folded into layer 0's recurrent MMA)
   const char *bk_env = getenv("JANUS_REC_BWD");  // dev experiment knob: 'p' = plain (unsplit) kernel
-  const bool bwd_wave = L == 2 && B <= 64 && !g.opts.serial_layers && !drop && !(bk_env && bk_env[0] == 'p') &&
-                        rec_bwd_wf_grid(H) <= 148;
+  const bool bwd_wave = g.fused_ar || (L == 2 && B <= 64 && !g.opts.serial_layers && !drop &&
+                                        !(bk_env && bk_env[0] == 'p') && rec_bwd_wf_grid(H) <= 148);
   const bool overlap = g.nccl && g.nccl2 && g.side;  // dp_overlap() held at init
+  const bool fused = g.fused_ar && g.far.arena && bwd_wave;
+  const unsigned fused_epoch = fused ? ++g.far.epoch : 0u;
+  int fused_tiles = 0;
   GemmOp dwdec;  // dW_dec | db_dec = dy^T [h_top | 1]
   dwdec.M = V; dwdec.N = H + 1; dwdec.K = TB;
   dwdec.A = bf(p.off.dy); dwdec.lda = Vp; dwdec.a_mn = 1;
   dwdec.B = layer_in(L); dwdec.ldb = Hp; dwdec.b_mn = 1;
-  dwdec.ep.C = fp(p.off.gWdec); dwdec.ep.ldc = Hp;
+  dwdec.ep.C = ar(p.off.gWdec); dwdec.ep.ldc = Hp;
   LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
                    (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
   {
@@ -635,7 +685,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
         return JANUS_ERR_CUDA;
       for (const DpSeg &sg : dp_segments(g))  // the split communicator's segments (dW_dec | db_dec)
         if (sg.comm == 2) {
-          janus_status r = dp_allreduce_sum2(g, fp(sg.begin), (sg.end - sg.begin) / 4, g.side);
+          janus_status r = dp_allreduce_sum2(g, ar(sg.begin), (sg.end - sg.begin) / 4, g.side);
           if (r != JANUS_OK) return r;
         }
       if (cudaEventRecord(g.ev_join, g.side) != cudaSuccess) return JANUS_ERR_CUDA;
@@ -671,12 +721,12 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     a.M = G4; a.N = H; a.K = TB;
     a.A = bf(p.off.DZ[l]); a.lda = p.Gz; a.a_mn = 1;
     a.B = bf(p.off.Hs[l]); a.ldb = Hp; a.b_mn = 1;
-    a.ep.C = fp(p.off.gWhh[l]); a.ep.ldc = Hp;
+    a.ep.C = ar(p.off.gWhh[l]); a.ep.ldc = Hp;
     b2 = GemmOp();  // dW_ih | db = dz^T [x | 1]
     b2.M = G4; b2.N = In + 1; b2.K = TB;
     b2.A = bf(p.off.DZ[l]); b2.lda = p.Gz; b2.a_mn = 1;
     b2.B = xin; b2.ldb = Inp; b2.b_mn = 1;
-    b2.ep.C = fp(p.off.gWih[l]); b2.ep.ldc = Inp;
+    b2.ep.C = ar(p.off.gWih[l]); b2.ep.ldc = Inp;
   };
   if (bwd_wave) {  // every weight gradient + the embedding dgrad in one grouped launch
     GemmOp ops[6];
@@ -693,6 +743,13 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       c2.A = bf(p.off.DZ[0]); c2.lda = p.Gz;
       c2.B = bf(p.off.Wih_b[0]); c2.ldb = Ep; c2.b_mn = 1;
       c2.ep.C = fp(p.off.dX[0]); c2.ep.ldc = Ep;
+    }
+    if (fused) {  // NEXT-3: each gradient tile reduced across ranks by the epilogue as it finishes
+      FusedReduce fr[6];
+      FusedGeom geo[6];
+      int ng = 0;
+      fused_tiles = lm_fused_plan(g, !overlap, fused_epoch, fr, geo, &ng);
+      for (int i = 0; i < n; ++i) ops[i].ep.fr = fr[i];
     }
     LCHK("gemm_wgrad", gemm_bf16_group(ops, n, st));
   }
@@ -727,11 +784,11 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   if (g.nccl) {
     // DP: dense embedding gradient, one allreduce(sum) of the whole gradient arena
     if (p.lr_E != 0)
-      LCHK("dp_scatter", launch_scatter_rows(fp(p.off.seg_grad), Ep, seg_word, nseg, fp(p.off.dEd), V, E, st));
+      LCHK("dp_scatter", launch_scatter_rows(fp(p.off.seg_grad), Ep, seg_word, nseg, ar(p.off.dEd), V, E, st));
     g.prof.mark("dp_allreduce", st);
     for (const DpSeg &sg : dp_segments(g))
       if (sg.comm == 1) {
-        janus_status r = dp_allreduce_sum(g, fp(sg.begin), (sg.end - sg.begin) / 4, st);
+        janus_status r = dp_allreduce_sum(g, ar(sg.begin), (sg.end - sg.begin) / 4, st);
         if (r != JANUS_OK) return r;
       }
     if (overlap && cudaStreamWaitEvent(st, g.ev_join, 0) != cudaSuccess) return JANUS_ERR_CUDA;
@@ -742,6 +799,10 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     janus_status r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
     if (r != JANUS_OK) return r;
   }
+  if (fused) {  // every tile of this step reduced (the owners' pushes into this rank landed)
+    FusedReduce f0 = fused_descriptor(g.far, 0, 0, fused_epoch);
+    LCHK("fused_wait", launch_fused_wait(f0, fused_tiles, st));
+  }
   // ---- the all-or-nothing commit (P:164, P:266 (4))
   CommitList cl{};
   auto add = [&](CommitSeg s) { cl.s[cl.n++] = s; };
@@ -749,9 +810,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   for (int l = 0; l < L; ++l) {
     const int In = l ? H : E, Inp = l ? Hp : Ep;
     CommitSeg s{};
-    if (p.lr_Wih[l] != 0) { s = {}; s.kind = C_DENSE_IL; s.dst = P.Wih[l]; s.grad = fp(p.off.gWih[l]); s.rows = G4; s.cols = In; s.ldg = Inp; s.H = H; s.lr = p.lr_Wih[l] / nr; add(s); }
-    if (p.lr_b[l] != 0) { s = {}; s.kind = C_BIAS_COL_IL; s.dst = P.b[l]; s.grad = fp(p.off.gWih[l]); s.rows = G4; s.cols = 1; s.ldg = Inp; s.col = In; s.H = H; s.lr = p.lr_b[l] / nr; add(s); }
-    if (p.lr_Whh[l] != 0) { s = {}; s.kind = C_DENSE_IL; s.dst = P.Whh[l]; s.grad = fp(p.off.gWhh[l]); s.rows = G4; s.cols = H; s.ldg = Hp; s.H = H; s.lr = p.lr_Whh[l] / nr; add(s); }
+    if (p.lr_Wih[l] != 0) { s = {}; s.kind = C_DENSE_IL; s.dst = P.Wih[l]; s.grad = ar(p.off.gWih[l]); s.rows = G4; s.cols = In; s.ldg = Inp; s.H = H; s.lr = p.lr_Wih[l] / nr; add(s); }
+    if (p.lr_b[l] != 0) { s = {}; s.kind = C_BIAS_COL_IL; s.dst = P.b[l]; s.grad = ar(p.off.gWih[l]); s.rows = G4; s.cols = 1; s.ldg = Inp; s.col = In; s.H = H; s.lr = p.lr_b[l] / nr; add(s); }
+    if (p.lr_Whh[l] != 0) { s = {}; s.kind = C_DENSE_IL; s.dst = P.Whh[l]; s.grad = ar(p.off.gWhh[l]); s.rows = G4; s.cols = H; s.ldg = Hp; s.H = H; s.lr = p.lr_Whh[l] / nr; add(s); }
     if (p.write_h) {
       s = {}; s.kind = C_COPY; s.dst = P.h[l]; s.grad = fp(p.off.hT[l]); s.rows = B; s.cols = H; add(s);
       s = {}; s.kind = C_COPY; s.dst = P.c[l]; s.grad = fp(p.off.cT[l]); s.rows = B; s.cols = H; add(s);
@@ -759,10 +820,10 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   }
   {
     CommitSeg s{};
-    if (p.lr_Wdec != 0) { s = {}; s.kind = C_DENSE; s.dst = P.Wdec; s.grad = fp(p.off.gWdec); s.rows = V; s.cols = H; s.ldg = Hp; s.lr = p.lr_Wdec / nr; add(s); }
-    if (p.lr_bdec != 0) { s = {}; s.kind = C_BIAS_COL; s.dst = P.bdec; s.grad = fp(p.off.gWdec); s.rows = V; s.cols = 1; s.ldg = Hp; s.col = H; s.lr = p.lr_bdec / nr; add(s); }
+    if (p.lr_Wdec != 0) { s = {}; s.kind = C_DENSE; s.dst = P.Wdec; s.grad = ar(p.off.gWdec); s.rows = V; s.cols = H; s.ldg = Hp; s.lr = p.lr_Wdec / nr; add(s); }
+    if (p.lr_bdec != 0) { s = {}; s.kind = C_BIAS_COL; s.dst = P.bdec; s.grad = ar(p.off.gWdec); s.rows = V; s.cols = 1; s.ldg = Hp; s.col = H; s.lr = p.lr_bdec / nr; add(s); }
     if (p.lr_E != 0 && !g.nccl) { s = {}; s.kind = C_SPARSE_ROWS; s.dst = P.E; s.grad = fp(p.off.seg_grad); s.cols = E; s.ldg = Ep; s.rows_idx = seg_word; s.nrows = nseg; s.lr = p.lr_E / nr; add(s); }
-    if (p.lr_E != 0 && g.nccl) { s = {}; s.kind = C_DENSE; s.dst = P.E; s.grad = fp(p.off.dEd); s.rows = V; s.cols = E; s.ldg = E; s.lr = p.lr_E / nr; add(s); }
+    if (p.lr_E != 0 && g.nccl) { s = {}; s.kind = C_DENSE; s.dst = P.E; s.grad = ar(p.off.dEd); s.rows = V; s.cols = E; s.ldg = E; s.lr = p.lr_E / nr; add(s); }
     if (p.write_tag && P.tag) { s = {}; s.kind = C_TAG; s.idst = P.tag; s.ival = 1; add(s); }
   }
   if (p.train_arg >= 0 && !p.train_specialised)  // the training Switch evaluated on the device
@@ -791,9 +852,24 @@ janus_status run_lm_null(Graph &g, const janus_failure &f, const janus_tensor &w
   unsigned *bars = reinterpret_cast<unsigned *>(W + p.off.barriers);
   LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
   LCHK("set_failure", launch_set_failure(dst, f.assumption_id, f.index, f.observed, st));
+  if (g.fused_ar && g.far.arena) {
+    // the fused reduction's part of the step: publish every tile, reduce the tiles this rank
+    // owns (stale data: the agreement aborts the step), wait for the owners' pushes
+    const unsigned ep = ++g.far.epoch;
+    FusedReduce fr[6], frg[6];
+    FusedGeom geo[6];
+    int ng = 0;
+    const int tiles = lm_fused_plan(g, g.nccl2 == nullptr, ep, fr, geo, &ng);
+    int k = 0;
+    for (int i = 0; i < 6 && k < ng; ++i)
+      if (fr[i].win) frg[k++] = fr[i];
+    LCHK("fused_null", launch_fused_null(frg, geo, ng, st));
+    LCHK("fused_wait", launch_fused_wait(fused_descriptor(g.far, 0, 0, ep), tiles, st));
+  }
   // the same per-communicator sequence as a full step (dp_segments in order)
   for (const DpSeg &sg : dp_segments(g)) {
-    float *b = reinterpret_cast<float *>(W + sg.begin);
+    float *b = g.far.arena ? reinterpret_cast<float *>(static_cast<uint8_t *>(g.far.arena) + (sg.begin - p.off.arena_begin))
+                           : reinterpret_cast<float *>(W + sg.begin);
     r = sg.comm == 2 ? dp_allreduce_sum2(g, b, (sg.end - sg.begin) / 4, st)
                      : dp_allreduce_sum(g, b, (sg.end - sg.begin) / 4, st);
     if (r != JANUS_OK) return r;

@@ -52,7 +52,7 @@ class JanusBuildOpts(C.Structure):
     _fields_ = [("world_size", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_uint8 * 128),
                 ("gemm_dtype", C.c_int32), ("strip_asserts", C.c_int32),
                 ("fail_assert_id", C.c_int32), ("serial_layers", C.c_int32), ("tree_grid", C.c_int32),
-                ("force_dp", C.c_int32), ("no_dp_overlap", C.c_int32), ("reserved", C.c_int32 * 1)]
+                ("force_dp", C.c_int32), ("no_dp_overlap", C.c_int32), ("fused_allreduce", C.c_int32)]
 
 
 class JanusSessionOpts(C.Structure):
@@ -227,7 +227,7 @@ class Graph:
 
     def __init__(self, program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False,
                  fail_assert_id=-1, **ablation):
-        """ablation: serial_layers, tree_grid, force_dp, no_dp_overlap (janus_build_opts)."""
+        """ablation: serial_layers, tree_grid, force_dp, no_dp_overlap, fused_allreduce (janus_build_opts)."""
         self.program = program
         opts = _build_opts(program, gemm, world_size, rank, nccl_id, strip_asserts, fail_assert_id, **ablation)
         self._ops = marshal_ops(program)
@@ -292,8 +292,9 @@ lib.janus_nccl_unique_id.argtypes = [C.c_void_p]
 
 
 def _build_opts(program, gemm=None, world_size=1, rank=0, nccl_id=None, strip_asserts=False, fail_assert_id=-1,
-                serial_layers=False, tree_grid=0, force_dp=False, no_dp_overlap=False):
+                serial_layers=False, tree_grid=0, force_dp=False, no_dp_overlap=False, fused_allreduce=False):
     opts = JanusBuildOpts()
+    opts.fused_allreduce = int(fused_allreduce)
     opts.serial_layers, opts.tree_grid = int(serial_layers), int(tree_grid)
     opts.force_dp, opts.no_dp_overlap = int(force_dp), int(no_dp_overlap)
     opts.world_size, opts.rank = world_size, rank

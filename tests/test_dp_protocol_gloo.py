@@ -154,3 +154,16 @@ def test_agreement_every_rank_decodes_the_same_outcome(two_ranks, name):
         (ASSUMPTION_FAILED, dict(assumption_id=3, rank=1, index=2, observed=8)),
     ]
     assert o0 == expect
+
+
+def test_fused_reduction_leaves_only_the_embedding_gradient_to_nccl():
+    """With fused_allreduce the weight gradients are reduced in the GEMM epilogue (NEXT-3); the
+    step's NCCL segments shrink to the dense embedding gradient (rank-independent plan)."""
+    from paper_1812_01329_b200 import janus as J
+    prog = pg.lstm_lm_program(V=64, E=40, H=48, L=2, B=8, T=6, lr=0.5)
+    plain = J.Graph(prog, world_size=2, rank=0, nccl_id=bytes(128))
+    fused = J.Graph(prog, world_size=2, rank=1, nccl_id=bytes(128), fused_allreduce=True)
+    ed = J.dev_workspace_region_bytes(plain, "lm.dEd")
+    a0, alen = J.dev_workspace_region_bytes(plain, "arena")
+    assert [s[0] for s in J.dev_dp_segments(plain)] == [2, 1]
+    assert J.dev_dp_segments(fused) == [(1, ed[0], a0 + alen - ed[0])]

@@ -125,3 +125,42 @@ def test_lm_whole_step_deterministic():
         assert st == I.OK
         outs.append((loss.item(), to_host(dev)))
     assert outs[0][0] == outs[1][0] and _same(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("size,pull", [("small", False), ("small", True), ("c2", True)])
+def test_fused_gradient_reduction_single_rank(size, pull, monkeypatch):
+    """NEXT-3 on a 1-rank communicator: the weight gradients live in NCCL symmetric windows and
+    are reduced tile by tile in the weight-gradient GEMM's epilogue (publish, owner sum in rank
+    order, push, per-tile epoch flags) instead of an NCCL allreduce. With one rank the sum is the
+    tile itself, so the step must equal the NCCL path bit for bit (same grouped launch: no early
+    dW_dec allreduce on either side), across steps (epochs) and around a null step. pull=True
+    (JANUS_FUSED_FORCE_PULL) runs the owner's pull / sum / push data path, which one rank skips."""
+    if pull:
+        monkeypatch.setenv("JANUS_FUSED_FORCE_PULL", "1")
+    if size == "small":
+        B, T, V, E, H = 8, 6, 64, 40, 48
+    else:
+        B, T, V, E, H = 64, 35, 10000, 650, 650
+    prog = pg.lstm_lm_program(V=V, E=E, H=H, L=2, B=B, T=T, lr=0.5)
+    janus = J()
+    g1 = janus.Graph(prog, force_dp=True, no_dp_overlap=True)
+    g2 = janus.Graph(prog, force_dp=True, no_dp_overlap=True, fused_allreduce=True)
+    state = gen.uniform_params(prog, 9, 0.05)
+    batches = list(gen.lm_batches(gen.SEED_C2, B, T, V, 3))
+    d1, d2 = to_dev(state), to_dev(state)
+    w1, w2 = g1.new_workspace(), g2.new_workspace()
+    for k, args in enumerate(batches):
+        l1, l2 = torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda")
+        s1, _ = g1.run(to_dev(list(args)), d1, w1, outs=[l1])
+        s2, _ = g2.run(to_dev(list(args)), d2, w2, outs=[l2])
+        assert s1 == s2 == I.OK and l1.item() == l2.item()
+        assert _same(to_host(d1), to_host(d2)), f"step {k}"
+        if k == 0:  # a null step (dispatch miss: B-1 rows) on both, then the next step as usual
+            tok, tgt, ln = args
+            a = [tok[:B - 1], tgt[:B - 1], ln[:B - 1]]
+            s1, f1 = g1.run(to_dev(a), d1, w1)
+            s2, f2 = g2.run(to_dev(a), d2, w2)
+            assert s1 == s2 == I.ASSUMPTION_FAILED and f1 == f2
+    if size == "small":
+        ora = I.run_graph_step(prog, list(batches[0]), state, mode="bf16")
+        assert ora.status == I.OK
