@@ -117,6 +117,33 @@ struct PhaseProf {
   }
 };
 
+// Identity of a captured step: the same workspace, state tensors, batch width and stream replay
+// the same graph (every argument is staged into fixed workspace slots first).
+struct GraphKey {
+  const void *W = nullptr;
+  const void *state[64] = {};
+  int width = 0;
+  const void *stream = nullptr;
+  bool operator==(const GraphKey &o) const {
+    if (W != o.W || width != o.width || stream != o.stream) return false;
+    for (int k = 0; k < 64; ++k)
+      if (state[k] != o.state[k]) return false;
+    return true;
+  }
+};
+struct StepGraph {
+  void *exec = nullptr;  // cudaGraphExec_t
+  GraphKey key;
+  uint64_t kernels = 0;  // launches one replay stands for
+  bool seen = false;     // a direct run with seen_key happened: the next one captures
+  GraphKey seen_key;
+  bool failed = false;   // capture not possible: direct launches only
+  void reset() {
+    if (exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+    exec = nullptr;
+  }
+};
+
 struct Graph {
   PhaseProf prof;
   std::vector<janus_op> ops;
@@ -149,6 +176,7 @@ struct Graph {
   // imperative executor writes anywhere in it, so running it on the same buffer clears this)
   const void *ws_ready = nullptr;
   unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*16*T u64)
+  StepGraph cg;                         // the LM step captured as one CUDA graph (host_lm.cpp)
 };
 
 // host_graph.cpp

@@ -455,6 +455,7 @@ int32_t janus_dev_phase_report(const janus_graph *g, char *buf, size_t len) {
 
 void janus_graph_destroy(janus_graph *g) {
   if (!g) return;
+  g->cg.reset();
   dp_destroy(*g);
   if (g->h_status) cudaFreeHost(g->h_status);
   delete g;
