@@ -669,7 +669,7 @@ def main():
                      "mean_width": T, "padded_fraction": 1.0 - vtok / (B * T),
                      "host_syncs_per_step": syncs}
     out["clocks"] = clk.summary()
-    if not args.no_extras and args.workload == "c2":
+    if not args.no_extras and args.workload == "c2" and world == 1:  # the scaling runs time the headline only
         out.update(extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank, ms_step))
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()
