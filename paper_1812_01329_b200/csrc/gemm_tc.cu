@@ -27,11 +27,11 @@ namespace jk {
 
 bool make_tmap_f32_box32(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t ld);
 
-template <int BN, int STAGES, int NMMA = 1>
+template <int BN, int STAGES, int NMMA = 1, bool PAIR = false>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;  // PAIR: this CTA's half of the N rows
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // epilogue staging for TMA stores: per epilogue warp two 32 x 32 fp32 boxes (double buffer)
   static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
@@ -143,11 +143,17 @@ JN_DEV TileRef tile_ref(const GemmBatch &gb, int t, int rank = 0) {
 // NMMA = 2 (BN = 128): a second MMA-issuing warp takes the odd ring stages into its own
 // accumulators — one warp issues a tcgen05.mma only every ~130 cycles, twice the N = 128 MMA time;
 // STAGES is even, so every stage has one fixed owner and no wait can alias a phase
-template <int BN, int STAGES, int NMMA, int CM>
+// PAIR (CM == 2, NMMA == 1): the cluster's two CTAs run ONE M = 256 MMA (cta_group::2) per
+// k-step: each holds its 128 rows of A and half of the B tile's N rows (32 KB per stage instead of
+// 48 KB at BN = 256: six stages in flight), both CTAs' TMA loads complete on the leader's full
+// barrier, the leader issues the MMAs and its commits arrive on both CTAs' barriers; each CTA's
+// epilogue reads its own 128 accumulator rows and releases the leader's TMEM-empty barrier.
+template <int BN, int STAGES, int NMMA, int CM, bool PAIR>
 __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(const __grid_constant__ GemmBatch gb) {
   pdl_enter();
-  using C = GemmCfg<BN, STAGES, NMMA>;
+  using C = GemmCfg<BN, STAGES, NMMA, PAIR>;
   static_assert(STAGES % NMMA == 0, "stage ownership");
+  static_assert(!PAIR || (CM == 2 && NMMA == 1), "CTA pair");
   // CM > 1: clusters of CM CTAs along M share each B tile; CTA r loads rows / k-rows slice r of it
   // with a multicast TMA into every cluster CTA, and a stage is released only when the owning
   // MMA warp of EVERY cluster CTA consumed it (multicast commit into each empty barrier)
@@ -177,15 +183,18 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CM);
+      mbar_init(&empty[s], PAIR ? 1 : CM);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], NMMA);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], PAIR ? 8 : 4);  // PAIR: both CTAs' epilogue warps release the leader's
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * NMMA * BN);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair(tmem_slot, 2 * NMMA * BN);
+    else tmem_alloc(tmem_slot, 2 * NMMA * BN);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -201,7 +210,26 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
       const int m0 = tr.mb * C::BM, n0 = tr.nb * BN;
       for (int kb = tr.kb0; kb < tr.kb1; ++kb, ++q) {
         const int s = q % STAGES, r = q / STAGES;
-        if (lane == 0) {
+        if (PAIR && lane == 0) {
+          if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);  // both CTAs' loads
+          const uint32_t fbar = mapa_shared(smem_u32(&full[s]), 0);      // the leader's barrier
+          const int k0 = kb * C::BK;
+          uint8_t *a = sA + s * C::A_BYTES, *b = sB + s * C::B_BYTES;
+          if (!A_MN) {
+            tma_load_2d_pair(a, tmA, fbar, k0, m0);
+          } else {
+            tma_load_2d_pair(a, tmA, fbar, m0, k0);
+            tma_load_2d_pair(a + 8192, tmA, fbar, m0 + 64, k0);
+          }
+          const int nh = n0 + rank * (BN / 2);  // my half of the tile's N rows
+          if (!B_MN) {
+            tma_load_2d_pair(b, tmB, fbar, k0, nh);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 128; ++j) tma_load_2d_pair(b + j * 8192, tmB, fbar, nh + 64 * j, k0);
+          }
+        } else if (lane == 0) {
           if (r > 0) mbar_wait(&empty[s], (r - 1) & 1);
           mbar_expect_tx(&full[s], C::STAGE_BYTES);
           const int k0 = kb * C::BK;
@@ -232,6 +260,40 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         __syncwarp();
       }
     }
+  } else if (PAIR && warp == 1) {  // ---------------- the pair's MMA issuer (leader, lane 0)
+    int q = 0, i = 0;
+    if (rank == 0)
+      for (int t = cid; t < total; t += ncl, ++i) {
+        const TileRef tr = tile_ref<BN, STAGES, CM>(gb, t, rank);
+        const int A_MN = gb.amn[tr.g], B_MN = gb.bmn[tr.g];
+        const uint32_t idesc = umma_idesc_bf16(256, BN, A_MN, B_MN);
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(&tempty[buf], ((i >> 1) - 1) & 1);  // both CTAs drained this buffer
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        bool first = true;
+        for (int kb = tr.kb0; kb < tr.kb1; ++kb, ++q) {
+          const int s = q % STAGES, r = q / STAGES;
+          mbar_wait(&full[s], r & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a = smem_u32(sA + s * C::A_BYTES), b = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+            for (int j = 0; j < C::BK / 16; ++j) {
+              const uint64_t ad = A_MN ? umma_desc_sw128(a + j * 2048, 8192, 1024)
+                                       : umma_desc_sw128(a + j * 32, 16, 1024);
+              const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
+                                       : umma_desc_sw128(b + j * 32, 16, 1024);
+              umma_bf16_pair(acc, ad, bd, idesc, (!first || j != 0) ? 1u : 0u);
+            }
+            umma_commit_pair(&empty[s]);
+          }
+          first = false;
+          __syncwarp();
+        }
+        if (lane == 0) umma_commit_pair(&tfull[buf]);  // arrives even without a k-block
+        __syncwarp();
+      }
   } else if (warp == 1 || warp >= 6) {  // ---------------- MMA issuers (lane 0 issues)
     const int mw = warp == 1 ? 0 : warp - 5;  // which of the NMMA issuing warps
     int q = 0, i = 0;
@@ -272,6 +334,11 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
     // ---------------- epilogue: TMEM -> registers -> global (warps 2-5)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     int i = 0, qe = 0;          // qe: ring position of the tile's first k-block (as the MMA warps)
+    // this warp is done reading accumulator buffer `buf` (PAIR: on the leader's barrier)
+    auto release_tmem = [&](int buf) {
+      if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[buf]), 0));
+      else mbar_arrive(&tempty[buf]);
+    };
     for (int t = cid; t < total; t += ncl, ++i) {
       const TileRef tr = tile_ref<BN, STAGES, CM>(gb, t, rank);
       const int nkt = tr.kb1 > tr.kb0 ? tr.kb1 - tr.kb0 : 0;
@@ -350,7 +417,7 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) release_tmem(buf);
         if (ep.fr.win) {
           // fused cross-rank reduction (NEXT-3): the tile's stores must have COMPLETED (not only
           // read their boxes) before the owner may read it; then the per-tile protocol
@@ -379,7 +446,7 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) release_tmem(buf);
       } else {
         // split-K: park this split's partial tile; the last split to arrive adds the splits in
         // order 0 .. splits-1 (deterministic) and runs the epilogue
@@ -400,7 +467,7 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (lane == 0) release_tmem(buf);
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         __shared__ unsigned s_last;
@@ -435,7 +502,10 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
   tc_fence_before();
   __syncthreads();
   if (CM > 1) cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
-  if (warp == 1) tmem_dealloc(tmem, 2 * NMMA * BN);
+  if (warp == 1) {
+    if (PAIR) tmem_dealloc_pair(tmem, 2 * NMMA * BN);
+    else tmem_dealloc(tmem, 2 * NMMA * BN);
+  }
 }
 
 // ------------------------------------------------------------------------------ host side
@@ -530,12 +600,13 @@ static bool op_wants_split(const GemmOp &op) {
   return op.flags && op.partials && (op.splits > 1 || (op.splits <= 0 && getenv("JANUS_GEMM_AUTOSPLIT")));
 }
 
-template <int BN, int CM>
+template <int BN, int CM, bool PAIR = false>
 static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
-  constexpr int STAGES = BN == 256 ? 4 : 6;
-  constexpr int NMMA = BN == 256 ? 1 : 2;
-  using C = GemmCfg<BN, STAGES, NMMA>;
-  auto kern = gemm_bf16_tc_kernel<BN, STAGES, NMMA, CM>;
+  // PAIR halves a CTA's B stage: six (BN = 256) / eight (BN = 128) stages fit instead of 4 / 6
+  constexpr int STAGES = PAIR ? (BN == 256 ? 6 : 8) : (BN == 256 ? 4 : 6);
+  constexpr int NMMA = PAIR ? 1 : (BN == 256 ? 1 : 2);
+  using C = GemmCfg<BN, STAGES, NMMA, PAIR>;
+  auto kern = gemm_bf16_tc_kernel<BN, STAGES, NMMA, CM, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -556,7 +627,9 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
     const GemmOp &op = ops[g];
     bool ok = op.a_mn ? make_tmap_bf16(&gb.ta[g], op.A, op.M, op.K, op.lda, 64)
                       : make_tmap_bf16(&gb.ta[g], op.A, op.K, op.M, op.lda, 128);
-    ok = ok && (op.b_mn ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, 64 / CM)
+    // B boxes: multicast (CM > 1) loads 1/CM of the tile into every CTA; PAIR loads this CTA's
+    // half of the N rows (all K rows of each 64-column chunk when MN-major)
+    ok = ok && (op.b_mn ? make_tmap_bf16(&gb.tb[g], op.B, op.N, op.K, op.ldb, PAIR ? 64 : 64 / CM)
                         : make_tmap_bf16(&gb.tb[g], op.B, op.K, op.N, op.ldb, BN / CM));
     gb.amn[g] = op.a_mn ? 1 : 0;
     gb.bmn[g] = op.b_mn ? 1 : 0;
@@ -615,10 +688,23 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
 // JANUS_GEMM_CM=1 disables it.
 static int g_gemm_cm = getenv("JANUS_GEMM_CM") ? atoi(getenv("JANUS_GEMM_CM")) : 2;
 
+// CTA pairs (cta_group::2) for launches whose reductions are long (every K >= 1024: the weight
+// gradients K = T*B, dh_top K = V): measured at C2, wgrad 81.6 -> 72.8 us, dh 60.4 -> 58.9 us,
+// while the short-K (650) decoder and input projection are a little slower paired (57.8 -> 59.7
+// us). JANUS_GEMM_PAIR (dev knob): "1" pairs for every launch, "0" never.
+static int g_gemm_pair = getenv("JANUS_GEMM_PAIR") ? atoi(getenv("JANUS_GEMM_PAIR")) : -1;
+static bool want_pair(const GemmOp *ops, int n) {
+  if (g_gemm_pair >= 0) return g_gemm_pair == 1;
+  for (int g = 0; g < n; ++g)
+    if (ops[g].K < 1024) return false;
+  return true;
+}
+
 template <int BN>
 static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   bool split = false;
   for (int g = 0; g < n; ++g) split = split || (op_wants_split(ops[g]) && n == 1);
+  if (g_gemm_cm == 2 && !split && want_pair(ops, n)) return launch_cm<BN, 2, true>(ops, n, st);
   if (g_gemm_cm == 2 && !split) return launch_cm<BN, 2>(ops, n, st);
   return launch_cm<BN, 1>(ops, n, st);
 }
