@@ -265,6 +265,14 @@ janus_status janus_run_imperative(janus_graph *g, const janus_tensor *args, int3
                                   const janus_tensor *outs, int32_t n_outs,
                                   janus_tensor workspace, void *cuda_stream);
 
+/* The caller wrote a state tensor outside the library (an optimizer, a checkpoint load, an
+ * in-place update). The LM step keeps bf16 working copies of its weight matrices (R1)
+ * that its own commit refreshes (P:164 commit, P:282 deferred update), so a step skips the re-cast
+ * while the masters were written only by the library since its last run; this call makes the
+ * next step of every graph re-cast. Required after any such write; never fails. (The Python
+ * binding calls it itself when a state tensor's version counter moved.) */
+janus_status janus_state_changed(void);
+
 /* Cumulative counters of this graph: kernel launches issued by the library, host
  * synchronisations, and aborts (ASSUMPTION_FAILED returns). */
 janus_status janus_counters(const janus_graph *g, uint64_t *launches, uint64_t *host_syncs,

@@ -1,5 +1,6 @@
 // host.h — host runtime of libjanus: the graph object, speculative lowering plans, dispatch.
 #pragma once
+#include <atomic>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -124,8 +125,9 @@ struct GraphKey {
   const void *state[64] = {};
   int width = 0;
   const void *stream = nullptr;
+  bool cast = true;  // the step re-casts the bf16 operand copies (false: the last commit refreshed them)
   bool operator==(const GraphKey &o) const {
-    if (W != o.W || width != o.width || stream != o.stream) return false;
+    if (W != o.W || width != o.width || stream != o.stream || cast != o.cast) return false;
     for (int k = 0; k < 64; ++k)
       if (state[k] != o.state[k]) return false;
     return true;
@@ -177,7 +179,18 @@ struct Graph {
   const void *ws_ready = nullptr;
   unsigned long long *probe = nullptr;  // dev hook: recurrent-kernel timeline buffer (2*128*16*T u64)
   StepGraph cg;                         // the LM step captured as one CUDA graph (host_lm.cpp)
+  // bf16 operand copies (R1) kept current by the commit: valid for the next run when no library
+  // call that may write state (any graph, the imperative executor) and no janus_state_changed
+  // happened since this graph's last run, on the same workspace and the same master pointers
+  unsigned long long copies_epoch = ~0ull;  // state_epoch value after the run that left them valid
+  bool copies_in = false;                   // set by janus_run for run_lm: the copies match the masters
+  bool copies_out = false;                  // set by run_lm: the enqueued step leaves them matching
+  const void *copies_W = nullptr;
+  const void *copies_src[9] = {};
 };
+
+// bumped by every library call that may write a state tensor, and by janus_state_changed
+extern std::atomic<unsigned long long> state_epoch;
 
 // host_graph.cpp
 janus_status validate_graph(Graph &g, std::string &err);

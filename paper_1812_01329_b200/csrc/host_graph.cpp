@@ -18,6 +18,8 @@
 
 namespace jk {
 
+std::atomic<unsigned long long> state_epoch{0};
+
 static int arity(int k) {
   switch (k) {
     case JOP_ARG: case JOP_CONST: case JOP_STATE_READ: case JOP_TA_NEW: return 0;
@@ -310,6 +312,12 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
   if (n_args < g->n_args || n_state < g->n_state) return JANUS_ERR_INVALID;
   janus_failure f{};
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  // the bf16 operand copies the last commit refreshed are current iff no state-writing call
+  // (this one excepted) happened since (host.h copies_epoch)
+  const unsigned long long e0 = state_epoch.fetch_add(1);
+  g->copies_in = e0 == g->copies_epoch;
+  g->copies_out = false;
+  g->copies_epoch = ~0ull;
   // a workspace this graph has not initialised (new, or written by the imperative executor or
   // another graph since) is zero-filled first: the device program relies on zero pads
   auto ready = [&]() -> janus_status {
@@ -318,6 +326,7 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
     if (!workspace.data || have < g->ws_bytes) return JANUS_ERR_INVALID;
     if (cudaMemsetAsync(workspace.data, 0, g->ws_bytes, st) != cudaSuccess) return JANUS_ERR_CUDA;
     g->gflags_ws = nullptr;
+    g->copies_in = false;
     g->ws_ready = workspace.data;
     return JANUS_OK;
   };
@@ -338,6 +347,7 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
       return r == JANUS_OK ? JANUS_ASSUMPTION_FAILED : r;
     }
     // cache miss: nothing is launched, nothing mutated
+    if (g->copies_in) g->copies_epoch = e0 + 1;
     if (fail) *fail = f;
     return JANUS_ASSUMPTION_FAILED;
   }
@@ -352,7 +362,15 @@ janus_status janus_run(janus_graph *g, const janus_tensor *args, int32_t n_args,
     return rn == JANUS_OK || rn == JANUS_ERR_RUNTIME ? JANUS_ERR_INVALID : rn;
   }
   if (r == JANUS_ASSUMPTION_FAILED) g->aborts++;
+  // the commit kept the copies current, or nothing committed (all-or-nothing)
+  if (g->copies_out && (r == JANUS_OK || r == JANUS_ASSUMPTION_FAILED || r == JANUS_ERR_RUNTIME))
+    g->copies_epoch = e0 + 1;
   return r;
+}
+
+janus_status janus_state_changed(void) {
+  state_epoch.fetch_add(1);
+  return JANUS_OK;
 }
 
 janus_status janus_run_imperative(janus_graph *g, const janus_tensor *args, int32_t n_args,
@@ -361,6 +379,7 @@ janus_status janus_run_imperative(janus_graph *g, const janus_tensor *args, int3
                                   janus_tensor workspace, void *cuda_stream) {
   if (!g || (!args && n_args) || (!state && n_state)) return JANUS_ERR_INVALID;
   if (g->ws_ready == workspace.data) g->ws_ready = nullptr;
+  state_epoch.fetch_add(1);
   return run_imperative(*g, args, n_args, state, n_state, outs, n_outs, workspace,
                         static_cast<cudaStream_t>(cuda_stream));
 }

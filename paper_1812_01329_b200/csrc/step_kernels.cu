@@ -226,12 +226,21 @@ cudaError_t launch_fill_col(__nv_bfloat16 *X, int rows, int ld, int col, float v
 }
 
 // ------------------------------------------------------------------------------ fused prep
-// Every per-step operand copy of the LM step in ONE launch (blockIdx.y = segment): row casts
-// (optionally gate-interleaving), the interleaved transpose of W_hh, bias interleave, ones-column
-// fill. Each segment strides its own work units over blockIdx.x.
-__global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
+// Every per-step operand copy of the LM step in ONE launch: row casts (optionally
+// gate-interleaving), the interleaved transpose of W_hh, bias interleave, ones-column fill. Each
+// segment owns a block range of the 1-D grid sized to its work (launch_prep) and strides its work
+// units over that range (bx of gx blocks).
+JN_DEV int seg_of_block(const int *blk, int n, int *bx, int *gx) {
+  int k = 0;
+  while (k + 1 < n && (int)blockIdx.x >= blk[k + 1]) ++k;
+  *bx = (int)blockIdx.x - blk[k];
+  *gx = blk[k + 1] - blk[k];
+  return k;
+}
+__global__ void __launch_bounds__(256, 5) prep_kernel(PrepList pl) {
   pdl_enter();
-  const PrepSeg sg = pl.s[blockIdx.y];
+  int bx, gx;
+  const PrepSeg sg = pl.s[seg_of_block(pl.blk, pl.n, &bx, &gx)];
   switch (sg.kind) {
     case P_CAST_ROWS: {
       // HBM-bound copy: every load of PR rows x (<= 2) 512-column chunks is issued before any
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
       constexpr int PR = 8;
       const bool pairs = ((sg.ld_src | sg.cols) & 1) == 0 && (reinterpret_cast<uintptr_t>(sg.src) & 7) == 0;
       const int nkc = (sg.ld_dst + 511) / 512;
-      for (int r0 = blockIdx.x * PR; r0 < sg.rows; r0 += gridDim.x * PR) {
+      for (int r0 = bx * PR; r0 < sg.rows; r0 += gx * PR) {
         for (int kc0 = 0; kc0 < nkc; kc0 += 2) {
           float2 v[PR][2];
 #pragma unroll
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
       __shared__ float tile[32][129];
       const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
       const int H = sg.H, nti = (4 * H + 31) / 32, ntp = (H + 127) / 128;
-      for (int tb = blockIdx.x; tb < nti * ntp; tb += gridDim.x) {
+      for (int tb = bx; tb < nti * ntp; tb += gx) {
         const int ri0 = (tb % nti) * 32, u0 = (tb / nti) * 128;
         float v[4][4];  // all 16 loads of the panel in flight before the shared-memory stores
 #pragma unroll
@@ -295,13 +304,13 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
       }
     } break;
     case P_BIAS_IL:
-      for (int ri = blockIdx.x * blockDim.x + threadIdx.x; ri < 4 * sg.H; ri += gridDim.x * blockDim.x)
+      for (int ri = bx * blockDim.x + threadIdx.x; ri < 4 * sg.H; ri += gx * blockDim.x)
         sg.fdst[ri] = sg.src[(ri & 3) * sg.H + (ri >> 2)];
       break;
     case P_FILL_COL: {  // dst[r][col] = 1, dst[r][col+1 .. ld_dst) = 0
       const int w = max(1, sg.ld_dst - sg.cols);
       const long long n = (long long)sg.rows * w;
-      for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+      for (long long e = bx * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gx * blockDim.x) {
         const int r = (int)(e / w), k = (int)(e - (long long)r * w);
         sg.dst[(size_t)r * sg.ld_dst + sg.cols + k] = __float2bfloat16_rn(k == 0 ? 1.f : 0.f);
       }
@@ -309,10 +318,26 @@ __global__ void __launch_bounds__(256) prep_kernel(PrepList pl) {
   }
 }
 
-cudaError_t launch_prep(const PrepList &pl, cudaStream_t s) {
-  if (pl.n <= 0) return cudaSuccess;
+// blocks of a segment: half its grid-stride work units (two per block), at least 1, at most 4 / SM
+// blocks of a segment: one per two of its grid-stride work units, at least 1, at most 4 per SM
+// (measured at C2 against one unit per block and against 4 / SM for every segment: the prep
+// and commit phases 25.9 / 38.7 us vs 27.9 / 40.6 and 30.1 / 44.1 us)
+static int seg_blocks(long long units) { return (int)std::max(1LL, std::min<long long>(4 * NSM, (units + 1) / 2)); }
+cudaError_t launch_prep(const PrepList &pl0, cudaStream_t s) {
+  if (pl0.n <= 0) return cudaSuccess;
+  PrepList pl = pl0;
+  pl.blk[0] = 0;
+  for (int k = 0; k < pl.n; ++k) {
+    const PrepSeg &g = pl.s[k];
+    long long u = 1;
+    if (g.kind == P_CAST_ROWS) u = (g.rows + 7) / 8;
+    else if (g.kind == P_CAST_T_IL) u = (long long)((4 * g.H + 31) / 32) * ((g.H + 127) / 128);
+    else if (g.kind == P_BIAS_IL) u = (4LL * g.H + 255) / 256;
+    else if (g.kind == P_FILL_COL) u = ((long long)g.rows * std::max(1, g.ld_dst - g.cols) + 255) / 256;
+    pl.blk[k + 1] = pl.blk[k] + seg_blocks(u);
+  }
   {
-    const cudaError_t pe_ = launch_pdl(prep_kernel, dim3(dim3(2 * NSM, pl.n)), dim3(256), 0, s, pl);
+    const cudaError_t pe_ = launch_pdl(prep_kernel, dim3(pl.blk[pl.n]), dim3(256), 0, s, pl);
     if (pe_ != cudaSuccess) return pe_;
   }
   return cudaGetLastError();
@@ -973,20 +998,21 @@ cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_w
 
 // ------------------------------------------------------------------------------ commit
 // Predicated on the device status: with any failure nothing is written (all-or-nothing).
-__global__ void commit_kernel(CommitList cl, const DevStatus *st) {
+__global__ void __launch_bounds__(256, 6) commit_kernel(CommitList cl, const DevStatus *st) {
   pdl_enter();
   if (st->status != 0) return;
-  const CommitSeg sg = cl.s[blockIdx.y];
+  int bx, gx;
+  const CommitSeg sg = cl.s[seg_of_block(cl.blk, cl.n, &bx, &gx)];
   if (sg.pred && *sg.pred == 0) return;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gx * blockDim.x;
+  const long long tid = bx * (long long)blockDim.x + threadIdx.x;
   switch (sg.kind) {
     case C_DENSE:  // 4 rows per block iteration, 2 columns per thread, loads before stores
     case C_DENSE_IL: {
       const int ng = sg.ng ? sg.ng : 4;
       const bool pairs = ((sg.cols | sg.ldg) & 1) == 0 &&
                          ((reinterpret_cast<uintptr_t>(sg.dst) | reinterpret_cast<uintptr_t>(sg.grad)) & 7) == 0;
-      for (int r0 = blockIdx.x * CR_ROWS; r0 < sg.rows; r0 += gridDim.x * CR_ROWS) {
+      for (int r0 = bx * CR_ROWS; r0 < sg.rows; r0 += gx * CR_ROWS) {
         for (int k0 = 0; k0 < sg.cols; k0 += 512) {
           const int k = k0 + 2 * threadIdx.x;
           float2 dv[CR_ROWS], gv[CR_ROWS];
@@ -1010,9 +1036,64 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
               const float2 o = make_float2(dv[q].x - sg.lr * gv[q].x, dv[q].y - sg.lr * gv[q].y);
               if (pairs) *reinterpret_cast<float2 *>(d) = o;
               else { d[0] = o.x; if (k + 1 < sg.cols) d[1] = o.y; }
+              if (sg.bcopy) {  // the next step's bf16 working copy of this master (R1)
+                const int rb = sg.kind == C_DENSE ? rc : ng * (rc % sg.H) + rc / sg.H;
+                __nv_bfloat16 *bc = sg.bcopy + (size_t)rb * sg.ldb + k;
+                if (pairs) *reinterpret_cast<__nv_bfloat162 *>(bc) = __floats2bfloat162_rn(o.x, o.y);
+                else { bc[0] = __float2bfloat16_rn(o.x); if (k + 1 < sg.cols) bc[1] = __float2bfloat16_rn(o.y); }
+              }
             }
           }
         }
+      }
+    } break;
+    case C_DENSE_IL_T: {
+      // 32 interleaved rows x 64 columns per tile: update the master rows, write the row copy,
+      // and through shared memory the transposed copy tcopy[k][ri] (coalesced along ri)
+      __shared__ __nv_bfloat16 tt[32][72];
+      const int R = 4 * sg.H, nti = (R + 31) / 32, ntk = (sg.cols + 63) / 64;
+      const int tr = threadIdx.x >> 3, tc = (threadIdx.x & 7) * 8;  // this thread: row tr, 8 columns
+      for (int tb = bx; tb < nti * ntk; tb += gx) {
+        const int ri0 = (tb % nti) * 32, k0 = (tb / nti) * 64;
+        const int ri = ri0 + tr, rc = (ri & 3) * sg.H + (ri >> 2);
+        float2 dv[4], gv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + tc + 2 * j;
+          dv[j] = gv[j] = make_float2(0.f, 0.f);
+          if (ri < R && k < sg.cols) {  // cols and pitches even: pairs stay inside a row
+            dv[j] = *reinterpret_cast<const float2 *>(sg.dst + (size_t)rc * sg.cols + k);
+            gv[j] = __ldcs(reinterpret_cast<const float2 *>(sg.grad + (size_t)ri * sg.ldg + k));
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + tc + 2 * j;
+          const float2 o = make_float2(dv[j].x - sg.lr * gv[j].x, dv[j].y - sg.lr * gv[j].y);
+          const __nv_bfloat162 ob = __floats2bfloat162_rn(o.x, o.y);
+          if (ri < R && k < sg.cols) {
+            *reinterpret_cast<float2 *>(sg.dst + (size_t)rc * sg.cols + k) = o;
+            *reinterpret_cast<__nv_bfloat162 *>(sg.bcopy + (size_t)ri * sg.ldb + k) = ob;
+          }
+          *reinterpret_cast<__nv_bfloat162 *>(&tt[tr][tc + 2 * j]) = ob;
+        }
+        __syncthreads();
+        {  // 64 k rows x 32 ri: thread -> k = k0 + t / 4, 8 consecutive ri
+          const int kk = threadIdx.x >> 2, r8 = (threadIdx.x & 3) * 8;
+          const int k = k0 + kk;
+          if (k < sg.cols) {
+            __nv_bfloat16 *td = sg.tcopy + (size_t)k * sg.ldt + ri0 + r8;
+            if (ri0 + r8 + 8 <= R && ((reinterpret_cast<uintptr_t>(td) & 15) == 0)) {
+              __align__(16) __nv_bfloat16 v8[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v8[i] = tt[r8 + i][kk];
+              *reinterpret_cast<uint4 *>(td) = *reinterpret_cast<const uint4 *>(v8);
+            } else {
+              for (int i = 0; i < 8 && ri0 + r8 + i < R; ++i) td[i] = tt[r8 + i][kk];
+            }
+          }
+        }
+        __syncthreads();
       }
     } break;
     case C_TREE_BIAS:  // b blocks (i, f, o, u): internal gates (i, f_l, f_r, o, u), leaf (i, o, u)
@@ -1055,10 +1136,26 @@ __global__ void commit_kernel(CommitList cl, const DevStatus *st) {
   }
 }
 
-cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s) {
-  if (cl.n <= 0) return cudaSuccess;
+cudaError_t launch_commit(const CommitList &cl0, const DevStatus *st, cudaStream_t s) {
+  if (cl0.n <= 0) return cudaSuccess;
+  CommitList cl = cl0;
+  cl.blk[0] = 0;
+  for (int k = 0; k < cl.n; ++k) {
+    const CommitSeg &g = cl.s[k];
+    long long u;
+    switch (g.kind) {
+      case C_DENSE: case C_DENSE_IL: u = (g.rows + CR_ROWS - 1) / CR_ROWS; break;
+      case C_DENSE_IL_T: u = (long long)((4 * g.H + 31) / 32) * ((g.cols + 63) / 64); break;
+      case C_TREE_BIAS: u = (4LL * g.H + 255) / 256; break;
+      case C_BIAS_COL: case C_BIAS_COL_IL: u = (g.rows + 255) / 256; break;
+      case C_COPY: u = ((long long)g.rows * g.cols + 255) / 256; break;
+      case C_TAG: u = 1; break;
+      default: u = 8LL * NSM;  // C_SPARSE_ROWS: the row count is known on the device only
+    }
+    cl.blk[k + 1] = cl.blk[k] + seg_blocks(u);
+  }
   {
-    const cudaError_t pe_ = launch_pdl(commit_kernel, dim3(dim3(4 * NSM, cl.n)), dim3(256), 0, s, cl, st);
+    const cudaError_t pe_ = launch_pdl(commit_kernel, dim3(cl.blk[cl.n]), dim3(256), 0, s, cl, st);
     if (pe_ != cudaSuccess) return pe_;
   }
   return cudaGetLastError();

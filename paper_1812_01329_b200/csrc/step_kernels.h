@@ -69,6 +69,7 @@ constexpr int MAX_PREP = 24;
 struct PrepList {
   int n;
   PrepSeg s[MAX_PREP];
+  int blk[MAX_PREP + 1];  // set by launch_prep: segment k owns blocks [blk[k], blk[k+1]) of the 1-D grid
 };
 cudaError_t launch_prep(const PrepList &pl, cudaStream_t s);
 cudaError_t launch_cast_rows(const float *src, int R, int Cc, int ld_src, __nv_bfloat16 *dst,
@@ -167,7 +168,8 @@ cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_w
 
 // commit segments (P:164 all-or-nothing, P:282 deferred update)
 enum CommitKind { C_DENSE = 0, C_DENSE_IL = 1, C_BIAS_COL = 2, C_BIAS_COL_IL = 3, C_COPY = 4,
-                  C_TAG = 5, C_SPARSE_ROWS = 6, C_TREE_BIAS = 7 };
+                  C_TAG = 5, C_SPARSE_ROWS = 6, C_TREE_BIAS = 7,
+                  C_DENSE_IL_T = 8 /* C_DENSE_IL with a transposed copy: 32 x 64 tiles */ };
 struct CommitSeg {
   int kind;
   float *dst;          // master (fp32) or state destination
@@ -185,11 +187,15 @@ struct CommitSeg {
   const float *grad2;  // C_TREE_BIAS: leaf wgrad (bias column col2, pitch ldg2)
   int ldg2, col2;
   const int *pred;     // device predicate (`if training:` Switch): skip the segment when *pred == 0
+  // bf16 working copies refreshed from the committed masters (R1), so the next step needs no cast:
+  __nv_bfloat16 *bcopy; int ldb;  // row copy: row ri (interleaved, C_DENSE_IL*) or rc (C_DENSE)
+  __nv_bfloat16 *tcopy; int ldt;  // C_DENSE_IL_T: transposed copy, tcopy[k][ri]
 };
 constexpr int MAX_COMMIT = 24;
 struct CommitList {
   int n;
   CommitSeg s[MAX_COMMIT];
+  int blk[MAX_COMMIT + 1];  // set by launch_commit: segment k owns blocks [blk[k], blk[k+1])
 };
 cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s);
 

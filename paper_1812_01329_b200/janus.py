@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -71,7 +72,8 @@ lib = C.CDLL(LIB_PATH)
 EXPORTS = ["janus_graph_build", "janus_workspace_bytes", "janus_run", "janus_run_imperative",
            "janus_counters", "janus_describe", "janus_graph_destroy", "janus_status_str",
            "janus_abi_version", "janus_session_create", "janus_session_workspace_bytes",
-           "janus_session_step", "janus_session_stats", "janus_session_destroy", "janus_relax"]
+           "janus_session_step", "janus_session_stats", "janus_session_destroy", "janus_relax",
+           "janus_state_changed"]
 DEV_EXPORTS = ["janus_dev_gemm_bf16", "janus_dev_gemm_bf16_splitk"]
 
 _P = C.c_void_p
@@ -128,6 +130,7 @@ _sigs = {
     "janus_graph_destroy": (None, [C.c_void_p]),
     "janus_status_str": (C.c_char_p, [C.c_int]),
     "janus_abi_version": (C.c_int32, []),
+    "janus_state_changed": (C.c_int, []),
     "janus_session_create": (C.c_int, [C.POINTER(JanusOp), C.c_int32, C.POINTER(JanusAssumption), C.c_int32,
                                        C.POINTER(JanusBuildOpts), C.POINTER(JanusSessionOpts),
                                        C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
@@ -222,6 +225,30 @@ class JanusError(RuntimeError):
     pass
 
 
+_seen_state = {}   # id(tensor) -> (weakref, _version) at the last library call
+
+
+def _note_state(state):
+    """janus_state_changed when a state tensor was written outside the library since the last
+    call (torch bumps _version on every in-place write; a different tensor object counts too): the
+    LM step then re-casts its bf16 operand copies instead of trusting the ones its commit refreshed."""
+    changed = False
+    for t in state:
+        v = getattr(t, "_version", None)
+        if v is None:
+            changed = True
+            continue
+        e = _seen_state.get(id(t))
+        if e is None or e[0]() is not t or e[1] != v:
+            changed = True
+            _seen_state[id(t)] = (weakref.ref(t), v)
+    if changed:
+        lib.janus_state_changed()
+        if len(_seen_state) > 4096:
+            for k in [k for k, e in _seen_state.items() if e[0]() is None]:
+                del _seen_state[k]
+
+
 class Graph:
     """A speculatively specialised graph (janus_graph_build) for one Program."""
 
@@ -256,6 +283,7 @@ class Graph:
 
     def run(self, args, state, workspace, outs=(), stream=None):
         """janus_run: returns (status, failure dict or None)."""
+        _note_state(state)
         a, s, o = _jt_array(args), _jt_array(state), _jt_array(outs)
         f = JanusFailure()
         r = lib.janus_run(self.h, a, len(args), s, len(state), o, len(outs), to_jt(workspace),
@@ -266,6 +294,7 @@ class Graph:
         return r, fail
 
     def run_imperative(self, args, state, workspace, outs=(), stream=None):
+        _note_state(state)
         a, s, o = _jt_array(args), _jt_array(state), _jt_array(outs)
         return lib.janus_run_imperative(self.h, a, len(args), s, len(state), o, len(outs),
                                         to_jt(workspace), _stream(stream))
@@ -345,6 +374,7 @@ class Session:
     def step(self, args, state, outs=(), stream=None):
         """janus_session_step: returns (status, info dict)."""
         import torch
+        _note_state(state)
         a, s, o = _jt_array(args), _jt_array(state), _jt_array(outs)
         info = JanusStepInfo()
         for _ in range(4):
