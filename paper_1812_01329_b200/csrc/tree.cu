@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
     if (live) {
       const int pos = s.lvl_off[h] + hist[h] + wcnt[warp][h] + rank_w;
       s.order[pos] = n;
-      s.irank[n] = h > 0 ? pos - s.lvl_off[1] : -1;
+      s.irank[n] = h > 0 ? pos - s.lvl_off[1] : -1 - pos;  // leaves: -1 - (level-0 position)
     }
     __syncthreads();
   }
@@ -422,7 +422,7 @@ struct Ring {
 // tmA32 (optional): the A map with a 32-row box, used for tiles with <= 32 valid rows (the
 // upper levels of a forest): the MMA still reads 128 smem rows, but rows past the box only feed
 // accumulator rows the epilogue discards, and the level's A traffic drops 4x.
-template <int NT, bool STAGED = false, int NS = T_STAGES, typename Pre, typename Epi>
+template <int NT, int STAGED = 0, int NS = T_STAGES, typename Pre, typename Epi>
 JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, int row0, int M,
                       int NTOT, int K, Pre pre, Epi epi, int nmw, unsigned long long *pr = nullptr,
                       const CUtensorMap *tmA32 = nullptr) {
@@ -512,7 +512,12 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (threadIdx.x == 0) pr[2] = gtimer();
       }
-      if constexpr (STAGED) {
+      if constexpr (STAGED == 2) {  // staged for every warp of the CTA (below)
+        float *zr = rg.zst + threadIdx.x * (NT + 1);
+#pragma unroll
+        for (int i = 0; i < NT; ++i) zr[i] = z[i];
+        (void)ctx;
+      } else if constexpr (STAGED) {
         float *zr = rg.zst + threadIdx.x * (NT + 1);
 #pragma unroll
         for (int i = 0; i < NT; ++i) zr[i] = z[i];
@@ -528,11 +533,16 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
         if (threadIdx.x == 0) pr[3] = pr[1];
       }
     }
+    if constexpr (STAGED == 2) {  // the producer and MMA warps are idle now: all warps share the epilogue
+      __syncthreads();
+      epi(m * 128, min(128, M - m * 128), nn * NT);
+    }
     rg.q += nk;
     rg.tiles += 1;
     tc_fence_before();
     __syncthreads();  // TMEM accumulator free for the next tile
     tc_fence_after();
+    if (STAGED == 2 && pr && threadIdx.x == 0) { pr[1] = gtimer(); pr[3] = pr[1]; }
   }
 }
 
@@ -853,6 +863,157 @@ cudaError_t launch_tree_fwd(const TreeBufs &t, const TreeDims &d, const TreeSche
   return coop(fn, grid, smem, args, str);
 }
 
+// =============================================================================== cell backward
+// The cell backward of one (node, unit) once its dh is final (a node's h feeds only its parent,
+// or the classifier for a root) and its dc too (written by the parent's cell backward; 0 for a
+// root): rb(dz) into the node's DZ row and dc into both children. rk = irank[n] (>= 0: internal,
+// row rk of the internal-node arrays; < 0: leaf at level-0 position -1 - rk); kl / kr = the
+// node's children (internal nodes only). TreeRNN: dz = dh (1 - h^2), leaves are frozen.
+struct CellIn { float g[5], c, cl, cr, dc; };
+// loads only (read-only data through the non-coherent path; dc is written by this kernel's
+// earlier levels, so it goes through L2), so a batch of items can have all its loads in flight
+template <bool RNN>
+JN_DEV void cell_load(const TreeBufs &t, const TreeDims &d, int n, int rk, int u, CellIn &x) {
+  const int H = d.H;
+  if (rk >= 0) {
+    x.c = __ldg(t.c_int + (size_t)rk * H + u);
+    if constexpr (!RNN) {
+      const float *g = t.gates_int + (size_t)rk * 5 * H + 5 * u;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) x.g[q] = __ldg(g + q);
+      x.cl = __ldg(t.stage_c + (size_t)rk * 2 * H + u);
+      x.cr = __ldg(t.stage_c + (size_t)rk * 2 * H + H + u);
+      x.dc = __ldcg(t.dc_node + (size_t)n * H + u);
+    }
+  } else if constexpr (!RNN) {
+    const int pos = -1 - rk;
+    const float *g = t.gates_leaf + (size_t)pos * 3 * H + 3 * u;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) x.g[q] = __ldg(g + q);
+    x.c = __ldg(t.c_leaf + (size_t)pos * H + u);
+    x.dc = __ldcg(t.dc_node + (size_t)n * H + u);
+  }
+}
+template <bool RNN>
+JN_DEV void cell_apply(const TreeBufs &t, const TreeDims &d, int rk, int kl, int kr, int u, float dh,
+                       const CellIn &x) {
+  const int H = d.H;
+  if (rk >= 0) {
+    if constexpr (RNN) {
+      t.DZ_int[(size_t)rk * d.P5 + u] = __float2bfloat16_rn(dh * (1.f - x.c * x.c));
+    } else {
+      const float ig = x.g[0], fl = x.g[1], fr = x.g[2], og = x.g[3], ug = x.g[4];
+      const float tc = tanh_t(x.c);
+      const float dout = dh * tc;
+      const float dc = x.dc + dh * og * (1.f - tc * tc);
+      __nv_bfloat16 *dz = t.DZ_int + (size_t)rk * d.P5 + 5 * u;
+      dz[0] = __float2bfloat16_rn(dc * ug * ig * (1.f - ig));
+      dz[1] = __float2bfloat16_rn(dc * x.cl * fl * (1.f - fl));
+      dz[2] = __float2bfloat16_rn(dc * x.cr * fr * (1.f - fr));
+      dz[3] = __float2bfloat16_rn(dout * og * (1.f - og));
+      dz[4] = __float2bfloat16_rn(dc * ig * (1.f - ug * ug));
+      t.dc_node[(size_t)kl * H + u] = dc * fl;
+      t.dc_node[(size_t)kr * H + u] = dc * fr;
+    }
+  } else if constexpr (!RNN) {
+    const int pos = -1 - rk;
+    const float ig = x.g[0], og = x.g[1], ug = x.g[2];
+    const float tc = tanh_t(x.c);
+    const float dc = x.dc + dh * og * (1.f - tc * tc);
+    __nv_bfloat16 *dz = t.DZ_leaf + (size_t)pos * d.P3 + 3 * u;
+    dz[0] = __float2bfloat16_rn(dc * ug * ig * (1.f - ig));
+    dz[1] = __float2bfloat16_rn(dh * tc * og * (1.f - og));
+    dz[2] = __float2bfloat16_rn(dc * ig * (1.f - ug * ug));
+  }
+}
+// Four consecutive units u0 .. u0+3 (u0 % 4 == 0, H % 4 == 0: every row and unit group 16-B
+// aligned): 16-B loads, 8-/16-B stores.
+struct CellIn4 { float4 g[5], c, cl, cr, dc; };
+template <bool RNN>
+JN_DEV void cell4_load(const TreeBufs &t, const TreeDims &d, int n, int rk, int u0, CellIn4 &x) {
+  const int H = d.H;
+  if (rk >= 0) {
+    x.c = __ldg(reinterpret_cast<const float4 *>(t.c_int + rk * H + u0));
+    if constexpr (!RNN) {
+      const float4 *g = reinterpret_cast<const float4 *>(t.gates_int + rk * 5 * H + 5 * u0);
+#pragma unroll
+      for (int q = 0; q < 5; ++q) x.g[q] = __ldg(g + q);
+      x.cl = __ldg(reinterpret_cast<const float4 *>(t.stage_c + rk * 2 * H + u0));
+      x.cr = __ldg(reinterpret_cast<const float4 *>(t.stage_c + rk * 2 * H + H + u0));
+      x.dc = __ldcg(reinterpret_cast<const float4 *>(t.dc_node + n * H + u0));
+    }
+  } else if constexpr (!RNN) {
+    const int pos = -1 - rk;
+    const float4 *g = reinterpret_cast<const float4 *>(t.gates_leaf + pos * 3 * H + 3 * u0);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) x.g[q] = __ldg(g + q);
+    x.c = __ldg(reinterpret_cast<const float4 *>(t.c_leaf + pos * H + u0));
+    x.dc = __ldcg(reinterpret_cast<const float4 *>(t.dc_node + n * H + u0));
+  }
+}
+JN_DEV float f4(const float4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+JN_DEV uint32_t pack_bf2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t *>(&h);
+}
+template <bool RNN>
+JN_DEV void cell4_apply(const TreeBufs &t, const TreeDims &d, int rk, int kl, int kr, int u0, const float *dh,
+                        const CellIn4 &x) {
+  const int H = d.H;
+  if (rk >= 0) {
+    if constexpr (RNN) {
+      float v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { const float h = f4(x.c, i); v[i] = dh[i] * (1.f - h * h); }
+      *reinterpret_cast<uint2 *>(t.DZ_int + (size_t)rk * d.P5 + u0) = make_uint2(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]));
+    } else {
+      const float *gf = reinterpret_cast<const float *>(x.g);  // 20 gates, 5 per unit
+      float dz[20], dcl[4], dcr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float ig = gf[5 * i], fl = gf[5 * i + 1], fr = gf[5 * i + 2], og = gf[5 * i + 3], ug = gf[5 * i + 4];
+        const float tc = tanh_t(f4(x.c, i));
+        const float dc = f4(x.dc, i) + dh[i] * og * (1.f - tc * tc);
+        dz[5 * i] = dc * ug * ig * (1.f - ig);
+        dz[5 * i + 1] = dc * f4(x.cl, i) * fl * (1.f - fl);
+        dz[5 * i + 2] = dc * f4(x.cr, i) * fr * (1.f - fr);
+        dz[5 * i + 3] = dh[i] * tc * og * (1.f - og);
+        dz[5 * i + 4] = dc * ig * (1.f - ug * ug);
+        dcl[i] = dc * fl;
+        dcr[i] = dc * fr;
+      }
+      uint2 *o = reinterpret_cast<uint2 *>(t.DZ_int + (size_t)rk * d.P5 + 5 * u0);  // 40 B: 8-B aligned
+#pragma unroll
+      for (int q = 0; q < 5; ++q) o[q] = make_uint2(pack_bf2(dz[4 * q], dz[4 * q + 1]), pack_bf2(dz[4 * q + 2], dz[4 * q + 3]));
+      *reinterpret_cast<float4 *>(t.dc_node + kl * H + u0) = make_float4(dcl[0], dcl[1], dcl[2], dcl[3]);
+      *reinterpret_cast<float4 *>(t.dc_node + kr * H + u0) = make_float4(dcr[0], dcr[1], dcr[2], dcr[3]);
+    }
+  } else if constexpr (!RNN) {
+    const int pos = -1 - rk;
+    const float *gf = reinterpret_cast<const float *>(x.g);  // 12 gates, 3 per unit
+    float dz[12];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float ig = gf[3 * i], og = gf[3 * i + 1], ug = gf[3 * i + 2];
+      const float tc = tanh_t(f4(x.c, i));
+      const float dc = f4(x.dc, i) + dh[i] * og * (1.f - tc * tc);
+      dz[3 * i] = dc * ug * ig * (1.f - ig);
+      dz[3 * i + 1] = dh[i] * tc * og * (1.f - og);
+      dz[3 * i + 2] = dc * ig * (1.f - ug * ug);
+    }
+    uint2 *o = reinterpret_cast<uint2 *>(t.DZ_leaf + (size_t)pos * d.P3 + 3 * u0);  // 24 B
+#pragma unroll
+    for (int q = 0; q < 3; ++q) o[q] = make_uint2(pack_bf2(dz[4 * q], dz[4 * q + 1]), pack_bf2(dz[4 * q + 2], dz[4 * q + 3]));
+  }
+}
+
+template <bool RNN>
+JN_DEV void node_cell_bwd(const TreeBufs &t, const TreeDims &d, int n, int rk, int kl, int kr, int u, float dh) {
+  CellIn x;
+  cell_load<RNN>(t, d, n, rk, u, x);
+  cell_apply<RNN>(t, d, rk, kl, kr, u, dh, x);
+}
+
 // =============================================================================== root classifier
 // y = rb(h_root) rb(W_c)^T + b_c; loss = mean over trees of xent(y, label) (reading Q6);
 // dy = (softmax - onehot) / B; dW_c = sum rb(dy)^T rb(h); db_c = sum rb(dy); dh_root = rb(dy) rb(W_c).
@@ -916,15 +1077,27 @@ __global__ void __launch_bounds__(256) tree_root_kernel(TreeBufs t, TreeDims d, 
     for (int tr = 0; tr < nt; ++tr) acc += dyr[tr * C + c];
     part[C * H + c] = acc;
   }
-  // dh of each root node (dc of a root = 0)
-  for (int e = threadIdx.x; e < nt * H; e += blockDim.x) {
-    const int tr = e / H, k = e - tr * H;
+  // dh of each root node (dc of a root = 0) and the root's cell backward: the backward kernel
+  // then starts with the top level's dgrad
+  const int uq = (H & 3) == 0 ? 4 : 1;  // units per item (16-B vectors when H % 4 == 0)
+  for (int e = threadIdx.x; e < nt * (H / uq); e += blockDim.x) {
+    const int tr = e / (H / uq), k = (e - tr * (H / uq)) * uq;
     const int root = sroot[tr];
     if (root < 0 || root >= d.N) continue;
-    float acc = 0.f;
-    for (int c = 0; c < C; ++c) acc += dyr[tr * C + c] * bf16_round(__ldg(t.Wc + (size_t)c * H + k));
-    t.dh_node[(size_t)root * H + k] = acc;
-    t.dc_node[(size_t)root * H + k] = 0.f;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < C; ++c)
+      for (int i = 0; i < uq; ++i) acc[i] += dyr[tr * C + c] * bf16_round(__ldg(t.Wc + (size_t)c * H + k + i));
+    for (int i = 0; i < uq; ++i) t.dc_node[(size_t)root * H + k + i] = 0.f;
+    const int rk = s.irank[root];
+    const int kl = rk >= 0 && !d.rnn ? t.left[root] : 0, kr = rk >= 0 && !d.rnn ? t.right[root] : 0;
+    if (uq == 4) {
+      if (d.rnn) { CellIn4 x; cell4_load<true>(t, d, root, rk, k, x); cell4_apply<true>(t, d, rk, kl, kr, k, acc, x); }
+      else { CellIn4 x; cell4_load<false>(t, d, root, rk, k, x); cell4_apply<false>(t, d, rk, kl, kr, k, acc, x); }
+    } else if (d.rnn) {
+      node_cell_bwd<true>(t, d, root, rk, kl, kr, k, acc[0]);
+    } else {
+      node_cell_bwd<false>(t, d, root, rk, kl, kr, k, acc[0]);
+    }
   }
   // the last block sums the shares in block order
   __threadfence();
@@ -961,7 +1134,11 @@ struct TreeBwdMaps {
 // memory for the whole launch and only streams dz per level (the dgrad's B operand does not
 // change between levels); else both operands stream through the ring.
 constexpr int T_RES_CHUNKS = 24;  // resident K chunks (5H <= 1536)
-constexpr int T_RES_NT = 32;
+constexpr int T_RES_NT = 16;  // narrow tiles: 2H / 16 CTAs share each level's fused epilogue
+
+// Per tile row (a parent of the level): its two children, their internal ranks and (internal
+// children) the grandchildren that receive dc — loaded while the MMAs run.
+struct BwdRowMeta { int ch[2], rk[2], gk[2][2]; };
 
 template <bool RES, bool RNN>
 __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__ TreeBwdMaps mp,
@@ -970,15 +1147,19 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   extern __shared__ uint8_t smem_raw[];
   uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                               ~uintptr_t(1023));
+  constexpr int BNT = RES ? T_RES_NT : 64;
+  constexpr int BW_STAGES = RES ? T_STAGES : 6;  // streamed B: room for the staged 64-column tile
   Ring rg;
   rg.sA = base;
-  rg.sB = base + T_STAGES * T_ASTAGE;
-  uint8_t *after = RES ? rg.sB + T_RES_CHUNKS * T_RES_NT * 128 : rg.sB + T_STAGES * T_BSTAGE;
+  rg.sB = base + BW_STAGES * T_ASTAGE;
+  uint8_t *after = RES ? rg.sB + T_RES_CHUNKS * T_RES_NT * 128 : rg.sB + BW_STAGES * T_BSTAGE;
   rg.full = reinterpret_cast<uint64_t *>(after);
-  rg.empty = rg.full + T_STAGES;
-  rg.tfull = rg.empty + T_STAGES;
+  rg.empty = rg.full + BW_STAGES;
+  rg.tfull = rg.empty + BW_STAGES;
   uint64_t *bres_bar = rg.tfull + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bres_bar + 1);
+  rg.zst = reinterpret_cast<float *>(after + 256);
+  BwdRowMeta *meta = reinterpret_cast<BwdRowMeta *>(rg.zst + 128 * (BNT + 1));
   const int warp = threadIdx.x >> 5;
   const int H = d.H;
   const int NGH = RNN ? H : 5 * H;  // K of the dgrad (dz width)
@@ -992,7 +1173,7 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
     rg.bres_nn = (int)blockIdx.x < res_groups * res_ntile ? (int)blockIdx.x % res_ntile : -1;
   }
   if (threadIdx.x == 128) {
-    for (int i = 0; i < T_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
+    for (int i = 0; i < BW_STAGES; ++i) { mbar_init(&rg.full[i], 1); mbar_init(&rg.empty[i], 1); }
     mbar_init(rg.tfull, T_NMW);
     mbar_init(bres_bar, 1);
     fence_barrier_init();
@@ -1013,86 +1194,75 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   const int L = s.meta[0], n0 = s.meta[2], nint = s.meta[3];
   unsigned int ep = 0;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  // Top-down over the internal levels. The dz rows of level l are complete when its turn comes:
+  // the roots' by the classifier kernel, every other node's by its parent's level (higher).
+  // One grid barrier per level: [dh_l ; dh_r] = rb(dz) U lands per tile column, and since a
+  // child's h feeds only its parent, that column of the child's dh is final — the epilogue runs
+  // the child's cell backward right there (its DZ row, its children's dc; leaves too).
   for (int l = L - 1; l >= 1; --l) {
     const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
-    // (a) cell backward of this level's nodes: their dh / dc were written by the parents
-    if constexpr (RNN) {  // TreeRNN: dz = dh (1 - h^2)
-      for (long long e = gt; e < (long long)cnt * H; e += gs) {
-        const int row = (int)(e / H), u = (int)(e % H);
-        const int ir = r0 + row, n = s.order[p0 + row];
-        const float h = t.c_int[(size_t)ir * H + u];
-        t.DZ_int[(size_t)ir * d.P5 + u] = __float2bfloat16_rn(t.dh_node[(size_t)n * H + u] * (1.f - h * h));
-      }
-    } else
-    for (long long e = gt; e < (long long)cnt * H; e += gs) {
-      const int row = (int)(e / H), u = (int)(e % H);
-      const int ir = r0 + row, n = s.order[p0 + row];
-      const float dh = t.dh_node[(size_t)n * H + u];
-      const float *g = t.gates_int + (size_t)ir * 5 * H + 5 * u;
-      const float ig = g[0], fl = g[1], fr = g[2], og = g[3], ug = g[4];
-      const float tc = tanh_t(t.c_int[(size_t)ir * H + u]);
-      const float dout = dh * tc;
-      const float dc = t.dc_node[(size_t)n * H + u] + dh * og * (1.f - tc * tc);
-      const float cl = t.stage_c[(size_t)ir * 2 * H + u], cr = t.stage_c[(size_t)ir * 2 * H + H + u];
-      __nv_bfloat16 *dz = t.DZ_int + (size_t)ir * d.P5 + 5 * u;
-      dz[0] = __float2bfloat16_rn(dc * ug * ig * (1.f - ig));
-      dz[1] = __float2bfloat16_rn(dc * cl * fl * (1.f - fl));
-      dz[2] = __float2bfloat16_rn(dc * cr * fr * (1.f - fr));
-      dz[3] = __float2bfloat16_rn(dout * og * (1.f - og));
-      dz[4] = __float2bfloat16_rn(dc * ig * (1.f - ug * ug));
-      const int lc = t.left[n], rc = t.right[n];
-      t.dc_node[(size_t)lc * H + u] = dc * fl;
-      t.dc_node[(size_t)rc * H + u] = dc * fr;
-    }
-    fence_proxy_async_global();
-    grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
-    // (b) [dh_l ; dh_r] = rb(dz) U, scattered to the two children (each child has one parent)
-    constexpr int BNT = RES ? T_RES_NT : 64;
-    tile_loop<BNT>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, NGH, [&](int row, int) {
-      int2 c = make_int2(0, 0);
+    tile_loop<BNT, 2, BW_STAGES>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, NGH, [&](int row, int) {
       if (row >= 0) {
+        BwdRowMeta m;
         const int n = s.order[p0 + row];
-        c = make_int2(t.left[n], t.right[n]);
+        m.ch[0] = t.left[n];
+        m.ch[1] = t.right[n];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          m.rk[c] = s.irank[m.ch[c]];
+          m.gk[c][0] = m.rk[c] >= 0 && !RNN ? t.left[m.ch[c]] : 0;
+          m.gk[c][1] = m.rk[c] >= 0 && !RNN ? t.right[m.ch[c]] : 0;
+        }
+        meta[threadIdx.x] = m;
       }
-      return c;
-    }, [&](int row, int col0, float *z, int2 ch) {
-      const int lc = ch.x, rc = ch.y;
-      const bool vec = (H % 4) == 0;  // then a 4-column group never straddles the two children
+      return 0;
+    }, [&](int, int nrows, int col0) {
+      // every warp of the CTA over the tile's (row, 4-column) items, IB per thread with all
+      // their loads issued before any store; scalar items when H % 4 != 0
+      constexpr int IB = 2;
+      const int nth = blockDim.x;
+      if ((H & 3) == 0) {
+        constexpr int NQ = BNT / 4;
+        const int items = nrows * NQ;
+        for (int i0 = threadIdx.x; i0 < items; i0 += nth * IB) {
+          CellIn4 x[IB];
+          int rl[IB], k[IB];
 #pragma unroll
-      for (int j = 0; j < BNT; j += 4) {
-        const int k = col0 + j;
-        if (k >= 2 * H) break;
-        float *dst = k < H ? t.dh_node + (size_t)lc * H + k : t.dh_node + (size_t)rc * H + (k - H);
-        if (vec) {
-          *reinterpret_cast<float4 *>(dst) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
-        } else {
+          for (int b = 0; b < IB; ++b) {
+            const int i = i0 + nth * b;
+            rl[b] = i / NQ;
+            k[b] = col0 + 4 * (i - rl[b] * NQ);
+            if (i < items && k[b] < 2 * H) {
+              const int side = k[b] >= H ? 1 : 0;
+              const BwdRowMeta &m = meta[rl[b]];
+              cell4_load<RNN>(t, d, m.ch[side], m.rk[side], k[b] - side * H, x[b]);
+            }
+          }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int ki = k + i;
-            if (ki >= 2 * H) break;
-            if (ki < H) t.dh_node[(size_t)lc * H + ki] = z[j + i];
-            else t.dh_node[(size_t)rc * H + (ki - H)] = z[j + i];
+          for (int b = 0; b < IB; ++b) {
+            if (i0 + nth * b < items && k[b] < 2 * H) {
+              const int side = k[b] >= H ? 1 : 0;
+              const BwdRowMeta &m = meta[rl[b]];
+              cell4_apply<RNN>(t, d, m.rk[side], m.gk[side][0], m.gk[side][1], k[b] - side * H,
+                               rg.zst + rl[b] * (BNT + 1) + (k[b] - col0), x[b]);
+            }
           }
         }
+      } else {
+        const int items = nrows * BNT;
+        for (int i = threadIdx.x; i < items; i += nth) {
+          const int rl = i / BNT, j = i - rl * BNT, k = col0 + j;
+          if (k >= 2 * H) continue;
+          const int side = k >= H ? 1 : 0;
+          const BwdRowMeta &m = meta[rl];
+          node_cell_bwd<RNN>(t, d, m.ch[side], m.rk[side], m.gk[side][0], m.gk[side][1], k - side * H,
+                             rg.zst[rl * (BNT + 1) + j]);
+        }
       }
-    }, (NGH + 63) / 64 >= 16 ? 4 : ((NGH + 63) / 64 >= 8 ? 2 : 1),
+    }, (NGH + 63) / 64 >= 16 ? (RES ? 4 : 3) : ((NGH + 63) / 64 >= 8 ? 2 : 1),  // a fixed warp per stage
        t.dbg ? t.dbg + 3 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.dz32);
+    fence_proxy_async_global();  // the children's DZ rows feed the next level's TMA loads
     grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
-  }
-  // leaves: dz = [di i(1-i), do o(1-o), du (1-u^2)]  (TreeRNN: frozen word vectors, nothing)
-  if constexpr (!RNN)
-  for (long long e = gt; e < (long long)n0 * H; e += gs) {
-    const int pos = (int)(e / H), u = (int)(e % H);
-    const int n = s.order[pos];
-    const float dh = t.dh_node[(size_t)n * H + u];
-    const float *g = t.gates_leaf + (size_t)pos * 3 * H + 3 * u;
-    const float ig = g[0], og = g[1], ug = g[2];
-    const float tc = tanh_t(t.c_leaf[(size_t)pos * H + u]);
-    const float dc = t.dc_node[(size_t)n * H + u] + dh * og * (1.f - tc * tc);
-    __nv_bfloat16 *dz = t.DZ_leaf + (size_t)pos * d.P3 + 3 * u;
-    dz[0] = __float2bfloat16_rn(dc * ug * ig * (1.f - ig));
-    dz[1] = __float2bfloat16_rn(dh * tc * og * (1.f - og));
-    dz[2] = __float2bfloat16_rn(dc * ig * (1.f - ug * ug));
   }
   // zero the dz rows of the last partial 64-row K chunk of the wgrad GEMMs
   for (long long e = gt; e < (long long)(((nint + 63) & ~63) - nint) * d.P5; e += gs)
@@ -1123,7 +1293,8 @@ cudaError_t launch_tree_bwd(const TreeBufs &t, const TreeDims &d, const TreeSche
     key = k;
   }
   const bool res = ((int)ngh + 63) / 64 <= T_RES_CHUNKS && grid >= (2 * d.H + T_RES_NT - 1) / T_RES_NT;
-  const int smem = res ? 1024 + T_STAGES * T_ASTAGE + T_RES_CHUNKS * T_RES_NT * 128 + 256 : tree_smem();
+  const int stage = 256 + 128 * ((res ? T_RES_NT : 64) + 1) * 4 + 128 * (int)sizeof(BwdRowMeta);
+  const int smem = 1024 + (res ? T_STAGES * T_ASTAGE + T_RES_CHUNKS * T_RES_NT * 128 : 6 * (T_ASTAGE + T_BSTAGE)) + stage;
   const void *fn = d.rnn ? (res ? (const void *)tree_bwd_kernel<true, true> : (const void *)tree_bwd_kernel<false, true>)
                          : (res ? (const void *)tree_bwd_kernel<true, false> : (const void *)tree_bwd_kernel<false, false>);
   cudaError_t e = set_smem_once(fn, smem);

@@ -70,16 +70,17 @@ for l in range(1, L):
     print(f"  level {l:2d} ({int(lvl[l + 1] - lvl[l]):4d} nodes, {int(act.sum())} CTAs): "
           f"mainloop {(pr[act, 0].max() - start) / 1e3:5.2f} us  tmem {((pr[act, 2] - pr[act, 0]).max()) / 1e3:5.2f} us  epilogue {((pr[act, 1] - pr[act, 2]).max()) / 1e3:5.2f} us")
 
-# backward dgrad tile loops: level l runs after barrier 2 * (L - 1 - l) + 2 of the backward kernel
-print("-- backward dgrad levels")
+# backward dgrad tile loops (one barrier per level: the cell backward runs in the dgrad
+# epilogue): level l runs after barrier L - 2 - l of the backward kernel (the top level at entry)
+print("-- backward dgrad levels (+ fused cell backward)")
 ab, rb = p[1, :, :grid, 0], p[1, :, :grid, 1]
 for l in range(L - 1, 0, -1):
     pr = q5[l, :grid]
     act = pr[:, 0] > 0
     if not act.any():
         continue
-    k = 2 * (L - 1 - l) + 1
-    start = np.median(rb[k])
+    k = L - 2 - l
+    start = np.median(rb[k]) if k >= 0 else np.min(ab[0])
     print(f"  level {l:2d} ({int(lvl[l + 1] - lvl[l]):4d} nodes, {int(act.sum())} CTAs): "
           f"mainloop {(pr[act, 0].max() - start) / 1e3:5.2f} us  tmem {((pr[act, 2] - pr[act, 0]).max()) / 1e3:5.2f} us  epilogue {((pr[act, 1] - pr[act, 2]).max()) / 1e3:5.2f} us")
 
