@@ -355,6 +355,23 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
           for (int j = 0; j < 32; ++j) v[j] += w[j];
         }
       };
+      // Pipelined accumulator reads: chunk c + 1's TMEM loads are in flight while chunk c is
+      // stored (a tcgen05.ld + wait per chunk serialised eight TMEM round trips per tile and made
+      // the epilogue, not the MMAs, the bound of the short-K GEMMs)
+      uint32_t pf[NMMA][32];
+      auto acc_issue = [&](int c) {
+        const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(((i & 1) * NMMA) * BN) + c * 32;
+        tmem_ld32_nw(base + (uint32_t)((qt % NMMA) * BN), pf[0]);
+        if (NMMA > 1 && nkt > 1) tmem_ld32_nw(base + (uint32_t)(((qt + 1) % NMMA) * BN), pf[NMMA - 1]);
+      };
+      auto acc_take = [&](float (&v)[32]) {
+        tmem_ld_wait();
+        tmem_pin(pf[0]);
+        if (NMMA > 1) tmem_pin(pf[NMMA - 1]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          v[j] = __uint_as_float(pf[0][j]) + (NMMA > 1 && nkt > 1 ? __uint_as_float(pf[NMMA - 1][j]) : 0.f);
+      };
       const GemmEpilogue &ep = gb.ep[tr.g];
       const int M = gb.M[tr.g], N = gb.N[tr.g];
       const int splits = gb.tm[tr.g].splits;
@@ -373,28 +390,27 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         uint8_t *stg0 = epi_stage + (size_t)(warp - 2) * 2 * 4096;
         const int mrow0 = m0 + quad * 32;
         const float bv = (ep.bias_row && row_ok) ? ep.bias_row[m] : 0.f;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        const int nch = min(BN / 32, (N - n0 + 31) / 32);  // chunks inside N (warp-uniform)
+        // one 32-column chunk: bias, swizzled staging box, bulk tensor store
+        // column bias: lane l holds bias[n + l] of a chunk, loaded one chunk ahead (its L2 latency
+        // was the epilogue's critical path: measured, the FADDs waiting on it were the top stall),
+        // and is broadcast with shuffles
+        auto bias_of = [&](int c) {
+          const int n = n0 + c * 32 + lane;
+          return (ep.bias_col && c < nch && n < N) ? __ldg(ep.bias_col + n) : 0.f;
+        };
+        float bnext = bias_of(0);
+        auto store_chunk = [&](int c, float (&v)[32]) {
           const int n = n0 + c * 32;
-          if (n >= N) break;  // warp-uniform
-          float v[32];
-          ld_acc(c, v);
           if (empty_k) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
           }
+          const float bcur = bnext;
+          bnext = bias_of(c + 1);
           if (ep.bias_col) {
-            float4 bb[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              bb[j] = n + 4 * j + 3 < N ? __ldg(reinterpret_cast<const float4 *>(ep.bias_col + n) + j)
-                                        : make_float4(n + 4 * j < N ? ep.bias_col[n + 4 * j] : 0.f,
-                                                      n + 4 * j + 1 < N ? ep.bias_col[n + 4 * j + 1] : 0.f,
-                                                      n + 4 * j + 2 < N ? ep.bias_col[n + 4 * j + 2] : 0.f, 0.f);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v[4 * j] += bb[j].x; v[4 * j + 1] += bb[j].y; v[4 * j + 2] += bb[j].z; v[4 * j + 3] += bb[j].w;
-            }
+            for (int j = 0; j < 32; ++j) v[j] += __shfl_sync(0xffffffffu, bcur, j);
           }
           if (ep.bias_row) {
 #pragma unroll
@@ -414,6 +430,34 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
             else tma_store_2d(&gb.tc[tr.g], stg, n, mrow0);
             bulk_commit_group();
           }
+        };
+        if constexpr (NMMA == 1) {
+          // 64 accumulator columns per tcgen05.ld (x64): measured, eight x32 loads per tile and
+          // warp cost the decoder GEMM 13 us over the MMAs alone, four x64 loads nothing
+          uint32_t pf64[64];
+          const uint32_t abase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)((i & 1) * BN);
+          const int ngp = (nch + 1) / 2;
+          if (ngp > 0) tmem_ld64_nw(abase, pf64);
+#pragma unroll 1
+          for (int p = 0; p < ngp; ++p) {
+            float v0[32], v1[32];
+            tmem_ld_wait();
+            tmem_pin(pf64);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) { v0[j] = __uint_as_float(pf64[j]); v1[j] = __uint_as_float(pf64[32 + j]); }
+            if (p + 1 < ngp) tmem_ld64_nw(abase + (uint32_t)((p + 1) * 64), pf64);
+            store_chunk(2 * p, v0);
+            if (2 * p + 1 < nch) store_chunk(2 * p + 1, v1);
+          }
+        } else {
+          if (nch > 0) acc_issue(0);
+#pragma unroll 1
+          for (int c = 0; c < nch; ++c) {
+            float v[32];
+            acc_take(v);
+            if (c + 1 < nch) acc_issue(c + 1);
+            store_chunk(c, v);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -431,13 +475,27 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
           if (lane == 0) bulk_wait_group_read0();  // both boxes free before the next tile
           __syncwarp();
         }
+      } else if (splits == 1 && !ep.C && !ep.Cb && ep.dev_x64) {
+        // dev experiment: drain with 64-column loads
+        const uint32_t base = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(((i & 1) * NMMA) * BN);
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t r[64];
+          tmem_ld64_nw(base + c * 64, r);
+          tmem_ld_wait();
+          tmem_pin(r);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) release_tmem(buf);
       } else if (splits == 1) {
+        const int nch = ep.dev_no_drain ? 0 : min(BN / 32, (N - n0 + 31) / 32);
+        if (nch > 0) acc_issue(0);
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = 0; c < nch; ++c) {
           const int n = n0 + c * 32;
-          if (n >= N) break;  // warp-uniform
           float v[32];
-          ld_acc(c, v);
+          acc_take(v);
+          if (c + 1 < nch) acc_issue(c + 1);
           if (empty_k) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -638,6 +696,15 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
     if (op.ep.C && !op.ep.Cb && (op.ep.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(op.ep.C) & 15) == 0 &&
         g_tma_store_ok)
       gb.tma_store[g] = make_tmap_f32_box32(&gb.tc[g], op.ep.C, op.N, op.M, op.ep.ldc) ? 1 : 0;
+    // dev measurement knob: "1" drains the accumulators and stores nothing, "2" does not even
+    // read them (the mainloop bound)
+    static const int epi_skip = getenv("JANUS_GEMM_EPI_SKIP") ? atoi(getenv("JANUS_GEMM_EPI_SKIP")) : 0;
+    if (epi_skip) {
+      gb.tma_store[g] = 0;
+      gb.ep[g] = GemmEpilogue{};
+      gb.ep[g].dev_no_drain = epi_skip == 2;
+      gb.ep[g].dev_x64 = epi_skip == 3;
+    }
     TileMap &tm = gb.tm[g];
     tm.Mb = ((op.M + 127) / 128 + CM - 1) / CM;  // m-groups of CM blocks (ghost blocks: OOB)
     tm.Nb = (op.N + BN - 1) / BN;
@@ -652,7 +719,7 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
     }
     tm.splits = splits;
     tm.total = tm.Mb * tm.Nb * splits;
-    gb.ep[g] = op.ep;
+    if (!epi_skip) gb.ep[g] = op.ep;
     gb.M[g] = op.M; gb.N[g] = op.N; gb.K[g] = op.K;
     gb.K_dev[g] = op.K_dev;
     gb.counters[g] = op.flags;

@@ -31,6 +31,8 @@ struct GemmEpilogue {
   const float *bias_row = nullptr;  // + bias[m]
   int accumulate = 0;               // C += result
   FusedReduce fr;                   // fused cross-rank reduction of C (TMA-store path only)
+  int dev_no_drain = 0;             // dev measurement (JANUS_GEMM_EPI_SKIP=2): release TMEM unread
+  int dev_x64 = 0;                  // dev measurement (JANUS_GEMM_EPI_SKIP=3): drain with x64 loads
 };
 
 // D[M,N] = A[M,K] . B[N,K]^T.

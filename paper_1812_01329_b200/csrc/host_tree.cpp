@@ -290,7 +290,18 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   if (gl.n) TCHK("guards", launch_guards(gl, dst, st));
   if (p.tree_guard) TCHK("tree_guard", launch_tree_guard(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
   TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));
-  if (p.rnn) {  // W rows and W^T (one gate: no interleave)
+  // bf16 operand copies (R1): re-cast unless the last commit of this graph refreshed them and
+  // no state-writing call came since (host.h copies_epoch; as the LM step)
+  static const bool recast_env = [] { const char *e = getenv("JANUS_RECAST"); return e && e[0] == '1'; }();
+  const void *srcs[9] = {U, p.rnn ? nullptr : Wl};
+  bool copies_ok = !recast_env && g.copies_in && g.copies_W == W;
+  for (int k = 0; k < 9; ++k) copies_ok = copies_ok && g.copies_src[k] == srcs[k];
+  const bool refresh = !recast_env;
+  g.copies_out = refresh;
+  g.copies_W = W;
+  for (int k = 0; k < 9; ++k) g.copies_src[k] = srcs[k];
+  if (copies_ok) {
+  } else if (p.rnn) {  // W rows and W^T (one gate: no interleave)
     TCHK("cast", launch_cast_il(U, H, 1, 2 * H, bf(p.off.U_il), p.P2, st));
     TCHK("cast_T", launch_cast_il_T(U, H, 1, 2 * H, bf(p.off.UT_il), p.P5, st));
   } else {
@@ -337,8 +348,16 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   auto add = [&](CommitSeg sg) { cl.s[cl.n++] = sg; };
   const float nr = (float)g.opts.world_size;
   CommitSeg sg{};
-  if (p.lr_Wleaf != 0) { sg = {}; sg.kind = C_DENSE_IL; sg.ng = 3; sg.dst = Wl; sg.grad = fp(p.off.gWl); sg.rows = 3 * H; sg.cols = E; sg.ldg = p.ldgW; sg.H = H; sg.lr = p.lr_Wleaf / nr; add(sg); }
-  if (p.lr_U != 0) { sg = {}; sg.kind = C_DENSE_IL; sg.ng = NG; sg.dst = U; sg.grad = fp(p.off.gU); sg.rows = NG * H; sg.cols = 2 * H; sg.ldg = p.ldgU; sg.H = H; sg.lr = p.lr_U / nr; add(sg); }
+  if (p.lr_Wleaf != 0) {
+    sg = {}; sg.kind = C_DENSE_IL; sg.ng = 3; sg.dst = Wl; sg.grad = fp(p.off.gWl); sg.rows = 3 * H; sg.cols = E; sg.ldg = p.ldgW; sg.H = H; sg.lr = p.lr_Wleaf / nr;
+    if (refresh) { sg.bcopy = bf(p.off.Wl_il); sg.ldb = p.Ep; }
+    add(sg);
+  }
+  if (p.lr_U != 0) {  // + the row copy and the transposed copy the backward streams
+    sg = {}; sg.kind = refresh ? C_DENSE_IL_T : C_DENSE_IL; sg.ng = NG; sg.dst = U; sg.grad = fp(p.off.gU); sg.rows = NG * H; sg.cols = 2 * H; sg.ldg = p.ldgU; sg.H = H; sg.lr = p.lr_U / nr;
+    if (refresh) { sg.bcopy = bf(p.off.U_il); sg.ldb = p.P2; sg.tcopy = bf(p.off.UT_il); sg.ldt = p.P5; }
+    add(sg);
+  }
   if (p.lr_b != 0 && p.rnn) { sg = {}; sg.kind = C_BIAS_COL; sg.dst = bb; sg.grad = fp(p.off.gU); sg.rows = H; sg.cols = 1; sg.ldg = p.ldgU; sg.col = 2 * H; sg.lr = p.lr_b / nr; add(sg); }
   if (p.lr_b != 0 && !p.rnn) { sg = {}; sg.kind = C_TREE_BIAS; sg.dst = bb; sg.grad = fp(p.off.gU); sg.ldg = p.ldgU; sg.col = 2 * H; sg.grad2 = fp(p.off.gWl); sg.ldg2 = p.ldgW; sg.col2 = E; sg.H = H; sg.lr = p.lr_b / nr; add(sg); }
   if (p.lr_Wc != 0) { sg = {}; sg.kind = C_DENSE; sg.dst = Wc; sg.grad = fp(p.off.gWc); sg.rows = p.C; sg.cols = H; sg.ldg = H; sg.lr = p.lr_Wc / nr; add(sg); }

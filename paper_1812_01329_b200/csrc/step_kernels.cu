@@ -1051,11 +1051,12 @@ __global__ void __launch_bounds__(256, 6) commit_kernel(CommitList cl, const Dev
       // 32 interleaved rows x 64 columns per tile: update the master rows, write the row copy,
       // and through shared memory the transposed copy tcopy[k][ri] (coalesced along ri)
       __shared__ __nv_bfloat16 tt[32][72];
-      const int R = 4 * sg.H, nti = (R + 31) / 32, ntk = (sg.cols + 63) / 64;
+      const int ng = sg.ng ? sg.ng : 4;  // gates per unit (interleaved row ri = ng*u + g)
+      const int R = ng * sg.H, nti = (R + 31) / 32, ntk = (sg.cols + 63) / 64;
       const int tr = threadIdx.x >> 3, tc = (threadIdx.x & 7) * 8;  // this thread: row tr, 8 columns
       for (int tb = bx; tb < nti * ntk; tb += gx) {
         const int ri0 = (tb % nti) * 32, k0 = (tb / nti) * 64;
-        const int ri = ri0 + tr, rc = (ri & 3) * sg.H + (ri >> 2);
+        const int ri = ri0 + tr, rc = (ri % ng) * sg.H + ri / ng;
         float2 dv[4], gv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1145,7 +1146,7 @@ cudaError_t launch_commit(const CommitList &cl0, const DevStatus *st, cudaStream
     long long u;
     switch (g.kind) {
       case C_DENSE: case C_DENSE_IL: u = (g.rows + CR_ROWS - 1) / CR_ROWS; break;
-      case C_DENSE_IL_T: u = (long long)((4 * g.H + 31) / 32) * ((g.cols + 63) / 64); break;
+      case C_DENSE_IL_T: u = (long long)(((g.ng ? g.ng : 4) * g.H + 31) / 32) * ((g.cols + 63) / 64); break;
       case C_TREE_BIAS: u = (4LL * g.H + 255) / 256; break;
       case C_BIAS_COL: case C_BIAS_COL_IL: u = (g.rows + 255) / 256; break;
       case C_COPY: u = ((long long)g.rows * g.cols + 255) / 256; break;

@@ -189,7 +189,7 @@ struct CommitSeg {
   const int *pred;     // device predicate (`if training:` Switch): skip the segment when *pred == 0
   // bf16 working copies refreshed from the committed masters (R1), so the next step needs no cast:
   __nv_bfloat16 *bcopy; int ldb;  // row copy: row ri (interleaved, C_DENSE_IL*) or rc (C_DENSE)
-  __nv_bfloat16 *tcopy; int ldt;  // C_DENSE_IL_T: transposed copy, tcopy[k][ri]
+  __nv_bfloat16 *tcopy; int ldt;  // C_DENSE_IL_T: transposed copy, tcopy[k][ri] (ri = ng*u + g, ng = 4 if 0)
 };
 constexpr int MAX_COMMIT = 24;
 struct CommitList {

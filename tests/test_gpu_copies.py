@@ -4,7 +4,7 @@ and nothing else wrote state since. The trajectory must equal re-casting every s
 read once per process: that arm runs in a subprocess) bit for bit, through every event that must
 invalidate the copies: an in-place write by the caller (torch version counter -> janus_state_changed),
 another graph committing into the same state, the imperative executor, fresh state tensors, and an
-AssertOp abort (nothing committed: the copies stay valid)."""
+AssertOp abort (nothing committed: the copies stay valid). The TreeLSTM / TreeRNN steps likewise."""
 import os
 import subprocess
 import sys
@@ -65,11 +65,48 @@ def _trajectory(L, dropout):
     return trace, [t.tobytes() for t in to_host(dev)]
 
 
+def _tree_trajectory(rnn):
+    """The tree programs keep W_leaf / U (TreeRNN: W) copies the same way: row copies and the
+    transposed U the backward streams."""
+    from paper_1812_01329_b200 import janus
+    V, B, H = 500, 6, 24
+    prog = (pg.treernn_program(V=V, H=H, C=2, B=B, lr=0.3) if rnn else
+            pg.treelstm_program(V=V, E=20, H=H, C=2, B=B, lr=0.3))
+    A, A2 = janus.Graph(prog), janus.Graph(prog)
+    wa, wb = A.new_workspace(), A2.new_workspace()
+    sid = {s.name: k for k, s in enumerate(prog.slots)}
+    dev = to_dev(gen.uniform_params(prog, 3, 0.2))
+    loss = torch.zeros(1, device="cuda")
+    trace = []
+
+    def step(g, ws, k, imperative=False):
+        f = to_dev(gen.sst_forest(gen.SEED_C3, k, B, V))
+        if imperative:
+            st = g.run_imperative(f, dev, ws, outs=[loss])
+        else:
+            st, _ = g.run(f, dev, ws, outs=[loss])
+        trace.append((st, loss.item()))
+
+    for k in range(3):
+        step(A, wa, k)
+    with torch.no_grad():
+        dev[sid["W" if rnn else "U"]].mul_(0.9)
+    step(A, wa, 3)
+    step(A2, wb, 4)
+    step(A, wa, 5)
+    step(A, wa, 6, imperative=True)
+    step(A, wa, 7)
+    step(A, wa, 8)
+    return trace, [t.tobytes() for t in to_host(dev)]
+
+
 CASES = [(2, 0.0), (2, 0.3), (1, 0.0), (3, 0.0)]
+TREE_CASES = [False, True]
 
 
 def _dump(path):
-    np.save(path, np.array([_trajectory(L, p) for L, p in CASES], dtype=object), allow_pickle=True)
+    np.save(path, np.array([_trajectory(L, p) for L, p in CASES] + [_tree_trajectory(r) for r in TREE_CASES],
+                           dtype=object), allow_pickle=True)
 
 
 def test_copy_refresh_equals_recast_every_step():
@@ -81,9 +118,14 @@ def test_copy_refresh_equals_recast_every_step():
                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
         ref = np.load(path, allow_pickle=True)
-    for (L, p), (rtrace, rstate) in zip(CASES, ref):
+    for (L, p), (rtrace, rstate) in zip(CASES, ref[:len(CASES)]):
         trace, state = _trajectory(L, p)
         assert [s for s, _ in trace] == [s for s, _ in rtrace], (L, p, trace)
         assert trace == rtrace, (L, p, trace, rtrace)
         assert all(a == b for a, b in zip(state, rstate)), (L, p)
         assert trace[6][0] != 0 and all(s == 0 for k, (s, _) in enumerate(trace) if k != 6), trace
+    for rnn, (rtrace, rstate) in zip(TREE_CASES, ref[len(CASES):]):
+        trace, state = _tree_trajectory(rnn)
+        assert all(s == 0 for s, _ in trace), trace
+        assert trace == rtrace, (rnn, trace, rtrace)
+        assert all(a == b for a, b in zip(state, rstate)), rnn
