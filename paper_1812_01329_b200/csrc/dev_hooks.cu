@@ -3,6 +3,7 @@
 #include "../../include/janus_dev.h"
 #include "common.cuh"
 #include "gemm_tc.h"
+#include <stdlib.h>
 
 extern "C" int32_t janus_dev_gemm_bf16(int32_t M, int32_t N, int32_t K, const void *A, int32_t lda,
                                        int32_t a_mn, const void *B, int32_t ldb, int32_t b_mn,
@@ -49,6 +50,8 @@ extern "C" int32_t janus_dev_gemm_bf16_splitk(int32_t M, int32_t N, int32_t K, c
   op.partials = partials;
   op.partials_cap = npart;
   op.splits = splits;
+  // dev knob: the two-way reduce-add split (GemmOp::split_add; C must be zero on entry)
+  op.split_add = getenv("JANUS_GEMM_SPLIT_ADD") && getenv("JANUS_GEMM_SPLIT_ADD")[0] == '1';
   cudaError_t e = jk::gemm_bf16(op, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? 0 : (int32_t)e;
 }

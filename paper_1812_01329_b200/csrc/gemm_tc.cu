@@ -106,6 +106,7 @@ struct GemmBatch {
   CUtensorMap ta[GB_MAX], tb[GB_MAX];
   CUtensorMap tc[GB_MAX];        // fp32 D, box {32, 32}, 128-B swizzle (TMA-store epilogue)
   int tma_store[GB_MAX];         // 1: epilogue through tc (fp32 D only, no bf16 copy)
+  int split_add[GB_MAX];         // 1: the K splits reduce-add into C (GemmOp::split_add)
   int amn[GB_MAX], bmn[GB_MAX];  // operand majors per GEMM (runtime: one kernel serves all four)
   GemmEpilogue ep[GB_MAX];
   int M[GB_MAX], N[GB_MAX], K[GB_MAX];
@@ -383,7 +384,8 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const bool row_ok = m < M;
-      if (splits == 1 && gb.tma_store[tr.g]) {
+      const bool sadd = gb.split_add[tr.g] != 0;
+      if ((splits == 1 || sadd) && gb.tma_store[tr.g]) {
         // TMA-store epilogue: each 32 x 32 block of this warp's rows goes registers -> swizzled
         // smem box -> one bulk tensor store (or reduce-add when accumulating), asynchronously;
         // two boxes per warp alternate (wait_group.read 1 before a box is rewritten)
@@ -395,9 +397,10 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         // column bias: lane l holds bias[n + l] of a chunk, loaded one chunk ahead (its L2 latency
         // was the epilogue's critical path: measured, the FADDs waiting on it were the top stall),
         // and is broadcast with shuffles
+        const bool add_bias = ep.bias_col && (!sadd || tr.sp == 0);  // split_add: split 0 adds it
         auto bias_of = [&](int c) {
           const int n = n0 + c * 32 + lane;
-          return (ep.bias_col && c < nch && n < N) ? __ldg(ep.bias_col + n) : 0.f;
+          return (add_bias && c < nch && n < N) ? __ldg(ep.bias_col + n) : 0.f;
         };
         float bnext = bias_of(0);
         auto store_chunk = [&](int c, float (&v)[32]) {
@@ -408,11 +411,11 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
           }
           const float bcur = bnext;
           bnext = bias_of(c + 1);
-          if (ep.bias_col) {
+          if (add_bias) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += __shfl_sync(0xffffffffu, bcur, j);
           }
-          if (ep.bias_row) {
+          if (ep.bias_row && (!sadd || tr.sp == 0)) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += bv;
           }
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
           fence_proxy_async_shared();
           __syncwarp();
           if (lane == 0) {
-            if (ep.accumulate) tma_reduce_add_2d(&gb.tc[tr.g], stg, n, mrow0);
+            if (ep.accumulate || sadd) tma_reduce_add_2d(&gb.tc[tr.g], stg, n, mrow0);
             else tma_store_2d(&gb.tc[tr.g], stg, n, mrow0);
             bulk_commit_group();
           }
@@ -655,6 +658,7 @@ static int choose_splits(int tiles, int nk, int nsm, size_t cap_tiles) {
 
 // may this op run split-K (single launch with scratch, explicit or automatic splits)?
 static bool op_wants_split(const GemmOp &op) {
+  if (op.split_add) return false;  // no scratch: the split rides the normal (clustered) kernel
   return op.flags && op.partials && (op.splits > 1 || (op.splits <= 0 && getenv("JANUS_GEMM_AUTOSPLIT")));
 }
 
@@ -712,10 +716,17 @@ static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
     const size_t cap_tiles = op.partials ? op.partials_cap / (128 * BN) : 0;
     int splits = 1;
     if (op.ep.fr.win && !gb.tma_store[g]) return cudaErrorInvalidValue;  // fused reduction: TMA-store path
-    if (CM == 1 && n == 1 && op.flags && op.partials && !op.ep.fr.win) {  // split-K only for single launches (own scratch)
+    gb.split_add[g] = 0;
+    if (op.split_add && op.splits == 2 && gb.tma_store[g] && !op.ep.accumulate && !op.ep.fr.win) {
+      splits = 2;  // K halves reduce-added into the zeroed C
+      gb.split_add[g] = 1;
+    } else
+    // split-K only for single launches (own scratch); with clusters (multicast / CTA pairs) only
+    // when asked for explicitly: both CTAs of a cluster take the same split of K
+    if (n == 1 && op.flags && op.partials && !op.ep.fr.win && (CM == 1 || op.splits > 1)) {
       splits = op.splits > 0 ? op.splits : choose_splits(tm.Mb * tm.Nb, nk, g_num_sms, cap_tiles);
       splits = std::max(1, std::min(splits, 64));
-      if ((size_t)tm.Mb * tm.Nb * splits > cap_tiles) splits = 1;
+      if ((size_t)tm.Mb * CM * tm.Nb * splits > cap_tiles) splits = 1;  // tile ids span Mb * CM rows
     }
     tm.splits = splits;
     tm.total = tm.Mb * tm.Nb * splits;
@@ -771,6 +782,9 @@ template <int BN>
 static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
   bool split = false;
   for (int g = 0; g < n; ++g) split = split || (op_wants_split(ops[g]) && n == 1);
+  // an explicit split of a long-K single launch keeps the CTA pair (same split on both CTAs)
+  const bool pair_split = split && n == 1 && ops[0].splits > 1 && want_pair(ops, n);
+  if (g_gemm_cm == 2 && pair_split) return launch_cm<BN, 2, true>(ops, n, st);
   if (g_gemm_cm == 2 && !split && want_pair(ops, n)) return launch_cm<BN, 2, true>(ops, n, st);
   if (g_gemm_cm == 2 && !split) return launch_cm<BN, 2>(ops, n, st);
   return launch_cm<BN, 1>(ops, n, st);
@@ -820,6 +834,10 @@ cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
   if (m > GB_MAX) return cudaErrorInvalidValue;
   // one launch for the whole group (the operand majors are per-GEMM runtime properties)
+  static const int bn_env = getenv("JANUS_GEMM_BN") ? atoi(getenv("JANUS_GEMM_BN")) : 0;  // dev knob
+  const int bn = m == 1 ? (bn_env ? bn_env : live[0].bn) : 0;
+  if (bn == 256) return launch<256>(live, m, st);
+  if (bn == 128) return launch<128>(live, m, st);
   if (use_bn256(live, m)) return launch<256>(live, m, st);
   return launch<128>(live, m, st);
 }

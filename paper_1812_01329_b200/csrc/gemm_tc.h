@@ -56,6 +56,11 @@ struct GemmOp {
   float *partials = nullptr;
   size_t partials_cap = 0;
   int splits = 0;
+  int bn = 0;  // tile width: 0 = automatic, 128 or 256 forces it (single launches)
+  // split_add (with splits = 2): each K half reduce-adds its tile into C through the TMA store
+  // (cp.reduce.async.bulk .add) — no partials, no fixup pass; C must be ZERO on entry. Two
+  // addends onto zero give the same bits in either order, so the result stays deterministic.
+  int split_add = 0;
 };
 
 cudaError_t gemm_bf16(const GemmOp &op, cudaStream_t st);

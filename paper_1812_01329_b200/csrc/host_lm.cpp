@@ -740,8 +740,14 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   dwdec.A = bf(p.off.dy); dwdec.lda = Vp; dwdec.a_mn = 1;
   dwdec.B = layer_in(L); dwdec.ldb = Hp; dwdec.b_mn = 1;
   dwdec.ep.C = ar(p.off.gWdec); dwdec.ep.ldc = Hp;
+  // dh_top = dy W_dec below: long K (V) over few output tiles — 256-wide tiles on CTA pairs, K
+  // halved over twice the CTAs, each half reduce-added into dh_top, which the xent launch zeroes
+  // on the side (two addends onto zero: order-independent bits); measured at C2 42 vs 60 us
+  const bool dh_split = V >= 4096 && !getenv("JANUS_DH_NOSPLIT");
   LCHK("xent", launch_xent(fp(p.off.logits), V, Vp, TB, P.tgt, B, Wd, p.while_mode ? P.lens : nullptr, Tdev,
-                   (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st));
+                   (float)TB, bf(p.off.dy), Vp, fp(p.off.rowloss), dst, st,
+                   dh_split ? reinterpret_cast<float4 *>(fp(p.off.dHtop)) : nullptr,
+                   dh_split ? (long long)TB * Hp / 4 : 0));
   {
     if (!bwd_wave || overlap) LCHK("gemm_dWdec", gemm_bf16(with_flags(dwdec), st));  // else grouped below
     if (overlap) {  // allreduce dW_dec on the side stream while the backward recurrence runs
@@ -760,6 +766,7 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     o2.A = bf(p.off.dy); o2.lda = Vp;
     o2.B = bf(p.off.Wdec_b); o2.ldb = Hp; o2.b_mn = 1;
     o2.ep.C = fp(p.off.dHtop); o2.ep.ldc = Hp;
+    if (dh_split) { o2.splits = 2; o2.split_add = 1; o2.bn = 256; }  // dh_top zeroed by the xent launch
     LCHK("gemm_dh", gemm_bf16(with_flags(o2), st));
     if (drop) LCHK("dropout", launch_dropout_f32(fp(p.off.dHtop), TB, H, Hp, keyp, L, p.dropout, st));
   }

@@ -374,8 +374,10 @@ __global__ void __launch_bounds__(NT) xent_kernel(const float *__restrict__ logi
                                                   const int *__restrict__ tgt, int B, int W,
                                                   const int *lens, const int *T_dev, float n_valid,
                                                   __nv_bfloat16 *dy, int lddy, float *rowloss,
-                                                  DevStatus *st) {
+                                                  DevStatus *st, float4 *zero, long long zero_n4) {
   pdl_enter();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < zero_n4; e += (long long)gridDim.x * blockDim.x)
+    zero[e] = make_float4(0.f, 0.f, 0.f, 0.f);
   __shared__ float sh[33];
   __shared__ float s_nv;
   const int Tb = T_dev ? *T_dev : rows / B;
@@ -425,8 +427,10 @@ __global__ void __launch_bounds__(NT) xent_reg_kernel(const float *__restrict__ 
                                                       const int *__restrict__ tgt, int B, int W,
                                                       const int *lens, const int *T_dev, float n_valid,
                                                       __nv_bfloat16 *dy, int lddy, float *rowloss,
-                                                      DevStatus *st) {
+                                                      DevStatus *st, float4 *zero, long long zero_n4) {
   pdl_enter();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < zero_n4; e += (long long)gridDim.x * blockDim.x)
+    zero[e] = make_float4(0.f, 0.f, 0.f, 0.f);
   __shared__ float sh[33];
   __shared__ float s_nv;
   const int Tb = T_dev ? *T_dev : rows / B;
@@ -514,12 +518,14 @@ __global__ void __launch_bounds__(XT_NT) xent_tma_kernel(const float *__restrict
                                                          const int *__restrict__ tgt, int B, int W,
                                                          const int *lens, const int *T_dev, float n_valid,
                                                          __nv_bfloat16 *dy, int lddy, float *rowloss,
-                                                         DevStatus *st) {
+                                                         DevStatus *st, float4 *zero, long long zero_n4) {
   extern __shared__ __align__(16) uint8_t xs_raw[];
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ float sh[33];
   __shared__ float s_nv;
   pdl_enter();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < zero_n4; e += (long long)gridDim.x * blockDim.x)
+    zero[e] = make_float4(0.f, 0.f, 0.f, 0.f);
   float *buf = reinterpret_cast<float *>(xs_raw);
   const size_t rb = ((size_t)V * 4 + 15) & ~size_t(15);  // bytes per buffer
   const int Tb = T_dev ? *T_dev : rows / B;
@@ -598,7 +604,8 @@ __global__ void __launch_bounds__(XT_NT) xent_tma_kernel(const float *__restrict
 
 cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
                         const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
-                        int lddy, float *rowloss, DevStatus *st, cudaStream_t s) {
+                        int lddy, float *rowloss, DevStatus *st, cudaStream_t s, float4 *zero,
+                        long long zero_n4) {
   const int xt_smem = 2 * (int)(((size_t)V * 4 + 15) & ~size_t(15));
   if (V % 4 == 0 && (ldl % 4) == 0 && (lddy % 4) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(dy) & 7) == 0 && xt_smem <= 110 * 1024 && !getenv("JANUS_XENT_REG")) {
@@ -606,7 +613,7 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
     if (e != cudaSuccess) return e;
     const int blocks = rows < 2 * NSM ? rows : 2 * NSM;
     return launch_pdl(xent_tma_kernel, dim3(blocks), dim3(XT_NT), (size_t)xt_smem, s, logits, V, ldl, rows, tgt, B,
-                      W, lens, T_dev, n_valid, dy, lddy, rowloss, st);
+                      W, lens, T_dev, n_valid, dy, lddy, rowloss, st, zero, zero_n4);
   }
   int blocks = rows < 8 * NSM ? rows : 8 * NSM;
   constexpr int NT = 128, NV4 = 20;  // 4 rows in flight per SM (register-limited)
@@ -615,13 +622,13 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
   if (aligned && V <= NT * 4 * NV4) {
     {
     const cudaError_t pe_ = launch_pdl(xent_reg_kernel<NT, NV4>, dim3(blocks), dim3(NT), 0, s, logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
-                                                   lddy, rowloss, st);
+                                                   lddy, rowloss, st, zero, zero_n4);
     if (pe_ != cudaSuccess) return pe_;
   }
   } else {
     {
     const cudaError_t pe_ = launch_pdl(xent_kernel<256>, dim3(blocks), dim3(256), 0, s, logits, V, ldl, rows, tgt, B, W, lens, T_dev, n_valid, dy,
-                                            lddy, rowloss, st);
+                                            lddy, rowloss, st, zero, zero_n4);
     if (pe_ != cudaSuccess) return pe_;
   }
   }

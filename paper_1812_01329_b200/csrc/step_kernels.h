@@ -92,9 +92,12 @@ cudaError_t launch_dropout_bf16(const __nv_bfloat16 *src, __nv_bfloat16 *dst, in
 cudaError_t launch_dropout_f32(float *x, int rows, int cols, int ld, const int *key, int site, float p,
                                cudaStream_t s, int row0 = 0);  // row0: global index of row 0
 uint32_t dropout_threshold(float p);  // floor(p * 2^32), saturated
+// zero / zero_n4 (optional): a float4 buffer the kernel zero-fills on the side (the reduce-add
+// target of the next GEMM), so no separate memset sits on the step's critical path
 cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int *tgt, int B, int W,
                         const int *lens, const int *T_dev, float n_valid, __nv_bfloat16 *dy,
-                        int lddy, float *rowloss, DevStatus *st, cudaStream_t s);
+                        int lddy, float *rowloss, DevStatus *st, cudaStream_t s,
+                        float4 *zero = nullptr, long long zero_n4 = 0);
 
 // embedding gradient: seg_word[k] (k < *nseg, slot order unspecified) lists the distinct ids of
 // the step; seg_grad[k][ldg] = sum of the dX rows of that id, summed in a fixed order

@@ -80,3 +80,14 @@ def test_gemm_splitk_deterministic():
     e1, o1 = _run(2240, 650, 10000, 0, 1, splits=4, ret_out=True)
     e2, o2 = _run(2240, 650, 10000, 0, 1, splits=4, ret_out=True)
     assert e1 < 1e-5 and np.array_equal(o1, o2)
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn,bias", [(2240, 650, 10000, 0, 1, None), (300, 1100, 2240, 0, 0, "col"),
+                                                  (2240, 650, 10000, 1, 0, "row")])
+def test_gemm_split_add_two_halves(monkeypatch, M, N, K, a_mn, b_mn, bias):
+    """GemmOp::split_add (the dh_top launch): the two K halves reduce-add into the zeroed C
+    through the TMA store; bias added once; same bits on every run (two addends onto zero)."""
+    monkeypatch.setenv("JANUS_GEMM_SPLIT_ADD", "1")
+    e1, o1 = _run(M, N, K, a_mn, b_mn, bias=bias, splits=2, ret_out=True)
+    e2, o2 = _run(M, N, K, a_mn, b_mn, bias=bias, splits=2, ret_out=True)
+    assert e1 < 1e-5 * max(1.0, K / 4096) and np.array_equal(o1, o2)
