@@ -37,6 +37,9 @@ struct GemmCfg {
   static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int THREADS = 192 + 32 * (NMMA - 1);  // warp 6: the second MMA warp
+  // two accumulators of NMMA x BN columns, allocated as a power of two >= 32 (BN = 192: 512)
+  static constexpr int TMEM_NEED = 2 * NMMA * BN;
+  static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
 };
 
 struct TileMap {
@@ -193,8 +196,8 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
     fence_barrier_init();
   }
   if (warp == 1) {
-    if (PAIR) tmem_alloc_pair(tmem_slot, 2 * NMMA * BN);
-    else tmem_alloc(tmem_slot, 2 * NMMA * BN);
+    if (PAIR) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    else tmem_alloc(tmem_slot, C::TMEM_COLS);
   }
   tc_fence_before();
   __syncthreads();
@@ -564,8 +567,8 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
   __syncthreads();
   if (CM > 1) cluster_sync_all();  // no CTA leaves while peers may still signal its barriers
   if (warp == 1) {
-    if (PAIR) tmem_dealloc_pair(tmem, 2 * NMMA * BN);
-    else tmem_dealloc(tmem, 2 * NMMA * BN);
+    if (PAIR) tmem_dealloc_pair(tmem, C::TMEM_COLS);
+    else tmem_dealloc(tmem, C::TMEM_COLS);
   }
 }
 
@@ -665,8 +668,10 @@ static bool op_wants_split(const GemmOp &op) {
 template <int BN, int CM, bool PAIR = false>
 static cudaError_t launch_cm(const GemmOp *ops, int n, cudaStream_t st) {
   // PAIR halves a CTA's B stage: six (BN = 256) / eight (BN = 128) stages fit instead of 4 / 6
-  constexpr int STAGES = PAIR ? (BN == 256 ? 6 : 8) : (BN == 256 ? 4 : 6);
-  constexpr int NMMA = PAIR ? 1 : (BN == 256 ? 1 : 2);
+  // (BN = 192, for launches whose tile count 256-wide tiles would round badly onto 148 SMs:
+  // 40 KB stages, four of them)
+  constexpr int STAGES = PAIR ? (BN == 256 ? 6 : 8) : (BN == 256 ? 4 : BN == 192 ? 4 : 6);
+  constexpr int NMMA = PAIR ? 1 : (BN == 128 ? 2 : 1);
   using C = GemmCfg<BN, STAGES, NMMA, PAIR>;
   auto kern = gemm_bf16_tc_kernel<BN, STAGES, NMMA, CM, PAIR>;
   static bool attr = false;
@@ -780,12 +785,15 @@ static bool want_pair(const GemmOp *ops, int n) {
 
 template <int BN>
 static cudaError_t launch(const GemmOp *ops, int n, cudaStream_t st) {
+  static_assert(BN == 128 || BN == 192 || BN == 256, "tile width");
   bool split = false;
   for (int g = 0; g < n; ++g) split = split || (op_wants_split(ops[g]) && n == 1);
   // an explicit split of a long-K single launch keeps the CTA pair (same split on both CTAs)
   const bool pair_split = split && n == 1 && ops[0].splits > 1 && want_pair(ops, n);
-  if (g_gemm_cm == 2 && pair_split) return launch_cm<BN, 2, true>(ops, n, st);
-  if (g_gemm_cm == 2 && !split && want_pair(ops, n)) return launch_cm<BN, 2, true>(ops, n, st);
+  if constexpr (BN != 192) {  // CTA pairs split B's N rows in 64-row halves: BN = 128 / 256
+    if (g_gemm_cm == 2 && pair_split) return launch_cm<BN, 2, true>(ops, n, st);
+    if (g_gemm_cm == 2 && !split && want_pair(ops, n)) return launch_cm<BN, 2, true>(ops, n, st);
+  }
   if (g_gemm_cm == 2 && !split) return launch_cm<BN, 2>(ops, n, st);
   return launch_cm<BN, 1>(ops, n, st);
 }
@@ -835,8 +843,21 @@ cudaError_t gemm_bf16_group(const GemmOp *ops, int n, cudaStream_t st) {
   if (m > GB_MAX) return cudaErrorInvalidValue;
   // one launch for the whole group (the operand majors are per-GEMM runtime properties)
   static const int bn_env = getenv("JANUS_GEMM_BN") ? atoi(getenv("JANUS_GEMM_BN")) : 0;  // dev knob
-  const int bn = m == 1 ? (bn_env ? bn_env : live[0].bn) : 0;
+  int bn = m == 1 ? (bn_env ? bn_env : live[0].bn) : 0;
+  if (m == 1 && bn == 0 && wide_of(live[0])) {
+    // a single launch takes the tile width with the least work per SM: rounds of tiles over the
+    // SMs x tile width (ties to the wider tile). The 2240 x 2600 input projection: 256-wide
+    // tiles are 198 = 1.34 rounds, 192-wide 252 = 1.7 rounds
+    const int mb = (live[0].M + 127) / 128;
+    long best = -1;
+    for (int w : {256, 192, 128}) {
+      const long tiles = (long)mb * ((live[0].N + w - 1) / w);
+      const long cost = (tiles + 147) / 148 * w;
+      if (best < 0 || cost < best) { best = cost; bn = w; }
+    }
+  }
   if (bn == 256) return launch<256>(live, m, st);
+  if (bn == 192) return launch<192>(live, m, st);
   if (bn == 128) return launch<128>(live, m, st);
   if (use_bn256(live, m)) return launch<256>(live, m, st);
   return launch<128>(live, m, st);
