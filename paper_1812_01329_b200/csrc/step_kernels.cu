@@ -577,27 +577,34 @@ __global__ void __launch_bounds__(XT_NT) xent_tma_kernel(const float *__restrict
       const float4 v = y4[q];
       m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
     }
+    // the target logit (for the loss) before the buffer is overwritten with the exponentials: read
+    // ahead of the reduction's barrier
+    const float ytg = threadIdx.x == 0 ? reinterpret_cast<const float *>(y4)[tg] : 0.f;
     m = block_reduce<XT_NT>(m, sh, true);
     float sum = 0.f;
-    for (int q = threadIdx.x; q < V4; q += XT_NT) {
+    float4 *e4 = const_cast<float4 *>(y4);
+    for (int q = threadIdx.x; q < V4; q += XT_NT) {  // exp once: kept in place for the dy pass
       const float4 v = y4[q];
-      sum += (__expf(v.x - m) + __expf(v.y - m)) + (__expf(v.z - m) + __expf(v.w - m));
+      const float4 e = make_float4(__expf(v.x - m), __expf(v.y - m), __expf(v.z - m), __expf(v.w - m));
+      e4[q] = e;
+      sum += (e.x + e.y) + (e.z + e.w);
     }
     sum = block_reduce<XT_NT>(sum, sh, false);
     const float lse = m + logf(sum);
     const float sc = inv / sum;
     for (int q = threadIdx.x; q < V4; q += XT_NT) {
-      const float4 v = y4[q];
+      const float4 v = e4[q];  // this thread's own exponentials
       const int c = 4 * q;
-      const float p0 = __expf(v.x - m) * sc - (c == tg ? inv : 0.f);
-      const float p1 = __expf(v.y - m) * sc - (c + 1 == tg ? inv : 0.f);
-      const float p2 = __expf(v.z - m) * sc - (c + 2 == tg ? inv : 0.f);
-      const float p3 = __expf(v.w - m) * sc - (c + 3 == tg ? inv : 0.f);
+      const float p0 = v.x * sc - (c == tg ? inv : 0.f);
+      const float p1 = v.y * sc - (c + 1 == tg ? inv : 0.f);
+      const float p2 = v.z * sc - (c + 2 == tg ? inv : 0.f);
+      const float p3 = v.w * sc - (c + 3 == tg ? inv : 0.f);
       __nv_bfloat162 lo = __floats2bfloat162_rn(p0, p1);
       __nv_bfloat162 hi = __floats2bfloat162_rn(p2, p3);
       d2[q] = make_uint2(*reinterpret_cast<unsigned *>(&lo), *reinterpret_cast<unsigned *>(&hi));
     }
-    if (threadIdx.x == 0) rowloss[r] = (lse - reinterpret_cast<const float *>(y4)[tg]) * inv;
+    if (threadIdx.x == 0) rowloss[r] = (lse - ytg) * inv;
+    fence_proxy_async_shared();  // this thread's generic writes of buffer k precede the refill
     __syncthreads();  // every read of buffer k is done before it is refilled (iteration i + 2)
   }
 }
