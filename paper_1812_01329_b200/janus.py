@@ -273,7 +273,7 @@ class Graph:
         self.workspace_bytes = n.value
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # (module globals are gone at interpreter exit)
             lib.janus_graph_destroy(self.h)
             self.h = None
 
@@ -362,7 +362,7 @@ class Session:
         self.workspace = None
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:
             lib.janus_session_destroy(self.h)
             self.h = None
 

@@ -22,6 +22,12 @@ elif wl == "c1":
 elif wl == "c2small":
     prog = pg.lstm_lm_program(V=300, E=72, H=100, L=2, B=33, T=9, lr=0.5)
     batches = list(gen.lm_batches(gen.SEED_C2, 33, 9, 300, steps))
+elif wl == "c2v":  # V >= 4096: the split-K reduce-add dh_top launch, small otherwise
+    prog = pg.lstm_lm_program(V=5000, E=64, H=64, L=2, B=16, T=5, lr=0.5)
+    batches = list(gen.lm_batches(gen.SEED_C2, 16, 5, 5000, steps))
+elif wl == "c3rnn":
+    prog = pg.treernn_program(V=50, H=32, C=2, B=6, lr=0.2)
+    batches = [gen.sst_forest(gen.SEED_C3, k, 6, 50, max_leaves=12) for k in range(steps)]
 elif wl == "c3":
     prog = pg.treelstm_program(V=20000, E=300, H=300, C=2, B=25, lr=0.05)
     batches = [gen.sst_forest(gen.SEED_C3, k, 25, 20000) for k in range(steps)]
