@@ -26,9 +26,14 @@
 
 namespace jk {
 
+// bf16 operand copies of the tcgen05 GEMM path (imp_kernels.h set_scratch)
+static size_t imp_gemm_scratch_bytes(const Graph &g) {
+  const size_t plan = g.kind == "lstm_lm" ? g.lm.ws_bytes : g.kind == "treelstm" ? g.tree.ws_bytes : 0;
+  return std::min<size_t>(plan, 256u << 20);
+}
 size_t imperative_ws_bytes(const Graph &g) {
   const size_t plan = g.kind == "lstm_lm" ? g.lm.ws_bytes : g.kind == "treelstm" ? g.tree.ws_bytes : 0;
-  return 3 * plan + (64u << 20);
+  return 3 * plan + (64u << 20) + imp_gemm_scratch_bytes(g);
 }
 
 namespace {
@@ -93,7 +98,7 @@ struct Interp {
     return base + o;
   }
   void ck(cudaError_t e) {
-    ++launches;
+    launches += 1 + imp::take_extra_launches();
     if (e != cudaSuccess) throw Err{JANUS_ERR_CUDA, cudaGetErrorString(e)};
   }
   int new_val(IVal v) {
@@ -847,6 +852,9 @@ janus_status run_imperative(Graph &g, const janus_tensor *args, int n_args,
   I.bf16 = g.opts.gemm_dtype != JANUS_F32;
   I.base = static_cast<uint8_t *>(ws.data);
   I.cap = cap;
+  const size_t scr = imp_gemm_scratch_bytes(g);
+  imp::set_scratch(scr ? I.alloc(scr) : nullptr, scr);
+  (void)imp::take_extra_launches();
   janus_status result = JANUS_OK;
   // Data parallel: every rank runs its own shard imperatively, then ONE allreduce(sum) of
   // a gradient arena = [grad of every SGD-updated slot, ascending slot | runtime-error count]. The

@@ -3,6 +3,7 @@
 // load at the same points as the graph path (reading R).
 #include "common.cuh"
 #include "imp_kernels.h"
+#include "gemm_tc.h"
 
 namespace jk {
 namespace imp {
@@ -12,6 +13,52 @@ JN_DEV float rnd(float x, bool r) { return r ? bf16_round(x) : x; }
 static int blocks_for(int64_t n, int per = 256) {
   int64_t b = (n + per - 1) / per;
   return (int)(b < 8 * NSM ? (b > 0 ? b : 1) : 8 * NSM);
+}
+
+// ------------------------------------------------------------------------------ tcgen05 path
+static thread_local uint8_t *g_scr = nullptr;
+static thread_local size_t g_scr_bytes = 0;
+static thread_local uint64_t g_extra = 0;
+void set_scratch(void *p, size_t bytes) {
+  g_scr = static_cast<uint8_t *>(p);
+  g_scr_bytes = p ? bytes : 0;
+}
+uint64_t take_extra_launches() {
+  const uint64_t e = g_extra;
+  g_extra = 0;
+  return e;
+}
+static int r8i(int x) { return (x + 7) & ~7; }
+// dst[r][0..ldd) = rb(src[r][0..cols)), zero beyond cols
+__global__ void cast_pad_k(__nv_bfloat16 *dst, int ldd, const float *src, int lds, int rows, int cols) {
+  const int64_t n = (int64_t)rows * ldd;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / ldd), c = (int)(e - (int64_t)r * ldd);
+    dst[e] = __float2bfloat16_rn(c < cols ? src[(size_t)r * lds + c] : 0.f);
+  }
+}
+// C[M][N] (+)= A . B^T with A stored [a_rows][a_cols] (pitch lda, a_mn: [K][M]) and B likewise;
+// false when this call stays on the SIMT kernel (f32 mode, too little work, scratch too small)
+static bool tc_gemm(float *C, int ldc, bool acc, const float *A, int a_rows, int a_cols, int lda, bool a_mn,
+                    const float *B, int b_rows, int b_cols, int ldb, bool b_mn, int M, int N, int K,
+                    bool rx, bool rw, cudaStream_t s, cudaError_t *err) {
+  if (!rx || !rw || (long long)M * N * K < (1ll << 21) || M <= 0 || N <= 0 || K <= 0) return false;
+  const size_t abytes = (((size_t)a_rows * r8i(a_cols) * 2) + 255) & ~size_t(255);
+  const size_t bbytes = (size_t)b_rows * r8i(b_cols) * 2;
+  if (!g_scr || abytes + bbytes > g_scr_bytes) return false;
+  __nv_bfloat16 *Ab = reinterpret_cast<__nv_bfloat16 *>(g_scr), *Bb = reinterpret_cast<__nv_bfloat16 *>(g_scr + abytes);
+  cast_pad_k<<<blocks_for((int64_t)a_rows * r8i(a_cols)), 256, 0, s>>>(Ab, r8i(a_cols), A, lda, a_rows, a_cols);
+  cast_pad_k<<<blocks_for((int64_t)b_rows * r8i(b_cols)), 256, 0, s>>>(Bb, r8i(b_cols), B, ldb, b_rows, b_cols);
+  g_extra += 2;
+  GemmOp op;
+  op.M = M; op.N = N; op.K = K;
+  op.A = Ab; op.lda = r8i(a_cols); op.a_mn = a_mn;
+  op.B = Bb; op.ldb = r8i(b_cols); op.b_mn = b_mn;
+  op.ep.C = C; op.ep.ldc = ldc; op.ep.accumulate = acc;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = gemm_bf16(op, s);
+  *err = e;
+  return true;
 }
 
 // ------------------------------------------------------------------------------ GEMMs (16x16 tiles)
@@ -35,6 +82,8 @@ __global__ void gemm_nt_k(float *Y, const float *X, const float *W, int n, int N
 }
 cudaError_t gemm_nt(float *Y, const float *X, const float *W, int n, int N, int K, int ldx, int ldw,
                     int ldy, bool acc, bool rx, bool rw, cudaStream_t s) {
+  cudaError_t te;
+  if (tc_gemm(Y, ldy, acc, X, n, K, ldx, false, W, N, K, ldw, false, n, N, K, rx, rw, s, &te)) return te;
   dim3 g((N + TS - 1) / TS, (n + TS - 1) / TS);
   gemm_nt_k<<<g, dim3(TS, TS), 0, s>>>(Y, X, W, n, N, K, ldx, ldw, ldy, acc, rx, rw);
   return cudaGetLastError();
@@ -58,6 +107,9 @@ __global__ void gemm_nn_k(float *Y, const float *D, const float *W, int n, int N
 }
 cudaError_t gemm_nn(float *Y, const float *D, const float *W, int n, int N, int K, int ldd, int ldw,
                     int ldy, bool acc, bool rd, bool rw, cudaStream_t s) {
+  // Y[n][K] = D[n][N] . W[N][K]: reduction over N; W is the MN-major ([K_red][N_out]) operand
+  cudaError_t te;
+  if (tc_gemm(Y, ldy, acc, D, n, N, ldd, false, W, N, K, ldw, true, n, K, N, rd, rw, s, &te)) return te;
   dim3 g((K + TS - 1) / TS, (n + TS - 1) / TS);
   gemm_nn_k<<<g, dim3(TS, TS), 0, s>>>(Y, D, W, n, N, K, ldd, ldw, ldy, acc, rd, rw);
   return cudaGetLastError();
@@ -83,6 +135,9 @@ __global__ void gemm_tn_k(float *G, const float *D, const float *X, int n, int N
 }
 cudaError_t gemm_tn(float *G, const float *D, const float *X, int n, int N, int K, int ldd, int ldx,
                     int ldg, bool acc, bool rd, bool rx, cudaStream_t s) {
+  // G[N][K] = D[n][N]^T . X[n][K]: reduction over n; both operands MN-major
+  cudaError_t te;
+  if (tc_gemm(G, ldg, acc, D, n, N, ldd, true, X, n, K, ldx, true, N, K, n, rd, rx, s, &te)) return te;
   dim3 g((K + TS - 1) / TS, (N + TS - 1) / TS);
   gemm_tn_k<<<g, dim3(TS, TS), 0, s>>>(G, D, X, n, N, K, ldd, ldx, ldg, acc, rd, rx);
   return cudaGetLastError();
@@ -498,8 +553,83 @@ __global__ void xent_k(float *loss, float *dy, const float *logits, const int *t
     *loss = a;
   }
 }
+// Row-parallel form (one block per row; the single-block kernel above took 39 ms of a 67 ms
+// imperative C2 step): valid-row count, per-row loss and dy, then the loss summed in row order
+// (deterministic). Same arithmetic per element as xent_k.
+__global__ void count_valid_k(float *n_valid, const int *mask, int n) {
+  __shared__ int part[256];
+  int k = 0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) k += mask[r] != 0;
+  part[threadIdx.x] = k;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) a += part[i];
+    *n_valid = (float)(a > 0 ? a : 1);
+  }
+}
+__device__ float block_sum_max(float v, float *sh, bool is_max) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const float x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, x) : v + x;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = sh[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) a = is_max ? fmaxf(a, sh[i]) : a + sh[i];
+    sh[32] = a;
+  }
+  __syncthreads();
+  const float r = sh[32];
+  __syncthreads();
+  return r;
+}
+__global__ void xent_rows_k(float *rowloss, float *dy, const float *logits, const int *tgt, const int *mask,
+                            const float *n_valid, int C, int *err) {
+  __shared__ float sh[33];
+  const int r = blockIdx.x;
+  const float *y = logits + (size_t)r * C;
+  float *d = dy + (size_t)r * C;
+  if (mask[r] == 0) {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) d[c] = 0.f;
+    if (threadIdx.x == 0) rowloss[r] = 0.f;
+    return;
+  }
+  int t = tgt[r];
+  if (t < 0 || t >= C) {
+    if (threadIdx.x == 0) atomicOr(err, 2);
+    t = 0;
+  }
+  const float sn = *n_valid;
+  float m = -INFINITY;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) m = fmaxf(m, y[c]);
+  m = block_sum_max(m, sh, true);
+  float sm = 0.f;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) sm += expf(y[c] - m);
+  sm = block_sum_max(sm, sh, false);
+  const float lse = m + logf(sm);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) d[c] = (expf(y[c] - lse) - (c == t ? 1.f : 0.f)) / sn;
+  if (threadIdx.x == 0) rowloss[r] = (lse - y[t]) / sn;
+}
+__global__ void sum_rows_k(float *loss, const float *rowloss, int n) {  // in row order
+  if (threadIdx.x == 0) {
+    float a = 0.f;
+    for (int r = 0; r < n; ++r) a += rowloss[r];
+    *loss = a;
+  }
+}
 cudaError_t xent(float *loss, float *dy, const float *logits, const int *tgt, const int *mask, int n,
                  int C, int *err, cudaStream_t s) {
+  if (g_scr && g_scr_bytes >= (size_t)(n + 1) * 4 && n > 0) {
+    float *nv = reinterpret_cast<float *>(g_scr), *rowloss = nv + 1;
+    count_valid_k<<<1, 256, 0, s>>>(nv, mask, n);
+    xent_rows_k<<<n, 256, 0, s>>>(rowloss, dy, logits, tgt, mask, nv, C, err);
+    sum_rows_k<<<1, 32, 0, s>>>(loss, rowloss, n);
+    g_extra += 2;
+    return cudaGetLastError();
+  }
   xent_k<<<1, 1024, 0, s>>>(loss, dy, logits, tgt, mask, n, C, err);
   return cudaGetLastError();
 }

@@ -7,6 +7,13 @@
 namespace jk {
 namespace imp {
 
+// GEMMs: with both operands rounded to bf16 (the graph's R1/R2/R3 rounding points) and enough
+// work, the operands are cast into the scratch set here and the product runs on the tcgen05 GEMM
+// (gemm_tc.cu, fp32 accumulate); otherwise a SIMT kernel rounds on load. set_scratch: device bytes
+// for the two bf16 operand copies (stream-ordered reuse, one GEMM at a time); take_extra_launches:
+// launches issued beyond one per call since the last query (the casts).
+void set_scratch(void *p, size_t bytes);
+uint64_t take_extra_launches();
 // Y[n][N] (+)= X[n][K] . W[N][K]^T          (rx / rw: round the operand to bf16 on load)
 cudaError_t gemm_nt(float *Y, const float *X, const float *W, int n, int N, int K, int ldx, int ldw,
                     int ldy, bool acc, bool rx, bool rw, cudaStream_t s);
