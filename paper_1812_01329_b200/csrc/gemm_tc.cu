@@ -779,7 +779,7 @@ static int g_gemm_pair = getenv("JANUS_GEMM_PAIR") ? atoi(getenv("JANUS_GEMM_PAI
 static bool want_pair(const GemmOp *ops, int n) {
   if (g_gemm_pair >= 0) return g_gemm_pair == 1;
   for (int g = 0; g < n; ++g)
-    if (ops[g].K < 1024) return false;
+    if (ops[g].K < 1024 || ops[g].M <= 128) return false;  // (one 128-row block: a pair would idle half)
   return true;
 }
 
