@@ -171,10 +171,15 @@ typedef struct {
  *                   node, at most `value` nodes per tree — the structure the level-batched
  *                   lowering of the recursive InvokeOp (P:224, P:316 fn6) relies on (RUNTIME)
  *   JA_VALUE_EQ     int32 args[target][0] == value (constant promotion)        (RUNTIME)
+ *   JA_BRANCH_ARM   the Switch whose predicate is int32 args[target][0] (taken when != 0, as the
+ *                   SWITCH op reads it) takes arm `value` (1: true arm, 0: false arm): the
+ *                   untaken arm is dropped and the branch asserted ("speculates the
+ *                   branch ... single arm"); unlike VALUE_EQ any non-zero predicate satisfies the
+ *                   true arm; observed = the predicate value                            (RUNTIME)
  * ------------------------------------------------------------------------------------------- */
 typedef enum {
   JA_DTYPE_EQ = 0, JA_SHAPE_MATCH = 1, JA_TRIP_COUNT = 2, JA_TYPE_TAG = 3, JA_RANGE = 4,
-  JA_TREE_BINARY = 5, JA_VALUE_EQ = 6
+  JA_TREE_BINARY = 5, JA_VALUE_EQ = 6, JA_BRANCH_ARM = 7
 } janus_assumption_kind;
 
 enum { JANUS_MODE_DISPATCH = 0, JANUS_MODE_RUNTIME = 1 };
@@ -374,7 +379,7 @@ void janus_session_destroy(janus_session *s); /* NULL-safe */
  *                  a rank mismatch drops the assumption (kind level)
  *   TRIP_COUNT  -> RANGE [1, value] on the same argument: the loop is regenerated as a bounded
  *                  device While (P:222 Enter/Exit/NextIteration) instead of unrolled
- *   TYPE_TAG, VALUE_EQ, RANGE, TREE_BINARY -> dropped (the construct is evaluated on the
+ *   TYPE_TAG, VALUE_EQ, BRANCH_ARM, RANGE, TREE_BINARY -> dropped (the construct is evaluated on the
  *                  device or the graph loses its device program)
  * *out receives the relaxed assumption (same id) unless *dropped = 1. Pure host function. */
 janus_status janus_relax(const janus_assumption *a, const janus_tensor *observed,

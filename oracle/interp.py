@@ -167,6 +167,11 @@ def check_runtime(prog, args, state):
         elif a.kind == "VALUE_EQ":
             x = np.asarray(args[a.target])
             r = _first_fail(x.reshape(-1)[:1] != a.value, x)
+        elif a.kind == "BRANCH_ARM":
+            # the Switch on args[target][0] (predicate = value != 0, as the SWITCH op reads it)
+            # takes arm `value` (P:226-228 single-arm speculation)
+            x = np.asarray(args[a.target])
+            r = _first_fail((x.reshape(-1)[:1] != 0) != (a.value != 0), x)
         elif a.kind == "RANGE":
             x = np.asarray(args[a.target], np.int64)
             hi = a.hi
@@ -561,14 +566,30 @@ class GraphExec:
 
 
 # =============================================================================== commit
+def clip_scale(prog, effects, grads, n_ranks):
+    """Global gradient-norm clipping (reading R15: Zaremba et al. [51], the LM P:312 follows,
+    clip the gradient's global L2 norm; janus_build_opts.clip_norm = c, 0 = off): with G the
+    rank-averaged gradient of every parameter the step updates, the update uses
+    g * min(1, c / ||G||_2) — i.e. c / ||G|| when ||G|| > c, else the gradient unchanged."""
+    c = float(prog.meta.get("clip_norm", 0.0) or 0.0)
+    slots = sorted({e[2] for e in effects if e[1] == "sgd"})
+    if c <= 0 or not slots:
+        return 1.0
+    sq = sum(float(np.sum((np.asarray(grads[k], np.float64) / n_ranks) ** 2)) for k in slots)
+    norm = np.sqrt(sq)
+    return c / norm if norm > c else 1.0
+
+
 def _commit(prog, state, effects, grads, n_ranks):
     """Apply the effect log in sequence order (P:266 (4)): SGD on the fp32 master with the
-    rank-averaged gradient (reading Q13), then state write-backs."""
+    rank-averaged gradient (reading Q13), scaled by the global-norm clip (R15), then state
+    write-backs."""
     new = [np.array(s, copy=True) for s in state]
+    scale = clip_scale(prog, effects, grads, n_ranks)
     for seq, kind, slot, v, lr in sorted(effects, key=lambda e: e[0]):
         if kind == "sgd":
             g = grads[slot] / n_ranks
-            new[slot] = (new[slot].astype(np.float64) - lr * g).astype(new[slot].dtype)
+            new[slot] = (new[slot].astype(np.float64) - (lr * scale) * g).astype(new[slot].dtype)
         else:
             new[slot] = np.asarray(v.data).astype(new[slot].dtype).reshape(new[slot].shape)
     return new

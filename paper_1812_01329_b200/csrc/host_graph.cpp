@@ -155,7 +155,7 @@ janus_status validate_graph(Graph &g, std::string &err) {
       err = buf;
       return JANUS_ERR_INVALID;
     }
-    if (a.kind < JA_DTYPE_EQ || a.kind > JA_VALUE_EQ || (a.mode != 0 && a.mode != 1)) {
+    if (a.kind < JA_DTYPE_EQ || a.kind > JA_BRANCH_ARM || (a.mode != 0 && a.mode != 1)) {
       snprintf(buf, sizeof buf, "assumption %u: bad kind/mode", a.id);
       err = buf;
       return JANUS_ERR_INVALID;

@@ -212,12 +212,13 @@ bool lower_lm(Graph &g, std::string &why) {
     if (a.kind == JA_TYPE_TAG && a.target == p.slot_tag && a.value == 1) p.tag_specialised = true;
     // the training Switch with its value speculated (constant promotion): only the taken
     // arm is kept and the VALUE_EQ AssertOp checks it
-    if (a.kind == JA_VALUE_EQ && a.mode == JANUS_MODE_RUNTIME && p.train_arg >= 0 && a.target == p.train_arg &&
-        a.value != 0)
+    if ((a.kind == JA_VALUE_EQ || a.kind == JA_BRANCH_ARM) && a.mode == JANUS_MODE_RUNTIME && p.train_arg >= 0 &&
+        a.target == p.train_arg && a.value != 0)
       p.train_specialised = true;
   }
   for (const auto &a : g.asms)
-    if (a.mode == JANUS_MODE_RUNTIME && (a.kind == JA_VALUE_EQ || a.kind == JA_RANGE || a.kind == JA_TRIP_COUNT) &&
+    if (a.mode == JANUS_MODE_RUNTIME &&
+        (a.kind == JA_VALUE_EQ || a.kind == JA_BRANCH_ARM || a.kind == JA_RANGE || a.kind == JA_TRIP_COUNT) &&
         (a.target < 0 || a.target > (p.train_arg >= 0 ? 3 : 2))) {
       why = "runtime assumption on an unknown argument";
       return false;
@@ -235,6 +236,7 @@ bool lower_lm(Graph &g, std::string &why) {
     if (a.kind == JA_TRIP_COUNT) r.kind = G_ALL_EQ;
     else if (a.kind == JA_RANGE) r.kind = G_RANGE;
     else if (a.kind == JA_VALUE_EQ) r.kind = G_FIRST_EQ;
+    else if (a.kind == JA_BRANCH_ARM) r.kind = G_FIRST_TRUTH;
     else if (a.kind == JA_TYPE_TAG) { r.kind = G_FIRST_EQ; r.slot = a.target; r.arg = -1; }
     else { why = "unsupported runtime assumption for this graph"; return false; }
     if (g.opts.strip_asserts) continue;

@@ -44,8 +44,8 @@ std::string key_of(const janus_failure &f, const janus_tensor &t) {
 
 const char *kind_name(int k) {
   static const char *n[] = {"DTYPE_EQ", "SHAPE_MATCH", "TRIP_COUNT", "TYPE_TAG",
-                            "RANGE",    "TREE_BINARY", "VALUE_EQ"};
-  return k >= 0 && k <= 6 ? n[k] : "?";
+                            "RANGE",    "TREE_BINARY", "VALUE_EQ",   "BRANCH_ARM"};
+  return k >= 0 && k <= 7 ? n[k] : "?";
 }
 
 std::string asm_text(const janus_assumption &a) {
@@ -224,7 +224,7 @@ janus_status janus_relax(const janus_assumption *a, const janus_tensor *observed
       out->ref_arg = -1;
       out->ref_dim = -1;
       return JANUS_OK;
-    case JA_TYPE_TAG: case JA_VALUE_EQ: case JA_RANGE: case JA_TREE_BINARY:
+    case JA_TYPE_TAG: case JA_VALUE_EQ: case JA_BRANCH_ARM: case JA_RANGE: case JA_TREE_BINARY:
       *dropped = 1;
       return JANUS_OK;
   }

@@ -46,11 +46,12 @@ __global__ void guards_kernel(GuardList gl, DevStatus *st) {
     if (threadIdx.x == 0) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | mask);
     return;
   }
-  const long long n = g.kind == G_FIRST_EQ ? 1 : g.n;
+  const long long n = (g.kind == G_FIRST_EQ || g.kind == G_FIRST_TRUTH) ? 1 : g.n;
   for (long long i = threadIdx.x; i < n; i += blockDim.x) {
     const long long v = g.data[i];
     bool bad = false;
     if (g.kind == G_ALL_EQ || g.kind == G_FIRST_EQ) bad = v != g.value;
+    else if (g.kind == G_FIRST_TRUTH) bad = (v != 0) != (g.value != 0);
     else if (g.kind == G_RANGE) bad = v < g.lo || v > g.hi;
     if (bad) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | (unsigned long long)i);
   }

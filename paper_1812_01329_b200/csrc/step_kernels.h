@@ -26,7 +26,8 @@ constexpr int IDX_BITS = 40;
 
 // A RUNTIME assumption evaluated on the device (AssertOp).
 enum GuardKind { G_ALL_EQ = 0, G_FIRST_EQ = 1, G_RANGE = 2, G_FORCED = 3,
-                 G_TREE = 4 /* evaluated by the forest guard; listed for the observed lookup */ };
+                 G_TREE = 4 /* evaluated by the forest guard; listed for the observed lookup */,
+                 G_FIRST_TRUTH = 5 /* (data[0] != 0) == (value != 0): a branch arm */ };
 struct GuardDesc {
   int kind;
   unsigned int id;

@@ -95,6 +95,30 @@ def test_training_switch_speculated_value_eq():
     assert_state_parity(prog, state, got, imp.state, 2e-2, what="eval fallback")
 
 
+def test_training_switch_speculated_branch_arm():
+    """The same Switch speculated by BRANCH_ARM (the control-flow assumption): every
+    non-zero flag takes the true arm (training = 1 and 5 both commit the update, parity with the
+    oracle); training = 0 fails bit-exactly as {8, 0, 0} with nothing committed."""
+    B, T, V = 8, 6, 64
+    prog = pg.lstm_lm_program(V=V, E=40, H=48, L=2, B=B, T=T, lr=0.5, training_flag=True,
+                              flag_speculation="branch")
+    janus = J()
+    g = janus.Graph(prog)
+    assert g.device_path and "train=specialised" in g.describe(), g.build_message
+    tok, tgt, ln = list(gen.lm_batches(gen.SEED_C2, B, T, V, 1))[0]
+    _run_parity(prog, "bf16", 2e-2, [(tok, tgt, ln, np.array([1], np.int32)),
+                                     (tok, tgt, ln, np.array([5], np.int32))])
+    ws = g.new_workspace()
+    state = gen.uniform_params(prog, 5, 0.1)
+    args = [tok, tgt, ln, np.array([0], np.int32)]
+    ora = I.run_graph_step(prog, args, state, mode="bf16")
+    dev = to_dev(state)
+    st, fail, _ = _step(g, ws, args, dev)
+    assert st == ora.status == I.ASSUMPTION_FAILED
+    assert _fail_tuple(fail) == _ora_tuple(ora) == (8, 0, 0)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(to_host(dev), state))
+
+
 def test_training_switch_on_the_device():
     """Without the VALUE_EQ assumption (what janus_relax leaves after it breaks) the Switch is
     evaluated on the device: the commit kernel reads training[0]; both arms match the oracle."""

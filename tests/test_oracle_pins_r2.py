@@ -404,3 +404,31 @@ def test_training_switch_eval_step_and_value_eq_guard():
         assert (r.failure.assumption_id, r.failure.index, r.failure.observed) == (8, 0, flag)
         assert all(x.tobytes() == y.tobytes() for x, y in zip(r.state, st))
     assert I.run_graph_step(spec, tr, st, mode="f32").status == I.OK
+
+
+def test_branch_arm_speculation():
+    """BRANCH_ARM (the branch is speculated, the untaken arm dropped, the branch
+    asserted): the true-arm assumption holds for every non-zero predicate — a speculated graph step
+    with training = 1 or 7 equals the plain program's training step bit for bit — and fails only
+    on 0, reporting {8, index 0, observed 0}; the false-arm form holds only for 0."""
+    B, T, V, E, H, L = 2, 3, 7, 3, 4, 2
+    spec = pg.lstm_lm_program(V=V, E=E, H=H, L=L, B=B, T=T, lr=0.5, training_flag=True, flag_speculation="branch")
+    assert [(a.id, a.kind, a.target, a.value) for a in spec.assumptions if a.kind == "BRANCH_ARM"] == \
+        [(8, "BRANCH_ARM", 3, 1)]
+    plain = pg.lstm_lm_program(V=V, E=E, H=H, L=L, B=B, T=T, lr=0.5, speculate="none")
+    st, _ = _lm_state(plain, 61, 0.5, B, H, L)
+    st = [np.asarray(x, np.float32) if np.asarray(x).dtype.kind == "f" else x for x in st]
+    a3 = _ragged(B, T, V, [T] * B, seed=4)
+    ref = I.run_graph_step(plain, a3, st, mode="f32")
+    for flag in (1, 7):
+        r = I.run_graph_step(spec, a3 + [np.array([flag], np.int32)], st, mode="f32")
+        assert r.status == I.OK
+        assert all(x.tobytes() == y.tobytes() for x, y in zip(r.state, ref.state))
+    r = I.run_graph_step(spec, a3 + [np.array([0], np.int32)], st, mode="f32")
+    assert r.status == I.ASSUMPTION_FAILED
+    assert (r.failure.assumption_id, r.failure.index, r.failure.observed) == (8, 0, 0)
+    assert all(x.tobytes() == y.tobytes() for x, y in zip(r.state, st))
+    false_arm = pg.Program("t", [], [pg.Assumption(4, "BRANCH_ARM", 1, 0, value=0)], [], [], 0, 0.0)
+    assert I.check_runtime(false_arm, [np.array([0], np.int32)], []) is None
+    f = I.check_runtime(false_arm, [np.array([5], np.int32)], [])
+    assert (f.assumption_id, f.index, f.observed) == (4, 0, 5)

@@ -42,6 +42,7 @@ def test_relax_control_flow_and_types():
     assert r.dtype == I64 and r.kind == pg.ASM_CODE["DTYPE_EQ"]
     # single-arm branch / constant / tree-structure / range assumptions are dropped
     for a in (Assumption(3, "TYPE_TAG", RUNTIME, 9, value=1), Assumption(6, "VALUE_EQ", RUNTIME, 3, value=1),
+              Assumption(7, "BRANCH_ARM", RUNTIME, 3, value=1),
               Assumption(8, "TREE_BINARY", RUNTIME, 0, hi=10, value=127),
               Assumption(2, "RANGE", RUNTIME, 2, lo=1, hi=35)):
         assert janus.relax(a) is None

@@ -30,7 +30,8 @@ OP_KINDS = [
 ]
 OP_CODE = {k: i for i, k in enumerate(OP_KINDS)}
 
-ASM_KINDS = ["DTYPE_EQ", "SHAPE_MATCH", "TRIP_COUNT", "TYPE_TAG", "RANGE", "TREE_BINARY", "VALUE_EQ"]
+ASM_KINDS = ["DTYPE_EQ", "SHAPE_MATCH", "TRIP_COUNT", "TYPE_TAG", "RANGE", "TREE_BINARY", "VALUE_EQ",
+             "BRANCH_ARM"]
 ASM_CODE = {k: i for i, k in enumerate(ASM_KINDS)}
 DISPATCH, RUNTIME = 0, 1
 
@@ -127,7 +128,7 @@ def lstm_lm_slots(V, E, H, L, B):
 
 
 def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", max_T=None,
-                    training_flag=False, dropout=0.0):
+                    training_flag=False, dropout=0.0, flag_speculation="value", clip_norm=0.0):
     """Generic graph of one truncated-BPTT step of the Figure 1 RNN model:
 
         state = self.state (zeros if it is still None)          # attribute read, P:266 (1)
@@ -140,7 +141,9 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     Arguments: 0 tokens i32[B,W], 1 targets i32[B,W], 2 lengths i32[B]; with training_flag also
     3 training i32[1]: the optimizer update runs only `if training:` (the train / evaluate branch
     of P:312), speculated on its profiled value (constant promotion) by a RUNTIME VALUE_EQ
-    assumption (id 8): the single taken arm is kept and asserted.
+    assumption (id 8): the single taken arm is kept and asserted; with
+    flag_speculation="branch" the assumption is BRANCH_ARM instead — the Switch takes its true arm
+    (any non-zero flag), the control-flow speculation itself rather than the value.
     dropout = p > 0: the Zaremba et al. [51] regularised model (PTB medium: H = 650, p =
     0.5): dropout on every non-recurrent connection — the embedding output, each layer's output
     into the next layer and the top layer's output into the decoder (DROPOUT sites 0 .. L) — with
@@ -252,7 +255,8 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     if training_flag:
         args.append(("training", I32, (1,)))
         if speculate != "none":
-            asms += [Assumption(8, "VALUE_EQ", RUNTIME, 3, value=1),
+            asms += [Assumption(8, "VALUE_EQ" if flag_speculation == "value" else "BRANCH_ARM", RUNTIME, 3,
+                                value=1),
                      Assumption(9, "DTYPE_EQ", DISPATCH, 3, dtype=I32)]
     if dropout:
         args.append(("dropout_key", I32, (2,)))
@@ -262,7 +266,7 @@ def lstm_lm_program(V, E, H, L, B, T, lr, *, speculate="unroll", gemm="bf16", ma
     return Program(f"lstm_lm_L{L}_H{H}" + (f"_drop{dropout:g}" if dropout else ""), g.ops, asms, slots, args, 1, lr,
                    meta=dict(model="lstm_lm", V=V, E=E, H=H, L=L, B=B, T=T, W=W, gemm=gemm,
                              speculate=speculate, training_flag=training_flag, dropout=dropout,
-                             key_arg=key_arg if dropout else -1))
+                             key_arg=key_arg if dropout else -1, clip_norm=clip_norm))
 
 
 # ------------------------------------------------------------------------------------------------
@@ -276,7 +280,7 @@ def treernn_slots(V, H, C):
             Slot("b_c", F32, (C,), True)]
 
 
-def treernn_program(V, H, C, B, lr, *, max_nodes=127, speculate="levels", gemm="bf16"):
+def treernn_program(V, H, C, B, lr, *, max_nodes=127, speculate="levels", gemm="bf16", clip_norm=0.0):
     """Generic graph of one TreeRNN training step (Socher et al. [37]; Table 2):
 
         def node(n):                                    # function 1, recursive (InvokeOp)
@@ -353,7 +357,7 @@ def treernn_program(V, H, C, B, lr, *, max_nodes=127, speculate="levels", gemm="
     args = [("kind", I32, None), ("left", I32, None), ("right", I32, None), ("word", I32, None),
             ("tree_off", I32, (B + 1,)), ("label", I32, (B,))]
     return Program(f"treernn_H{H}", g.ops, asms, slots, args, 1, lr,
-                   meta=dict(model="treernn", V=V, E=H, H=H, C=C, B=B, gemm=gemm,
+                   meta=dict(model="treernn", V=V, E=H, H=H, C=C, B=B, gemm=gemm, clip_norm=clip_norm,
                              max_nodes=max_nodes, speculate=speculate))
 
 
@@ -366,7 +370,7 @@ def treelstm_slots(V, E, H, C):
             Slot("b_c", F32, (C,), True)]
 
 
-def treelstm_program(V, E, H, C, B, lr, *, max_nodes=127, speculate="levels", gemm="bf16"):
+def treelstm_program(V, E, H, C, B, lr, *, max_nodes=127, speculate="levels", gemm="bf16", clip_norm=0.0):
     """Generic graph of one TreeLSTM training step:
 
         def node(n):                                    # function 1, recursive (InvokeOp)
@@ -449,7 +453,7 @@ def treelstm_program(V, E, H, C, B, lr, *, max_nodes=127, speculate="levels", ge
     args = [("kind", I32, None), ("left", I32, None), ("right", I32, None), ("word", I32, None),
             ("tree_off", I32, (B + 1,)), ("label", I32, (B,))]
     return Program(f"treelstm_H{H}", g.ops, asms, slots, args, 1, lr,
-                   meta=dict(model="treelstm", V=V, E=E, H=H, C=C, B=B, gemm=gemm,
+                   meta=dict(model="treelstm", V=V, E=E, H=H, C=C, B=B, gemm=gemm, clip_norm=clip_norm,
                              max_nodes=max_nodes, speculate=speculate))
 
 
