@@ -10,8 +10,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libjanus.so")
+# dev-only kernel variants for A/B measurements: JANUS_VARIANT=tag builds _build_tag/libjanus_tag.so
+# with JANUS_VARIANT_FLAGS added (the binding loads it when JANUS_VARIANT is set); unset = the product
+VARIANT = os.environ.get("JANUS_VARIANT", "")
+BUILD = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(HERE, f"libjanus_{VARIANT}.so" if VARIANT else "libjanus.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -31,6 +34,8 @@ def flags():
          "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"] + ARCH
     if inc:
         f += ["-I", inc]
+    if VARIANT:
+        f += os.environ.get("JANUS_VARIANT_FLAGS", "").split()
     return f
 
 

@@ -280,16 +280,12 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
           const int s = q % STAGES, r = q / STAGES;
           mbar_wait(&full[s], r & 1);
           tc_fence_after();
-          if (lane == 0) {
+          if (elect_one_sync()) {
             const uint32_t a = smem_u32(sA + s * C::A_BYTES), b = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-            for (int j = 0; j < C::BK / 16; ++j) {
-              const uint64_t ad = A_MN ? umma_desc_sw128(a + j * 2048, 8192, 1024)
-                                       : umma_desc_sw128(a + j * 32, 16, 1024);
-              const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
-                                       : umma_desc_sw128(b + j * 32, 16, 1024);
-              umma_bf16_pair(acc, ad, bd, idesc, (!first || j != 0) ? 1u : 0u);
-            }
+            static_assert(C::BK == 64, "one umma_bf16_pair_k64 per k-block");
+            umma_bf16_pair_k64(acc, A_MN ? umma_desc_sw128(a, 8192, 1024) : umma_desc_sw128(a, 16, 1024),
+                               B_MN ? umma_desc_sw128(b, 8192, 1024) : umma_desc_sw128(b, 16, 1024), idesc,
+                               first ? 0u : 1u, A_MN ? 128 : 2, B_MN ? 128 : 2);
             umma_commit_pair(&empty[s]);
           }
           first = false;
@@ -315,16 +311,12 @@ __global__ void __launch_bounds__(192 + 32 * (NMMA - 1), 1) gemm_bf16_tc_kernel(
         const int s = q % STAGES, r = q / STAGES;
         mbar_wait(&full[s], r & 1);
         tc_fence_after();
-        if (lane == 0) {
+        if (elect_one_sync()) {
           const uint32_t a = smem_u32(sA + s * C::A_BYTES), b = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-          for (int j = 0; j < C::BK / 16; ++j) {
-            const uint64_t ad = A_MN ? umma_desc_sw128(a + j * 2048, 8192, 1024)
-                                     : umma_desc_sw128(a + j * 32, 16, 1024);
-            const uint64_t bd = B_MN ? umma_desc_sw128(b + j * 2048, 8192, 1024)
-                                     : umma_desc_sw128(b + j * 32, 16, 1024);
-            umma_bf16(acc, ad, bd, idesc, (!first || j != 0) ? 1u : 0u);
-          }
+          static_assert(C::BK == 64, "one umma_bf16_k64 per k-block");
+          umma_bf16_k64(acc, A_MN ? umma_desc_sw128(a, 8192, 1024) : umma_desc_sw128(a, 16, 1024),
+                        B_MN ? umma_desc_sw128(b, 8192, 1024) : umma_desc_sw128(b, 16, 1024), idesc,
+                        first ? 0u : 1u, A_MN ? 128 : 2, B_MN ? 128 : 2);
           if (CM == 1) umma_commit(&empty[s]);
           else umma_commit_mc(&empty[s], cmask);
         }

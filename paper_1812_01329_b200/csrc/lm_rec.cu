@@ -25,7 +25,10 @@
 
 namespace jk {
 
-constexpr int REC_NMW = 4;       // MMA-issuing warps (one tcgen05.mma stream each, own accumulator)
+#ifndef JANUS_REC_NMW
+#define JANUS_REC_NMW 1
+#endif
+constexpr int REC_NMW = JANUS_REC_NMW;  // MMA-issuing warps (one tcgen05.mma stream each, own accumulator)
 constexpr int REC_THREADS = 160 + 32 * REC_NMW;
 constexpr int REC_UPC = 16;      // hidden units per CTA
 constexpr int REC_MAX_SLOTS = 48;
@@ -145,8 +148,9 @@ JN_DEV void issue_step(const uint8_t *srcA, const uint8_t *srcB, const RecLayout
   }
 }
 
-// MMA issuers (warps 5 .. 5+REC_NMW-1, lane 0 each). A single issuing warp sustains only about
-// one tcgen05.mma per ~130 cycles whatever N is (measured: scripts/bench_mma.cu), and the
+// MMA issuers (warps 5 .. 5+REC_NMW-1, one elected lane each, four MMAs per asm statement: a
+// single thread then issues back to back at ~35 cycles per M = 64 MMA, scripts/bench_mma_issue.cu;
+// under `lane == 0` with per-MMA descriptors it was ~130-150 cycles, scripts/bench_mma.cu), and the
 // recurrent MMAs are small (N = 64 / 32 / 16), so the step's K chunks are dealt round-robin to
 // REC_NMW warps, each accumulating into its own TMEM tile (columns w * NCOL); the epilogue sums
 // the tiles. Warp w: D_w = sum over chunks j = w (mod REC_NMW) of A_j . W_j^T (W chunk j at
@@ -169,10 +173,8 @@ JN_DEV void mma_step(const RecLayout &ly, uint8_t *sA, uint8_t *sW, int wchunk, 
       const int j = first + c;
       if (j % REC_NMW != w) continue;
       const uint32_t ca = sa + c * ly.cb, cw = smem_u32(sW + (size_t)j * wchunk);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(acc, umma_desc_sw128(ca + kk * 32, 16, 1024), umma_desc_sw128(cw + kk * 32, 16, 1024),
-                  idesc, (j != w || kk != 0) ? 1u : 0u);
+      umma_bf16_k64(acc, umma_desc_sw128(ca, 16, 1024), umma_desc_sw128(cw, 16, 1024), idesc, j != w ? 1u : 0u,
+                    2, 2);
     }
     umma_commit(&empty[s]);  // the slot is free once every issuing warp's MMAs on it completed
     if (pr && k < 4) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pr[9 + 2 * k]));
@@ -378,7 +380,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       }
       if (threadIdx.x == 128) PROBE(t, 2);
     } else if (warp >= 5) {
-      if ((threadIdx.x & 31) == 0) {
+      if (elect_one_sync()) {
         mma_step<NG>(ly, sA, sW, WCH, full, empty, tfull, tempty, tmem, idesc, t, warp - 5,
                      (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + t) * 16 : nullptr);
         if (warp == 5) PROBE(t, 4);
@@ -581,7 +583,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
       }
       __syncwarp();
     } else if (warp >= 5) {
-      if (has_next && (threadIdx.x & 31) == 0) {
+      if (has_next && elect_one_sync()) {
         mma_step<16>(ly, sA, sW, 2048, full, empty, tfull, tempty, tmem, idesc, nmma, warp - 5,
                            (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr);
         if (warp == 5) PROBE(ti, 4);
@@ -838,7 +840,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
       }
       __syncwarp();
     } else if (warp >= 5) {
-      if (nstep > 0 && lane == 0) {
+      if (nstep > 0 && elect_one_sync()) {
         mma_step<C::CUNITS>(lys, sA, sW, C::WCH, full, empty, tfull, tempty, tmem, idesc, nm, warp - 5,
                             (a.dbg && warp == 5) ? a.dbg + ((size_t)blockIdx.x * a.T + ti) * 16 : nullptr,
                             q_ring);

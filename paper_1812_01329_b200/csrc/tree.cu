@@ -21,7 +21,10 @@
 
 namespace jk {
 
-constexpr int T_NMW = 4;          // MMA-issuing warps (one accumulator each; ~130 cycles per issue)
+#ifndef JANUS_T_NMW
+#define JANUS_T_NMW 4
+#endif
+constexpr int T_NMW = JANUS_T_NMW;          // MMA-issuing warps (one accumulator each; ~130 cycles per issue)
 constexpr int TT = 160 + 32 * T_NMW;  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
 // ring stages: a multiple of T_NMW, so a stage is always consumed by the same MMA warp (it owns
 // chunks q = w mod T_NMW) and that warp can never wait on a stage two phases ahead of its loads

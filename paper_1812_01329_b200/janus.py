@@ -15,7 +15,8 @@ import numpy as np
 from workloads import programs as pg
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libjanus.so")
+LIB_PATH = os.path.join(HERE, f"libjanus_{os.environ['JANUS_VARIANT']}.so" if os.environ.get("JANUS_VARIANT")
+                        else "libjanus.so")  # JANUS_VARIANT: dev-only A/B builds (build.py)
 
 OK, ASSUMPTION_FAILED, ERR_INVALID, ERR_UNSUPPORTED, ERR_RUNTIME, ERR_CUDA, ERR_NCCL, ERR_WORKSPACE = range(8)
 STATUS_NAMES = ["OK", "ASSUMPTION_FAILED", "ERR_INVALID", "ERR_UNSUPPORTED", "ERR_RUNTIME",

@@ -9,6 +9,10 @@
 //   V4 dsst  : cluster; slice pushed with st.shared::cluster.v4 to every peer, then a remote
 //              release-arrive on each peer's mbarrier
 //   V5 dsbulk: cluster; slice staged in own smem, cp.async.bulk smem->peer smem per peer
+//   G5 dpoll : grid; no flags and no fences: every word of the slice carries the step number and
+//              the consumers load the whole block with relaxed vector loads, re-loading any
+//              granule that still holds an older value (the data is its own flag)
+//   G6 dpoll1: G5, but warp 0 first polls one word per producer slice before the full load
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/bx.bin scripts/bench_xchg.cu
 #include <cstdio>
 #include <cstdlib>
@@ -111,6 +115,52 @@ __global__ void k_grid(uint8_t *xbuf, unsigned *flags, int steps, int slice, uns
   if (threadIdx.x == 0) out[blockIdx.x] = (gtime() - t0) / (steps - 8);
 }
 
+
+// ----------------------------------------------------------------------------- data-as-flag
+template <int MODE>
+__global__ void k_dpoll(uint8_t *xbuf, int steps, int slice, unsigned long long *out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  const int G = gridDim.x;
+  unsigned long long t0 = 0;
+  const size_t blk = (size_t)G * slice;
+  for (int t = 0; t < steps; ++t) {
+    if (t == 8 && threadIdx.x == 0) t0 = gtime();
+    const unsigned tag = (unsigned)t + 1u;
+    uint8_t *base = xbuf + (size_t)(t % 64) * blk;
+    uint8_t *dst = base + (size_t)blockIdx.x * slice;
+    for (int o = threadIdx.x * 16; o < slice; o += blockDim.x * 16)
+      *reinterpret_cast<uint4 *>(dst + o) = make_uint4(tag, tag, tag, tag);
+    if (MODE == 6 && threadIdx.x < 32) {
+      for (int c = threadIdx.x; c < G; c += 32) {
+        unsigned x;
+        do { asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(base + (size_t)c * slice + slice - 4) : "memory"); } while (x != tag);
+      }
+    }
+    if (MODE == 6) __syncthreads();
+    constexpr int NB = 8;
+    for (size_t o0 = (size_t)threadIdx.x * 16; o0 < blk; o0 += (size_t)blockDim.x * 16 * NB) {
+      uint4 v[NB];
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const size_t o = o0 + (size_t)k * blockDim.x * 16;
+        if (o < blk)
+          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "l"(base + o) : "memory");
+      }
+#pragma unroll
+      for (int k = 0; k < NB; ++k) {
+        const size_t o = o0 + (size_t)k * blockDim.x * 16;
+        if (o >= blk) continue;
+        while (v[k].x != tag || v[k].y != tag || v[k].z != tag || v[k].w != tag)
+          asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "l"(base + o) : "memory");
+        *reinterpret_cast<uint4 *>(sm + o) = v[k];
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = (gtime() - t0) / (steps - 8);
+}
+
 // ----------------------------------------------------------------------------- cluster variants
 template <int MODE>
 __global__ void k_clu(uint8_t *xbuf, int steps, int slice, unsigned long long *out) {
@@ -194,6 +244,30 @@ int main() {
   void *gf[] = {(void *)k_grid<0>, (void *)k_grid<1>, (void *)k_grid<2>, (void *)k_grid<3>, (void *)k_grid<4>};
   const char *gn[] = {"flags", "count", "sync0", "acqpoll", "warprel"};
   for (auto f : gf) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  if (getenv("BX_DPOLL")) {
+    void *df[] = {(void *)k_dpoll<5>, (void *)k_dpoll<6>};
+    const char *dn[] = {"dpoll", "dpoll1"};
+    for (auto f : df) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    for (int G : {41, 82, 123})
+      for (int slice : {2048}) {
+        for (int m = 0; m < 3; ++m) {
+          cudaMemset(flags, 0, 1 << 20);
+          cudaMemset(xbuf, 0, 1 << 30);
+          int st = steps, sl = slice;
+          void *args[] = {&xbuf, &flags, &st, &sl, &out};
+          void *args2[] = {&xbuf, &st, &sl, &out};
+          for (int th : {128, 256}) {
+            if (m == 0) { if (th == 256) continue; cudaLaunchCooperativeKernel(gf[3], G, th, args, 200 << 10, 0); }
+            else cudaLaunchCooperativeKernel(df[m - 1], G, th, args2, 200 << 10, 0);
+            cudaError_t e = cudaDeviceSynchronize();
+            char nm[32];
+            snprintf(nm, sizeof nm, "%s/%d", m == 0 ? "acqpoll" : dn[m - 1], th);
+            report(nm, G, 0, slice, out, e);
+          }
+        }
+      }
+    return 0;
+  }
   if (getenv("BX_GRID_ONLY")) {
     for (int G : {41, 82, 123})
       for (int slice : {2048}) {
