@@ -291,6 +291,14 @@ JN_DEV void st_cluster_v4(uint32_t caddr, float4 v) {
                "f"(v.w)
                : "memory");
 }
+// 16-B store into a peer CTA's shared memory that completes 16 bytes of transaction count on the
+// peer's mbarrier (both shared::cluster addresses from mapa_shared): no proxy fence, no staging
+JN_DEV void st_async_v4(uint32_t caddr, float a, float b, float c, float d, uint32_t peer_bar_caddr) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   caddr),
+               "f"(a), "f"(b), "f"(c), "f"(d), "r"(peer_bar_caddr)
+               : "memory");
+}
 // bulk copy of this CTA's shared memory into a peer CTA's shared memory (DSMEM), completing
 // `bytes` of transaction count on the peer's mbarrier (both peer addresses from mapa_shared)
 JN_DEV void bulk_s2cluster(uint32_t dst_caddr, const void *src, uint32_t bytes, uint32_t peer_bar_caddr) {

@@ -70,13 +70,39 @@ JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
   fence_proxy_async_global();  // the bulk copies (async proxy) read what the generic proxy wrote
 }
 
+// Producer side of an exchange step: its generic-proxy stores of the exchange block, before the
+// release. (The consumer fences generic -> async proxy itself after its acquire, before the bulk
+// copy.) JANUS_PROD_PROXY_FENCE=0 measures the step without the producer-side fence.
+#ifndef JANUS_PROD_PROXY_FENCE
+#define JANUS_PROD_PROXY_FENCE 1
+#endif
+JN_DEV void prod_proxy_fence() {
+#if JANUS_PROD_PROXY_FENCE
+  fence_proxy_async_global();
+#endif
+}
 // Named barrier of the four epilogue warps (threads 0-127) — the other warps run ahead.
 JN_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // Epilogue: this step's exchange-block writes are done (fenced for the async proxy by the caller);
-// thread 0 releases the CTA's step flag once all four epilogue warps got here.
+// thread 0 releases the CTA's step flag once all four epilogue warps got here. Measured and not
+// the default (JANUS_WARP_RELEASE=1): each epilogue warp releasing its own rows with one
+// red.release.gpu.add on the flag (no CTA barrier; 4 increments per step) — faster in the
+// exchange microbenchmark (scripts/bench_xchg.cu "warprel"), slower in the kernels (C2 forward
+// 0.189 -> 0.197 ms, backward 0.246 -> 0.254 ms: four times the atomics on every polled line).
+#ifndef JANUS_WARP_RELEASE
+#define JANUS_WARP_RELEASE 0
+#endif
+constexpr unsigned REC_EPW = JANUS_WARP_RELEASE ? 4u : 1u;  // flag increments per published step
+JN_DEV unsigned flag_of(unsigned steps) { return steps * REC_EPW; }
 JN_DEV void epi_publish(unsigned int *flag, unsigned int v) {
+#if JANUS_WARP_RELEASE
+  (void)v;
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+#else
   epi_bar();
   if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+#endif
 }
 // Epilogue warp: its TMEM reads of this step completed -> the MMA warps may overwrite the tiles.
 JN_DEV void epi_tmem_release(uint64_t *tempty) {
@@ -347,7 +373,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
   unsigned int *flags = a.barrier;  // flags[c] = 1 + last step whose h block CTA c has written
   fence_proxy_async_global();
-  publish_flag(&flags[cx.cta * REC_FS], 1);
+  publish_flag(&flags[cx.cta * REC_FS], flag_of(1));
   const int T = a.T_dev ? *a.T_dev : a.T;
   constexpr uint32_t idesc = umma_idesc_bf16(M64 ? 64 : 128, NG, 0, 0);
   const int nacc = min(REC_NMW, nk);  // accumulator tiles in use
@@ -370,7 +396,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
         const int p0 = c0 / upc;
         const int p1 = min(run_a ? cx.nflagsA : cx.nflagsB, (c0 + 64 * nch + upc - 1) / upc);
         wait_flags_acq(run_a ? cx.flagsA : cx.flagsB, p0, p1,
-                       run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1);
+                       flag_of(run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1));
         if (threadIdx.x == 128) {
           if (k == 0) PROBE(t, 1);
           fence_proxy_async_global();  // generic-proxy writes of the producers -> async-proxy reads
@@ -443,7 +469,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       }
       // critical path first: the exchange copy of h_t, then the step flag; the rest after
       if (row) write_x(t + 1, hb);
-      fence_proxy_async_global();
+      prod_proxy_fence();
       if (threadIdx.x == 0) PROBE(t, 6);
       epi_publish(&flags[cx.cta * REC_FS], (unsigned)t + 2);
       if (threadIdx.x == 0) PROBE(t, 7);
@@ -574,7 +600,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     if (warp == 4) {
       if (has_next) {
         if (threadIdx.x == 128) PROBE(ti, 0);
-        wait_flags_warp(flags, gridDim.x, (unsigned)(T - 1 - t));  // dz_{t+1} fully written
+        wait_flags_warp(flags, gridDim.x, flag_of((unsigned)(T - 1 - t)));  // dz_{t+1} fully written
         if (threadIdx.x == 128) {
           PROBE(ti, 1);
           issue_step(dzsw + (size_t)(t + 1) * nk * ly.cb, nullptr, ly, sA, full, empty, nmma);
@@ -662,7 +688,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
         for (int k = 0; k < 8; ++k)
           *reinterpret_cast<uint4 *>(chunk + sw128_off(b, k)) = reinterpret_cast<const uint4 *>(dzb)[k];
       }
-      fence_proxy_async_global();
+      prod_proxy_fence();
       if (threadIdx.x == 0) PROBE(ti, 6);
       epi_publish(&flags[blockIdx.x * REC_FS], (unsigned)(T - t));
       if (threadIdx.x == 0) PROBE(ti, 7);
@@ -689,6 +715,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // (u0 = 16 * blockIdx.x, the same ownership, dz exchange layout and flags as the plain kernel)
 // and receives their partials from its KS_CL-1 peers, summed in a fixed order (deterministic).
 constexpr int KS_CL = 4;
+#ifndef JANUS_KS_STASYNC
+#define JANUS_KS_STASYNC 1  // partial tiles by st.async from registers (0: staged + bulk copies)
+#endif
 template <int UPC>
 struct KsCfg {
   static constexpr int CUNITS = KS_CL * UPC;              // units per cluster = MMA N
@@ -816,7 +845,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
             unsigned x;
             do {
               asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(cx.flagsA + c * REC_FS) : "memory");
-            } while (x < (unsigned)(T - t));
+            } while (x < flag_of((unsigned)(T - t)));
           }
           __syncwarp();
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -829,7 +858,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
             unsigned x;
             do {
               asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
-            } while (x < (unsigned)(T - 1 - t));
+            } while (x < flag_of((unsigned)(T - 1 - t)));
           }
           __syncwarp();
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -877,6 +906,65 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
       for (int u = 0; u < HU; ++u) dh[u] = 0.f;
       if (has_x) {
         const int par = nx & 1;
+#if JANUS_KS_STASYNC
+        // partial dh tiles leave straight from registers: st.async of each 16-B piece into the
+        // peer's red[par] slot, completing on the peer's redfull[par] (no staging, proxy fence or
+        // single-thread bulk issue); only this CTA's own partial goes through `stage`
+        static_assert(REC_NMW == 1, "one accumulator");
+        if (threadIdx.x == 0) mbar_expect_tx(&redfull[par], (KS_CL - 1) * C::TILE);
+        if (nstep > 0) {
+          mbar_wait(tfull, nm & 1);
+          if (threadIdx.x == 0) PROBE(ti, 5);
+          __syncwarp();
+          tc_fence_after();
+        }
+        epi_bar();  // every thread summed the previous step's stage
+        {  // M = 64: accumulator row i in TMEM lane (i % 16) + 32 (i / 16); lanes 16-31 idle
+          const int srow = 16 * warp + lane;
+          const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+          uint32_t r[KS_CL][UPC];
+          if (nstep > 0) {
+#pragma unroll
+            for (int p = 0; p < KS_CL; ++p) {
+              if constexpr (UPC == 16) tmem_ld16_nw(ta + UPC * p, r[p]);
+              else tmem_ld8_nw(ta + UPC * p, r[p]);
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int p = 0; p < KS_CL; ++p) tmem_pin(r[p]);
+          } else {
+#pragma unroll
+            for (int p = 0; p < KS_CL; ++p)
+#pragma unroll
+              for (int i = 0; i < UPC; ++i) r[p][i] = 0u;
+          }
+          if (nstep > 0) epi_tmem_release(tempty);
+          if (lane < 16) {
+#pragma unroll
+            for (int p = 0; p < KS_CL; ++p) {
+              const float *v = reinterpret_cast<const float *>(r[p]);
+              if (p == rank) {
+                float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + srow) * UPC);
+#pragma unroll
+                for (int q = 0; q < UPC / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              } else {
+                const int slot = rank < p ? rank : rank - 1;  // my sender slot inside peer p
+                const uint32_t dst =
+                    mapa_shared(smem_u32(red + ((size_t)(par * (KS_CL - 1) + slot) * 64 + srow) * UPC), p);
+                const uint32_t pbar = mapa_shared(smem_u32(&redfull[par]), p);
+#pragma unroll
+                for (int q = 0; q < UPC / 4; ++q)
+                  st_async_v4(dst + 16 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], pbar);
+              }
+            }
+          }
+        }
+        if (threadIdx.x == 0) PROBE(ti, 3);
+        epi_bar();  // own partial rows visible to every summing thread
+        if (threadIdx.x == 0) PROBE(ti, 14);
+        mbar_wait_cluster(&redfull[par], (nx >> 1) & 1);
+        if (threadIdx.x == 0) PROBE(ti, 15);
+#else
         if (threadIdx.x == 0) {
           bulk_wait_group_read0();  // the previous step's stage has been read out by the copies
           mbar_expect_tx(&redfull[par], (KS_CL - 1) * C::TILE);
@@ -943,6 +1031,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
         }
         mbar_wait(&redfull[par], (nx >> 1) & 1);
         if (threadIdx.x == 0) PROBE(ti, 15);
+#endif
 #pragma unroll
         for (int p = 0; p < KS_CL; ++p) {  // fixed order over the K-slices: deterministic
           const float *src = p == rank ? stage + (size_t)rank * 64 * UPC
@@ -986,7 +1075,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
         for (int k = 0; k < HU / 2; ++k)
           *reinterpret_cast<uint4 *>(chunk + sw128_off(eb, g0 + k)) = reinterpret_cast<const uint4 *>(dzb)[k];
       }
-      fence_proxy_async_global();
+      prod_proxy_fence();
       if (threadIdx.x == 0) PROBE(ti, 6);
       if (active) epi_publish(&flags[lcta * REC_FS], (unsigned)(T - t));
       if (threadIdx.x == 0) PROBE(ti, 7);
