@@ -45,6 +45,16 @@ JN_DEV float tanh_f(float x) {
 // Step flags are REC_FS words apart (one 128-B line each): a CTA's release store then shares its
 // line with no other producer while ~100 consumers poll.
 constexpr int REC_FS = 32;
+// Spin-wait backoff of the step-flag polls (JANUS_POLL_NS > 0: __nanosleep between polls, less
+// L2 traffic on the polled lines)
+#ifndef JANUS_POLL_NS
+#define JANUS_POLL_NS 0
+#endif
+JN_DEV void poll_backoff() {
+#if JANUS_POLL_NS > 0
+  __nanosleep(JANUS_POLL_NS);
+#endif
+}
 
 // Dataflow synchronisation between the CTAs of a recurrent launch. Every step writes a fresh row
 // block (h_t / dz_t), so there are no write-after-read hazards — only read-after-write: a CTA
@@ -63,6 +73,7 @@ JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
     unsigned x;
     do {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
+      if (x < v) poll_backoff();
     } while (x < v);
   }
   __syncwarp();
@@ -233,6 +244,7 @@ JN_DEV void wait_flag_set(const unsigned int *flags, int n, unsigned int v) {
     unsigned x;
     do {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
+      if (x < v) poll_backoff();
     } while (x < v);
   }
 }
@@ -270,6 +282,7 @@ JN_DEV void wait_flags_acq(const unsigned int *flags, int p0, int p1, unsigned i
     unsigned x;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
+      if (x < v) poll_backoff();
     } while (x < v);
   }
   __syncwarp();  // bar.warp.sync orders every lane's acquire before lane 0's copy issue
@@ -387,16 +400,24 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
       // of this layer (or h_t of the layer below, which runs ahead), run B = this layer's h_{t-1}.
       const uint8_t *srcA = hswA + (size_t)(t + cx.blkA_off) * nkh * ly.cb;
       const uint8_t *srcB = hsw + (size_t)t * nkh * ly.cb;
-      for (int k = 0; k < ly.nops; ++k) {
+      // the producers' step flags of an op, its flag target
+      auto op_flags = [&](int k, int &p0, int &p1, const unsigned int *&fl, unsigned &tgt) {
         int first, nch;
         op_range(ly, k, first, nch);
         const bool run_a = first < ly.nka;
         const int upc = run_a ? cx.upcA : cx.upcB;
         const int c0 = (run_a ? first : first - ly.nka) * 64;  // first unit of the op
-        const int p0 = c0 / upc;
-        const int p1 = min(run_a ? cx.nflagsA : cx.nflagsB, (c0 + 64 * nch + upc - 1) / upc);
-        wait_flags_acq(run_a ? cx.flagsA : cx.flagsB, p0, p1,
-                       flag_of(run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1));
+        p0 = c0 / upc;
+        p1 = min(run_a ? cx.nflagsA : cx.nflagsB, (c0 + 64 * nch + upc - 1) / upc);
+        fl = run_a ? cx.flagsA : cx.flagsB;
+        tgt = flag_of(run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1);
+      };
+      for (int k = 0; k < ly.nops; ++k) {
+        int p0, p1;
+        const unsigned int *fl;
+        unsigned tgt;
+        op_flags(k, p0, p1, fl, tgt);
+        wait_flags_acq(fl, p0, p1, tgt);
         if (threadIdx.x == 128) {
           if (k == 0) PROBE(t, 1);
           fence_proxy_async_global();  // generic-proxy writes of the producers -> async-proxy reads
@@ -845,6 +866,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
             unsigned x;
             do {
               asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(cx.flagsA + c * REC_FS) : "memory");
+              if (x < flag_of((unsigned)(T - t))) poll_backoff();
             } while (x < flag_of((unsigned)(T - t)));
           }
           __syncwarp();
@@ -858,6 +880,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
             unsigned x;
             do {
               asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
+              if (x < flag_of((unsigned)(T - 1 - t))) poll_backoff();
             } while (x < flag_of((unsigned)(T - 1 - t)));
           }
           __syncwarp();

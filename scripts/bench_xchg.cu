@@ -13,6 +13,9 @@
 //              the consumers load the whole block with relaxed vector loads, re-loading any
 //              granule that still holds an older value (the data is its own flag)
 //   G6 dpoll1: G5, but warp 0 first polls one word per producer slice before the full load
+//   G7 bpoll : no flags and no fences: the consumer bulk-copies the block speculatively right
+//              after writing its own slice, every thread checks the words it owns in shared
+//              memory, and pieces holding an older step's words are copied again until clean
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/bx.bin scripts/bench_xchg.cu
 #include <cstdio>
 #include <cstdlib>
@@ -161,6 +164,79 @@ __global__ void k_dpoll(uint8_t *xbuf, int steps, int slice, unsigned long long 
   if (threadIdx.x == 0) out[blockIdx.x] = (gtime() - t0) / (steps - 8);
 }
 
+
+// bulk-copy speculation: pieces of PB bytes; a piece is clean when none of its words holds an
+// older tag (every word of step t's block carries t + 1)
+template <int PB>
+__global__ void k_bpoll(uint8_t *xbuf, int steps, int slice, unsigned long long *out, unsigned *retries) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_bad[512];
+  __shared__ int s_nbad;
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) { bar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  __syncthreads();
+  unsigned long long t0 = 0;
+  unsigned nretry = 0;
+  uint32_t phase = 0;
+  const size_t blk = (size_t)G * slice;
+  const int npc = (int)((blk + PB - 1) / PB);
+  for (int t = 0; t < steps; ++t) {
+    if (t == 8 && threadIdx.x == 0) t0 = gtime();
+    const unsigned tag = (unsigned)t + 1u;
+    uint8_t *base = xbuf + (size_t)(t % 64) * blk;
+    uint8_t *dst = base + (size_t)blockIdx.x * slice;
+    for (int o = threadIdx.x * 16; o < slice; o += blockDim.x * 16)
+      *reinterpret_cast<uint4 *>(dst + o) = make_uint4(tag, tag, tag, tag);
+    // first round: every piece
+    if (threadIdx.x == 0) { s_nbad = npc; }
+    for (int i = threadIdx.x; i < npc; i += blockDim.x) s_bad[i] = i;
+    __syncthreads();
+    while (true) {
+      const int nb = s_nbad;
+      if (nb == 0) break;
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        uint32_t bytes = 0;
+        for (int i = 0; i < nb; ++i) {
+          const size_t o = (size_t)s_bad[i] * PB;
+          bytes += (uint32_t)min((size_t)PB, blk - o);
+        }
+        bar_expect(&bar, bytes);
+        for (int i = 0; i < nb; ++i) {
+          const size_t o = (size_t)s_bad[i] * PB;
+          const uint32_t n = (uint32_t)min((size_t)PB, blk - o);
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s32(sm + o)),
+                       "l"(base + o), "r"(n), "r"(s32(&bar)) : "memory");
+        }
+      }
+      bar_wait(&bar, phase & 1);
+      ++phase;
+      __syncthreads();
+      if (threadIdx.x == 0) s_nbad = 0;
+      __syncthreads();
+      // verify: thread handles words of the re-copied pieces
+      for (int i = 0; i < nb; ++i) {
+        const size_t o = (size_t)s_bad[i] * PB;
+        const int n = (int)min((size_t)PB, blk - o);
+        bool bad = false;
+        for (int w = threadIdx.x * 16; w < n; w += blockDim.x * 16) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(sm + o + w);
+          bad |= v.x != tag || v.y != tag || v.z != tag || v.w != tag;
+        }
+        if (__syncthreads_or(bad)) {
+          if (threadIdx.x == 0) { s_bad[s_nbad++] = s_bad[i]; }
+        }
+      }
+      __syncthreads();
+      if (s_nbad && threadIdx.x == 0) ++nretry;
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[blockIdx.x] = (gtime() - t0) / (steps - 8); retries[blockIdx.x] = nretry; }
+}
+
 // ----------------------------------------------------------------------------- cluster variants
 template <int MODE>
 __global__ void k_clu(uint8_t *xbuf, int steps, int slice, unsigned long long *out) {
@@ -244,6 +320,37 @@ int main() {
   void *gf[] = {(void *)k_grid<0>, (void *)k_grid<1>, (void *)k_grid<2>, (void *)k_grid<3>, (void *)k_grid<4>};
   const char *gn[] = {"flags", "count", "sync0", "acqpoll", "warprel"};
   for (auto f : gf) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+  if (getenv("BX_BPOLL")) {
+    unsigned *retries;
+    cudaMalloc(&retries, 1024 * 4);
+    cudaFuncSetAttribute(k_bpoll<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    cudaFuncSetAttribute(k_bpoll<32768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    cudaFuncSetAttribute(gf[3], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    for (int G : {41, 82})
+      for (int slice : {2048}) {
+        for (int m = 0; m < 3; ++m) {
+          cudaMemset(flags, 0, 1 << 20);
+          cudaMemset(xbuf, 0, 1 << 30);
+          int st = steps, sl = slice;
+          void *args[] = {&xbuf, &flags, &st, &sl, &out};
+          void *args2[] = {&xbuf, &st, &sl, &out, &retries};
+          if (m == 0) cudaLaunchCooperativeKernel(gf[3], G, 128, args, 200 << 10, 0);
+          else if (m == 1) cudaLaunchCooperativeKernel((void *)k_bpoll<8192>, G, 128, args2, 200 << 10, 0);
+          else cudaLaunchCooperativeKernel((void *)k_bpoll<32768>, G, 128, args2, 200 << 10, 0);
+          cudaError_t e = cudaDeviceSynchronize();
+          const char *nm[] = {"acqpoll", "bpoll8K", "bpoll32K"};
+          report(nm[m], G, 0, slice, out, e);
+          if (m) {
+            std::vector<unsigned> r(G);
+            cudaMemcpy(r.data(), retries, G * 4, cudaMemcpyDeviceToHost);
+            unsigned long long tot = 0;
+            for (unsigned x : r) tot += x;
+            printf("        retries per CTA-step: %.3f\n", (double)tot / G / steps);
+          }
+        }
+      }
+    return 0;
+  }
   if (getenv("BX_DPOLL")) {
     void *df[] = {(void *)k_dpoll<5>, (void *)k_dpoll<6>};
     const char *dn[] = {"dpoll", "dpoll1"};
