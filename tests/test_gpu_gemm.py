@@ -1,4 +1,5 @@
-"""tcgen05 GEMM vs the oracle's contraction (fp64 of the same bf16-rounded operands)."""
+"""tcgen05 GEMM vs the oracle's contraction (fp64 of the same bf16-rounded operands): every output
+element within the fp32 summation bound gamma_K * sum_k |a_k b_k|, plus the relative-norm check."""
 import numpy as np
 import pytest
 
@@ -46,6 +47,20 @@ def _run(M, N, K, a_mn, b_mn, bias=None, acc=False, seed=0, splits=None, ret_out
     if acc:
         ref += np.asarray(C0, np.float32)[:, :N]
     got = dC.cpu().double().numpy()[:, :N]
+    # element-wise: bf16 x bf16 products are exact in fp32, so each output differs from the fp64
+    # reference by at most the fp32 summation error, |err| <= gamma_n * sum_k |a_k b_k| (+ the
+    # rounding of the bias / old C terms), gamma_n ~ n u with n = K + 2 terms, u = 2^-24; a factor
+    # two of slack for the split / tile summation order
+    absref = np.abs(A) @ np.abs(B).T
+    if bcol is not None:
+        absref += np.abs(bcol.cpu().double().numpy())[None, :]
+    if brow is not None:
+        absref += np.abs(brow.cpu().double().numpy())[:, None]
+    if acc:
+        absref += np.abs(np.asarray(C0, np.float32)[:, :N])
+    bound = 2.0 * (K + 2) * 2.0 ** -24 * absref + 1e-30
+    worst = (np.abs(got - ref) / bound).max()
+    assert worst <= 1.0, f"element-wise fp32 summation bound exceeded by {worst:.3g}x"
     err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
     return (err, got) if ret_out else err
 
