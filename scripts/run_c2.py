@@ -1,6 +1,6 @@
 """Run N C2 training steps through janus_run (for ncu / sanitizer captures; no timing).
 
-usage: python scripts/run_c2.py [steps] [c2|c3|c4|c1]"""
+usage: python scripts/run_c2.py [steps] [c2|c2big|c3|c4|c1]"""
 import os
 import sys
 
@@ -16,6 +16,9 @@ wl = sys.argv[2] if len(sys.argv) > 2 else "c2"
 if wl == "c2":
     prog = pg.lstm_lm_program(V=10000, E=650, H=650, L=2, B=64, T=35, lr=1.0)
     batches = list(gen.lm_batches(gen.SEED_C2, 64, 35, 10000, steps))
+elif wl == "c2big":  # V = 10^5: the xent / commit / embedding-gradient kernels stream >= 256 MB
+    prog = pg.lstm_lm_program(V=100000, E=650, H=650, L=2, B=64, T=35, lr=1.0)
+    batches = list(gen.lm_batches(gen.SEED_C2, 64, 35, 100000, steps))
 elif wl == "c1":
     prog = pg.lstm_lm_program(V=32, E=16, H=16, L=1, B=4, T=8, lr=0.1, gemm="f32")
     batches = [b for b in gen.c1_batches()[:steps]]
