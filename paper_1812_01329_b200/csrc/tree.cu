@@ -461,7 +461,7 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
       // ring chunk q goes to MMA warp q % T_NMW (a fixed owner per stage), accumulating into
       // its own TMEM tile
       const int w = warp - 5;
-      if ((threadIdx.x & 31) == 0) {
+      if (elect_one_sync()) {
         if (res && !rg.bres_ready) {
           mbar_wait(rg.bres_bar, 0);
           rg.bres_ready = true;
@@ -474,10 +474,8 @@ JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, 
           tc_fence_after();
           const uint32_t a = smem_u32(rg.sA + s * T_ASTAGE);
           const uint32_t b = res ? smem_u32(rg.sBres + kc * NT * 128) : smem_u32(rg.sB + s * T_BSTAGE);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16(acc, umma_desc_sw128(a + k * 32, 16, 1024),
-                      umma_desc_sw128(b + k * 32, 16, 1024), idesc, (kc != kc0 || k != 0) ? 1u : 0u);
+          umma_bf16_k64(acc, umma_desc_sw128(a, 16, 1024), umma_desc_sw128(b, 16, 1024), idesc,
+                        kc != kc0 ? 1u : 0u, 2, 2);
           umma_commit(&rg.empty[s]);
         }
         umma_commit(rg.tfull);  // arrives even with no chunk (nk < T_NMW)
