@@ -22,9 +22,9 @@
 namespace jk {
 
 #ifndef JANUS_T_NMW
-#define JANUS_T_NMW 4
+#define JANUS_T_NMW 2
 #endif
-constexpr int T_NMW = JANUS_T_NMW;          // MMA-issuing warps (one accumulator each; ~130 cycles per issue)
+constexpr int T_NMW = JANUS_T_NMW;  // MMA-issuing warps (one accumulator each); 2: C3 B=25 0.271 -> 0.264 ms, B=256 0.562 -> 0.570 (1: 0.264 / 0.577)
 constexpr int TT = 160 + 32 * T_NMW;  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
 // ring stages: a multiple of T_NMW, so a stage is always consumed by the same MMA warp (it owns
 // chunks q = w mod T_NMW) and that warp can never wait on a stage two phases ahead of its loads
@@ -429,6 +429,7 @@ template <int NT, int STAGED = 0, int NS = T_STAGES, typename Pre, typename Epi>
 JN_DEV void tile_loop(Ring &rg, const CUtensorMap *tmA, const CUtensorMap *tmB, int row0, int M,
                       int NTOT, int K, Pre pre, Epi epi, int nmw, unsigned long long *pr = nullptr,
                       const CUtensorMap *tmA32 = nullptr) {
+  nmw = min(nmw, T_NMW);        // the launch has T_NMW MMA warps
   while (NS % nmw) nmw >>= 1;  // a fixed MMA warp per ring stage
   // nmw in {1, 2, 4} MMA warps take part (T_STAGES % nmw == 0 keeps a fixed owner per stage):
   // more warps for long reductions, fewer TMEM tiles for the epilogue to sum on short ones
