@@ -254,7 +254,7 @@ def extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank
         w_ms, wo_ms = statistics.median(ab["with"]), statistics.median(ab["without"])
         out["guard_overhead"] = {"ms_with_asserts": w_ms, "ms_without": wo_ms, "overhead": w_ms / wo_ms - 1.0,
                                  "method": f"C2, strip_asserts A/B, interleaved, median of 5 x {K} steps "
-                                           "(noise ~ +-2%; the guard kernel's own share is phases_ms_per_step['guards'])"}
+                                           "(noise ~ +-2%; the runtime guards run inside the step's first launch, phases_ms_per_step['init'])"}
     # --- imperative per-op executor on the same workload (the paper's "Imp." column)
     if world == 1:
         loss = torch.zeros(1, device="cuda")

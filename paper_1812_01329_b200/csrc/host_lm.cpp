@@ -646,9 +646,13 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     o.partials_cap = (size_t)GEMM_PART_TILES * 128 * 256;
     return o;
   };
-  LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
-  if (p.while_mode) LCHK("trip", launch_trip(P.lens, B, Tw, dst, st));
-  if (gl.n) LCHK("guards", launch_guards(gl, dst, st));
+  if (p.while_mode) {
+    LCHK("init", launch_step_init(dst, bars, p.nbar, st, p.bf16 ? rec_flag_words(1) : 1));
+    LCHK("trip", launch_trip(P.lens, B, Tw, dst, st));
+    if (gl.n) LCHK("guards", launch_guards(gl, dst, st));
+  } else {
+    LCHK("init", launch_step_init_guards(dst, bars, p.nbar, p.bf16 ? rec_flag_words(1) : 1, gl, st));
+  }
   // operand copies (R1): interleaved / transposed bf16 working copies of the fp32 masters, the
   // interleaved biases and the ones columns — one fused launch
   {

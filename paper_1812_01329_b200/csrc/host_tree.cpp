@@ -286,10 +286,9 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
     gd.kind = G_TREE; gd.id = p.tree_guard_id; gd.data = argp[0]; gd.n = N; gd.data2 = argp[4];
     gl.g[gl.n++] = gd;
   }
-  TCHK("init", launch_step_init(dst, bars, 64, st));  // (the forward zeroes its level counters)
-  if (gl.n) TCHK("guards", launch_guards(gl, dst, st));
-  if (p.tree_guard) TCHK("tree_guard", launch_tree_guard(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
-  TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));
+  TCHK("init", launch_step_init_guards(dst, bars, 64, 1, gl, st));  // (the forward zeroes its level counters)
+  if (p.tree_guard) TCHK("schedule", launch_tree_guard_schedule(t, d, s, p.tree_guard_id, p.V, p.max_nodes, dst, st));
+  else TCHK("schedule", launch_tree_schedule(t, d, s, dst, st));
   // bf16 operand copies (R1): re-cast unless the last commit of this graph refreshed them and
   // no state-writing call came since (host.h copies_epoch; as the LM step)
   static const bool recast_env = [] { const char *e = getenv("JANUS_RECAST"); return e && e[0] == '1'; }();

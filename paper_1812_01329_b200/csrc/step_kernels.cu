@@ -37,17 +37,15 @@ cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cu
 
 // One block per assumption; each failing element proposes (id << 40 | index) to an atomicMin,
 // so the reported failure is the minimum id and, within it, the first element (reading Q9).
-__global__ void guards_kernel(GuardList gl, DevStatus *st) {
-  pdl_enter();
-  const GuardDesc g = gl.g[blockIdx.x];
+JN_DEV void guard_eval(const GuardDesc &g, DevStatus *st, int tid, int nthr) {
   const unsigned long long mask = (1ull << IDX_BITS) - 1;
   if (g.kind == G_TREE) return;  // evaluated by tree_guard_kernel
   if (g.kind == G_FORCED) {
-    if (threadIdx.x == 0) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | mask);
+    if (tid == 0) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | mask);
     return;
   }
   const long long n = (g.kind == G_FIRST_EQ || g.kind == G_FIRST_TRUTH) ? 1 : g.n;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+  for (long long i = tid; i < n; i += nthr) {
     const long long v = g.data[i];
     bool bad = false;
     if (g.kind == G_ALL_EQ || g.kind == G_FIRST_EQ) bad = v != g.value;
@@ -55,6 +53,38 @@ __global__ void guards_kernel(GuardList gl, DevStatus *st) {
     else if (g.kind == G_RANGE) bad = v < g.lo || v > g.hi;
     if (bad) atomicMin(&st->key, ((unsigned long long)g.id << IDX_BITS) | (unsigned long long)i);
   }
+}
+__global__ void guards_kernel(GuardList gl, DevStatus *st) {
+  pdl_enter();
+  guard_eval(gl.g[blockIdx.x], st, threadIdx.x, blockDim.x);
+}
+
+// The step's first launch when nothing runs between the init and the guards: one block zeroes
+// the status word and the step flags, then evaluates every runtime guard (one launch instead of
+// two; bar.sync orders thread 0's key reset before the block's atomicMin proposals).
+__global__ void __launch_bounds__(512) step_init_guards_kernel(DevStatus *st, unsigned int *bar, int nbar,
+                                                              int stride, GuardList gl) {
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    st->key = KEY_PASS;
+    st->observed = 0;
+    st->runtime_err = 0;
+    st->status = 0;
+    st->loss = 0.f;
+    st->trip = 0;
+    st->flags = 0;
+  }
+  for (int k = threadIdx.x; k * stride < nbar; k += blockDim.x) bar[(size_t)k * stride] = 0;
+  __syncthreads();
+  for (int j = 0; j < gl.n; ++j) guard_eval(gl.g[j], st, threadIdx.x, blockDim.x);
+}
+cudaError_t launch_step_init_guards(DevStatus *st, unsigned int *barriers, int nbar, int stride,
+                                    const GuardList &gl, cudaStream_t s) {
+  {
+    const cudaError_t pe_ = launch_pdl(step_init_guards_kernel, dim3(1), dim3(512), 0, s, st, barriers, nbar, stride, gl);
+    if (pe_ != cudaSuccess) return pe_;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s) {

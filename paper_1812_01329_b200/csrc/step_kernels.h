@@ -45,6 +45,9 @@ struct GuardList {
 // status word := PASS; zeroes words 0, stride, 2 stride, ... < nbar of the step-flag area
 cudaError_t launch_step_init(DevStatus *st, unsigned int *barriers, int nbar, cudaStream_t s, int stride = 1);
 cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s);
+// init + guards in one single-block launch (the step's first launch)
+cudaError_t launch_step_init_guards(DevStatus *st, unsigned int *barriers, int nbar, int stride,
+                                    const GuardList &gl, cudaStream_t s);
 
 // gather X[t*B+b] = rb(E[tok[b][t]]) (bf16, ld) with X[:, E] = 1 (ones column for bias grads);
 // ids outside [0,V) set runtime_err and read row 0.

@@ -128,10 +128,8 @@ JN_DEV void grid_sync(unsigned int *ctr, unsigned int target, unsigned long long
 // failing element is reported (observed = off[t] for offsets, kind[n] for nodes).
 constexpr int TREE_GUARD_SMEM_INTS = 48 * 1024;  // offsets + parent counts in shared memory up to 192 KB
 
-__global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d, TreeSched s,
-                                                          unsigned id, long long V, long long maxn,
-                                                          DevStatus *st) {
-  pdl_enter();
+JN_DEV void tree_guard_body(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
+                            long long V, long long maxn, DevStatus *st) {
   __shared__ int s_badoff;
   __shared__ int s_badnode;
   const int N = d.N, B = d.B;
@@ -194,6 +192,12 @@ __global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d
     atomicMin(&st->key, ((unsigned long long)id << IDX_BITS) | (unsigned long long)s_badnode);
   (void)mask;
 }
+__global__ void __launch_bounds__(1024) tree_guard_kernel(TreeBufs t, TreeDims d, TreeSched s,
+                                                          unsigned id, long long V, long long maxn,
+                                                          DevStatus *st) {
+  pdl_enter();
+  tree_guard_body(t, d, s, id, V, maxn, st);
+}
 
 cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
                               long long V, long long max_nodes, DevStatus *st, cudaStream_t str) {
@@ -213,16 +217,15 @@ cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSc
 constexpr int TREE_SCHED_SMEM_NODES = 13 * 1024;  // heights + children in shared memory up to 156 KB
 constexpr int TREE_SCHED_SMEM_OFF = 4096;         // + the tree offsets (16 KB)
 
-__global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
-                                                             const DevStatus *st) {
-  pdl_enter();
+JN_DEV void tree_schedule_body(const TreeBufs &t, const TreeDims &d, const TreeSched &s, const DevStatus *st) {
   __shared__ int hist[TREE_MAX_LEVELS + 1];
   __shared__ int running[TREE_MAX_LEVELS + 1];
   __shared__ unsigned short wcnt[32][TREE_MAX_LEVELS];
   __shared__ int s_L;
   const int N = d.N, B = d.B;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (st->key != KEY_PASS) {  // the forest failed its AssertOp: nothing downstream may run
+  if (*reinterpret_cast<const volatile unsigned long long *>(&st->key) != KEY_PASS) {
+    // the forest failed its AssertOp: nothing downstream may run
     if (tid == 0) { s.meta[0] = 0; s.meta[1] = 0; s.meta[2] = 0; s.meta[3] = 0; }
     return;
   }
@@ -385,6 +388,21 @@ __global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDim
   if (pb && tid == 0) pb[5] = gtimer();
   (void)st;
 }
+__global__ void __launch_bounds__(1024) tree_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
+                                                             const DevStatus *st) {
+  pdl_enter();
+  tree_schedule_body(t, d, s, st);
+}
+// TREE_BINARY guard and level schedule in one single-block launch (both are one block of 1024
+// threads; bar.sync orders the guard's key proposals before the schedule reads the key)
+__global__ void __launch_bounds__(1024) tree_guard_schedule_kernel(TreeBufs t, TreeDims d, TreeSched s,
+                                                                   unsigned id, long long V, long long maxn,
+                                                                   DevStatus *st) {
+  pdl_enter();
+  tree_guard_body(t, d, s, id, V, maxn, st);
+  __syncthreads();
+  tree_schedule_body(t, d, s, st);
+}
 
 cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                                  const DevStatus *st, cudaStream_t str) {
@@ -394,6 +412,22 @@ cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const Tre
   if (e != cudaSuccess) return e;
   {
     const cudaError_t pe_ = launch_pdl(tree_schedule_kernel, dim3(1), dim3(1024), smem, str, t, d, s, st);
+    if (pe_ != cudaSuccess) return pe_;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tree_guard_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
+                                       long long V, long long max_nodes, DevStatus *st, cudaStream_t str) {
+  const int gsmem = d.B + 1 + d.N <= TREE_GUARD_SMEM_INTS ? (d.B + 1 + d.N) * 4 : 0;
+  const int ssmem = d.N <= TREE_SCHED_SMEM_NODES
+                        ? (3 * d.N + TREE_SCHED_SMEM_OFF + (d.N <= 2048 ? d.N : 0)) * 4 : 0;
+  cudaError_t e = set_smem_once((const void *)tree_guard_schedule_kernel,
+                                std::max(TREE_GUARD_SMEM_INTS, 3 * TREE_SCHED_SMEM_NODES + TREE_SCHED_SMEM_OFF) * 4);
+  if (e != cudaSuccess) return e;
+  {
+    const cudaError_t pe_ = launch_pdl(tree_guard_schedule_kernel, dim3(1), dim3(1024), std::max(gsmem, ssmem), str, t, d,
+                                       s, id, V, max_nodes, st);
     if (pe_ != cudaSuccess) return pe_;
   }
   return cudaGetLastError();

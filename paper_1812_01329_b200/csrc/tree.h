@@ -58,6 +58,8 @@ struct TreeBufs {
 
 cudaError_t launch_tree_guard(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
                               long long V, long long max_nodes, DevStatus *st, cudaStream_t str);
+cudaError_t launch_tree_guard_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s, unsigned id,
+                                       long long V, long long max_nodes, DevStatus *st, cudaStream_t str);
 cudaError_t launch_tree_schedule(const TreeBufs &t, const TreeDims &d, const TreeSched &s,
                                  const DevStatus *st, cudaStream_t str);
 // forward: leaf gather, leaf level, internal levels (one cooperative launch)
