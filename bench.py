@@ -159,6 +159,31 @@ def cpu_baseline():
             "host_cpus": os.cpu_count()}
 
 
+def cpu_baseline_modes():
+    """SURVEY §8(d) oracle modes beside the headline baseline: the C2 step on ONE thread (BLAS
+    limited through threadpoolctl) and a C3 TreeLSTM step (B=25) on all threads."""
+    from oracle import interp as I
+    res = {}
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            dt = oracle_sample(8, 35)
+        res["c2_1thread"] = {"value": 8 / dt, "unit": "samples/s", "cores": 1,
+                             "sample": f"B=8 sequences x T=35 of the C2 model through oracle.run_graph_step in {dt:.1f} s"}
+    except Exception as e:  # threadpoolctl missing: report why
+        res["c2_1thread"] = {"unavailable": str(e)[:120]}
+    tp = pg.treelstm_program(V=20000, E=300, H=300, C=2, B=25, lr=0.05)
+    state = gen.uniform_params(tp, 1, 0.05)
+    forest = list(gen.sst_forest(gen.SEED_C3, 0, 25, 20000))
+    t0 = time.perf_counter()
+    r = I.run_graph_step(tp, forest, state)
+    dt = time.perf_counter() - t0
+    assert r.status == I.OK
+    res["c3_b25"] = {"value": 25 / dt, "unit": "sentences/s", "cores": _blas_threads(),
+                     "sample": f"one C3 step (B=25 trees, H=E=300) through oracle.run_graph_step in {dt:.2f} s"}
+    return res
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -673,6 +698,8 @@ def main():
         out.update(extras(J, torch, g, ws, state, dev_batches, stream, timed, args, world, rank, ms_step))
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline()
+        if not args.no_extras and world == 1:
+            out["cpu_baseline_modes"] = cpu_baseline_modes()
     if rank == 0:
         emit(out)
     if world > 1:
