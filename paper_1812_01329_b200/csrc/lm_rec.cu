@@ -736,6 +736,9 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // (u0 = 16 * blockIdx.x, the same ownership, dz exchange layout and flags as the plain kernel)
 // and receives their partials from its KS_CL-1 peers, summed in a fixed order (deterministic).
 constexpr int KS_CL = 4;
+#ifndef JANUS_BWD_OPWAIT
+#define JANUS_BWD_OPWAIT 0  // 1: run B waited for and copied op by op (measured 0.248 -> 0.250 ms: not kept)
+#endif
 #ifndef JANUS_KS_STASYNC
 #define JANUS_KS_STASYNC 1  // partial tiles by st.async from registers (0: staged + bulk copies)
 #endif
@@ -874,6 +877,25 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
           fence_proxy_async_global();
           if (threadIdx.x == 128) issue_step(srcA, srcB, lys, sA, full, empty, 0, 0, opsA, q_ring);
         }
+#if JANUS_BWD_OPWAIT
+        if (nbs > 0) {
+          // this layer's dz_{t+1}, op by op: wait (acquire polls) only for the producers of the
+          // op's chunks, then issue its copy — the early chunks' copies and MMAs overlap the
+          // arrival of the later producers (as the forward); chunk j is produced by CTAs
+          // [16 j / UPC, 16 (j + 1) / UPC)
+          for (int k = opsA; k < lys.nops; ++k) {
+            int first, nch;
+            op_range(lys, k, first, nch);  // run-B chunk indices first - na .. of my slice
+            const int j0 = b0 + first - na;
+            wait_flags_acq(flags, j0 * 16 / UPC, (j0 + nch) * 16 / UPC, flag_of((unsigned)(T - 1 - t)));
+            if (threadIdx.x == 128) {
+              fence_proxy_async_global();
+              issue_step(srcA, srcB, lys, sA, full, empty, 0, k, k + 1, q_ring);
+            }
+            __syncwarp();
+          }
+        }
+#else
         if (nbs > 0) {  // this layer's dz_{t+1}: chunk j is produced by CTAs [16 j / UPC, 16 (j + 1) / UPC)
           const int p0 = b0 * 16 / UPC, p1 = (b0 + nbs) * 16 / UPC;
           for (int c = p0 + lane; c < p1; c += 32) {
@@ -888,6 +910,7 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
           fence_proxy_async_global();
           if (threadIdx.x == 128) issue_step(srcA, srcB, lys, sA, full, empty, 0, opsA, 1 << 30, q_ring);
         }
+#endif
         if (threadIdx.x == 128) PROBE(ti, 2);
       }
       __syncwarp();
