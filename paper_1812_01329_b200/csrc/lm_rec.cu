@@ -25,10 +25,9 @@
 
 namespace jk {
 
-#ifndef JANUS_REC_NMW
-#define JANUS_REC_NMW 1
-#endif
-constexpr int REC_NMW = JANUS_REC_NMW;  // MMA-issuing warps (one tcgen05.mma stream each, own accumulator)
+// MMA-issuing warps (one tcgen05.mma stream each, own accumulator): with the elect.sync issue one
+// warp keeps the M = 64 MMAs pipe-bound (round 1 used four to hide a slow per-MMA issue)
+constexpr int REC_NMW = 1;
 constexpr int REC_THREADS = 160 + 32 * REC_NMW;
 constexpr int REC_UPC = 16;      // hidden units per CTA
 constexpr int REC_MAX_SLOTS = 48;
@@ -45,16 +44,6 @@ JN_DEV float tanh_f(float x) {
 // Step flags are REC_FS words apart (one 128-B line each): a CTA's release store then shares its
 // line with no other producer while ~100 consumers poll.
 constexpr int REC_FS = 32;
-// Spin-wait backoff of the step-flag polls (JANUS_POLL_NS > 0: __nanosleep between polls, less
-// L2 traffic on the polled lines)
-#ifndef JANUS_POLL_NS
-#define JANUS_POLL_NS 0
-#endif
-JN_DEV void poll_backoff() {
-#if JANUS_POLL_NS > 0
-  __nanosleep(JANUS_POLL_NS);
-#endif
-}
 
 // Dataflow synchronisation between the CTAs of a recurrent launch. Every step writes a fresh row
 // block (h_t / dz_t), so there are no write-after-read hazards — only read-after-write: a CTA
@@ -73,7 +62,6 @@ JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
     unsigned x;
     do {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
-      if (x < v) poll_backoff();
     } while (x < v);
   }
   __syncwarp();
@@ -82,38 +70,16 @@ JN_DEV void wait_flags_warp(const unsigned int *flags, int n, unsigned int v) {
 }
 
 // Producer side of an exchange step: its generic-proxy stores of the exchange block, before the
-// release. (The consumer fences generic -> async proxy itself after its acquire, before the bulk
-// copy.) JANUS_PROD_PROXY_FENCE=0 measures the step without the producer-side fence.
-#ifndef JANUS_PROD_PROXY_FENCE
-#define JANUS_PROD_PROXY_FENCE 1
-#endif
-JN_DEV void prod_proxy_fence() {
-#if JANUS_PROD_PROXY_FENCE
-  fence_proxy_async_global();
-#endif
-}
+// release (the consumer fences generic -> async proxy itself after its acquire, before the copy)
+JN_DEV void prod_proxy_fence() { fence_proxy_async_global(); }
 // Named barrier of the four epilogue warps (threads 0-127) — the other warps run ahead.
 JN_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // Epilogue: this step's exchange-block writes are done (fenced for the async proxy by the caller);
-// thread 0 releases the CTA's step flag once all four epilogue warps got here. Measured and not
-// the default (JANUS_WARP_RELEASE=1): each epilogue warp releasing its own rows with one
-// red.release.gpu.add on the flag (no CTA barrier; 4 increments per step) — faster in the
-// exchange microbenchmark (scripts/bench_xchg.cu "warprel"), slower in the kernels (C2 forward
-// 0.189 -> 0.197 ms, backward 0.246 -> 0.254 ms: four times the atomics on every polled line).
-#ifndef JANUS_WARP_RELEASE
-#define JANUS_WARP_RELEASE 0
-#endif
-constexpr unsigned REC_EPW = JANUS_WARP_RELEASE ? 4u : 1u;  // flag increments per published step
-JN_DEV unsigned flag_of(unsigned steps) { return steps * REC_EPW; }
+// thread 0 releases the CTA's step flag once all four epilogue warps got here. (Measured slower:
+// each epilogue warp releasing its own rows with a red.release.gpu.add.)
 JN_DEV void epi_publish(unsigned int *flag, unsigned int v) {
-#if JANUS_WARP_RELEASE
-  (void)v;
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
-#else
   epi_bar();
   if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
-#endif
 }
 // Epilogue warp: its TMEM reads of this step completed -> the MMA warps may overwrite the tiles.
 JN_DEV void epi_tmem_release(uint64_t *tempty) {
@@ -244,7 +210,6 @@ JN_DEV void wait_flag_set(const unsigned int *flags, int n, unsigned int v) {
     unsigned x;
     do {
       asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
-      if (x < v) poll_backoff();
     } while (x < v);
   }
 }
@@ -282,7 +247,6 @@ JN_DEV void wait_flags_acq(const unsigned int *flags, int p0, int p1, unsigned i
     unsigned x;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
-      if (x < v) poll_backoff();
     } while (x < v);
   }
   __syncwarp();  // bar.warp.sync orders every lane's acquire before lane 0's copy issue
@@ -386,7 +350,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
   const int len_b = (MASKED && row) ? a.lens[b] : 0;
   unsigned int *flags = a.barrier;  // flags[c] = 1 + last step whose h block CTA c has written
   fence_proxy_async_global();
-  publish_flag(&flags[cx.cta * REC_FS], flag_of(1));
+  publish_flag(&flags[cx.cta * REC_FS], (1));
   const int T = a.T_dev ? *a.T_dev : a.T;
   constexpr uint32_t idesc = umma_idesc_bf16(M64 ? 64 : 128, NG, 0, 0);
   const int nacc = min(REC_NMW, nk);  // accumulator tiles in use
@@ -410,7 +374,7 @@ JN_DEV void fwd_body(const FwdCtx &cx, const CUtensorMap *tmWa, const CUtensorMa
         p0 = c0 / upc;
         p1 = min(run_a ? cx.nflagsA : cx.nflagsB, (c0 + 64 * nch + upc - 1) / upc);
         fl = run_a ? cx.flagsA : cx.flagsB;
-        tgt = flag_of(run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1);
+        tgt = (run_a ? (unsigned)(t + 1 + cx.blkA_off) : (unsigned)t + 1);
       };
       for (int k = 0; k < ly.nops; ++k) {
         int p0, p1;
@@ -621,7 +585,7 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
     if (warp == 4) {
       if (has_next) {
         if (threadIdx.x == 128) PROBE(ti, 0);
-        wait_flags_warp(flags, gridDim.x, flag_of((unsigned)(T - 1 - t)));  // dz_{t+1} fully written
+        wait_flags_warp(flags, gridDim.x, ((unsigned)(T - 1 - t)));  // dz_{t+1} fully written
         if (threadIdx.x == 128) {
           PROBE(ti, 1);
           issue_step(dzsw + (size_t)(t + 1) * nk * ly.cb, nullptr, ly, sA, full, empty, nmma);
@@ -736,12 +700,6 @@ __global__ void __launch_bounds__(REC_THREADS, 1)
 // (u0 = 16 * blockIdx.x, the same ownership, dz exchange layout and flags as the plain kernel)
 // and receives their partials from its KS_CL-1 peers, summed in a fixed order (deterministic).
 constexpr int KS_CL = 4;
-#ifndef JANUS_BWD_OPWAIT
-#define JANUS_BWD_OPWAIT 0  // 1: run B waited for and copied op by op (measured 0.248 -> 0.250 ms: not kept)
-#endif
-#ifndef JANUS_KS_STASYNC
-#define JANUS_KS_STASYNC 1  // partial tiles by st.async from registers (0: staged + bulk copies)
-#endif
 template <int UPC>
 struct KsCfg {
   static constexpr int CUNITS = KS_CL * UPC;              // units per cluster = MMA N
@@ -869,48 +827,26 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
             unsigned x;
             do {
               asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(cx.flagsA + c * REC_FS) : "memory");
-              if (x < flag_of((unsigned)(T - t))) poll_backoff();
-            } while (x < flag_of((unsigned)(T - t)));
+            } while (x < ((unsigned)(T - t)));
           }
           __syncwarp();
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           fence_proxy_async_global();
           if (threadIdx.x == 128) issue_step(srcA, srcB, lys, sA, full, empty, 0, 0, opsA, q_ring);
         }
-#if JANUS_BWD_OPWAIT
-        if (nbs > 0) {
-          // this layer's dz_{t+1}, op by op: wait (acquire polls) only for the producers of the
-          // op's chunks, then issue its copy — the early chunks' copies and MMAs overlap the
-          // arrival of the later producers (as the forward); chunk j is produced by CTAs
-          // [16 j / UPC, 16 (j + 1) / UPC)
-          for (int k = opsA; k < lys.nops; ++k) {
-            int first, nch;
-            op_range(lys, k, first, nch);  // run-B chunk indices first - na .. of my slice
-            const int j0 = b0 + first - na;
-            wait_flags_acq(flags, j0 * 16 / UPC, (j0 + nch) * 16 / UPC, flag_of((unsigned)(T - 1 - t)));
-            if (threadIdx.x == 128) {
-              fence_proxy_async_global();
-              issue_step(srcA, srcB, lys, sA, full, empty, 0, k, k + 1, q_ring);
-            }
-            __syncwarp();
-          }
-        }
-#else
         if (nbs > 0) {  // this layer's dz_{t+1}: chunk j is produced by CTAs [16 j / UPC, 16 (j + 1) / UPC)
           const int p0 = b0 * 16 / UPC, p1 = (b0 + nbs) * 16 / UPC;
           for (int c = p0 + lane; c < p1; c += 32) {
             unsigned x;
             do {
               asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(flags + c * REC_FS) : "memory");
-              if (x < flag_of((unsigned)(T - 1 - t))) poll_backoff();
-            } while (x < flag_of((unsigned)(T - 1 - t)));
+            } while (x < ((unsigned)(T - 1 - t)));
           }
           __syncwarp();
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           fence_proxy_async_global();
           if (threadIdx.x == 128) issue_step(srcA, srcB, lys, sA, full, empty, 0, opsA, 1 << 30, q_ring);
         }
-#endif
         if (threadIdx.x == 128) PROBE(ti, 2);
       }
       __syncwarp();
@@ -952,7 +888,6 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
       for (int u = 0; u < HU; ++u) dh[u] = 0.f;
       if (has_x) {
         const int par = nx & 1;
-#if JANUS_KS_STASYNC
         // partial dh tiles leave straight from registers: st.async of each 16-B piece into the
         // peer's red[par] slot, completing on the peer's redfull[par] (no staging, proxy fence or
         // single-thread bulk issue); only this CTA's own partial goes through `stage`
@@ -1010,74 +945,6 @@ JN_DEV void ks_body(const KsCtx &cx, const CUtensorMap *tmWa, const CUtensorMap 
         if (threadIdx.x == 0) PROBE(ti, 14);
         mbar_wait_cluster(&redfull[par], (nx >> 1) & 1);
         if (threadIdx.x == 0) PROBE(ti, 15);
-#else
-        if (threadIdx.x == 0) {
-          bulk_wait_group_read0();  // the previous step's stage has been read out by the copies
-          mbar_expect_tx(&redfull[par], (KS_CL - 1) * C::TILE);
-        }
-        if (nstep > 0) {
-          mbar_wait(tfull, nm & 1);
-          if (threadIdx.x == 0) PROBE(ti, 5);
-          __syncwarp();
-          tc_fence_after();
-        }
-        epi_bar();  // stage free
-        {  // M = 64: accumulator row i in TMEM lane (i % 16) + 32 (i / 16); tcgen05.ld is
-           // .sync.aligned, so every lane of the warp loads and lanes 16-31 skip the store
-          const int srow = 16 * warp + lane;
-          const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
-          const int nacc = min(REC_NMW, nstep);
-#pragma unroll
-          for (int p = 0; p < KS_CL; ++p) {
-            float v[UPC];
-#pragma unroll
-            for (int i = 0; i < UPC; ++i) v[i] = 0.f;
-            if (nacc > 0) {  // every tile's load in flight, one wait
-              uint32_t r0[UPC], r1[UPC], r2[UPC], r3[UPC];
-              auto ld = [&](int w, uint32_t (&r)[UPC]) {
-                if constexpr (UPC == 16) tmem_ld16_nw(ta + w * C::CUNITS + UPC * p, r);
-                else tmem_ld8_nw(ta + w * C::CUNITS + UPC * p, r);
-              };
-              ld(0, r0);
-              if (nacc > 1) ld(1, r1);
-              if (nacc > 2) ld(2, r2);
-              if (nacc > 3) ld(3, r3);
-              tmem_ld_wait();
-              tmem_pin(r0); tmem_pin(r1); tmem_pin(r2); tmem_pin(r3);
-#pragma unroll
-              for (int i = 0; i < UPC; ++i) {
-                float acc = __uint_as_float(r0[i]);
-                if (nacc > 1) acc += __uint_as_float(r1[i]);
-                if (nacc > 2) acc += __uint_as_float(r2[i]);
-                if (nacc > 3) acc += __uint_as_float(r3[i]);
-                v[i] = acc;
-              }
-            }
-            if (lane < 16) {
-              float4 *dst = reinterpret_cast<float4 *>(stage + ((size_t)p * 64 + srow) * UPC);
-#pragma unroll
-              for (int q = 0; q < UPC / 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            }
-          }
-        }
-        if (nstep > 0) epi_tmem_release(tempty);
-        if (threadIdx.x == 0) PROBE(ti, 3);
-        fence_proxy_async_shared();
-        epi_bar();
-        if (threadIdx.x == 0) {
-#pragma unroll
-          for (int p = 0; p < KS_CL; ++p) {
-            if (p == rank) continue;
-            const int slot = rank < p ? rank : rank - 1;  // my sender slot inside peer p
-            const uint32_t dst = mapa_shared(smem_u32(red + (size_t)(par * (KS_CL - 1) + slot) * 64 * UPC), p);
-            bulk_s2cluster(dst, stage + (size_t)p * 64 * UPC, C::TILE, mapa_shared(smem_u32(&redfull[par]), p));
-          }
-          bulk_commit_group();
-          PROBE(ti, 14);
-        }
-        mbar_wait(&redfull[par], (nx >> 1) & 1);
-        if (threadIdx.x == 0) PROBE(ti, 15);
-#endif
 #pragma unroll
         for (int p = 0; p < KS_CL; ++p) {  // fixed order over the K-slices: deterministic
           const float *src = p == rank ? stage + (size_t)rank * 64 * UPC

@@ -21,10 +21,9 @@
 
 namespace jk {
 
-#ifndef JANUS_T_NMW
-#define JANUS_T_NMW 2
-#endif
-constexpr int T_NMW = JANUS_T_NMW;  // MMA-issuing warps (one accumulator each); 2: C3 B=25 0.271 -> 0.264 ms, B=256 0.562 -> 0.570 (1: 0.264 / 0.577)
+// MMA-issuing warps (one accumulator each); measured with the elect.sync issue: 2 -> C3 B=25
+// 0.271 -> 0.264 ms against 4 (B=256 0.562 -> 0.570), 1 -> 0.264 / 0.577
+constexpr int T_NMW = 2;
 constexpr int TT = 160 + 32 * T_NMW;  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
 // ring stages: a multiple of T_NMW, so a stage is always consumed by the same MMA warp (it owns
 // chunks q = w mod T_NMW) and that warp can never wait on a stage two phases ahead of its loads
