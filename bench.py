@@ -88,6 +88,9 @@ def gemm_flops(name, V, E, H, TB):
 
 # ----------------------------------------------------------------------------- clocks
 class Clocks:
+    """nvidia-smi sampler (50 ms) started before the warm-up; a reader thread timestamps every
+    line, and the summary keeps the samples taken inside the timed window (the warm-up steps keep
+    the GPU busy until the sampler is producing, so a short timed region still gets samples)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -95,37 +98,62 @@ class Clocks:
     def __init__(self, gpu):
         self.gpu = gpu
         self.p = None
+        self.lines = []  # (arrival time, fields)
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
+        import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "50"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except OSError:
             self.p = None
+            return self
+
+        def reader():
+            for line in self.p.stdout:
+                if line.strip():
+                    self.lines.append((time.time(), line.strip().split(",")))
+        self.th = threading.Thread(target=reader, daemon=True)
+        self.th.start()
+        return self
+
+    def producing(self):
+        return self.p is None or len(self.lines) > 0
+
+    def __enter__(self):  # the timed window
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.p is None:
             return
         self.p.terminate()
         try:
-            out, _ = self.p.communicate(timeout=5)
+            self.p.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.p.kill()
-            out, _ = self.p.communicate()
-        self.rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        self.th.join(timeout=2)
 
     def summary(self):
-        rows = getattr(self, "rows", [])
-        if not rows:
+        if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        lo, hi = (self.t0 or 0.0) - 0.06, (self.t1 or 1e30) + 0.06  # one sampling period of slack
+        rows = [r for t, r in self.lines if lo <= t <= hi]
+        window = "timed region"
+        if not rows:  # no sample landed inside a very short window: the nearest ones after it
+            rows = [r for t, r in self.lines if t >= lo][:3]
+            window = "first samples after the timed region began"
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if "Active" in v and "Not" not in v})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "window": window}
 
 
 # ----------------------------------------------------------------------------- CPU baselines
@@ -592,11 +620,19 @@ def main():
             ms = float(t.item())
         return ms
 
+    clk = Clocks(local).start()
     for k in range(args.warmup):
         step(k)
+    t_wait = time.time()
+    k = args.warmup
+    while not clk.producing() and time.time() - t_wait < 3.0:  # keep the GPU busy until sampling
+        step(k)
+        k += 1
+    torch.cuda.synchronize()
     c0 = g.counters()
-    with Clocks(local) as clk:
+    with clk:
         ms = timed(lambda k: step(k), args.steps)
+    clk.stop()
     c1 = g.counters()
     launches = (c1["launches"] - c0["launches"]) // args.steps
     syncs = (c1["host_syncs"] - c0["host_syncs"]) / args.steps
