@@ -150,7 +150,8 @@ bool lower_tree(Graph &g, std::string &why) {
   auto take = [&](size_t bytes) { size_t r = o; o = a256(o + bytes); return r; };
   p.off.status = take(sizeof(DevStatus));
   // 64 grid-barrier words, then one 128-B line per level: the forward's per-level arrival counters
-  p.off.barriers = take((64 + (size_t)TREE_MAX_LEVELS * 32) * sizeof(unsigned));
+  // (+ the backward's per-level arrival counters, one line per level)
+  p.off.barriers = take((64 + 2 * (size_t)TREE_MAX_LEVELS * 32) * sizeof(unsigned));
   p.off.stage_args = take((4ull * N + 2ull * (p.B + 1)) * sizeof(int));
   p.off.height = take((size_t)N * 4); p.off.order = take((size_t)N * 4); p.off.irank = take((size_t)N * 4);
   p.off.pslot = take((size_t)N * 4); p.off.tree_of = take((size_t)N * 4); p.off.pcount = take((size_t)N * 4);
@@ -265,6 +266,7 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   t.c_leaf = fp(p.off.c_leaf); t.root_h = fp(p.off.root_h); t.dh_node = fp(p.off.dh_node);
   t.dc_node = fp(p.off.dc_node); t.DZ_int = bf(p.off.DZ_int); t.DZ_leaf = bf(p.off.DZ_leaf);
   t.gWc = fp(p.off.gWc); t.gbc = fp(p.off.gbc); t.rowloss = fp(p.off.rowloss); t.barrier = bars;
+  t.bwd_lvl = bars + 64 + TREE_MAX_LEVELS * 32;
   t.dbg = g.probe;
   t.root_part = fp(p.off.root_part);
 

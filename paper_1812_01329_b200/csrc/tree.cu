@@ -24,7 +24,8 @@ namespace jk {
 // MMA-issuing warps (one accumulator each); measured with the elect.sync issue: 2 -> C3 B=25
 // 0.271 -> 0.264 ms against 4 (B=256 0.562 -> 0.570), 1 -> 0.264 / 0.577
 constexpr int T_NMW = 2;
-constexpr int TT = 160 + 32 * T_NMW;  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
+constexpr int TT = 160 + 32 * T_NMW;
+  // threads: warps 0-3 epilogue, warp 4 TMA, warps 5.. MMA
 // ring stages: a multiple of T_NMW, so a stage is always consumed by the same MMA warp (it owns
 // chunks q = w mod T_NMW) and that warp can never wait on a stage two phases ahead of its loads
 constexpr int T_STAGES = 8;  // backward ring; the forward uses 6 (or 4) to fit its staging buffers
@@ -651,7 +652,10 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
     for (int i = threadIdx.x; i < (RNN ? H : 4 * H); i += blockDim.x) sbias[i] = t.b[i];
     // the per-level arrival counters (first used after the leaf level's grid barrier)
     if (blockIdx.x == 0)
-      for (int l = threadIdx.x; l < TREE_MAX_LEVELS; l += blockDim.x) t.barrier[64 + l * 32] = 0;
+      for (int l = threadIdx.x; l < TREE_MAX_LEVELS; l += blockDim.x) {
+        t.barrier[64 + l * 32] = 0;
+        t.bwd_lvl[l * 32] = 0;  // the backward launch's counters (it runs after this kernel)
+      }
   }
   fence_proxy_async_global();
   grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
@@ -1227,15 +1231,35 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
   rg.q = 0;
   rg.tiles = 0;
   const int L = s.meta[0], n0 = s.meta[2], nint = s.meta[3];
-  unsigned int ep = 0;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   // Top-down over the internal levels. The dz rows of level l are complete when its turn comes:
   // the roots' by the classifier kernel, every other node's by its parent's level (higher).
-  // One grid barrier per level: [dh_l ; dh_r] = rb(dz) U lands per tile column, and since a
+  // Per level: [dh_l ; dh_r] = rb(dz) U lands per tile column, and since a
   // child's h feeds only its parent, that column of the child's dh is final — the epilogue runs
   // the child's cell backward right there (its DZ row, its children's dc; leaves too).
+  // Per-level arrival counters instead of a grid barrier per level (as the forward): only the CTAs
+  // with tiles at a level take part; each waits for the previous (higher) level's workers, then
+  // arrives on its level's counter. A node's dz row / dc come from its parent's / grandparent's
+  // level, which is higher still: the chain of release / acquire pairs orders those writes too.
+  const int ntile_nb = RES ? res_ntile : (2 * H + BNT - 1) / BNT;
+  auto workers = [&](int l) {
+    const int mt = (s.lvl_off[l + 1] - s.lvl_off[l] + 127) / 128;
+    return RES ? min(mt, res_groups) * res_ntile : min((int)gridDim.x, mt * ntile_nb);
+  };
   for (int l = L - 1; l >= 1; --l) {
     const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
+    if ((int)blockIdx.x >= workers(l)) continue;
+    if (l < L - 1) {
+      if (threadIdx.x == 0) {
+        const unsigned int target = (unsigned)workers(l + 1);
+        unsigned int v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(t.bwd_lvl + (l + 1) * 32) : "memory");
+        } while (v < target);
+      }
+      __syncthreads();
+      fence_proxy_async_global();
+    }
     tile_loop<BNT, 2, BW_STAGES>(rg, &mp.dz, &mp.ut, r0, cnt, 2 * H, NGH, [&](int row, int) {
       if (row >= 0) {
         BwdRowMeta m;
@@ -1297,7 +1321,8 @@ __global__ void __launch_bounds__(TT, 1) tree_bwd_kernel(const __grid_constant__
     }, (NGH + 63) / 64 >= 16 ? (RES ? 4 : 3) : ((NGH + 63) / 64 >= 8 ? 2 : 1),  // a fixed warp per stage
        t.dbg ? t.dbg + 3 * 256 * 256 * 2 + ((size_t)l * 256 + blockIdx.x) * 4 : nullptr, &mp.dz32);
     fence_proxy_async_global();  // the children's DZ rows feed the next level's TMA loads
-    grid_sync(t.barrier, ++ep * gridDim.x, t.dbg ? t.dbg + 256 * 256 * 2 : nullptr);
+    __syncthreads();  // every thread's stores of the level precede the release (bar.sync cumulativity)
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.bwd_lvl + l * 32) : "memory");
   }
   // zero the dz rows of the last partial 64-row K chunk of the wgrad GEMMs
   for (long long e = gt; e < (long long)(((nint + 63) & ~63) - nint) * d.P5; e += gs)

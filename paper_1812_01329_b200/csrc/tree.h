@@ -52,6 +52,7 @@ struct TreeBufs {
   float *rowloss;              // [B]
   float *root_part;            // [ceil(B/8)][C*H + C] per-block classifier-gradient partials
   unsigned int *barrier;       // grid barrier counters (zeroed by step init)
+  unsigned int *bwd_lvl;       // backward per-level arrival counters (one 128-B line per level; zeroed by the forward)
   unsigned long long *dbg;     // dev hook (janus_dev_set_probe): per-barrier arrival / release
                                // %globaltimer of every CTA, [2 kernels][256 syncs][256 CTAs][2]
 };
