@@ -663,6 +663,7 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   // ---- level 0: leaves. z = x W_leaf^T; i, o = sigmoid, u = tanh; c = i u; h = o tanh(c)
   const bool vec = (H % 4) == 0;
   if constexpr (!RNN) {
+  const int leaf_workers = min((int)gridDim.x, ((n0 + 127) / 128) * ((3 * H + 47) / 48));  // tiles of the leaf GEMM
   tile_loop<48, true, NS>(rg, &mp.x_leaf, &mp.w_leaf, 0, n0, 3 * H, E, [&](int pos, int) {
     if (pos >= 0) {  // row metadata into shared memory while the MMAs run
       const int n = s.order[pos], ps = s.pslot[n];
@@ -709,7 +710,12 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
     }
   }, (E + 63) / 64 >= 8 ? 2 : 1);
   fence_proxy_async_global();
-  grid_sync(t.barrier, ++ep * gridDim.x, t.dbg);
+  // the leaf level's workers arrive on level 0's counter (the first internal level waits for it,
+  // as every internal level waits for the one below) instead of a grid barrier
+  if ((int)blockIdx.x < leaf_workers) {
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.barrier + 64) : "memory");
+  }
   }  // !RNN (TreeRNN leaves were placed in phase 0)
   // ---- internal levels: z = [h_l; h_r] U^T; c = i u + f_l c_l + f_r c_r; h = o tanh(c)
   // Internal levels: only the CTAs with tiles at a level take part in it. A CTA waits for the
@@ -726,9 +732,10 @@ __global__ void __launch_bounds__(TT, 1) tree_fwd_kernel(const __grid_constant__
   for (int l = 1; l < L; ++l) {
     const int p0 = s.lvl_off[l], cnt = s.lvl_off[l + 1] - p0, r0 = p0 - s.lvl_off[1];
     if ((int)blockIdx.x >= workers(l)) continue;
-    if (l > 1) {
+    if (l > 1 || !RNN) {  // level 1 waits for the leaf level's workers (TreeRNN: placed in phase 0)
       if (threadIdx.x == 0) {
-        const unsigned int target = (unsigned)workers(l - 1);
+        const unsigned int target =
+            (unsigned)(l > 1 ? workers(l - 1) : min((int)gridDim.x, ((n0 + 127) / 128) * ((3 * H + 47) / 48)));
         unsigned int v;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(lvl_ctr + (l - 1) * 32) : "memory");
