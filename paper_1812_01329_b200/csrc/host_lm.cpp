@@ -871,7 +871,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       }
     if (overlap && cudaStreamWaitEvent(st, g.ev_join, 0) != cudaSuccess) return JANUS_ERR_CUDA;
   }
-  LCHK("finalize", launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
+  // single rank: the finalize runs as one extra block of the commit launch (below)
+  const bool fin_in_commit = !g.nccl && !fused;
+  if (!fin_in_commit) LCHK("finalize", launch_finalize(fp(p.off.rowloss), TB, gl, dst, g.opts.world_size, st));
   if (g.nccl) {  // every rank learns the same status before anything commits (reading Q12)
     g.prof.mark("dp_agree", st);
     janus_status r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
@@ -922,7 +924,8 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   if (p.train_arg >= 0 && !p.train_specialised)  // the training Switch evaluated on the device
     for (int k = 0; k < cl.n; ++k)
       if (cl.s[k].kind != C_COPY && cl.s[k].kind != C_TAG) cl.s[k].pred = argp[3];
-  LCHK("commit", launch_commit(cl, dst, st));
+  if (fin_in_commit) LCHK("commit", launch_commit_finalize(cl, FinalizeArgs{fp(p.off.rowloss), TB, gl}, dst, st));
+  else LCHK("commit", launch_commit(cl, dst, st));
   return JANUS_OK;
   };  // enqueue
   const janus_status er = enqueue();

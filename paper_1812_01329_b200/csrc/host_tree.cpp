@@ -339,7 +339,8 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
       if (r == JANUS_OK) r = dp_allreduce_sum(g, fp(sg.begin), (sg.end - sg.begin) / 4, st);
     if (r != JANUS_OK) return r;
   }
-  TCHK("finalize", launch_finalize(fp(p.off.rowloss), B, gl, dst, g.opts.world_size, st));
+  // single rank: the finalize runs as one extra block of the commit launch (below)
+  if (g.nccl) TCHK("finalize", launch_finalize(fp(p.off.rowloss), B, gl, dst, g.opts.world_size, st));
   if (g.nccl) {
     janus_status r = dp_agree(g, dst, reinterpret_cast<long long *>(W + p.off.dp_scratch), st);
     if (r != JANUS_OK) return r;
@@ -363,7 +364,8 @@ janus_status run_tree(Graph &g, const janus_tensor *args, int n_args, const janu
   if (p.lr_b != 0 && !p.rnn) { sg = {}; sg.kind = C_TREE_BIAS; sg.dst = bb; sg.grad = fp(p.off.gU); sg.ldg = p.ldgU; sg.col = 2 * H; sg.grad2 = fp(p.off.gWl); sg.ldg2 = p.ldgW; sg.col2 = E; sg.H = H; sg.lr = p.lr_b / nr; add(sg); }
   if (p.lr_Wc != 0) { sg = {}; sg.kind = C_DENSE; sg.dst = Wc; sg.grad = fp(p.off.gWc); sg.rows = p.C; sg.cols = H; sg.ldg = H; sg.lr = p.lr_Wc / nr; add(sg); }
   if (p.lr_bc != 0) { sg = {}; sg.kind = C_DENSE; sg.dst = bc; sg.grad = fp(p.off.gbc); sg.rows = 1; sg.cols = p.C; sg.ldg = p.C; sg.lr = p.lr_bc / nr; add(sg); }
-  TCHK("commit", launch_commit(cl, dst, st));
+  if (g.nccl) TCHK("commit", launch_commit(cl, dst, st));
+  else TCHK("commit", launch_commit_finalize(cl, FinalizeArgs{fp(p.off.rowloss), B, gl}, dst, st));
   return finish(g, dst, outs, n_outs, st, fail);
 }
 

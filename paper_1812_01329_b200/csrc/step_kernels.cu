@@ -953,8 +953,7 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
 }
 
 // ------------------------------------------------------------------------------ finalize
-__global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, DevStatus *st) {
-  pdl_enter();
+JN_DEV void finalize_body(const float *rowloss, int rows, const GuardList &gl, DevStatus *st) {
   __shared__ float sh[1024];
   float acc = 0.f;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) acc += rowloss[i];
@@ -984,6 +983,10 @@ __global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, De
       st->status = 0;
     }
   }
+}
+__global__ void finalize_kernel(const float *rowloss, int rows, GuardList gl, DevStatus *st) {
+  pdl_enter();
+  finalize_body(rowloss, rows, gl, st);
 }
 
 cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
@@ -1043,9 +1046,7 @@ cudaError_t launch_scatter_rows(const float *seg_grad, int ldg, const int *seg_w
 
 // ------------------------------------------------------------------------------ commit
 // Predicated on the device status: with any failure nothing is written (all-or-nothing).
-__global__ void __launch_bounds__(256, 6) commit_kernel(CommitList cl, const DevStatus *st) {
-  pdl_enter();
-  if (st->status != 0) return;
+JN_DEV void commit_body(const CommitList &cl) {
   int bx, gx;
   const CommitSeg sg = cl.s[seg_of_block(cl.blk, cl.n, &bx, &gx)];
   if (sg.pred && *sg.pred == 0) return;
@@ -1182,8 +1183,27 @@ __global__ void __launch_bounds__(256, 6) commit_kernel(CommitList cl, const Dev
   }
 }
 
-cudaError_t launch_commit(const CommitList &cl0, const DevStatus *st, cudaStream_t s) {
-  if (cl0.n <= 0) return cudaSuccess;
+__global__ void __launch_bounds__(256, 6) commit_kernel(CommitList cl, const DevStatus *st) {
+  pdl_enter();
+  if (st->status != 0) return;
+  commit_body(cl);
+}
+// The step's finalize folded into the commit launch: its last block sums the loss rows and writes
+// the status word while the commit blocks decide all-or-nothing from the same inputs the status
+// is computed from (the minimum failing key and the runtime-error flags), so no block waits for
+// another (single-rank steps; with data parallelism the agreed status must precede the commit).
+__global__ void __launch_bounds__(256, 6) commit_finalize_kernel(CommitList cl, FinalizeArgs fa, DevStatus *st) {
+  pdl_enter();
+  if ((int)blockIdx.x == cl.blk[cl.n]) {
+    finalize_body(fa.rowloss, fa.rows, fa.gl, st);
+    return;
+  }
+  if (st->key != KEY_PASS || st->runtime_err != 0) return;
+  commit_body(cl);
+}
+
+static cudaError_t launch_commit_impl(const CommitList &cl0, const FinalizeArgs *fa, DevStatus *st, cudaStream_t s) {
+  if (cl0.n <= 0 && !fa) return cudaSuccess;
   CommitList cl = cl0;
   cl.blk[0] = 0;
   for (int k = 0; k < cl.n; ++k) {
@@ -1201,10 +1221,18 @@ cudaError_t launch_commit(const CommitList &cl0, const DevStatus *st, cudaStream
     cl.blk[k + 1] = cl.blk[k] + seg_blocks(u);
   }
   {
-    const cudaError_t pe_ = launch_pdl(commit_kernel, dim3(cl.blk[cl.n]), dim3(256), 0, s, cl, st);
+    const cudaError_t pe_ = fa ? launch_pdl(commit_finalize_kernel, dim3(cl.blk[cl.n] + 1), dim3(256), 0, s, cl, *fa, st)
+                               : launch_pdl(commit_kernel, dim3(cl.blk[cl.n]), dim3(256), 0, s, cl,
+                                            static_cast<const DevStatus *>(st));
     if (pe_ != cudaSuccess) return pe_;
   }
   return cudaGetLastError();
+}
+cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s) {
+  return launch_commit_impl(cl, nullptr, const_cast<DevStatus *>(st), s);
+}
+cudaError_t launch_commit_finalize(const CommitList &cl, const FinalizeArgs &fa, DevStatus *st, cudaStream_t s) {
+  return launch_commit_impl(cl, &fa, st, s);
 }
 
 }  // namespace jk

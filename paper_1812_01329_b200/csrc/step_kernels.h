@@ -205,5 +205,13 @@ struct CommitList {
   int blk[MAX_COMMIT + 1];  // set by launch_commit: segment k owns blocks [blk[k], blk[k+1])
 };
 cudaError_t launch_commit(const CommitList &cl, const DevStatus *st, cudaStream_t s);
+// finalize (loss sum, status word) folded into the commit launch as one extra block; the commit
+// blocks take their all-or-nothing decision from the key and runtime-error flags (single rank)
+struct FinalizeArgs {
+  const float *rowloss;
+  int rows;
+  GuardList gl;
+};
+cudaError_t launch_commit_finalize(const CommitList &cl, const FinalizeArgs &fa, DevStatus *st, cudaStream_t s);
 
 }  // namespace jk
