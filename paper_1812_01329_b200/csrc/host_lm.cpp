@@ -680,9 +680,8 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
       sg.kind = P_CAST_ROWS; sg.src = P.Wdec; sg.dst = bf(p.off.Wdec_b); sg.rows = V; sg.cols = H;
       sg.ld_src = H; sg.ld_dst = Hp; sg.H = 0; add(sg);
     }
-    LCHK("cast", launch_prep(pl, st));
+    LCHK("cast", launch_prep_gather(pl, P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
   }
-  LCHK("gather", launch_gather(P.E, V, E, P.tok, B, Wd, Tw, Tdev, bf(p.off.X), Ep, dst, st));
   const bool drop = p.key_arg >= 0;  // Zaremba dropout: site 0 on the embedding output (in place)
   if (drop) LCHK("dropout", launch_dropout_bf16(bf(p.off.X), bf(p.off.X), TB, E, Ep, keyp, 0, p.dropout, st));
   // input of layer l (l >= 1) and of the decoder: the layer below's h, or its dropped copy

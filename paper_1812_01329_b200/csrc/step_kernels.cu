@@ -98,14 +98,13 @@ cudaError_t launch_guards(const GuardList &gl, DevStatus *st, cudaStream_t s) {
 
 // ------------------------------------------------------------------------------ gather
 // one warp per row; X[t*B+b][k] = rb(E[id][k]); ones column at k = Edim.
-__global__ void gather_kernel(const float *__restrict__ E, int V, int Edim, const int *__restrict__ tok,
-                              int B, int W, int T, const int *T_dev, __nv_bfloat16 *X, int ldx,
-                              DevStatus *st) {
-  pdl_enter();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+// blk / nblk: this block among the nblk blocks doing the gather
+JN_DEV void gather_body(const float *__restrict__ E, int V, int Edim, const int *__restrict__ tok, int B, int W,
+                        int T, const int *T_dev, __nv_bfloat16 *X, int ldx, DevStatus *st, int blk, int nblk) {
+  const int warp = (blk * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int rows = T * B;
   const int Tb = T_dev ? *T_dev : T;
-  for (int r = warp; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+  for (int r = warp; r < rows; r += (nblk * blockDim.x) >> 5) {
     const int t = r / B, b = r - t * B;
     int id = tok[(size_t)b * W + t];
     if (id < 0 || id >= V) {
@@ -132,6 +131,12 @@ __global__ void gather_kernel(const float *__restrict__ E, int V, int Edim, cons
     }
     for (int k = Edim + lane; k < ldx; k += 32) dst[k] = __float2bfloat16_rn(k == Edim ? 1.f : 0.f);
   }
+}
+__global__ void gather_kernel(const float *__restrict__ E, int V, int Edim, const int *__restrict__ tok,
+                              int B, int W, int T, const int *T_dev, __nv_bfloat16 *X, int ldx,
+                              DevStatus *st) {
+  pdl_enter();
+  gather_body(E, V, Edim, tok, B, W, T, T_dev, X, ldx, st, blockIdx.x, gridDim.x);
 }
 
 cudaError_t launch_gather(const float *E, int V, int Edim, const int *tok, int B, int W, int T,
@@ -268,8 +273,7 @@ JN_DEV int seg_of_block(const int *blk, int n, int *bx, int *gx) {
   *gx = blk[k + 1] - blk[k];
   return k;
 }
-__global__ void __launch_bounds__(256, 5) prep_kernel(PrepList pl) {
-  pdl_enter();
+JN_DEV void prep_body(const PrepList &pl) {
   int bx, gx;
   const PrepSeg sg = pl.s[seg_of_block(pl.blk, pl.n, &bx, &gx)];
   switch (sg.kind) {
@@ -353,6 +357,25 @@ __global__ void __launch_bounds__(256, 5) prep_kernel(PrepList pl) {
 // blocks of a segment: one per two of its grid-stride work units, at least 1, at most 4 per SM
 // (measured at C2 against one unit per block and against 4 / SM for every segment: the prep
 // and commit phases 25.9 / 38.7 us vs 27.9 / 40.6 and 30.1 / 44.1 us)
+__global__ void __launch_bounds__(256, 5) prep_kernel(PrepList pl) {
+  pdl_enter();
+  prep_body(pl);
+}
+// operand prep and the embedding gather in one launch: blocks [0, prep) run the prep segments,
+// the rest the gather (independent work; one launch boundary fewer)
+__global__ void __launch_bounds__(256, 5) prep_gather_kernel(PrepList pl, const float *__restrict__ E, int V,
+                                                           int Edim, const int *__restrict__ tok, int B, int W,
+                                                           int T, const int *T_dev, __nv_bfloat16 *X, int ldx,
+                                                           DevStatus *st) {
+  pdl_enter();
+  const int np = pl.blk[pl.n];
+  if ((int)blockIdx.x < np) {
+    prep_body(pl);
+    return;
+  }
+  gather_body(E, V, Edim, tok, B, W, T, T_dev, X, ldx, st, blockIdx.x - np, gridDim.x - np);
+}
+
 static int seg_blocks(long long units) { return (int)std::max(1LL, std::min<long long>(4 * NSM, (units + 1) / 2)); }
 cudaError_t launch_prep(const PrepList &pl0, cudaStream_t s) {
   if (pl0.n <= 0) return cudaSuccess;
@@ -369,6 +392,28 @@ cudaError_t launch_prep(const PrepList &pl0, cudaStream_t s) {
   }
   {
     const cudaError_t pe_ = launch_pdl(prep_kernel, dim3(pl.blk[pl.n]), dim3(256), 0, s, pl);
+    if (pe_ != cudaSuccess) return pe_;
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_prep_gather(const PrepList &pl0, const float *E, int V, int Edim, const int *tok, int B, int W,
+                              int T, const int *T_dev, __nv_bfloat16 *X, int ldx, DevStatus *st, cudaStream_t s) {
+  PrepList pl = pl0;
+  pl.blk[0] = 0;
+  for (int k = 0; k < pl.n; ++k) {
+    const PrepSeg &g = pl.s[k];
+    long long u = 1;
+    if (g.kind == P_CAST_ROWS) u = (g.rows + 7) / 8;
+    else if (g.kind == P_CAST_T_IL) u = (long long)((4 * g.H + 31) / 32) * ((g.H + 127) / 128);
+    else if (g.kind == P_BIAS_IL) u = (4LL * g.H + 255) / 256;
+    else if (g.kind == P_FILL_COL) u = ((long long)g.rows * std::max(1, g.ld_dst - g.cols) + 255) / 256;
+    pl.blk[k + 1] = pl.blk[k] + seg_blocks(u);
+  }
+  {
+    int gblocks = (T * B * 32 + 255) / 256;
+    gblocks = gblocks < 4 * NSM ? gblocks : 4 * NSM;
+    const cudaError_t pe_ = launch_pdl(prep_gather_kernel, dim3(pl.blk[pl.n] + gblocks), dim3(256), 0, s, pl, E, V,
+                                       Edim, tok, B, W, T, T_dev, X, ldx, st);
     if (pe_ != cudaSuccess) return pe_;
   }
   return cudaGetLastError();

@@ -76,6 +76,9 @@ struct PrepList {
   int blk[MAX_PREP + 1];  // set by launch_prep: segment k owns blocks [blk[k], blk[k+1]) of the 1-D grid
 };
 cudaError_t launch_prep(const PrepList &pl, cudaStream_t s);
+// launch_prep and launch_gather in one launch (prep blocks first, then the gather's)
+cudaError_t launch_prep_gather(const PrepList &pl, const float *E, int V, int Edim, const int *tok, int B, int W,
+                              int T, const int *T_dev, __nv_bfloat16 *X, int ldx, DevStatus *st, cudaStream_t s);
 cudaError_t launch_cast_rows(const float *src, int R, int Cc, int ld_src, __nv_bfloat16 *dst,
                              int ld_dst, int interleave_H, cudaStream_t s);
 cudaError_t launch_cast_transpose_interleaved(const float *W, int H, __nv_bfloat16 *WT, int ldwt,
