@@ -165,6 +165,8 @@ struct Graph {
   void *nccl = nullptr;  // ncclComm_t when world_size > 1
   void *nccl2 = nullptr; // second communicator (split) for the collective that overlaps the backward
   cudaStream_t side = nullptr;             // stream of the overlapped collective
+  cudaStream_t bk_side = nullptr;          // single-rank LM: the embedding-gradient bucketing beside the forward
+  cudaEvent_t ev_bk_fork = nullptr, ev_bk_join = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool dp = false;       // data-parallel collectives in the step (fixed at build)
   bool fused_ar = false; // NEXT-3: weight gradients reduced in the wgrad GEMM epilogue (fixed at build)

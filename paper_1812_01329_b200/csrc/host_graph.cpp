@@ -476,6 +476,12 @@ void janus_graph_destroy(janus_graph *g) {
   if (!g) return;
   g->cg.reset();
   dp_destroy(*g);
+  if (g->bk_side) {
+    cudaStreamSynchronize(g->bk_side);
+    cudaStreamDestroy(g->bk_side);
+  }
+  if (g->ev_bk_fork) cudaEventDestroy(g->ev_bk_fork);
+  if (g->ev_bk_join) cudaEventDestroy(g->ev_bk_join);
   if (g->h_status) cudaFreeHost(g->h_status);
   delete g;
 }

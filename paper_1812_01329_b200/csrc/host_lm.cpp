@@ -692,6 +692,14 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   // two layers: one wavefront launch (layer 1 one step behind layer 0, its input projection
   // fused into the recurrent MMA) unless disabled or too wide for one CTA per SM
   const bool wavefront = L == 2 && !g.opts.serial_layers && !drop && rec_fwd_wf_grid(H) <= 148;
+  // single rank, fixed trip count: the embedding-gradient bucketing runs on a side stream beside
+  // the forward recurrence (its CTAs leave SMs free); the stream and events are created once
+  const bool early_bucket = p.lr_E != 0 && !g.nccl && !p.while_mode && wavefront && [&] {
+    if (g.bk_side) return true;
+    return cudaStreamCreateWithFlags(&g.bk_side, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&g.ev_bk_fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&g.ev_bk_join, cudaEventDisableTiming) == cudaSuccess;
+  }();
   auto rec_args = [&](int l) {
     RecFwdArgs ra;
     ra.B = B; ra.H = H; ra.T = Tw; ra.T_dev = Tdev; ra.lens = p.while_mode ? P.lens : nullptr;
@@ -714,6 +722,18 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
     op.B = bf(p.off.Wih_b[l]); op.ldb = Inp;
     op.ep.C = fp(p.off.G[l]); op.ep.ldc = p.Gz; op.ep.bias_col = fp(p.off.bil[l]);
     LCHK(l ? "gemm_in1" : "gemm_in0", gemm_bf16(with_flags(op), st));
+    if (l == 0 && early_bucket) {
+      // the embedding-gradient bucketing depends on the token ids only: one block on a side
+      // stream beside the forward recurrence (which leaves SMs free), joined before the sums
+      if (cudaEventRecord(g.ev_bk_fork, st) != cudaSuccess || cudaStreamWaitEvent(g.bk_side, g.ev_bk_fork, 0) != cudaSuccess)
+        return JANUS_ERR_CUDA;
+      if (launch_embed_grad(P.tok, B, Wd, Tw, Tdev, V, nullptr, Ep, E, reinterpret_cast<int *>(W + p.off.seg_word),
+                            reinterpret_cast<int *>(W + p.off.ehist), fp(p.off.seg_grad), Ep,
+                            reinterpret_cast<int *>(W + p.off.nseg), g.bk_side, 1) != cudaSuccess)
+        return JANUS_ERR_CUDA;
+      g.launches++;
+      if (cudaEventRecord(g.ev_bk_join, g.bk_side) != cudaSuccess) return JANUS_ERR_CUDA;
+    }
     if (wavefront) {
       LCHK("rec_fwd01", lstm_rec_fwd_wavefront(rec_args(0), rec_args(1), bf(p.off.Whh_b[0]), bf(p.off.Wih_b[1]),
                                                bf(p.off.Whh_b[1]), Hp, fp(p.off.bil[1]), p.while_mode, st));
@@ -853,10 +873,11 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   int *seg_word = reinterpret_cast<int *>(W + p.off.seg_word);
   int *nseg = reinterpret_cast<int *>(W + p.off.nseg);
   if (p.lr_E != 0) {
+    if (early_bucket && cudaStreamWaitEvent(st, g.ev_bk_join, 0) != cudaSuccess) return JANUS_ERR_CUDA;
     LCHK("embed_grad", launch_embed_grad(P.tok, B, Wd, Tw, Tdev, V, fp(p.off.dX[0]), Ep, E, seg_word,
                                          reinterpret_cast<int *>(W + p.off.ehist), fp(p.off.seg_grad),
-                                         Ep, nseg, st));
-    g.launches++;  // embed grad is two kernels
+                                         Ep, nseg, st, early_bucket ? 2 : 0));
+    if (!early_bucket) g.launches++;  // embed grad is two kernels
   }
   if (g.nccl) {
     // DP: dense embedding gradient, one allreduce(sum) of the whole gradient arena

@@ -963,11 +963,11 @@ __global__ void __launch_bounds__(EG_WARPS * 32, 2) embed_segsum_kernel(
 
 cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev, int V,
                               const float *dX, int ldx, int Edim, int *seg_word, int *owner,
-                              float *seg_grad, int ldg, int *nseg, cudaStream_t s) {
+                              float *seg_grad, int ldg, int *nseg, cudaStream_t s, int part) {
   if (T * B > EG_MAX) return cudaErrorInvalidValue;
   const int owner_sm = V <= EG_OWNER_SMEM;
   cudaError_t e = cudaSuccess;
-  if (!owner_sm) {
+  if (!owner_sm && part != 2) {
     e = cudaMemsetAsync(owner, 0x7f, (size_t)V * sizeof(int), s);  // INT_MAX-ish
     if (e != cudaSuccess) return e;
   }
@@ -976,11 +976,12 @@ cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_
   const int bsmem = (3 * EG_MAX + (owner_sm ? V : 0)) * 4;
   e = set_smem_once((const void *)embed_bucket_kernel, (3 * EG_MAX + EG_OWNER_SMEM) * 4);
   if (e != cudaSuccess) return e;
-  {
+  if (part != 2) {
     const cudaError_t pe_ = launch_pdl(embed_bucket_kernel, dim3(1), dim3(1024), bsmem, s, tok, B, W, T, T_dev, owner, V, owner_sm, seg_word, seg_start, nseg,
                                              list);
     if (pe_ != cudaSuccess) return pe_;
   }
+  if (part == 1) return cudaGetLastError();
   auto go = [&](auto kern, int nq) {
     const int smem = EG_MAX * 4 + EG_WARPS * nq * 32 * 4;
     cudaError_t r = set_smem_once((const void *)kern, smem);

@@ -112,7 +112,8 @@ cudaError_t launch_xent(const float *logits, int V, int ldl, int rows, const int
 // occurrence (deterministic).
 cudaError_t launch_embed_grad(const int *tok, int B, int W, int T, const int *T_dev, int V,
                               const float *dX, int ldx, int Edim, int *seg_word, int *owner,
-                              float *seg_grad, int ldg, int *nseg, cudaStream_t s);
+                              float *seg_grad, int ldg, int *nseg, cudaStream_t s,
+                              int part = 0);  // part 1: the bucketing only, 2: the segment sums only
 
 // loss = sum(rowloss) / n_valid... rowloss already carries the 1/n_valid scale; status decode.
 cudaError_t launch_finalize(const float *rowloss, int rows, const GuardList &gl, DevStatus *st,
