@@ -666,7 +666,7 @@ def main():
     peak_src = pk["source"] + " bf16_tflops_sustained (kernels timed inside the step)"
     ncu = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "r2d_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2e_ncu_traffic.json")) as f:
             ncu = json.load(f)
     except (OSError, ValueError):
         pass
@@ -696,7 +696,7 @@ def main():
                 "flops_per_launch": rec_fl, "avg_launch_ms": rec_avg,
                 "step_period_us": rec_avg * 1000.0 / T,
                 "peak_source": peak_src, "share_of_step": rec_ms / step_ms if step_ms else None,
-                "traffic_source": "profiles/r2d_ncu_traffic.json (ncu --set full of one C2 step, dram read+write per launch; summary profiles/r2d_ncu_c2_summary.txt)",
+                "traffic_source": "profiles/r2e_ncu_traffic.json (ncu --set full of one C2 step, dram read+write per launch; summary profiles/r2e_ncu_c2_summary.txt)",
                 "note": "latency-bound: T=35 dependent steps per launch; the step period is the bound, not the tensor pipe"}
     gemms = [r for r in rows if r[3]]
     top = gemms[0] if gemms else rows[0]

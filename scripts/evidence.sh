@@ -8,7 +8,7 @@ timeout 600 python -m pytest tests -m gpu -x -q > $o/${tag}_gputest.log 2>&1; ec
 timeout 900 python bench.py > $o/${tag}_bench.json 2> $o/${tag}_bench.err; echo "bench rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/${tag}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-extras --no-cpu-baseline > $o/${tag}_ncu_launch.log 2>&1; echo "launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on --launch-skip 30 --launch-count 15 \
+timeout 900 ncu --set full --clock-control none --import-source on --launch-skip 24 --launch-count 12 \
   -o $o/${tag}_c2_full -f python scripts/run_c2.py 3 > $o/${tag}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 # the dominant kernel alone (small report, committed): rec_bwd of step 3
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:lstm_rec_bwd --launch-skip 2 --launch-count 1 \
