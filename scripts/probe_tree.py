@@ -86,5 +86,5 @@ for l in range(L - 1, 0, -1):
 
 sc = pp[4 * 256 * 256 * 2: 4 * 256 * 256 * 2 + 8]
 if sc[0] > 0:
-    names = ["init", "stage children", "height walk", "histogram+offsets", "stable placement", "parent slots"]
-    print("-- schedule kernel phases (us):", {names[i]: round((sc[i + 1] - sc[i]) / 1e3, 2) for i in range(5)})
+    names = ["init + stage children", "heights", "histogram+offsets", "stable placement", "parent slots"]
+    print("-- schedule kernel phases (us):", {names[i]: round((sc[i + 1] - sc[i]) / 1e3, 2) for i in range(5)})  # interval i = probe i+1 - probe i
