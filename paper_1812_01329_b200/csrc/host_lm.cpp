@@ -692,9 +692,9 @@ janus_status run_lm(Graph &g, const janus_tensor *args, const janus_tensor *stat
   // two layers: one wavefront launch (layer 1 one step behind layer 0, its input projection
   // fused into the recurrent MMA) unless disabled or too wide for one CTA per SM
   const bool wavefront = L == 2 && !g.opts.serial_layers && !drop && rec_fwd_wf_grid(H) <= 148;
-  // single rank, fixed trip count: the embedding-gradient bucketing runs on a side stream beside
+  // single rank: the embedding-gradient bucketing runs on a side stream beside
   // the forward recurrence (its CTAs leave SMs free); the stream and events are created once
-  const bool early_bucket = p.lr_E != 0 && !g.nccl && !p.while_mode && wavefront && [&] {
+  const bool early_bucket = p.lr_E != 0 && !g.nccl && wavefront && [&] {
     if (g.bk_side) return true;
     return cudaStreamCreateWithFlags(&g.bk_side, cudaStreamNonBlocking) == cudaSuccess &&
            cudaEventCreateWithFlags(&g.ev_bk_fork, cudaEventDisableTiming) == cudaSuccess &&
